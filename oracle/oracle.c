@@ -1,0 +1,100 @@
+/*
+ * oracle/oracle.c — the CPU ORACLE.  TEST INFRASTRUCTURE ONLY.
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+ * --impl reference legs may load this.  The product path
+ * (paper_2402_01816_b200/) never calls, links or includes it, and this file
+ * shares no code, header or constant with it.
+ *
+ * What it computes (§Definition of sorting, lines 121-142): the
+ * *stable ascending* sort ("AscLeft": ties keep their input order left to
+ * right) of contiguous binary64 keys, optionally moving a u32 payload with each
+ * key.  Keys are ordered by IEEE `<`, so -0.0 == +0.0 and their relative order
+ * is fixed by stability (reading R2).  NaN is rejected (reading R1,
+ * SPEC.md:93 "NaN-like unordered keys rejected at ingestion").
+ *
+ * How (plain, slow, single-threaded, no tuning):
+ *   - top-down binary divide&conquer mergesort with a 100% distant buffer
+ *     allocated once before recursing (§Forgotten art);
+ *   - split mid = lo + (hi-lo)/2 (reading R4);
+ *   - Knuth's merge: the right run's head is taken only if it is strictly
+ *     smaller than the left run's head, so the left run wins ties
+ *     ("Knuthsort"; "left element wins ties");
+ *   - the merged run is copied back from the buffer (no nocopy alternation,
+ *     no insertion-sort cutoff: the plainest correct form).
+ *   %RAM of this oracle is 2.0 (PAPER.md:26 formula, buffer = n elements).
+ *
+ * oracle_merge_runs(): one merge *level* of the same mergesort over runs of
+ * length L ("per recursion-level one read-scan with comparisons ... and one
+ * write-scan") — the definition a single GPU merge pass must
+ * reproduce.
+ */
+#include <stddef.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* Knuth merge of a[lo:mid) and a[mid:hi) into t[lo:hi); left wins ties. */
+static void merge_into(const double *k, const uint32_t *v, double *tk, uint32_t *tv,
+                       size_t lo, size_t mid, size_t hi)
+{
+    size_t i = lo, j = mid, o = lo;
+    while (i < mid && j < hi) {
+        if (k[j] < k[i]) {               /* take right only if strictly smaller */
+            tk[o] = k[j];
+            if (v) tv[o] = v[j];
+            ++j;
+        } else {
+            tk[o] = k[i];
+            if (v) tv[o] = v[i];
+            ++i;
+        }
+        ++o;
+    }
+    while (i < mid) { tk[o] = k[i]; if (v) tv[o] = v[i]; ++i; ++o; }
+    while (j < hi) { tk[o] = k[j]; if (v) tv[o] = v[j]; ++j; ++o; }
+}
+
+static void msort(double *k, uint32_t *v, double *tk, uint32_t *tv, size_t lo, size_t hi)
+{
+    if (hi - lo <= 1) return;
+    size_t mid = lo + (hi - lo) / 2;
+    msort(k, v, tk, tv, lo, mid);
+    msort(k, v, tk, tv, mid, hi);
+    merge_into(k, v, tk, tv, lo, mid, hi);
+    memcpy(k + lo, tk + lo, (hi - lo) * sizeof(double));
+    if (v) memcpy(v + lo, tv + lo, (hi - lo) * sizeof(uint32_t));
+}
+
+/* Sorts keys[0:n) (and vals, if non-NULL) in place.
+ * Returns 0 on success, 1 if a key is NaN (input untouched), 2 on OOM. */
+int oracle_sort_f64_u32(double *keys, uint32_t *vals, size_t n)
+{
+    for (size_t i = 0; i < n; ++i)
+        if (keys[i] != keys[i]) return 1;
+    if (n < 2) return 0;
+    double *tk = (double *)malloc(n * sizeof(double));
+    uint32_t *tv = vals ? (uint32_t *)malloc(n * sizeof(uint32_t)) : NULL;
+    if (!tk || (vals && !tv)) { free(tk); free(tv); return 2; }
+    msort(keys, vals, tk, tv, 0, n);
+    free(tk);
+    free(tv);
+    return 0;
+}
+
+/* One merge level: for q = 0,1,..: merges the sorted runs
+ * in[2qL : 2qL+L) and in[2qL+L : 2qL+2L) (clipped to n) into out[2qL : ...).
+ * Returns 0, or 1 on NaN. */
+int oracle_merge_runs(const double *keys, const uint32_t *vals, size_t n, size_t L,
+                      double *out_keys, uint32_t *out_vals)
+{
+    for (size_t i = 0; i < n; ++i)
+        if (keys[i] != keys[i]) return 1;
+    if (L == 0) return 1;
+    for (size_t lo = 0; lo < n; lo += 2 * L) {
+        size_t mid = lo + L < n ? lo + L : n;
+        size_t hi = lo + 2 * L < n ? lo + 2 * L : n;
+        merge_into(keys, vals, out_keys, out_vals, lo, mid, hi);
+    }
+    return 0;
+}
