@@ -1,0 +1,29 @@
+# Builds the product library (CUDA, sm_100a only) and the test-only C objects.
+NVCC ?= /usr/local/cuda/bin/nvcc
+ARCH := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC,-O3 -shared --expt-relaxed-constexpr
+PKG := paper_2402_01816_b200
+LIB := $(PKG)/libgns.so
+SRCS := $(PKG)/csrc/gns.cu $(PKG)/csrc/gns_kernels.cuh include/gns.h
+
+all: $(LIB) oracle/liboracle.so synth/libsynth.so
+
+$(LIB): $(SRCS)
+	$(NVCC) $(NVFLAGS) -o $@ $(PKG)/csrc/gns.cu
+
+oracle/liboracle.so: oracle/oracle.c
+	gcc -O2 -std=c11 -shared -fPIC -o $@ $<
+
+synth/libsynth.so: synth/gen.c
+	gcc -O2 -std=c11 -shared -fPIC -o $@ $<
+
+ptxas: $(SRCS)
+	$(NVCC) $(NVFLAGS) -Xptxas -v -o /tmp/gns_ptxas.so $(PKG)/csrc/gns.cu 2>&1 | grep -E "Function properties|registers|spill|Compiling entry" 
+
+sass: $(LIB)
+	/usr/local/cuda/bin/cuobjdump -sass $(LIB)
+
+clean:
+	rm -f $(LIB) oracle/liboracle.so synth/libsynth.so
+
+.PHONY: all ptxas sass clean

@@ -1,0 +1,487 @@
+#!/usr/bin/env python3
+"""bench.py — headline benchmark of the B200-native stable f64 mergesort.
+
+Metric (BASELINE.json): sorted keys/s at n = 2^24 f64 (configs[1]: U(0,1),
+key-only, buffer fraction 1.0) and its HBM-roofline fraction; tFootprint =
+%RAM x time.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config 2] [--frac 1.0] [--no-footprint]
+
+One process per GPU (torchrun for N > 1).  The sort does not shard without an
+exchange step: N > 1 runs N independent replicas, one per GPU,
+"scaling": "weak".  Timing: W untimed warm-up steps; each timed step restores
+the unsorted input (untimed D2D copy) and flushes L2 (untimed 256 MiB write),
+then CUDA events on the sort's stream bracket exactly one sort; the K step
+times are summed; barrier + synchronize on both sides; max over ranks.
+
+The oracle (oracle/) is executed only in the cpu_baseline leg and by
+--impl reference, on the host cores, never on the GPU path.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402  (inputs only; holds none of the method)
+
+METRIC = "sorted keys/sec at n=2^24 f64 (and HBM roofline %); tFootprint=%RAM x time"
+UNIT = "keys/s"
+FALLBACK_HBM_GBS = 6650.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", type=int, default=2, help="BASELINE config index (1..5)")
+    ap.add_argument("--sub", default="asc", help="config 4 sub-pattern")
+    ap.add_argument("--frac", type=float, default=1.0)
+    ap.add_argument("--no-footprint", action="store_true",
+                    help="skip the config-5 tFootprint comparison (1.0 vs 0.5)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-only", action="store_true",
+                    help="one warm-up + one sort, no timing loops (for ncu)")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return rank, world, local
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy read+write)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md: 6.65 TB/s)"
+
+
+def workload(cfg: int, sub: str, frac: float, rank: int):
+    case = synth.config(cfg, sub)
+    if rank:   # weak-scaling replicas: each rank its own seeded input of the same recipe
+        n = case.keys.size
+        case.keys = {1: synth.permutation, 2: synth.uniform, 3: lambda n, s: synth.ties(n, s, 24),
+                     5: synth.uniform}.get(cfg, lambda n, s: case.keys)(n, 1000 * cfg + 7919 * rank)
+    return case
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+            time.sleep(0.25)
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = max(mx, float(f[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------- reference arm
+def run_reference(args, rank, world):
+    """--impl reference: the CPU oracle (this tier's reference arm), rank 0 only."""
+    if rank != 0:
+        return
+    import oracle
+    case = synth.config(args.config, args.sub)
+    n = case.keys.size
+    sample_n = min(n, 1 << 22)
+    keys = case.keys[:sample_n].copy()
+    vals = None if case.vals is None else case.vals[:sample_n].copy()
+    for _ in range(args.warmup if args.warmup < 2 else 1):
+        oracle.sort(keys, vals)
+    t = 0.0
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        oracle.sort(keys, vals)
+        t += time.perf_counter() - t0
+    v = sample_n * args.steps / t
+    sample = (f"each step: oracle stable mergesort of the first 2^{sample_n.bit_length() - 1} keys of "
+              f"{case.name} on 1 host core (warm-up {min(args.warmup, 1)} step)")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": config_json(case, args.frac),
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def config_json(case, frac):
+    n = case.keys.size
+    return {"workload": f"{case.name}: n=2^{n.bit_length() - 1} f64 keys"
+                        f"{' + u32 payload' if case.vals is not None else ' key-only'}, buffer fraction {frac}",
+            "n": n, "payload": case.vals is not None, "buffer_fraction": frac, "shape": case.shape,
+            "l2": "flushed (256 MiB write) before every timed step",
+            "input_restore": "untimed device-to-device copy of the unsorted input before every timed step"}
+
+
+# --------------------------------------------------------------------- ours
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import paper_2402_01816_b200 as gns
+
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py needs a CUDA GPU (no CPU fallback)")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+        pg = dist
+
+    case = workload(args.config, args.sub, args.frac, rank)
+    n = case.keys.size
+    hv = case.vals is not None
+    s = 12 if hv else 8
+    plan = gns.plan(n, args.frac, hv)
+    stream = torch.cuda.current_stream(dev)
+    st = int(stream.cuda_stream)
+
+    src_k = torch.from_numpy(case.keys).to(dev)
+    src_v = torch.from_numpy(case.vals).to(dev) if hv else None
+    k = torch.empty_like(src_k)
+    v = torch.empty_like(src_v) if hv else None
+    ws = gns.alloc_workspace(n, args.frac, hv, dev)
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    flush = torch.empty(max(256 << 20, 2 * l2), dtype=torch.uint8, device=dev)
+
+    def restore():
+        k.copy_(src_k)
+        if hv:
+            v.copy_(src_v)
+        flush.fill_(1)
+
+    def sort_once():
+        gns.sort_(k, v, args.frac, workspace=ws)
+
+    for _ in range(max(args.warmup, 3 if not args.profile_only else 1)):
+        restore()
+        sort_once()
+    torch.cuda.synchronize()
+    if args.profile_only:
+        restore()
+        sort_once()
+        torch.cuda.synchronize()
+        print(json.dumps({"profile_only": True, "n": n}))
+        return
+
+    # ---------------------------------------------------------- timed region
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if pg:
+        pg.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            restore()
+            ev[i][0].record(stream)
+            sort_once()
+            ev[i][1].record(stream)
+        torch.cuda.synchronize()
+    if pg:
+        pg.barrier()
+    t_ms = sum(a.elapsed_time(b) for a, b in ev)
+    t_max = t_ms
+    if pg:
+        tt = torch.tensor([t_ms], dtype=torch.float64, device=dev)
+        pg.all_reduce(tt, op=pg.ReduceOp.MAX)
+        t_max = float(tt.item())
+    value = world * n * args.steps / (t_max / 1e3)
+    ms_per_step = t_max / args.steps
+
+    # validity of the last output: GPU-side properties only (the oracle is not
+    # used here): non-decreasing, same multiset of key bits (two wrapping
+    # moment hashes), and for index payloads: ties in ascending index order.
+    ok_sorted = bool((k[1:] >= k[:-1]).all().item()) if n > 1 else True
+    kb, sb = k.view(torch.int64), src_k.view(torch.int64)
+    ok_perm = bool((kb.sum() == sb.sum()).item() and ((kb * kb).sum() == (sb * sb).sum()).item())
+    if hv and n > 1:
+        tie = k[1:] == k[:-1]
+        ok_perm = ok_perm and bool((v[1:].to(torch.int64)[tie] > v[:-1].to(torch.int64)[tie]).all().item())
+
+    # ------------------------------------------- per-kernel timing (roofline)
+    roof = kernel_roofline(gns, torch, dev, stream, src_k, src_v, k, v, n, hv, s, plan, restore)
+    peak, peak_src = measured_peaks()
+    achieved = roof["merge_pass_gbs"]
+    traffic = ncu_traffic(case, args.frac)
+
+    # ----------------------------------------------------------- end-to-end
+    e2e = end_to_end(gns, torch, dev, stream, case, args, n, hv, ws)
+
+    footprint = None
+    if rank == 0 and world == 1 and not args.no_footprint and args.config == 2:
+        footprint = footprint_cfg5(gns, torch, dev, stream, flush)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(case)
+
+    launches_per_step = launches(plan, args.frac, n)
+    ram = 1.0 + plan["workspace_bytes"] / (n * s)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded SplitMix64, see DESIGN.md §3)",
+        "config": dict(config_json(case, args.frac), parallelism=f"replicas{world}" if world > 1 else "single"),
+        "roofline": {"bound": "hbm", "kernel": "merge pass (K2 partition + K3 merge), avg over "
+                     f"{plan['merge_passes']} passes", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": 2 * n * s,
+                     "share_of_step": roof["merge_share"],
+                     "whole_sort": {"bytes_lower_bound": plan["bytes_lower_bound"], "hbm_passes": plan["hbm_passes"],
+                                    "achieved": plan["bytes_lower_bound"] / (ms_per_step / 1e3) / 1e9,
+                                    "frac": plan["bytes_lower_bound"] / (ms_per_step / 1e3) / 1e9 / peak},
+                     "per_kernel_ms": roof["per_kernel_ms"]},
+        "e2e": e2e,
+        "gpu_launches": launches_per_step * args.steps,
+        "clocks": clk.summary(),
+        "ram_pct": ram, "tfootprint_ms": ram * ms_per_step,
+        "valid": {"sorted": ok_sorted, "same_multiset_and_stable_ties": ok_perm},
+    }
+    if cpu:
+        line["cpu_baseline"] = cpu
+    if footprint:
+        line["footprint_cfg5"] = footprint
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if pg:
+        pg.barrier()
+        pg.destroy_process_group()
+
+
+def launches(plan, frac, n):
+    T = plan["tile"]
+    if n <= 1:
+        return 0
+    if n <= T:
+        return 1
+    if frac == 1.0:
+        return 1 + 2 * plan["merge_passes"]
+    nl = plan["left_len"]
+    nr = n - nl
+
+    def lr(m):
+        r = -(-m // T)
+        return 1 + 2 * max(0, (r - 1).bit_length()) if m > 0 else 0
+    return lr(nl) + lr(nr) + 3   # + partition, deps, top merge (memset is a copy-engine op)
+
+
+def kernel_roofline(gns, torch, dev, stream, src_k, src_v, k, v, n, hv, s, plan, restore, reps=5):
+    """Times each kernel of a 1.0-mode sort through the step-level C-ABI, with
+    CUDA events on the launching stream between launches (same kernels and
+    order as gns_sort: tile sort, then merge passes ping-ponging)."""
+    st = int(stream.cuda_stream)
+    T = plan["tile"]
+    M = plan["merge_passes"]
+    buf_k = torch.empty_like(k)
+    buf_v = torch.empty_like(v) if hv else None
+    mws = torch.empty(max(1, gns.gns_merge_workspace_bytes(n)), dtype=torch.uint8, device=dev)
+    tile_ms, merge_ms = [], []
+    for _ in range(reps):
+        restore()
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(M + 2)]
+        cur_k, cur_v, oth_k, oth_v = (k, v, buf_k, buf_v) if M % 2 == 0 else (buf_k, buf_v, k, v)
+        evs[0].record(stream)
+        rc = gns.gns_tile_sort(k.data_ptr(), v.data_ptr() if hv else None, cur_k.data_ptr(),
+                               cur_v.data_ptr() if hv else None, n, st)
+        assert rc == 0, gns.gns_last_error_string()
+        evs[1].record(stream)
+        for p in range(M):
+            rc = gns.gns_merge_pass(cur_k.data_ptr(), cur_v.data_ptr() if hv else None, oth_k.data_ptr(),
+                                    oth_v.data_ptr() if hv else None, n, T << p, mws.data_ptr(),
+                                    mws.numel(), st)
+            assert rc == 0, gns.gns_last_error_string()
+            evs[p + 2].record(stream)
+            cur_k, cur_v, oth_k, oth_v = oth_k, oth_v, cur_k, cur_v
+        torch.cuda.synchronize()
+        tile_ms.append(evs[0].elapsed_time(evs[1]))
+        merge_ms.append([evs[p + 1].elapsed_time(evs[p + 2]) for p in range(M)])
+    tile = float(np.median(tile_ms))
+    per_pass = [float(np.median([r[p] for r in merge_ms])) for p in range(M)]
+    mavg = float(np.mean(per_pass)) if M else 0.0
+    total = tile + sum(per_pass)
+    return {"merge_pass_gbs": (2 * n * s) / (mavg / 1e3) / 1e9 if M else 0.0,
+            "merge_share": sum(per_pass) / total if total else 0.0,
+            "per_kernel_ms": {"tile_sort": tile, "merge_passes": per_pass,
+                              "tile_sort_gbs": (2 * n * s) / (tile / 1e3) / 1e9}}
+
+
+def ncu_traffic(case, frac):
+    """DRAM bytes per merge-pass launch from the committed ncu --set full
+    summary for this workload (profiles/ncu_merge_traffic.json), or None."""
+    p = os.path.join(ROOT, "profiles", "ncu_merge_traffic.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        if d.get("n") == case.keys.size and d.get("payload") == (case.vals is not None):
+            return d["dram_bytes_per_launch"]
+    except Exception:
+        pass
+    return None
+
+
+def end_to_end(gns, torch, dev, stream, case, args, n, hv, ws, steps=None):
+    """Same metric through the public C-ABI call, from pinned host memory:
+    H2D copy of the input, the sort, D2H copy of the sorted result, all inside
+    the timed region."""
+    steps = steps or max(3, min(args.steps, 10))
+    hk = torch.from_numpy(case.keys).pin_memory()
+    hv_ = torch.from_numpy(case.vals).pin_memory() if hv else None
+    ok = torch.empty(n, dtype=torch.float64).pin_memory()
+    ov = torch.empty(n, dtype=torch.uint32).pin_memory() if hv else None
+    dk = torch.empty(n, dtype=torch.float64, device=dev)
+    dv = torch.empty(n, dtype=torch.uint32, device=dev) if hv else None
+
+    def step():
+        dk.copy_(hk, non_blocking=True)
+        if hv:
+            dv.copy_(hv_, non_blocking=True)
+        gns.sort_(dk, dv, args.frac, workspace=ws)
+        ok.copy_(dk, non_blocking=True)
+        if hv:
+            ov.copy_(dv, non_blocking=True)
+
+    step()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(steps):
+        step()
+    b.record(stream)
+    torch.cuda.synchronize()
+    t = a.elapsed_time(b) / 1e3
+    by = n * (12 if hv else 8)
+    return {"value": n * steps / t, "unit": UNIT, "h2d_bytes_per_step": by, "d2h_bytes_per_step": by,
+            "steps": steps, "path": "pinned host -> gns_sort_f64_ws -> pinned host"}
+
+
+def footprint_cfg5(gns, torch, dev, stream, flush, reps=5):
+    """configs[4]: n = 2^27 U(0,1) + u32 index, buffer 1.0 vs 0.5: runtime,
+    %RAM (nominal = exact workspace bytes) and tFootprint."""
+    case = synth.config(5)
+    n = case.keys.size
+    src_k = torch.from_numpy(case.keys).to(dev)
+    src_v = torch.from_numpy(case.vals).to(dev)
+    k, v = torch.empty_like(src_k), torch.empty_like(src_v)
+    out = {"workload": "cfg5: n=2^27 f64 U(0,1) + u32 index", "n": n}
+    first = None
+    for frac in (1.0, 0.5):
+        ws = gns.alloc_workspace(n, frac, True, dev)
+        times = []
+        for i in range(reps + 2):
+            k.copy_(src_k)
+            v.copy_(src_v)
+            flush.fill_(1)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            gns.sort_(k, v, frac, workspace=ws)
+            b.record(stream)
+            torch.cuda.synchronize()
+            if i >= 2:
+                times.append(a.elapsed_time(b))
+        if first is None:
+            first = k.clone(), v.clone()
+        else:
+            same = bool(torch.equal(first[0].view(torch.int64), k.view(torch.int64)) and
+                        torch.equal(first[1].view(torch.int32), v.view(torch.int32)))
+            out["modes_agree_bitexact"] = same
+        ram = 1.0 + ws.numel() / (n * 12)
+        ms = float(np.median(times))
+        out[str(frac)] = {"ms": ms, "keys_per_s": n / (ms / 1e3), "ram_pct": ram,
+                          "tfootprint_ms": ram * ms, "workspace_bytes": int(ws.numel())}
+        del ws
+    out["tfootprint_0.5_lt_1.0"] = out["0.5"]["tfootprint_ms"] < out["1.0"]["tfootprint_ms"]
+    return out
+
+
+def cpu_baseline(case):
+    """The oracle, as it stands, on the host: the full workload sorted 3x on 1
+    core (~10 s)."""
+    import oracle
+    keys = case.keys
+    vals = case.vals
+    reps = 3
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        oracle.sort(keys, vals)
+    t = time.perf_counter() - t0
+    return {"value": keys.size * reps / t, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"{case.name}, full n={keys.size}, sorted {reps}x by the single-threaded oracle "
+                      f"(host has {os.cpu_count()} cores)"}
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,135 @@
+/*
+ * gns.h — C-ABI of the B200-native greeNsort hot path (arXiv 2402.01816).
+ *
+ * What the library computes: the STABLE ASCENDING sort ("AscLeft") of n
+ * contiguous IEEE binary64 keys in device memory, optionally moving a u32
+ * payload with each key, by binary divide&conquer merge sort under a buffer
+ * budget.  Citations are PAPER.md (= /root/reference/PAPER.md) line numbers:
+ *   - sorting = rearrangement into ascending order, stable: ties keep their
+ *     input order left to right (§Definition of sorting, Knuth's
+ *     definition, target "AscLeft");
+ *   - keys compare by IEEE `<`: -0.0 == +0.0, stability fixes their order, and
+ *     every output key keeps its input bits;
+ *   - per merge level one read-scan with comparisons and one write-scan
+ *     (§Merging or partitioning?), alternating between data and a
+ *     100% buffer (Nocopy-Mergesort) with Knuth's merge, the left
+ *     run winning ties ("Knuthsort");
+ *   - buffer fraction 0.5: the left half is sorted into a half-size buffer, the
+ *     right half in place, then both are merged back into the data
+ *     (Timsort's <=50% buffer merge; Frogsort's "50% or less
+ *     local buffer", PAPER.md:13/260/291; buffer sharing between branches as in
+ *     Frogsort3) so %RAM = (dataRAM+bufferRAM)/dataRAM
+ *      is 1.5 instead of 2.0.
+ *
+ * Conventions for every entry point:
+ *   - Pointers named keys/vals/src/dst/ws are DEVICE pointers.  The caller owns
+ *     them; they must stay valid and untouched until the enqueued work on
+ *     `stream` completes.
+ *   - keys and vals must be 32-byte aligned (cudaMalloc / torch give >= 256 B);
+ *     otherwise GNS_ERR_MISALIGNED.
+ *   - Every call is asynchronous on `stream` (0 = legacy default stream): a
+ *     return of GNS_OK means the kernels are enqueued.  No host sync, except
+ *     that the non-_ws sorts allocate their buffer stream-ordered
+ *     (cudaMallocAsync/cudaFreeAsync on `stream`).
+ *   - Argument errors are detected before anything is enqueued: the data is
+ *     untouched.  GNS_ERR_CUDA reports a launch/runtime error; the message is
+ *     in gns_last_error_string() (thread-local).
+ *   - NaN keys are a precondition violation: the contents of keys/vals after
+ *     the call are then unspecified, but every access stays inside
+ *     keys/vals/the buffer and the call terminates.
+ *   - n in {0, 1} returns GNS_OK with no launch; pointers may be NULL if n == 0.
+ *   - Reentrant: no global mutable state; concurrent calls on different streams
+ *     with disjoint buffers are allowed.
+ */
+#ifndef GNS_H
+#define GNS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st *gns_stream_t;   /* == cudaStream_t */
+
+typedef enum {
+    GNS_OK = 0,
+    GNS_ERR_INVALID_ARGUMENT = 1,      /* NULL pointer with n > 0, n > GNS_MAX_N, bad run_len */
+    GNS_ERR_UNSUPPORTED_FRACTION = 2,  /* buffer_fraction not exactly 1.0 or 0.5               */
+    GNS_ERR_OUT_OF_MEMORY = 3,         /* buffer allocation failed; input untouched            */
+    GNS_ERR_CUDA = 4,                  /* CUDA launch/runtime error                             */
+    GNS_ERR_WORKSPACE_TOO_SMALL = 5,   /* ws NULL or ws_bytes < gns_workspace_bytes(...)        */
+    GNS_ERR_MISALIGNED = 6             /* keys/vals/ws not 32-byte aligned                      */
+} gns_status;
+
+#define GNS_MAX_N ((size_t)0x7FFFFFFF)   /* 2^31 - 1 elements */
+
+/* ---- the sort (rows a1-a7 of SURVEY.md §8) -------------------------------
+ * keys[0:n) (and vals[0:n)) are replaced by their stable ascending sort.
+ * buffer_fraction: 1.0 -> buffer of n elements (%RAM 2.0);
+ *                  0.5 -> buffer of ceil(n/2) elements rounded up to 32
+ *                         (%RAM 1.5 for even n >= 64).
+ * For n <= GNS_TILE the sort runs in place with no buffer in either mode. */
+gns_status gns_sort_f64(double *keys, size_t n, double buffer_fraction, gns_stream_t stream);
+gns_status gns_sort_pairs_f64_u32(double *keys, uint32_t *vals, size_t n,
+                                  double buffer_fraction, gns_stream_t stream);
+
+/* Caller-owned workspace variants: ws must hold gns_workspace_bytes(...)
+ * bytes (32-byte aligned).  ws is the whole bufferRAM of the call. */
+size_t gns_workspace_bytes(size_t n, double buffer_fraction, int with_vals);
+gns_status gns_sort_f64_ws(double *keys, size_t n, double buffer_fraction,
+                           void *ws, size_t ws_bytes, gns_stream_t stream);
+gns_status gns_sort_pairs_f64_u32_ws(double *keys, uint32_t *vals, size_t n,
+                                     double buffer_fraction, void *ws, size_t ws_bytes,
+                                     gns_stream_t stream);
+
+/* Pass schedule of a sort (host only, no CUDA call). */
+typedef struct {
+    int tile;                   /* GNS_TILE: elements per tile-sort CTA                  */
+    int merge_tile;             /* elements per merge CTA                                 */
+    int merge_passes;           /* HBM merge passes (1.0 mode; the 0.5 mode has the same) */
+    int hbm_passes;             /* P = 1 (tile sort) + merge_passes                       */
+    size_t left_len;            /* 0.5 mode: elements sorted into the buffer (nl)         */
+    size_t workspace_bytes;     /* = gns_workspace_bytes(n, fraction, with_vals)          */
+    size_t buffer_elems;        /* key(+val) slots in the workspace (bufferRAM / s)       */
+    size_t bytes_lower_bound;   /* P * 2 * n * s, s = 8 or 12: the algorithmic bytes      */
+} gns_plan_info;
+gns_status gns_plan(size_t n, double buffer_fraction, int with_vals, gns_plan_info *out);
+
+/* ---- the steps, exposed for per-step parity tests and per-kernel timing -- */
+
+/* Row a2 (K1): stable sort of each GNS_TILE-element tile of src into the same
+ * range of dst (dst == src allowed; otherwise the ranges must not overlap).
+ * vals may both be NULL (key-only). */
+gns_status gns_tile_sort(const double *src_keys, const uint32_t *src_vals,
+                         double *dst_keys, uint32_t *dst_vals, size_t n, gns_stream_t stream);
+
+/* Rows a3+a4 (K2+K3): one merge level.  For q = 0,1,..: merges the sorted runs
+ * src[2qL : 2qL+L) and src[2qL+L : 2qL+2L) (clipped to n) into dst[2qL : ..).
+ * run_len L must be a positive multiple of GNS_TILE.  src and dst must not
+ * overlap.  ws: >= gns_merge_workspace_bytes(n) bytes (co-rank array). */
+size_t gns_merge_workspace_bytes(size_t n);
+gns_status gns_merge_pass(const double *src_keys, const uint32_t *src_vals,
+                          double *dst_keys, uint32_t *dst_vals, size_t n, size_t run_len,
+                          void *ws, size_t ws_bytes, gns_stream_t stream);
+
+/* Row a6 (K2+K4): ordered in-place top merge of the 0.5 mode.  left_keys[0:nl)
+ * (a separate buffer) and keys[nl:n) are sorted runs; the stable merge (left
+ * wins ties) is written to keys[0:n).  Requires nl >= n - nl, nl % 32 == 0 and
+ * left_* not overlapping keys/vals.  ws: >= gns_merge_workspace_bytes(n). */
+gns_status gns_merge_inplace_top(double *keys, uint32_t *vals, const double *left_keys,
+                                 const uint32_t *left_vals, size_t nl, size_t n,
+                                 void *ws, size_t ws_bytes, gns_stream_t stream);
+
+/* Compile-time geometry of this build. */
+int gns_tile_elems(void);
+int gns_merge_tile_elems(void);
+
+const char *gns_status_string(gns_status s);
+const char *gns_last_error_string(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GNS_H */

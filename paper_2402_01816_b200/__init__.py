@@ -1,0 +1,236 @@
+"""Thin Python binding of the C-ABI in ``include/gns.h`` (``libgns.so``).
+
+Argument marshalling only: every step of the sort runs in the CUDA kernels of
+``csrc/``.  There is no CPU fallback — importing this package without the
+built library raises, and every call with a non-OK status raises
+:class:`GnsError`.
+
+Names mirror the C entry points (``gns_sort_f64`` ...).  Each takes torch CUDA
+tensors (memory and streams are PyTorch's; the work is ours) and enqueues on
+``torch.cuda.current_stream()`` unless a stream is given.  Convenience:
+:func:`sort_` sorts ``keys`` (and ``vals``) in place.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libgns.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} is missing: build it with `make` or `python -c 'import __graft_entry__ as g; g.build()'`. "
+        "There is no CPU fallback.")
+
+_lib = ctypes.CDLL(LIB_PATH)
+
+GNS_OK = 0
+STATUS = {
+    0: "GNS_OK", 1: "GNS_ERR_INVALID_ARGUMENT", 2: "GNS_ERR_UNSUPPORTED_FRACTION",
+    3: "GNS_ERR_OUT_OF_MEMORY", 4: "GNS_ERR_CUDA", 5: "GNS_ERR_WORKSPACE_TOO_SMALL",
+    6: "GNS_ERR_MISALIGNED",
+}
+
+_vp = ctypes.c_void_p
+_sz = ctypes.c_size_t
+_d = ctypes.c_double
+_i = ctypes.c_int
+
+
+class gns_plan_info(ctypes.Structure):
+    _fields_ = [("tile", ctypes.c_int), ("merge_tile", ctypes.c_int),
+                ("merge_passes", ctypes.c_int), ("hbm_passes", ctypes.c_int),
+                ("left_len", _sz), ("workspace_bytes", _sz), ("buffer_elems", _sz),
+                ("bytes_lower_bound", _sz)]
+
+
+def _sig(name, argtypes, restype=ctypes.c_int):
+    f = getattr(_lib, name)
+    f.argtypes = argtypes
+    f.restype = restype
+    return f
+
+
+_c = {
+    "gns_sort_f64": _sig("gns_sort_f64", [_vp, _sz, _d, _vp]),
+    "gns_sort_pairs_f64_u32": _sig("gns_sort_pairs_f64_u32", [_vp, _vp, _sz, _d, _vp]),
+    "gns_workspace_bytes": _sig("gns_workspace_bytes", [_sz, _d, _i], _sz),
+    "gns_sort_f64_ws": _sig("gns_sort_f64_ws", [_vp, _sz, _d, _vp, _sz, _vp]),
+    "gns_sort_pairs_f64_u32_ws": _sig("gns_sort_pairs_f64_u32_ws", [_vp, _vp, _sz, _d, _vp, _sz, _vp]),
+    "gns_plan": _sig("gns_plan", [_sz, _d, _i, ctypes.POINTER(gns_plan_info)]),
+    "gns_tile_sort": _sig("gns_tile_sort", [_vp, _vp, _vp, _vp, _sz, _vp]),
+    "gns_merge_workspace_bytes": _sig("gns_merge_workspace_bytes", [_sz], _sz),
+    "gns_merge_pass": _sig("gns_merge_pass", [_vp, _vp, _vp, _vp, _sz, _sz, _vp, _sz, _vp]),
+    "gns_merge_inplace_top": _sig("gns_merge_inplace_top", [_vp, _vp, _vp, _vp, _sz, _sz, _vp, _sz, _vp]),
+    "gns_tile_elems": _sig("gns_tile_elems", []),
+    "gns_merge_tile_elems": _sig("gns_merge_tile_elems", []),
+    "gns_status_string": _sig("gns_status_string", [_i], ctypes.c_char_p),
+    "gns_last_error_string": _sig("gns_last_error_string", [], ctypes.c_char_p),
+}
+
+EXPORTED = tuple(_c)
+
+
+class GnsError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        self.status = status
+        msg = _c["gns_last_error_string"]().decode(errors="replace")
+        super().__init__(f"{where}: {STATUS.get(status, status)}: {msg}")
+
+
+def _check(rc: int, where: str) -> None:
+    if rc != GNS_OK:
+        raise GnsError(rc, where)
+
+
+# ----------------------------------------------------------- raw-pointer layer
+# The C names, taking integers (device pointers, sizes, a cudaStream_t handle).
+
+def gns_sort_f64(keys_ptr: int, n: int, buffer_fraction: float, stream: int) -> int:
+    return _c["gns_sort_f64"](keys_ptr, n, buffer_fraction, stream)
+
+
+def gns_sort_pairs_f64_u32(keys_ptr: int, vals_ptr: int, n: int, buffer_fraction: float, stream: int) -> int:
+    return _c["gns_sort_pairs_f64_u32"](keys_ptr, vals_ptr, n, buffer_fraction, stream)
+
+
+def gns_workspace_bytes(n: int, buffer_fraction: float, with_vals: bool) -> int:
+    return _c["gns_workspace_bytes"](n, buffer_fraction, int(bool(with_vals)))
+
+
+def gns_sort_f64_ws(keys_ptr, n, buffer_fraction, ws_ptr, ws_bytes, stream) -> int:
+    return _c["gns_sort_f64_ws"](keys_ptr, n, buffer_fraction, ws_ptr, ws_bytes, stream)
+
+
+def gns_sort_pairs_f64_u32_ws(keys_ptr, vals_ptr, n, buffer_fraction, ws_ptr, ws_bytes, stream) -> int:
+    return _c["gns_sort_pairs_f64_u32_ws"](keys_ptr, vals_ptr, n, buffer_fraction, ws_ptr, ws_bytes, stream)
+
+
+def gns_plan(n: int, buffer_fraction: float, with_vals: bool) -> gns_plan_info:
+    info = gns_plan_info()
+    _check(_c["gns_plan"](n, buffer_fraction, int(bool(with_vals)), ctypes.byref(info)), "gns_plan")
+    return info
+
+
+def gns_tile_sort(src_k, src_v, dst_k, dst_v, n, stream) -> int:
+    return _c["gns_tile_sort"](src_k, src_v, dst_k, dst_v, n, stream)
+
+
+def gns_merge_workspace_bytes(n: int) -> int:
+    return _c["gns_merge_workspace_bytes"](n)
+
+
+def gns_merge_pass(src_k, src_v, dst_k, dst_v, n, run_len, ws, ws_bytes, stream) -> int:
+    return _c["gns_merge_pass"](src_k, src_v, dst_k, dst_v, n, run_len, ws, ws_bytes, stream)
+
+
+def gns_merge_inplace_top(keys, vals, left_k, left_v, nl, n, ws, ws_bytes, stream) -> int:
+    return _c["gns_merge_inplace_top"](keys, vals, left_k, left_v, nl, n, ws, ws_bytes, stream)
+
+
+def gns_tile_elems() -> int:
+    return _c["gns_tile_elems"]()
+
+
+def gns_merge_tile_elems() -> int:
+    return _c["gns_merge_tile_elems"]()
+
+
+def gns_status_string(s: int) -> str:
+    return _c["gns_status_string"](s).decode()
+
+
+def gns_last_error_string() -> str:
+    return _c["gns_last_error_string"]().decode(errors="replace")
+
+
+# --------------------------------------------------------------- torch layer
+
+def _stream_handle(stream) -> int:
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+def _ptr(t) -> Optional[int]:
+    if t is None:
+        return None
+    return int(t.data_ptr())
+
+
+def _check_keys(keys, vals):
+    import torch
+    if keys.dtype != torch.float64 or not keys.is_cuda or not keys.is_contiguous():
+        raise TypeError("keys must be a contiguous CUDA float64 tensor")
+    if vals is not None:
+        if vals.dtype != torch.uint32 or not vals.is_cuda or not vals.is_contiguous():
+            raise TypeError("vals must be a contiguous CUDA uint32 tensor")
+        if vals.numel() != keys.numel():
+            raise ValueError("keys and vals differ in length")
+
+
+def sort_(keys, vals=None, buffer_fraction: float = 1.0, workspace=None, stream=None):
+    """Stable ascending in-place sort of ``keys`` (and ``vals``) on the GPU.
+
+    ``workspace``: optional uint8 CUDA tensor of >= workspace_bytes(...) bytes;
+    without it the library allocates its buffer stream-ordered."""
+    _check_keys(keys, vals)
+    n = keys.numel()
+    st = _stream_handle(stream)
+    if workspace is None:
+        if vals is None:
+            rc = gns_sort_f64(_ptr(keys), n, buffer_fraction, st)
+        else:
+            rc = gns_sort_pairs_f64_u32(_ptr(keys), _ptr(vals), n, buffer_fraction, st)
+    else:
+        wb = workspace.numel() * workspace.element_size()
+        if vals is None:
+            rc = gns_sort_f64_ws(_ptr(keys), n, buffer_fraction, _ptr(workspace), wb, st)
+        else:
+            rc = gns_sort_pairs_f64_u32_ws(_ptr(keys), _ptr(vals), n, buffer_fraction, _ptr(workspace), wb, st)
+    _check(rc, "sort_")
+    return keys, vals
+
+
+def workspace_bytes(n: int, buffer_fraction: float = 1.0, with_vals: bool = False) -> int:
+    return gns_workspace_bytes(n, buffer_fraction, with_vals)
+
+
+def alloc_workspace(n: int, buffer_fraction: float = 1.0, with_vals: bool = False, device="cuda"):
+    import torch
+    return torch.empty(max(1, workspace_bytes(n, buffer_fraction, with_vals)), dtype=torch.uint8, device=device)
+
+
+def tile_sort(src_k, src_v=None, dst_k=None, dst_v=None, stream=None):
+    """Row a2: sort each gns_tile_elems() tile of src into dst (default: in place)."""
+    _check_keys(src_k, src_v)
+    dst_k = src_k if dst_k is None else dst_k
+    dst_v = src_v if dst_v is None else dst_v
+    _check(gns_tile_sort(_ptr(src_k), _ptr(src_v), _ptr(dst_k), _ptr(dst_v), src_k.numel(),
+                         _stream_handle(stream)), "tile_sort")
+    return dst_k, dst_v
+
+
+def merge_pass(src_k, src_v, dst_k, dst_v, run_len: int, workspace, stream=None):
+    """Rows a3+a4: one merge level over runs of ``run_len`` (src -> dst)."""
+    _check_keys(src_k, src_v)
+    wb = workspace.numel() * workspace.element_size()
+    _check(gns_merge_pass(_ptr(src_k), _ptr(src_v), _ptr(dst_k), _ptr(dst_v), src_k.numel(), run_len,
+                          _ptr(workspace), wb, _stream_handle(stream)), "merge_pass")
+    return dst_k, dst_v
+
+
+def merge_inplace_top(keys, vals, left_k, left_v, nl: int, workspace, stream=None):
+    """Row a6: merge left_k[0:nl) (buffer) with keys[nl:n) into keys[0:n)."""
+    _check_keys(keys, vals)
+    wb = workspace.numel() * workspace.element_size()
+    _check(gns_merge_inplace_top(_ptr(keys), _ptr(vals), _ptr(left_k), _ptr(left_v), nl, keys.numel(),
+                                 _ptr(workspace), wb, _stream_handle(stream)), "merge_inplace_top")
+    return keys, vals
+
+
+def plan(n: int, buffer_fraction: float = 1.0, with_vals: bool = False) -> dict:
+    p = gns_plan(n, buffer_fraction, with_vals)
+    return {f: getattr(p, f) for f, _ in gns_plan_info._fields_}

@@ -1,0 +1,420 @@
+// gns.cu — host planner, launcher and C-ABI (include/gns.h) of the B200-native
+// stable f64 mergesort hot path (greeNsort, arXiv 2402.01816).
+//
+// Row a1 (validate & plan), a5 (0.5-mode orchestration), a7 (buffer
+// allocation and %RAM accounting) of SURVEY.md §8 live here; the kernels are in
+// gns_kernels.cuh.  Everything is enqueued on the caller's stream; nothing here
+// calls into the oracle or any CPU sort.
+#include "../../include/gns.h"
+#include "gns_kernels.cuh"
+
+#include <cuda_runtime.h>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+using namespace gns;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+gns_status fail(gns_status s, const char *msg)
+{
+    g_last_error = msg;
+    return s;
+}
+
+gns_status check(cudaError_t e, const char *where)
+{
+    if (e == cudaSuccess) return GNS_OK;
+    g_last_error = std::string(where) + ": " + cudaGetErrorString(e);
+    return GNS_ERR_CUDA;
+}
+
+#define GNS_TRY(expr)                        \
+    do {                                     \
+        gns_status _s = (expr);              \
+        if (_s != GNS_OK) return _s;         \
+    } while (0)
+
+inline size_t ceil_div(size_t a, size_t b) { return (a + b - 1) / b; }
+inline size_t align_up(size_t a, size_t b) { return ceil_div(a, b) * b; }
+
+int merge_passes_for(size_t n)
+{
+    if (n <= (size_t)TILE) return 0;
+    size_t runs = ceil_div(n, TILE);
+    int p = 0;
+    while (((size_t)1 << p) < runs) ++p;
+    return p;
+}
+
+// 0.5 mode split: the left (larger) half goes to the buffer.  Rounded up to 32
+// elements so that data + nl stays 256-byte (keys) / 128-byte (vals) aligned.
+size_t left_len(size_t n)
+{
+    size_t nl = align_up(ceil_div(n, 2), 32);
+    return nl < n ? nl : n;
+}
+
+bool is_aligned(const void *p, size_t a) { return ((uintptr_t)p % a) == 0; }
+
+// Workspace layout (one allocation = the whole bufferRAM of a call).
+struct Layout {
+    size_t buf_elems = 0;   // buffer key(+val) slots
+    size_t off_k = 0, off_v = 0, off_corank = 0, off_deps = 0, off_flags = 0, total = 0;
+    int ntiles = 0;         // merge tiles over the whole array
+};
+
+Layout layout(size_t n, bool half, bool hv)
+{
+    Layout L;
+    if (n <= (size_t)TILE) return L;   // one tile, sorted in place, no buffer
+    L.buf_elems = half ? left_len(n) : n;
+    L.ntiles = (int)ceil_div(n, MTILE);
+    size_t o = 0;
+    L.off_k = o;
+    o = align_up(o + L.buf_elems * sizeof(double), 256);
+    L.off_v = o;
+    if (hv) o = align_up(o + L.buf_elems * sizeof(uint32_t), 256);
+    L.off_corank = o;
+    o = align_up(o + (size_t)(L.ntiles + 1) * sizeof(int), 256);
+    L.off_deps = o;
+    if (half) o = align_up(o + (size_t)L.ntiles * sizeof(int2), 256);
+    L.off_flags = o;
+    if (half) o = align_up(o + (size_t)(L.ntiles + 1) * sizeof(unsigned), 256);
+    L.total = o;
+    return L;
+}
+
+// Size of the co-rank array only (gns_merge_pass / gns_merge_inplace_top).
+size_t merge_ws(size_t n)
+{
+    size_t nt = ceil_div(n, MTILE);
+    return align_up((nt + 1) * sizeof(int), 256) + align_up(nt * sizeof(int2), 256) +
+           align_up((nt + 1) * sizeof(unsigned), 256);
+}
+
+// Per-device one-time kernel attributes (dynamic shared memory > 48 KB).
+std::mutex g_attr_mu;
+unsigned long long g_attr_done = 0;   // bit per device ordinal
+
+gns_status ensure_attrs()
+{
+    int dev = 0;
+    GNS_TRY(check(cudaGetDevice(&dev), "cudaGetDevice"));
+    if (dev >= 64) return fail(GNS_ERR_CUDA, "device ordinal >= 64");
+    std::lock_guard<std::mutex> lk(g_attr_mu);
+    if (g_attr_done & (1ull << dev)) return GNS_OK;
+    const int k1 = (int)(K1_SMEM_KEYS + sizeof(uint32_t) * K1_SV);
+    const int k3 = (int)(K3_SMEM_KEYS + sizeof(uint32_t) * K3_SK);
+    GNS_TRY(check(cudaFuncSetAttribute(tile_sort_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, k1), "attr"));
+    GNS_TRY(check(cudaFuncSetAttribute(tile_sort_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, k1), "attr"));
+    GNS_TRY(check(cudaFuncSetAttribute(merge_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, k3), "attr"));
+    GNS_TRY(check(cudaFuncSetAttribute(merge_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, k3), "attr"));
+    GNS_TRY(check(cudaFuncSetAttribute(merge_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, k3), "attr"));
+    GNS_TRY(check(cudaFuncSetAttribute(merge_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, k3), "attr"));
+    g_attr_done |= (1ull << dev);
+    return GNS_OK;
+}
+
+// ------------------------------------------------------------------ launches
+gns_status launch_tile_sort(const double *sk, const uint32_t *sv, double *dk, uint32_t *dv, size_t n,
+                            cudaStream_t st)
+{
+    if (n == 0) return GNS_OK;
+    const unsigned grid = (unsigned)ceil_div(n, TILE);
+    const bool hv = sv != nullptr;
+    const size_t smem = K1_SMEM_KEYS + (hv ? sizeof(uint32_t) * K1_SV : 0);
+    if (hv) tile_sort_kernel<true><<<grid, NT, smem, st>>>(sk, sv, dk, dv, (long long)n);
+    else tile_sort_kernel<false><<<grid, NT, smem, st>>>(sk, nullptr, dk, nullptr, (long long)n);
+    return check(cudaGetLastError(), "tile_sort_kernel");
+}
+
+gns_status launch_merge(const MergeGeo &g, int *corank, int2 *deps, unsigned *flags, bool inplace,
+                        cudaStream_t st)
+{
+    const int ntiles = (int)ceil_div((size_t)g.n, MTILE);
+    const bool hv = g.av != nullptr;
+    partition_kernel<<<(unsigned)ceil_div((size_t)ntiles * 32, 256), 256, 0, st>>>(g, ntiles, corank);
+    GNS_TRY(check(cudaGetLastError(), "partition_kernel"));
+    const size_t smem = K3_SMEM_KEYS + (hv ? sizeof(uint32_t) * K3_SK : 0);
+    if (!inplace) {
+        if (hv) merge_kernel<true, false><<<ntiles, NT, smem, st>>>(g, corank, nullptr, nullptr, nullptr);
+        else merge_kernel<false, false><<<ntiles, NT, smem, st>>>(g, corank, nullptr, nullptr, nullptr);
+        return check(cudaGetLastError(), "merge_kernel");
+    }
+    inplace_deps_kernel<<<(unsigned)ceil_div(ntiles, 256), 256, 0, st>>>(corank, ntiles, g.L, g.n, deps);
+    GNS_TRY(check(cudaGetLastError(), "inplace_deps_kernel"));
+    GNS_TRY(check(cudaMemsetAsync(flags, 0, (size_t)(ntiles + 1) * sizeof(unsigned), st), "memset flags"));
+    unsigned *ticket = flags + ntiles;
+    if (hv) merge_kernel<true, true><<<ntiles, NT, smem, st>>>(g, corank, deps, flags, ticket);
+    else merge_kernel<false, true><<<ntiles, NT, smem, st>>>(g, corank, deps, flags, ticket);
+    return check(cudaGetLastError(), "merge_kernel<inplace>");
+}
+
+MergeGeo uniform_geo(const double *sk, const uint32_t *sv, double *dk, uint32_t *dv, size_t n, size_t L)
+{
+    MergeGeo g;
+    g.ak = sk;
+    g.av = sv;
+    g.bk = sk + L;
+    g.bv = sv ? sv + L : nullptr;
+    g.ok = dk;
+    g.ov = dv;
+    g.n = (long long)n;
+    g.L = (long long)L;
+    return g;
+}
+
+// Sorts region R = (rk, rv)[0:len) using partner region P of >= len slots as
+// ping-pong buffer (Nocopy-Mergesort).  The result ends in P if
+// `final_in_partner`, else in R.  Parity picks the tile-sort destination so
+// no copy pass is ever needed (an odd number of merge levels starts from P).
+gns_status sort_range(double *rk, uint32_t *rv, double *pk_, uint32_t *pv_, size_t len,
+                      bool final_in_partner, int *corank, cudaStream_t st)
+{
+    if (len == 0) return GNS_OK;
+    const int M = merge_passes_for(len);
+    const bool tile_to_partner = final_in_partner ^ (bool)(M & 1);
+    double *ck = tile_to_partner ? pk_ : rk;
+    uint32_t *cv = tile_to_partner ? pv_ : rv;
+    double *ok = tile_to_partner ? rk : pk_;
+    uint32_t *ov = tile_to_partner ? rv : pv_;
+    GNS_TRY(launch_tile_sort(rk, rv, ck, cv, len, st));
+    for (int p = 0; p < M; ++p) {
+        const size_t L = (size_t)TILE << p;
+        MergeGeo g = uniform_geo(ck, cv, ok, ov, len, L);
+        GNS_TRY(launch_merge(g, corank, nullptr, nullptr, false, st));
+        std::swap(ck, ok);
+        std::swap(cv, ov);
+    }
+    return GNS_OK;
+}
+
+gns_status validate_fraction(double f, bool *half)
+{
+    if (f == 1.0) { *half = false; return GNS_OK; }
+    if (f == 0.5) { *half = true; return GNS_OK; }
+    return fail(GNS_ERR_UNSUPPORTED_FRACTION, "buffer_fraction must be exactly 1.0 or 0.5");
+}
+
+gns_status validate_data(const double *keys, const uint32_t *vals, bool hv, size_t n)
+{
+    if (n > GNS_MAX_N) return fail(GNS_ERR_INVALID_ARGUMENT, "n > GNS_MAX_N");
+    if (n == 0) return GNS_OK;
+    if (!keys || (hv && !vals)) return fail(GNS_ERR_INVALID_ARGUMENT, "NULL keys/vals with n > 0");
+    if (!is_aligned(keys, 32) || (hv && !is_aligned(vals, 32)))
+        return fail(GNS_ERR_MISALIGNED, "keys/vals must be 32-byte aligned");
+    return GNS_OK;
+}
+
+// The sort proper (rows a1..a7).  ws already validated and sized.
+gns_status run_sort(double *keys, uint32_t *vals, size_t n, bool half, unsigned char *ws, cudaStream_t st)
+{
+    if (n <= 1) return GNS_OK;
+    GNS_TRY(ensure_attrs());
+    const bool hv = vals != nullptr;
+    if (n <= (size_t)TILE)   // one tile: in place, no buffer
+        return launch_tile_sort(keys, vals, keys, vals, n, st);
+    const Layout Lo = layout(n, half, hv);
+    double *bk = reinterpret_cast<double *>(ws + Lo.off_k);
+    uint32_t *bv = hv ? reinterpret_cast<uint32_t *>(ws + Lo.off_v) : nullptr;
+    int *corank = reinterpret_cast<int *>(ws + Lo.off_corank);
+    if (!half) return sort_range(keys, vals, bk, bv, n, false, corank, st);
+
+    // 0.5 mode (row a5): left half -> buffer, right half in place with the
+    // dead left region as its partner, then the ordered in-place top merge.
+    const size_t nl = left_len(n), nr = n - nl;
+    GNS_TRY(sort_range(keys, vals, bk, bv, nl, true, corank, st));
+    GNS_TRY(sort_range(keys + nl, hv ? vals + nl : nullptr, keys, vals, nr, false, corank, st));
+    MergeGeo g;
+    g.ak = bk;
+    g.av = bv;
+    g.bk = keys + nl;
+    g.bv = hv ? vals + nl : nullptr;
+    g.ok = keys;
+    g.ov = vals;
+    g.n = (long long)n;
+    g.L = (long long)nl;
+    int2 *deps = reinterpret_cast<int2 *>(ws + Lo.off_deps);
+    unsigned *flags = reinterpret_cast<unsigned *>(ws + Lo.off_flags);
+    return launch_merge(g, corank, deps, flags, true, st);
+}
+
+gns_status sort_alloc(double *keys, uint32_t *vals, bool hv, size_t n, double frac, cudaStream_t st)
+{
+    bool half = false;
+    GNS_TRY(validate_fraction(frac, &half));
+    GNS_TRY(validate_data(keys, vals, hv, n));
+    if (n <= 1) return GNS_OK;
+    const Layout Lo = layout(n, half, hv);
+    unsigned char *ws = nullptr;
+    if (Lo.total) {
+        cudaError_t e = cudaMallocAsync((void **)&ws, Lo.total, st);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            if (e == cudaErrorMemoryAllocation) return fail(GNS_ERR_OUT_OF_MEMORY, "cudaMallocAsync: out of memory");
+            return check(e, "cudaMallocAsync");
+        }
+    }
+    gns_status s = run_sort(keys, hv ? vals : nullptr, n, half, ws, st);
+    if (ws) {
+        gns_status f = check(cudaFreeAsync(ws, st), "cudaFreeAsync");
+        if (s == GNS_OK) s = f;
+    }
+    return s;
+}
+
+gns_status sort_ws(double *keys, uint32_t *vals, bool hv, size_t n, double frac, void *ws, size_t ws_bytes,
+                   cudaStream_t st)
+{
+    bool half = false;
+    GNS_TRY(validate_fraction(frac, &half));
+    GNS_TRY(validate_data(keys, vals, hv, n));
+    if (n <= 1) return GNS_OK;
+    const Layout Lo = layout(n, half, hv);
+    if (Lo.total) {
+        if (!ws || ws_bytes < Lo.total) return fail(GNS_ERR_WORKSPACE_TOO_SMALL, "workspace too small");
+        if (!is_aligned(ws, 32)) return fail(GNS_ERR_MISALIGNED, "ws must be 32-byte aligned");
+    }
+    return run_sort(keys, hv ? vals : nullptr, n, half, (unsigned char *)ws, st);
+}
+
+}  // namespace
+
+// ======================================================================= C-ABI
+extern "C" {
+
+gns_status gns_sort_f64(double *keys, size_t n, double buffer_fraction, gns_stream_t stream)
+{
+    return sort_alloc(keys, nullptr, false, n, buffer_fraction, (cudaStream_t)stream);
+}
+
+gns_status gns_sort_pairs_f64_u32(double *keys, uint32_t *vals, size_t n, double buffer_fraction,
+                                  gns_stream_t stream)
+{
+    return sort_alloc(keys, vals, true, n, buffer_fraction, (cudaStream_t)stream);
+}
+
+size_t gns_workspace_bytes(size_t n, double buffer_fraction, int with_vals)
+{
+    bool half = false;
+    if (validate_fraction(buffer_fraction, &half) != GNS_OK || n > GNS_MAX_N) return 0;
+    return layout(n, half, with_vals != 0).total;
+}
+
+gns_status gns_sort_f64_ws(double *keys, size_t n, double buffer_fraction, void *ws, size_t ws_bytes,
+                           gns_stream_t stream)
+{
+    return sort_ws(keys, nullptr, false, n, buffer_fraction, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+gns_status gns_sort_pairs_f64_u32_ws(double *keys, uint32_t *vals, size_t n, double buffer_fraction,
+                                     void *ws, size_t ws_bytes, gns_stream_t stream)
+{
+    return sort_ws(keys, vals, true, n, buffer_fraction, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+gns_status gns_plan(size_t n, double buffer_fraction, int with_vals, gns_plan_info *out)
+{
+    bool half = false;
+    GNS_TRY(validate_fraction(buffer_fraction, &half));
+    if (!out) return fail(GNS_ERR_INVALID_ARGUMENT, "out == NULL");
+    if (n > GNS_MAX_N) return fail(GNS_ERR_INVALID_ARGUMENT, "n > GNS_MAX_N");
+    const Layout Lo = layout(n, half, with_vals != 0);
+    const size_t s = with_vals ? 12 : 8;
+    std::memset(out, 0, sizeof(*out));
+    out->tile = TILE;
+    out->merge_tile = MTILE;
+    out->merge_passes = merge_passes_for(n);
+    out->hbm_passes = n > 1 ? 1 + out->merge_passes : 0;
+    out->left_len = (half && n > (size_t)TILE) ? left_len(n) : 0;
+    out->workspace_bytes = Lo.total;
+    out->buffer_elems = Lo.buf_elems;
+    out->bytes_lower_bound = (size_t)out->hbm_passes * 2 * n * s;
+    return GNS_OK;
+}
+
+gns_status gns_tile_sort(const double *src_keys, const uint32_t *src_vals, double *dst_keys,
+                         uint32_t *dst_vals, size_t n, gns_stream_t stream)
+{
+    const bool hv = src_vals != nullptr || dst_vals != nullptr;
+    if (hv && (!src_vals || !dst_vals)) return fail(GNS_ERR_INVALID_ARGUMENT, "src_vals/dst_vals: both or neither");
+    GNS_TRY(validate_data(src_keys, src_vals, hv, n));
+    GNS_TRY(validate_data(dst_keys, dst_vals, hv, n));
+    if (n == 0) return GNS_OK;
+    GNS_TRY(ensure_attrs());
+    return launch_tile_sort(src_keys, src_vals, dst_keys, dst_vals, n, (cudaStream_t)stream);
+}
+
+size_t gns_merge_workspace_bytes(size_t n) { return merge_ws(n); }
+
+gns_status gns_merge_pass(const double *src_keys, const uint32_t *src_vals, double *dst_keys,
+                          uint32_t *dst_vals, size_t n, size_t run_len, void *ws, size_t ws_bytes,
+                          gns_stream_t stream)
+{
+    const bool hv = src_vals != nullptr || dst_vals != nullptr;
+    if (hv && (!src_vals || !dst_vals)) return fail(GNS_ERR_INVALID_ARGUMENT, "src_vals/dst_vals: both or neither");
+    GNS_TRY(validate_data(src_keys, src_vals, hv, n));
+    GNS_TRY(validate_data(dst_keys, dst_vals, hv, n));
+    if (run_len == 0 || run_len % TILE != 0 || run_len > (size_t)1 << 30)
+        return fail(GNS_ERR_INVALID_ARGUMENT, "run_len must be a positive multiple of gns_tile_elems() <= 2^30");
+    if (n == 0) return GNS_OK;
+    if (!ws || ws_bytes < merge_ws(n)) return fail(GNS_ERR_WORKSPACE_TOO_SMALL, "workspace too small");
+    GNS_TRY(ensure_attrs());
+    MergeGeo g = uniform_geo(src_keys, src_vals, dst_keys, dst_vals, n, run_len);
+    return launch_merge(g, (int *)ws, nullptr, nullptr, false, (cudaStream_t)stream);
+}
+
+gns_status gns_merge_inplace_top(double *keys, uint32_t *vals, const double *left_keys,
+                                 const uint32_t *left_vals, size_t nl, size_t n, void *ws, size_t ws_bytes,
+                                 gns_stream_t stream)
+{
+    const bool hv = vals != nullptr || left_vals != nullptr;
+    if (hv && (!vals || !left_vals)) return fail(GNS_ERR_INVALID_ARGUMENT, "vals/left_vals: both or neither");
+    GNS_TRY(validate_data(keys, vals, hv, n));
+    GNS_TRY(validate_data(left_keys, left_vals, hv, nl));
+    if (nl > n || nl < n - nl || nl % 32 != 0 || nl == 0)
+        return fail(GNS_ERR_INVALID_ARGUMENT, "need n-nl <= nl <= n, nl % 32 == 0, nl > 0");
+    if (!ws || ws_bytes < merge_ws(n)) return fail(GNS_ERR_WORKSPACE_TOO_SMALL, "workspace too small");
+    GNS_TRY(ensure_attrs());
+    const size_t nt = ceil_div(n, MTILE);
+    unsigned char *w = (unsigned char *)ws;
+    int *corank = (int *)w;
+    int2 *deps = (int2 *)(w + align_up((nt + 1) * sizeof(int), 256));
+    unsigned *flags = (unsigned *)((unsigned char *)deps + align_up(nt * sizeof(int2), 256));
+    MergeGeo g;
+    g.ak = left_keys;
+    g.av = left_vals;
+    g.bk = keys + nl;
+    g.bv = hv ? vals + nl : nullptr;
+    g.ok = keys;
+    g.ov = vals;
+    g.n = (long long)n;
+    g.L = (long long)nl;
+    return launch_merge(g, corank, deps, flags, true, (cudaStream_t)stream);
+}
+
+int gns_tile_elems(void) { return TILE; }
+int gns_merge_tile_elems(void) { return MTILE; }
+
+const char *gns_status_string(gns_status s)
+{
+    switch (s) {
+    case GNS_OK: return "GNS_OK";
+    case GNS_ERR_INVALID_ARGUMENT: return "GNS_ERR_INVALID_ARGUMENT";
+    case GNS_ERR_UNSUPPORTED_FRACTION: return "GNS_ERR_UNSUPPORTED_FRACTION";
+    case GNS_ERR_OUT_OF_MEMORY: return "GNS_ERR_OUT_OF_MEMORY";
+    case GNS_ERR_CUDA: return "GNS_ERR_CUDA";
+    case GNS_ERR_WORKSPACE_TOO_SMALL: return "GNS_ERR_WORKSPACE_TOO_SMALL";
+    case GNS_ERR_MISALIGNED: return "GNS_ERR_MISALIGNED";
+    }
+    return "GNS_ERR_UNKNOWN";
+}
+
+const char *gns_last_error_string(void) { return g_last_error.c_str(); }
+
+}  // extern "C"

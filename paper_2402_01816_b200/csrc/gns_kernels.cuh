@@ -1,0 +1,400 @@
+// gns_kernels.cuh — sm_100a device code of the stable f64 mergesort hot path.
+//
+// Kernels (PAPER.md line cites in each):
+//   K1 tile_sort_kernel      (row a2) stable sort of one TILE-element tile per CTA
+//   K2 partition_kernel      (row a3) stable co-rank (merge-path) split per output tile
+//   K3 merge_kernel<.,false> (row a4) one merge level, src -> dst ping-pong
+//   K4 merge_kernel<.,true>  (row a6) ordered in-place top merge of the 0.5 mode
+//      inplace_deps_kernel   (row a6) which earlier tiles each K4 tile must wait for
+//
+// No code here is shared with oracle/ (the CPU oracle); the two are compared
+// only through their outputs.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace gns {
+
+constexpr int NT = 256;            // threads per CTA
+constexpr int VT = 16;             // items per thread
+constexpr int TILE = NT * VT;      // K1 tile = 4096 elements
+constexpr int MTILE = NT * VT;     // K3/K4 output tile = 4096 elements
+
+// Padded shared-memory index (K1 only): one pad slot per 16 doubles / 32 u32
+// so that the blocked accesses (thread t touches t*VT + v) are conflict free.
+__device__ __forceinline__ int pk(int e) { return e + (e >> 4); }
+__device__ __forceinline__ int pv(int e) { return e + (e >> 5); }
+constexpr int K1_SK = TILE + (TILE >> 4) + 4;
+constexpr int K1_SV = TILE + (TILE >> 5) + 4;
+constexpr size_t K1_SMEM_KEYS = sizeof(double) * K1_SK;
+constexpr size_t K3_SK = MTILE + 4;
+constexpr size_t K3_SMEM_KEYS = sizeof(double) * K3_SK;
+
+struct Ident { __device__ __forceinline__ int operator()(int e) const { return e; } };
+struct PadK { __device__ __forceinline__ int operator()(int e) const { return pk(e); } };
+struct PadV { __device__ __forceinline__ int operator()(int e) const { return pv(e); } };
+
+// ---------------------------------------------------------------- global I/O
+// 256-bit vector accesses (LDG/STG.E.ENL2.256 on sm_100a).
+__device__ __forceinline__ void ld_v4(const double *p, double &a, double &b, double &c, double &d)
+{
+    asm volatile("ld.global.v4.f64 {%0,%1,%2,%3}, [%4];"
+                 : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p));
+}
+__device__ __forceinline__ void st_v4(double *p, double a, double b, double c, double d)
+{
+    asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};"
+                 :: "l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
+}
+__device__ __forceinline__ void ld_v8(const uint32_t *p, uint32_t *u)
+{
+    asm volatile("ld.global.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3]),
+                   "=r"(u[4]), "=r"(u[5]), "=r"(u[6]), "=r"(u[7]) : "l"(p));
+}
+__device__ __forceinline__ void st_v8(uint32_t *p, const uint32_t *u)
+{
+    asm volatile("st.global.v8.u32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
+                 :: "l"(p), "r"(u[0]), "r"(u[1]), "r"(u[2]), "r"(u[3]),
+                    "r"(u[4]), "r"(u[5]), "r"(u[6]), "r"(u[7]) : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire(const unsigned *p)
+{
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release(unsigned *p, unsigned v)
+{
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
+}
+
+// Writes a thread's VT consecutive outputs (keys [+vals]) starting at out[pos].
+// `m` = how many of them are valid (tail); full segments use 256-bit stores
+// (pos is a multiple of VT and the arrays are 32-byte aligned).
+template <bool HV>
+__device__ __forceinline__ void store_segment(double *ok, uint32_t *ov, long long pos, int m,
+                                              const double (&k)[VT], const uint32_t (&v)[VT])
+{
+    if (m >= VT) {
+#pragma unroll
+        for (int x = 0; x < VT; x += 4) st_v4(ok + pos + x, k[x], k[x + 1], k[x + 2], k[x + 3]);
+        if (HV) {
+#pragma unroll
+            for (int x = 0; x < VT; x += 8) st_v8(ov + pos + x, &v[x]);
+        }
+    } else {
+#pragma unroll
+        for (int x = 0; x < VT; ++x)
+            if (x < m) {
+                ok[pos + x] = k[x];
+                if (HV) ov[pos + x] = v[x];
+            }
+    }
+}
+
+// ------------------------------------------------------------ merge device code
+// Stable co-rank (merge path) of diagonal d for sorted runs A[0:na), B[0:nb)
+// in shared memory: the number of A elements among the first d outputs of the
+// stable merge in which A (the left run) wins ties (Knuth's merge;
+// SPEC.md:290).  Predicate: A[m] <= B[d-1-m]  =>  the m-th A element precedes.
+template <class IX>
+__device__ __forceinline__ int merge_path_smem(const double *s, int a0, int na, int b0, int nb, int d, IX ix)
+{
+    int lo = max(0, d - nb), hi = min(d, na);
+    while (lo < hi) {
+        int m = (lo + hi) >> 1;
+        if (s[ix(a0 + m)] <= s[ix(b0 + d - 1 - m)]) lo = m + 1;
+        else hi = m;
+    }
+    return lo;
+}
+
+// Serial merge of VT outputs from shared memory, starting at A index ai and B
+// index bi (ends aend/bend, exclusive).  B's head is taken only if strictly
+// smaller than A's (left wins ties).  Reads one slot past a run end at most
+// (the shared arrays carry spare slots; the value is never used).
+template <bool HV, class IK, class IV>
+__device__ __forceinline__ void serial_merge(const double *sk, const uint32_t *sv, int ai, int aend,
+                                             int bi, int bend, double (&k)[VT], uint32_t (&v)[VT],
+                                             IK ik, IV iv)
+{
+    double ka = sk[ik(ai)], kb = sk[ik(bi)];
+#pragma unroll
+    for (int x = 0; x < VT; ++x) {
+        const bool p = (bi < bend) && ((ai >= aend) || (kb < ka));
+        k[x] = p ? kb : ka;
+        const int src = p ? bi : ai;
+        if (HV) v[x] = sv[iv(src)];
+        const int nxt = src + 1;
+        if (p) bi = nxt; else ai = nxt;
+        const double kn = sk[ik(nxt)];
+        if (p) kb = kn; else ka = kn;
+    }
+}
+
+// --------------------------------------------------------------- K1 tile sort
+// Each thread loads VT consecutive keys (256-bit loads), sorts them with an
+// odd-even transposition network (compare-exchange only of adjacent items and
+// only on strict `>`: stable), then log2(NT) rounds of shared-memory merge-path
+// merges double the sorted run length from VT to TILE.  Each round is one
+// "read-scan with comparisons and one write-scan" of PAPER.md:150, done on
+// chip.  The tail tile is padded with +inf keys placed AFTER every real key, so
+// stability puts real keys (including real +inf) first; pads are never stored.
+template <bool HV>
+__global__ void __launch_bounds__(NT, 2)
+tile_sort_kernel(const double *src_k, const uint32_t *src_v, double *dst_k, uint32_t *dst_v, long long n)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double *sk = reinterpret_cast<double *>(smem_raw);
+    uint32_t *sv = reinterpret_cast<uint32_t *>(smem_raw + K1_SMEM_KEYS);
+
+    const long long base = (long long)blockIdx.x * TILE;
+    const int cnt = (int)min((long long)TILE, n - base);
+    const int tid = threadIdx.x;
+    const int e0 = tid * VT;
+
+    double k[VT];
+    uint32_t v[VT];
+    if (e0 + VT <= cnt) {
+#pragma unroll
+        for (int x = 0; x < VT; x += 4) ld_v4(src_k + base + e0 + x, k[x], k[x + 1], k[x + 2], k[x + 3]);
+        if (HV) {
+#pragma unroll
+            for (int x = 0; x < VT; x += 8) ld_v8(src_v + base + e0 + x, &v[x]);
+        }
+    } else {
+#pragma unroll
+        for (int x = 0; x < VT; ++x) {
+            const bool ok = e0 + x < cnt;
+            k[x] = ok ? src_k[base + e0 + x] : __longlong_as_double(0x7FF0000000000000LL);
+            if (HV) v[x] = ok ? src_v[base + e0 + x] : 0u;
+        }
+    }
+
+    // in-register stable transposition sort
+#pragma unroll
+    for (int r = 0; r < VT; ++r) {
+#pragma unroll
+        for (int i = r & 1; i + 1 < VT; i += 2) {
+            const bool p = k[i + 1] < k[i];
+            const double lo = p ? k[i + 1] : k[i];
+            const double hi = p ? k[i] : k[i + 1];
+            k[i] = lo;
+            k[i + 1] = hi;
+            if (HV) {
+                const uint32_t vl = p ? v[i + 1] : v[i];
+                const uint32_t vh = p ? v[i] : v[i + 1];
+                v[i] = vl;
+                v[i + 1] = vh;
+            }
+        }
+    }
+
+    // shared-memory merge rounds: runs of VT*coop/2 -> VT*coop
+#pragma unroll 1
+    for (int coop = 2; coop <= NT; coop <<= 1) {
+#pragma unroll
+        for (int x = 0; x < VT; ++x) {
+            sk[pk(e0 + x)] = k[x];
+            if (HV) sv[pv(e0 + x)] = v[x];
+        }
+        __syncthreads();
+        const int local = tid & (coop - 1);
+        const int a0 = (tid - local) * VT;
+        const int run = (coop >> 1) * VT;
+        const int b0 = a0 + run;
+        const int d = local * VT;
+        const int i = merge_path_smem(sk, a0, run, b0, run, d, PadK());
+        serial_merge<HV>(sk, sv, a0 + i, b0, b0 + d - i, b0 + run, k, v, PadK(), PadV());
+        __syncthreads();
+    }
+
+    store_segment<HV>(dst_k, dst_v, base + e0, cnt - e0, k, v);
+}
+
+// ----------------------------------------------------------- merge geometry
+// Pair q merges A_q = ak[q*2L : q*2L + na_q) with B_q = bk[q*2L : q*2L + nb_q)
+// into out[q*2L : ...), na_q = min(L, n - 2qL), nb_q = clamp(n - 2qL - L, 0, L).
+//   uniform pass : ak = src, bk = src + L, out = dst
+//   0.5 top merge: ak = buffer, bk = data + nl, L = nl, out = data (one pair)
+struct MergeGeo {
+    const double *ak;
+    const uint32_t *av;
+    const double *bk;
+    const uint32_t *bv;
+    double *ok;
+    uint32_t *ov;
+    long long n;
+    long long L;
+};
+
+struct TileSpan {
+    long long g0, pbase;
+    int na, nb, k0, k1;
+};
+
+__device__ __forceinline__ TileSpan tile_span(const MergeGeo &g, int t)
+{
+    TileSpan s;
+    s.g0 = (long long)t * MTILE;
+    const long long span = 2 * g.L;
+    s.pbase = (s.g0 / span) * span;
+    const long long rem = g.n - s.pbase;
+    s.na = (int)min(g.L, rem);
+    s.nb = (int)max(0LL, min(g.L, rem - g.L));
+    s.k0 = (int)(s.g0 - s.pbase);
+    s.k1 = min(s.k0 + MTILE, s.na + s.nb);
+    return s;
+}
+
+// ---------------------------------------------------------- K2 partition
+// One warp per output tile: the stable co-rank of the tile's first diagonal,
+// found by a 32-ary search (each round probes 32 split points in parallel and
+// keeps the interval between the last true and first false predicate), about
+// 5 dependent rounds at L = 2^23 instead of 23 for a binary search.
+// "parallelize over an arbitrary number of processes".
+__global__ void __launch_bounds__(256)
+partition_kernel(MergeGeo g, int ntiles, int *__restrict__ corank)
+{
+    const int warp = (int)((blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5);
+    const int lane = threadIdx.x & 31;
+    if (warp >= ntiles) return;
+    const TileSpan s = tile_span(g, warp);
+    const double *A = g.ak + s.pbase;
+    const double *B = g.bk + s.pbase;
+    const int d = s.k0;
+    int lo = max(0, d - s.nb), hi = min(d, s.na);
+    while (lo < hi) {
+        const int span = hi - lo;
+        int m, nprobe;
+        if (span <= 32) {
+            m = lo + lane;
+            nprobe = span;
+        } else {
+            m = lo + (int)(((long long)span * (lane + 1)) / 33);
+            nprobe = 32;
+        }
+        bool p = false;
+        if (lane < nprobe) p = A[m] <= B[d - 1 - m];
+        const unsigned bal = __ballot_sync(0xFFFFFFFFu, p);
+        const int c = __popc(bal);
+        const int m_prev = __shfl_sync(0xFFFFFFFFu, m, (c > 0 ? c - 1 : 0));
+        const int m_next = __shfl_sync(0xFFFFFFFFu, m, (c < nprobe ? c : 0));
+        const int nlo = (c == 0) ? lo : m_prev + 1;
+        const int nhi = (c == nprobe) ? hi : m_next;
+        lo = nlo;
+        hi = max(nlo, nhi);
+    }
+    if (lane == 0) corank[warp] = lo;
+}
+
+// ---------------------------------------------- K4 dependency ranges (row a6)
+// In the in-place top merge, output tile t writes data[k0:k1); tile u reads
+// B = data[L + j0(u) : L + j1(u)).  Tile t may only write once every earlier
+// tile u < t whose read range intersects its write range has loaded its
+// inputs (later tiles never intersect: k1(t) <= L + j1(t) <= L + j0(u)).
+// deps[t] = {u_lo, u_hi} (empty if u_lo > u_hi).
+__device__ __forceinline__ long long j_start(const int *corank, int u)
+{
+    return (long long)u * MTILE - corank[u];
+}
+
+__global__ void __launch_bounds__(256)
+inplace_deps_kernel(const int *__restrict__ corank, int ntiles, long long L, long long n, int2 *deps)
+{
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= ntiles) return;
+    const long long k0 = (long long)t * MTILE;
+    const long long k1 = min(k0 + MTILE, n);
+    // u_lo: first u in [0,t) with L + j1(u) > k0, where j1(u) = j_start(u+1)
+    int lo = 0, hi = t;
+    while (lo < hi) {
+        const int m = (lo + hi) >> 1;
+        if (L + j_start(corank, m + 1) > k0) hi = m;
+        else lo = m + 1;
+    }
+    const int u_lo = lo;
+    // u_hi: last u in [0,t) with L + j0(u) < k1
+    lo = 0;
+    hi = t;
+    while (lo < hi) {
+        const int m = (lo + hi) >> 1;
+        if (L + j_start(corank, m) < k1) lo = m + 1;
+        else hi = m;
+    }
+    deps[t] = make_int2(u_lo, lo - 1);
+}
+
+// ------------------------------------------------------------ K3 / K4 merge
+// One CTA per MTILE-element output tile.  Loads A[i0:i1) and B[j0:j1)
+// (exactly the inputs of its outputs, from the co-ranks) coalesced into shared
+// memory, each thread finds its own diagonal by merge path and merges VT
+// outputs serially (left wins ties), then writes them with 256-bit stores.
+// INPLACE (K4): tiles are taken in atomic-ticket order; after loading, a tile
+// publishes flags[t] (release); before writing, it waits (acquire) on the
+// flags of the earlier tiles in deps[t].  Deadlock-free: a tile only waits on
+// smaller tickets, whose CTAs are already resident and never wait on it.
+template <bool HV, bool INPLACE>
+__global__ void __launch_bounds__(NT, 2)
+merge_kernel(MergeGeo g, const int *__restrict__ corank, const int2 *__restrict__ deps,
+             unsigned *flags, unsigned *ticket)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double *sk = reinterpret_cast<double *>(smem_raw);
+    uint32_t *sv = reinterpret_cast<uint32_t *>(smem_raw + K3_SMEM_KEYS);
+    __shared__ int s_t;
+
+    const int tid = threadIdx.x;
+    int t;
+    if (INPLACE) {
+        if (tid == 0) s_t = (int)atomicAdd(ticket, 1u);
+        __syncthreads();
+        t = s_t;
+    } else {
+        t = blockIdx.x;
+    }
+    const TileSpan s = tile_span(g, t);
+    const int cnt = s.k1 - s.k0;
+    // co-ranks; clamped so that even a non-monotone split (NaN keys) stays in bounds
+    const int i0 = corank[t];
+    int i1 = (s.k1 == s.na + s.nb) ? s.na : corank[t + 1];
+    i1 = min(min(max(max(i1, i0), s.k1 - s.nb), i0 + cnt), s.na);
+    const int j0 = s.k0 - i0;
+    const int ca = i1 - i0;
+
+    const double *A = g.ak + s.pbase + i0;
+    const double *B = g.bk + s.pbase + j0 - ca;     // B[e] for e in [ca, cnt)
+    const uint32_t *Av = HV ? g.av + s.pbase + i0 : nullptr;
+    const uint32_t *Bv = HV ? g.bv + s.pbase + j0 - ca : nullptr;
+#pragma unroll
+    for (int r = 0; r < VT; ++r) {
+        const int e = tid + r * NT;
+        if (e < cnt) {
+            const bool fa = e < ca;
+            sk[e] = fa ? A[e] : B[e];
+            if (HV) sv[e] = fa ? Av[e] : Bv[e];
+        }
+    }
+    __syncthreads();
+
+    if (INPLACE) {
+        if (tid == 0) {
+            __threadfence();
+            st_release(flags + t, 1u);
+        }
+        const int2 dp = deps[t];
+        for (int u = dp.x + tid; u <= dp.y; u += NT)
+            while (ld_acquire(flags + u) == 0u) { __nanosleep(64); }
+        __syncthreads();
+    }
+
+    const int d = min(tid * VT, cnt);
+    const int i = merge_path_smem(sk, 0, ca, ca, cnt - ca, d, Ident());
+    double k[VT];
+    uint32_t v[VT];
+    serial_merge<HV>(sk, sv, i, ca, ca + d - i, cnt, k, v, Ident(), Ident());
+    store_segment<HV>(g.ok, g.ov, s.g0 + tid * VT, cnt - d, k, v);
+}
+
+}  // namespace gns

@@ -1,0 +1,90 @@
+"""C-ABI contract checks that need no GPU: the library loads, exports every
+symbol include/gns.h declares, plans passes/bytes correctly, and rejects bad
+arguments before touching CUDA."""
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "gns.h")
+
+
+@pytest.fixture(scope="session")
+def gns():
+    lib = os.path.join(ROOT, "paper_2402_01816_b200", "libgns.so")
+    srcs = [os.path.join(ROOT, "paper_2402_01816_b200", "csrc", f) for f in ("gns.cu", "gns_kernels.cuh")] + [HEADER]
+    if not os.path.exists(lib) or any(os.path.getmtime(s) > os.path.getmtime(lib) for s in srcs):
+        subprocess.check_call(["make", "-C", ROOT, "paper_2402_01816_b200/libgns.so"])
+    import paper_2402_01816_b200 as g
+    return g
+
+
+def declared_functions():
+    txt = open(HEADER).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(gns_[a-z0-9_]+)\s*\(", txt)))
+
+
+def test_exports_every_declared_symbol(gns):
+    names = declared_functions()
+    assert len(names) >= 14
+    out = subprocess.check_output(["nm", "-D", "--defined-only", gns.LIB_PATH]).decode()
+    exported = set(re.findall(r"\bT (gns_\w+)", out))
+    missing = [n for n in names if n not in exported]
+    assert not missing, missing
+    assert set(names) == set(gns.EXPORTED)
+
+
+def test_sm100a_only(gns):
+    out = subprocess.check_output(["/usr/local/cuda/bin/cuobjdump", "--list-elf", gns.LIB_PATH]).decode()
+    assert "sm_100a" in out
+    archs = set(re.findall(r"sm_\d+a?", out))
+    assert archs == {"sm_100a"}, archs
+
+
+def test_geometry_and_plan(gns):
+    T = gns.gns_tile_elems()
+    assert T == gns.gns_merge_tile_elems() == 4096
+    p = gns.plan(1 << 24, 1.0, False)
+    assert p["merge_passes"] == 12 and p["hbm_passes"] == 13
+    assert p["bytes_lower_bound"] == 13 * 2 * (1 << 24) * 8
+    assert p["buffer_elems"] == 1 << 24
+    p = gns.plan(1 << 27, 0.5, True)
+    assert p["hbm_passes"] == 16 and p["left_len"] == 1 << 26 and p["buffer_elems"] == 1 << 26
+    assert p["bytes_lower_bound"] == 16 * 2 * (1 << 27) * 12
+    p = gns.plan(T, 0.5, True)
+    assert p["workspace_bytes"] == 0 and p["hbm_passes"] == 1
+    p = gns.plan(T + 1, 1.0, False)
+    assert p["merge_passes"] == 1
+    assert gns.plan(0, 1.0, False)["hbm_passes"] == 0
+
+
+def test_workspace_ram_pct(gns):
+    from oracle import footprint
+    n = 1 << 27
+    for frac, want in ((1.0, 2.0), (0.5, 1.5)):
+        ws = gns.workspace_bytes(n, frac, True)
+        r = footprint.ram_pct(n * 12, ws)
+        assert want <= r < want + 1e-3, (frac, r)
+    assert gns.workspace_bytes(n, 0.7, True) == 0
+
+
+def test_argument_errors_before_any_cuda_call(gns):
+    # all of these must return before touching CUDA (there is no GPU here)
+    assert gns.gns_sort_f64(None, 10, 1.0, None) == 1
+    assert gns.gns_sort_f64(256, 10, 0.75, None) == 2
+    assert gns.gns_sort_f64(264, 10, 1.0, None) == 6            # 8-byte but not 32-byte aligned
+    assert gns.gns_sort_pairs_f64_u32(256, None, 10, 1.0, None) == 1
+    assert gns.gns_sort_f64(256, (1 << 31), 1.0, None) == 1
+    assert gns.gns_sort_f64_ws(256, 1 << 20, 1.0, None, 0, None) == 5
+    assert gns.gns_sort_f64_ws(256, 1 << 20, 1.0, 256, 10, None) == 5
+    assert gns.gns_merge_pass(256, None, 512, None, 1000, 100, 256, 1 << 20, None) == 1
+    assert gns.gns_merge_inplace_top(256, None, 512, None, 10, 100, 256, 1 << 20, None) == 1
+    # n in {0, 1}: OK, no launch
+    assert gns.gns_sort_f64(None, 0, 1.0, None) == 0
+    assert gns.gns_sort_f64(256, 1, 0.5, None) == 0
+    assert gns.gns_status_string(6) == "GNS_ERR_MISALIGNED"
+    assert gns.gns_sort_f64(264, 10, 1.0, None) == 6
+    assert "aligned" in gns.gns_last_error_string()

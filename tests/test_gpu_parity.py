@@ -1,0 +1,221 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle,
+bit-exact on keys and payload (the stable result is unique).
+
+Covers every §8(a) row: the full sort in both buffer modes (a1, a5, a7), the
+tile sort (a2), one merge pass incl. its co-rank partition (a3+a4), the
+in-place top merge with its hazard protocol (a6), at edge sizes (empty, 1,
+tile +-1, several tiles with ragged tails, pass boundaries), all five
+BASELINE configs at full size, ties, signed zeros and +-inf.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from checks import assert_bitexact, check_invariants
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def gns():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    import paper_2402_01816_b200 as g
+    return g
+
+
+def to_dev(k, v):
+    tk = torch.from_numpy(np.ascontiguousarray(k)).cuda()
+    tv = None if v is None else torch.from_numpy(np.ascontiguousarray(v, dtype=np.uint32)).cuda()
+    return tk, tv
+
+
+def gpu_sort(gns, k, v, frac, use_ws=False):
+    tk, tv = to_dev(k, v)
+    ws = gns.alloc_workspace(k.size, frac, v is not None) if use_ws else None
+    gns.sort_(tk, tv, frac, workspace=ws)
+    torch.cuda.synchronize()
+    return tk.cpu().numpy(), (None if tv is None else tv.cpu().numpy())
+
+
+def check_against_oracle(gns, k, v, frac, use_ws=False, what=""):
+    gk, gv = gpu_sort(gns, k, v, frac, use_ws)
+    ek, ev = oracle.sort(k, v)
+    assert_bitexact(gk, ek, gv, ev, what=what)
+
+
+T = 4096
+EDGE_SIZES = [0, 1, 2, 3, 31, 32, 33, 255, 1000, T - 1, T, T + 1, 2 * T - 1, 2 * T, 2 * T + 1,
+              3 * T, 3 * T + 17, 4 * T + 1, 8 * T - 5, 8 * T + 3, 9 * T, 65521, (1 << 16) + 1,
+              (1 << 17) - 1, 100003]
+
+
+@pytest.mark.parametrize("frac", [1.0, 0.5])
+@pytest.mark.parametrize("payload", [False, True])
+@pytest.mark.parametrize("n", EDGE_SIZES)
+def test_edge_sizes_ties(gns, n, payload, frac):
+    k = synth.ties(n, 77 + n, 7)
+    k[::5] *= -1.0                      # -0.0 / +0.0 mix, negative keys
+    v = synth.iota_u32(n) if payload else None
+    check_against_oracle(gns, k, v, frac, what=f"n={n}")
+
+
+@pytest.mark.parametrize("frac", [1.0, 0.5])
+@pytest.mark.parametrize("n", [T + 1, 5 * T + 77, 1 << 18, (1 << 20) + 12345])
+def test_uniform_pairs_ws(gns, n, frac):
+    k = synth.uniform(n, 9000 + n)
+    v = synth.iota_u32(n)[::-1].copy()   # payload need not be the index
+    check_against_oracle(gns, k, v, frac, use_ws=True, what=f"n={n}")
+
+
+def test_specials_inf_zero(gns):
+    n = 3 * T + 5
+    rng = np.random.default_rng(5)
+    pool = np.array([-np.inf, np.inf, -0.0, 0.0, 1.0, -1.0, 5e-324, -5e-324, np.finfo(np.float64).max])
+    k = pool[rng.integers(0, pool.size, n)]
+    v = synth.iota_u32(n)
+    for frac in (1.0, 0.5):
+        check_against_oracle(gns, k, v, frac, what="specials")
+
+
+def test_exhaustive_tiny(gns):
+    import itertools
+    for alphabet in ((0.0, 1.0, 2.0), (-0.0, 0.0, 1.0)):
+        for n in range(0, 7):
+            for seq in itertools.product(alphabet, repeat=n):
+                k = np.array(seq, dtype=np.float64)
+                v = synth.iota_u32(n)
+                check_against_oracle(gns, k, v, 1.0, what=str(seq))
+
+
+# ------------------------------------------------------------- per-step parity
+
+def test_tile_sort_step(gns):
+    n = 7 * T + 123
+    k = synth.ties(n, 4242, 50)
+    v = synth.iota_u32(n)
+    tk, tv = to_dev(k, v)
+    ok, ov = torch.empty_like(tk), torch.empty_like(tv)
+    gns.tile_sort(tk, tv, ok, ov)
+    torch.cuda.synchronize()
+    gk, gv = ok.cpu().numpy(), ov.cpu().numpy()
+    for lo in range(0, n, T):
+        ek, ev = oracle.sort(k[lo:lo + T], v[lo:lo + T])
+        assert_bitexact(gk[lo:lo + T], ek, gv[lo:lo + T], ev, what=f"tile {lo // T}")
+
+
+@pytest.mark.parametrize("payload", [False, True])
+@pytest.mark.parametrize("L_tiles,n", [(1, 2 * T), (1, 5 * T + 3), (2, 11 * T + 999), (4, 9 * T), (8, 3 * T + 1)])
+def test_merge_pass_step(gns, L_tiles, n, payload):
+    L = L_tiles * T
+    k = synth.ties(n, 31 + n, 9)
+    v = synth.iota_u32(n) if payload else None
+    # presort runs of L with the oracle, then one merge level on both sides
+    k2 = k.copy()
+    v2 = None if v is None else v.copy()
+    for lo in range(0, n, L):
+        sk, sv = oracle.sort(k2[lo:lo + L], None if v2 is None else v2[lo:lo + L])
+        k2[lo:lo + L] = sk
+        if v2 is not None:
+            v2[lo:lo + L] = sv
+    ek, ev = oracle.merge_runs(k2, v2, L)
+    tk, tv = to_dev(k2, v2)
+    ok = torch.empty_like(tk)
+    ov = None if tv is None else torch.empty_like(tv)
+    ws = torch.empty(gns.gns_merge_workspace_bytes(n), dtype=torch.uint8, device="cuda")
+    gns.merge_pass(tk, tv, ok, ov, L, ws)
+    torch.cuda.synchronize()
+    assert_bitexact(ok.cpu().numpy(), ek, None if ov is None else ov.cpu().numpy(), ev)
+
+
+def _inplace_case(layout, n, nl, rng):
+    nr = n - nl
+    if layout == "left_small":          # all left < all right: no cross-tile hazard
+        a = np.sort(rng.random(nl)); b = np.sort(rng.random(nr)) + 2.0
+    elif layout == "left_big":          # all left > all right: hazard n/(2T) tiles back
+        a = np.sort(rng.random(nl)) + 2.0; b = np.sort(rng.random(nr))
+    elif layout == "interleave":        # hazard with the previous tile
+        a = np.arange(nl, dtype=np.float64) * 2.0; b = np.arange(nr, dtype=np.float64) * 2.0 + 1.0
+    elif layout == "ties":
+        a = np.sort(rng.integers(0, 3, nl)).astype(np.float64)
+        b = np.sort(rng.integers(0, 3, nr)).astype(np.float64)
+    else:
+        a = np.sort(rng.random(nl)); b = np.sort(rng.random(nr))
+    return a, b
+
+
+@pytest.mark.parametrize("layout", ["left_small", "left_big", "interleave", "ties", "random"])
+def test_inplace_top_merge_hazards(gns, layout):
+    """Row a6 stress: the dead region of the data array and
+    the unused buffer tail are poisoned with NaN, so a read-after-overwrite
+    shows up as a wrong output.  Repeated to give races a chance."""
+    rng = np.random.default_rng(123)
+    for rep, (n, nl) in enumerate([(64 * T, 32 * T), (64 * T + 40, 32 * T + 32), (20 * T + 7, 10 * T + 32)] * 4):
+        a, b = _inplace_case(layout, n, nl, rng)
+        va = np.arange(nl, dtype=np.uint32)
+        vb = np.arange(nl, n, dtype=np.uint32)
+        ek, ev = oracle.merge_runs(np.concatenate([a, b]), np.concatenate([va, vb]), nl)
+        data = np.full(n, np.nan)
+        data[nl:] = b
+        vals = np.full(n, 0xDEADBEEF, dtype=np.uint32)
+        vals[nl:] = vb
+        tk, tv = to_dev(data, vals)
+        lk, lv = to_dev(a, va)
+        ws = torch.empty(gns.gns_merge_workspace_bytes(n), dtype=torch.uint8, device="cuda")
+        gns.merge_inplace_top(tk, tv, lk, lv, nl, ws)
+        torch.cuda.synchronize()
+        assert_bitexact(tk.cpu().numpy(), ek, tv.cpu().numpy(), ev, what=f"{layout} rep {rep}")
+
+
+# ------------------------------------------------------- BASELINE configs, full size
+
+def _config_cases():
+    cases = [(1, ""), (2, ""), (3, "")] + [(4, s) for s in synth.CONFIG4_SUBS] + [(5, "")]
+    return cases
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("c,sub", _config_cases())
+def test_baseline_configs_full_size(gns, c, sub):
+    case = synth.config(c, sub)
+    k, v = case.keys, case.vals
+    n = k.size
+    if c in (1, 4):
+        # closed form (permutations of 0..n-1): keys -> i, payload -> inverse permutation
+        ek = np.arange(n, dtype=np.float64)
+        ev = None
+        if v is not None:
+            ev = np.empty(n, dtype=np.uint32)
+            ev[k.astype(np.int64)] = v
+    else:
+        ek, ev = oracle.sort(k, v)
+    for frac in case.fractions + ([0.5] if c in (2, 3) else []):
+        gk, gv = gpu_sort(gns, k, v, frac, use_ws=True)
+        assert_bitexact(gk, ek, gv, ev, what=f"{case.name} frac={frac}")
+        if c == 3:
+            check_invariants(k, gk, v, gv, payload_is_index=True)
+
+
+def test_error_paths_leave_data_untouched(gns):
+    k = synth.uniform(5000, 1)
+    tk, _ = to_dev(k, None)
+    before = tk.clone()
+    assert gns.gns_sort_f64(int(tk.data_ptr()), 5000, 0.3, 0) == 2
+    assert gns.gns_sort_f64(int(tk.data_ptr()) + 8, 4999, 1.0, 0) == 6
+    assert gns.gns_sort_f64_ws(int(tk.data_ptr()), 5000, 1.0, 0, 0, 0) == 5
+    torch.cuda.synchronize()
+    assert torch.equal(before, tk)
+
+
+def test_nan_memory_safe(gns):
+    """NaN is a precondition violation (header: contents unspecified), but the
+    call must not fault, must terminate, and the context must stay usable."""
+    n = 6 * T + 11
+    k = synth.uniform(n, 3)
+    k[::7] = np.nan
+    v = synth.iota_u32(n)
+    for frac in (1.0, 0.5):
+        gpu_sort(gns, k, v, frac)
+    check_against_oracle(gns, synth.uniform(n, 4), v, 0.5, what="after NaN")
