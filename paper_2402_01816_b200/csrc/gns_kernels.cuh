@@ -20,19 +20,24 @@ constexpr int VT = 16;             // items per thread
 constexpr int TILE = NT * VT;      // K1 tile = 4096 elements
 constexpr int MTILE = NT * VT;     // K3/K4 output tile = 4096 elements
 
-// Padded shared-memory index (K1 only): one pad slot per 16 doubles / 32 u32
-// so that the blocked accesses (thread t touches t*VT + v) are conflict free.
-__device__ __forceinline__ int pk(int e) { return e + (e >> 4); }
-__device__ __forceinline__ int pv(int e) { return e + (e >> 5); }
-constexpr int K1_SK = TILE + (TILE >> 4) + 4;
-constexpr int K1_SV = TILE + (TILE >> 5) + 4;
+// Swizzled shared-memory index.  Three access patterns must be conflict free:
+// coalesced fills (lane t touches e0 + t), blocked register spills (lane t
+// touches 16t + v) and the merge-path reads (lane t near base + 8t, because a
+// thread's VT outputs consume ~VT/2 from each run).  XOR-ing the slot within
+// its 128-byte row with the row index spreads all three over the 32 banks:
+//   doubles: 16 per row, slot = e ^ ((e >> 4) & 15)
+//   u32    : 32 per row, slot = e ^ ((e >> 5) & 31)
+// Both are bijections within each aligned row, so no extra space is needed.
+__device__ __forceinline__ int swk(int e) { return e ^ ((e >> 4) & 15); }
+__device__ __forceinline__ int swv(int e) { return e ^ ((e >> 5) & 31); }
+constexpr int K1_SK = TILE + 32;      // + spare slots for one-past-end reads
+constexpr int K1_SV = TILE + 32;
 constexpr size_t K1_SMEM_KEYS = sizeof(double) * K1_SK;
-constexpr size_t K3_SK = MTILE + 4;
+constexpr size_t K3_SK = MTILE + 32;
 constexpr size_t K3_SMEM_KEYS = sizeof(double) * K3_SK;
 
-struct Ident { __device__ __forceinline__ int operator()(int e) const { return e; } };
-struct PadK { __device__ __forceinline__ int operator()(int e) const { return pk(e); } };
-struct PadV { __device__ __forceinline__ int operator()(int e) const { return pv(e); } };
+struct SwK { __device__ __forceinline__ int operator()(int e) const { return swk(e); } };
+struct SwV { __device__ __forceinline__ int operator()(int e) const { return swv(e); } };
 
 // ---------------------------------------------------------------- global I/O
 // 256-bit vector accesses (LDG/STG.E.ENL2.256 on sm_100a).
@@ -142,7 +147,7 @@ __device__ __forceinline__ void serial_merge(const double *sk, const uint32_t *s
 // chip.  The tail tile is padded with +inf keys placed AFTER every real key, so
 // stability puts real keys (including real +inf) first; pads are never stored.
 template <bool HV>
-__global__ void __launch_bounds__(NT, 2)
+__global__ void __launch_bounds__(NT, 3)
 tile_sort_kernel(const double *src_k, const uint32_t *src_v, double *dst_k, uint32_t *dst_v, long long n)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -196,8 +201,8 @@ tile_sort_kernel(const double *src_k, const uint32_t *src_v, double *dst_k, uint
     for (int coop = 2; coop <= NT; coop <<= 1) {
 #pragma unroll
         for (int x = 0; x < VT; ++x) {
-            sk[pk(e0 + x)] = k[x];
-            if (HV) sv[pv(e0 + x)] = v[x];
+            sk[swk(e0 + x)] = k[x];
+            if (HV) sv[swv(e0 + x)] = v[x];
         }
         __syncthreads();
         const int local = tid & (coop - 1);
@@ -205,8 +210,8 @@ tile_sort_kernel(const double *src_k, const uint32_t *src_v, double *dst_k, uint
         const int run = (coop >> 1) * VT;
         const int b0 = a0 + run;
         const int d = local * VT;
-        const int i = merge_path_smem(sk, a0, run, b0, run, d, PadK());
-        serial_merge<HV>(sk, sv, a0 + i, b0, b0 + d - i, b0 + run, k, v, PadK(), PadV());
+        const int i = merge_path_smem(sk, a0, run, b0, run, d, SwK());
+        serial_merge<HV>(sk, sv, a0 + i, b0, b0 + d - i, b0 + run, k, v, SwK(), SwV());
         __syncthreads();
     }
 
@@ -336,7 +341,7 @@ inplace_deps_kernel(const int *__restrict__ corank, int ntiles, long long L, lon
 // flags of the earlier tiles in deps[t].  Deadlock-free: a tile only waits on
 // smaller tickets, whose CTAs are already resident and never wait on it.
 template <bool HV, bool INPLACE>
-__global__ void __launch_bounds__(NT, 2)
+__global__ void __launch_bounds__(NT, 3)
 merge_kernel(MergeGeo g, const int *__restrict__ corank, const int2 *__restrict__ deps,
              unsigned *flags, unsigned *ticket)
 {
@@ -367,13 +372,25 @@ merge_kernel(MergeGeo g, const int *__restrict__ corank, const int2 *__restrict_
     const double *B = g.bk + s.pbase + j0 - ca;     // B[e] for e in [ca, cnt)
     const uint32_t *Av = HV ? g.av + s.pbase + i0 : nullptr;
     const uint32_t *Bv = HV ? g.bv + s.pbase + j0 - ca : nullptr;
+    // All VT loads are issued before any shared store (addresses clamped into
+    // the tile instead of branching), so each thread has VT loads in flight.
+    {
+        double tk[VT];
+        uint32_t tv[VT];
 #pragma unroll
-    for (int r = 0; r < VT; ++r) {
-        const int e = tid + r * NT;
-        if (e < cnt) {
+        for (int r = 0; r < VT; ++r) {
+            const int e = min(tid + r * NT, cnt - 1);
             const bool fa = e < ca;
-            sk[e] = fa ? A[e] : B[e];
-            if (HV) sv[e] = fa ? Av[e] : Bv[e];
+            tk[r] = fa ? A[e] : B[e];
+            if (HV) tv[r] = fa ? Av[e] : Bv[e];
+        }
+#pragma unroll
+        for (int r = 0; r < VT; ++r) {
+            const int e = tid + r * NT;
+            if (e < cnt) {
+                sk[swk(e)] = tk[r];
+                if (HV) sv[swv(e)] = tv[r];
+            }
         }
     }
     __syncthreads();
@@ -390,10 +407,10 @@ merge_kernel(MergeGeo g, const int *__restrict__ corank, const int2 *__restrict_
     }
 
     const int d = min(tid * VT, cnt);
-    const int i = merge_path_smem(sk, 0, ca, ca, cnt - ca, d, Ident());
+    const int i = merge_path_smem(sk, 0, ca, ca, cnt - ca, d, SwK());
     double k[VT];
     uint32_t v[VT];
-    serial_merge<HV>(sk, sv, i, ca, ca + d - i, cnt, k, v, Ident(), Ident());
+    serial_merge<HV>(sk, sv, i, ca, ca + d - i, cnt, k, v, SwK(), SwV());
     store_segment<HV>(g.ok, g.ov, s.g0 + tid * VT, cnt - d, k, v);
 }
 
