@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 #include <cstdio>
 #include <cstring>
+#include <algorithm>
 #include <mutex>
 #include <string>
 
@@ -100,6 +101,7 @@ size_t merge_ws(size_t n)
 // Per-device one-time kernel attributes (dynamic shared memory > 48 KB).
 std::mutex g_attr_mu;
 unsigned long long g_attr_done = 0;   // bit per device ordinal
+int g_num_sms[64];
 
 gns_status ensure_attrs()
 {
@@ -116,8 +118,20 @@ gns_status ensure_attrs()
     GNS_TRY(check(cudaFuncSetAttribute(merge_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, k3), "attr"));
     GNS_TRY(check(cudaFuncSetAttribute(merge_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, k3), "attr"));
     GNS_TRY(check(cudaFuncSetAttribute(merge_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, k3), "attr"));
+    const int kp1 = (int)(PIPE_STAGES * pipe_stage_bytes(true));
+    const int kp0 = (int)(PIPE_STAGES * pipe_stage_bytes(false));
+    GNS_TRY(check(cudaFuncSetAttribute(merge_pipe_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kp1), "attr"));
+    GNS_TRY(check(cudaFuncSetAttribute(merge_pipe_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kp0), "attr"));
+    GNS_TRY(check(cudaDeviceGetAttribute(&g_num_sms[dev], cudaDevAttrMultiProcessorCount, dev), "sm count"));
     g_attr_done |= (1ull << dev);
     return GNS_OK;
+}
+
+int num_sms()
+{
+    int dev = 0;
+    cudaGetDevice(&dev);
+    return (dev >= 0 && dev < 64 && g_num_sms[dev] > 0) ? g_num_sms[dev] : 148;
 }
 
 // ------------------------------------------------------------------ launches
@@ -133,8 +147,8 @@ gns_status launch_tile_sort(const double *sk, const uint32_t *sv, double *dk, ui
     return check(cudaGetLastError(), "tile_sort_kernel");
 }
 
-gns_status launch_merge(const MergeGeo &g, int *corank, int2 *deps, unsigned *flags, bool inplace,
-                        cudaStream_t st)
+gns_status launch_merge(const MergeGeo &g, const double *lim_a, const double *lim_b, int *corank, int2 *deps,
+                        unsigned *flags, bool inplace, cudaStream_t st)
 {
     const int ntiles = (int)ceil_div((size_t)g.n, MTILE);
     const bool hv = g.av != nullptr;
@@ -142,9 +156,15 @@ gns_status launch_merge(const MergeGeo &g, int *corank, int2 *deps, unsigned *fl
     GNS_TRY(check(cudaGetLastError(), "partition_kernel"));
     const size_t smem = K3_SMEM_KEYS + (hv ? sizeof(uint32_t) * K3_SK : 0);
     if (!inplace) {
-        if (hv) merge_kernel<true, false><<<ntiles, NT, smem, st>>>(g, corank, nullptr, nullptr, nullptr);
-        else merge_kernel<false, false><<<ntiles, NT, smem, st>>>(g, corank, nullptr, nullptr, nullptr);
-        return check(cudaGetLastError(), "merge_kernel");
+        PipeGeo pg;
+        pg.g = g;
+        pg.a_lim = lim_a;
+        pg.b_lim = lim_b;
+        const int grid = std::min(ntiles, 2 * num_sms());
+        const size_t psmem = PIPE_STAGES * pipe_stage_bytes(hv);
+        if (hv) merge_pipe_kernel<true><<<grid, NT, psmem, st>>>(pg, corank, ntiles);
+        else merge_pipe_kernel<false><<<grid, NT, psmem, st>>>(pg, corank, ntiles);
+        return check(cudaGetLastError(), "merge_pipe_kernel");
     }
     inplace_deps_kernel<<<(unsigned)ceil_div(ntiles, 256), 256, 0, st>>>(corank, ntiles, g.L, g.n, deps);
     GNS_TRY(check(cudaGetLastError(), "inplace_deps_kernel"));
@@ -187,7 +207,7 @@ gns_status sort_range(double *rk, uint32_t *rv, double *pk_, uint32_t *pv_, size
     for (int p = 0; p < M; ++p) {
         const size_t L = (size_t)TILE << p;
         MergeGeo g = uniform_geo(ck, cv, ok, ov, len, L);
-        GNS_TRY(launch_merge(g, corank, nullptr, nullptr, false, st));
+        GNS_TRY(launch_merge(g, ck + len, ck + len, corank, nullptr, nullptr, false, st));
         std::swap(ck, ok);
         std::swap(cv, ov);
     }
@@ -241,7 +261,7 @@ gns_status run_sort(double *keys, uint32_t *vals, size_t n, bool half, unsigned 
     g.L = (long long)nl;
     int2 *deps = reinterpret_cast<int2 *>(ws + Lo.off_deps);
     unsigned *flags = reinterpret_cast<unsigned *>(ws + Lo.off_flags);
-    return launch_merge(g, corank, deps, flags, true, st);
+    return launch_merge(g, bk + nl, keys + n, corank, deps, flags, true, st);
 }
 
 gns_status sort_alloc(double *keys, uint32_t *vals, bool hv, size_t n, double frac, cudaStream_t st)
@@ -366,7 +386,7 @@ gns_status gns_merge_pass(const double *src_keys, const uint32_t *src_vals, doub
     if (!ws || ws_bytes < merge_ws(n)) return fail(GNS_ERR_WORKSPACE_TOO_SMALL, "workspace too small");
     GNS_TRY(ensure_attrs());
     MergeGeo g = uniform_geo(src_keys, src_vals, dst_keys, dst_vals, n, run_len);
-    return launch_merge(g, (int *)ws, nullptr, nullptr, false, (cudaStream_t)stream);
+    return launch_merge(g, src_keys + n, src_keys + n, (int *)ws, nullptr, nullptr, false, (cudaStream_t)stream);
 }
 
 gns_status gns_merge_inplace_top(double *keys, uint32_t *vals, const double *left_keys,
@@ -395,7 +415,7 @@ gns_status gns_merge_inplace_top(double *keys, uint32_t *vals, const double *lef
     g.ov = vals;
     g.n = (long long)n;
     g.L = (long long)nl;
-    return launch_merge(g, corank, deps, flags, true, (cudaStream_t)stream);
+    return launch_merge(g, left_keys + nl, keys + n, corank, deps, flags, true, (cudaStream_t)stream);
 }
 
 int gns_tile_elems(void) { return TILE; }

@@ -74,6 +74,45 @@ __device__ __forceinline__ void st_release(unsigned *p, unsigned v)
     asm volatile("st.release.gpu.global.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
 }
 
+// ---- mbarrier + TMA bulk copy (cp.async.bulk, SASS UBLKCP) helpers
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init()
+{
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
+{
+    asm volatile("{\n\t.reg .pred p;\n"
+                 "GNS_WAIT_%=:\n\t"
+                 "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+                 "@!p bra GNS_WAIT_%=;\n}"
+                 :: "r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+// 1-D bulk copy global -> shared, completion counted on `bar` (16-byte aligned
+// addresses, size a multiple of 16).  L2 evict-first: every byte is read once.
+__device__ __forceinline__ void tma_load_1d(void *dst, const void *src, uint32_t bytes, uint64_t *bar,
+                                            uint64_t policy)
+{
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+                 " [%0], [%1], %2, [%3], %4;"
+                 :: "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy) : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first()
+{
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+
 // Writes a thread's VT consecutive outputs (keys [+vals]) starting at out[pos].
 // `m` = how many of them are valid (tail); full segments use 256-bit stores
 // (pos is a multiple of VT and the arrays are 32-byte aligned).
@@ -412,6 +451,154 @@ merge_kernel(MergeGeo g, const int *__restrict__ corank, const int2 *__restrict_
     uint32_t v[VT];
     serial_merge<HV>(sk, sv, i, ca, ca + d - i, cnt, k, v, SwK(), SwV());
     store_segment<HV>(g.ok, g.ov, s.g0 + tid * VT, cnt - d, k, v);
+}
+
+
+// ------------------------------------------------ K3 pipelined (persistent)
+// The production merge pass.  A persistent grid (2 CTAs per SM) walks the
+// output tiles t = blockIdx.x, +gridDim.x, ...; each CTA double-buffers its
+// tiles in shared memory: while all 256 threads merge tile i from one stage,
+// the TMA engine (cp.async.bulk, issued by one thread) streams the inputs of
+// tile i+1 -- exactly A[i0:i1) and B[j0:j1), from the co-ranks -- into the
+// other stage, so HBM reads run continuously under the merge arithmetic.
+// Keys and vals of global element g land in the same shared slot
+// (slot = base + (g mod 4) + ...), which keeps every bulk copy 16-byte
+// aligned for both 8-byte keys and 4-byte vals; at most one key / three vals
+// at an unaligned array end are read with plain loads instead.
+constexpr int PIPE_STAGES = 2;
+constexpr int PIPE_SLOTS = MTILE + 32;
+constexpr size_t pipe_stage_bytes(bool hv) { return PIPE_SLOTS * (sizeof(double) + (hv ? sizeof(uint32_t) : 0)); }
+
+struct PipeGeo {
+    MergeGeo g;
+    const double *a_lim;   // end of the array holding the A runs (keys)
+    const double *b_lim;   // end of the array holding the B runs (keys)
+};
+
+struct PipeMeta {
+    int t, ca, cb, offa, bslot;
+};
+
+// Thread-0 side: computes tile t's input slices and issues their bulk copies
+// into stage buffers sk/sv, completing on `bar`.  Leftover unaligned tail
+// elements are copied with plain loads (made visible by the caller's barrier).
+template <bool HV>
+__device__ __forceinline__ void pipe_issue(const PipeGeo &pg, const int *__restrict__ corank, int t,
+                                           double *sk, uint32_t *sv, uint64_t *bar, PipeMeta *meta,
+                                           uint64_t policy)
+{
+    const MergeGeo &g = pg.g;
+    const TileSpan s = tile_span(g, t);
+    const int cnt = s.k1 - s.k0;
+    const int i0 = corank[t];
+    int i1 = (s.k1 == s.na + s.nb) ? s.na : corank[t + 1];
+    i1 = min(min(max(max(i1, i0), s.k1 - s.nb), i0 + cnt), s.na);
+    const int j0 = s.k0 - i0;
+    const int ca = i1 - i0, cb = cnt - ca;
+    const double *Ak = g.ak + s.pbase + i0;
+    const double *Bk = g.bk + s.pbase + j0;
+    const uint32_t *Av = HV ? g.av + s.pbase + i0 : nullptr;
+    const uint32_t *Bv = HV ? g.bv + s.pbase + j0 : nullptr;
+    const int offa = (int)(((uintptr_t)Ak >> 3) & 3);
+    const int offb = (int)(((uintptr_t)Bk >> 3) & 3);
+    const int bbase = (offa + ca + 3) & ~3;
+    // one run: elements [0, c) of K/V, shared slot of element e = sbase + off + e
+    auto run = [&](const double *K, const uint32_t *V, int c, int off, int sbase, const double *lim) {
+        if (c <= 0) return;
+        const long long avail = lim - K;       // elements readable from K
+        // keys: 16-byte chunks of 2
+        const int ks = -(off & 1);
+        int ke = ks + ((c - ks + 1) & ~1);
+        if (ke > avail) ke = ks + (int)((avail - ks) & ~1LL);
+        if (ke > ks) {
+            tma_load_1d(sk + sbase + off + ks, K + ks, (uint32_t)(ke - ks) * 8u, bar, policy);
+        }
+        for (int e = max(ke, 0); e < c; ++e) sk[sbase + off + e] = K[e];
+        if (HV) {
+            const int vs = -off;
+            int ve = vs + ((c - vs + 3) & ~3);
+            if (ve > avail) ve = vs + (int)((avail - vs) & ~3LL);
+            if (ve > vs) {
+                tma_load_1d(sv + sbase + off + vs, V + vs, (uint32_t)(ve - vs) * 4u, bar, policy);
+            }
+            for (int e = max(ve, 0); e < c; ++e) sv[sbase + off + e] = V[e];
+        }
+    };
+    // expect_tx must be posted before the copies can complete the phase:
+    // count first, then arrive, then issue.
+    {
+        // dry run of the byte count (same arithmetic as run())
+        auto bytes = [&](const double *K, int c, int off, const double *lim) -> uint32_t {
+            if (c <= 0) return 0;
+            const long long avail = lim - K;
+            uint32_t b = 0;
+            const int ks = -(off & 1);
+            int ke = ks + ((c - ks + 1) & ~1);
+            if (ke > avail) ke = ks + (int)((avail - ks) & ~1LL);
+            if (ke > ks) b += (uint32_t)(ke - ks) * 8u;
+            if (HV) {
+                const int vs = -off;
+                int ve = vs + ((c - vs + 3) & ~3);
+                if (ve > avail) ve = vs + (int)((avail - vs) & ~3LL);
+                if (ve > vs) b += (uint32_t)(ve - vs) * 4u;
+            }
+            return b;
+        };
+        const uint32_t total = bytes(Ak, ca, offa, pg.a_lim) + bytes(Bk, cb, offb, pg.b_lim);
+        mbar_arrive_expect_tx(bar, total);
+    }
+    run(Ak, Av, ca, offa, 0, pg.a_lim);
+    run(Bk, Bv, cb, offb, bbase, pg.b_lim);
+    meta->t = t;
+    meta->ca = ca;
+    meta->cb = cb;
+    meta->offa = offa;
+    meta->bslot = bbase + offb;
+}
+
+struct Lin { __device__ __forceinline__ int operator()(int e) const { return e; } };
+
+template <bool HV>
+__global__ void __launch_bounds__(NT, 2)
+merge_pipe_kernel(PipeGeo pg, const int *__restrict__ corank, int ntiles)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ __align__(8) uint64_t bars[PIPE_STAGES];
+    __shared__ PipeMeta meta[PIPE_STAGES];
+    auto skb = [&](int st) { return reinterpret_cast<double *>(smem_raw + st * pipe_stage_bytes(HV)); };
+    auto svb = [&](int st) {
+        return reinterpret_cast<uint32_t *>(smem_raw + st * pipe_stage_bytes(HV) + PIPE_SLOTS * sizeof(double));
+    };
+    const int tid = threadIdx.x;
+    const int G = gridDim.x;
+    uint64_t policy = 0;
+    if (tid == 0) {
+        policy = policy_evict_first();
+        for (int st = 0; st < PIPE_STAGES; ++st) mbar_init(&bars[st], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    int t = blockIdx.x;
+    if (tid == 0 && t < ntiles) pipe_issue<HV>(pg, corank, t, skb(0), svb(0), &bars[0], &meta[0], policy);
+    __syncthreads();
+    for (int i = 0; t < ntiles; ++i, t += G) {
+        const int st = i & 1;
+        const int tn = t + G;
+        if (tid == 0 && tn < ntiles)
+            pipe_issue<HV>(pg, corank, tn, skb(st ^ 1), svb(st ^ 1), &bars[st ^ 1], &meta[st ^ 1], policy);
+        mbar_wait(&bars[st], (uint32_t)((i >> 1) & 1));
+        const PipeMeta m = meta[st];
+        const int cnt = m.ca + m.cb;
+        const int d = min(tid * VT, cnt);
+        const double *sk = skb(st);
+        const uint32_t *sv = svb(st);
+        const int ii = merge_path_smem(sk, m.offa, m.ca, m.bslot, m.cb, d, Lin());
+        double k[VT];
+        uint32_t v[VT];
+        serial_merge<HV>(sk, sv, m.offa + ii, m.offa + m.ca, m.bslot + d - ii, m.bslot + m.cb, k, v, Lin(), Lin());
+        store_segment<HV>(pg.g.ok, pg.g.ov, (long long)t * MTILE + tid * VT, cnt - d, k, v);
+        __syncthreads();   // stage st fully consumed (and next meta visible) before it is refilled
+    }
 }
 
 }  // namespace gns
