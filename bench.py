@@ -296,7 +296,7 @@ def main():
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded SplitMix64, see DESIGN.md §3)",
         "config": dict(config_json(case, args.frac), parallelism=f"replicas{world}" if world > 1 else "single"),
-        "roofline": {"bound": "hbm", "kernel": "merge pass (K2 partition + K3 merge), avg over "
+        "roofline": {"bound": "hbm", "kernel": "merge pass (merge_fused_kernel: K2 co-rank search + K3 merge in one kernel), avg over "
                      f"{plan['merge_passes']} passes", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": 2 * n * s,
@@ -329,14 +329,14 @@ def launches(plan, frac, n):
     if n <= T:
         return 1
     if frac == 1.0:
-        return 1 + 2 * plan["merge_passes"]
+        return 1 + plan["merge_passes"]          # tile sort + one fused merge kernel per pass
     nl = plan["left_len"]
     nr = n - nl
 
     def lr(m):
         r = -(-m // T)
-        return 1 + 2 * max(0, (r - 1).bit_length()) if m > 0 else 0
-    return lr(nl) + lr(nr) + 3   # + partition, deps, top merge (memset is a copy-engine op)
+        return 1 + max(0, (r - 1).bit_length()) if m > 0 else 0
+    return lr(nl) + lr(nr) + 3   # + partition, deps (also clears the flags), top merge
 
 
 def kernel_roofline(gns, torch, dev, stream, src_k, src_v, k, v, n, hv, s, plan, restore, reps=5):

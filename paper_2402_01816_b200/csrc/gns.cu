@@ -10,6 +10,7 @@
 
 #include <cuda_runtime.h>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <algorithm>
 #include <mutex>
@@ -122,6 +123,8 @@ gns_status ensure_attrs()
     const int kp0 = (int)(PIPE_STAGES * pipe_stage_bytes(false));
     GNS_TRY(check(cudaFuncSetAttribute(merge_pipe_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kp1), "attr"));
     GNS_TRY(check(cudaFuncSetAttribute(merge_pipe_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kp0), "attr"));
+    GNS_TRY(check(cudaFuncSetAttribute(merge_fused_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kp1), "attr"));
+    GNS_TRY(check(cudaFuncSetAttribute(merge_fused_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kp0), "attr"));
     GNS_TRY(check(cudaDeviceGetAttribute(&g_num_sms[dev], cudaDevAttrMultiProcessorCount, dev), "sm count"));
     g_attr_done |= (1ull << dev);
     return GNS_OK;
@@ -135,6 +138,37 @@ int num_sms()
 }
 
 // ------------------------------------------------------------------ launches
+// GNS_PDL=1 in the environment enables programmatic dependent launch (off by
+// default: measured slower on B200 with the persistent merge kernels).
+bool pdl_enabled()
+{
+    static const bool on = [] {
+        const char *e = std::getenv("GNS_PDL");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
+
+// Every kernel is launched with programmatic stream serialization (PDL): it
+// may be scheduled while its predecessor drains and blocks in
+// griddepcontrol.wait until the predecessor's writes are visible.
+template <typename... KArgs, typename... Args>
+gns_status launch_pdl(const char *what, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                      cudaStream_t st, Args... args)
+{
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return check(cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...), what);
+}
+
 gns_status launch_tile_sort(const double *sk, const uint32_t *sv, double *dk, uint32_t *dv, size_t n,
                             cudaStream_t st)
 {
@@ -142,9 +176,9 @@ gns_status launch_tile_sort(const double *sk, const uint32_t *sv, double *dk, ui
     const unsigned grid = (unsigned)ceil_div(n, TILE);
     const bool hv = sv != nullptr;
     const size_t smem = K1_SMEM_KEYS + (hv ? sizeof(uint32_t) * K1_SV : 0);
-    if (hv) tile_sort_kernel<true><<<grid, NT, smem, st>>>(sk, sv, dk, dv, (long long)n);
-    else tile_sort_kernel<false><<<grid, NT, smem, st>>>(sk, nullptr, dk, nullptr, (long long)n);
-    return check(cudaGetLastError(), "tile_sort_kernel");
+    if (hv) return launch_pdl("tile_sort_kernel", tile_sort_kernel<true>, grid, NT, smem, st, sk, sv, dk, dv, (long long)n);
+    return launch_pdl("tile_sort_kernel", tile_sort_kernel<false>, grid, NT, smem, st, sk, (const uint32_t *)nullptr,
+                      dk, (uint32_t *)nullptr, (long long)n);
 }
 
 gns_status launch_merge(const MergeGeo &g, const double *lim_a, const double *lim_b, int *corank, int2 *deps,
@@ -152,27 +186,29 @@ gns_status launch_merge(const MergeGeo &g, const double *lim_a, const double *li
 {
     const int ntiles = (int)ceil_div((size_t)g.n, MTILE);
     const bool hv = g.av != nullptr;
-    partition_kernel<<<(unsigned)ceil_div((size_t)ntiles * 32, 256), 256, 0, st>>>(g, ntiles, corank);
-    GNS_TRY(check(cudaGetLastError(), "partition_kernel"));
-    const size_t smem = K3_SMEM_KEYS + (hv ? sizeof(uint32_t) * K3_SK : 0);
     if (!inplace) {
+        // K2+K3 fused: partition inside the persistent pipelined merge kernel
         PipeGeo pg;
         pg.g = g;
         pg.a_lim = lim_a;
         pg.b_lim = lim_b;
-        const int grid = std::min(ntiles, 2 * num_sms());
         const size_t psmem = PIPE_STAGES * pipe_stage_bytes(hv);
-        if (hv) merge_pipe_kernel<true><<<grid, NT, psmem, st>>>(pg, corank, ntiles);
-        else merge_pipe_kernel<false><<<grid, NT, psmem, st>>>(pg, corank, ntiles);
-        return check(cudaGetLastError(), "merge_pipe_kernel");
+        const int ctas = std::min(ntiles, 2 * num_sms());
+        const int per = (int)ceil_div(ntiles, ctas);
+        const int grid = (int)ceil_div(ntiles, per);
+        if (hv) return launch_pdl("merge_fused_kernel", merge_fused_kernel<true>, grid, FUSED_THREADS, psmem, st, pg, ntiles, per);
+        return launch_pdl("merge_fused_kernel", merge_fused_kernel<false>, grid, FUSED_THREADS, psmem, st, pg, ntiles, per);
     }
-    inplace_deps_kernel<<<(unsigned)ceil_div(ntiles, 256), 256, 0, st>>>(corank, ntiles, g.L, g.n, deps);
-    GNS_TRY(check(cudaGetLastError(), "inplace_deps_kernel"));
-    GNS_TRY(check(cudaMemsetAsync(flags, 0, (size_t)(ntiles + 1) * sizeof(unsigned), st), "memset flags"));
+    GNS_TRY(launch_pdl("partition_kernel", partition_kernel, (unsigned)ceil_div((size_t)ntiles * 32, 256), 256, 0, st,
+                       g, ntiles, corank));
+    const size_t smem = K3_SMEM_KEYS + (hv ? sizeof(uint32_t) * K3_SK : 0);
+    GNS_TRY(launch_pdl("inplace_deps_kernel", inplace_deps_kernel, (unsigned)ceil_div(ntiles + 1, 256), 256, 0, st,
+                       (const int *)corank, ntiles, g.L, g.n, deps, flags));
     unsigned *ticket = flags + ntiles;
-    if (hv) merge_kernel<true, true><<<ntiles, NT, smem, st>>>(g, corank, deps, flags, ticket);
-    else merge_kernel<false, true><<<ntiles, NT, smem, st>>>(g, corank, deps, flags, ticket);
-    return check(cudaGetLastError(), "merge_kernel<inplace>");
+    if (hv) return launch_pdl("merge_kernel<inplace>", merge_kernel<true, true>, ntiles, NT, smem, st, g,
+                              (const int *)corank, (const int2 *)deps, flags, ticket);
+    return launch_pdl("merge_kernel<inplace>", merge_kernel<false, true>, ntiles, NT, smem, st, g, (const int *)corank,
+                      (const int2 *)deps, flags, ticket);
 }
 
 MergeGeo uniform_geo(const double *sk, const uint32_t *sv, double *dk, uint32_t *dv, size_t n, size_t L)

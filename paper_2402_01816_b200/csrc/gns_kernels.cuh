@@ -74,6 +74,12 @@ __device__ __forceinline__ void st_release(unsigned *p, unsigned v)
     asm volatile("st.release.gpu.global.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
 }
 
+// ---- programmatic dependent launch (PDL): every kernel of a sort waits for
+// its predecessor's completion before touching memory, and lets its successor
+// be scheduled early, hiding the launch latency between the ~25 launches.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // ---- mbarrier + TMA bulk copy (cp.async.bulk, SASS UBLKCP) helpers
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count)
@@ -189,6 +195,8 @@ template <bool HV>
 __global__ void __launch_bounds__(NT, 3)
 tile_sort_kernel(const double *src_k, const uint32_t *src_v, double *dst_k, uint32_t *dst_v, long long n)
 {
+    pdl_wait();
+    pdl_trigger();
     extern __shared__ __align__(16) unsigned char smem_raw[];
     double *sk = reinterpret_cast<double *>(smem_raw);
     uint32_t *sv = reinterpret_cast<uint32_t *>(smem_raw + K1_SMEM_KEYS);
@@ -298,13 +306,11 @@ __device__ __forceinline__ TileSpan tile_span(const MergeGeo &g, int t)
 // keeps the interval between the last true and first false predicate), about
 // 5 dependent rounds at L = 2^23 instead of 23 for a binary search.
 // "parallelize over an arbitrary number of processes".
-__global__ void __launch_bounds__(256)
-partition_kernel(MergeGeo g, int ntiles, int *__restrict__ corank)
+// Warp-cooperative stable co-rank of tile t's first diagonal (all 32 lanes
+// return the result).
+__device__ __forceinline__ int warp_corank(const MergeGeo &g, int t, int lane)
 {
-    const int warp = (int)((blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5);
-    const int lane = threadIdx.x & 31;
-    if (warp >= ntiles) return;
-    const TileSpan s = tile_span(g, warp);
+    const TileSpan s = tile_span(g, t);
     const double *A = g.ak + s.pbase;
     const double *B = g.bk + s.pbase;
     const int d = s.k0;
@@ -330,7 +336,55 @@ partition_kernel(MergeGeo g, int ntiles, int *__restrict__ corank)
         lo = nlo;
         hi = max(nlo, nhi);
     }
-    if (lane == 0) corank[warp] = lo;
+    return lo;
+}
+
+// Co-rank search by a group of W lanes (W = 16: two independent searches per
+// warp, (W+1)-ary).  `gl` = lane within the group; `mask` = the group's lanes.
+template <int W>
+__device__ __forceinline__ int group_corank(const MergeGeo &g, int t, int gl, unsigned mask, int gbase)
+{
+    const TileSpan s = tile_span(g, t);
+    const double *A = g.ak + s.pbase;
+    const double *B = g.bk + s.pbase;
+    const int d = s.k0;
+    int lo = max(0, d - s.nb), hi = min(d, s.na);
+    while (true) {
+        // group-uniform loop condition (all lanes of the group see the same lo/hi)
+        if (lo >= hi) break;
+        const int span = hi - lo;
+        int m, nprobe;
+        if (span <= W) {
+            m = lo + gl;
+            nprobe = span;
+        } else {
+            m = lo + (int)(((long long)span * (gl + 1)) / (W + 1));
+            nprobe = W;
+        }
+        bool p = false;
+        if (gl < nprobe) p = A[m] <= B[d - 1 - m];
+        const unsigned bal = (__ballot_sync(mask, p) & mask) >> gbase;
+        const int c = __popc(bal);
+        const int m_prev = __shfl_sync(mask, m, gbase + (c > 0 ? c - 1 : 0));
+        const int m_next = __shfl_sync(mask, m, gbase + (c < nprobe ? c : 0));
+        const int nlo = (c == 0) ? lo : m_prev + 1;
+        const int nhi = (c == nprobe) ? hi : m_next;
+        lo = nlo;
+        hi = max(nlo, nhi);
+    }
+    return lo;
+}
+
+__global__ void __launch_bounds__(256)
+partition_kernel(MergeGeo g, int ntiles, int *__restrict__ corank)
+{
+    pdl_wait();
+    pdl_trigger();
+    const int warp = (int)((blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5);
+    const int lane = threadIdx.x & 31;
+    if (warp >= ntiles) return;
+    const int c = warp_corank(g, warp, lane);
+    if (lane == 0) corank[warp] = c;
 }
 
 // ---------------------------------------------- K4 dependency ranges (row a6)
@@ -345,10 +399,15 @@ __device__ __forceinline__ long long j_start(const int *corank, int u)
 }
 
 __global__ void __launch_bounds__(256)
-inplace_deps_kernel(const int *__restrict__ corank, int ntiles, long long L, long long n, int2 *deps)
+inplace_deps_kernel(const int *__restrict__ corank, int ntiles, long long L, long long n, int2 *deps,
+                    unsigned *flags)
 {
+    pdl_wait();
+    pdl_trigger();
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= ntiles) return;
+    if (t > ntiles) return;
+    flags[t] = 0u;           // flags[0:ntiles) = "loaded", flags[ntiles] = ticket counter
+    if (t == ntiles) return;
     const long long k0 = (long long)t * MTILE;
     const long long k1 = min(k0 + MTILE, n);
     // u_lo: first u in [0,t) with L + j1(u) > k0, where j1(u) = j_start(u+1)
@@ -384,6 +443,8 @@ __global__ void __launch_bounds__(NT, 3)
 merge_kernel(MergeGeo g, const int *__restrict__ corank, const int2 *__restrict__ deps,
              unsigned *flags, unsigned *ticket)
 {
+    pdl_wait();
+    pdl_trigger();
     extern __shared__ __align__(16) unsigned char smem_raw[];
     double *sk = reinterpret_cast<double *>(smem_raw);
     uint32_t *sv = reinterpret_cast<uint32_t *>(smem_raw + K3_SMEM_KEYS);
@@ -483,15 +544,14 @@ struct PipeMeta {
 // into stage buffers sk/sv, completing on `bar`.  Leftover unaligned tail
 // elements are copied with plain loads (made visible by the caller's barrier).
 template <bool HV>
-__device__ __forceinline__ void pipe_issue(const PipeGeo &pg, const int *__restrict__ corank, int t,
+__device__ __forceinline__ void pipe_issue(const PipeGeo &pg, int t, int i0, int i1next,
                                            double *sk, uint32_t *sv, uint64_t *bar, PipeMeta *meta,
                                            uint64_t policy)
 {
     const MergeGeo &g = pg.g;
     const TileSpan s = tile_span(g, t);
     const int cnt = s.k1 - s.k0;
-    const int i0 = corank[t];
-    int i1 = (s.k1 == s.na + s.nb) ? s.na : corank[t + 1];
+    int i1 = (s.k1 == s.na + s.nb) ? s.na : i1next;
     i1 = min(min(max(max(i1, i0), s.k1 - s.nb), i0 + cnt), s.na);
     const int j0 = s.k0 - i0;
     const int ca = i1 - i0, cb = cnt - ca;
@@ -559,9 +619,10 @@ __device__ __forceinline__ void pipe_issue(const PipeGeo &pg, const int *__restr
 struct Lin { __device__ __forceinline__ int operator()(int e) const { return e; } };
 
 template <bool HV>
-__global__ void __launch_bounds__(NT, 2)
+__global__ void __launch_bounds__(NT, HV ? 2 : 3)
 merge_pipe_kernel(PipeGeo pg, const int *__restrict__ corank, int ntiles)
 {
+    pdl_wait();
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ __align__(8) uint64_t bars[PIPE_STAGES];
     __shared__ PipeMeta meta[PIPE_STAGES];
@@ -579,13 +640,15 @@ merge_pipe_kernel(PipeGeo pg, const int *__restrict__ corank, int ntiles)
     }
     __syncthreads();
     int t = blockIdx.x;
-    if (tid == 0 && t < ntiles) pipe_issue<HV>(pg, corank, t, skb(0), svb(0), &bars[0], &meta[0], policy);
+    if (tid == 0 && t < ntiles)
+        pipe_issue<HV>(pg, t, corank[t], t + 1 < ntiles ? corank[t + 1] : 0, skb(0), svb(0), &bars[0], &meta[0], policy);
     __syncthreads();
     for (int i = 0; t < ntiles; ++i, t += G) {
         const int st = i & 1;
         const int tn = t + G;
         if (tid == 0 && tn < ntiles)
-            pipe_issue<HV>(pg, corank, tn, skb(st ^ 1), svb(st ^ 1), &bars[st ^ 1], &meta[st ^ 1], policy);
+            pipe_issue<HV>(pg, tn, corank[tn], tn + 1 < ntiles ? corank[tn + 1] : 0, skb(st ^ 1), svb(st ^ 1),
+                           &bars[st ^ 1], &meta[st ^ 1], policy);
         mbar_wait(&bars[st], (uint32_t)((i >> 1) & 1));
         const PipeMeta m = meta[st];
         const int cnt = m.ca + m.cb;
@@ -599,6 +662,124 @@ merge_pipe_kernel(PipeGeo pg, const int *__restrict__ corank, int ntiles)
         store_segment<HV>(pg.g.ok, pg.g.ov, (long long)t * MTILE + tid * VT, cnt - d, k, v);
         __syncthreads();   // stage st fully consumed (and next meta visible) before it is refilled
     }
+    pdl_trigger();         // successor may launch while the last tiles drain
+}
+
+
+// ------------------------------------- K2+K3 fused: the production merge pass
+// Same pipeline as merge_pipe_kernel, but the co-rank partition (row a3) is
+// done inside the kernel: CTA c owns the contiguous tiles [first, last), so
+// it needs the splits at first..last only (tile t ends where t+1 starts).
+// Warps 0-7 merge; warp 8 is a dedicated search warp that runs ahead
+// computing splits into a shared ring (32-ary warp searches, ~5 dependent
+// rounds each) while the merge warps work, so no partition kernel, no
+// co-rank array in HBM and no extra launch per pass.  At kernel start all 9
+// warps compute the first splits in parallel.
+constexpr int SEARCH_WARPS = 2;
+constexpr int FUSED_THREADS = NT + 32 * SEARCH_WARPS;
+constexpr int SPL_RING = 64;
+
+__device__ __forceinline__ void bar_merge_warps() { asm volatile("bar.sync 1, %0;" :: "n"(NT) : "memory"); }
+
+template <bool HV>
+__global__ void __launch_bounds__(FUSED_THREADS, 2)
+merge_fused_kernel(PipeGeo pg, int ntiles, int per_cta)
+{
+    pdl_wait();
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ __align__(8) uint64_t bars[PIPE_STAGES];
+    __shared__ PipeMeta meta[PIPE_STAGES];
+    __shared__ int spl[SPL_RING];
+    __shared__ volatile int spl_tag[SPL_RING];   // spl_tag[j % R] == j  <=>  split j is in spl[j % R]
+    __shared__ volatile int spl_used;            // splits [0, spl_used) may be overwritten
+    auto skb = [&](int st) { return reinterpret_cast<double *>(smem_raw + st * pipe_stage_bytes(HV)); };
+    auto svb = [&](int st) {
+        return reinterpret_cast<uint32_t *>(smem_raw + st * pipe_stage_bytes(HV) + PIPE_SLOTS * sizeof(double));
+    };
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    const int first = blockIdx.x * per_cta;
+    const int last = min(first + per_cta, ntiles);
+    const int m = last - first;            // tiles of this CTA
+    if (m <= 0) return;
+    const int nspl = (last < ntiles) ? m + 1 : m;   // splits j = 0..nspl-1 (tile first+j's start)
+    for (int j = tid; j < SPL_RING; j += FUSED_THREADS) spl_tag[j] = -1;
+    __syncthreads();
+    // phase 0: the first splits, one per warp, full-warp (lowest latency) searches
+    const int init = min(nspl, FUSED_THREADS / 32);
+    if (warp < init) {
+        const int c = warp_corank(pg.g, first + warp, lane);
+        if (lane == 0) {
+            spl[warp] = c;
+            spl_tag[warp] = warp;
+        }
+    }
+    uint64_t policy = 0;
+    if (tid == 0) {
+        policy = policy_evict_first();
+        for (int st = 0; st < PIPE_STAGES; ++st) mbar_init(&bars[st], 1);
+        fence_mbar_init();
+        spl_used = 0;
+    }
+    __syncthreads();
+
+    if (warp >= NT / 32) {
+        // search warps: two concurrent 16-lane searches per warp, splits
+        // init + 2*sw + h, step 2*SEARCH_WARPS; at most SPL_RING ahead.
+        const int sw = warp - NT / 32;
+        const int h = lane >> 4, gl = lane & 15;
+        const unsigned mask = 0xFFFFu << (16 * h);
+        for (int j0 = init + 2 * sw; j0 < nspl; j0 += 2 * SEARCH_WARPS) {
+            const int j = j0 + h;
+            while (j0 + 1 - spl_used >= SPL_RING) { __nanosleep(64); }
+            if (j < nspl) {
+                const int c = group_corank<16>(pg.g, first + j, gl, mask, 16 * h);
+                if (gl == 0) {
+                    spl[j % SPL_RING] = c;
+                    __threadfence_block();
+                    spl_tag[j % SPL_RING] = j;
+                }
+            }
+            __syncwarp();
+        }
+        return;
+    }
+
+    // merge warps
+    auto get_split = [&](int j) -> int {
+        while (spl_tag[j % SPL_RING] != j) { }
+        return spl[j % SPL_RING];
+    };
+    if (tid == 0) {
+        pipe_issue<HV>(pg, first, get_split(0), (1 < nspl) ? get_split(1) : 0, skb(0), svb(0), &bars[0], &meta[0],
+                       policy);
+        spl_used = 1;
+    }
+    bar_merge_warps();
+    for (int i = 0; i < m; ++i) {
+        const int st = i & 1;
+        const int t = first + i;
+        if (tid == 0 && i + 1 < m) {
+            const int j = i + 1;
+            pipe_issue<HV>(pg, t + 1, get_split(j), (j + 1 < nspl) ? get_split(j + 1) : 0, skb(st ^ 1), svb(st ^ 1),
+                           &bars[st ^ 1], &meta[st ^ 1], policy);
+            spl_used = j;
+        }
+        mbar_wait(&bars[st], (uint32_t)((i >> 1) & 1));
+        const PipeMeta mt = meta[st];
+        const int cnt = mt.ca + mt.cb;
+        const int d = min(tid * VT, cnt);
+        const double *sk = skb(st);
+        const uint32_t *sv = svb(st);
+        const int ii = merge_path_smem(sk, mt.offa, mt.ca, mt.bslot, mt.cb, d, Lin());
+        double k[VT];
+        uint32_t v[VT];
+        serial_merge<HV>(sk, sv, mt.offa + ii, mt.offa + mt.ca, mt.bslot + d - ii, mt.bslot + mt.cb, k, v, Lin(),
+                         Lin());
+        store_segment<HV>(pg.g.ok, pg.g.ov, (long long)t * MTILE + tid * VT, cnt - d, k, v);
+        bar_merge_warps();
+    }
+    pdl_trigger();
 }
 
 }  // namespace gns
