@@ -123,8 +123,26 @@ gns_status ensure_attrs()
     const int kp0 = (int)(PIPE_STAGES * pipe_stage_bytes(false));
     GNS_TRY(check(cudaFuncSetAttribute(merge_pipe_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kp1), "attr"));
     GNS_TRY(check(cudaFuncSetAttribute(merge_pipe_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kp0), "attr"));
-    GNS_TRY(check(cudaFuncSetAttribute(merge_fused_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kp1), "attr"));
-    GNS_TRY(check(cudaFuncSetAttribute(merge_fused_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kp0), "attr"));
+#define GNS_FUSED_ATTR(HV, S, D)                                                                          \
+    GNS_TRY(check(cudaFuncSetAttribute(merge_fused_kernel<HV, S, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                       (int)fused_smem(HV, S)), "attr"))
+    GNS_FUSED_ATTR(true, 2, false);
+    GNS_FUSED_ATTR(true, 2, true);
+    GNS_FUSED_ATTR(false, 2, false);
+    GNS_FUSED_ATTR(false, 2, true);
+    GNS_FUSED_ATTR(false, 3, false);
+    GNS_FUSED_ATTR(false, 3, true);
+    GNS_TRY(check(cudaFuncSetAttribute(merge_fused_kernel<true, 2, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)fused_smem(true, 2)), "attr"));
+    GNS_TRY(check(cudaFuncSetAttribute(merge_fused_kernel<false, 2, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)fused_smem(false, 2)), "attr"));
+    GNS_TRY(check(cudaFuncSetAttribute(merge_fused_kernel<false, 2, false, false, true>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fused_smem(false, 2)), "attr"));
+    GNS_TRY(check(cudaFuncSetAttribute(merge_async_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)fused_smem(true, 2)), "attr"));
+    GNS_TRY(check(cudaFuncSetAttribute(merge_async_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)fused_smem(false, 2)), "attr"));
+#undef GNS_FUSED_ATTR
     GNS_TRY(check(cudaDeviceGetAttribute(&g_num_sms[dev], cudaDevAttrMultiProcessorCount, dev), "sm count"));
     g_attr_done |= (1ull << dev);
     return GNS_OK;
@@ -138,6 +156,15 @@ int num_sms()
 }
 
 // ------------------------------------------------------------------ launches
+int merge_variant()
+{
+    static const int v = [] {
+        const char *e = std::getenv("GNS_MERGE_VARIANT");
+        return e ? std::atoi(e) : 0;
+    }();
+    return v;
+}
+
 // GNS_PDL=1 in the environment enables programmatic dependent launch (off by
 // default: measured slower on B200 with the persistent merge kernels).
 bool pdl_enabled()
@@ -192,12 +219,31 @@ gns_status launch_merge(const MergeGeo &g, const double *lim_a, const double *li
         pg.g = g;
         pg.a_lim = lim_a;
         pg.b_lim = lim_b;
-        const size_t psmem = PIPE_STAGES * pipe_stage_bytes(hv);
+        // GNS_MERGE_VARIANT (A/B): bit0 = decoupled warps, bit1 = 3 stages (key-only)
+        const int var = merge_variant();
+        const bool dec = var & 1;
+        const int S = (!hv && (var & 2)) ? 3 : 2;
+        const size_t psmem = fused_smem(hv, S);
         const int ctas = std::min(ntiles, 2 * num_sms());
         const int per = (int)ceil_div(ntiles, ctas);
         const int grid = (int)ceil_div(ntiles, per);
-        if (hv) return launch_pdl("merge_fused_kernel", merge_fused_kernel<true>, grid, FUSED_THREADS, psmem, st, pg, ntiles, per);
-        return launch_pdl("merge_fused_kernel", merge_fused_kernel<false>, grid, FUSED_THREADS, psmem, st, pg, ntiles, per);
+        auto kern = (var & 16) ? merge_fused_kernel<false, 2, false, false, true> : (var & 8) ? (hv ? merge_fused_kernel<true, 2, false, true> : merge_fused_kernel<false, 2, false, true>)
+                  : hv ? (dec ? merge_fused_kernel<true, 2, true> : merge_fused_kernel<true, 2, false>)
+                       : (S == 3 ? (dec ? merge_fused_kernel<false, 3, true> : merge_fused_kernel<false, 3, false>)
+                                 : (dec ? merge_fused_kernel<false, 2, true> : merge_fused_kernel<false, 2, false>));
+        if (var & 32) {
+            if (hv) return launch_pdl("merge_async_kernel", merge_async_kernel<true>, grid, FUSED_THREADS,
+                                      fused_smem(true, 2), st, pg, ntiles, per);
+            return launch_pdl("merge_async_kernel", merge_async_kernel<false>, grid, FUSED_THREADS, fused_smem(false, 2),
+                              st, pg, ntiles, per);
+        }
+        const int *pre = nullptr;
+        if (var & 4) {   // A/B: precomputed splits from the separate partition kernel
+            GNS_TRY(launch_pdl("partition_kernel", partition_kernel, (unsigned)ceil_div((size_t)ntiles * 32, 256), 256,
+                               0, st, g, ntiles, corank));
+            pre = corank;
+        }
+        return launch_pdl("merge_fused_kernel", kern, grid, FUSED_THREADS, psmem, st, pg, ntiles, per, pre);
     }
     GNS_TRY(launch_pdl("partition_kernel", partition_kernel, (unsigned)ceil_div((size_t)ntiles * 32, 256), 256, 0, st,
                        g, ntiles, corank));

@@ -95,6 +95,15 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t by
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(smem_u32(bar)), "r"(bytes)
                  : "memory");
 }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes)
+{
+    asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar)
+{
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" :: "r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
 {
     asm volatile("{\n\t.reg .pred p;\n"
@@ -103,6 +112,21 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
                  "@!p bra GNS_WAIT_%=;\n}"
                  :: "r"(smem_u32(bar)), "r"(parity) : "memory");
 }
+// cp.async (LDGSTS) of one 8- or 4-byte element, and the mbarrier arrival that
+// fires when all of this thread's earlier cp.asyncs have landed.
+__device__ __forceinline__ void cp_async_8(void *dst, const void *src)
+{
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" :: "r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_4(void *dst, const void *src)
+{
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" :: "r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_mbar_arrive(uint64_t *bar)
+{
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" :: "r"(smem_u32(bar)) : "memory");
+}
+
 // 1-D bulk copy global -> shared, completion counted on `bar` (16-byte aligned
 // addresses, size a multiple of 16).  L2 evict-first: every byte is read once.
 __device__ __forceinline__ void tma_load_1d(void *dst, const void *src, uint32_t bytes, uint64_t *bar,
@@ -180,6 +204,59 @@ __device__ __forceinline__ void serial_merge(const double *sk, const uint32_t *s
         if (p) bi = nxt; else ai = nxt;
         const double kn = sk[ik(nxt)];
         if (p) kb = kn; else ka = kn;
+    }
+}
+
+// Two independent merge paths / serial merges per thread, interleaved so the
+// two dependency chains overlap (ILP 2): the thread's VT outputs are split into
+// halves starting at diagonals d and d + VT/2.
+template <class IX>
+__device__ __forceinline__ void merge_path_smem2(const double *s, int a0, int na, int b0, int nb, int d1, int d2,
+                                                 IX ix, int &r1, int &r2)
+{
+    int lo1 = max(0, d1 - nb), hi1 = min(d1, na);
+    int lo2 = max(0, d2 - nb), hi2 = min(d2, na);
+    while (lo1 < hi1 || lo2 < hi2) {
+        const int m1 = (lo1 + hi1) >> 1, m2 = (lo2 + hi2) >> 1;
+        const bool a1 = lo1 < hi1, a2 = lo2 < hi2;
+        const double x1 = s[ix(a0 + m1)], y1 = s[ix(b0 + max(d1 - 1 - m1, 0))];
+        const double x2 = s[ix(a0 + m2)], y2 = s[ix(b0 + max(d2 - 1 - m2, 0))];
+        const bool p1 = x1 <= y1, p2 = x2 <= y2;
+        if (a1) { if (p1) lo1 = m1 + 1; else hi1 = m1; }
+        if (a2) { if (p2) lo2 = m2 + 1; else hi2 = m2; }
+    }
+    r1 = lo1;
+    r2 = lo2;
+}
+
+template <bool HV, class IK, class IV>
+__device__ __forceinline__ void serial_merge2(const double *sk, const uint32_t *sv, int ai, int bi, int ci, int di,
+                                              int aend, int bend, double (&k)[VT], uint32_t (&v)[VT], IK ik, IV iv)
+{
+    // chain 1 fills k[0 .. VT/2), chain 2 fills k[VT/2 .. VT); both merge the
+    // same runs A = [.., aend), B = [.., bend) from different starting points.
+    constexpr int H = VT / 2;
+    double ka = sk[ik(ai)], kb = sk[ik(bi)];
+    double kc = sk[ik(ci)], kd = sk[ik(di)];
+#pragma unroll
+    for (int x = 0; x < H; ++x) {
+        const bool p = (bi < bend) && ((ai >= aend) || (kb < ka));
+        const bool q = (di < bend) && ((ci >= aend) || (kd < kc));
+        k[x] = p ? kb : ka;
+        k[H + x] = q ? kd : kc;
+        const int s1 = p ? bi : ai;
+        const int s2 = q ? di : ci;
+        if (HV) {
+            v[x] = sv[iv(s1)];
+            v[H + x] = sv[iv(s2)];
+        }
+        const int n1 = s1 + 1, n2 = s2 + 1;
+        if (p) bi = n1; else ai = n1;
+        if (q) di = n2; else ci = n2;
+        const double kn1 = sk[ik(n1)];
+        const double kn2 = sk[ik(n2)];
+        if (p) kb = kn1; else ka = kn1;
+        if (q) kd = kn2; else kc = kn2;
     }
 }
 
@@ -584,8 +661,7 @@ __device__ __forceinline__ void pipe_issue(const PipeGeo &pg, int t, int i0, int
             for (int e = max(ve, 0); e < c; ++e) sv[sbase + off + e] = V[e];
         }
     };
-    // expect_tx must be posted before the copies can complete the phase:
-    // count first, then arrive, then issue.
+    // Post the expected byte count first (no arrival yet), then issue.
     {
         // dry run of the byte count (same arithmetic as run())
         auto bytes = [&](const double *K, int c, int off, const double *lim) -> uint32_t {
@@ -605,7 +681,7 @@ __device__ __forceinline__ void pipe_issue(const PipeGeo &pg, int t, int i0, int
             return b;
         };
         const uint32_t total = bytes(Ak, ca, offa, pg.a_lim) + bytes(Bk, cb, offb, pg.b_lim);
-        mbar_arrive_expect_tx(bar, total);
+        mbar_expect_tx(bar, total);
     }
     run(Ak, Av, ca, offa, 0, pg.a_lim);
     run(Bk, Bv, cb, offb, bbase, pg.b_lim);
@@ -614,6 +690,10 @@ __device__ __forceinline__ void pipe_issue(const PipeGeo &pg, int t, int i0, int
     meta->cb = cb;
     meta->offa = offa;
     meta->bslot = bbase + offb;
+    // The stage's phase completes only after this arrive (the barrier expects
+    // one arrival) and the bulk-copy bytes: everything written above by this
+    // thread (meta, unaligned tail elements) is released to the waiters.
+    mbar_arrive(bar);
 }
 
 struct Lin { __device__ __forceinline__ int operator()(int e) const { return e; } };
@@ -678,17 +758,25 @@ merge_pipe_kernel(PipeGeo pg, const int *__restrict__ corank, int ntiles)
 constexpr int SEARCH_WARPS = 2;
 constexpr int FUSED_THREADS = NT + 32 * SEARCH_WARPS;
 constexpr int SPL_RING = 64;
-
 __device__ __forceinline__ void bar_merge_warps() { asm volatile("bar.sync 1, %0;" :: "n"(NT) : "memory"); }
+constexpr size_t fused_smem(bool hv, int stages) { return stages * pipe_stage_bytes(hv); }
 
-template <bool HV>
+// Two consumption schemes (A/B-selectable at launch):
+//  DECOUPLED = false: the 8 merge warps meet at a named barrier after every
+//    tile; thread 0 refills the freed stage with tile i + S - 1 at the start
+//    of iteration i.
+//  DECOUPLED = true: no CTA barrier; each warp waits on the stage's "full"
+//    mbarrier, merges its 512 outputs, and bumps the stage's consumed counter;
+//    the last reader refills the stage with tile i + S.
+template <bool HV, int S, bool DECOUPLED, bool DUAL = false, bool COPY_ONLY = false>
 __global__ void __launch_bounds__(FUSED_THREADS, 2)
-merge_fused_kernel(PipeGeo pg, int ntiles, int per_cta)
+merge_fused_kernel(PipeGeo pg, int ntiles, int per_cta, const int *__restrict__ pre)
 {
     pdl_wait();
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    __shared__ __align__(8) uint64_t bars[PIPE_STAGES];
-    __shared__ PipeMeta meta[PIPE_STAGES];
+    __shared__ __align__(8) uint64_t bars[S];
+    __shared__ PipeMeta meta[S];
+    __shared__ int consumed[S];
     __shared__ int spl[SPL_RING];
     __shared__ volatile int spl_tag[SPL_RING];   // spl_tag[j % R] == j  <=>  split j is in spl[j % R]
     __shared__ volatile int spl_used;            // splits [0, spl_used) may be overwritten
@@ -706,18 +794,21 @@ merge_fused_kernel(PipeGeo pg, int ntiles, int per_cta)
     for (int j = tid; j < SPL_RING; j += FUSED_THREADS) spl_tag[j] = -1;
     __syncthreads();
     // phase 0: the first splits, one per warp, full-warp (lowest latency) searches
-    const int init = min(nspl, FUSED_THREADS / 32);
-    if (warp < init) {
+    // (pre != nullptr: splits were precomputed by partition_kernel; A/B only)
+    const int init = pre ? nspl : min(nspl, FUSED_THREADS / 32);
+    if (!pre && warp < init) {
         const int c = warp_corank(pg.g, first + warp, lane);
         if (lane == 0) {
             spl[warp] = c;
             spl_tag[warp] = warp;
         }
     }
-    uint64_t policy = 0;
+    uint64_t policy = policy_evict_first();
     if (tid == 0) {
-        policy = policy_evict_first();
-        for (int st = 0; st < PIPE_STAGES; ++st) mbar_init(&bars[st], 1);
+        for (int st = 0; st < S; ++st) {
+            mbar_init(&bars[st], 1);
+            consumed[st] = 0;
+        }
         fence_mbar_init();
         spl_used = 0;
     }
@@ -747,36 +838,199 @@ merge_fused_kernel(PipeGeo pg, int ntiles, int per_cta)
 
     // merge warps
     auto get_split = [&](int j) -> int {
+        if (pre) return pre[first + j];
         while (spl_tag[j % SPL_RING] != j) { }
         return spl[j % SPL_RING];
     };
-    if (tid == 0) {
-        pipe_issue<HV>(pg, first, get_split(0), (1 < nspl) ? get_split(1) : 0, skb(0), svb(0), &bars[0], &meta[0],
-                       policy);
-        spl_used = 1;
-    }
-    bar_merge_warps();
+    auto issue = [&](int i) {      // tile first+i into stage i % S
+        const int st = i % S;
+        pipe_issue<HV>(pg, first + i, get_split(i), (i + 1 < nspl) ? get_split(i + 1) : 0, skb(st), svb(st),
+                       &bars[st], &meta[st], policy);
+        spl_used = i;
+    };
+    if (tid == 0)
+        for (int i = 0; i < (DECOUPLED ? S : S - 1) && i < m; ++i) issue(i);
+    if (!DECOUPLED) bar_merge_warps();
     for (int i = 0; i < m; ++i) {
-        const int st = i & 1;
-        const int t = first + i;
-        if (tid == 0 && i + 1 < m) {
-            const int j = i + 1;
-            pipe_issue<HV>(pg, t + 1, get_split(j), (j + 1 < nspl) ? get_split(j + 1) : 0, skb(st ^ 1), svb(st ^ 1),
-                           &bars[st ^ 1], &meta[st ^ 1], policy);
-            spl_used = j;
-        }
-        mbar_wait(&bars[st], (uint32_t)((i >> 1) & 1));
+        const int st = i % S;
+        if (!DECOUPLED && tid == 0 && i + S - 1 < m) issue(i + S - 1);
+        mbar_wait(&bars[st], (uint32_t)((i / S) & 1));
         const PipeMeta mt = meta[st];
         const int cnt = mt.ca + mt.cb;
         const int d = min(tid * VT, cnt);
         const double *sk = skb(st);
         const uint32_t *sv = svb(st);
-        const int ii = merge_path_smem(sk, mt.offa, mt.ca, mt.bslot, mt.cb, d, Lin());
         double k[VT];
         uint32_t v[VT];
-        serial_merge<HV>(sk, sv, mt.offa + ii, mt.offa + mt.ca, mt.bslot + d - ii, mt.bslot + mt.cb, k, v, Lin(),
-                         Lin());
-        store_segment<HV>(pg.g.ok, pg.g.ov, (long long)t * MTILE + tid * VT, cnt - d, k, v);
+        if (COPY_ONLY) {   // A/B timing probe only: no merge, wrong output
+#pragma unroll
+            for (int x = 0; x < VT; ++x) {
+                k[x] = sk[min(d + x, MTILE)];
+                if (HV) v[x] = sv[min(d + x, MTILE)];
+            }
+        } else if (DUAL) {
+            const int d2 = min(tid * VT + VT / 2, cnt);
+            int i1, i2;
+            merge_path_smem2(sk, mt.offa, mt.ca, mt.bslot, mt.cb, d, d2, Lin(), i1, i2);
+            serial_merge2<HV>(sk, sv, mt.offa + i1, mt.bslot + d - i1, mt.offa + i2, mt.bslot + d2 - i2,
+                              mt.offa + mt.ca, mt.bslot + mt.cb, k, v, Lin(), Lin());
+        } else {
+            const int ii = merge_path_smem(sk, mt.offa, mt.ca, mt.bslot, mt.cb, d, Lin());
+            serial_merge<HV>(sk, sv, mt.offa + ii, mt.offa + mt.ca, mt.bslot + d - ii, mt.bslot + mt.cb, k, v, Lin(),
+                             Lin());
+        }
+        if (DECOUPLED) {
+            __syncwarp();
+            if (lane == 0) {
+                __threadfence_block();
+                const int old = atomicAdd(&consumed[st], 1);
+                if (old == NT / 32 - 1) {
+                    consumed[st] = 0;
+                    if (i + S < m) issue(i + S);
+                }
+            }
+        }
+        store_segment<HV>(pg.g.ok, pg.g.ov, (long long)(first + i) * MTILE + tid * VT, cnt - d, k, v);
+        if (!DECOUPLED) bar_merge_warps();
+    }
+    pdl_trigger();
+}
+
+
+// ------------------------- K2+K3 fused, cp.async variant (swizzled stage layout)
+// Like merge_fused_kernel<., 2, false>, but the stage is filled by all 256
+// merge threads with per-element cp.async (LDGSTS) into the XOR-swizzled
+// layout (slot swk(e) / swv(e)), so the merge-path and serial-merge reads
+// (lanes ~VT/2 apart in each run) are bank-conflict free; completion is
+// tracked by cp.async.mbarrier.arrive on the stage's mbarrier (count = 256).
+struct TileIn {
+    int ca, cb;
+    const double *Ak, *Bk;
+    const uint32_t *Av, *Bv;
+};
+
+__device__ __forceinline__ TileIn tile_inputs(const MergeGeo &g, int t, int i0, int i1next)
+{
+    const TileSpan s = tile_span(g, t);
+    const int cnt = s.k1 - s.k0;
+    int i1 = (s.k1 == s.na + s.nb) ? s.na : i1next;
+    i1 = min(min(max(max(i1, i0), s.k1 - s.nb), i0 + cnt), s.na);
+    const int j0 = s.k0 - i0;
+    TileIn r;
+    r.ca = i1 - i0;
+    r.cb = cnt - r.ca;
+    r.Ak = g.ak + s.pbase + i0;
+    r.Bk = g.bk + s.pbase + j0;
+    r.Av = g.av ? g.av + s.pbase + i0 : nullptr;
+    r.Bv = g.bv ? g.bv + s.pbase + j0 : nullptr;
+    return r;
+}
+
+template <bool HV>
+__global__ void __launch_bounds__(FUSED_THREADS, 2)
+merge_async_kernel(PipeGeo pg, int ntiles, int per_cta)
+{
+    pdl_wait();
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ __align__(8) uint64_t bars[2];
+    __shared__ TileIn tin[3];
+    __shared__ int spl[SPL_RING];
+    __shared__ volatile int spl_tag[SPL_RING];
+    __shared__ volatile int spl_used;
+    auto skb = [&](int st) { return reinterpret_cast<double *>(smem_raw + st * pipe_stage_bytes(HV)); };
+    auto svb = [&](int st) {
+        return reinterpret_cast<uint32_t *>(smem_raw + st * pipe_stage_bytes(HV) + PIPE_SLOTS * sizeof(double));
+    };
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    const int first = blockIdx.x * per_cta;
+    const int last = min(first + per_cta, ntiles);
+    const int m = last - first;
+    if (m <= 0) return;
+    const int nspl = (last < ntiles) ? m + 1 : m;
+    for (int j = tid; j < SPL_RING; j += FUSED_THREADS) spl_tag[j] = -1;
+    __syncthreads();
+    const int init = min(nspl, FUSED_THREADS / 32);
+    if (warp < init) {
+        const int c = warp_corank(pg.g, first + warp, lane);
+        if (lane == 0) {
+            spl[warp] = c;
+            spl_tag[warp] = warp;
+        }
+    }
+    if (tid == 0) {
+        mbar_init(&bars[0], NT);
+        mbar_init(&bars[1], NT);
+        fence_mbar_init();
+        spl_used = 0;
+    }
+    __syncthreads();
+
+    if (warp >= NT / 32) {
+        const int sw = warp - NT / 32;
+        const int h = lane >> 4, gl = lane & 15;
+        const unsigned mask = 0xFFFFu << (16 * h);
+        for (int j0 = init + 2 * sw; j0 < nspl; j0 += 2 * SEARCH_WARPS) {
+            const int j = j0 + h;
+            while (j0 + 1 - spl_used >= SPL_RING) { __nanosleep(64); }
+            if (j < nspl) {
+                const int c = group_corank<16>(pg.g, first + j, gl, mask, 16 * h);
+                if (gl == 0) {
+                    spl[j % SPL_RING] = c;
+                    __threadfence_block();
+                    spl_tag[j % SPL_RING] = j;
+                }
+            }
+            __syncwarp();
+        }
+        return;
+    }
+
+    auto get_split = [&](int j) -> int {
+        while (spl_tag[j % SPL_RING] != j) { }
+        return spl[j % SPL_RING];
+    };
+    auto plan = [&](int i) {       // thread 0: inputs of tile first+i -> tin[i % 3]
+        tin[i % 3] = tile_inputs(pg.g, first + i, get_split(i), (i + 1 < nspl) ? get_split(i + 1) : 0);
+        spl_used = i;
+    };
+    auto load = [&](int i) {       // all merge threads: cp.async tile first+i into stage i & 1
+        const TileIn ti = tin[i % 3];
+        const int cnt = ti.ca + ti.cb;
+        double *sk = skb(i & 1);
+        uint32_t *sv = svb(i & 1);
+#pragma unroll
+        for (int r = 0; r < VT; ++r) {
+            const int e = tid + r * NT;
+            if (e < cnt) {
+                const bool fa = e < ti.ca;
+                cp_async_8(sk + swk(e), fa ? ti.Ak + e : ti.Bk + (e - ti.ca));
+                if (HV) cp_async_4(sv + swv(e), fa ? ti.Av + e : ti.Bv + (e - ti.ca));
+            }
+        }
+        cp_async_mbar_arrive(&bars[i & 1]);
+    };
+    if (tid == 0) {
+        plan(0);
+        if (m > 1) plan(1);
+    }
+    bar_merge_warps();
+    load(0);
+    for (int i = 0; i < m; ++i) {
+        const int st = i & 1;
+        if (i + 1 < m) load(i + 1);
+        if (tid == 0 && i + 2 < m) plan(i + 2);
+        mbar_wait(&bars[st], (uint32_t)((i >> 1) & 1));
+        const TileIn ti = tin[i % 3];
+        const int cnt = ti.ca + ti.cb;
+        const int d = min(tid * VT, cnt);
+        const double *sk = skb(st);
+        const uint32_t *sv = svb(st);
+        double k[VT];
+        uint32_t v[VT];
+        const int ii = merge_path_smem(sk, 0, ti.ca, ti.ca, ti.cb, d, SwK());
+        serial_merge<HV>(sk, sv, ii, ti.ca, ti.ca + d - ii, cnt, k, v, SwK(), SwV());
+        store_segment<HV>(pg.g.ok, pg.g.ov, (long long)(first + i) * MTILE + tid * VT, cnt - d, k, v);
         bar_merge_warps();
     }
     pdl_trigger();
