@@ -142,6 +142,10 @@ gns_status ensure_attrs()
                                        (int)fused_smem(true, 2)), "attr"));
     GNS_TRY(check(cudaFuncSetAttribute(merge_async_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)fused_smem(false, 2)), "attr"));
+    GNS_TRY(check(cudaFuncSetAttribute(merge_tstore_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)ts_smem(true)), "attr"));
+    GNS_TRY(check(cudaFuncSetAttribute(merge_tstore_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)ts_smem(false)), "attr"));
 #undef GNS_FUSED_ATTR
     GNS_TRY(check(cudaDeviceGetAttribute(&g_num_sms[dev], cudaDevAttrMultiProcessorCount, dev), "sm count"));
     g_attr_done |= (1ull << dev);
@@ -156,11 +160,45 @@ int num_sms()
 }
 
 // ------------------------------------------------------------------ launches
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn()
+{
+    static EncodeTiledFn fn = [] {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return (EncodeTiledFn) nullptr;
+        return (EncodeTiledFn)p;
+    }();
+    return fn;
+}
+
+// Keys array of n doubles as a 2-D tensor [n/16][16], box [256][16], 128-B swizzle.
+gns_status key_store_map(double *keys, size_t n, CUtensorMap *map)
+{
+    EncodeTiledFn fn = encode_fn();
+    if (!fn) return fail(GNS_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    cuuint64_t dims[2] = {16, (cuuint64_t)(n / 16)};
+    cuuint64_t strides[1] = {16 * sizeof(double)};
+    cuuint32_t box[2] = {16, (cuuint32_t)(MTILE / 16)};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, keys, dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(GNS_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+    return GNS_OK;
+}
+
 int merge_variant()
 {
     static const int v = [] {
         const char *e = std::getenv("GNS_MERGE_VARIANT");
-        return e ? std::atoi(e) : 0;
+        return e ? std::atoi(e) : 64;
     }();
     return v;
 }
@@ -219,7 +257,10 @@ gns_status launch_merge(const MergeGeo &g, const double *lim_a, const double *li
         pg.g = g;
         pg.a_lim = lim_a;
         pg.b_lim = lim_b;
-        // GNS_MERGE_VARIANT (A/B): bit0 = decoupled warps, bit1 = 3 stages (key-only)
+        // GNS_MERGE_VARIANT (A/B experiments; default 64 = TMA tensor-store kernel):
+        // 0 = TMA-load/STG pipeline, bit0 = decoupled warps, bit1 = 3 stages (key-only),
+        // bit2 = precomputed splits, bit3 = dual chains, bit4 = copy-only probe,
+        // bit5 = cp.async swizzled loads, bit6 = TMA tensor stores
         const int var = merge_variant();
         const bool dec = var & 1;
         const int S = (!hv && (var & 2)) ? 3 : 2;
@@ -231,6 +272,14 @@ gns_status launch_merge(const MergeGeo &g, const double *lim_a, const double *li
                   : hv ? (dec ? merge_fused_kernel<true, 2, true> : merge_fused_kernel<true, 2, false>)
                        : (S == 3 ? (dec ? merge_fused_kernel<false, 3, true> : merge_fused_kernel<false, 3, false>)
                                  : (dec ? merge_fused_kernel<false, 2, true> : merge_fused_kernel<false, 2, false>));
+        if (var & 64) {
+            CUtensorMap map;
+            GNS_TRY(key_store_map(g.ok, (size_t)g.n, &map));
+            if (hv) return launch_pdl("merge_tstore_kernel", merge_tstore_kernel<true>, grid, FUSED_THREADS,
+                                      ts_smem(true), st, pg, ntiles, per, map);
+            return launch_pdl("merge_tstore_kernel", merge_tstore_kernel<false>, grid, FUSED_THREADS, ts_smem(false),
+                              st, pg, ntiles, per, map);
+        }
         if (var & 32) {
             if (hv) return launch_pdl("merge_async_kernel", merge_async_kernel<true>, grid, FUSED_THREADS,
                                       fused_smem(true, 2), st, pg, ntiles, per);

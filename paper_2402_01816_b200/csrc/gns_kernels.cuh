@@ -11,6 +11,7 @@
 // only through their outputs.
 #pragma once
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace gns {
@@ -112,6 +113,22 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
                  "@!p bra GNS_WAIT_%=;\n}"
                  :: "r"(smem_u32(bar)), "r"(parity) : "memory");
 }
+// TMA tensor store (2-D map over the key array viewed as [n/16][16] doubles,
+// 128-byte swizzle) from shared memory, and its bulk-group completion.
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap *map, const void *src, int c0, int c1)
+{
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];"
+                 :: "l"(map), "r"(smem_u32(src)), "r"(c0), "r"(c1) : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void sts128(void *p, double a, double b)
+{
+    asm volatile("st.shared.v2.f64 [%0], {%1, %2};" :: "r"(smem_u32(p)), "d"(a), "d"(b) : "memory");
+}
+
 // cp.async (LDGSTS) of one 8- or 4-byte element, and the mbarrier arrival that
 // fires when all of this thread's earlier cp.asyncs have landed.
 __device__ __forceinline__ void cp_async_8(void *dst, const void *src)
@@ -1033,6 +1050,147 @@ merge_async_kernel(PipeGeo pg, int ntiles, int per_cta)
         store_segment<HV>(pg.g.ok, pg.g.ov, (long long)(first + i) * MTILE + tid * VT, cnt - d, k, v);
         bar_merge_warps();
     }
+    pdl_trigger();
+}
+
+
+// ------------------------ K2+K3 fused, TMA-store variant (bulk tensor stores)
+// Same load side as merge_fused_kernel<., 2, false>.  After a tile is merged,
+// the consumed input stage becomes the output staging buffer: thread t writes
+// its 16 outputs (= row t of a [256][16] double box) with conflict-free
+// st.shared.v2 into the 128-byte-swizzled layout, and one thread stores the
+// whole 32 KB tile with one cp.async.bulk.tensor (UTMASTG), instead of 32
+// 256-bit STGs per warp that each touch 32 cache lines.  Vals (if any) keep
+// the direct 256-bit stores.
+constexpr int TS_KEY_SLOTS = MTILE + 128;                       // 33,792 B = 33 KiB
+constexpr size_t TS_VAL_BYTES = ((MTILE + 128) * 4 + 1023) / 1024 * 1024;
+constexpr size_t ts_stage_bytes(bool hv) { return TS_KEY_SLOTS * 8 + (hv ? TS_VAL_BYTES : 0); }
+constexpr size_t ts_smem(bool hv) { return 2 * ts_stage_bytes(hv) + 1024; }
+
+template <bool HV>
+__global__ void __launch_bounds__(FUSED_THREADS, 2)
+merge_tstore_kernel(PipeGeo pg, int ntiles, int per_cta, const __grid_constant__ CUtensorMap omap)
+{
+    pdl_wait();
+    extern __shared__ __align__(16) unsigned char smem_raw0[];
+    unsigned char *smem_raw =
+        reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw0) + 1023) & ~uintptr_t(1023));
+    __shared__ __align__(8) uint64_t bars[2];
+    __shared__ PipeMeta meta[2];
+    __shared__ int spl[SPL_RING];
+    __shared__ volatile int spl_tag[SPL_RING];
+    __shared__ volatile int spl_used;
+    auto skb = [&](int st) { return reinterpret_cast<double *>(smem_raw + st * ts_stage_bytes(HV)); };
+    auto svb = [&](int st) {
+        return reinterpret_cast<uint32_t *>(smem_raw + st * ts_stage_bytes(HV) + TS_KEY_SLOTS * sizeof(double));
+    };
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    const int first = blockIdx.x * per_cta;
+    const int last = min(first + per_cta, ntiles);
+    const int m = last - first;
+    if (m <= 0) return;
+    const int nspl = (last < ntiles) ? m + 1 : m;
+    for (int j = tid; j < SPL_RING; j += FUSED_THREADS) spl_tag[j] = -1;
+    __syncthreads();
+    const int init = min(nspl, FUSED_THREADS / 32);
+    if (warp < init) {
+        const int c = warp_corank(pg.g, first + warp, lane);
+        if (lane == 0) {
+            spl[warp] = c;
+            spl_tag[warp] = warp;
+        }
+    }
+    uint64_t policy = policy_evict_first();
+    if (tid == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        fence_mbar_init();
+        spl_used = 0;
+    }
+    __syncthreads();
+
+    if (warp >= NT / 32) {
+        const int sw = warp - NT / 32;
+        const int h = lane >> 4, gl = lane & 15;
+        const unsigned mask = 0xFFFFu << (16 * h);
+        for (int j0 = init + 2 * sw; j0 < nspl; j0 += 2 * SEARCH_WARPS) {
+            const int j = j0 + h;
+            while (j0 + 1 - spl_used >= SPL_RING) { __nanosleep(64); }
+            if (j < nspl) {
+                const int c = group_corank<16>(pg.g, first + j, gl, mask, 16 * h);
+                if (gl == 0) {
+                    spl[j % SPL_RING] = c;
+                    __threadfence_block();
+                    spl_tag[j % SPL_RING] = j;
+                }
+            }
+            __syncwarp();
+        }
+        return;
+    }
+
+    auto get_split = [&](int j) -> int {
+        while (spl_tag[j % SPL_RING] != j) { }
+        return spl[j % SPL_RING];
+    };
+    auto issue = [&](int i) {
+        const int st = i & 1;
+        pipe_issue<HV>(pg, first + i, get_split(i), (i + 1 < nspl) ? get_split(i + 1) : 0, skb(st), svb(st),
+                       &bars[st], &meta[st], policy);
+        spl_used = i;
+    };
+    const long long n = pg.g.n;
+    const long long full_rows = n >> 4;              // rows stored by TMA; a partial last row is stored by hand
+    if (tid == 0) {
+        issue(0);
+        if (m > 1) issue(1);
+    }
+    for (int i = 0; i < m; ++i) {
+        const int st = i & 1;
+        mbar_wait(&bars[st], (uint32_t)((i >> 1) & 1));
+        const PipeMeta mt = meta[st];
+        const int cnt = mt.ca + mt.cb;
+        const int d = min(tid * VT, cnt);
+        double *sk = skb(st);
+        const uint32_t *sv = svb(st);
+        double k[VT];
+        uint32_t v[VT];
+        const int ii = merge_path_smem(sk, mt.offa, mt.ca, mt.bslot, mt.cb, d, Lin());
+        serial_merge<HV>(sk, sv, mt.offa + ii, mt.offa + mt.ca, mt.bslot + d - ii, mt.bslot + mt.cb, k, v, Lin(),
+                         Lin());
+        const long long t = first + i;
+        const long long row = t * (MTILE / 16) + tid;    // global row of this thread's 16 outputs
+        bar_merge_warps();                               // stage st fully read
+        unsigned char *rowp = reinterpret_cast<unsigned char *>(sk) + tid * 128;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) sts128(rowp + ((c ^ (tid & 7)) << 4), k[2 * c], k[2 * c + 1]);
+        fence_proxy_async();
+        if (HV) {
+            const int mv = cnt - d;
+            if (mv >= VT) {
+#pragma unroll
+                for (int x = 0; x < VT; x += 8) st_v8(pg.g.ov + row * 16 + x, &v[x]);
+            } else {
+#pragma unroll
+                for (int x = 0; x < VT; ++x)
+                    if (x < mv) pg.g.ov[row * 16 + x] = v[x];
+            }
+        }
+        if (row == full_rows && d < cnt) {                  // the partial last row (n % 16 != 0)
+#pragma unroll
+            for (int x = 0; x < VT; ++x)
+                if (x < cnt - d) pg.g.ok[row * 16 + x] = k[x];
+        }
+        bar_merge_warps();
+        if (tid == 0) {
+            tma_store_2d(&omap, sk, 0, (int)(t * (MTILE / 16)));
+            bulk_commit();
+            bulk_wait_read0();                            // staging read out -> stage reusable
+            if (i + 2 < m) issue(i + 2);
+        }
+    }
+    if (tid == 0) bulk_wait0();
     pdl_trigger();
 }
 
