@@ -296,7 +296,7 @@ def main():
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded SplitMix64, see DESIGN.md §3)",
         "config": dict(config_json(case, args.frac), parallelism=f"replicas{world}" if world > 1 else "single"),
-        "roofline": {"bound": "hbm", "kernel": "merge pass (merge_fused_kernel: K2 co-rank search + K3 merge in one kernel), avg over "
+        "roofline": {"bound": "hbm", "kernel": "merge pass (merge_tstore_kernel: K2 co-rank search warps + K3 TMA-pipelined merge, one launch per pass), avg over "
                      f"{plan['merge_passes']} passes", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": 2 * n * s,

@@ -111,42 +111,17 @@ gns_status ensure_attrs()
     if (dev >= 64) return fail(GNS_ERR_CUDA, "device ordinal >= 64");
     std::lock_guard<std::mutex> lk(g_attr_mu);
     if (g_attr_done & (1ull << dev)) return GNS_OK;
-    const int k1 = (int)(K1_SMEM_KEYS + sizeof(uint32_t) * K1_SV);
     const int k3 = (int)(K3_SMEM_KEYS + sizeof(uint32_t) * K3_SK);
-    GNS_TRY(check(cudaFuncSetAttribute(tile_sort_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, k1), "attr"));
-    GNS_TRY(check(cudaFuncSetAttribute(tile_sort_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, k1), "attr"));
-    GNS_TRY(check(cudaFuncSetAttribute(merge_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, k3), "attr"));
-    GNS_TRY(check(cudaFuncSetAttribute(merge_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, k3), "attr"));
     GNS_TRY(check(cudaFuncSetAttribute(merge_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, k3), "attr"));
     GNS_TRY(check(cudaFuncSetAttribute(merge_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, k3), "attr"));
-    const int kp1 = (int)(PIPE_STAGES * pipe_stage_bytes(true));
-    const int kp0 = (int)(PIPE_STAGES * pipe_stage_bytes(false));
-    GNS_TRY(check(cudaFuncSetAttribute(merge_pipe_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kp1), "attr"));
-    GNS_TRY(check(cudaFuncSetAttribute(merge_pipe_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kp0), "attr"));
-#define GNS_FUSED_ATTR(HV, S, D)                                                                          \
-    GNS_TRY(check(cudaFuncSetAttribute(merge_fused_kernel<HV, S, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                       (int)fused_smem(HV, S)), "attr"))
-    GNS_FUSED_ATTR(true, 2, false);
-    GNS_FUSED_ATTR(true, 2, true);
-    GNS_FUSED_ATTR(false, 2, false);
-    GNS_FUSED_ATTR(false, 2, true);
-    GNS_FUSED_ATTR(false, 3, false);
-    GNS_FUSED_ATTR(false, 3, true);
-    GNS_TRY(check(cudaFuncSetAttribute(merge_fused_kernel<true, 2, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)fused_smem(true, 2)), "attr"));
-    GNS_TRY(check(cudaFuncSetAttribute(merge_fused_kernel<false, 2, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)fused_smem(false, 2)), "attr"));
-    GNS_TRY(check(cudaFuncSetAttribute(merge_fused_kernel<false, 2, false, false, true>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fused_smem(false, 2)), "attr"));
-    GNS_TRY(check(cudaFuncSetAttribute(merge_async_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)fused_smem(true, 2)), "attr"));
-    GNS_TRY(check(cudaFuncSetAttribute(merge_async_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)fused_smem(false, 2)), "attr"));
     GNS_TRY(check(cudaFuncSetAttribute(merge_tstore_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)ts_smem(true)), "attr"));
     GNS_TRY(check(cudaFuncSetAttribute(merge_tstore_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)ts_smem(false)), "attr"));
-#undef GNS_FUSED_ATTR
+    GNS_TRY(check(cudaFuncSetAttribute(tile_sort2_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)t1_smem(true)), "attr"));
+    GNS_TRY(check(cudaFuncSetAttribute(tile_sort2_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)t1_smem(false)), "attr"));
     GNS_TRY(check(cudaDeviceGetAttribute(&g_num_sms[dev], cudaDevAttrMultiProcessorCount, dev), "sm count"));
     g_attr_done |= (1ull << dev);
     return GNS_OK;
@@ -178,29 +153,23 @@ EncodeTiledFn encode_fn()
     return fn;
 }
 
-// Keys array of n doubles as a 2-D tensor [n/16][16], box [256][16], 128-B swizzle.
-gns_status key_store_map(double *keys, size_t n, CUtensorMap *map)
+// 2-D tensor map for TMA: an array of n keys (f64, 16 per 128-byte row) or
+// vals (u32, 32 per row) viewed as [n / per_row][per_row], box [box_rows][per_row],
+// 128-byte swizzle.  A partial last row is outside the map (handled by hand).
+gns_status row_map(void *base, size_t n, bool f64, int box_rows, CUtensorMap *map)
 {
     EncodeTiledFn fn = encode_fn();
     if (!fn) return fail(GNS_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-    cuuint64_t dims[2] = {16, (cuuint64_t)(n / 16)};
-    cuuint64_t strides[1] = {16 * sizeof(double)};
-    cuuint32_t box[2] = {16, (cuuint32_t)(MTILE / 16)};
+    const int per_row = f64 ? 16 : 32;
+    cuuint64_t dims[2] = {(cuuint64_t)per_row, (cuuint64_t)(n / per_row)};
+    cuuint64_t strides[1] = {128};
+    cuuint32_t box[2] = {(cuuint32_t)per_row, (cuuint32_t)box_rows};
     cuuint32_t estr[2] = {1, 1};
-    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, keys, dims, strides, box, estr,
-                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
-                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    CUresult r = fn(map, f64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, base, dims,
+                    strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(GNS_ERR_CUDA, "cuTensorMapEncodeTiled failed");
     return GNS_OK;
-}
-
-int merge_variant()
-{
-    static const int v = [] {
-        const char *e = std::getenv("GNS_MERGE_VARIANT");
-        return e ? std::atoi(e) : 64;
-    }();
-    return v;
 }
 
 // GNS_PDL=1 in the environment enables programmatic dependent launch (off by
@@ -214,9 +183,6 @@ bool pdl_enabled()
     return on;
 }
 
-// Every kernel is launched with programmatic stream serialization (PDL): it
-// may be scheduled while its predecessor drains and blocks in
-// griddepcontrol.wait until the predecessor's writes are visible.
 template <typename... KArgs, typename... Args>
 gns_status launch_pdl(const char *what, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
                       cudaStream_t st, Args... args)
@@ -234,65 +200,51 @@ gns_status launch_pdl(const char *what, void (*kern)(KArgs...), dim3 grid, dim3 
     return check(cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...), what);
 }
 
+// Row a2 (K1).
 gns_status launch_tile_sort(const double *sk, const uint32_t *sv, double *dk, uint32_t *dv, size_t n,
                             cudaStream_t st)
 {
     if (n == 0) return GNS_OK;
     const unsigned grid = (unsigned)ceil_div(n, TILE);
     const bool hv = sv != nullptr;
-    const size_t smem = K1_SMEM_KEYS + (hv ? sizeof(uint32_t) * K1_SV : 0);
-    if (hv) return launch_pdl("tile_sort_kernel", tile_sort_kernel<true>, grid, NT, smem, st, sk, sv, dk, dv, (long long)n);
-    return launch_pdl("tile_sort_kernel", tile_sort_kernel<false>, grid, NT, smem, st, sk, (const uint32_t *)nullptr,
-                      dk, (uint32_t *)nullptr, (long long)n);
+    CUtensorMap m[4];
+    std::memset(m, 0, sizeof(m));
+    if (n >= (size_t)TILE) {          // full tiles move by TMA tensor copies; a ragged last tile by plain loads
+        GNS_TRY(row_map((void *)sk, n, true, TILE / 16, &m[0]));
+        GNS_TRY(row_map(dk, n, true, TILE / 16, &m[2]));
+        if (hv) {
+            GNS_TRY(row_map((void *)sv, n, false, TILE / 32, &m[1]));
+            GNS_TRY(row_map(dv, n, false, TILE / 32, &m[3]));
+        }
+    }
+    if (hv)
+        return launch_pdl("tile_sort2_kernel", tile_sort2_kernel<true>, grid, NT1, t1_smem(true), st, sk, sv, dk, dv,
+                          (long long)n, m[0], m[1], m[2], m[3]);
+    return launch_pdl("tile_sort2_kernel", tile_sort2_kernel<false>, grid, NT1, t1_smem(false), st, sk,
+                      (const uint32_t *)nullptr, dk, (uint32_t *)nullptr, (long long)n, m[0], m[1], m[2], m[3]);
 }
 
+// Rows a3+a4 (fused K2+K3, persistent TMA pipeline) or, in place, a6 (K2 +
+// dependency ranges + K4 with the ticket/flag protocol).
 gns_status launch_merge(const MergeGeo &g, const double *lim_a, const double *lim_b, int *corank, int2 *deps,
                         unsigned *flags, bool inplace, cudaStream_t st)
 {
     const int ntiles = (int)ceil_div((size_t)g.n, MTILE);
     const bool hv = g.av != nullptr;
     if (!inplace) {
-        // K2+K3 fused: partition inside the persistent pipelined merge kernel
         PipeGeo pg;
         pg.g = g;
         pg.a_lim = lim_a;
         pg.b_lim = lim_b;
-        // GNS_MERGE_VARIANT (A/B experiments; default 64 = TMA tensor-store kernel):
-        // 0 = TMA-load/STG pipeline, bit0 = decoupled warps, bit1 = 3 stages (key-only),
-        // bit2 = precomputed splits, bit3 = dual chains, bit4 = copy-only probe,
-        // bit5 = cp.async swizzled loads, bit6 = TMA tensor stores
-        const int var = merge_variant();
-        const bool dec = var & 1;
-        const int S = (!hv && (var & 2)) ? 3 : 2;
-        const size_t psmem = fused_smem(hv, S);
         const int ctas = std::min(ntiles, 2 * num_sms());
         const int per = (int)ceil_div(ntiles, ctas);
         const int grid = (int)ceil_div(ntiles, per);
-        auto kern = (var & 16) ? merge_fused_kernel<false, 2, false, false, true> : (var & 8) ? (hv ? merge_fused_kernel<true, 2, false, true> : merge_fused_kernel<false, 2, false, true>)
-                  : hv ? (dec ? merge_fused_kernel<true, 2, true> : merge_fused_kernel<true, 2, false>)
-                       : (S == 3 ? (dec ? merge_fused_kernel<false, 3, true> : merge_fused_kernel<false, 3, false>)
-                                 : (dec ? merge_fused_kernel<false, 2, true> : merge_fused_kernel<false, 2, false>));
-        if (var & 64) {
-            CUtensorMap map;
-            GNS_TRY(key_store_map(g.ok, (size_t)g.n, &map));
-            if (hv) return launch_pdl("merge_tstore_kernel", merge_tstore_kernel<true>, grid, FUSED_THREADS,
-                                      ts_smem(true), st, pg, ntiles, per, map);
-            return launch_pdl("merge_tstore_kernel", merge_tstore_kernel<false>, grid, FUSED_THREADS, ts_smem(false),
-                              st, pg, ntiles, per, map);
-        }
-        if (var & 32) {
-            if (hv) return launch_pdl("merge_async_kernel", merge_async_kernel<true>, grid, FUSED_THREADS,
-                                      fused_smem(true, 2), st, pg, ntiles, per);
-            return launch_pdl("merge_async_kernel", merge_async_kernel<false>, grid, FUSED_THREADS, fused_smem(false, 2),
-                              st, pg, ntiles, per);
-        }
-        const int *pre = nullptr;
-        if (var & 4) {   // A/B: precomputed splits from the separate partition kernel
-            GNS_TRY(launch_pdl("partition_kernel", partition_kernel, (unsigned)ceil_div((size_t)ntiles * 32, 256), 256,
-                               0, st, g, ntiles, corank));
-            pre = corank;
-        }
-        return launch_pdl("merge_fused_kernel", kern, grid, FUSED_THREADS, psmem, st, pg, ntiles, per, pre);
+        CUtensorMap map;
+        GNS_TRY(row_map(g.ok, (size_t)g.n, true, MTILE / 16, &map));
+        if (hv) return launch_pdl("merge_tstore_kernel", merge_tstore_kernel<true>, grid, FUSED_THREADS,
+                                  ts_smem(true), st, pg, ntiles, per, map);
+        return launch_pdl("merge_tstore_kernel", merge_tstore_kernel<false>, grid, FUSED_THREADS, ts_smem(false), st,
+                          pg, ntiles, per, map);
     }
     GNS_TRY(launch_pdl("partition_kernel", partition_kernel, (unsigned)ceil_div((size_t)ntiles * 32, 256), 256, 0, st,
                        g, ntiles, corank));

@@ -1,11 +1,12 @@
 // gns_kernels.cuh — sm_100a device code of the stable f64 mergesort hot path.
 //
 // Kernels (PAPER.md line cites in each):
-//   K1 tile_sort_kernel      (row a2) stable sort of one TILE-element tile per CTA
-//   K2 partition_kernel      (row a3) stable co-rank (merge-path) split per output tile
-//   K3 merge_kernel<.,false> (row a4) one merge level, src -> dst ping-pong
-//   K4 merge_kernel<.,true>  (row a6) ordered in-place top merge of the 0.5 mode
-//      inplace_deps_kernel   (row a6) which earlier tiles each K4 tile must wait for
+//   K1    tile_sort2_kernel    (row a2) stable sort of one 4096-key tile per CTA
+//   K2+K3 merge_tstore_kernel  (rows a3+a4) one merge level, src -> dst ping-pong,
+//                              co-rank search warps fused in
+//   K2    partition_kernel     (row a3) stable co-rank split per output tile (for K4)
+//   K4    merge_kernel<.,true> (row a6) ordered in-place top merge of the 0.5 mode
+//         inplace_deps_kernel  (row a6) which earlier tiles each K4 tile must wait for
 //
 // No code here is shared with oracle/ (the CPU oracle); the two are compared
 // only through their outputs.
@@ -31,9 +32,6 @@ constexpr int MTILE = NT * VT;     // K3/K4 output tile = 4096 elements
 // Both are bijections within each aligned row, so no extra space is needed.
 __device__ __forceinline__ int swk(int e) { return e ^ ((e >> 4) & 15); }
 __device__ __forceinline__ int swv(int e) { return e ^ ((e >> 5) & 31); }
-constexpr int K1_SK = TILE + 32;      // + spare slots for one-past-end reads
-constexpr int K1_SV = TILE + 32;
-constexpr size_t K1_SMEM_KEYS = sizeof(double) * K1_SK;
 constexpr size_t K3_SK = MTILE + 32;
 constexpr size_t K3_SMEM_KEYS = sizeof(double) * K3_SK;
 
@@ -120,6 +118,25 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap *map, const void 
     asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];"
                  :: "l"(map), "r"(smem_u32(src)), "r"(c0), "r"(c1) : "memory");
 }
+__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, int c0, int c1, uint64_t *bar)
+{
+    asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+                 :: "r"(smem_u32(dst)), "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void lds128(const void *p, double &a, double &b)
+{
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(a), "=d"(b) : "r"(smem_u32(p)));
+}
+__device__ __forceinline__ void lds128u(const void *p, uint32_t *u)
+{
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3])
+                 : "r"(smem_u32(p)));
+}
+__device__ __forceinline__ void sts128u(void *p, const uint32_t *u)
+{
+    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" :: "r"(smem_u32(p)), "r"(u[0]), "r"(u[1]), "r"(u[2]),
+                 "r"(u[3]) : "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
@@ -127,21 +144,6 @@ __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.
 __device__ __forceinline__ void sts128(void *p, double a, double b)
 {
     asm volatile("st.shared.v2.f64 [%0], {%1, %2};" :: "r"(smem_u32(p)), "d"(a), "d"(b) : "memory");
-}
-
-// cp.async (LDGSTS) of one 8- or 4-byte element, and the mbarrier arrival that
-// fires when all of this thread's earlier cp.asyncs have landed.
-__device__ __forceinline__ void cp_async_8(void *dst, const void *src)
-{
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" :: "r"(smem_u32(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_4(void *dst, const void *src)
-{
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" :: "r"(smem_u32(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_mbar_arrive(uint64_t *bar)
-{
-    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" :: "r"(smem_u32(bar)) : "memory");
 }
 
 // 1-D bulk copy global -> shared, completion counted on `bar` (16-byte aligned
@@ -222,141 +224,6 @@ __device__ __forceinline__ void serial_merge(const double *sk, const uint32_t *s
         const double kn = sk[ik(nxt)];
         if (p) kb = kn; else ka = kn;
     }
-}
-
-// Two independent merge paths / serial merges per thread, interleaved so the
-// two dependency chains overlap (ILP 2): the thread's VT outputs are split into
-// halves starting at diagonals d and d + VT/2.
-template <class IX>
-__device__ __forceinline__ void merge_path_smem2(const double *s, int a0, int na, int b0, int nb, int d1, int d2,
-                                                 IX ix, int &r1, int &r2)
-{
-    int lo1 = max(0, d1 - nb), hi1 = min(d1, na);
-    int lo2 = max(0, d2 - nb), hi2 = min(d2, na);
-    while (lo1 < hi1 || lo2 < hi2) {
-        const int m1 = (lo1 + hi1) >> 1, m2 = (lo2 + hi2) >> 1;
-        const bool a1 = lo1 < hi1, a2 = lo2 < hi2;
-        const double x1 = s[ix(a0 + m1)], y1 = s[ix(b0 + max(d1 - 1 - m1, 0))];
-        const double x2 = s[ix(a0 + m2)], y2 = s[ix(b0 + max(d2 - 1 - m2, 0))];
-        const bool p1 = x1 <= y1, p2 = x2 <= y2;
-        if (a1) { if (p1) lo1 = m1 + 1; else hi1 = m1; }
-        if (a2) { if (p2) lo2 = m2 + 1; else hi2 = m2; }
-    }
-    r1 = lo1;
-    r2 = lo2;
-}
-
-template <bool HV, class IK, class IV>
-__device__ __forceinline__ void serial_merge2(const double *sk, const uint32_t *sv, int ai, int bi, int ci, int di,
-                                              int aend, int bend, double (&k)[VT], uint32_t (&v)[VT], IK ik, IV iv)
-{
-    // chain 1 fills k[0 .. VT/2), chain 2 fills k[VT/2 .. VT); both merge the
-    // same runs A = [.., aend), B = [.., bend) from different starting points.
-    constexpr int H = VT / 2;
-    double ka = sk[ik(ai)], kb = sk[ik(bi)];
-    double kc = sk[ik(ci)], kd = sk[ik(di)];
-#pragma unroll
-    for (int x = 0; x < H; ++x) {
-        const bool p = (bi < bend) && ((ai >= aend) || (kb < ka));
-        const bool q = (di < bend) && ((ci >= aend) || (kd < kc));
-        k[x] = p ? kb : ka;
-        k[H + x] = q ? kd : kc;
-        const int s1 = p ? bi : ai;
-        const int s2 = q ? di : ci;
-        if (HV) {
-            v[x] = sv[iv(s1)];
-            v[H + x] = sv[iv(s2)];
-        }
-        const int n1 = s1 + 1, n2 = s2 + 1;
-        if (p) bi = n1; else ai = n1;
-        if (q) di = n2; else ci = n2;
-        const double kn1 = sk[ik(n1)];
-        const double kn2 = sk[ik(n2)];
-        if (p) kb = kn1; else ka = kn1;
-        if (q) kd = kn2; else kc = kn2;
-    }
-}
-
-// --------------------------------------------------------------- K1 tile sort
-// Each thread loads VT consecutive keys (256-bit loads), sorts them with an
-// odd-even transposition network (compare-exchange only of adjacent items and
-// only on strict `>`: stable), then log2(NT) rounds of shared-memory merge-path
-// merges double the sorted run length from VT to TILE.  Each round is one
-// "read-scan with comparisons and one write-scan" of PAPER.md:150, done on
-// chip.  The tail tile is padded with +inf keys placed AFTER every real key, so
-// stability puts real keys (including real +inf) first; pads are never stored.
-template <bool HV>
-__global__ void __launch_bounds__(NT, 3)
-tile_sort_kernel(const double *src_k, const uint32_t *src_v, double *dst_k, uint32_t *dst_v, long long n)
-{
-    pdl_wait();
-    pdl_trigger();
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    double *sk = reinterpret_cast<double *>(smem_raw);
-    uint32_t *sv = reinterpret_cast<uint32_t *>(smem_raw + K1_SMEM_KEYS);
-
-    const long long base = (long long)blockIdx.x * TILE;
-    const int cnt = (int)min((long long)TILE, n - base);
-    const int tid = threadIdx.x;
-    const int e0 = tid * VT;
-
-    double k[VT];
-    uint32_t v[VT];
-    if (e0 + VT <= cnt) {
-#pragma unroll
-        for (int x = 0; x < VT; x += 4) ld_v4(src_k + base + e0 + x, k[x], k[x + 1], k[x + 2], k[x + 3]);
-        if (HV) {
-#pragma unroll
-            for (int x = 0; x < VT; x += 8) ld_v8(src_v + base + e0 + x, &v[x]);
-        }
-    } else {
-#pragma unroll
-        for (int x = 0; x < VT; ++x) {
-            const bool ok = e0 + x < cnt;
-            k[x] = ok ? src_k[base + e0 + x] : __longlong_as_double(0x7FF0000000000000LL);
-            if (HV) v[x] = ok ? src_v[base + e0 + x] : 0u;
-        }
-    }
-
-    // in-register stable transposition sort
-#pragma unroll
-    for (int r = 0; r < VT; ++r) {
-#pragma unroll
-        for (int i = r & 1; i + 1 < VT; i += 2) {
-            const bool p = k[i + 1] < k[i];
-            const double lo = p ? k[i + 1] : k[i];
-            const double hi = p ? k[i] : k[i + 1];
-            k[i] = lo;
-            k[i + 1] = hi;
-            if (HV) {
-                const uint32_t vl = p ? v[i + 1] : v[i];
-                const uint32_t vh = p ? v[i] : v[i + 1];
-                v[i] = vl;
-                v[i + 1] = vh;
-            }
-        }
-    }
-
-    // shared-memory merge rounds: runs of VT*coop/2 -> VT*coop
-#pragma unroll 1
-    for (int coop = 2; coop <= NT; coop <<= 1) {
-#pragma unroll
-        for (int x = 0; x < VT; ++x) {
-            sk[swk(e0 + x)] = k[x];
-            if (HV) sv[swv(e0 + x)] = v[x];
-        }
-        __syncthreads();
-        const int local = tid & (coop - 1);
-        const int a0 = (tid - local) * VT;
-        const int run = (coop >> 1) * VT;
-        const int b0 = a0 + run;
-        const int d = local * VT;
-        const int i = merge_path_smem(sk, a0, run, b0, run, d, SwK());
-        serial_merge<HV>(sk, sv, a0 + i, b0, b0 + d - i, b0 + run, k, v, SwK(), SwV());
-        __syncthreads();
-    }
-
-    store_segment<HV>(dst_k, dst_v, base + e0, cnt - e0, k, v);
 }
 
 // ----------------------------------------------------------- merge geometry
@@ -715,347 +582,25 @@ __device__ __forceinline__ void pipe_issue(const PipeGeo &pg, int t, int i0, int
 
 struct Lin { __device__ __forceinline__ int operator()(int e) const { return e; } };
 
-template <bool HV>
-__global__ void __launch_bounds__(NT, HV ? 2 : 3)
-merge_pipe_kernel(PipeGeo pg, const int *__restrict__ corank, int ntiles)
-{
-    pdl_wait();
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    __shared__ __align__(8) uint64_t bars[PIPE_STAGES];
-    __shared__ PipeMeta meta[PIPE_STAGES];
-    auto skb = [&](int st) { return reinterpret_cast<double *>(smem_raw + st * pipe_stage_bytes(HV)); };
-    auto svb = [&](int st) {
-        return reinterpret_cast<uint32_t *>(smem_raw + st * pipe_stage_bytes(HV) + PIPE_SLOTS * sizeof(double));
-    };
-    const int tid = threadIdx.x;
-    const int G = gridDim.x;
-    uint64_t policy = 0;
-    if (tid == 0) {
-        policy = policy_evict_first();
-        for (int st = 0; st < PIPE_STAGES; ++st) mbar_init(&bars[st], 1);
-        fence_mbar_init();
-    }
-    __syncthreads();
-    int t = blockIdx.x;
-    if (tid == 0 && t < ntiles)
-        pipe_issue<HV>(pg, t, corank[t], t + 1 < ntiles ? corank[t + 1] : 0, skb(0), svb(0), &bars[0], &meta[0], policy);
-    __syncthreads();
-    for (int i = 0; t < ntiles; ++i, t += G) {
-        const int st = i & 1;
-        const int tn = t + G;
-        if (tid == 0 && tn < ntiles)
-            pipe_issue<HV>(pg, tn, corank[tn], tn + 1 < ntiles ? corank[tn + 1] : 0, skb(st ^ 1), svb(st ^ 1),
-                           &bars[st ^ 1], &meta[st ^ 1], policy);
-        mbar_wait(&bars[st], (uint32_t)((i >> 1) & 1));
-        const PipeMeta m = meta[st];
-        const int cnt = m.ca + m.cb;
-        const int d = min(tid * VT, cnt);
-        const double *sk = skb(st);
-        const uint32_t *sv = svb(st);
-        const int ii = merge_path_smem(sk, m.offa, m.ca, m.bslot, m.cb, d, Lin());
-        double k[VT];
-        uint32_t v[VT];
-        serial_merge<HV>(sk, sv, m.offa + ii, m.offa + m.ca, m.bslot + d - ii, m.bslot + m.cb, k, v, Lin(), Lin());
-        store_segment<HV>(pg.g.ok, pg.g.ov, (long long)t * MTILE + tid * VT, cnt - d, k, v);
-        __syncthreads();   // stage st fully consumed (and next meta visible) before it is refilled
-    }
-    pdl_trigger();         // successor may launch while the last tiles drain
-}
-
-
-// ------------------------------------- K2+K3 fused: the production merge pass
-// Same pipeline as merge_pipe_kernel, but the co-rank partition (row a3) is
-// done inside the kernel: CTA c owns the contiguous tiles [first, last), so
-// it needs the splits at first..last only (tile t ends where t+1 starts).
-// Warps 0-7 merge; warp 8 is a dedicated search warp that runs ahead
-// computing splits into a shared ring (32-ary warp searches, ~5 dependent
-// rounds each) while the merge warps work, so no partition kernel, no
-// co-rank array in HBM and no extra launch per pass.  At kernel start all 9
-// warps compute the first splits in parallel.
+// ------------------------------- shared pieces of the fused merge kernels
 constexpr int SEARCH_WARPS = 2;
 constexpr int FUSED_THREADS = NT + 32 * SEARCH_WARPS;
 constexpr int SPL_RING = 64;
+
 __device__ __forceinline__ void bar_merge_warps() { asm volatile("bar.sync 1, %0;" :: "n"(NT) : "memory"); }
-constexpr size_t fused_smem(bool hv, int stages) { return stages * pipe_stage_bytes(hv); }
 
-// Two consumption schemes (A/B-selectable at launch):
-//  DECOUPLED = false: the 8 merge warps meet at a named barrier after every
-//    tile; thread 0 refills the freed stage with tile i + S - 1 at the start
-//    of iteration i.
-//  DECOUPLED = true: no CTA barrier; each warp waits on the stage's "full"
-//    mbarrier, merges its 512 outputs, and bumps the stage's consumed counter;
-//    the last reader refills the stage with tile i + S.
-template <bool HV, int S, bool DECOUPLED, bool DUAL = false, bool COPY_ONLY = false>
-__global__ void __launch_bounds__(FUSED_THREADS, 2)
-merge_fused_kernel(PipeGeo pg, int ntiles, int per_cta, const int *__restrict__ pre)
-{
-    pdl_wait();
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    __shared__ __align__(8) uint64_t bars[S];
-    __shared__ PipeMeta meta[S];
-    __shared__ int consumed[S];
-    __shared__ int spl[SPL_RING];
-    __shared__ volatile int spl_tag[SPL_RING];   // spl_tag[j % R] == j  <=>  split j is in spl[j % R]
-    __shared__ volatile int spl_used;            // splits [0, spl_used) may be overwritten
-    auto skb = [&](int st) { return reinterpret_cast<double *>(smem_raw + st * pipe_stage_bytes(HV)); };
-    auto svb = [&](int st) {
-        return reinterpret_cast<uint32_t *>(smem_raw + st * pipe_stage_bytes(HV) + PIPE_SLOTS * sizeof(double));
-    };
-    const int tid = threadIdx.x;
-    const int warp = tid >> 5, lane = tid & 31;
-    const int first = blockIdx.x * per_cta;
-    const int last = min(first + per_cta, ntiles);
-    const int m = last - first;            // tiles of this CTA
-    if (m <= 0) return;
-    const int nspl = (last < ntiles) ? m + 1 : m;   // splits j = 0..nspl-1 (tile first+j's start)
-    for (int j = tid; j < SPL_RING; j += FUSED_THREADS) spl_tag[j] = -1;
-    __syncthreads();
-    // phase 0: the first splits, one per warp, full-warp (lowest latency) searches
-    // (pre != nullptr: splits were precomputed by partition_kernel; A/B only)
-    const int init = pre ? nspl : min(nspl, FUSED_THREADS / 32);
-    if (!pre && warp < init) {
-        const int c = warp_corank(pg.g, first + warp, lane);
-        if (lane == 0) {
-            spl[warp] = c;
-            spl_tag[warp] = warp;
-        }
-    }
-    uint64_t policy = policy_evict_first();
-    if (tid == 0) {
-        for (int st = 0; st < S; ++st) {
-            mbar_init(&bars[st], 1);
-            consumed[st] = 0;
-        }
-        fence_mbar_init();
-        spl_used = 0;
-    }
-    __syncthreads();
-
-    if (warp >= NT / 32) {
-        // search warps: two concurrent 16-lane searches per warp, splits
-        // init + 2*sw + h, step 2*SEARCH_WARPS; at most SPL_RING ahead.
-        const int sw = warp - NT / 32;
-        const int h = lane >> 4, gl = lane & 15;
-        const unsigned mask = 0xFFFFu << (16 * h);
-        for (int j0 = init + 2 * sw; j0 < nspl; j0 += 2 * SEARCH_WARPS) {
-            const int j = j0 + h;
-            while (j0 + 1 - spl_used >= SPL_RING) { __nanosleep(64); }
-            if (j < nspl) {
-                const int c = group_corank<16>(pg.g, first + j, gl, mask, 16 * h);
-                if (gl == 0) {
-                    spl[j % SPL_RING] = c;
-                    __threadfence_block();
-                    spl_tag[j % SPL_RING] = j;
-                }
-            }
-            __syncwarp();
-        }
-        return;
-    }
-
-    // merge warps
-    auto get_split = [&](int j) -> int {
-        if (pre) return pre[first + j];
-        while (spl_tag[j % SPL_RING] != j) { }
-        return spl[j % SPL_RING];
-    };
-    auto issue = [&](int i) {      // tile first+i into stage i % S
-        const int st = i % S;
-        pipe_issue<HV>(pg, first + i, get_split(i), (i + 1 < nspl) ? get_split(i + 1) : 0, skb(st), svb(st),
-                       &bars[st], &meta[st], policy);
-        spl_used = i;
-    };
-    if (tid == 0)
-        for (int i = 0; i < (DECOUPLED ? S : S - 1) && i < m; ++i) issue(i);
-    if (!DECOUPLED) bar_merge_warps();
-    for (int i = 0; i < m; ++i) {
-        const int st = i % S;
-        if (!DECOUPLED && tid == 0 && i + S - 1 < m) issue(i + S - 1);
-        mbar_wait(&bars[st], (uint32_t)((i / S) & 1));
-        const PipeMeta mt = meta[st];
-        const int cnt = mt.ca + mt.cb;
-        const int d = min(tid * VT, cnt);
-        const double *sk = skb(st);
-        const uint32_t *sv = svb(st);
-        double k[VT];
-        uint32_t v[VT];
-        if (COPY_ONLY) {   // A/B timing probe only: no merge, wrong output
-#pragma unroll
-            for (int x = 0; x < VT; ++x) {
-                k[x] = sk[min(d + x, MTILE)];
-                if (HV) v[x] = sv[min(d + x, MTILE)];
-            }
-        } else if (DUAL) {
-            const int d2 = min(tid * VT + VT / 2, cnt);
-            int i1, i2;
-            merge_path_smem2(sk, mt.offa, mt.ca, mt.bslot, mt.cb, d, d2, Lin(), i1, i2);
-            serial_merge2<HV>(sk, sv, mt.offa + i1, mt.bslot + d - i1, mt.offa + i2, mt.bslot + d2 - i2,
-                              mt.offa + mt.ca, mt.bslot + mt.cb, k, v, Lin(), Lin());
-        } else {
-            const int ii = merge_path_smem(sk, mt.offa, mt.ca, mt.bslot, mt.cb, d, Lin());
-            serial_merge<HV>(sk, sv, mt.offa + ii, mt.offa + mt.ca, mt.bslot + d - ii, mt.bslot + mt.cb, k, v, Lin(),
-                             Lin());
-        }
-        if (DECOUPLED) {
-            __syncwarp();
-            if (lane == 0) {
-                __threadfence_block();
-                const int old = atomicAdd(&consumed[st], 1);
-                if (old == NT / 32 - 1) {
-                    consumed[st] = 0;
-                    if (i + S < m) issue(i + S);
-                }
-            }
-        }
-        store_segment<HV>(pg.g.ok, pg.g.ov, (long long)(first + i) * MTILE + tid * VT, cnt - d, k, v);
-        if (!DECOUPLED) bar_merge_warps();
-    }
-    pdl_trigger();
-}
-
-
-// ------------------------- K2+K3 fused, cp.async variant (swizzled stage layout)
-// Like merge_fused_kernel<., 2, false>, but the stage is filled by all 256
-// merge threads with per-element cp.async (LDGSTS) into the XOR-swizzled
-// layout (slot swk(e) / swv(e)), so the merge-path and serial-merge reads
-// (lanes ~VT/2 apart in each run) are bank-conflict free; completion is
-// tracked by cp.async.mbarrier.arrive on the stage's mbarrier (count = 256).
-struct TileIn {
-    int ca, cb;
-    const double *Ak, *Bk;
-    const uint32_t *Av, *Bv;
-};
-
-__device__ __forceinline__ TileIn tile_inputs(const MergeGeo &g, int t, int i0, int i1next)
-{
-    const TileSpan s = tile_span(g, t);
-    const int cnt = s.k1 - s.k0;
-    int i1 = (s.k1 == s.na + s.nb) ? s.na : i1next;
-    i1 = min(min(max(max(i1, i0), s.k1 - s.nb), i0 + cnt), s.na);
-    const int j0 = s.k0 - i0;
-    TileIn r;
-    r.ca = i1 - i0;
-    r.cb = cnt - r.ca;
-    r.Ak = g.ak + s.pbase + i0;
-    r.Bk = g.bk + s.pbase + j0;
-    r.Av = g.av ? g.av + s.pbase + i0 : nullptr;
-    r.Bv = g.bv ? g.bv + s.pbase + j0 : nullptr;
-    return r;
-}
-
-template <bool HV>
-__global__ void __launch_bounds__(FUSED_THREADS, 2)
-merge_async_kernel(PipeGeo pg, int ntiles, int per_cta)
-{
-    pdl_wait();
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    __shared__ __align__(8) uint64_t bars[2];
-    __shared__ TileIn tin[3];
-    __shared__ int spl[SPL_RING];
-    __shared__ volatile int spl_tag[SPL_RING];
-    __shared__ volatile int spl_used;
-    auto skb = [&](int st) { return reinterpret_cast<double *>(smem_raw + st * pipe_stage_bytes(HV)); };
-    auto svb = [&](int st) {
-        return reinterpret_cast<uint32_t *>(smem_raw + st * pipe_stage_bytes(HV) + PIPE_SLOTS * sizeof(double));
-    };
-    const int tid = threadIdx.x;
-    const int warp = tid >> 5, lane = tid & 31;
-    const int first = blockIdx.x * per_cta;
-    const int last = min(first + per_cta, ntiles);
-    const int m = last - first;
-    if (m <= 0) return;
-    const int nspl = (last < ntiles) ? m + 1 : m;
-    for (int j = tid; j < SPL_RING; j += FUSED_THREADS) spl_tag[j] = -1;
-    __syncthreads();
-    const int init = min(nspl, FUSED_THREADS / 32);
-    if (warp < init) {
-        const int c = warp_corank(pg.g, first + warp, lane);
-        if (lane == 0) {
-            spl[warp] = c;
-            spl_tag[warp] = warp;
-        }
-    }
-    if (tid == 0) {
-        mbar_init(&bars[0], NT);
-        mbar_init(&bars[1], NT);
-        fence_mbar_init();
-        spl_used = 0;
-    }
-    __syncthreads();
-
-    if (warp >= NT / 32) {
-        const int sw = warp - NT / 32;
-        const int h = lane >> 4, gl = lane & 15;
-        const unsigned mask = 0xFFFFu << (16 * h);
-        for (int j0 = init + 2 * sw; j0 < nspl; j0 += 2 * SEARCH_WARPS) {
-            const int j = j0 + h;
-            while (j0 + 1 - spl_used >= SPL_RING) { __nanosleep(64); }
-            if (j < nspl) {
-                const int c = group_corank<16>(pg.g, first + j, gl, mask, 16 * h);
-                if (gl == 0) {
-                    spl[j % SPL_RING] = c;
-                    __threadfence_block();
-                    spl_tag[j % SPL_RING] = j;
-                }
-            }
-            __syncwarp();
-        }
-        return;
-    }
-
-    auto get_split = [&](int j) -> int {
-        while (spl_tag[j % SPL_RING] != j) { }
-        return spl[j % SPL_RING];
-    };
-    auto plan = [&](int i) {       // thread 0: inputs of tile first+i -> tin[i % 3]
-        tin[i % 3] = tile_inputs(pg.g, first + i, get_split(i), (i + 1 < nspl) ? get_split(i + 1) : 0);
-        spl_used = i;
-    };
-    auto load = [&](int i) {       // all merge threads: cp.async tile first+i into stage i & 1
-        const TileIn ti = tin[i % 3];
-        const int cnt = ti.ca + ti.cb;
-        double *sk = skb(i & 1);
-        uint32_t *sv = svb(i & 1);
-#pragma unroll
-        for (int r = 0; r < VT; ++r) {
-            const int e = tid + r * NT;
-            if (e < cnt) {
-                const bool fa = e < ti.ca;
-                cp_async_8(sk + swk(e), fa ? ti.Ak + e : ti.Bk + (e - ti.ca));
-                if (HV) cp_async_4(sv + swv(e), fa ? ti.Av + e : ti.Bv + (e - ti.ca));
-            }
-        }
-        cp_async_mbar_arrive(&bars[i & 1]);
-    };
-    if (tid == 0) {
-        plan(0);
-        if (m > 1) plan(1);
-    }
-    bar_merge_warps();
-    load(0);
-    for (int i = 0; i < m; ++i) {
-        const int st = i & 1;
-        if (i + 1 < m) load(i + 1);
-        if (tid == 0 && i + 2 < m) plan(i + 2);
-        mbar_wait(&bars[st], (uint32_t)((i >> 1) & 1));
-        const TileIn ti = tin[i % 3];
-        const int cnt = ti.ca + ti.cb;
-        const int d = min(tid * VT, cnt);
-        const double *sk = skb(st);
-        const uint32_t *sv = svb(st);
-        double k[VT];
-        uint32_t v[VT];
-        const int ii = merge_path_smem(sk, 0, ti.ca, ti.ca, ti.cb, d, SwK());
-        serial_merge<HV>(sk, sv, ii, ti.ca, ti.ca + d - ii, cnt, k, v, SwK(), SwV());
-        store_segment<HV>(pg.g.ok, pg.g.ov, (long long)(first + i) * MTILE + tid * VT, cnt - d, k, v);
-        bar_merge_warps();
-    }
-    pdl_trigger();
-}
-
-
-// ------------------------ K2+K3 fused, TMA-store variant (bulk tensor stores)
-// Same load side as merge_fused_kernel<., 2, false>.  After a tile is merged,
+// ---------------------------- K2+K3 fused: the production merge pass (row a3+a4)
+// A persistent grid (2 CTAs per SM); CTA c owns the contiguous output tiles
+// [first, last) of 4096 keys, so it needs the co-rank splits at first..last
+// only (tile t ends where t+1 starts).  Warps 8-9 are search warps: they run
+// ahead computing the splits (two concurrent 16-lane 17-ary warp searches per
+// warp, predicate A[m] <= B[d-1-m]) into a shared ring; at kernel start all 10
+// warps compute the first splits in parallel.  Warps 0-7 merge.  Thread 0
+// issues TMA bulk copies (cp.async.bulk, UBLKCP) of exactly A[i0:i1) and
+// B[j0:j1) into a double-buffered stage; keys and vals of global element g
+// share one shared slot (offset g mod 4) so every copy is 16-byte aligned.
+// Each thread merges 16 outputs (merge path + serial merge, left wins ties).
+// After a tile is merged,
 // the consumed input stage becomes the output staging buffer: thread t writes
 // its 16 outputs (= row t of a [256][16] double box) with conflict-free
 // st.shared.v2 into the 128-byte-swizzled layout, and one thread stores the
@@ -1073,8 +618,9 @@ merge_tstore_kernel(PipeGeo pg, int ntiles, int per_cta, const __grid_constant__
 {
     pdl_wait();
     extern __shared__ __align__(16) unsigned char smem_raw0[];
-    unsigned char *smem_raw =
-        reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw0) + 1023) & ~uintptr_t(1023));
+    // 1 KiB alignment for the swizzled TMA boxes; pointer arithmetic (not an
+    // integer round trip) keeps the shared address space visible to ptxas.
+    unsigned char *smem_raw = smem_raw0 + ((1024u - (smem_u32(smem_raw0) & 1023u)) & 1023u);
     __shared__ __align__(8) uint64_t bars[2];
     __shared__ PipeMeta meta[2];
     __shared__ int spl[SPL_RING];
@@ -1191,6 +737,177 @@ merge_tstore_kernel(PipeGeo pg, int ntiles, int per_cta, const __grid_constant__
         }
     }
     if (tid == 0) bulk_wait0();
+    pdl_trigger();
+}
+
+
+// ------------------------------------------------- K1 v2: TMA-fed tile sort
+// 128 threads x 32 keys (TILE = 4096).  The tile arrives by one TMA tensor
+// load (2-D maps: keys [n/16][16] f64, vals [n/32][32] u32, 128-byte swizzle)
+// and leaves by one TMA tensor store; the blocked register<->smem transfers
+// use 16-byte accesses in the swizzled layout.  In registers: two stable
+// odd-even transposition sorts of 16; then log2(4096/16) = 8 shared-memory
+// merge rounds (round 0 merges each thread's own two halves, no search).  With
+// 32 outputs per thread the merge-path searches per key are halved vs VT=16.
+constexpr int NT1 = 128;
+constexpr int VT1 = 32;
+static_assert(NT1 * VT1 == TILE, "tile geometry");
+constexpr size_t T1_KEY_BYTES = TILE * 8 + 1024;
+constexpr size_t T1_VAL_BYTES = TILE * 4 + 1024;
+constexpr size_t t1_smem(bool hv) { return T1_KEY_BYTES + (hv ? T1_VAL_BYTES : 0) + 1024; }
+
+// merge-round layouts (blocked spill e = 32t + x and merge reads conflict-light)
+__device__ __forceinline__ int swm(int e) { return e ^ ((e >> 5) & 15); }
+__device__ __forceinline__ int swmv(int e) { return e ^ ((e >> 5) & 31); }
+struct SwM { __device__ __forceinline__ int operator()(int e) const { return swm(e); } };
+struct SwMV { __device__ __forceinline__ int operator()(int e) const { return swmv(e); } };
+// TMA 128-byte swizzle layouts (16-byte chunk c of row r stored at chunk c ^ (r & 7))
+__device__ __forceinline__ int tk_slot(int e)     // doubles, 16 per row
+{
+    const int r = e >> 4;
+    return (r << 4) | ((((e >> 1) & 7) ^ (r & 7)) << 1) | (e & 1);
+}
+__device__ __forceinline__ int tv_slot(int e)     // u32, 32 per row
+{
+    const int r = e >> 5;
+    return (r << 5) | ((((e >> 2) & 7) ^ (r & 7)) << 2) | (e & 3);
+}
+
+template <int O, bool HV>
+__device__ __forceinline__ void transpose_sort16(double (&k)[VT1], uint32_t (&v)[VT1])
+{
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+#pragma unroll
+        for (int i = r & 1; i + 1 < 16; i += 2) {
+            const bool p = k[O + i + 1] < k[O + i];
+            const double lo = p ? k[O + i + 1] : k[O + i];
+            const double hi = p ? k[O + i] : k[O + i + 1];
+            k[O + i] = lo;
+            k[O + i + 1] = hi;
+            if (HV) {
+                const uint32_t vl = p ? v[O + i + 1] : v[O + i];
+                const uint32_t vh = p ? v[O + i] : v[O + i + 1];
+                v[O + i] = vl;
+                v[O + i + 1] = vh;
+            }
+        }
+    }
+}
+
+template <bool HV>
+__device__ __forceinline__ void serial_merge32(const double *sk, const uint32_t *sv, int ai, int aend, int bi, int bend,
+                                               double (&k)[VT1], uint32_t (&v)[VT1])
+{
+    double ka = sk[swm(ai)], kb = sk[swm(bi)];
+#pragma unroll
+    for (int x = 0; x < VT1; ++x) {
+        const bool p = (bi < bend) && ((ai >= aend) || (kb < ka));
+        k[x] = p ? kb : ka;
+        const int src = p ? bi : ai;
+        if (HV) v[x] = sv[swmv(src)];
+        const int nxt = src + 1;
+        if (p) bi = nxt; else ai = nxt;
+        const double kn = sk[swm(nxt)];
+        if (p) kb = kn; else ka = kn;
+    }
+}
+
+template <bool HV>
+__global__ void __launch_bounds__(NT1, HV ? 3 : 4)
+tile_sort2_kernel(const double *src_k, const uint32_t *src_v, double *dst_k, uint32_t *dst_v, long long n,
+                  const __grid_constant__ CUtensorMap ksrc, const __grid_constant__ CUtensorMap vsrc,
+                  const __grid_constant__ CUtensorMap kdst, const __grid_constant__ CUtensorMap vdst)
+{
+    pdl_wait();
+    extern __shared__ __align__(16) unsigned char smem_raw0[];
+    unsigned char *smem = smem_raw0 + ((1024u - (smem_u32(smem_raw0) & 1023u)) & 1023u);
+    double *sk = reinterpret_cast<double *>(smem);
+    uint32_t *sv = reinterpret_cast<uint32_t *>(smem + T1_KEY_BYTES);
+    __shared__ __align__(8) uint64_t bar;
+    const int tid = threadIdx.x;
+    const long long tile = blockIdx.x;
+    const long long base = tile * TILE;
+    const int cnt = (int)min((long long)TILE, n - base);
+    const bool full = cnt == TILE;
+    double k[VT1];
+    uint32_t v[VT1];
+    if (full) {
+        if (tid == 0) {
+            mbar_init(&bar, 1);
+            fence_mbar_init();
+            mbar_expect_tx(&bar, (uint32_t)(TILE * 8 + (HV ? TILE * 4 : 0)));
+            tma_load_2d(sk, &ksrc, 0, (int)(tile * (TILE / 16)), &bar);
+            if (HV) tma_load_2d(sv, &vsrc, 0, (int)(tile * (TILE / 32)), &bar);
+            mbar_arrive(&bar);
+        }
+        __syncthreads();
+        mbar_wait(&bar, 0);
+#pragma unroll
+        for (int c = 0; c < VT1 / 2; ++c) lds128(sk + tk_slot(tid * VT1 + 2 * c), k[2 * c], k[2 * c + 1]);
+        if (HV) {
+#pragma unroll
+            for (int c = 0; c < VT1 / 4; ++c) lds128u(sv + tv_slot(tid * VT1 + 4 * c), &v[4 * c]);
+        }
+    } else {
+#pragma unroll
+        for (int x = 0; x < VT1; ++x) {
+            const int e = tid * VT1 + x;
+            const bool ok = e < cnt;
+            k[x] = ok ? src_k[base + e] : __longlong_as_double(0x7FF0000000000000LL);
+            if (HV) v[x] = ok ? src_v[base + e] : 0u;
+        }
+    }
+    transpose_sort16<0, HV>(k, v);
+    transpose_sort16<16, HV>(k, v);
+    const int e0 = tid * VT1;
+    __syncthreads();                       // the TMA-layout reads are done before the first spill
+#pragma unroll 1
+    for (int coop = 1; coop <= NT1; coop <<= 1) {
+#pragma unroll
+        for (int x = 0; x < VT1; ++x) {
+            sk[swm(e0 + x)] = k[x];
+            if (HV) sv[swmv(e0 + x)] = v[x];
+        }
+        __syncthreads();
+        if (coop == 1) {                   // merge the thread's own two sorted halves
+            serial_merge32<HV>(sk, sv, e0, e0 + 16, e0 + 16, e0 + 32, k, v);
+        } else {
+            const int local = tid & (coop - 1);
+            const int a0 = (tid - local) * VT1;
+            const int run = (coop >> 1) * VT1;
+            const int b0 = a0 + run;
+            const int d = local * VT1;
+            const int i = merge_path_smem(sk, a0, run, b0, run, d, SwM());
+            serial_merge32<HV>(sk, sv, a0 + i, b0, b0 + d - i, b0 + run, k, v);
+        }
+        __syncthreads();
+    }
+    if (full) {
+#pragma unroll
+        for (int c = 0; c < VT1 / 2; ++c) sts128(sk + tk_slot(e0 + 2 * c), k[2 * c], k[2 * c + 1]);
+        if (HV) {
+#pragma unroll
+            for (int c = 0; c < VT1 / 4; ++c) sts128u(sv + tv_slot(e0 + 4 * c), &v[4 * c]);
+        }
+        fence_proxy_async();
+        __syncthreads();
+        if (tid == 0) {
+            tma_store_2d(&kdst, sk, 0, (int)(tile * (TILE / 16)));
+            if (HV) tma_store_2d(&vdst, sv, 0, (int)(tile * (TILE / 32)));
+            bulk_commit();
+            bulk_wait_read0();
+        }
+    } else {
+#pragma unroll
+        for (int x = 0; x < VT1; ++x) {
+            const int e = e0 + x;
+            if (e < cnt) {
+                dst_k[base + e] = k[x];
+                if (HV) dst_v[base + e] = v[x];
+            }
+        }
+    }
     pdl_trigger();
 }
 
