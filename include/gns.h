@@ -70,7 +70,7 @@ typedef enum {
  * buffer_fraction: 1.0 -> buffer of n elements (%RAM 2.0);
  *                  0.5 -> buffer of ceil(n/2) elements rounded up to 32
  *                         (%RAM 1.5 for even n >= 64).
- * For n <= GNS_TILE the sort runs in place with no buffer in either mode. */
+ * For n <= gns_tile_elems() the sort runs in place with no buffer in either mode. */
 gns_status gns_sort_f64(double *keys, size_t n, double buffer_fraction, gns_stream_t stream);
 gns_status gns_sort_pairs_f64_u32(double *keys, uint32_t *vals, size_t n,
                                   double buffer_fraction, gns_stream_t stream);
@@ -86,7 +86,7 @@ gns_status gns_sort_pairs_f64_u32_ws(double *keys, uint32_t *vals, size_t n,
 
 /* Pass schedule of a sort (host only, no CUDA call). */
 typedef struct {
-    int tile;                   /* GNS_TILE: elements per tile-sort CTA                  */
+    int tile;                   /* gns_tile_elems(): elements per tile-sort CTA          */
     int merge_tile;             /* elements per merge CTA                                 */
     int merge_passes;           /* HBM merge passes (1.0 mode; the 0.5 mode has the same) */
     int hbm_passes;             /* P = 1 (tile sort) + merge_passes                       */
@@ -99,7 +99,7 @@ gns_status gns_plan(size_t n, double buffer_fraction, int with_vals, gns_plan_in
 
 /* ---- the steps, exposed for per-step parity tests and per-kernel timing -- */
 
-/* Row a2 (K1): stable sort of each GNS_TILE-element tile of src into the same
+/* Row a2 (K1): stable sort of each gns_tile_elems()-element tile of src into the same
  * range of dst (dst == src allowed; otherwise the ranges must not overlap).
  * vals may both be NULL (key-only). */
 gns_status gns_tile_sort(const double *src_keys, const uint32_t *src_vals,
@@ -107,7 +107,8 @@ gns_status gns_tile_sort(const double *src_keys, const uint32_t *src_vals,
 
 /* Rows a3+a4 (K2+K3): one merge level.  For q = 0,1,..: merges the sorted runs
  * src[2qL : 2qL+L) and src[2qL+L : 2qL+2L) (clipped to n) into dst[2qL : ..).
- * run_len L must be a positive multiple of GNS_TILE.  src and dst must not
+ * run_len L must be a positive multiple of gns_merge_tile_elems()/2 (so every
+ * pair starts on a merge-tile boundary), at most 2^30.  src and dst must not
  * overlap.  ws: >= gns_merge_workspace_bytes(n) bytes (co-rank array). */
 size_t gns_merge_workspace_bytes(size_t n);
 gns_status gns_merge_pass(const double *src_keys, const uint32_t *src_vals,

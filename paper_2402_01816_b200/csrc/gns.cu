@@ -210,11 +210,11 @@ gns_status launch_tile_sort(const double *sk, const uint32_t *sv, double *dk, ui
     CUtensorMap m[4];
     std::memset(m, 0, sizeof(m));
     if (n >= (size_t)TILE) {          // full tiles move by TMA tensor copies; a ragged last tile by plain loads
-        GNS_TRY(row_map((void *)sk, n, true, TILE / 16, &m[0]));
-        GNS_TRY(row_map(dk, n, true, TILE / 16, &m[2]));
+        GNS_TRY(row_map((void *)sk, n, true, 256, &m[0]));
+        GNS_TRY(row_map(dk, n, true, 256, &m[2]));
         if (hv) {
-            GNS_TRY(row_map((void *)sv, n, false, TILE / 32, &m[1]));
-            GNS_TRY(row_map(dv, n, false, TILE / 32, &m[3]));
+            GNS_TRY(row_map((void *)sv, n, false, 256, &m[1]));
+            GNS_TRY(row_map(dv, n, false, 256, &m[3]));
         }
     }
     if (hv)
@@ -463,8 +463,8 @@ gns_status gns_merge_pass(const double *src_keys, const uint32_t *src_vals, doub
     if (hv && (!src_vals || !dst_vals)) return fail(GNS_ERR_INVALID_ARGUMENT, "src_vals/dst_vals: both or neither");
     GNS_TRY(validate_data(src_keys, src_vals, hv, n));
     GNS_TRY(validate_data(dst_keys, dst_vals, hv, n));
-    if (run_len == 0 || run_len % TILE != 0 || run_len > (size_t)1 << 30)
-        return fail(GNS_ERR_INVALID_ARGUMENT, "run_len must be a positive multiple of gns_tile_elems() <= 2^30");
+    if (run_len == 0 || run_len % (MTILE / 2) != 0 || run_len > (size_t)1 << 30)
+        return fail(GNS_ERR_INVALID_ARGUMENT, "run_len must be a positive multiple of gns_merge_tile_elems()/2, <= 2^30");
     if (n == 0) return GNS_OK;
     if (!ws || ws_bytes < merge_ws(n)) return fail(GNS_ERR_WORKSPACE_TOO_SMALL, "workspace too small");
     GNS_TRY(ensure_attrs());

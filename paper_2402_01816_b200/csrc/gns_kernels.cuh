@@ -17,10 +17,13 @@
 
 namespace gns {
 
-constexpr int NT = 256;            // threads per CTA
-constexpr int VT = 16;             // items per thread
-constexpr int TILE = NT * VT;      // K1 tile = 4096 elements
+constexpr int NT = 256;            // merge threads per CTA
+constexpr int VT = 16;             // outputs per merge thread
 constexpr int MTILE = NT * VT;     // K3/K4 output tile = 4096 elements
+constexpr int NT1 = 256;           // K1 threads per CTA
+constexpr int VT1 = 32;            // K1 keys per thread
+constexpr int TILE = NT1 * VT1;    // K1 tile = 8192 elements (runs entering the merge passes)
+static_assert(TILE % MTILE == 0, "pair boundaries must fall on merge-tile boundaries");
 
 // Swizzled shared-memory index.  Three access patterns must be conflict free:
 // coalesced fills (lane t touches e0 + t), blocked register spills (lane t
@@ -742,16 +745,13 @@ merge_tstore_kernel(PipeGeo pg, int ntiles, int per_cta, const __grid_constant__
 
 
 // ------------------------------------------------- K1 v2: TMA-fed tile sort
-// 128 threads x 32 keys (TILE = 4096).  The tile arrives by one TMA tensor
+// 256 threads x 32 keys (TILE = 8192).  The tile arrives by TMA tensor
 // load (2-D maps: keys [n/16][16] f64, vals [n/32][32] u32, 128-byte swizzle)
 // and leaves by one TMA tensor store; the blocked register<->smem transfers
 // use 16-byte accesses in the swizzled layout.  In registers: two stable
 // odd-even transposition sorts of 16; then log2(4096/16) = 8 shared-memory
 // merge rounds (round 0 merges each thread's own two halves, no search).  With
 // 32 outputs per thread the merge-path searches per key are halved vs VT=16.
-constexpr int NT1 = 128;
-constexpr int VT1 = 32;
-static_assert(NT1 * VT1 == TILE, "tile geometry");
 constexpr size_t T1_KEY_BYTES = TILE * 8 + 1024;
 constexpr size_t T1_VAL_BYTES = TILE * 4 + 1024;
 constexpr size_t t1_smem(bool hv) { return T1_KEY_BYTES + (hv ? T1_VAL_BYTES : 0) + 1024; }
@@ -814,7 +814,7 @@ __device__ __forceinline__ void serial_merge32(const double *sk, const uint32_t 
 }
 
 template <bool HV>
-__global__ void __launch_bounds__(NT1, HV ? 3 : 4)
+__global__ void __launch_bounds__(NT1, 2)
 tile_sort2_kernel(const double *src_k, const uint32_t *src_v, double *dst_k, uint32_t *dst_v, long long n,
                   const __grid_constant__ CUtensorMap ksrc, const __grid_constant__ CUtensorMap vsrc,
                   const __grid_constant__ CUtensorMap kdst, const __grid_constant__ CUtensorMap vdst)
@@ -837,8 +837,12 @@ tile_sort2_kernel(const double *src_k, const uint32_t *src_v, double *dst_k, uin
             mbar_init(&bar, 1);
             fence_mbar_init();
             mbar_expect_tx(&bar, (uint32_t)(TILE * 8 + (HV ? TILE * 4 : 0)));
-            tma_load_2d(sk, &ksrc, 0, (int)(tile * (TILE / 16)), &bar);
-            if (HV) tma_load_2d(sv, &vsrc, 0, (int)(tile * (TILE / 32)), &bar);
+#pragma unroll
+            for (int b = 0; b < TILE / 4096; ++b) {          // boxes of 256 rows
+                tma_load_2d(sk + b * 4096, &ksrc, 0, (int)(tile * (TILE / 16) + b * 256), &bar);
+                if (HV && (b & 1) == 0)
+                    tma_load_2d(sv + b * 4096, &vsrc, 0, (int)(tile * (TILE / 32) + (b / 2) * 256), &bar);
+            }
             mbar_arrive(&bar);
         }
         __syncthreads();
@@ -893,8 +897,11 @@ tile_sort2_kernel(const double *src_k, const uint32_t *src_v, double *dst_k, uin
         fence_proxy_async();
         __syncthreads();
         if (tid == 0) {
-            tma_store_2d(&kdst, sk, 0, (int)(tile * (TILE / 16)));
-            if (HV) tma_store_2d(&vdst, sv, 0, (int)(tile * (TILE / 32)));
+#pragma unroll
+            for (int b = 0; b < TILE / 4096; ++b) {
+                tma_store_2d(&kdst, sk + b * 4096, 0, (int)(tile * (TILE / 16) + b * 256));
+                if (HV && (b & 1) == 0) tma_store_2d(&vdst, sv + b * 4096, 0, (int)(tile * (TILE / 32) + (b / 2) * 256));
+            }
             bulk_commit();
             bulk_wait_read0();
         }

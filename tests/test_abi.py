@@ -46,14 +46,20 @@ def test_sm100a_only(gns):
 
 def test_geometry_and_plan(gns):
     T = gns.gns_tile_elems()
-    assert T == gns.gns_merge_tile_elems() == 4096
+    M = gns.gns_merge_tile_elems()
+    assert M == 4096 and T % M == 0 and T >= M
+
+    def passes(n):
+        runs = -(-n // T)
+        return 0 if n <= T else (runs - 1).bit_length()
+
     p = gns.plan(1 << 24, 1.0, False)
-    assert p["merge_passes"] == 12 and p["hbm_passes"] == 13
-    assert p["bytes_lower_bound"] == 13 * 2 * (1 << 24) * 8
+    assert p["merge_passes"] == passes(1 << 24) and p["hbm_passes"] == 1 + passes(1 << 24)
+    assert p["bytes_lower_bound"] == p["hbm_passes"] * 2 * (1 << 24) * 8
     assert p["buffer_elems"] == 1 << 24
     p = gns.plan(1 << 27, 0.5, True)
-    assert p["hbm_passes"] == 16 and p["left_len"] == 1 << 26 and p["buffer_elems"] == 1 << 26
-    assert p["bytes_lower_bound"] == 16 * 2 * (1 << 27) * 12
+    assert p["hbm_passes"] == 1 + passes(1 << 27) and p["left_len"] == 1 << 26 and p["buffer_elems"] == 1 << 26
+    assert p["bytes_lower_bound"] == p["hbm_passes"] * 2 * (1 << 27) * 12
     p = gns.plan(T, 0.5, True)
     assert p["workspace_bytes"] == 0 and p["hbm_passes"] == 1
     p = gns.plan(T + 1, 1.0, False)
@@ -80,7 +86,7 @@ def test_argument_errors_before_any_cuda_call(gns):
     assert gns.gns_sort_f64(256, (1 << 31), 1.0, None) == 1
     assert gns.gns_sort_f64_ws(256, 1 << 20, 1.0, None, 0, None) == 5
     assert gns.gns_sort_f64_ws(256, 1 << 20, 1.0, 256, 10, None) == 5
-    assert gns.gns_merge_pass(256, None, 512, None, 1000, 100, 256, 1 << 20, None) == 1
+    assert gns.gns_merge_pass(256, None, 512, None, 1000, 100, 256, 1 << 20, None) == 1   # run_len % 2048
     assert gns.gns_merge_inplace_top(256, None, 512, None, 10, 100, 256, 1 << 20, None) == 1
     # n in {0, 1}: OK, no launch
     assert gns.gns_sort_f64(None, 0, 1.0, None) == 0

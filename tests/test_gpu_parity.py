@@ -46,10 +46,15 @@ def check_against_oracle(gns, k, v, frac, use_ws=False, what=""):
     assert_bitexact(gk, ek, gv, ev, what=what)
 
 
-T = 4096
+T = 4096          # merge tile; the tile-sort tile (gns_tile_elems) is a multiple of it
+T1 = 8192         # tile-sort tile of this build (checked in test_tile_geometry)
 EDGE_SIZES = [0, 1, 2, 3, 31, 32, 33, 255, 1000, T - 1, T, T + 1, 2 * T - 1, 2 * T, 2 * T + 1,
               3 * T, 3 * T + 17, 4 * T + 1, 8 * T - 5, 8 * T + 3, 9 * T, 65521, (1 << 16) + 1,
-              (1 << 17) - 1, 100003]
+              (1 << 17) - 1, 100003, T1 - 1, T1 + 1, 2 * T1 + 7, 4 * T1 + 1]
+
+
+def test_tile_geometry(gns):
+    assert gns.gns_tile_elems() == T1 and gns.gns_merge_tile_elems() == T
 
 
 @pytest.mark.parametrize("frac", [1.0, 0.5])
@@ -93,6 +98,7 @@ def test_exhaustive_tiny(gns):
 # ------------------------------------------------------------- per-step parity
 
 def test_tile_sort_step(gns):
+    T = gns.gns_tile_elems()
     n = 7 * T + 123
     k = synth.ties(n, 4242, 50)
     v = synth.iota_u32(n)
@@ -199,12 +205,14 @@ def test_baseline_configs_full_size(gns, c, sub):
 
 
 def test_error_paths_leave_data_untouched(gns):
-    k = synth.uniform(5000, 1)
+    n = 3 * gns.gns_tile_elems() + 5          # > one tile, so a workspace is required
+    k = synth.uniform(n, 1)
     tk, _ = to_dev(k, None)
     before = tk.clone()
-    assert gns.gns_sort_f64(int(tk.data_ptr()), 5000, 0.3, 0) == 2
-    assert gns.gns_sort_f64(int(tk.data_ptr()) + 8, 4999, 1.0, 0) == 6
-    assert gns.gns_sort_f64_ws(int(tk.data_ptr()), 5000, 1.0, 0, 0, 0) == 5
+    assert gns.gns_sort_f64(int(tk.data_ptr()), n, 0.3, 0) == 2
+    assert gns.gns_sort_f64(int(tk.data_ptr()) + 8, n - 1, 1.0, 0) == 6
+    assert gns.gns_sort_f64_ws(int(tk.data_ptr()), n, 1.0, 0, 0, 0) == 5
+    assert gns.gns_sort_f64_ws(int(tk.data_ptr()), n, 1.0, 256, 64, 0) == 5
     torch.cuda.synchronize()
     assert torch.equal(before, tk)
 
