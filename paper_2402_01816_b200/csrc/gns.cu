@@ -111,12 +111,13 @@ gns_status ensure_attrs()
     if (dev >= 64) return fail(GNS_ERR_CUDA, "device ordinal >= 64");
     std::lock_guard<std::mutex> lk(g_attr_mu);
     if (g_attr_done & (1ull << dev)) return GNS_OK;
-    const int k3 = (int)(K3_SMEM_KEYS + sizeof(uint32_t) * K3_SK);
-    GNS_TRY(check(cudaFuncSetAttribute(merge_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, k3), "attr"));
-    GNS_TRY(check(cudaFuncSetAttribute(merge_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, k3), "attr"));
     GNS_TRY(check(cudaFuncSetAttribute(merge_tstore_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)ts_smem(true)), "attr"));
     GNS_TRY(check(cudaFuncSetAttribute(merge_tstore_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)ts_smem(false)), "attr"));
+    GNS_TRY(check(cudaFuncSetAttribute(merge_inplace_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)ts_smem(true)), "attr"));
+    GNS_TRY(check(cudaFuncSetAttribute(merge_inplace_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)ts_smem(false)), "attr"));
     GNS_TRY(check(cudaFuncSetAttribute(tile_sort2_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)t1_smem(true)), "attr"));
@@ -248,14 +249,20 @@ gns_status launch_merge(const MergeGeo &g, const double *lim_a, const double *li
     }
     GNS_TRY(launch_pdl("partition_kernel", partition_kernel, (unsigned)ceil_div((size_t)ntiles * 32, 256), 256, 0, st,
                        g, ntiles, corank));
-    const size_t smem = K3_SMEM_KEYS + (hv ? sizeof(uint32_t) * K3_SK : 0);
     GNS_TRY(launch_pdl("inplace_deps_kernel", inplace_deps_kernel, (unsigned)ceil_div(ntiles + 1, 256), 256, 0, st,
                        (const int *)corank, ntiles, g.L, g.n, deps, flags));
     unsigned *ticket = flags + ntiles;
-    if (hv) return launch_pdl("merge_kernel<inplace>", merge_kernel<true, true>, ntiles, NT, smem, st, g,
-                              (const int *)corank, (const int2 *)deps, flags, ticket);
-    return launch_pdl("merge_kernel<inplace>", merge_kernel<false, true>, ntiles, NT, smem, st, g, (const int *)corank,
-                      (const int2 *)deps, flags, ticket);
+    PipeGeo pg;
+    pg.g = g;
+    pg.a_lim = lim_a;
+    pg.b_lim = lim_b;
+    CUtensorMap map;
+    GNS_TRY(row_map(g.ok, (size_t)g.n, true, MTILE / 16, &map));
+    const int grid = std::min(ntiles, 2 * num_sms());
+    if (hv) return launch_pdl("merge_inplace_kernel", merge_inplace_kernel<true>, grid, NT, ts_smem(true), st, pg,
+                              ntiles, (const int *)corank, (const int2 *)deps, flags, ticket, map);
+    return launch_pdl("merge_inplace_kernel", merge_inplace_kernel<false>, grid, NT, ts_smem(false), st, pg, ntiles,
+                      (const int *)corank, (const int2 *)deps, flags, ticket, map);
 }
 
 MergeGeo uniform_geo(const double *sk, const uint32_t *sv, double *dk, uint32_t *dv, size_t n, size_t L)

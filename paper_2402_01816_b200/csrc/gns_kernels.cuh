@@ -5,7 +5,7 @@
 //   K2+K3 merge_tstore_kernel  (rows a3+a4) one merge level, src -> dst ping-pong,
 //                              co-rank search warps fused in
 //   K2    partition_kernel     (row a3) stable co-rank split per output tile (for K4)
-//   K4    merge_kernel<.,true> (row a6) ordered in-place top merge of the 0.5 mode
+//   K4    merge_inplace_kernel (row a6) ordered in-place top merge of the 0.5 mode
 //         inplace_deps_kernel  (row a6) which earlier tiles each K4 tile must wait for
 //
 // No code here is shared with oracle/ (the CPU oracle); the two are compared
@@ -25,39 +25,12 @@ constexpr int VT1 = 32;            // K1 keys per thread
 constexpr int TILE = NT1 * VT1;    // K1 tile = 8192 elements (runs entering the merge passes)
 static_assert(TILE % MTILE == 0, "pair boundaries must fall on merge-tile boundaries");
 
-// Swizzled shared-memory index.  Three access patterns must be conflict free:
-// coalesced fills (lane t touches e0 + t), blocked register spills (lane t
-// touches 16t + v) and the merge-path reads (lane t near base + 8t, because a
-// thread's VT outputs consume ~VT/2 from each run).  XOR-ing the slot within
-// its 128-byte row with the row index spreads all three over the 32 banks:
-//   doubles: 16 per row, slot = e ^ ((e >> 4) & 15)
-//   u32    : 32 per row, slot = e ^ ((e >> 5) & 31)
-// Both are bijections within each aligned row, so no extra space is needed.
-__device__ __forceinline__ int swk(int e) { return e ^ ((e >> 4) & 15); }
-__device__ __forceinline__ int swv(int e) { return e ^ ((e >> 5) & 31); }
-constexpr size_t K3_SK = MTILE + 32;
-constexpr size_t K3_SMEM_KEYS = sizeof(double) * K3_SK;
-
-struct SwK { __device__ __forceinline__ int operator()(int e) const { return swk(e); } };
-struct SwV { __device__ __forceinline__ int operator()(int e) const { return swv(e); } };
-
 // ---------------------------------------------------------------- global I/O
 // 256-bit vector accesses (LDG/STG.E.ENL2.256 on sm_100a).
-__device__ __forceinline__ void ld_v4(const double *p, double &a, double &b, double &c, double &d)
-{
-    asm volatile("ld.global.v4.f64 {%0,%1,%2,%3}, [%4];"
-                 : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p));
-}
 __device__ __forceinline__ void st_v4(double *p, double a, double b, double c, double d)
 {
     asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};"
                  :: "l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
-}
-__device__ __forceinline__ void ld_v8(const uint32_t *p, uint32_t *u)
-{
-    asm volatile("ld.global.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                 : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3]),
-                   "=r"(u[4]), "=r"(u[5]), "=r"(u[6]), "=r"(u[7]) : "l"(p));
 }
 __device__ __forceinline__ void st_v8(uint32_t *p, const uint32_t *u)
 {
@@ -144,6 +117,7 @@ __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.comm
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 __device__ __forceinline__ void sts128(void *p, double a, double b)
 {
     asm volatile("st.shared.v2.f64 [%0], {%1, %2};" :: "r"(smem_u32(p)), "d"(a), "d"(b) : "memory");
@@ -392,92 +366,6 @@ inplace_deps_kernel(const int *__restrict__ corank, int ntiles, long long L, lon
     }
     deps[t] = make_int2(u_lo, lo - 1);
 }
-
-// ------------------------------------------------------------ K3 / K4 merge
-// One CTA per MTILE-element output tile.  Loads A[i0:i1) and B[j0:j1)
-// (exactly the inputs of its outputs, from the co-ranks) coalesced into shared
-// memory, each thread finds its own diagonal by merge path and merges VT
-// outputs serially (left wins ties), then writes them with 256-bit stores.
-// INPLACE (K4): tiles are taken in atomic-ticket order; after loading, a tile
-// publishes flags[t] (release); before writing, it waits (acquire) on the
-// flags of the earlier tiles in deps[t].  Deadlock-free: a tile only waits on
-// smaller tickets, whose CTAs are already resident and never wait on it.
-template <bool HV, bool INPLACE>
-__global__ void __launch_bounds__(NT, 3)
-merge_kernel(MergeGeo g, const int *__restrict__ corank, const int2 *__restrict__ deps,
-             unsigned *flags, unsigned *ticket)
-{
-    pdl_wait();
-    pdl_trigger();
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    double *sk = reinterpret_cast<double *>(smem_raw);
-    uint32_t *sv = reinterpret_cast<uint32_t *>(smem_raw + K3_SMEM_KEYS);
-    __shared__ int s_t;
-
-    const int tid = threadIdx.x;
-    int t;
-    if (INPLACE) {
-        if (tid == 0) s_t = (int)atomicAdd(ticket, 1u);
-        __syncthreads();
-        t = s_t;
-    } else {
-        t = blockIdx.x;
-    }
-    const TileSpan s = tile_span(g, t);
-    const int cnt = s.k1 - s.k0;
-    // co-ranks; clamped so that even a non-monotone split (NaN keys) stays in bounds
-    const int i0 = corank[t];
-    int i1 = (s.k1 == s.na + s.nb) ? s.na : corank[t + 1];
-    i1 = min(min(max(max(i1, i0), s.k1 - s.nb), i0 + cnt), s.na);
-    const int j0 = s.k0 - i0;
-    const int ca = i1 - i0;
-
-    const double *A = g.ak + s.pbase + i0;
-    const double *B = g.bk + s.pbase + j0 - ca;     // B[e] for e in [ca, cnt)
-    const uint32_t *Av = HV ? g.av + s.pbase + i0 : nullptr;
-    const uint32_t *Bv = HV ? g.bv + s.pbase + j0 - ca : nullptr;
-    // All VT loads are issued before any shared store (addresses clamped into
-    // the tile instead of branching), so each thread has VT loads in flight.
-    {
-        double tk[VT];
-        uint32_t tv[VT];
-#pragma unroll
-        for (int r = 0; r < VT; ++r) {
-            const int e = min(tid + r * NT, cnt - 1);
-            const bool fa = e < ca;
-            tk[r] = fa ? A[e] : B[e];
-            if (HV) tv[r] = fa ? Av[e] : Bv[e];
-        }
-#pragma unroll
-        for (int r = 0; r < VT; ++r) {
-            const int e = tid + r * NT;
-            if (e < cnt) {
-                sk[swk(e)] = tk[r];
-                if (HV) sv[swv(e)] = tv[r];
-            }
-        }
-    }
-    __syncthreads();
-
-    if (INPLACE) {
-        if (tid == 0) {
-            __threadfence();
-            st_release(flags + t, 1u);
-        }
-        const int2 dp = deps[t];
-        for (int u = dp.x + tid; u <= dp.y; u += NT)
-            while (ld_acquire(flags + u) == 0u) { __nanosleep(64); }
-        __syncthreads();
-    }
-
-    const int d = min(tid * VT, cnt);
-    const int i = merge_path_smem(sk, 0, ca, ca, cnt - ca, d, SwK());
-    double k[VT];
-    uint32_t v[VT];
-    serial_merge<HV>(sk, sv, i, ca, ca + d - i, cnt, k, v, SwK(), SwV());
-    store_segment<HV>(g.ok, g.ov, s.g0 + tid * VT, cnt - d, k, v);
-}
-
 
 // ------------------------------------------------ K3 pipelined (persistent)
 // The production merge pass.  A persistent grid (2 CTAs per SM) walks the
@@ -915,6 +803,126 @@ tile_sort2_kernel(const double *src_k, const uint32_t *src_v, double *dst_k, uin
             }
         }
     }
+    pdl_trigger();
+}
+
+
+// ------------------------- K4 v2: pipelined ordered in-place top merge (row a6)
+// The 0.5 mode's last merge: A = the buffer (left half, sorted), B = data[nl:n)
+// (right half, sorted), output = data[0:n).  Persistent CTAs claim output
+// tiles in atomic-ticket order (so every claimed tile belongs to a running
+// CTA), load each tile's inputs by TMA bulk copies (co-ranks precomputed by
+// partition_kernel) into a double-buffered stage and publish flags[t]
+// (st.release.gpu) as soon as that load has landed.  Before a tile's outputs
+// are stored (TMA tensor store of the keys, 256-bit stores of the vals), the
+// tile waits (ld.acquire.gpu) on the flags of the earlier tiles whose B read
+// range intersects its write range (deps[], inplace_deps_kernel).  Later tiles
+// never intersect: k1(t) <= nl + j1(t) <= nl + j0(u) for u > t.  Deadlock-free:
+// the smallest tile in flight only depends on tiles whose loads have landed.
+template <bool HV>
+__global__ void __launch_bounds__(NT, 2)
+merge_inplace_kernel(PipeGeo pg, int ntiles, const int *__restrict__ corank, const int2 *__restrict__ deps,
+                     unsigned *flags, unsigned *ticket, const __grid_constant__ CUtensorMap omap)
+{
+    pdl_wait();
+    extern __shared__ __align__(16) unsigned char smem_raw0[];
+    unsigned char *smem_raw = smem_raw0 + ((1024u - (smem_u32(smem_raw0) & 1023u)) & 1023u);
+    __shared__ __align__(8) uint64_t bars[2];
+    __shared__ PipeMeta meta[2];
+    __shared__ int s_next;
+    auto skb = [&](int st) { return reinterpret_cast<double *>(smem_raw + st * ts_stage_bytes(HV)); };
+    auto svb = [&](int st) {
+        return reinterpret_cast<uint32_t *>(smem_raw + st * ts_stage_bytes(HV) + TS_KEY_SLOTS * sizeof(double));
+    };
+    const int tid = threadIdx.x;
+    uint64_t policy = policy_evict_first();
+    if (tid == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        fence_mbar_init();
+    }
+    // claim the first two tiles
+    int tcur = -1, tnext = -1;
+    if (tid == 0) {
+        const int a = (int)atomicAdd(ticket, 1u);
+        if (a < ntiles) {
+            pipe_issue<HV>(pg, a, corank[a], a + 1 < ntiles ? corank[a + 1] : 0, skb(0), svb(0), &bars[0], &meta[0],
+                           policy);
+            const int b = (int)atomicAdd(ticket, 1u);
+            if (b < ntiles)
+                pipe_issue<HV>(pg, b, corank[b], b + 1 < ntiles ? corank[b + 1] : 0, skb(1), svb(1), &bars[1],
+                               &meta[1], policy);
+            s_next = b;
+        } else {
+            s_next = ntiles;
+        }
+        meta[0].t = a;   // (a >= ntiles: nothing to do)
+    }
+    __syncthreads();
+    tcur = meta[0].t;
+    tnext = s_next;
+    const long long n = pg.g.n;
+    const long long full_rows = n >> 4;
+    for (int i = 0; tcur < ntiles; ++i) {
+        const int st = i & 1;
+        mbar_wait(&bars[st], (uint32_t)((i >> 1) & 1));
+        if (tid == 0) st_release(flags + tcur, 1u);           // inputs of tile tcur are in shared memory
+        const PipeMeta mt = meta[st];
+        const int cnt = mt.ca + mt.cb;
+        const int d = min(tid * VT, cnt);
+        double *sk = skb(st);
+        const uint32_t *sv = svb(st);
+        double k[VT];
+        uint32_t v[VT];
+        const int ii = merge_path_smem(sk, mt.offa, mt.ca, mt.bslot, mt.cb, d, Lin());
+        serial_merge<HV>(sk, sv, mt.offa + ii, mt.offa + mt.ca, mt.bslot + d - ii, mt.bslot + mt.cb, k, v, Lin(),
+                         Lin());
+        const long long row = (long long)tcur * (MTILE / 16) + tid;
+        __syncthreads();                                       // stage st fully read
+        unsigned char *rowp = reinterpret_cast<unsigned char *>(sk) + tid * 128;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) sts128(rowp + ((c ^ (tid & 7)) << 4), k[2 * c], k[2 * c + 1]);
+        fence_proxy_async();
+        // wait until every earlier tile that reads B slots we overwrite has loaded
+        const int2 dp = deps[tcur];
+        for (int u = dp.x + tid; u <= dp.y; u += NT)
+            while (ld_acquire(flags + u) == 0u) { __nanosleep(32); }
+        fence_proxy_async_global();
+        if (HV) {
+            const int mv = cnt - d;
+            if (mv >= VT) {
+#pragma unroll
+                for (int x = 0; x < VT; x += 8) st_v8(pg.g.ov + row * 16 + x, &v[x]);
+            } else {
+#pragma unroll
+                for (int x = 0; x < VT; ++x)
+                    if (x < mv) pg.g.ov[row * 16 + x] = v[x];
+            }
+        }
+        if (row == full_rows && d < cnt) {
+#pragma unroll
+            for (int x = 0; x < VT; ++x)
+                if (x < cnt - d) pg.g.ok[row * 16 + x] = k[x];
+        }
+        __syncthreads();
+        if (tid == 0) {
+            tma_store_2d(&omap, sk, 0, tcur * (MTILE / 16));
+            bulk_commit();
+            bulk_wait_read0();
+            int c = ntiles;
+            if (tnext < ntiles) {
+                c = (int)atomicAdd(ticket, 1u);
+                if (c < ntiles)
+                    pipe_issue<HV>(pg, c, corank[c], c + 1 < ntiles ? corank[c + 1] : 0, skb(st), svb(st), &bars[st],
+                                   &meta[st], policy);
+            }
+            s_next = c;
+        }
+        __syncthreads();
+        tcur = tnext;
+        tnext = s_next;
+    }
+    if (tid == 0) bulk_wait0();
     pdl_trigger();
 }
 
