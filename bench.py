@@ -301,7 +301,8 @@ def main():
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": 2 * n * s,
                      "share_of_step": roof["merge_share"],
-                     "whole_sort": {"bytes_lower_bound": plan["bytes_lower_bound"], "hbm_passes": plan["hbm_passes"],
+                     "whole_sort": {"bytes_lower_bound": plan["bytes_lower_bound"],
+                                    "element_passes": plan["element_passes"],
                                     "achieved": plan["bytes_lower_bound"] / (ms_per_step / 1e3) / 1e9,
                                     "frac": plan["bytes_lower_bound"] / (ms_per_step / 1e3) / 1e9 / peak},
                      "per_kernel_ms": roof["per_kernel_ms"]},
@@ -323,20 +324,8 @@ def main():
 
 
 def launches(plan, frac, n):
-    T = plan["tile"]
-    if n <= 1:
-        return 0
-    if n <= T:
-        return 1
-    if frac == 1.0:
-        return 1 + plan["merge_passes"]          # tile sort + one fused merge kernel per pass
-    nl = plan["left_len"]
-    nr = n - nl
-
-    def lr(m):
-        r = -(-m // T)
-        return 1 + max(0, (r - 1).bit_length()) if m > 0 else 0
-    return lr(nl) + lr(nr) + 3   # + partition, deps (also clears the flags), top merge
+    """Kernel launches of one sort, from the library's own schedule (gns_plan)."""
+    return plan["launches"]
 
 
 def kernel_roofline(gns, torch, dev, stream, src_k, src_v, k, v, n, hv, s, plan, restore, reps=5):
@@ -428,9 +417,10 @@ def end_to_end(gns, torch, dev, stream, case, args, n, hv, ws, steps=None):
             "steps": steps, "path": "pinned host -> gns_sort_f64_ws -> pinned host"}
 
 
-def footprint_cfg5(gns, torch, dev, stream, flush, reps=5):
-    """configs[4]: n = 2^27 U(0,1) + u32 index, buffer 1.0 vs 0.5: runtime,
-    %RAM (nominal = exact workspace bytes) and tFootprint."""
+def footprint_cfg5(gns, torch, dev, stream, flush, reps=3):
+    """configs[4]: n = 2^27 U(0,1) + u32 index at buffer fractions 1.0, 0.5
+    (the BASELINE pair) and the NEXT-f1 sweep 0.25, 0.125, 1/16: runtime,
+    %RAM (exact workspace bytes) and tFootprint = %RAM x runTime."""
     case = synth.config(5)
     n = case.keys.size
     src_k = torch.from_numpy(case.keys).to(dev)
@@ -438,10 +428,11 @@ def footprint_cfg5(gns, torch, dev, stream, flush, reps=5):
     k, v = torch.empty_like(src_k), torch.empty_like(src_v)
     out = {"workload": "cfg5: n=2^27 f64 U(0,1) + u32 index", "n": n}
     first = None
-    for frac in (1.0, 0.5):
+    agree = True
+    for frac in (1.0, 0.5, 0.25, 0.125, 0.0625):
         ws = gns.alloc_workspace(n, frac, True, dev)
         times = []
-        for i in range(reps + 2):
+        for i in range(reps + 1):
             k.copy_(src_k)
             v.copy_(src_v)
             flush.fill_(1)
@@ -450,20 +441,23 @@ def footprint_cfg5(gns, torch, dev, stream, flush, reps=5):
             gns.sort_(k, v, frac, workspace=ws)
             b.record(stream)
             torch.cuda.synchronize()
-            if i >= 2:
+            if i >= 1:
                 times.append(a.elapsed_time(b))
         if first is None:
             first = k.clone(), v.clone()
         else:
-            same = bool(torch.equal(first[0].view(torch.int64), k.view(torch.int64)) and
-                        torch.equal(first[1].view(torch.int32), v.view(torch.int32)))
-            out["modes_agree_bitexact"] = same
+            agree = agree and bool(torch.equal(first[0].view(torch.int64), k.view(torch.int64)) and
+                                   torch.equal(first[1].view(torch.int32), v.view(torch.int32)))
         ram = 1.0 + ws.numel() / (n * 12)
         ms = float(np.median(times))
         out[str(frac)] = {"ms": ms, "keys_per_s": n / (ms / 1e3), "ram_pct": ram,
-                          "tfootprint_ms": ram * ms, "workspace_bytes": int(ws.numel())}
+                          "tfootprint_ms": ram * ms, "workspace_bytes": int(ws.numel()),
+                          "element_passes": gns.plan(n, frac, True)["element_passes"]}
         del ws
+    out["all_fractions_agree_bitexact"] = agree
     out["tfootprint_0.5_lt_1.0"] = out["0.5"]["tfootprint_ms"] < out["1.0"]["tfootprint_ms"]
+    out["argmin_tfootprint_fraction"] = min((f for f in out if f.replace(".", "").isdigit()),
+                                            key=lambda f: out[f]["tfootprint_ms"])
     return out
 
 

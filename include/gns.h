@@ -56,7 +56,7 @@ typedef struct CUstream_st *gns_stream_t;   /* == cudaStream_t */
 typedef enum {
     GNS_OK = 0,
     GNS_ERR_INVALID_ARGUMENT = 1,      /* NULL pointer with n > 0, n > GNS_MAX_N, bad run_len */
-    GNS_ERR_UNSUPPORTED_FRACTION = 2,  /* buffer_fraction not exactly 1.0 or 0.5               */
+    GNS_ERR_UNSUPPORTED_FRACTION = 2,  /* buffer_fraction not 1.0 and not in [1/64, 0.5]        */
     GNS_ERR_OUT_OF_MEMORY = 3,         /* buffer allocation failed; input untouched            */
     GNS_ERR_CUDA = 4,                  /* CUDA launch/runtime error                             */
     GNS_ERR_WORKSPACE_TOO_SMALL = 5,   /* ws NULL or ws_bytes < gns_workspace_bytes(...)        */
@@ -69,7 +69,13 @@ typedef enum {
  * keys[0:n) (and vals[0:n)) are replaced by their stable ascending sort.
  * buffer_fraction: 1.0 -> buffer of n elements (%RAM 2.0);
  *                  0.5 -> buffer of ceil(n/2) elements rounded up to 32
- *                         (%RAM 1.5 for even n >= 64).
+ *                         (%RAM 1.5 for even n >= 64);
+ *                  p in [1/64, 0.5) -> buffer of ceil(p*n) elements rounded up
+ *                         to 32 (%RAM ~ 1+p): the right part is sorted first
+ *                         (recursively, same buffer), then the left p*n
+ *                         elements are sorted into the buffer and merged back
+ *                         in place (Frogsort2/3's imbalanced split and shared
+ *                         buffer).  More passes, less RAM.
  * For n <= gns_tile_elems() the sort runs in place with no buffer in either mode. */
 gns_status gns_sort_f64(double *keys, size_t n, double buffer_fraction, gns_stream_t stream);
 gns_status gns_sort_pairs_f64_u32(double *keys, uint32_t *vals, size_t n,
@@ -88,12 +94,16 @@ gns_status gns_sort_pairs_f64_u32_ws(double *keys, uint32_t *vals, size_t n,
 typedef struct {
     int tile;                   /* gns_tile_elems(): elements per tile-sort CTA          */
     int merge_tile;             /* elements per merge CTA                                 */
-    int merge_passes;           /* HBM merge passes (1.0 mode; the 0.5 mode has the same) */
-    int hbm_passes;             /* P = 1 (tile sort) + merge_passes                       */
+    int merge_passes;           /* HBM merge passes of a 1.0-mode sort of n               */
+    int hbm_passes;             /* ceil(element_passes)                                   */
+    int launches;               /* kernel launches of the sort                            */
+    double element_passes;      /* sum over all steps of elements moved through HBM / n;  */
+                                /* 1.0 mode: 1 + merge_passes; 0.5 mode about the same    */
     size_t left_len;            /* 0.5 mode: elements sorted into the buffer (nl)         */
     size_t workspace_bytes;     /* = gns_workspace_bytes(n, fraction, with_vals)          */
     size_t buffer_elems;        /* key(+val) slots in the workspace (bufferRAM / s)       */
-    size_t bytes_lower_bound;   /* P * 2 * n * s, s = 8 or 12: the algorithmic bytes      */
+    size_t bytes_lower_bound;   /* element_passes * n * 2 * s, s = 8 or 12: algorithmic   */
+                                /* bytes (one read-scan + one write-scan per level)       */
 } gns_plan_info;
 gns_status gns_plan(size_t n, double buffer_fraction, int with_vals, gns_plan_info *out);
 
@@ -115,10 +125,11 @@ gns_status gns_merge_pass(const double *src_keys, const uint32_t *src_vals,
                           double *dst_keys, uint32_t *dst_vals, size_t n, size_t run_len,
                           void *ws, size_t ws_bytes, gns_stream_t stream);
 
-/* Row a6 (K2+K4): ordered in-place top merge of the 0.5 mode.  left_keys[0:nl)
- * (a separate buffer) and keys[nl:n) are sorted runs; the stable merge (left
- * wins ties) is written to keys[0:n).  Requires nl >= n - nl, nl % 32 == 0 and
- * left_* not overlapping keys/vals.  ws: >= gns_merge_workspace_bytes(n). */
+/* Row a6 (K2+K4): ordered in-place top merge of the limited-buffer modes.
+ * left_keys[0:nl) (a separate buffer) and keys[nl:n) are sorted runs; the
+ * stable merge (left wins ties) is written to keys[0:n).  Requires
+ * 0 < nl <= n, nl % 32 == 0 and left_* not overlapping keys/vals.
+ * ws: >= gns_merge_workspace_bytes(n). */
 gns_status gns_merge_inplace_top(double *keys, uint32_t *vals, const double *left_keys,
                                  const uint32_t *left_vals, size_t nl, size_t n,
                                  void *ws, size_t ws_bytes, gns_stream_t stream);

@@ -42,6 +42,7 @@ _i = ctypes.c_int
 class gns_plan_info(ctypes.Structure):
     _fields_ = [("tile", ctypes.c_int), ("merge_tile", ctypes.c_int),
                 ("merge_passes", ctypes.c_int), ("hbm_passes", ctypes.c_int),
+                ("launches", ctypes.c_int), ("element_passes", ctypes.c_double),
                 ("left_len", _sz), ("workspace_bytes", _sz), ("buffer_elems", _sz),
                 ("bytes_lower_bound", _sz)]
 

@@ -10,6 +10,7 @@
 
 #include <cuda_runtime.h>
 #include <cstdio>
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <algorithm>
@@ -70,11 +71,19 @@ struct Layout {
     int ntiles = 0;         // merge tiles over the whole array
 };
 
-Layout layout(size_t n, bool half, bool hv)
+// Buffer mode (row a5 and NEXT f1): FULL = 100 % buffer (ping-pong with the
+// data), LIMITED = a buffer of `buf` elements (multiple of 32); fraction 0.5
+// gives buf = left_len(n) (the 0.5 mode), smaller fractions recurse.
+struct Mode {
+    bool limited = false;
+    size_t buf = 0;
+};
+
+Layout layout(size_t n, const Mode &m, bool hv)
 {
     Layout L;
     if (n <= (size_t)TILE) return L;   // one tile, sorted in place, no buffer
-    L.buf_elems = half ? left_len(n) : n;
+    L.buf_elems = m.limited ? m.buf : n;
     L.ntiles = (int)ceil_div(n, MTILE);
     size_t o = 0;
     L.off_k = o;
@@ -84,9 +93,9 @@ Layout layout(size_t n, bool half, bool hv)
     L.off_corank = o;
     o = align_up(o + (size_t)(L.ntiles + 1) * sizeof(int), 256);
     L.off_deps = o;
-    if (half) o = align_up(o + (size_t)L.ntiles * sizeof(int2), 256);
+    if (m.limited) o = align_up(o + (size_t)L.ntiles * sizeof(int2), 256);
     L.off_flags = o;
-    if (half) o = align_up(o + (size_t)(L.ntiles + 1) * sizeof(unsigned), 256);
+    if (m.limited) o = align_up(o + (size_t)(L.ntiles + 1) * sizeof(unsigned), 256);
     L.total = o;
     return L;
 }
@@ -276,6 +285,7 @@ MergeGeo uniform_geo(const double *sk, const uint32_t *sv, double *dk, uint32_t 
     g.ov = dv;
     g.n = (long long)n;
     g.L = (long long)L;
+    g.single = 0;
     return g;
 }
 
@@ -304,11 +314,24 @@ gns_status sort_range(double *rk, uint32_t *rv, double *pk_, uint32_t *pv_, size
     return GNS_OK;
 }
 
-gns_status validate_fraction(double f, bool *half)
+constexpr double GNS_MIN_FRACTION = 1.0 / 64.0;
+
+// buffer_fraction: exactly 1.0 (100 % buffer, %RAM 2.0), or p in [1/64, 0.5]:
+// a buffer of ceil(p*n) elements rounded up to 32 (%RAM ~ 1 + p).
+gns_status mode_for(double f, size_t n, Mode *m)
 {
-    if (f == 1.0) { *half = false; return GNS_OK; }
-    if (f == 0.5) { *half = true; return GNS_OK; }
-    return fail(GNS_ERR_UNSUPPORTED_FRACTION, "buffer_fraction must be exactly 1.0 or 0.5");
+    if (f == 1.0) {
+        m->limited = false;
+        m->buf = n;
+        return GNS_OK;
+    }
+    if (!(f >= GNS_MIN_FRACTION && f <= 0.5))
+        return fail(GNS_ERR_UNSUPPORTED_FRACTION, "buffer_fraction must be 1.0 or in [1/64, 0.5]");
+    m->limited = true;
+    const size_t b = align_up((size_t)std::ceil(f * (double)n), 32);
+    m->buf = b < n ? b : n;
+    if (f == 0.5) m->buf = left_len(n);
+    return GNS_OK;
 }
 
 gns_status validate_data(const double *keys, const uint32_t *vals, bool hv, size_t n)
@@ -321,46 +344,108 @@ gns_status validate_data(const double *keys, const uint32_t *vals, bool hv, size
     return GNS_OK;
 }
 
+// Ordered in-place merge of A = buffer[0:nl) and B = data[lo+nl : lo+len)
+// into data[lo : lo+len) (row a6, K2 + deps + K4).
+gns_status top_merge(double *keys, uint32_t *vals, double *bk, uint32_t *bv, size_t lo, size_t len, size_t nl,
+                     int *corank, int2 *deps, unsigned *flags, cudaStream_t st)
+{
+    const bool hv = vals != nullptr;
+    MergeGeo g;
+    g.ak = bk;
+    g.av = bv;
+    g.bk = keys + lo + nl;
+    g.bv = hv ? vals + lo + nl : nullptr;
+    g.ok = keys + lo;
+    g.ov = hv ? vals + lo : nullptr;
+    g.n = (long long)len;
+    g.L = (long long)nl;
+    g.single = 1;
+    return launch_merge(g, bk + nl, keys + lo + len, corank, deps, flags, true, st);
+}
+
+// One step of a limited-buffer sort, also used by gns_plan to count element passes.
+struct Sched {
+    double elem_passes = 0;     // sum over steps of (HBM passes of the step x elements) / n
+    int launches = 0;
+};
+
+void count_sort_range(size_t len, Sched *sc, size_t n)
+{
+    if (!len) return;
+    const int M = merge_passes_for(len);
+    sc->elem_passes += (double)(1 + M) * (double)len / (double)n;
+    sc->launches += 1 + M;
+}
+
+// Limited-buffer sort of data[lo : lo+len) with a buffer of b elements
+// (Frogsort2/3-style imbalanced split): if the 0.5 scheme
+// fits (b >= left_len(len)), left half -> buffer, right half in place using the
+// dead left region, in-place top merge.  Otherwise the right part
+// data[lo+b : lo+len) is sorted first (recursively, same buffer), then the
+// left b elements are sorted into the buffer and merged in place.
+gns_status sort_limited(double *keys, uint32_t *vals, size_t lo, size_t len, size_t b, double *bk, uint32_t *bv,
+                        int *corank, int2 *deps, unsigned *flags, cudaStream_t st, Sched *sc, size_t n)
+{
+    const bool hv = vals != nullptr;
+    double *dk = keys + lo;
+    uint32_t *dv = hv ? vals + lo : nullptr;
+    if (len <= (size_t)TILE) {
+        if (sc) {
+            count_sort_range(len, sc, n);
+            return GNS_OK;
+        }
+        return launch_tile_sort(dk, dv, dk, dv, len, st);
+    }
+    const size_t nl = left_len(len);
+    if (b >= nl) {
+        const size_t nr = len - nl;
+        if (sc) {
+            count_sort_range(nl, sc, n);
+            count_sort_range(nr, sc, n);
+            sc->elem_passes += (double)len / (double)n;
+            sc->launches += 3;
+            return GNS_OK;
+        }
+        GNS_TRY(sort_range(dk, dv, bk, bv, nl, true, corank, st));
+        GNS_TRY(sort_range(dk + nl, hv ? dv + nl : nullptr, dk, dv, nr, false, corank, st));
+        return top_merge(keys, vals, bk, bv, lo, len, nl, corank, deps, flags, st);
+    }
+    GNS_TRY(sort_limited(keys, vals, lo + b, len - b, b, bk, bv, corank, deps, flags, st, sc, n));
+    if (sc) {
+        count_sort_range(b, sc, n);
+        sc->elem_passes += (double)len / (double)n;
+        sc->launches += 3;
+        return GNS_OK;
+    }
+    GNS_TRY(sort_range(dk, dv, bk, bv, b, true, corank, st));
+    return top_merge(keys, vals, bk, bv, lo, len, b, corank, deps, flags, st);
+}
+
 // The sort proper (rows a1..a7).  ws already validated and sized.
-gns_status run_sort(double *keys, uint32_t *vals, size_t n, bool half, unsigned char *ws, cudaStream_t st)
+gns_status run_sort(double *keys, uint32_t *vals, size_t n, const Mode &m, unsigned char *ws, cudaStream_t st)
 {
     if (n <= 1) return GNS_OK;
     GNS_TRY(ensure_attrs());
     const bool hv = vals != nullptr;
     if (n <= (size_t)TILE)   // one tile: in place, no buffer
         return launch_tile_sort(keys, vals, keys, vals, n, st);
-    const Layout Lo = layout(n, half, hv);
+    const Layout Lo = layout(n, m, hv);
     double *bk = reinterpret_cast<double *>(ws + Lo.off_k);
     uint32_t *bv = hv ? reinterpret_cast<uint32_t *>(ws + Lo.off_v) : nullptr;
     int *corank = reinterpret_cast<int *>(ws + Lo.off_corank);
-    if (!half) return sort_range(keys, vals, bk, bv, n, false, corank, st);
-
-    // 0.5 mode (row a5): left half -> buffer, right half in place with the
-    // dead left region as its partner, then the ordered in-place top merge.
-    const size_t nl = left_len(n), nr = n - nl;
-    GNS_TRY(sort_range(keys, vals, bk, bv, nl, true, corank, st));
-    GNS_TRY(sort_range(keys + nl, hv ? vals + nl : nullptr, keys, vals, nr, false, corank, st));
-    MergeGeo g;
-    g.ak = bk;
-    g.av = bv;
-    g.bk = keys + nl;
-    g.bv = hv ? vals + nl : nullptr;
-    g.ok = keys;
-    g.ov = vals;
-    g.n = (long long)n;
-    g.L = (long long)nl;
+    if (!m.limited) return sort_range(keys, vals, bk, bv, n, false, corank, st);
     int2 *deps = reinterpret_cast<int2 *>(ws + Lo.off_deps);
     unsigned *flags = reinterpret_cast<unsigned *>(ws + Lo.off_flags);
-    return launch_merge(g, bk + nl, keys + n, corank, deps, flags, true, st);
+    return sort_limited(keys, vals, 0, n, m.buf, bk, bv, corank, deps, flags, st, nullptr, n);
 }
 
 gns_status sort_alloc(double *keys, uint32_t *vals, bool hv, size_t n, double frac, cudaStream_t st)
 {
-    bool half = false;
-    GNS_TRY(validate_fraction(frac, &half));
+    Mode m;
+    GNS_TRY(mode_for(frac, n, &m));
     GNS_TRY(validate_data(keys, vals, hv, n));
     if (n <= 1) return GNS_OK;
-    const Layout Lo = layout(n, half, hv);
+    const Layout Lo = layout(n, m, hv);
     unsigned char *ws = nullptr;
     if (Lo.total) {
         cudaError_t e = cudaMallocAsync((void **)&ws, Lo.total, st);
@@ -370,7 +455,7 @@ gns_status sort_alloc(double *keys, uint32_t *vals, bool hv, size_t n, double fr
             return check(e, "cudaMallocAsync");
         }
     }
-    gns_status s = run_sort(keys, hv ? vals : nullptr, n, half, ws, st);
+    gns_status s = run_sort(keys, hv ? vals : nullptr, n, m, ws, st);
     if (ws) {
         gns_status f = check(cudaFreeAsync(ws, st), "cudaFreeAsync");
         if (s == GNS_OK) s = f;
@@ -381,16 +466,16 @@ gns_status sort_alloc(double *keys, uint32_t *vals, bool hv, size_t n, double fr
 gns_status sort_ws(double *keys, uint32_t *vals, bool hv, size_t n, double frac, void *ws, size_t ws_bytes,
                    cudaStream_t st)
 {
-    bool half = false;
-    GNS_TRY(validate_fraction(frac, &half));
+    Mode m;
+    GNS_TRY(mode_for(frac, n, &m));
     GNS_TRY(validate_data(keys, vals, hv, n));
     if (n <= 1) return GNS_OK;
-    const Layout Lo = layout(n, half, hv);
+    const Layout Lo = layout(n, m, hv);
     if (Lo.total) {
         if (!ws || ws_bytes < Lo.total) return fail(GNS_ERR_WORKSPACE_TOO_SMALL, "workspace too small");
         if (!is_aligned(ws, 32)) return fail(GNS_ERR_MISALIGNED, "ws must be 32-byte aligned");
     }
-    return run_sort(keys, hv ? vals : nullptr, n, half, (unsigned char *)ws, st);
+    return run_sort(keys, hv ? vals : nullptr, n, m, (unsigned char *)ws, st);
 }
 
 }  // namespace
@@ -411,9 +496,9 @@ gns_status gns_sort_pairs_f64_u32(double *keys, uint32_t *vals, size_t n, double
 
 size_t gns_workspace_bytes(size_t n, double buffer_fraction, int with_vals)
 {
-    bool half = false;
-    if (validate_fraction(buffer_fraction, &half) != GNS_OK || n > GNS_MAX_N) return 0;
-    return layout(n, half, with_vals != 0).total;
+    Mode m;
+    if (mode_for(buffer_fraction, n, &m) != GNS_OK || n > GNS_MAX_N) return 0;
+    return layout(n, m, with_vals != 0).total;
 }
 
 gns_status gns_sort_f64_ws(double *keys, size_t n, double buffer_fraction, void *ws, size_t ws_bytes,
@@ -430,21 +515,31 @@ gns_status gns_sort_pairs_f64_u32_ws(double *keys, uint32_t *vals, size_t n, dou
 
 gns_status gns_plan(size_t n, double buffer_fraction, int with_vals, gns_plan_info *out)
 {
-    bool half = false;
-    GNS_TRY(validate_fraction(buffer_fraction, &half));
+    Mode m;
+    GNS_TRY(mode_for(buffer_fraction, n, &m));
     if (!out) return fail(GNS_ERR_INVALID_ARGUMENT, "out == NULL");
     if (n > GNS_MAX_N) return fail(GNS_ERR_INVALID_ARGUMENT, "n > GNS_MAX_N");
-    const Layout Lo = layout(n, half, with_vals != 0);
+    const Layout Lo = layout(n, m, with_vals != 0);
     const size_t s = with_vals ? 12 : 8;
     std::memset(out, 0, sizeof(*out));
     out->tile = TILE;
     out->merge_tile = MTILE;
     out->merge_passes = merge_passes_for(n);
-    out->hbm_passes = n > 1 ? 1 + out->merge_passes : 0;
-    out->left_len = (half && n > (size_t)TILE) ? left_len(n) : 0;
+    Sched sc;
+    if (n <= 1) {
+        sc.elem_passes = 0;
+    } else if (n <= (size_t)TILE || !m.limited) {
+        count_sort_range(n, &sc, n);
+    } else {
+        sort_limited(nullptr, nullptr, 0, n, m.buf, nullptr, nullptr, nullptr, nullptr, nullptr, 0, &sc, n);
+    }
+    out->element_passes = sc.elem_passes;
+    out->launches = sc.launches;
+    out->hbm_passes = (int)std::ceil(sc.elem_passes - 1e-9);
+    out->left_len = (m.limited && n > (size_t)TILE) ? std::min(m.buf, left_len(n)) : 0;
     out->workspace_bytes = Lo.total;
     out->buffer_elems = Lo.buf_elems;
-    out->bytes_lower_bound = (size_t)out->hbm_passes * 2 * n * s;
+    out->bytes_lower_bound = (size_t)std::llround(sc.elem_passes * (double)n) * 2 * s;
     return GNS_OK;
 }
 
@@ -487,8 +582,8 @@ gns_status gns_merge_inplace_top(double *keys, uint32_t *vals, const double *lef
     if (hv && (!vals || !left_vals)) return fail(GNS_ERR_INVALID_ARGUMENT, "vals/left_vals: both or neither");
     GNS_TRY(validate_data(keys, vals, hv, n));
     GNS_TRY(validate_data(left_keys, left_vals, hv, nl));
-    if (nl > n || nl < n - nl || nl % 32 != 0 || nl == 0)
-        return fail(GNS_ERR_INVALID_ARGUMENT, "need n-nl <= nl <= n, nl % 32 == 0, nl > 0");
+    if (nl > n || nl % 32 != 0 || nl == 0)
+        return fail(GNS_ERR_INVALID_ARGUMENT, "need 0 < nl <= n, nl % 32 == 0");
     if (!ws || ws_bytes < merge_ws(n)) return fail(GNS_ERR_WORKSPACE_TOO_SMALL, "workspace too small");
     GNS_TRY(ensure_attrs());
     const size_t nt = ceil_div(n, MTILE);
@@ -505,6 +600,7 @@ gns_status gns_merge_inplace_top(double *keys, uint32_t *vals, const double *lef
     g.ov = vals;
     g.n = (long long)n;
     g.L = (long long)nl;
+    g.single = 1;
     return launch_merge(g, left_keys + nl, keys + n, corank, deps, flags, true, (cudaStream_t)stream);
 }
 

@@ -207,7 +207,8 @@ __device__ __forceinline__ void serial_merge(const double *sk, const uint32_t *s
 // Pair q merges A_q = ak[q*2L : q*2L + na_q) with B_q = bk[q*2L : q*2L + nb_q)
 // into out[q*2L : ...), na_q = min(L, n - 2qL), nb_q = clamp(n - 2qL - L, 0, L).
 //   uniform pass : ak = src, bk = src + L, out = dst
-//   0.5 top merge: ak = buffer, bk = data + nl, L = nl, out = data (one pair)
+//   in-place top merge (single = 1): ak = buffer, bk = data + nl, L = nl,
+//                  out = data, one pair with na = nl, nb = n - nl
 struct MergeGeo {
     const double *ak;
     const uint32_t *av;
@@ -217,6 +218,7 @@ struct MergeGeo {
     uint32_t *ov;
     long long n;
     long long L;
+    int single;     // 1: one pair, A = ak[0:L), B = bk[0:n-L) (any lengths; the in-place top merge)
 };
 
 struct TileSpan {
@@ -228,11 +230,17 @@ __device__ __forceinline__ TileSpan tile_span(const MergeGeo &g, int t)
 {
     TileSpan s;
     s.g0 = (long long)t * MTILE;
-    const long long span = 2 * g.L;
-    s.pbase = (s.g0 / span) * span;
-    const long long rem = g.n - s.pbase;
-    s.na = (int)min(g.L, rem);
-    s.nb = (int)max(0LL, min(g.L, rem - g.L));
+    if (g.single) {
+        s.pbase = 0;
+        s.na = (int)g.L;
+        s.nb = (int)(g.n - g.L);
+    } else {
+        const long long span = 2 * g.L;
+        s.pbase = (s.g0 / span) * span;
+        const long long rem = g.n - s.pbase;
+        s.na = (int)min(g.L, rem);
+        s.nb = (int)max(0LL, min(g.L, rem - g.L));
+    }
     s.k0 = (int)(s.g0 - s.pbase);
     s.k1 = min(s.k0 + MTILE, s.na + s.nb);
     return s;

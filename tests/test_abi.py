@@ -77,6 +77,26 @@ def test_workspace_ram_pct(gns):
     assert gns.workspace_bytes(n, 0.7, True) == 0
 
 
+def test_limited_buffer_fractions(gns):
+    """NEXT f1: buffer fractions p in [1/64, 0.5]: %RAM ~ 1 + p, more passes
+    as p shrinks (the Frogsort2 trade-off)."""
+    from oracle import footprint
+    n = 1 << 27
+    prev = None
+    for p in (0.5, 0.25, 0.125, 1 / 16, 1 / 64):
+        info = gns.plan(n, p, True)
+        r = footprint.ram_pct(n * 12, info["workspace_bytes"])
+        assert 1 + p <= r < 1 + p + 1e-3, (p, r)
+        if prev is not None:
+            assert info["element_passes"] >= prev
+        prev = info["element_passes"]
+        assert info["bytes_lower_bound"] == round(info["element_passes"] * n) * 2 * 12
+    assert gns.plan(n, 0.5, True)["element_passes"] == gns.plan(n, 1.0, True)["element_passes"]
+    for bad in (0.0, 0.75, 1 / 128, 1.5, -1.0):
+        assert gns.workspace_bytes(n, bad, True) == 0
+        assert gns.gns_sort_f64(256, 10000, bad, None) == 2
+
+
 def test_argument_errors_before_any_cuda_call(gns):
     # all of these must return before touching CUDA (there is no GPU here)
     assert gns.gns_sort_f64(None, 10, 1.0, None) == 1

@@ -75,6 +75,17 @@ def test_uniform_pairs_ws(gns, n, frac):
     check_against_oracle(gns, k, v, frac, use_ws=True, what=f"n={n}")
 
 
+@pytest.mark.parametrize("frac", [0.25, 0.3, 0.125, 1 / 16, 1 / 64])
+@pytest.mark.parametrize("n", [T1 + 1, 5 * T1 + 333, 20 * T1 + 7])
+def test_limited_buffer_fractions(gns, n, frac):
+    """NEXT f1: buffer fraction p < 0.5 (recursive imbalanced split + in-place
+    merges); same unique stable result."""
+    k = synth.ties(n, 600 + n, 11)
+    v = synth.iota_u32(n)
+    check_against_oracle(gns, k, v, frac, use_ws=True, what=f"n={n} p={frac}")
+    check_against_oracle(gns, synth.uniform(n, 700 + n), None, frac, what=f"n={n} p={frac} key-only")
+
+
 def test_specials_inf_zero(gns):
     n = 3 * T + 5
     rng = np.random.default_rng(5)
