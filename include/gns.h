@@ -65,6 +65,17 @@ typedef enum {
 
 #define GNS_MAX_N ((size_t)0x7FFFFFFF)   /* 2^31 - 1 elements */
 
+/* The four stable API targets of PAPER.md:137-142 (§Definition of sorting,
+ * "AscLeft, AscRight, DescLeft and DescRight"): key direction x the memory
+ * direction in which ties keep their input order.  AscLeft is the default of
+ * every other entry point. */
+typedef enum {
+    GNS_ASC_LEFT = 0,    /* ascending, ties in input order (left to right)          */
+    GNS_ASC_RIGHT = 1,   /* ascending, ties in reverse input order = reverse(DescLeft) */
+    GNS_DESC_LEFT = 2,   /* descending, ties in input order                          */
+    GNS_DESC_RIGHT = 3   /* descending, ties in reverse input order = reverse(AscLeft) */
+} gns_target;
+
 /* ---- the sort (rows a1-a7 of SURVEY.md §8) -------------------------------
  * keys[0:n) (and vals[0:n)) are replaced by their stable ascending sort.
  * buffer_fraction: 1.0 -> buffer of n elements (%RAM 2.0);
@@ -89,6 +100,14 @@ gns_status gns_sort_f64_ws(double *keys, size_t n, double buffer_fraction,
 gns_status gns_sort_pairs_f64_u32_ws(double *keys, uint32_t *vals, size_t n,
                                      double buffer_fraction, void *ws, size_t ws_bytes,
                                      gns_stream_t stream);
+
+/* NEXT f3: any of the four targets.  vals may be NULL (key-only).  ws may be
+ * NULL (buffer allocated stream-ordered) or a workspace of
+ * gns_workspace_bytes(n, buffer_fraction, vals != NULL) bytes.  The Right
+ * targets add one in-place reversal pass.  Errors as above, plus
+ * GNS_ERR_INVALID_ARGUMENT for an unknown target. */
+gns_status gns_sort_target_f64(double *keys, uint32_t *vals, size_t n, double buffer_fraction, gns_target target,
+                               void *ws, size_t ws_bytes, gns_stream_t stream);
 
 /* Pass schedule of a sort (host only, no CUDA call). */
 typedef struct {

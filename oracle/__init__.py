@@ -15,6 +15,10 @@ Functions and the passages they follow:
   (permutations -> identity keys + inverse permutation), a textbook stable
   counting sort (heavy ties), ``numpy.argsort(kind="stable")`` and the SPEC.md
   worked examples in ``tests/golden/``.
+* :func:`sort_target` — the four API targets AscLeft/AscRight/DescLeft/
+  DescRight (NEXT f3): the same mergesort, merge rule per
+  target.  Pinned by brute force on (key, +-index) orders, the SPEC.md:72
+  DescLeft example, and AscLeft == :func:`sort`.
 * :func:`merge_runs` — one merge level over runs of length L.
   Pinned by the SPEC.md ``mergeKnuth`` examples and by brute force.
 * :mod:`oracle.footprint` — %RAM and tFootprint.  Pinned by the
@@ -57,6 +61,8 @@ def lib():
         up = ctypes.POINTER(ctypes.c_uint32)
         L.oracle_sort_f64_u32.argtypes = [dp, up, ctypes.c_size_t]
         L.oracle_sort_f64_u32.restype = ctypes.c_int
+        L.oracle_sort_target.argtypes = [dp, up, ctypes.c_size_t, ctypes.c_int]
+        L.oracle_sort_target.restype = ctypes.c_int
         L.oracle_merge_runs.argtypes = [dp, up, ctypes.c_size_t, ctypes.c_size_t, dp, up]
         L.oracle_merge_runs.restype = ctypes.c_int
         _lib = L
@@ -82,6 +88,23 @@ def sort(keys: np.ndarray, vals: Optional[np.ndarray] = None
         raise OracleNaNError("NaN key")
     if rc != 0:
         raise MemoryError("oracle")
+    return k, v
+
+
+TARGETS = {"AscLeft": 0, "AscRight": 1, "DescLeft": 2, "DescRight": 3}
+
+
+def sort_target(keys: np.ndarray, vals: Optional[np.ndarray], target: str
+                ) -> Tuple[np.ndarray, Optional[np.ndarray]]:
+    """The four stable API targets, NEXT f3."""
+    k = np.array(keys, dtype=np.float64, copy=True, order="C")
+    v = None if vals is None else np.array(vals, dtype=np.uint32, copy=True, order="C")
+    dp, up = _ptrs(k, v)
+    rc = lib().oracle_sort_target(dp, up, k.size, TARGETS[target])
+    if rc == 1:
+        raise OracleNaNError("NaN key")
+    if rc != 0:
+        raise ValueError("oracle_sort_target failed")
     return k, v
 
 

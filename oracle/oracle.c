@@ -24,6 +24,12 @@
  *     no insertion-sort cutoff: the plainest correct form).
  *   %RAM of this oracle is 2.0 (PAPER.md:26 formula, buffer = n elements).
  *
+ * oracle_sort_target(): the four stable API targets of PAPER.md:137-142
+ * (AscLeft, AscRight, DescLeft, DescRight), each written out as the same plain
+ * mergesort with its own merge rule: the right run's head is taken iff it must
+ * precede the left run's head in the target order, ties included for the
+ * *Right targets (ties in reverse input order).  (NEXT f3.)
+ *
  * oracle_merge_runs(): one merge *level* of the same mergesort over runs of
  * length L ("per recursion-level one read-scan with comparisons ... and one
  * write-scan") — the definition a single GPU merge pass must
@@ -64,6 +70,65 @@ static void msort(double *k, uint32_t *v, double *tk, uint32_t *tv, size_t lo, s
     merge_into(k, v, tk, tv, lo, mid, hi);
     memcpy(k + lo, tk + lo, (hi - lo) * sizeof(double));
     if (v) memcpy(v + lo, tv + lo, (hi - lo) * sizeof(uint32_t));
+}
+
+/* target: 0 AscLeft, 1 AscRight, 2 DescLeft, 3 DescRight.  take_right(l, r):
+ * the right head goes first.  AscLeft: r < l.  AscRight: r <= l.
+ * DescLeft: r > l.  DescRight: r >= l. */
+static int take_right(int target, double l, double r)
+{
+    switch (target) {
+    case 1: return r <= l;
+    case 2: return r > l;
+    case 3: return r >= l;
+    default: return r < l;
+    }
+}
+
+static void merge_into_t(const double *k, const uint32_t *v, double *tk, uint32_t *tv,
+                         size_t lo, size_t mid, size_t hi, int target)
+{
+    size_t i = lo, j = mid, o = lo;
+    while (i < mid && j < hi) {
+        if (take_right(target, k[i], k[j])) {
+            tk[o] = k[j];
+            if (v) tv[o] = v[j];
+            ++j;
+        } else {
+            tk[o] = k[i];
+            if (v) tv[o] = v[i];
+            ++i;
+        }
+        ++o;
+    }
+    while (i < mid) { tk[o] = k[i]; if (v) tv[o] = v[i]; ++i; ++o; }
+    while (j < hi) { tk[o] = k[j]; if (v) tv[o] = v[j]; ++j; ++o; }
+}
+
+static void msort_t(double *k, uint32_t *v, double *tk, uint32_t *tv, size_t lo, size_t hi, int target)
+{
+    if (hi - lo <= 1) return;
+    size_t mid = lo + (hi - lo) / 2;
+    msort_t(k, v, tk, tv, lo, mid, target);
+    msort_t(k, v, tk, tv, mid, hi, target);
+    merge_into_t(k, v, tk, tv, lo, mid, hi, target);
+    memcpy(k + lo, tk + lo, (hi - lo) * sizeof(double));
+    if (v) memcpy(v + lo, tv + lo, (hi - lo) * sizeof(uint32_t));
+}
+
+int oracle_sort_target(double *keys, uint32_t *vals, size_t n, int target)
+{
+    for (size_t i = 0; i < n; ++i)
+        if (keys[i] != keys[i]) return 1;
+    if (target < 0 || target > 3) return 3;
+    if (n < 2) return 0;
+    double *tk = (double *)malloc(n * sizeof(double));
+    uint32_t *tv = vals ? (uint32_t *)malloc(n * sizeof(uint32_t)) : NULL;
+    if (!tk || (vals && !tv)) { free(tk); free(tv); return 2; }
+    msort_t(keys, vals, tk, tv, 0, n, target);
+    free(tk);
+    free(tv);
+    return 0;
 }
 
 /* Sorts keys[0:n) (and vals, if non-NULL) in place.

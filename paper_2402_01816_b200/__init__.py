@@ -60,6 +60,7 @@ _c = {
     "gns_workspace_bytes": _sig("gns_workspace_bytes", [_sz, _d, _i], _sz),
     "gns_sort_f64_ws": _sig("gns_sort_f64_ws", [_vp, _sz, _d, _vp, _sz, _vp]),
     "gns_sort_pairs_f64_u32_ws": _sig("gns_sort_pairs_f64_u32_ws", [_vp, _vp, _sz, _d, _vp, _sz, _vp]),
+    "gns_sort_target_f64": _sig("gns_sort_target_f64", [_vp, _vp, _sz, _d, _i, _vp, _sz, _vp]),
     "gns_plan": _sig("gns_plan", [_sz, _d, _i, ctypes.POINTER(gns_plan_info)]),
     "gns_tile_sort": _sig("gns_tile_sort", [_vp, _vp, _vp, _vp, _sz, _vp]),
     "gns_merge_workspace_bytes": _sig("gns_merge_workspace_bytes", [_sz], _sz),
@@ -107,6 +108,13 @@ def gns_sort_f64_ws(keys_ptr, n, buffer_fraction, ws_ptr, ws_bytes, stream) -> i
 
 def gns_sort_pairs_f64_u32_ws(keys_ptr, vals_ptr, n, buffer_fraction, ws_ptr, ws_bytes, stream) -> int:
     return _c["gns_sort_pairs_f64_u32_ws"](keys_ptr, vals_ptr, n, buffer_fraction, ws_ptr, ws_bytes, stream)
+
+
+TARGETS = {"AscLeft": 0, "AscRight": 1, "DescLeft": 2, "DescRight": 3}
+
+
+def gns_sort_target_f64(keys_ptr, vals_ptr, n, buffer_fraction, target, ws_ptr, ws_bytes, stream) -> int:
+    return _c["gns_sort_target_f64"](keys_ptr, vals_ptr, n, buffer_fraction, target, ws_ptr, ws_bytes, stream)
 
 
 def gns_plan(n: int, buffer_fraction: float, with_vals: bool) -> gns_plan_info:
@@ -172,14 +180,22 @@ def _check_keys(keys, vals):
             raise ValueError("keys and vals differ in length")
 
 
-def sort_(keys, vals=None, buffer_fraction: float = 1.0, workspace=None, stream=None):
-    """Stable ascending in-place sort of ``keys`` (and ``vals``) on the GPU.
+def sort_(keys, vals=None, buffer_fraction: float = 1.0, workspace=None, stream=None, target: str = "AscLeft"):
+    """Stable in-place sort of ``keys`` (and ``vals``) on the GPU; ascending
+    with ties in input order unless ``target`` names another of the four API
+    targets (AscLeft, AscRight, DescLeft, DescRight).
 
     ``workspace``: optional uint8 CUDA tensor of >= workspace_bytes(...) bytes;
     without it the library allocates its buffer stream-ordered."""
     _check_keys(keys, vals)
     n = keys.numel()
     st = _stream_handle(stream)
+    if target != "AscLeft":
+        wp = _ptr(workspace) if workspace is not None else None
+        wb = workspace.numel() * workspace.element_size() if workspace is not None else 0
+        _check(gns_sort_target_f64(_ptr(keys), _ptr(vals), n, buffer_fraction, TARGETS[target], wp, wb, st),
+               "sort_")
+        return keys, vals
     if workspace is None:
         if vals is None:
             rc = gns_sort_f64(_ptr(keys), n, buffer_fraction, st)

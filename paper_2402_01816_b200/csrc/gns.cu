@@ -120,18 +120,21 @@ gns_status ensure_attrs()
     if (dev >= 64) return fail(GNS_ERR_CUDA, "device ordinal >= 64");
     std::lock_guard<std::mutex> lk(g_attr_mu);
     if (g_attr_done & (1ull << dev)) return GNS_OK;
-    GNS_TRY(check(cudaFuncSetAttribute(merge_tstore_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)ts_smem(true)), "attr"));
-    GNS_TRY(check(cudaFuncSetAttribute(merge_tstore_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)ts_smem(false)), "attr"));
-    GNS_TRY(check(cudaFuncSetAttribute(merge_inplace_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)ts_smem(true)), "attr"));
-    GNS_TRY(check(cudaFuncSetAttribute(merge_inplace_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)ts_smem(false)), "attr"));
-    GNS_TRY(check(cudaFuncSetAttribute(tile_sort2_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)t1_smem(true)), "attr"));
-    GNS_TRY(check(cudaFuncSetAttribute(tile_sort2_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)t1_smem(false)), "attr"));
+#define GNS_ATTR(K, BYTES) \
+    GNS_TRY(check(cudaFuncSetAttribute(K, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(BYTES)), "attr"))
+    GNS_ATTR((merge_tstore_kernel<true, false>), ts_smem(true));
+    GNS_ATTR((merge_tstore_kernel<false, false>), ts_smem(false));
+    GNS_ATTR((merge_tstore_kernel<true, true>), ts_smem(true));
+    GNS_ATTR((merge_tstore_kernel<false, true>), ts_smem(false));
+    GNS_ATTR((merge_inplace_kernel<true, false>), ts_smem(true));
+    GNS_ATTR((merge_inplace_kernel<false, false>), ts_smem(false));
+    GNS_ATTR((merge_inplace_kernel<true, true>), ts_smem(true));
+    GNS_ATTR((merge_inplace_kernel<false, true>), ts_smem(false));
+    GNS_ATTR((tile_sort2_kernel<true, false>), t1_smem(true));
+    GNS_ATTR((tile_sort2_kernel<false, false>), t1_smem(false));
+    GNS_ATTR((tile_sort2_kernel<true, true>), t1_smem(true));
+    GNS_ATTR((tile_sort2_kernel<false, true>), t1_smem(false));
+#undef GNS_ATTR
     GNS_TRY(check(cudaDeviceGetAttribute(&g_num_sms[dev], cudaDevAttrMultiProcessorCount, dev), "sm count"));
     g_attr_done |= (1ull << dev);
     return GNS_OK;
@@ -211,7 +214,7 @@ gns_status launch_pdl(const char *what, void (*kern)(KArgs...), dim3 grid, dim3 
 }
 
 // Row a2 (K1).
-gns_status launch_tile_sort(const double *sk, const uint32_t *sv, double *dk, uint32_t *dv, size_t n,
+gns_status launch_tile_sort(const double *sk, const uint32_t *sv, double *dk, uint32_t *dv, size_t n, bool desc,
                             cudaStream_t st)
 {
     if (n == 0) return GNS_OK;
@@ -227,51 +230,54 @@ gns_status launch_tile_sort(const double *sk, const uint32_t *sv, double *dk, ui
             GNS_TRY(row_map(dv, n, false, 256, &m[3]));
         }
     }
-    if (hv)
-        return launch_pdl("tile_sort2_kernel", tile_sort2_kernel<true>, grid, NT1, t1_smem(true), st, sk, sv, dk, dv,
-                          (long long)n, m[0], m[1], m[2], m[3]);
-    return launch_pdl("tile_sort2_kernel", tile_sort2_kernel<false>, grid, NT1, t1_smem(false), st, sk,
-                      (const uint32_t *)nullptr, dk, (uint32_t *)nullptr, (long long)n, m[0], m[1], m[2], m[3]);
+    const uint32_t *svv = hv ? sv : nullptr;
+    uint32_t *dvv = hv ? dv : nullptr;
+    auto kern = hv ? (desc ? tile_sort2_kernel<true, true> : tile_sort2_kernel<true, false>)
+                   : (desc ? tile_sort2_kernel<false, true> : tile_sort2_kernel<false, false>);
+    return launch_pdl("tile_sort2_kernel", kern, grid, NT1, t1_smem(hv), st, sk, svv, dk, dvv, (long long)n, m[0],
+                      m[1], m[2], m[3]);
 }
 
 // Rows a3+a4 (fused K2+K3, persistent TMA pipeline) or, in place, a6 (K2 +
 // dependency ranges + K4 with the ticket/flag protocol).
 gns_status launch_merge(const MergeGeo &g, const double *lim_a, const double *lim_b, int *corank, int2 *deps,
-                        unsigned *flags, bool inplace, cudaStream_t st)
+                        unsigned *flags, bool inplace, bool desc, cudaStream_t st)
 {
     const int ntiles = (int)ceil_div((size_t)g.n, MTILE);
     const bool hv = g.av != nullptr;
-    if (!inplace) {
-        PipeGeo pg;
-        pg.g = g;
-        pg.a_lim = lim_a;
-        pg.b_lim = lim_b;
-        const int ctas = std::min(ntiles, 2 * num_sms());
-        const int per = (int)ceil_div(ntiles, ctas);
-        const int grid = (int)ceil_div(ntiles, per);
-        CUtensorMap map;
-        GNS_TRY(row_map(g.ok, (size_t)g.n, true, MTILE / 16, &map));
-        if (hv) return launch_pdl("merge_tstore_kernel", merge_tstore_kernel<true>, grid, FUSED_THREADS,
-                                  ts_smem(true), st, pg, ntiles, per, map);
-        return launch_pdl("merge_tstore_kernel", merge_tstore_kernel<false>, grid, FUSED_THREADS, ts_smem(false), st,
-                          pg, ntiles, per, map);
-    }
-    GNS_TRY(launch_pdl("partition_kernel", partition_kernel, (unsigned)ceil_div((size_t)ntiles * 32, 256), 256, 0, st,
-                       g, ntiles, corank));
-    GNS_TRY(launch_pdl("inplace_deps_kernel", inplace_deps_kernel, (unsigned)ceil_div(ntiles + 1, 256), 256, 0, st,
-                       (const int *)corank, ntiles, g.L, g.n, deps, flags));
-    unsigned *ticket = flags + ntiles;
     PipeGeo pg;
     pg.g = g;
     pg.a_lim = lim_a;
     pg.b_lim = lim_b;
     CUtensorMap map;
     GNS_TRY(row_map(g.ok, (size_t)g.n, true, MTILE / 16, &map));
+    if (!inplace) {
+        const int ctas = std::min(ntiles, 2 * num_sms());
+        const int per = (int)ceil_div(ntiles, ctas);
+        const int grid = (int)ceil_div(ntiles, per);
+        auto kern = hv ? (desc ? merge_tstore_kernel<true, true> : merge_tstore_kernel<true, false>)
+                       : (desc ? merge_tstore_kernel<false, true> : merge_tstore_kernel<false, false>);
+        return launch_pdl("merge_tstore_kernel", kern, grid, FUSED_THREADS, ts_smem(hv), st, pg, ntiles, per, map);
+    }
+    GNS_TRY(launch_pdl("partition_kernel", desc ? partition_kernel<true> : partition_kernel<false>,
+                       (unsigned)ceil_div((size_t)ntiles * 32, 256), 256, 0, st, g, ntiles, corank));
+    GNS_TRY(launch_pdl("inplace_deps_kernel", inplace_deps_kernel, (unsigned)ceil_div(ntiles + 1, 256), 256, 0, st,
+                       (const int *)corank, ntiles, g.L, g.n, deps, flags));
+    unsigned *ticket = flags + ntiles;
     const int grid = std::min(ntiles, 2 * num_sms());
-    if (hv) return launch_pdl("merge_inplace_kernel", merge_inplace_kernel<true>, grid, NT, ts_smem(true), st, pg,
-                              ntiles, (const int *)corank, (const int2 *)deps, flags, ticket, map);
-    return launch_pdl("merge_inplace_kernel", merge_inplace_kernel<false>, grid, NT, ts_smem(false), st, pg, ntiles,
-                      (const int *)corank, (const int2 *)deps, flags, ticket, map);
+    auto kern = hv ? (desc ? merge_inplace_kernel<true, true> : merge_inplace_kernel<true, false>)
+                   : (desc ? merge_inplace_kernel<false, true> : merge_inplace_kernel<false, false>);
+    return launch_pdl("merge_inplace_kernel", kern, grid, NT, ts_smem(hv), st, pg, ntiles, (const int *)corank,
+                      (const int2 *)deps, flags, ticket, map);
+}
+
+gns_status launch_reverse(double *k, uint32_t *v, size_t n, cudaStream_t st)
+{
+    if (n < 2) return GNS_OK;
+    const unsigned grid = (unsigned)std::min<size_t>(ceil_div(n / 2, 256), (size_t)num_sms() * 8);
+    if (v) return launch_pdl("reverse_kernel", reverse_kernel<true>, grid, 256, 0, st, k, v, (long long)n);
+    return launch_pdl("reverse_kernel", reverse_kernel<false>, grid, 256, 0, st, k, (uint32_t *)nullptr,
+                      (long long)n);
 }
 
 MergeGeo uniform_geo(const double *sk, const uint32_t *sv, double *dk, uint32_t *dv, size_t n, size_t L)
@@ -294,7 +300,7 @@ MergeGeo uniform_geo(const double *sk, const uint32_t *sv, double *dk, uint32_t 
 // `final_in_partner`, else in R.  Parity picks the tile-sort destination so
 // no copy pass is ever needed (an odd number of merge levels starts from P).
 gns_status sort_range(double *rk, uint32_t *rv, double *pk_, uint32_t *pv_, size_t len,
-                      bool final_in_partner, int *corank, cudaStream_t st)
+                      bool final_in_partner, int *corank, bool desc, cudaStream_t st)
 {
     if (len == 0) return GNS_OK;
     const int M = merge_passes_for(len);
@@ -303,11 +309,11 @@ gns_status sort_range(double *rk, uint32_t *rv, double *pk_, uint32_t *pv_, size
     uint32_t *cv = tile_to_partner ? pv_ : rv;
     double *ok = tile_to_partner ? rk : pk_;
     uint32_t *ov = tile_to_partner ? rv : pv_;
-    GNS_TRY(launch_tile_sort(rk, rv, ck, cv, len, st));
+    GNS_TRY(launch_tile_sort(rk, rv, ck, cv, len, desc, st));
     for (int p = 0; p < M; ++p) {
         const size_t L = (size_t)TILE << p;
         MergeGeo g = uniform_geo(ck, cv, ok, ov, len, L);
-        GNS_TRY(launch_merge(g, ck + len, ck + len, corank, nullptr, nullptr, false, st));
+        GNS_TRY(launch_merge(g, ck + len, ck + len, corank, nullptr, nullptr, false, desc, st));
         std::swap(ck, ok);
         std::swap(cv, ov);
     }
@@ -347,7 +353,7 @@ gns_status validate_data(const double *keys, const uint32_t *vals, bool hv, size
 // Ordered in-place merge of A = buffer[0:nl) and B = data[lo+nl : lo+len)
 // into data[lo : lo+len) (row a6, K2 + deps + K4).
 gns_status top_merge(double *keys, uint32_t *vals, double *bk, uint32_t *bv, size_t lo, size_t len, size_t nl,
-                     int *corank, int2 *deps, unsigned *flags, cudaStream_t st)
+                     int *corank, int2 *deps, unsigned *flags, bool desc, cudaStream_t st)
 {
     const bool hv = vals != nullptr;
     MergeGeo g;
@@ -360,7 +366,7 @@ gns_status top_merge(double *keys, uint32_t *vals, double *bk, uint32_t *bv, siz
     g.n = (long long)len;
     g.L = (long long)nl;
     g.single = 1;
-    return launch_merge(g, bk + nl, keys + lo + len, corank, deps, flags, true, st);
+    return launch_merge(g, bk + nl, keys + lo + len, corank, deps, flags, true, desc, st);
 }
 
 // One step of a limited-buffer sort, also used by gns_plan to count element passes.
@@ -384,7 +390,7 @@ void count_sort_range(size_t len, Sched *sc, size_t n)
 // data[lo+b : lo+len) is sorted first (recursively, same buffer), then the
 // left b elements are sorted into the buffer and merged in place.
 gns_status sort_limited(double *keys, uint32_t *vals, size_t lo, size_t len, size_t b, double *bk, uint32_t *bv,
-                        int *corank, int2 *deps, unsigned *flags, cudaStream_t st, Sched *sc, size_t n)
+                        int *corank, int2 *deps, unsigned *flags, bool desc, cudaStream_t st, Sched *sc, size_t n)
 {
     const bool hv = vals != nullptr;
     double *dk = keys + lo;
@@ -394,7 +400,7 @@ gns_status sort_limited(double *keys, uint32_t *vals, size_t lo, size_t len, siz
             count_sort_range(len, sc, n);
             return GNS_OK;
         }
-        return launch_tile_sort(dk, dv, dk, dv, len, st);
+        return launch_tile_sort(dk, dv, dk, dv, len, desc, st);
     }
     const size_t nl = left_len(len);
     if (b >= nl) {
@@ -406,40 +412,52 @@ gns_status sort_limited(double *keys, uint32_t *vals, size_t lo, size_t len, siz
             sc->launches += 3;
             return GNS_OK;
         }
-        GNS_TRY(sort_range(dk, dv, bk, bv, nl, true, corank, st));
-        GNS_TRY(sort_range(dk + nl, hv ? dv + nl : nullptr, dk, dv, nr, false, corank, st));
-        return top_merge(keys, vals, bk, bv, lo, len, nl, corank, deps, flags, st);
+        GNS_TRY(sort_range(dk, dv, bk, bv, nl, true, corank, desc, st));
+        GNS_TRY(sort_range(dk + nl, hv ? dv + nl : nullptr, dk, dv, nr, false, corank, desc, st));
+        return top_merge(keys, vals, bk, bv, lo, len, nl, corank, deps, flags, desc, st);
     }
-    GNS_TRY(sort_limited(keys, vals, lo + b, len - b, b, bk, bv, corank, deps, flags, st, sc, n));
+    GNS_TRY(sort_limited(keys, vals, lo + b, len - b, b, bk, bv, corank, deps, flags, desc, st, sc, n));
     if (sc) {
         count_sort_range(b, sc, n);
         sc->elem_passes += (double)len / (double)n;
         sc->launches += 3;
         return GNS_OK;
     }
-    GNS_TRY(sort_range(dk, dv, bk, bv, b, true, corank, st));
-    return top_merge(keys, vals, bk, bv, lo, len, b, corank, deps, flags, st);
+    GNS_TRY(sort_range(dk, dv, bk, bv, b, true, corank, desc, st));
+    return top_merge(keys, vals, bk, bv, lo, len, b, corank, deps, flags, desc, st);
 }
 
 // The sort proper (rows a1..a7).  ws already validated and sized.
-gns_status run_sort(double *keys, uint32_t *vals, size_t n, const Mode &m, unsigned char *ws, cudaStream_t st)
+// target: 0 AscLeft, 1 AscRight, 2 DescLeft, 3 DescRight (NEXT f3).
+// AscRight = reverse(DescLeft), DescRight = reverse(AscLeft).
+gns_status run_sort(double *keys, uint32_t *vals, size_t n, const Mode &m, unsigned char *ws, int target,
+                    cudaStream_t st)
 {
     if (n <= 1) return GNS_OK;
     GNS_TRY(ensure_attrs());
     const bool hv = vals != nullptr;
-    if (n <= (size_t)TILE)   // one tile: in place, no buffer
-        return launch_tile_sort(keys, vals, keys, vals, n, st);
-    const Layout Lo = layout(n, m, hv);
-    double *bk = reinterpret_cast<double *>(ws + Lo.off_k);
-    uint32_t *bv = hv ? reinterpret_cast<uint32_t *>(ws + Lo.off_v) : nullptr;
-    int *corank = reinterpret_cast<int *>(ws + Lo.off_corank);
-    if (!m.limited) return sort_range(keys, vals, bk, bv, n, false, corank, st);
-    int2 *deps = reinterpret_cast<int2 *>(ws + Lo.off_deps);
-    unsigned *flags = reinterpret_cast<unsigned *>(ws + Lo.off_flags);
-    return sort_limited(keys, vals, 0, n, m.buf, bk, bv, corank, deps, flags, st, nullptr, n);
+    const bool right = target == 1 || target == 3;
+    const bool desc = (target == 2) || (target == 1);   // AscRight is reverse(DescLeft)
+    if (n <= (size_t)TILE) {   // one tile: in place, no buffer
+        GNS_TRY(launch_tile_sort(keys, vals, keys, vals, n, desc, st));
+    } else {
+        const Layout Lo = layout(n, m, hv);
+        double *bk = reinterpret_cast<double *>(ws + Lo.off_k);
+        uint32_t *bv = hv ? reinterpret_cast<uint32_t *>(ws + Lo.off_v) : nullptr;
+        int *corank = reinterpret_cast<int *>(ws + Lo.off_corank);
+        if (!m.limited) {
+            GNS_TRY(sort_range(keys, vals, bk, bv, n, false, corank, desc, st));
+        } else {
+            int2 *deps = reinterpret_cast<int2 *>(ws + Lo.off_deps);
+            unsigned *flags = reinterpret_cast<unsigned *>(ws + Lo.off_flags);
+            GNS_TRY(sort_limited(keys, vals, 0, n, m.buf, bk, bv, corank, deps, flags, desc, st, nullptr, n));
+        }
+    }
+    if (right) GNS_TRY(launch_reverse(keys, vals, n, st));
+    return GNS_OK;
 }
 
-gns_status sort_alloc(double *keys, uint32_t *vals, bool hv, size_t n, double frac, cudaStream_t st)
+gns_status sort_alloc(double *keys, uint32_t *vals, bool hv, size_t n, double frac, int target, cudaStream_t st)
 {
     Mode m;
     GNS_TRY(mode_for(frac, n, &m));
@@ -455,7 +473,7 @@ gns_status sort_alloc(double *keys, uint32_t *vals, bool hv, size_t n, double fr
             return check(e, "cudaMallocAsync");
         }
     }
-    gns_status s = run_sort(keys, hv ? vals : nullptr, n, m, ws, st);
+    gns_status s = run_sort(keys, hv ? vals : nullptr, n, m, ws, target, st);
     if (ws) {
         gns_status f = check(cudaFreeAsync(ws, st), "cudaFreeAsync");
         if (s == GNS_OK) s = f;
@@ -464,7 +482,7 @@ gns_status sort_alloc(double *keys, uint32_t *vals, bool hv, size_t n, double fr
 }
 
 gns_status sort_ws(double *keys, uint32_t *vals, bool hv, size_t n, double frac, void *ws, size_t ws_bytes,
-                   cudaStream_t st)
+                   int target, cudaStream_t st)
 {
     Mode m;
     GNS_TRY(mode_for(frac, n, &m));
@@ -475,7 +493,7 @@ gns_status sort_ws(double *keys, uint32_t *vals, bool hv, size_t n, double frac,
         if (!ws || ws_bytes < Lo.total) return fail(GNS_ERR_WORKSPACE_TOO_SMALL, "workspace too small");
         if (!is_aligned(ws, 32)) return fail(GNS_ERR_MISALIGNED, "ws must be 32-byte aligned");
     }
-    return run_sort(keys, hv ? vals : nullptr, n, m, (unsigned char *)ws, st);
+    return run_sort(keys, hv ? vals : nullptr, n, m, (unsigned char *)ws, target, st);
 }
 
 }  // namespace
@@ -485,13 +503,13 @@ extern "C" {
 
 gns_status gns_sort_f64(double *keys, size_t n, double buffer_fraction, gns_stream_t stream)
 {
-    return sort_alloc(keys, nullptr, false, n, buffer_fraction, (cudaStream_t)stream);
+    return sort_alloc(keys, nullptr, false, n, buffer_fraction, 0, (cudaStream_t)stream);
 }
 
 gns_status gns_sort_pairs_f64_u32(double *keys, uint32_t *vals, size_t n, double buffer_fraction,
                                   gns_stream_t stream)
 {
-    return sort_alloc(keys, vals, true, n, buffer_fraction, (cudaStream_t)stream);
+    return sort_alloc(keys, vals, true, n, buffer_fraction, 0, (cudaStream_t)stream);
 }
 
 size_t gns_workspace_bytes(size_t n, double buffer_fraction, int with_vals)
@@ -504,13 +522,22 @@ size_t gns_workspace_bytes(size_t n, double buffer_fraction, int with_vals)
 gns_status gns_sort_f64_ws(double *keys, size_t n, double buffer_fraction, void *ws, size_t ws_bytes,
                            gns_stream_t stream)
 {
-    return sort_ws(keys, nullptr, false, n, buffer_fraction, ws, ws_bytes, (cudaStream_t)stream);
+    return sort_ws(keys, nullptr, false, n, buffer_fraction, ws, ws_bytes, 0, (cudaStream_t)stream);
 }
 
 gns_status gns_sort_pairs_f64_u32_ws(double *keys, uint32_t *vals, size_t n, double buffer_fraction,
                                      void *ws, size_t ws_bytes, gns_stream_t stream)
 {
-    return sort_ws(keys, vals, true, n, buffer_fraction, ws, ws_bytes, (cudaStream_t)stream);
+    return sort_ws(keys, vals, true, n, buffer_fraction, ws, ws_bytes, 0, (cudaStream_t)stream);
+}
+
+gns_status gns_sort_target_f64(double *keys, uint32_t *vals, size_t n, double buffer_fraction, gns_target target,
+                               void *ws, size_t ws_bytes, gns_stream_t stream)
+{
+    if ((int)target < 0 || (int)target > 3) return fail(GNS_ERR_INVALID_ARGUMENT, "target must be 0..3");
+    if (ws) return sort_ws(keys, vals, vals != nullptr, n, buffer_fraction, ws, ws_bytes, (int)target,
+                           (cudaStream_t)stream);
+    return sort_alloc(keys, vals, vals != nullptr, n, buffer_fraction, (int)target, (cudaStream_t)stream);
 }
 
 gns_status gns_plan(size_t n, double buffer_fraction, int with_vals, gns_plan_info *out)
@@ -531,7 +558,7 @@ gns_status gns_plan(size_t n, double buffer_fraction, int with_vals, gns_plan_in
     } else if (n <= (size_t)TILE || !m.limited) {
         count_sort_range(n, &sc, n);
     } else {
-        sort_limited(nullptr, nullptr, 0, n, m.buf, nullptr, nullptr, nullptr, nullptr, nullptr, 0, &sc, n);
+        sort_limited(nullptr, nullptr, 0, n, m.buf, nullptr, nullptr, nullptr, nullptr, nullptr, false, 0, &sc, n);
     }
     out->element_passes = sc.elem_passes;
     out->launches = sc.launches;
@@ -552,7 +579,7 @@ gns_status gns_tile_sort(const double *src_keys, const uint32_t *src_vals, doubl
     GNS_TRY(validate_data(dst_keys, dst_vals, hv, n));
     if (n == 0) return GNS_OK;
     GNS_TRY(ensure_attrs());
-    return launch_tile_sort(src_keys, src_vals, dst_keys, dst_vals, n, (cudaStream_t)stream);
+    return launch_tile_sort(src_keys, src_vals, dst_keys, dst_vals, n, false, (cudaStream_t)stream);
 }
 
 size_t gns_merge_workspace_bytes(size_t n) { return merge_ws(n); }
@@ -571,7 +598,7 @@ gns_status gns_merge_pass(const double *src_keys, const uint32_t *src_vals, doub
     if (!ws || ws_bytes < merge_ws(n)) return fail(GNS_ERR_WORKSPACE_TOO_SMALL, "workspace too small");
     GNS_TRY(ensure_attrs());
     MergeGeo g = uniform_geo(src_keys, src_vals, dst_keys, dst_vals, n, run_len);
-    return launch_merge(g, src_keys + n, src_keys + n, (int *)ws, nullptr, nullptr, false, (cudaStream_t)stream);
+    return launch_merge(g, src_keys + n, src_keys + n, (int *)ws, nullptr, nullptr, false, false, (cudaStream_t)stream);
 }
 
 gns_status gns_merge_inplace_top(double *keys, uint32_t *vals, const double *left_keys,
@@ -601,7 +628,7 @@ gns_status gns_merge_inplace_top(double *keys, uint32_t *vals, const double *lef
     g.n = (long long)n;
     g.L = (long long)nl;
     g.single = 1;
-    return launch_merge(g, left_keys + nl, keys + n, corank, deps, flags, true, (cudaStream_t)stream);
+    return launch_merge(g, left_keys + nl, keys + n, corank, deps, flags, true, false, (cudaStream_t)stream);
 }
 
 int gns_tile_elems(void) { return TILE; }

@@ -164,17 +164,24 @@ __device__ __forceinline__ void store_segment(double *ok, uint32_t *ov, long lon
 }
 
 // ------------------------------------------------------------ merge device code
+// Key order of the sort target: ascending (AscLeft) or
+// descending (DescLeft); ties always keep input order (the left run wins).
+// The *Right targets are the reversal of the opposite-direction Left target
+// (gns.cu).  before<DESC>(x, y): x must be output strictly before y.
+template <bool DESC>
+__device__ __forceinline__ bool before(double x, double y) { return DESC ? (x > y) : (x < y); }
+
 // Stable co-rank (merge path) of diagonal d for sorted runs A[0:na), B[0:nb)
 // in shared memory: the number of A elements among the first d outputs of the
 // stable merge in which A (the left run) wins ties (Knuth's merge;
 // SPEC.md:290).  Predicate: A[m] <= B[d-1-m]  =>  the m-th A element precedes.
-template <class IX>
+template <bool DESC, class IX>
 __device__ __forceinline__ int merge_path_smem(const double *s, int a0, int na, int b0, int nb, int d, IX ix)
 {
     int lo = max(0, d - nb), hi = min(d, na);
     while (lo < hi) {
         int m = (lo + hi) >> 1;
-        if (s[ix(a0 + m)] <= s[ix(b0 + d - 1 - m)]) lo = m + 1;
+        if (!before<DESC>(s[ix(b0 + d - 1 - m)], s[ix(a0 + m)])) lo = m + 1;
         else hi = m;
     }
     return lo;
@@ -184,7 +191,7 @@ __device__ __forceinline__ int merge_path_smem(const double *s, int a0, int na, 
 // index bi (ends aend/bend, exclusive).  B's head is taken only if strictly
 // smaller than A's (left wins ties).  Reads one slot past a run end at most
 // (the shared arrays carry spare slots; the value is never used).
-template <bool HV, class IK, class IV>
+template <bool HV, bool DESC, class IK, class IV>
 __device__ __forceinline__ void serial_merge(const double *sk, const uint32_t *sv, int ai, int aend,
                                              int bi, int bend, double (&k)[VT], uint32_t (&v)[VT],
                                              IK ik, IV iv)
@@ -192,7 +199,7 @@ __device__ __forceinline__ void serial_merge(const double *sk, const uint32_t *s
     double ka = sk[ik(ai)], kb = sk[ik(bi)];
 #pragma unroll
     for (int x = 0; x < VT; ++x) {
-        const bool p = (bi < bend) && ((ai >= aend) || (kb < ka));
+        const bool p = (bi < bend) && ((ai >= aend) || before<DESC>(kb, ka));
         k[x] = p ? kb : ka;
         const int src = p ? bi : ai;
         if (HV) v[x] = sv[iv(src)];
@@ -254,6 +261,7 @@ __device__ __forceinline__ TileSpan tile_span(const MergeGeo &g, int t)
 // "parallelize over an arbitrary number of processes".
 // Warp-cooperative stable co-rank of tile t's first diagonal (all 32 lanes
 // return the result).
+template <bool DESC>
 __device__ __forceinline__ int warp_corank(const MergeGeo &g, int t, int lane)
 {
     const TileSpan s = tile_span(g, t);
@@ -272,7 +280,7 @@ __device__ __forceinline__ int warp_corank(const MergeGeo &g, int t, int lane)
             nprobe = 32;
         }
         bool p = false;
-        if (lane < nprobe) p = A[m] <= B[d - 1 - m];
+        if (lane < nprobe) p = !before<DESC>(B[d - 1 - m], A[m]);
         const unsigned bal = __ballot_sync(0xFFFFFFFFu, p);
         const int c = __popc(bal);
         const int m_prev = __shfl_sync(0xFFFFFFFFu, m, (c > 0 ? c - 1 : 0));
@@ -287,7 +295,7 @@ __device__ __forceinline__ int warp_corank(const MergeGeo &g, int t, int lane)
 
 // Co-rank search by a group of W lanes (W = 16: two independent searches per
 // warp, (W+1)-ary).  `gl` = lane within the group; `mask` = the group's lanes.
-template <int W>
+template <int W, bool DESC>
 __device__ __forceinline__ int group_corank(const MergeGeo &g, int t, int gl, unsigned mask, int gbase)
 {
     const TileSpan s = tile_span(g, t);
@@ -308,7 +316,7 @@ __device__ __forceinline__ int group_corank(const MergeGeo &g, int t, int gl, un
             nprobe = W;
         }
         bool p = false;
-        if (gl < nprobe) p = A[m] <= B[d - 1 - m];
+        if (gl < nprobe) p = !before<DESC>(B[d - 1 - m], A[m]);
         const unsigned bal = (__ballot_sync(mask, p) & mask) >> gbase;
         const int c = __popc(bal);
         const int m_prev = __shfl_sync(mask, m, gbase + (c > 0 ? c - 1 : 0));
@@ -321,6 +329,7 @@ __device__ __forceinline__ int group_corank(const MergeGeo &g, int t, int gl, un
     return lo;
 }
 
+template <bool DESC>
 __global__ void __launch_bounds__(256)
 partition_kernel(MergeGeo g, int ntiles, int *__restrict__ corank)
 {
@@ -329,7 +338,7 @@ partition_kernel(MergeGeo g, int ntiles, int *__restrict__ corank)
     const int warp = (int)((blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5);
     const int lane = threadIdx.x & 31;
     if (warp >= ntiles) return;
-    const int c = warp_corank(g, warp, lane);
+    const int c = warp_corank<DESC>(g, warp, lane);
     if (lane == 0) corank[warp] = c;
 }
 
@@ -511,7 +520,7 @@ constexpr size_t TS_VAL_BYTES = ((MTILE + 128) * 4 + 1023) / 1024 * 1024;
 constexpr size_t ts_stage_bytes(bool hv) { return TS_KEY_SLOTS * 8 + (hv ? TS_VAL_BYTES : 0); }
 constexpr size_t ts_smem(bool hv) { return 2 * ts_stage_bytes(hv) + 1024; }
 
-template <bool HV>
+template <bool HV, bool DESC>
 __global__ void __launch_bounds__(FUSED_THREADS, 2)
 merge_tstore_kernel(PipeGeo pg, int ntiles, int per_cta, const __grid_constant__ CUtensorMap omap)
 {
@@ -540,7 +549,7 @@ merge_tstore_kernel(PipeGeo pg, int ntiles, int per_cta, const __grid_constant__
     __syncthreads();
     const int init = min(nspl, FUSED_THREADS / 32);
     if (warp < init) {
-        const int c = warp_corank(pg.g, first + warp, lane);
+        const int c = warp_corank<DESC>(pg.g, first + warp, lane);
         if (lane == 0) {
             spl[warp] = c;
             spl_tag[warp] = warp;
@@ -563,7 +572,7 @@ merge_tstore_kernel(PipeGeo pg, int ntiles, int per_cta, const __grid_constant__
             const int j = j0 + h;
             while (j0 + 1 - spl_used >= SPL_RING) { __nanosleep(64); }
             if (j < nspl) {
-                const int c = group_corank<16>(pg.g, first + j, gl, mask, 16 * h);
+                const int c = group_corank<16, DESC>(pg.g, first + j, gl, mask, 16 * h);
                 if (gl == 0) {
                     spl[j % SPL_RING] = c;
                     __threadfence_block();
@@ -601,9 +610,9 @@ merge_tstore_kernel(PipeGeo pg, int ntiles, int per_cta, const __grid_constant__
         const uint32_t *sv = svb(st);
         double k[VT];
         uint32_t v[VT];
-        const int ii = merge_path_smem(sk, mt.offa, mt.ca, mt.bslot, mt.cb, d, Lin());
-        serial_merge<HV>(sk, sv, mt.offa + ii, mt.offa + mt.ca, mt.bslot + d - ii, mt.bslot + mt.cb, k, v, Lin(),
-                         Lin());
+        const int ii = merge_path_smem<DESC>(sk, mt.offa, mt.ca, mt.bslot, mt.cb, d, Lin());
+        serial_merge<HV, DESC>(sk, sv, mt.offa + ii, mt.offa + mt.ca, mt.bslot + d - ii, mt.bslot + mt.cb, k, v,
+                               Lin(), Lin());
         const long long t = first + i;
         const long long row = t * (MTILE / 16) + tid;    // global row of this thread's 16 outputs
         bar_merge_warps();                               // stage st fully read
@@ -669,14 +678,14 @@ __device__ __forceinline__ int tv_slot(int e)     // u32, 32 per row
     return (r << 5) | ((((e >> 2) & 7) ^ (r & 7)) << 2) | (e & 3);
 }
 
-template <int O, bool HV>
+template <int O, bool HV, bool DESC>
 __device__ __forceinline__ void transpose_sort16(double (&k)[VT1], uint32_t (&v)[VT1])
 {
 #pragma unroll
     for (int r = 0; r < 16; ++r) {
 #pragma unroll
         for (int i = r & 1; i + 1 < 16; i += 2) {
-            const bool p = k[O + i + 1] < k[O + i];
+            const bool p = before<DESC>(k[O + i + 1], k[O + i]);
             const double lo = p ? k[O + i + 1] : k[O + i];
             const double hi = p ? k[O + i] : k[O + i + 1];
             k[O + i] = lo;
@@ -691,14 +700,14 @@ __device__ __forceinline__ void transpose_sort16(double (&k)[VT1], uint32_t (&v)
     }
 }
 
-template <bool HV>
+template <bool HV, bool DESC>
 __device__ __forceinline__ void serial_merge32(const double *sk, const uint32_t *sv, int ai, int aend, int bi, int bend,
                                                double (&k)[VT1], uint32_t (&v)[VT1])
 {
     double ka = sk[swm(ai)], kb = sk[swm(bi)];
 #pragma unroll
     for (int x = 0; x < VT1; ++x) {
-        const bool p = (bi < bend) && ((ai >= aend) || (kb < ka));
+        const bool p = (bi < bend) && ((ai >= aend) || before<DESC>(kb, ka));
         k[x] = p ? kb : ka;
         const int src = p ? bi : ai;
         if (HV) v[x] = sv[swmv(src)];
@@ -709,7 +718,7 @@ __device__ __forceinline__ void serial_merge32(const double *sk, const uint32_t 
     }
 }
 
-template <bool HV>
+template <bool HV, bool DESC>
 __global__ void __launch_bounds__(NT1, 2)
 tile_sort2_kernel(const double *src_k, const uint32_t *src_v, double *dst_k, uint32_t *dst_v, long long n,
                   const __grid_constant__ CUtensorMap ksrc, const __grid_constant__ CUtensorMap vsrc,
@@ -754,12 +763,15 @@ tile_sort2_kernel(const double *src_k, const uint32_t *src_v, double *dst_k, uin
         for (int x = 0; x < VT1; ++x) {
             const int e = tid * VT1 + x;
             const bool ok = e < cnt;
-            k[x] = ok ? src_k[base + e] : __longlong_as_double(0x7FF0000000000000LL);
+            // pads sort after every real key (+inf ascending, -inf descending;
+            // real infinities come first among ties because pads are last)
+            k[x] = ok ? src_k[base + e] : __longlong_as_double(DESC ? (long long)0xFFF0000000000000ULL
+                                                                    : 0x7FF0000000000000LL);
             if (HV) v[x] = ok ? src_v[base + e] : 0u;
         }
     }
-    transpose_sort16<0, HV>(k, v);
-    transpose_sort16<16, HV>(k, v);
+    transpose_sort16<0, HV, DESC>(k, v);
+    transpose_sort16<16, HV, DESC>(k, v);
     const int e0 = tid * VT1;
     __syncthreads();                       // the TMA-layout reads are done before the first spill
 #pragma unroll 1
@@ -771,15 +783,15 @@ tile_sort2_kernel(const double *src_k, const uint32_t *src_v, double *dst_k, uin
         }
         __syncthreads();
         if (coop == 1) {                   // merge the thread's own two sorted halves
-            serial_merge32<HV>(sk, sv, e0, e0 + 16, e0 + 16, e0 + 32, k, v);
+            serial_merge32<HV, DESC>(sk, sv, e0, e0 + 16, e0 + 16, e0 + 32, k, v);
         } else {
             const int local = tid & (coop - 1);
             const int a0 = (tid - local) * VT1;
             const int run = (coop >> 1) * VT1;
             const int b0 = a0 + run;
             const int d = local * VT1;
-            const int i = merge_path_smem(sk, a0, run, b0, run, d, SwM());
-            serial_merge32<HV>(sk, sv, a0 + i, b0, b0 + d - i, b0 + run, k, v);
+            const int i = merge_path_smem<DESC>(sk, a0, run, b0, run, d, SwM());
+            serial_merge32<HV, DESC>(sk, sv, a0 + i, b0, b0 + d - i, b0 + run, k, v);
         }
         __syncthreads();
     }
@@ -827,7 +839,7 @@ tile_sort2_kernel(const double *src_k, const uint32_t *src_v, double *dst_k, uin
 // range intersects its write range (deps[], inplace_deps_kernel).  Later tiles
 // never intersect: k1(t) <= nl + j1(t) <= nl + j0(u) for u > t.  Deadlock-free:
 // the smallest tile in flight only depends on tiles whose loads have landed.
-template <bool HV>
+template <bool HV, bool DESC>
 __global__ void __launch_bounds__(NT, 2)
 merge_inplace_kernel(PipeGeo pg, int ntiles, const int *__restrict__ corank, const int2 *__restrict__ deps,
                      unsigned *flags, unsigned *ticket, const __grid_constant__ CUtensorMap omap)
@@ -882,9 +894,9 @@ merge_inplace_kernel(PipeGeo pg, int ntiles, const int *__restrict__ corank, con
         const uint32_t *sv = svb(st);
         double k[VT];
         uint32_t v[VT];
-        const int ii = merge_path_smem(sk, mt.offa, mt.ca, mt.bslot, mt.cb, d, Lin());
-        serial_merge<HV>(sk, sv, mt.offa + ii, mt.offa + mt.ca, mt.bslot + d - ii, mt.bslot + mt.cb, k, v, Lin(),
-                         Lin());
+        const int ii = merge_path_smem<DESC>(sk, mt.offa, mt.ca, mt.bslot, mt.cb, d, Lin());
+        serial_merge<HV, DESC>(sk, sv, mt.offa + ii, mt.offa + mt.ca, mt.bslot + d - ii, mt.bslot + mt.cb, k, v,
+                               Lin(), Lin());
         const long long row = (long long)tcur * (MTILE / 16) + tid;
         __syncthreads();                                       // stage st fully read
         unsigned char *rowp = reinterpret_cast<unsigned char *>(sk) + tid * 128;
@@ -931,6 +943,32 @@ merge_inplace_kernel(PipeGeo pg, int ntiles, const int *__restrict__ corank, con
         tnext = s_next;
     }
     if (tid == 0) bulk_wait0();
+    pdl_trigger();
+}
+
+
+// ------------------------------------- target reversal (NEXT f3, AscRight/DescRight)
+// AscRight = reverse(DescLeft), DescRight = reverse(AscLeft) (PAPER.md:137-142:
+// the Right targets are the Left targets read from the other end of memory).
+// In place: thread pairs element i with n-1-i; both ranges are read coalesced.
+template <bool HV>
+__global__ void __launch_bounds__(256)
+reverse_kernel(double *k, uint32_t *v, long long n)
+{
+    pdl_wait();
+    const long long half = n >> 1;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < half;
+         i += (long long)gridDim.x * blockDim.x) {
+        const long long j = n - 1 - i;
+        const double a = k[i], b = k[j];
+        k[i] = b;
+        k[j] = a;
+        if (HV) {
+            const uint32_t x = v[i], y = v[j];
+            v[i] = y;
+            v[j] = x;
+        }
+    }
     pdl_trigger();
 }
 

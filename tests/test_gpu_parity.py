@@ -86,6 +86,27 @@ def test_limited_buffer_fractions(gns, n, frac):
     check_against_oracle(gns, synth.uniform(n, 700 + n), None, frac, what=f"n={n} p={frac} key-only")
 
 
+@pytest.mark.parametrize("target", ["AscRight", "DescLeft", "DescRight"])
+@pytest.mark.parametrize("frac", [1.0, 0.5, 0.25])
+@pytest.mark.parametrize("n", [1, 1000, T1, 3 * T1 + 5, 100003])
+def test_targets(gns, n, frac, target):
+    """NEXT f3: the other three API targets, vs the oracle."""
+    k = synth.ties(n, 900 + n, 13)
+    k[::4] *= -1.0
+    k[::11] = np.inf
+    k[::13] = -np.inf
+    v = synth.iota_u32(n)
+    tk, tv = to_dev(k, v)
+    gns.sort_(tk, tv, frac, target=target)
+    torch.cuda.synchronize()
+    ek, ev = oracle.sort_target(k, v, target)
+    assert_bitexact(tk.cpu().numpy(), ek, tv.cpu().numpy(), ev, what=f"{target} n={n} p={frac}")
+    tk, _ = to_dev(k, None)
+    gns.sort_(tk, None, frac, target=target)
+    torch.cuda.synchronize()
+    assert_bitexact(tk.cpu().numpy(), ek, what=f"{target} key-only n={n}")
+
+
 def test_specials_inf_zero(gns):
     n = 3 * T + 5
     rng = np.random.default_rng(5)
@@ -220,7 +241,7 @@ def test_error_paths_leave_data_untouched(gns):
     k = synth.uniform(n, 1)
     tk, _ = to_dev(k, None)
     before = tk.clone()
-    assert gns.gns_sort_f64(int(tk.data_ptr()), n, 0.3, 0) == 2
+    assert gns.gns_sort_f64(int(tk.data_ptr()), n, 0.7, 0) == 2
     assert gns.gns_sort_f64(int(tk.data_ptr()) + 8, n - 1, 1.0, 0) == 6
     assert gns.gns_sort_f64_ws(int(tk.data_ptr()), n, 1.0, 0, 0, 0) == 5
     assert gns.gns_sort_f64_ws(int(tk.data_ptr()), n, 1.0, 256, 64, 0) == 5

@@ -189,3 +189,62 @@ def test_oracle_sort_equals_repeated_merge_levels():
         L *= 2
     ek, et = oracle.sort(keys, tags)
     assert_bitexact(k, ek, t, et)
+
+
+# ------------------------------------------------------------ NEXT f3: targets
+
+def brute_target(keys, tags, target):
+    """Insertion sort on the composite order the target defines:
+    AscLeft (k, i), AscRight (k, -i), DescLeft (-k, i), DescRight (-k, -i);
+    IEEE comparisons on k (so -0.0 == +0.0)."""
+    desc = target.startswith("Desc")
+    right = target.endswith("Right")
+
+    def before(a, b):     # a = (k, i) strictly precedes b
+        ka, ia = a
+        kb, ib = b
+        if (kb < ka) if desc else (ka < kb):
+            return True
+        if ka == kb:
+            return ia > ib if right else ia < ib
+        return False
+    a = list(zip(keys, tags))
+    for i in range(1, len(a)):
+        x = a[i]
+        j = i
+        while j > 0 and before(x, a[j - 1]):
+            a[j] = a[j - 1]
+            j -= 1
+        a[j] = x
+    return [k for k, _ in a], [t for _, t in a]
+
+
+@pytest.mark.parametrize("target", ["AscLeft", "AscRight", "DescLeft", "DescRight"])
+def test_targets_exhaustive_vs_brute_force(target):
+    for alphabet in ((0.0, 1.0, 2.0), (-0.0, 0.0, 1.0)):
+        for n in range(0, 7):
+            for seq in itertools.product(alphabet, repeat=n):
+                keys = np.array(seq, dtype=np.float64)
+                tags = np.arange(n, dtype=np.uint32)
+                ek, et = brute_target(list(keys), list(tags), target)
+                gk, gt = oracle.sort_target(keys, tags, target)
+                assert_bitexact(gk, np.array(ek, dtype=np.float64), gt, np.array(et, dtype=np.uint32),
+                                what=f"{target} {seq}")
+
+
+def test_targets_relations_and_golden():
+    rng = np.random.default_rng(3)
+    keys = rng.integers(0, 5, 3000).astype(np.float64)
+    tags = np.arange(3000, dtype=np.uint32)
+    al = oracle.sort_target(keys, tags, "AscLeft")
+    assert_bitexact(al[0], oracle.sort(keys, tags)[0], al[1], oracle.sort(keys, tags)[1])
+    for a, b in (("AscRight", "DescLeft"), ("DescRight", "AscLeft")):
+        ka, ta = oracle.sort_target(keys, tags, a)
+        kb, tb = oracle.sort_target(keys, tags, b)
+        assert_bitexact(ka, kb[::-1].copy(), ta, tb[::-1].copy(), what=f"{a} == reverse({b})")
+    with open(os.path.join(GOLDEN, "spec_examples.json")) as f:
+        g = json.load(f)
+    for ex in g["targets"]:
+        gk, gt = oracle.sort_target(np.array(ex["keys"], dtype=np.float64),
+                                    np.array(ex["tags"], dtype=np.uint32), ex["target"])
+        assert list(gk) == ex["out_keys"] and list(gt) == ex["out_tags"], ex["cite"]
