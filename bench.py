@@ -282,8 +282,10 @@ def main():
     e2e = end_to_end(gns, torch, dev, stream, case, args, n, hv, ws)
 
     footprint = None
+    presorted = None
     if rank == 0 and world == 1 and not args.no_footprint and args.config == 2:
         footprint = footprint_cfg5(gns, torch, dev, stream, flush)
+        presorted = config4(gns, torch, dev, stream, flush)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -316,6 +318,8 @@ def main():
         line["cpu_baseline"] = cpu
     if footprint:
         line["footprint_cfg5"] = footprint
+    if presorted:
+        line["presorted_cfg4"] = presorted
     if rank == 0:
         print(json.dumps(line), flush=True)
     if pg:
@@ -458,6 +462,33 @@ def footprint_cfg5(gns, torch, dev, stream, flush, reps=3):
     out["tfootprint_0.5_lt_1.0"] = out["0.5"]["tfootprint_ms"] < out["1.0"]["tfootprint_ms"]
     out["argmin_tfootprint_fraction"] = min((f for f in out if f.replace(".", "").isdigit()),
                                             key=lambda f: out[f]["tfootprint_ms"])
+    return out
+
+
+def config4(gns, torch, dev, stream, flush, reps=5):
+    """configs[3]: n = 2^24 presorted patterns, key-only, buffer 1.0.  Fully
+    ordered input takes the NEXT-f2 omission path (no merge pass moves data);
+    the others sort normally."""
+    out = {}
+    n = 1 << 24
+    ws = gns.alloc_workspace(n, 1.0, False, dev)
+    for sub in synth.CONFIG4_SUBS:
+        src = torch.from_numpy(synth.config(4, sub).keys).to(dev)
+        k = torch.empty_like(src)
+        ts = []
+        for i in range(reps + 1):
+            k.copy_(src)
+            flush.fill_(1)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            gns.sort_(k, None, 1.0, workspace=ws)
+            b.record(stream)
+            torch.cuda.synchronize()
+            if i:
+                ts.append(a.elapsed_time(b))
+        ok = bool((k[1:] >= k[:-1]).all().item())
+        ms = float(np.median(ts))
+        out[sub] = {"ms": ms, "keys_per_s": n / (ms / 1e3), "sorted": ok}
     return out
 
 

@@ -67,7 +67,7 @@ bool is_aligned(const void *p, size_t a) { return ((uintptr_t)p % a) == 0; }
 // Workspace layout (one allocation = the whole bufferRAM of a call).
 struct Layout {
     size_t buf_elems = 0;   // buffer key(+val) slots
-    size_t off_k = 0, off_v = 0, off_corank = 0, off_deps = 0, off_flags = 0, total = 0;
+    size_t off_k = 0, off_v = 0, off_corank = 0, off_deps = 0, off_flags = 0, off_adapt = 0, total = 0;
     int ntiles = 0;         // merge tiles over the whole array
 };
 
@@ -96,6 +96,8 @@ Layout layout(size_t n, const Mode &m, bool hv)
     if (m.limited) o = align_up(o + (size_t)L.ntiles * sizeof(int2), 256);
     L.off_flags = o;
     if (m.limited) o = align_up(o + (size_t)(L.ntiles + 1) * sizeof(unsigned), 256);
+    L.off_adapt = o;                   // the "input not presorted" word (NEXT f2)
+    o = align_up(o + sizeof(unsigned), 256);
     L.total = o;
     return L;
 }
@@ -215,7 +217,7 @@ gns_status launch_pdl(const char *what, void (*kern)(KArgs...), dim3 grid, dim3 
 
 // Row a2 (K1).
 gns_status launch_tile_sort(const double *sk, const uint32_t *sv, double *dk, uint32_t *dv, size_t n, bool desc,
-                            cudaStream_t st)
+                            cudaStream_t st, unsigned *unsorted = nullptr)
 {
     if (n == 0) return GNS_OK;
     const unsigned grid = (unsigned)ceil_div(n, TILE);
@@ -235,13 +237,14 @@ gns_status launch_tile_sort(const double *sk, const uint32_t *sv, double *dk, ui
     auto kern = hv ? (desc ? tile_sort2_kernel<true, true> : tile_sort2_kernel<true, false>)
                    : (desc ? tile_sort2_kernel<false, true> : tile_sort2_kernel<false, false>);
     return launch_pdl("tile_sort2_kernel", kern, grid, NT1, t1_smem(hv), st, sk, svv, dk, dvv, (long long)n, m[0],
-                      m[1], m[2], m[3]);
+                      m[1], m[2], m[3], unsorted);
 }
 
 // Rows a3+a4 (fused K2+K3, persistent TMA pipeline) or, in place, a6 (K2 +
 // dependency ranges + K4 with the ticket/flag protocol).
 gns_status launch_merge(const MergeGeo &g, const double *lim_a, const double *lim_b, int *corank, int2 *deps,
-                        unsigned *flags, bool inplace, bool desc, cudaStream_t st)
+                        unsigned *flags, bool inplace, bool desc, cudaStream_t st, const unsigned *unsorted = nullptr,
+                        const double *copy_k = nullptr, const uint32_t *copy_v = nullptr)
 {
     const int ntiles = (int)ceil_div((size_t)g.n, MTILE);
     const bool hv = g.av != nullptr;
@@ -257,7 +260,8 @@ gns_status launch_merge(const MergeGeo &g, const double *lim_a, const double *li
         const int grid = (int)ceil_div(ntiles, per);
         auto kern = hv ? (desc ? merge_tstore_kernel<true, true> : merge_tstore_kernel<true, false>)
                        : (desc ? merge_tstore_kernel<false, true> : merge_tstore_kernel<false, false>);
-        return launch_pdl("merge_tstore_kernel", kern, grid, FUSED_THREADS, ts_smem(hv), st, pg, ntiles, per, map);
+        return launch_pdl("merge_tstore_kernel", kern, grid, FUSED_THREADS, ts_smem(hv), st, pg, ntiles, per, map,
+                          unsorted, copy_k, copy_v);
     }
     GNS_TRY(launch_pdl("partition_kernel", desc ? partition_kernel<true> : partition_kernel<false>,
                        (unsigned)ceil_div((size_t)ntiles * 32, 256), 256, 0, st, g, ntiles, corank));
@@ -300,7 +304,7 @@ MergeGeo uniform_geo(const double *sk, const uint32_t *sv, double *dk, uint32_t 
 // `final_in_partner`, else in R.  Parity picks the tile-sort destination so
 // no copy pass is ever needed (an odd number of merge levels starts from P).
 gns_status sort_range(double *rk, uint32_t *rv, double *pk_, uint32_t *pv_, size_t len,
-                      bool final_in_partner, int *corank, bool desc, cudaStream_t st)
+                      bool final_in_partner, int *corank, bool desc, cudaStream_t st, unsigned *unsorted = nullptr)
 {
     if (len == 0) return GNS_OK;
     const int M = merge_passes_for(len);
@@ -309,11 +313,19 @@ gns_status sort_range(double *rk, uint32_t *rv, double *pk_, uint32_t *pv_, size
     uint32_t *cv = tile_to_partner ? pv_ : rv;
     double *ok = tile_to_partner ? rk : pk_;
     uint32_t *ov = tile_to_partner ? rv : pv_;
-    GNS_TRY(launch_tile_sort(rk, rv, ck, cv, len, desc, st));
+    double *tile_k = ck;
+    uint32_t *tile_v = cv;
+    // NEXT f2: with `unsorted` the tile sort also tests whether the input is
+    // already in order; if it is, every merge pass is omitted on the device.
+    if (unsorted && M > 0) GNS_TRY(check(cudaMemsetAsync(unsorted, 0, sizeof(unsigned), st), "memset"));
+    GNS_TRY(launch_tile_sort(rk, rv, ck, cv, len, desc, st, M > 0 ? unsorted : nullptr));
     for (int p = 0; p < M; ++p) {
         const size_t L = (size_t)TILE << p;
         MergeGeo g = uniform_geo(ck, cv, ok, ov, len, L);
-        GNS_TRY(launch_merge(g, ck + len, ck + len, corank, nullptr, nullptr, false, desc, st));
+        const bool last = p == M - 1;
+        const bool need_copy = last && (tile_k != ok);   // presorted data must end where the sort ends
+        GNS_TRY(launch_merge(g, ck + len, ck + len, corank, nullptr, nullptr, false, desc, st, unsorted,
+                             need_copy ? tile_k : nullptr, need_copy ? tile_v : nullptr));
         std::swap(ck, ok);
         std::swap(cv, ov);
     }
@@ -446,7 +458,8 @@ gns_status run_sort(double *keys, uint32_t *vals, size_t n, const Mode &m, unsig
         uint32_t *bv = hv ? reinterpret_cast<uint32_t *>(ws + Lo.off_v) : nullptr;
         int *corank = reinterpret_cast<int *>(ws + Lo.off_corank);
         if (!m.limited) {
-            GNS_TRY(sort_range(keys, vals, bk, bv, n, false, corank, desc, st));
+            unsigned *unsorted = reinterpret_cast<unsigned *>(ws + Lo.off_adapt);
+            GNS_TRY(sort_range(keys, vals, bk, bv, n, false, corank, desc, st, unsorted));
         } else {
             int2 *deps = reinterpret_cast<int2 *>(ws + Lo.off_deps);
             unsigned *flags = reinterpret_cast<unsigned *>(ws + Lo.off_flags);

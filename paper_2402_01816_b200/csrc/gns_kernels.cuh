@@ -522,9 +522,35 @@ constexpr size_t ts_smem(bool hv) { return 2 * ts_stage_bytes(hv) + 1024; }
 
 template <bool HV, bool DESC>
 __global__ void __launch_bounds__(FUSED_THREADS, 2)
-merge_tstore_kernel(PipeGeo pg, int ntiles, int per_cta, const __grid_constant__ CUtensorMap omap)
+merge_tstore_kernel(PipeGeo pg, int ntiles, int per_cta, const __grid_constant__ CUtensorMap omap,
+                    const unsigned *unsorted, const double *copy_k, const uint32_t *copy_v)
 {
     pdl_wait();
+    if (unsorted && *(volatile const unsigned *)unsorted == 0u) {
+        // NEXT f2: the whole input was already in order (tile sort found no
+        // descent), so every merge is an omission ("Omitsort").
+        // Only the last pass moves data, and only if the tile sort's output
+        // landed in the buffer (odd pass count): a plain copy back.
+        if (copy_k) {
+            const long long n = pg.g.n;
+            const long long lo = (long long)blockIdx.x * per_cta * MTILE;
+            const long long hi = min(n, lo + (long long)per_cta * MTILE);
+            for (long long i = lo + threadIdx.x * 4; i < hi; i += (long long)blockDim.x * 4) {
+                if (i + 4 <= hi) {
+                    const double4 x = *reinterpret_cast<const double4 *>(copy_k + i);
+                    *reinterpret_cast<double4 *>(pg.g.ok + i) = x;
+                    if (HV) *reinterpret_cast<uint4 *>(pg.g.ov + i) = *reinterpret_cast<const uint4 *>(copy_v + i);
+                } else {
+                    for (long long j = i; j < hi; ++j) {
+                        pg.g.ok[j] = copy_k[j];
+                        if (HV) pg.g.ov[j] = copy_v[j];
+                    }
+                }
+            }
+        }
+        pdl_trigger();
+        return;
+    }
     extern __shared__ __align__(16) unsigned char smem_raw0[];
     // 1 KiB alignment for the swizzled TMA boxes; pointer arithmetic (not an
     // integer round trip) keeps the shared address space visible to ptxas.
@@ -722,7 +748,8 @@ template <bool HV, bool DESC>
 __global__ void __launch_bounds__(NT1, 2)
 tile_sort2_kernel(const double *src_k, const uint32_t *src_v, double *dst_k, uint32_t *dst_v, long long n,
                   const __grid_constant__ CUtensorMap ksrc, const __grid_constant__ CUtensorMap vsrc,
-                  const __grid_constant__ CUtensorMap kdst, const __grid_constant__ CUtensorMap vdst)
+                  const __grid_constant__ CUtensorMap kdst, const __grid_constant__ CUtensorMap vdst,
+                  unsigned *unsorted)
 {
     pdl_wait();
     extern __shared__ __align__(16) unsigned char smem_raw0[];
@@ -770,9 +797,23 @@ tile_sort2_kernel(const double *src_k, const uint32_t *src_v, double *dst_k, uin
             if (HV) v[x] = ok ? src_v[base + e] : 0u;
         }
     }
+    const int e0 = tid * VT1;
+    if (unsorted) {
+        // NEXT f2 (Omitsort's presortedness test): does any key
+        // have to move before its predecessor?  Each thread checks its 32 keys
+        // and the key after them (the next thread's first, or the next tile's).
+        bool bad = false;
+#pragma unroll
+        for (int x = 0; x + 1 < VT1; ++x) bad |= before<DESC>(k[x + 1], k[x]);
+        const long long nx = base + e0 + VT1;
+        if (nx < n) {
+            const double kn = (full && e0 + VT1 < TILE) ? sk[tk_slot(e0 + VT1)] : src_k[nx];
+            bad |= before<DESC>(kn, k[VT1 - 1]);
+        }
+        if (__syncthreads_or(bad) && tid == 0) atomicOr(unsorted, 1u);
+    }
     transpose_sort16<0, HV, DESC>(k, v);
     transpose_sort16<16, HV, DESC>(k, v);
-    const int e0 = tid * VT1;
     __syncthreads();                       // the TMA-layout reads are done before the first spill
 #pragma unroll 1
     for (int coop = 1; coop <= NT1; coop <<= 1) {

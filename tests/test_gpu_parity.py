@@ -107,6 +107,31 @@ def test_targets(gns, n, frac, target):
     assert_bitexact(tk.cpu().numpy(), ek, what=f"{target} key-only n={n}")
 
 
+@pytest.mark.parametrize("target", ["AscLeft", "DescLeft", "AscRight", "DescRight"])
+@pytest.mark.parametrize("n", [3 * T1, 5 * T1 + 17, 16 * T1, 33 * T1 - 1])
+def test_presorted_fast_path(gns, n, target):
+    """NEXT f2: already-ordered input takes the omission path (no merge pass
+    moves data); one descent anywhere must take the full path.  Covers odd and
+    even merge-pass counts (the copy-back case) and ties."""
+    desc = target in ("DescLeft", "AscRight")        # AscRight = reverse(DescLeft)
+    base = np.sort(synth.ties(n, 55 + n, 1000))       # ordered, with ties
+    if desc:
+        base = base[::-1].copy()
+    v = synth.iota_u32(n)
+    cases = {"ordered": base}
+    for where in (T1 - 1, T1 + 100, n - 2):          # a descent at a tile boundary / inside / at the end
+        k = base.copy()
+        k[where], k[where + 1] = k[where + 1], k[where]
+        if k[where] != k[where + 1]:
+            cases[f"swap@{where}"] = k
+    for name, k in cases.items():
+        tk, tv = to_dev(k, v)
+        gns.sort_(tk, tv, 1.0, target=target)
+        torch.cuda.synchronize()
+        ek, ev = oracle.sort_target(k, v, target)
+        assert_bitexact(tk.cpu().numpy(), ek, tv.cpu().numpy(), ev, what=f"{target} {name} n={n}")
+
+
 def test_specials_inf_zero(gns):
     n = 3 * T + 5
     rng = np.random.default_rng(5)
