@@ -17,6 +17,12 @@ oracle/liboracle.so: oracle/oracle.c
 synth/libsynth.so: synth/gen.c
 	gcc -O2 -std=c11 -shared -fPIC -o $@ $<
 
+# bounds-asserting build for the GPU tests (GNS_LIB=libgns_debug.so)
+debug: $(PKG)/libgns_debug.so
+
+$(PKG)/libgns_debug.so: $(SRCS)
+	$(NVCC) $(NVFLAGS) -DGNS_DEBUG_BOUNDS -o $@ $(PKG)/csrc/gns.cu
+
 ptxas: $(SRCS)
 	$(NVCC) $(NVFLAGS) -Xptxas -v -o /tmp/gns_ptxas.so $(PKG)/csrc/gns.cu 2>&1 | grep -E "Function properties|registers|spill|Compiling entry" 
 
@@ -26,4 +32,4 @@ sass: $(LIB)
 clean:
 	rm -f $(LIB) oracle/liboracle.so synth/libsynth.so
 
-.PHONY: all ptxas sass clean
+.PHONY: all debug ptxas sass clean

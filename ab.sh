@@ -1,2 +1,3 @@
-python bench.py --steps 10 --warmup 3 --no-footprint --no-cpu-baseline > gpurun_out/b.log 2>&1; python -c "
-import json; d=json.loads(open('gpurun_out/b.log').read().strip().splitlines()[-1]); print(d['value']/1e9, d['e2e'])"
+GNS_LIB=libgns_debug.so timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/t_debug.log 2>&1; echo debug_rc=$?; tail -2 gpurun_out/t_debug.log
+GNS_LIB=libgns_debug.so python tools/sanitize_cases.py 2>&1 | tail -2
+for p in 0 1; do GNS_PDL=$p python tools/time_sort.py --tag pdl$p; GNS_PDL=$p python tools/time_sort.py --tag pdl$p --pairs --n 27 --frac 0.5; done

@@ -17,7 +17,9 @@ import os
 from typing import Optional
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgns.so")
+# GNS_LIB selects another build of the same library in this directory (e.g.
+# libgns_debug.so, the bounds-asserting build); default libgns.so.
+LIB_PATH = os.path.join(_HERE, os.environ.get("GNS_LIB", "libgns.so"))
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(

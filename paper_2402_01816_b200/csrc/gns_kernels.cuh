@@ -12,10 +12,29 @@
 // only through their outputs.
 #pragma once
 #include <cstdint>
+#include <cstdio>
 #include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace gns {
+
+// Debug build (make debug -> libgns_debug.so, GNS_LIB=libgns_debug.so): bounds
+// assertions on every shared-memory slot, slice and bulk-copy range.
+// compute-sanitizer is closed on this GPU pool, so these are the memory checks.
+#ifdef GNS_DEBUG_BOUNDS
+#define GNS_DASSERT(c)                                                                          \
+    do {                                                                                        \
+        if (!(c)) {                                                                             \
+            printf("GNS_DASSERT failed %s:%d block %d thread %d\n", __FILE__, __LINE__,          \
+                   (int)blockIdx.x, (int)threadIdx.x);                                          \
+            __trap();                                                                           \
+        }                                                                                       \
+    } while (0)
+#else
+#define GNS_DASSERT(c) \
+    do {               \
+    } while (0)
+#endif
 
 constexpr int NT = 256;            // merge threads per CTA
 constexpr int VT = 16;             // outputs per merge thread
@@ -196,6 +215,7 @@ __device__ __forceinline__ void serial_merge(const double *sk, const uint32_t *s
                                              int bi, int bend, double (&k)[VT], uint32_t (&v)[VT],
                                              IK ik, IV iv)
 {
+    GNS_DASSERT(ai >= 0 && bi >= 0 && aend <= bend && bend <= MTILE + 128);
     double ka = sk[ik(ai)], kb = sk[ik(bi)];
 #pragma unroll
     for (int x = 0; x < VT; ++x) {
@@ -205,6 +225,7 @@ __device__ __forceinline__ void serial_merge(const double *sk, const uint32_t *s
         if (HV) v[x] = sv[iv(src)];
         const int nxt = src + 1;
         if (p) bi = nxt; else ai = nxt;
+        GNS_DASSERT(nxt >= 0 && nxt < MTILE + 128);
         const double kn = sk[ik(nxt)];
         if (p) kb = kn; else ka = kn;
     }
@@ -432,9 +453,11 @@ __device__ __forceinline__ void pipe_issue(const PipeGeo &pg, int t, int i0, int
     const int offb = (int)(((uintptr_t)Bk >> 3) & 3);
     const int bbase = (offa + ca + 3) & ~3;
     // one run: elements [0, c) of K/V, shared slot of element e = sbase + off + e
+    GNS_DASSERT(i0 >= 0 && ca >= 0 && cb >= 0 && i0 + ca <= s.na && j0 >= 0 && j0 + cb <= s.nb);
     auto run = [&](const double *K, const uint32_t *V, int c, int off, int sbase, const double *lim) {
         if (c <= 0) return;
         const long long avail = lim - K;       // elements readable from K
+        GNS_DASSERT(avail >= c && sbase + off + c + 4 <= PIPE_SLOTS + 96);
         // keys: 16-byte chunks of 2
         const int ks = -(off & 1);
         int ke = ks + ((c - ks + 1) & ~1);
@@ -730,6 +753,7 @@ template <bool HV, bool DESC>
 __device__ __forceinline__ void serial_merge32(const double *sk, const uint32_t *sv, int ai, int aend, int bi, int bend,
                                                double (&k)[VT1], uint32_t (&v)[VT1])
 {
+    GNS_DASSERT(ai >= 0 && bi >= ai && bend <= TILE);
     double ka = sk[swm(ai)], kb = sk[swm(bi)];
 #pragma unroll
     for (int x = 0; x < VT1; ++x) {
@@ -739,6 +763,7 @@ __device__ __forceinline__ void serial_merge32(const double *sk, const uint32_t 
         if (HV) v[x] = sv[swmv(src)];
         const int nxt = src + 1;
         if (p) bi = nxt; else ai = nxt;
+        GNS_DASSERT(nxt >= 0 && nxt <= TILE);
         const double kn = sk[swm(nxt)];
         if (p) kb = kn; else ka = kn;
     }
@@ -946,6 +971,7 @@ merge_inplace_kernel(PipeGeo pg, int ntiles, const int *__restrict__ corank, con
         fence_proxy_async();
         // wait until every earlier tile that reads B slots we overwrite has loaded
         const int2 dp = deps[tcur];
+        GNS_DASSERT(dp.x >= 0 && dp.y < tcur);
         for (int u = dp.x + tid; u <= dp.y; u += NT)
             while (ld_acquire(flags + u) == 0u) { __nanosleep(32); }
         fence_proxy_async_global();
