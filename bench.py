@@ -254,12 +254,7 @@ def main():
     if pg:
         pg.barrier()
     t_ms = sum(a.elapsed_time(b) for a, b in ev)
-    t_max = t_ms
-    if pg:
-        tt = torch.tensor([t_ms], dtype=torch.float64, device=dev)
-        pg.all_reduce(tt, op=pg.ReduceOp.MAX)
-        t_max = float(tt.item())
-    value = world * n * args.steps / (t_max / 1e3)
+    t_max, value = aggregate(torch, pg, t_ms, n, args.steps, world, dev)
     ms_per_step = t_max / args.steps
 
     # validity of the last output: GPU-side properties only (the oracle is not
@@ -325,6 +320,18 @@ def main():
     if pg:
         pg.barrier()
         pg.destroy_process_group()
+
+
+def aggregate(torch, pg, t_ms, n, steps, world, device):
+    """Whole-job throughput of `world` replicas: every rank sorted `steps`
+    inputs of n keys in t_ms of device time; the job time is the max over
+    ranks (all_reduce MAX), value = world * n * steps / max_t."""
+    t_max = float(t_ms)
+    if pg is not None and world > 1:
+        tt = torch.tensor([t_ms], dtype=torch.float64, device=device)
+        pg.all_reduce(tt, op=pg.ReduceOp.MAX)
+        t_max = float(tt.item())
+    return t_max, world * n * steps / (t_max / 1e3)
 
 
 def launches(plan, frac, n):
