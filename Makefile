@@ -23,6 +23,12 @@ debug: $(PKG)/libgns_debug.so
 $(PKG)/libgns_debug.so: $(SRCS)
 	$(NVCC) $(NVFLAGS) -DGNS_DEBUG_BOUNDS -o $@ $(PKG)/csrc/gns.cu
 
+# phase-timing build for experiments (GNS_LIB=libgns_prof.so, tools/prof_merge.py)
+prof: $(PKG)/libgns_prof.so
+
+$(PKG)/libgns_prof.so: $(SRCS)
+	$(NVCC) $(NVFLAGS) -DGNS_PROF -o $@ $(PKG)/csrc/gns.cu
+
 ptxas: $(SRCS)
 	$(NVCC) $(NVFLAGS) -Xptxas -v -o /tmp/gns_ptxas.so $(PKG)/csrc/gns.cu 2>&1 | grep -E "Function properties|registers|spill|Compiling entry" 
 
@@ -32,4 +38,4 @@ sass: $(LIB)
 clean:
 	rm -f $(LIB) oracle/liboracle.so synth/libsynth.so
 
-.PHONY: all debug ptxas sass clean
+.PHONY: all debug prof ptxas sass clean

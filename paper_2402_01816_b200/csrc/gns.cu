@@ -67,7 +67,8 @@ bool is_aligned(const void *p, size_t a) { return ((uintptr_t)p % a) == 0; }
 // Workspace layout (one allocation = the whole bufferRAM of a call).
 struct Layout {
     size_t buf_elems = 0;   // buffer key(+val) slots
-    size_t off_k = 0, off_v = 0, off_corank = 0, off_deps = 0, off_flags = 0, off_adapt = 0, total = 0;
+    size_t off_k = 0, off_v = 0, off_corank = 0, off_deps = 0, off_flags = 0, off_adapt = 0, off_smp = 0, total = 0;
+    size_t nsmp = 0;        // keys per sample array (two arrays: data-side and buffer-side regions)
     int ntiles = 0;         // merge tiles over the whole array
 };
 
@@ -98,6 +99,9 @@ Layout layout(size_t n, const Mode &m, bool hv)
     if (m.limited) o = align_up(o + (size_t)(L.ntiles + 1) * sizeof(unsigned), 256);
     L.off_adapt = o;                   // the "input not presorted" word (NEXT f2)
     o = align_up(o + sizeof(unsigned), 256);
+    L.off_smp = o;                     // split-search samples, every SMP_G-th key of each region
+    L.nsmp = n / SMP_G + 2;
+    o = align_up(o + 2 * L.nsmp * sizeof(double), 256);
     L.total = o;
     return L;
 }
@@ -128,6 +132,8 @@ gns_status ensure_attrs()
     GNS_ATTR((merge_tstore_kernel<false, false>), ts_smem(false));
     GNS_ATTR((merge_tstore_kernel<true, true>), ts_smem(true));
     GNS_ATTR((merge_tstore_kernel<false, true>), ts_smem(false));
+    GNS_ATTR((merge_tstore_kernel<false, false, 3>), ts_smem(false, 3));
+    GNS_ATTR((merge_tstore_kernel<false, true, 3>), ts_smem(false, 3));
     GNS_ATTR((merge_inplace_kernel<true, false>), ts_smem(true));
     GNS_ATTR((merge_inplace_kernel<false, false>), ts_smem(false));
     GNS_ATTR((merge_inplace_kernel<true, true>), ts_smem(true));
@@ -200,6 +206,16 @@ bool pdl_enabled()
     return on;
 }
 
+// A/B knob for experiments: GNS_MERGE_STAGES=3 (key-only merge pass).
+int merge_stages()
+{
+    static const int v = [] {
+        const char *e = std::getenv("GNS_MERGE_STAGES");
+        return e ? std::atoi(e) : 2;
+    }();
+    return v;
+}
+
 template <typename... KArgs, typename... Args>
 gns_status launch_pdl(const char *what, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
                       cudaStream_t st, Args... args)
@@ -219,7 +235,7 @@ gns_status launch_pdl(const char *what, void (*kern)(KArgs...), dim3 grid, dim3 
 
 // Row a2 (K1).
 gns_status launch_tile_sort(const double *sk, const uint32_t *sv, double *dk, uint32_t *dv, size_t n, bool desc,
-                            cudaStream_t st, unsigned *unsorted = nullptr)
+                            cudaStream_t st, unsigned *unsorted = nullptr, double *smp = nullptr)
 {
     if (n == 0) return GNS_OK;
     const unsigned grid = (unsigned)ceil_div(n, TILE);
@@ -239,7 +255,7 @@ gns_status launch_tile_sort(const double *sk, const uint32_t *sv, double *dk, ui
     auto kern = hv ? (desc ? tile_sort2_kernel<true, true> : tile_sort2_kernel<true, false>)
                    : (desc ? tile_sort2_kernel<false, true> : tile_sort2_kernel<false, false>);
     return launch_pdl("tile_sort2_kernel", kern, grid, NT1, t1_smem(hv), st, sk, svv, dk, dvv, (long long)n, m[0],
-                      m[1], m[2], m[3], unsorted);
+                      m[1], m[2], m[3], unsorted, smp);
 }
 
 // Rows a3+a4 (fused K2+K3, persistent TMA pipeline) or, in place, a6 (K2 +
@@ -260,9 +276,11 @@ gns_status launch_merge(const MergeGeo &g, const double *lim_a, const double *li
         const int ctas = std::min(ntiles, 2 * num_sms());
         const int per = (int)ceil_div(ntiles, ctas);
         const int grid = (int)ceil_div(ntiles, per);
+        const int ns = (!hv && merge_stages() == 3) ? 3 : 2;
         auto kern = hv ? (desc ? merge_tstore_kernel<true, true> : merge_tstore_kernel<true, false>)
-                       : (desc ? merge_tstore_kernel<false, true> : merge_tstore_kernel<false, false>);
-        return launch_pdl("merge_tstore_kernel", kern, grid, FUSED_THREADS, ts_smem(hv), st, pg, ntiles, per, map,
+                       : ns == 3 ? (desc ? merge_tstore_kernel<false, true, 3> : merge_tstore_kernel<false, false, 3>)
+                                 : (desc ? merge_tstore_kernel<false, true> : merge_tstore_kernel<false, false>);
+        return launch_pdl("merge_tstore_kernel", kern, grid, WS_THREADS, ts_smem(hv, ns), st, pg, ntiles, per, map,
                           unsorted, copy_k, copy_v);
     }
     GNS_TRY(launch_pdl("partition_kernel", desc ? partition_kernel<true> : partition_kernel<false>,
@@ -286,7 +304,8 @@ gns_status launch_reverse(double *k, uint32_t *v, size_t n, cudaStream_t st)
                       (long long)n);
 }
 
-MergeGeo uniform_geo(const double *sk, const uint32_t *sv, double *dk, uint32_t *dv, size_t n, size_t L)
+MergeGeo uniform_geo(const double *sk, const uint32_t *sv, double *dk, uint32_t *dv, size_t n, size_t L,
+                     const double *sa = nullptr, double *so = nullptr)
 {
     MergeGeo g;
     g.ak = sk;
@@ -298,6 +317,10 @@ MergeGeo uniform_geo(const double *sk, const uint32_t *sv, double *dk, uint32_t 
     g.n = (long long)n;
     g.L = (long long)L;
     g.single = 0;
+    g.tpp = (int)(2 * L / MTILE);
+    g.tpp_log2 = (g.tpp & (g.tpp - 1)) ? -1 : __builtin_ctz((unsigned)g.tpp);
+    g.sa = (L % SMP_G == 0) ? sa : nullptr;
+    g.so = so;
     return g;
 }
 
@@ -305,8 +328,10 @@ MergeGeo uniform_geo(const double *sk, const uint32_t *sv, double *dk, uint32_t 
 // ping-pong buffer (Nocopy-Mergesort).  The result ends in P if
 // `final_in_partner`, else in R.  Parity picks the tile-sort destination so
 // no copy pass is ever needed (an odd number of merge levels starts from P).
+// smp: two sample arrays of >= len/SMP_G + 2 keys (R's and P's), or nullptr.
 gns_status sort_range(double *rk, uint32_t *rv, double *pk_, uint32_t *pv_, size_t len,
-                      bool final_in_partner, int *corank, bool desc, cudaStream_t st, unsigned *unsorted = nullptr)
+                      bool final_in_partner, int *corank, bool desc, cudaStream_t st, unsigned *unsorted = nullptr,
+                      double *smp_r = nullptr, double *smp_p = nullptr)
 {
     if (len == 0) return GNS_OK;
     const int M = merge_passes_for(len);
@@ -320,16 +345,19 @@ gns_status sort_range(double *rk, uint32_t *rv, double *pk_, uint32_t *pv_, size
     // NEXT f2: with `unsorted` the tile sort also tests whether the input is
     // already in order; if it is, every merge pass is omitted on the device.
     if (unsorted && M > 0) GNS_TRY(check(cudaMemsetAsync(unsorted, 0, sizeof(unsigned), st), "memset"));
-    GNS_TRY(launch_tile_sort(rk, rv, ck, cv, len, desc, st, M > 0 ? unsorted : nullptr));
+    double *cs = tile_to_partner ? smp_p : smp_r;      // samples of the region holding the current runs
+    double *os = tile_to_partner ? smp_r : smp_p;
+    GNS_TRY(launch_tile_sort(rk, rv, ck, cv, len, desc, st, M > 0 ? unsorted : nullptr, M > 0 ? cs : nullptr));
     for (int p = 0; p < M; ++p) {
         const size_t L = (size_t)TILE << p;
-        MergeGeo g = uniform_geo(ck, cv, ok, ov, len, L);
+        MergeGeo g = uniform_geo(ck, cv, ok, ov, len, L, cs, p + 1 < M ? os : nullptr);
         const bool last = p == M - 1;
         const bool need_copy = last && (tile_k != ok);   // presorted data must end where the sort ends
         GNS_TRY(launch_merge(g, ck + len, ck + len, corank, nullptr, nullptr, false, desc, st, unsorted,
                              need_copy ? tile_k : nullptr, need_copy ? tile_v : nullptr));
         std::swap(ck, ok);
         std::swap(cv, ov);
+        std::swap(cs, os);
     }
     return GNS_OK;
 }
@@ -380,6 +408,10 @@ gns_status top_merge(double *keys, uint32_t *vals, double *bk, uint32_t *bv, siz
     g.n = (long long)len;
     g.L = (long long)nl;
     g.single = 1;
+    g.tpp = 1;
+    g.tpp_log2 = 0;
+    g.sa = nullptr;
+    g.so = nullptr;
     return launch_merge(g, bk + nl, keys + lo + len, corank, deps, flags, true, desc, st);
 }
 
@@ -404,7 +436,8 @@ void count_sort_range(size_t len, Sched *sc, size_t n)
 // data[lo+b : lo+len) is sorted first (recursively, same buffer), then the
 // left b elements are sorted into the buffer and merged in place.
 gns_status sort_limited(double *keys, uint32_t *vals, size_t lo, size_t len, size_t b, double *bk, uint32_t *bv,
-                        int *corank, int2 *deps, unsigned *flags, bool desc, cudaStream_t st, Sched *sc, size_t n)
+                        int *corank, int2 *deps, unsigned *flags, bool desc, cudaStream_t st, Sched *sc, size_t n,
+                        double *s0 = nullptr, double *s1 = nullptr)
 {
     const bool hv = vals != nullptr;
     double *dk = keys + lo;
@@ -426,18 +459,18 @@ gns_status sort_limited(double *keys, uint32_t *vals, size_t lo, size_t len, siz
             sc->launches += 3;
             return GNS_OK;
         }
-        GNS_TRY(sort_range(dk, dv, bk, bv, nl, true, corank, desc, st));
-        GNS_TRY(sort_range(dk + nl, hv ? dv + nl : nullptr, dk, dv, nr, false, corank, desc, st));
+        GNS_TRY(sort_range(dk, dv, bk, bv, nl, true, corank, desc, st, nullptr, s0, s1));
+        GNS_TRY(sort_range(dk + nl, hv ? dv + nl : nullptr, dk, dv, nr, false, corank, desc, st, nullptr, s0, s1));
         return top_merge(keys, vals, bk, bv, lo, len, nl, corank, deps, flags, desc, st);
     }
-    GNS_TRY(sort_limited(keys, vals, lo + b, len - b, b, bk, bv, corank, deps, flags, desc, st, sc, n));
+    GNS_TRY(sort_limited(keys, vals, lo + b, len - b, b, bk, bv, corank, deps, flags, desc, st, sc, n, s0, s1));
     if (sc) {
         count_sort_range(b, sc, n);
         sc->elem_passes += (double)len / (double)n;
         sc->launches += 3;
         return GNS_OK;
     }
-    GNS_TRY(sort_range(dk, dv, bk, bv, b, true, corank, desc, st));
+    GNS_TRY(sort_range(dk, dv, bk, bv, b, true, corank, desc, st, nullptr, s0, s1));
     return top_merge(keys, vals, bk, bv, lo, len, b, corank, deps, flags, desc, st);
 }
 
@@ -459,13 +492,15 @@ gns_status run_sort(double *keys, uint32_t *vals, size_t n, const Mode &m, unsig
         double *bk = reinterpret_cast<double *>(ws + Lo.off_k);
         uint32_t *bv = hv ? reinterpret_cast<uint32_t *>(ws + Lo.off_v) : nullptr;
         int *corank = reinterpret_cast<int *>(ws + Lo.off_corank);
+        double *smp = reinterpret_cast<double *>(ws + Lo.off_smp);
         if (!m.limited) {
             unsigned *unsorted = reinterpret_cast<unsigned *>(ws + Lo.off_adapt);
-            GNS_TRY(sort_range(keys, vals, bk, bv, n, false, corank, desc, st, unsorted));
+            GNS_TRY(sort_range(keys, vals, bk, bv, n, false, corank, desc, st, unsorted, smp, smp + Lo.nsmp));
         } else {
             int2 *deps = reinterpret_cast<int2 *>(ws + Lo.off_deps);
             unsigned *flags = reinterpret_cast<unsigned *>(ws + Lo.off_flags);
-            GNS_TRY(sort_limited(keys, vals, 0, n, m.buf, bk, bv, corank, deps, flags, desc, st, nullptr, n));
+            GNS_TRY(sort_limited(keys, vals, 0, n, m.buf, bk, bv, corank, deps, flags, desc, st, nullptr, n, smp,
+                                 smp + Lo.nsmp));
         }
     }
     if (right) GNS_TRY(launch_reverse(keys, vals, n, st));
@@ -643,8 +678,34 @@ gns_status gns_merge_inplace_top(double *keys, uint32_t *vals, const double *lef
     g.n = (long long)n;
     g.L = (long long)nl;
     g.single = 1;
+    g.tpp = 1;
+    g.tpp_log2 = 0;
+    g.sa = nullptr;
+    g.so = nullptr;
     return launch_merge(g, left_keys + nl, keys + n, corank, deps, flags, true, false, (cudaStream_t)stream);
 }
+
+#ifdef GNS_PROF
+void gns_prof_reset(void)
+{
+    unsigned long long z[16] = {};
+    cudaMemcpyToSymbol(g_prof, z, sizeof(z));
+    unsigned long long tl[32][2];
+    for (int i = 0; i < 32; ++i) {
+        tl[i][0] = ~0ull;
+        tl[i][1] = 0;
+    }
+    cudaMemcpyToSymbol(g_tl, tl, sizeof(tl));
+}
+void gns_prof_timeline(unsigned long long *out)
+{
+    cudaMemcpyFromSymbol(out, g_tl, 64 * sizeof(unsigned long long));
+}
+void gns_prof_read(unsigned long long *out)
+{
+    cudaMemcpyFromSymbol(out, g_prof, 16 * sizeof(unsigned long long));
+}
+#endif
 
 int gns_tile_elems(void) { return TILE; }
 int gns_merge_tile_elems(void) { return MTILE; }

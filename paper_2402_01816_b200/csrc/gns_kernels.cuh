@@ -36,6 +36,30 @@ namespace gns {
     } while (0)
 #endif
 
+// Profiling build (make prof -> libgns_prof.so): thread 0 of each merge CTA
+// accumulates clock64 phase times into g_prof (tools/prof_merge.py).
+#ifdef GNS_PROF
+__device__ unsigned long long g_prof[16];
+// timeline: [launch slot][0] = min start, [1] = max end (globaltimer ns); slot 0 =
+// tile sort, slot 1 + log2(L / TILE) = merge pass of run length L
+__device__ unsigned long long g_tl[32][2];
+__device__ __forceinline__ unsigned long long gtimer()
+{
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define GNS_TL_START(slot) do { if (threadIdx.x == 0) atomicMin(&g_tl[slot][0], gtimer()); } while (0)
+#define GNS_TL_END(slot) do { if (threadIdx.x == 0) atomicMax(&g_tl[slot][1], gtimer()); } while (0)
+#define GNS_PT(var) const long long var = clock64()
+#define GNS_PADD(slot, v) acc[slot] += (unsigned long long)(v)
+#else
+#define GNS_PT(var) do {} while (0)
+#define GNS_PADD(slot, v) do {} while (0)
+#define GNS_TL_START(slot) do {} while (0)
+#define GNS_TL_END(slot) do {} while (0)
+#endif
+
 constexpr int NT = 256;            // merge threads per CTA
 constexpr int VT = 16;             // outputs per merge thread
 constexpr int MTILE = NT * VT;     // K3/K4 output tile = 4096 elements
@@ -247,6 +271,10 @@ struct MergeGeo {
     long long n;
     long long L;
     int single;     // 1: one pair, A = ak[0:L), B = bk[0:n-L) (any lengths; the in-place top merge)
+    int tpp;        // uniform pass: output tiles per pair, 2L / MTILE
+    int tpp_log2;   // log2(tpp) if tpp is a power of two, else -1
+    const double *sa;   // samples of the source region (key at every SMP_G-th position), or nullptr
+    double *so;         // samples of the output region written by this pass, or nullptr
 };
 
 struct TileSpan {
@@ -264,7 +292,8 @@ __device__ __forceinline__ TileSpan tile_span(const MergeGeo &g, int t)
         s.nb = (int)(g.n - g.L);
     } else {
         const long long span = 2 * g.L;
-        s.pbase = (s.g0 / span) * span;
+        const unsigned q = g.tpp_log2 >= 0 ? ((unsigned)t >> g.tpp_log2) : (unsigned)t / (unsigned)g.tpp;
+        s.pbase = (long long)q * span;
         const long long rem = g.n - s.pbase;
         s.na = (int)min(g.L, rem);
         s.nb = (int)max(0LL, min(g.L, rem - g.L));
@@ -348,6 +377,81 @@ __device__ __forceinline__ int group_corank(const MergeGeo &g, int t, int gl, un
         hi = max(nlo, nhi);
     }
     return lo;
+}
+
+// ------------------------------------------- sample-guided co-rank search
+// Every pass (and the tile sort) also writes the key at every SMP_G-th output
+// position into a small sample array (n / 512 keys, L2-resident).  The next
+// pass finds a split first on the samples -- Q(x) = A[x] <= B[y_lo(x)] with
+// x a multiple of G and y_lo(x) = G * floor((d-1-x) / G), monotone in x --
+// which brackets the co-rank c of diagonal d (d a multiple of G) in a window
+// of 2G: Q(x) true  => A[x] <= B[d-1-x]          => c >= x + 1;
+//        Q(x) false => B[d-1-x-G] <= B[y_lo(x)] < A[x] <= A[x+G] => c <= x + G.
+// Then the exact search runs in that window (2 rounds of 33-ary probes),
+// instead of ~5 rounds spread over the whole run.
+constexpr int SMP_LOG2 = 9;
+constexpr int SMP_G = 1 << SMP_LOG2;   // 512
+
+// (W+1)-ary search of the last true of a monotone predicate over [lo, hi]
+// (indices), by a group of W lanes; returns the number of trues in [lo, hi].
+template <int W, class P>
+__device__ __forceinline__ int group_count_true(int lo, int hi, int gl, unsigned mask, int gbase, P pred)
+{
+    // invariant: pred true on [lo0, lo), false on [hi, hi0]; answer in [lo, hi+1)
+    const int lo0 = lo;
+    hi += 1;
+    while (lo < hi) {
+        const int span = hi - lo;
+        int m, nprobe;
+        if (span <= W) {
+            m = lo + gl;
+            nprobe = span;
+        } else {
+            m = lo + (int)(((long long)span * (gl + 1)) / (W + 1));
+            nprobe = W;
+        }
+        bool p = false;
+        if (gl < nprobe) p = pred(m);
+        const unsigned bal = (__ballot_sync(mask, p) & mask) >> gbase;
+        const int c = __popc(bal);
+        const int m_prev = __shfl_sync(mask, m, gbase + (c > 0 ? c - 1 : 0));
+        const int m_next = __shfl_sync(mask, m, gbase + (c < nprobe ? c : 0));
+        const int nlo = (c == 0) ? lo : m_prev + 1;
+        const int nhi = (c == nprobe) ? hi : m_next;
+        lo = nlo;
+        hi = max(nlo, nhi);
+    }
+    return lo - lo0;
+}
+
+// Stable co-rank of tile t's first diagonal by a group of W lanes, sample-guided
+// when the pass has samples (uniform passes), else over the whole range.
+template <int W, bool DESC>
+__device__ __forceinline__ int tile_corank(const MergeGeo &g, int t, int gl, unsigned mask, int gbase)
+{
+    const TileSpan s = tile_span(g, t);
+    const double *A = g.ak + s.pbase;
+    const double *B = g.bk + s.pbase;
+    const int d = s.k0;
+    int lo = max(0, d - s.nb), hi = min(d, s.na);
+    if (lo >= hi) return lo;
+    if (g.sa != nullptr) {
+        const int s_lo = (lo + SMP_G - 1) >> SMP_LOG2;
+        const int s_hi = (hi - 1) >> SMP_LOG2;
+        if (s_lo <= s_hi) {
+            const double *SA = g.sa + (s.pbase >> SMP_LOG2);
+            const double *SB = g.sa + ((s.pbase + g.L) >> SMP_LOG2);
+            const int cnt = group_count_true<W>(s_lo, s_hi, gl, mask, gbase, [&](int sx) {
+                const int yb = (d - 1 - (sx << SMP_LOG2)) >> SMP_LOG2;
+                return !before<DESC>(SB[yb], SA[sx]);
+            });
+            if (cnt > 0) lo = max(lo, ((s_lo + cnt - 1) << SMP_LOG2) + 1);
+            if (s_lo + cnt <= s_hi) hi = min(hi, ((s_lo + cnt) << SMP_LOG2) + SMP_G);
+        }
+    }
+    // exact: number of m in [lo, hi) with A[m] <= B[d-1-m]
+    return lo + group_count_true<W>(lo, hi - 1, gl, mask, gbase,
+                                    [&](int m) { return !before<DESC>(B[d - 1 - m], A[m]); });
 }
 
 template <bool DESC>
@@ -515,7 +619,6 @@ struct Lin { __device__ __forceinline__ int operator()(int e) const { return e; 
 
 // ------------------------------- shared pieces of the fused merge kernels
 constexpr int SEARCH_WARPS = 2;
-constexpr int FUSED_THREADS = NT + 32 * SEARCH_WARPS;
 constexpr int SPL_RING = 64;
 
 __device__ __forceinline__ void bar_merge_warps() { asm volatile("bar.sync 1, %0;" :: "n"(NT) : "memory"); }
@@ -523,32 +626,46 @@ __device__ __forceinline__ void bar_merge_warps() { asm volatile("bar.sync 1, %0
 // ---------------------------- K2+K3 fused: the production merge pass (row a3+a4)
 // A persistent grid (2 CTAs per SM); CTA c owns the contiguous output tiles
 // [first, last) of 4096 keys, so it needs the co-rank splits at first..last
-// only (tile t ends where t+1 starts).  Warps 8-9 are search warps: they run
-// ahead computing the splits (two concurrent 16-lane 17-ary warp searches per
-// warp, predicate A[m] <= B[d-1-m]) into a shared ring; at kernel start all 10
-// warps compute the first splits in parallel.  Warps 0-7 merge.  Thread 0
-// issues TMA bulk copies (cp.async.bulk, UBLKCP) of exactly A[i0:i1) and
-// B[j0:j1) into a double-buffered stage; keys and vals of global element g
-// share one shared slot (offset g mod 4) so every copy is 16-byte aligned.
-// Each thread merges 16 outputs (merge path + serial merge, left wins ties).
-// After a tile is merged,
-// the consumed input stage becomes the output staging buffer: thread t writes
-// its 16 outputs (= row t of a [256][16] double box) with conflict-free
-// st.shared.v2 into the 128-byte-swizzled layout, and one thread stores the
-// whole 32 KB tile with one cp.async.bulk.tensor (UTMASTG), instead of 32
-// 256-bit STGs per warp that each touch 32 cache lines.  Vals (if any) keep
-// the direct 256-bit stores.
+// only (tile t ends where t+1 starts).  Warp roles (warp-specialised, no
+// CTA-wide barrier inside the tile loop):
+//   warps 0-7  merge: each thread merges 16 outputs of the tile in stage
+//              i % NS (merge path + serial merge, left wins ties), then writes
+//              them into the same stage as the output staging box;
+//   warp 8     producer (one lane): issues the TMA bulk copies (cp.async.bulk,
+//              UBLKCP) of exactly A[i0:i1) and B[j0:j1) into a free stage,
+//              and the TMA tensor store (UTMASTG) of each staged tile;
+//   warps 9-10 search: run ahead computing the splits (two concurrent 16-lane
+//              17-ary searches per warp, predicate A[m] <= B[d-1-m]) into a
+//              shared ring; at kernel start warps 0-7 compute the first splits.
+// Keys and vals of global element g share one shared slot (offset g mod 4) so
+// every copy is 16-byte aligned.  Stage hand-off: full[st] (producer -> merge
+// warps, tx-count of the bulk copies) and staged[st] (8 merge-warp arrivals ->
+// producer, after the swizzled output box is in shared memory).  The producer
+// reuses a stage for tile i+NS once the store of tile i has read it out.
+// Staging: thread t writes its 16 outputs (= row t of a [256][16] double box)
+// with conflict-free st.shared.v2 into the 128-byte-swizzled layout; one
+// cp.async.bulk.tensor stores the 32 KB tile.  Vals (if any) are stored by the
+// merge threads with 256-bit stores.
 constexpr int TS_KEY_SLOTS = MTILE + 128;                       // 33,792 B = 33 KiB
 constexpr size_t TS_VAL_BYTES = ((MTILE + 128) * 4 + 1023) / 1024 * 1024;
 constexpr size_t ts_stage_bytes(bool hv) { return TS_KEY_SLOTS * 8 + (hv ? TS_VAL_BYTES : 0); }
-constexpr size_t ts_smem(bool hv) { return 2 * ts_stage_bytes(hv) + 1024; }
+constexpr size_t ts_smem(bool hv, int ns = 2) { return ns * ts_stage_bytes(hv) + 1024; }
+constexpr int MERGE_WARPS = NT / 32;                 // 8
+constexpr int PRODUCER_WARP = MERGE_WARPS;           // 8
+constexpr int WS_THREADS = NT + 32 + 32 * SEARCH_WARPS;   // 352
 
-template <bool HV, bool DESC>
-__global__ void __launch_bounds__(FUSED_THREADS, 2)
+template <bool HV, bool DESC, int NS = 2>
+__global__ void __launch_bounds__(WS_THREADS, 2)
 merge_tstore_kernel(PipeGeo pg, int ntiles, int per_cta, const __grid_constant__ CUtensorMap omap,
                     const unsigned *unsorted, const double *copy_k, const uint32_t *copy_v)
 {
+#ifdef GNS_PROF
+    unsigned long long acc[16] = {};
+    const long long t_entry = clock64();
+    const int tl_slot = min(31, 1 + (63 - __clzll(pg.g.L)) - 13);
+#endif
     pdl_wait();
+    GNS_TL_START(tl_slot);
     if (unsorted && *(volatile const unsigned *)unsorted == 0u) {
         // NEXT f2: the whole input was already in order (tile sort found no
         // descent), so every merge is an omission ("Omitsort").
@@ -574,12 +691,16 @@ merge_tstore_kernel(PipeGeo pg, int ntiles, int per_cta, const __grid_constant__
         pdl_trigger();
         return;
     }
+#ifdef GNS_PROF
+    const long long t_flag = clock64();
+#endif
     extern __shared__ __align__(16) unsigned char smem_raw0[];
     // 1 KiB alignment for the swizzled TMA boxes; pointer arithmetic (not an
     // integer round trip) keeps the shared address space visible to ptxas.
     unsigned char *smem_raw = smem_raw0 + ((1024u - (smem_u32(smem_raw0) & 1023u)) & 1023u);
-    __shared__ __align__(8) uint64_t bars[2];
-    __shared__ PipeMeta meta[2];
+    __shared__ __align__(8) uint64_t full[NS];
+    __shared__ __align__(8) uint64_t staged[NS];
+    __shared__ PipeMeta meta[NS];
     __shared__ int spl[SPL_RING];
     __shared__ volatile int spl_tag[SPL_RING];
     __shared__ volatile int spl_used;
@@ -594,64 +715,112 @@ merge_tstore_kernel(PipeGeo pg, int ntiles, int per_cta, const __grid_constant__
     const int m = last - first;
     if (m <= 0) return;
     const int nspl = (last < ntiles) ? m + 1 : m;
-    for (int j = tid; j < SPL_RING; j += FUSED_THREADS) spl_tag[j] = -1;
-    __syncthreads();
-    const int init = min(nspl, FUSED_THREADS / 32);
-    if (warp < init) {
-        const int c = warp_corank<DESC>(pg.g, first + warp, lane);
-        if (lane == 0) {
-            spl[warp] = c;
-            spl_tag[warp] = warp;
-        }
-    }
-    uint64_t policy = policy_evict_first();
+    for (int j = tid; j < SPL_RING; j += WS_THREADS) spl_tag[j] = -1;
     if (tid == 0) {
-        mbar_init(&bars[0], 1);
-        mbar_init(&bars[1], 1);
+#pragma unroll
+        for (int b = 0; b < NS; ++b) {
+            mbar_init(&full[b], 1);
+            mbar_init(&staged[b], MERGE_WARPS);
+        }
         fence_mbar_init();
         spl_used = 0;
     }
     __syncthreads();
+    // the first splits: merge warps (idle until the first tile lands)
+    const int init = min(nspl, MERGE_WARPS);
+    auto publish = [&](int j, int c) {
+        spl[j % SPL_RING] = c;
+        __threadfence_block();
+        spl_tag[j % SPL_RING] = j;
+    };
 
-    if (warp >= NT / 32) {
-        const int sw = warp - NT / 32;
+    if (warp > PRODUCER_WARP) {
+        // ------------------------------------------------ search warps
+        const int sw = warp - PRODUCER_WARP - 1;
         const int h = lane >> 4, gl = lane & 15;
         const unsigned mask = 0xFFFFu << (16 * h);
         for (int j0 = init + 2 * sw; j0 < nspl; j0 += 2 * SEARCH_WARPS) {
             const int j = j0 + h;
             while (j0 + 1 - spl_used >= SPL_RING) { __nanosleep(64); }
             if (j < nspl) {
-                const int c = group_corank<16, DESC>(pg.g, first + j, gl, mask, 16 * h);
-                if (gl == 0) {
-                    spl[j % SPL_RING] = c;
-                    __threadfence_block();
-                    spl_tag[j % SPL_RING] = j;
-                }
+                const int c = tile_corank<16, DESC>(pg.g, first + j, gl, mask, 16 * h);
+                if (gl == 0) publish(j, c);
             }
             __syncwarp();
         }
         return;
     }
 
-    auto get_split = [&](int j) -> int {
-        while (spl_tag[j % SPL_RING] != j) { }
-        return spl[j % SPL_RING];
-    };
-    auto issue = [&](int i) {
-        const int st = i & 1;
-        pipe_issue<HV>(pg, first + i, get_split(i), (i + 1 < nspl) ? get_split(i + 1) : 0, skb(st), svb(st),
-                       &bars[st], &meta[st], policy);
-        spl_used = i;
-    };
+    if (warp == PRODUCER_WARP) {
+        // ------------------------------------------------ producer (one lane)
+        if (lane != 0) return;
+        const uint64_t policy = policy_evict_first();
+        auto get_split = [&](int j) -> int {
+#ifdef GNS_PROF
+            const long long a = clock64();
+            while (spl_tag[j % SPL_RING] != j) { }
+            acc[8] += clock64() - a;
+#else
+            while (spl_tag[j % SPL_RING] != j) { }
+#endif
+            return spl[j % SPL_RING];
+        };
+        auto issue = [&](int i) {
+            const int st = i % NS;
+            pipe_issue<HV>(pg, first + i, get_split(i), (i + 1 < nspl) ? get_split(i + 1) : 0, skb(st), svb(st),
+                           &full[st], &meta[st], policy);
+            spl_used = i;
+        };
+        for (int i = 0; i < NS && i < m; ++i) issue(i);
+#ifdef GNS_PROF
+        GNS_PADD(0, clock64() - t_entry);
+#endif
+        for (int i = 0; i < m; ++i) {
+            const int st = i % NS;
+            GNS_PT(p0);
+            mbar_wait(&staged[st], (uint32_t)((i / NS) & 1));     // tile i staged by the 8 merge warps
+            GNS_PT(p1);
+            GNS_PADD(1, p1 - p0);
+            tma_store_2d(&omap, skb(st), 0, (int)((long long)(first + i) * (MTILE / 16)));
+            bulk_commit();
+            if (i + NS < m) {
+                bulk_wait_read0();                                 // stage st read out -> reusable
+                GNS_PT(p2);
+                GNS_PADD(5, p2 - p1);
+                issue(i + NS);
+                GNS_PT(p3);
+                GNS_PADD(6, p3 - p2);
+            }
+        }
+        bulk_wait0();
+#ifdef GNS_PROF
+        atomicMax(&g_tl[tl_slot][1], gtimer());
+        acc[7] = clock64() - t_entry;
+        acc[9] = m;
+        acc[10] = 1;
+        for (int q = 0; q < 11; ++q) atomicAdd(&g_prof[q], acc[q]);
+#endif
+        pdl_trigger();
+        return;
+    }
+
+    // ---------------------------------------------------- merge warps 0-7
+    if (warp < init) {
+        const int c = tile_corank<32, DESC>(pg.g, first + warp, lane, 0xFFFFFFFFu, 0);
+        if (lane == 0) publish(warp, c);
+    }
+#ifdef GNS_PROF
+    const long long t_split0 = clock64();
+    long long t_full0 = 0;
+#endif
     const long long n = pg.g.n;
     const long long full_rows = n >> 4;              // rows stored by TMA; a partial last row is stored by hand
-    if (tid == 0) {
-        issue(0);
-        if (m > 1) issue(1);
-    }
     for (int i = 0; i < m; ++i) {
-        const int st = i & 1;
-        mbar_wait(&bars[st], (uint32_t)((i >> 1) & 1));
+        const int st = i % NS;
+        mbar_wait(&full[st], (uint32_t)((i / NS) & 1));
+#ifdef GNS_PROF
+        if (i == 0) t_full0 = clock64();
+#endif
         const PipeMeta mt = meta[st];
         const int cnt = mt.ca + mt.cb;
         const int d = min(tid * VT, cnt);
@@ -664,6 +833,8 @@ merge_tstore_kernel(PipeGeo pg, int ntiles, int per_cta, const __grid_constant__
                                Lin(), Lin());
         const long long t = first + i;
         const long long row = t * (MTILE / 16) + tid;    // global row of this thread's 16 outputs
+        if (pg.g.so != nullptr && (tid & (SMP_G / VT - 1)) == 0 && d < cnt)
+            pg.g.so[(row * 16) >> SMP_LOG2] = k[0];      // sample of output position row*16
         bar_merge_warps();                               // stage st fully read
         unsigned char *rowp = reinterpret_cast<unsigned char *>(sk) + tid * 128;
 #pragma unroll
@@ -685,15 +856,17 @@ merge_tstore_kernel(PipeGeo pg, int ntiles, int per_cta, const __grid_constant__
             for (int x = 0; x < VT; ++x)
                 if (x < cnt - d) pg.g.ok[row * 16 + x] = k[x];
         }
-        bar_merge_warps();
-        if (tid == 0) {
-            tma_store_2d(&omap, sk, 0, (int)(t * (MTILE / 16)));
-            bulk_commit();
-            bulk_wait_read0();                            // staging read out -> stage reusable
-            if (i + 2 < m) issue(i + 2);
-        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&staged[st]);
     }
-    if (tid == 0) bulk_wait0();
+#ifdef GNS_PROF
+    if (tid == 0) {
+        atomicAdd(&g_prof[11], (unsigned long long)(t_flag - t_entry));
+        atomicAdd(&g_prof[12], (unsigned long long)(t_split0 - t_entry));
+        atomicAdd(&g_prof[13], (unsigned long long)(t_full0 - t_entry));
+        atomicAdd(&g_prof[14], (unsigned long long)(clock64() - t_entry));
+    }
+#endif
     pdl_trigger();
 }
 
@@ -774,9 +947,10 @@ __global__ void __launch_bounds__(NT1, 2)
 tile_sort2_kernel(const double *src_k, const uint32_t *src_v, double *dst_k, uint32_t *dst_v, long long n,
                   const __grid_constant__ CUtensorMap ksrc, const __grid_constant__ CUtensorMap vsrc,
                   const __grid_constant__ CUtensorMap kdst, const __grid_constant__ CUtensorMap vdst,
-                  unsigned *unsorted)
+                  unsigned *unsorted, double *smp)
 {
     pdl_wait();
+    GNS_TL_START(0);
     extern __shared__ __align__(16) unsigned char smem_raw0[];
     unsigned char *smem = smem_raw0 + ((1024u - (smem_u32(smem_raw0) & 1023u)) & 1023u);
     double *sk = reinterpret_cast<double *>(smem);
@@ -861,6 +1035,8 @@ tile_sort2_kernel(const double *src_k, const uint32_t *src_v, double *dst_k, uin
         }
         __syncthreads();
     }
+    if (smp != nullptr && e0 < cnt && (tid & (SMP_G / VT1 - 1)) == 0)
+        smp[(base + e0) >> SMP_LOG2] = k[0];          // sample of output position base + e0
     if (full) {
 #pragma unroll
         for (int c = 0; c < VT1 / 2; ++c) sts128(sk + tk_slot(e0 + 2 * c), k[2 * c], k[2 * c + 1]);
@@ -889,6 +1065,7 @@ tile_sort2_kernel(const double *src_k, const uint32_t *src_v, double *dst_k, uin
             }
         }
     }
+    GNS_TL_END(0);
     pdl_trigger();
 }
 

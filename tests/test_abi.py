@@ -73,7 +73,7 @@ def test_workspace_ram_pct(gns):
     for frac, want in ((1.0, 2.0), (0.5, 1.5)):
         ws = gns.workspace_bytes(n, frac, True)
         r = footprint.ram_pct(n * 12, ws)
-        assert want <= r < want + 1e-3, (frac, r)
+        assert want <= r < want + 5e-3, (frac, r)   # + index arrays and split-search samples (DESIGN R7)
     assert gns.workspace_bytes(n, 0.7, True) == 0
 
 
@@ -86,7 +86,7 @@ def test_limited_buffer_fractions(gns):
     for p in (0.5, 0.25, 0.125, 1 / 16, 1 / 64):
         info = gns.plan(n, p, True)
         r = footprint.ram_pct(n * 12, info["workspace_bytes"])
-        assert 1 + p <= r < 1 + p + 1e-3, (p, r)
+        assert 1 + p <= r < 1 + p + 5e-3, (p, r)
         if prev is not None:
             assert info["element_passes"] >= prev
         prev = info["element_passes"]
