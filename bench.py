@@ -268,7 +268,7 @@ def main():
         ok_perm = ok_perm and bool((v[1:].to(torch.int64)[tie] > v[:-1].to(torch.int64)[tie]).all().item())
 
     # ------------------------------------------- per-kernel timing (roofline)
-    roof = kernel_roofline(gns, torch, dev, stream, src_k, src_v, k, v, n, hv, s, plan, restore)
+    roof = kernel_roofline(gns, torch, dev, stream, src_k, src_v, k, v, n, hv, s, plan, restore, ws, args.frac)
     peak, peak_src = measured_peaks()
     achieved = roof["merge_pass_gbs"]
     traffic = ncu_traffic(case, args.frac)
@@ -339,44 +339,27 @@ def launches(plan, frac, n):
     return plan["launches"]
 
 
-def kernel_roofline(gns, torch, dev, stream, src_k, src_v, k, v, n, hv, s, plan, restore, reps=5):
-    """Times each kernel of a 1.0-mode sort through the step-level C-ABI, with
-    CUDA events on the launching stream between launches (same kernels and
-    order as gns_sort: tile sort, then merge passes ping-ponging)."""
-    st = int(stream.cuda_stream)
-    T = plan["tile"]
-    M = plan["merge_passes"]
-    buf_k = torch.empty_like(k)
-    buf_v = torch.empty_like(v) if hv else None
-    mws = torch.empty(max(1, gns.gns_merge_workspace_bytes(n)), dtype=torch.uint8, device=dev)
-    tile_ms, merge_ms = [], []
+def kernel_roofline(gns, torch, dev, stream, src_k, src_v, k, v, n, hv, s, plan, restore, ws, frac, reps=5):
+    """Times every kernel of the product sort (gns_sort_*_ws, the same call the
+    timed region makes) with CUDA events recorded by the library on the
+    launching stream between launches (gns_timing_begin/end)."""
+    per = []
     for _ in range(reps):
         restore()
-        evs = [torch.cuda.Event(enable_timing=True) for _ in range(M + 2)]
-        cur_k, cur_v, oth_k, oth_v = (k, v, buf_k, buf_v) if M % 2 == 0 else (buf_k, buf_v, k, v)
-        evs[0].record(stream)
-        rc = gns.gns_tile_sort(k.data_ptr(), v.data_ptr() if hv else None, cur_k.data_ptr(),
-                               cur_v.data_ptr() if hv else None, n, st)
-        assert rc == 0, gns.gns_last_error_string()
-        evs[1].record(stream)
-        for p in range(M):
-            rc = gns.gns_merge_pass(cur_k.data_ptr(), cur_v.data_ptr() if hv else None, oth_k.data_ptr(),
-                                    oth_v.data_ptr() if hv else None, n, T << p, mws.data_ptr(),
-                                    mws.numel(), st)
-            assert rc == 0, gns.gns_last_error_string()
-            evs[p + 2].record(stream)
-            cur_k, cur_v, oth_k, oth_v = oth_k, oth_v, cur_k, cur_v
-        torch.cuda.synchronize()
-        tile_ms.append(evs[0].elapsed_time(evs[1]))
-        merge_ms.append([evs[p + 1].elapsed_time(evs[p + 2]) for p in range(M)])
-    tile = float(np.median(tile_ms))
-    per_pass = [float(np.median([r[p] for r in merge_ms])) for p in range(M)]
-    mavg = float(np.mean(per_pass)) if M else 0.0
-    total = tile + sum(per_pass)
-    return {"merge_pass_gbs": (2 * n * s) / (mavg / 1e3) / 1e9 if M else 0.0,
-            "merge_share": sum(per_pass) / total if total else 0.0,
-            "per_kernel_ms": {"tile_sort": tile, "merge_passes": per_pass,
-                              "tile_sort_gbs": (2 * n * s) / (tile / 1e3) / 1e9}}
+        assert gns.gns_timing_begin(256) == 0
+        gns.sort_(k, v, frac, workspace=ws, stream=stream)
+        per.append(gns.gns_timing_end())
+    kinds = [kd for kd, _ in per[0]]
+    med = [float(np.median([r[i][1] for r in per])) for i in range(len(kinds))]
+    tile = [t for kd, t in zip(kinds, med) if kd == 1]
+    merge = [t for kd, t in zip(kinds, med) if kd == 2]
+    total = sum(med)
+    mavg = float(np.mean(merge)) if merge else 0.0
+    return {"merge_pass_gbs": (2 * n * s) / (mavg / 1e3) / 1e9 if merge else 0.0,
+            "merge_share": sum(merge) / total if total else 0.0,
+            "per_kernel_ms": {"tile_sort": sum(tile), "merge_passes": merge,
+                              "tile_sort_gbs": (2 * n * s) / (sum(tile) / 1e3) / 1e9 if tile else 0.0,
+                              "launches": [[gns.LAUNCH_KINDS.get(kd, "other"), t] for kd, t in zip(kinds, med)]}}
 
 
 def ncu_traffic(case, frac):

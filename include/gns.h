@@ -153,6 +153,21 @@ gns_status gns_merge_inplace_top(double *keys, uint32_t *vals, const double *lef
                                  const uint32_t *left_vals, size_t nl, size_t n,
                                  void *ws, size_t ws_bytes, gns_stream_t stream);
 
+/* ---- launch timing (measurement) ---------------------------
+ * gns_timing_begin(max_launches): until gns_timing_end, every kernel this
+ * library launches FROM THE CALLING THREAD is bracketed by CUDA events recorded
+ * on the launching stream (one before the first launch, one after each).  The
+ * events serialise the launches (no programmatic overlap), so use it for
+ * per-kernel shares, not for whole-sort timing.  Launches beyond max_launches
+ * (1..4096) are not timed.  GNS_ERR_INVALID_ARGUMENT if already on.
+ * gns_timing_end(ms, kind, cap): waits for the last event, writes up to cap
+ * per-launch durations (milliseconds) and kinds (1 tile sort, 2 merge pass,
+ * 3 co-rank partition, 4 in-place dependency ranges, 5 in-place merge,
+ * 6 reversal, 0 other) in launch order, turns timing off and returns the number
+ * of timed launches (-1 if timing was off or an event failed). */
+gns_status gns_timing_begin(int max_launches);
+int gns_timing_end(float *ms, int *kind, int cap);
+
 /* Compile-time geometry of this build. */
 int gns_tile_elems(void);
 int gns_merge_tile_elems(void);

@@ -68,6 +68,8 @@ _c = {
     "gns_merge_workspace_bytes": _sig("gns_merge_workspace_bytes", [_sz], _sz),
     "gns_merge_pass": _sig("gns_merge_pass", [_vp, _vp, _vp, _vp, _sz, _sz, _vp, _sz, _vp]),
     "gns_merge_inplace_top": _sig("gns_merge_inplace_top", [_vp, _vp, _vp, _vp, _sz, _sz, _vp, _sz, _vp]),
+    "gns_timing_begin": _sig("gns_timing_begin", [_i]),
+    "gns_timing_end": _sig("gns_timing_end", [ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_int), _i]),
     "gns_tile_elems": _sig("gns_tile_elems", []),
     "gns_merge_tile_elems": _sig("gns_merge_tile_elems", []),
     "gns_status_string": _sig("gns_status_string", [_i], ctypes.c_char_p),
@@ -139,6 +141,23 @@ def gns_merge_pass(src_k, src_v, dst_k, dst_v, n, run_len, ws, ws_bytes, stream)
 
 def gns_merge_inplace_top(keys, vals, left_k, left_v, nl, n, ws, ws_bytes, stream) -> int:
     return _c["gns_merge_inplace_top"](keys, vals, left_k, left_v, nl, n, ws, ws_bytes, stream)
+
+
+def gns_timing_begin(max_launches: int) -> int:
+    return _c["gns_timing_begin"](max_launches)
+
+
+def gns_timing_end(cap: int = 4096):
+    """Returns [(kind, ms), ...] of the launches timed since gns_timing_begin."""
+    ms = (ctypes.c_float * cap)()
+    kind = (ctypes.c_int * cap)()
+    n = _c["gns_timing_end"](ms, kind, cap)
+    if n < 0:
+        raise GnsError(GNS_OK, "gns_timing_end")
+    return [(kind[i], ms[i]) for i in range(min(n, cap))]
+
+
+LAUNCH_KINDS = {1: "tile_sort", 2: "merge_pass", 3: "partition", 4: "inplace_deps", 5: "inplace_merge", 6: "reverse"}
 
 
 def gns_tile_elems() -> int:

@@ -16,6 +16,7 @@
 #include <algorithm>
 #include <mutex>
 #include <string>
+#include <vector>
 
 using namespace gns;
 
@@ -216,6 +217,26 @@ int merge_stages()
     return v;
 }
 
+// Launch timing (gns_timing_begin/end): one CUDA event on the launching stream
+// before the first launch and after every launch of the calling thread.
+struct Timing {
+    bool on = false;
+    int cap = 0;
+    std::vector<cudaEvent_t> ev;     // pool
+    std::vector<int> kind;           // kind of launch i (between ev[i] and ev[i+1])
+    int used = 0;                    // events recorded
+};
+thread_local Timing g_timing;
+
+int launch_kind(const char *what)
+{
+    static const char *names[] = {"tile_sort2_kernel", "merge_tstore_kernel", "partition_kernel",
+                                  "inplace_deps_kernel", "merge_inplace_kernel", "reverse_kernel"};
+    for (int i = 0; i < 6; ++i)
+        if (std::strcmp(what, names[i]) == 0) return i + 1;
+    return 0;
+}
+
 template <typename... KArgs, typename... Args>
 gns_status launch_pdl(const char *what, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
                       cudaStream_t st, Args... args)
@@ -230,7 +251,15 @@ gns_status launch_pdl(const char *what, void (*kern)(KArgs...), dim3 grid, dim3 
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = pdl_enabled() ? 1 : 0;
-    return check(cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...), what);
+    Timing &T = g_timing;
+    const bool timed = T.on && T.used + 2 <= T.cap;
+    if (timed && T.used == 0) cudaEventRecord(T.ev[T.used++], st);
+    gns_status r = check(cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...), what);
+    if (timed && r == GNS_OK) {
+        T.kind[T.used - 1] = launch_kind(what);
+        cudaEventRecord(T.ev[T.used++], st);
+    }
+    return r;
 }
 
 // Row a2 (K1).
@@ -706,6 +735,40 @@ void gns_prof_read(unsigned long long *out)
     cudaMemcpyFromSymbol(out, g_prof, 16 * sizeof(unsigned long long));
 }
 #endif
+
+gns_status gns_timing_begin(int max_launches)
+{
+    Timing &T = g_timing;
+    if (T.on) return fail(GNS_ERR_INVALID_ARGUMENT, "timing already on");
+    if (max_launches <= 0 || max_launches > 4096) return fail(GNS_ERR_INVALID_ARGUMENT, "max_launches in 1..4096");
+    const int need = max_launches + 1;
+    while ((int)T.ev.size() < need) {
+        cudaEvent_t e;
+        GNS_TRY(check(cudaEventCreate(&e), "cudaEventCreate"));
+        T.ev.push_back(e);
+    }
+    T.kind.assign(need, 0);
+    T.cap = need;
+    T.used = 0;
+    T.on = true;
+    return GNS_OK;
+}
+
+int gns_timing_end(float *ms, int *kind, int cap)
+{
+    Timing &T = g_timing;
+    if (!T.on) return -1;
+    T.on = false;
+    const int n = T.used > 0 ? T.used - 1 : 0;
+    if (n > 0 && cudaEventSynchronize(T.ev[T.used - 1]) != cudaSuccess) return -1;
+    for (int i = 0; i < n && i < cap; ++i) {
+        float t = 0.f;
+        cudaEventElapsedTime(&t, T.ev[i], T.ev[i + 1]);
+        if (ms) ms[i] = t;
+        if (kind) kind[i] = T.kind[i];
+    }
+    return n;
+}
 
 int gns_tile_elems(void) { return TILE; }
 int gns_merge_tile_elems(void) { return MTILE; }
