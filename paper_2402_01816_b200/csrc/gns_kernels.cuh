@@ -142,6 +142,15 @@ __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, i
     asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
                  :: "r"(smem_u32(dst)), "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar)) : "memory");
 }
+// Shared-memory f64 load at a 32-bit shared address (volatile: two such loads
+// under complementary predicates stay two predicated LDS instead of one LDS
+// followed by four 32-bit selects).
+__device__ __forceinline__ double lds_f64(uint32_t a)
+{
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+    return v;
+}
 __device__ __forceinline__ void lds128(const void *p, double &a, double &b)
 {
     asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(a), "=d"(b) : "r"(smem_u32(p)));
@@ -885,8 +894,28 @@ constexpr size_t t1_smem(bool hv) { return T1_KEY_BYTES + (hv ? T1_VAL_BYTES : 0
 
 // merge-round layouts (blocked spill e = 32t + x and merge reads conflict-light)
 __device__ __forceinline__ int swm(int e) { return e ^ ((e >> 5) & 15); }
+// Tile-sort key layout on absolute shared byte addresses (the key array is
+// 1 KiB aligned): the 8-byte slot within each 128-byte line is XORed with bits
+// 8-11 of the address (the 32-key row), so the blocked spill (thread t writes
+// row t) and stride-16 merge reads spread over the banks.  Working on byte
+// addresses saves the index->address shift in the merge steps.
+__device__ __forceinline__ uint32_t swa(uint32_t a) { return a ^ ((a >> 5) & 0x78u); }
 __device__ __forceinline__ int swmv(int e) { return e ^ ((e >> 5) & 31); }
 struct SwM { __device__ __forceinline__ int operator()(int e) const { return swm(e); } };
+// merge_path_smem over the tile-sort layout (keys at swa(base + 8e)).
+template <bool DESC>
+__device__ __forceinline__ int merge_path_tile(uint32_t base, int a0, int na, int b0, int nb, int d)
+{
+    int lo = max(0, d - nb), hi = min(d, na);
+    while (lo < hi) {
+        const int m = (lo + hi) >> 1;
+        const double b = lds_f64(swa(base + 8u * (b0 + d - 1 - m)));
+        const double a = lds_f64(swa(base + 8u * (a0 + m)));
+        if (!before<DESC>(b, a)) lo = m + 1;
+        else hi = m;
+    }
+    return lo;
+}
 struct SwMV { __device__ __forceinline__ int operator()(int e) const { return swmv(e); } };
 // TMA 128-byte swizzle layouts (16-byte chunk c of row r stored at chunk c ^ (r & 7))
 __device__ __forceinline__ int tk_slot(int e)     // doubles, 16 per row
@@ -922,23 +951,38 @@ __device__ __forceinline__ void transpose_sort16(double (&k)[VT1], uint32_t (&v)
     }
 }
 
+
+// Serial merge of VT1 outputs for the tile sort's merge rounds.  Heads ka/kb,
+// indices ai/bi; B's head is taken only if strictly before A's (left wins
+// ties).  The next key of the consumed side is loaded straight into that
+// side's head register (predicated loads), so a step costs one compare, two
+// selects for the output, the index update and the swizzled address.
 template <bool HV, bool DESC>
 __device__ __forceinline__ void serial_merge32(const double *sk, const uint32_t *sv, int ai, int aend, int bi, int bend,
                                                double (&k)[VT1], uint32_t (&v)[VT1])
 {
     GNS_DASSERT(ai >= 0 && bi >= ai && bend <= TILE);
-    double ka = sk[swm(ai)], kb = sk[swm(bi)];
+    const uint32_t base = smem_u32(sk);
+    // heads as (unswizzled) byte addresses; guards compare addresses
+    uint32_t pa = base + 8u * ai, pb = base + 8u * bi;
+    const uint32_t pae = base + 8u * aend, pbe = base + 8u * bend;
+    double ka = lds_f64(swa(pa)), kb = lds_f64(swa(pb));
 #pragma unroll
     for (int x = 0; x < VT1; ++x) {
-        const bool p = (bi < bend) && ((ai >= aend) || before<DESC>(kb, ka));
+        const bool p = (pb < pbe) && ((pa >= pae) || before<DESC>(kb, ka));
         k[x] = p ? kb : ka;
-        const int src = p ? bi : ai;
-        if (HV) v[x] = sv[swmv(src)];
-        const int nxt = src + 1;
-        if (p) bi = nxt; else ai = nxt;
-        GNS_DASSERT(nxt >= 0 && nxt <= TILE);
-        const double kn = sk[swm(nxt)];
-        if (p) kb = kn; else ka = kn;
+        const uint32_t src = p ? pb : pa;
+        if (HV) v[x] = sv[swmv((int)((src - base) >> 3))];
+        const uint32_t nxt = src + 8u;
+        GNS_DASSERT(nxt >= base && nxt <= base + 8u * TILE);
+        const uint32_t a = swa(nxt);
+        if (p) {
+            pb = nxt;
+            kb = lds_f64(a);
+        } else {
+            pa = nxt;
+            ka = lds_f64(a);
+        }
     }
 }
 
@@ -1011,14 +1055,20 @@ tile_sort2_kernel(const double *src_k, const uint32_t *src_v, double *dst_k, uin
         }
         if (__syncthreads_or(bad) && tid == 0) atomicOr(unsorted, 1u);
     }
-    transpose_sort16<0, HV, DESC>(k, v);
-    transpose_sort16<16, HV, DESC>(k, v);
+#ifndef GNS_TS_EXP
+#define GNS_TS_EXP 0
+#endif
+    if (GNS_TS_EXP != 1) {   // (timing experiments only: 1 = no register sort, 2 = no smem merge rounds)
+        transpose_sort16<0, HV, DESC>(k, v);
+        transpose_sort16<16, HV, DESC>(k, v);
+    }
     __syncthreads();                       // the TMA-layout reads are done before the first spill
 #pragma unroll 1
-    for (int coop = 1; coop <= NT1; coop <<= 1) {
+    for (int coop = 1; coop <= (GNS_TS_EXP == 2 ? 1 : NT1); coop <<= 1) {
 #pragma unroll
         for (int x = 0; x < VT1; ++x) {
-            sk[swm(e0 + x)] = k[x];
+            *reinterpret_cast<double *>(reinterpret_cast<unsigned char *>(sk) +
+                                        (swa(smem_u32(sk) + 8u * (e0 + x)) - smem_u32(sk))) = k[x];
             if (HV) sv[swmv(e0 + x)] = v[x];
         }
         __syncthreads();
@@ -1030,7 +1080,7 @@ tile_sort2_kernel(const double *src_k, const uint32_t *src_v, double *dst_k, uin
             const int run = (coop >> 1) * VT1;
             const int b0 = a0 + run;
             const int d = local * VT1;
-            const int i = merge_path_smem<DESC>(sk, a0, run, b0, run, d, SwM());
+            const int i = merge_path_tile<DESC>(smem_u32(sk), a0, run, b0, run, d);
             serial_merge32<HV, DESC>(sk, sv, a0 + i, b0, b0 + d - i, b0 + run, k, v);
         }
         __syncthreads();
