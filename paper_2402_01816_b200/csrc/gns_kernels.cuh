@@ -63,9 +63,14 @@ __device__ __forceinline__ unsigned long long gtimer()
 constexpr int NT = 256;            // merge threads per CTA
 constexpr int VT = 16;             // outputs per merge thread
 constexpr int MTILE = NT * VT;     // K3/K4 output tile = 4096 elements
-constexpr int NT1 = 256;           // K1 threads per CTA
+#ifndef GNS_NT1
+#define GNS_NT1 256
+#endif
+constexpr int NT1 = GNS_NT1;       // K1 threads per CTA (two CTAs per SM)
 constexpr int VT1 = 32;            // K1 keys per thread
 constexpr int TILE = NT1 * VT1;    // K1 tile = 8192 elements (runs entering the merge passes)
+constexpr int TILE_LOG2 = NT1 == 512 ? 14 : NT1 == 256 ? 13 : 12;
+static_assert((1 << TILE_LOG2) == TILE, "TILE must be 4096, 8192 or 16384");
 static_assert(TILE % MTILE == 0, "pair boundaries must fall on merge-tile boundaries");
 
 // ---------------------------------------------------------------- global I/O
@@ -671,7 +676,7 @@ merge_tstore_kernel(PipeGeo pg, int ntiles, int per_cta, const __grid_constant__
 #ifdef GNS_PROF
     unsigned long long acc[16] = {};
     const long long t_entry = clock64();
-    const int tl_slot = min(31, 1 + (63 - __clzll(pg.g.L)) - 13);
+    const int tl_slot = min(31, 1 + (63 - __clzll(pg.g.L)) - TILE_LOG2);
 #endif
     pdl_wait();
     GNS_TL_START(tl_slot);
@@ -987,7 +992,7 @@ __device__ __forceinline__ void serial_merge32(const double *sk, const uint32_t 
 }
 
 template <bool HV, bool DESC>
-__global__ void __launch_bounds__(NT1, 2)
+__global__ void __launch_bounds__(NT1, 512 / NT1)
 tile_sort2_kernel(const double *src_k, const uint32_t *src_v, double *dst_k, uint32_t *dst_v, long long n,
                   const __grid_constant__ CUtensorMap ksrc, const __grid_constant__ CUtensorMap vsrc,
                   const __grid_constant__ CUtensorMap kdst, const __grid_constant__ CUtensorMap vdst,
