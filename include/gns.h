@@ -109,6 +109,26 @@ gns_status gns_sort_pairs_f64_u32_ws(double *keys, uint32_t *vals, size_t n,
 gns_status gns_sort_target_f64(double *keys, uint32_t *vals, size_t n, double buffer_fraction, gns_target target,
                                void *ws, size_t ws_bytes, gns_stream_t stream);
 
+/* NEXT f3: 8-byte key types.  All share the layout of the f64 path (keys
+ * 8-byte aligned words, 32-byte aligned array); only the order differs:
+ *   GNS_KEY_F64 binary64 under IEEE < (-0.0 == +0.0; NaN is a precondition
+ *               violation, R1), GNS_KEY_I64 two's-complement
+ *               int64, GNS_KEY_U64 uint64.
+ * Stability (ties keep input order for the Left targets) as above: the
+ * output is the unique stable permutation, bit-exact. */
+typedef enum {
+    GNS_KEY_F64 = 0,
+    GNS_KEY_I64 = 1,
+    GNS_KEY_U64 = 2
+} gns_key_type;
+
+/* The general entry point: keys of any gns_key_type, optional u32 payload,
+ * any target, optional workspace (as gns_sort_target_f64).  keys points to n
+ * 8-byte keys (double / int64_t / uint64_t).  GNS_ERR_INVALID_ARGUMENT for an
+ * unknown key_type or target; other errors as above. */
+gns_status gns_sort_keys(void *keys, gns_key_type key_type, uint32_t *vals, size_t n, double buffer_fraction,
+                         gns_target target, void *ws, size_t ws_bytes, gns_stream_t stream);
+
 /* Pass schedule of a sort (host only, no CUDA call). */
 typedef struct {
     int tile;                   /* gns_tile_elems(): elements per tile-sort CTA          */

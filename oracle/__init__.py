@@ -19,6 +19,10 @@ Functions and the passages they follow:
   DescRight (NEXT f3): the same mergesort, merge rule per
   target.  Pinned by brute force on (key, +-index) orders, the SPEC.md:72
   DescLeft example, and AscLeft == :func:`sort`.
+* :func:`sort_keys` — the same mergesort over 8-byte keys of type f64, i64
+  or u64 (NEXT f3, key types), any target.  Pinned by brute force over tiny
+  inputs with extreme values (INT64_MIN/MAX, 2^63, 2^64-1: sorting u64 as
+  i64 or f64 fails the pin) and ``numpy.argsort(kind="stable")``.
 * :func:`merge_runs` — one merge level over runs of length L.
   Pinned by the SPEC.md ``mergeKnuth`` examples and by brute force.
 * :mod:`oracle.footprint` — %RAM and tFootprint.  Pinned by the
@@ -63,6 +67,9 @@ def lib():
         L.oracle_sort_f64_u32.restype = ctypes.c_int
         L.oracle_sort_target.argtypes = [dp, up, ctypes.c_size_t, ctypes.c_int]
         L.oracle_sort_target.restype = ctypes.c_int
+        L.oracle_sort_keys.argtypes = [ctypes.POINTER(ctypes.c_uint64), up, ctypes.c_size_t, ctypes.c_int,
+                                       ctypes.c_int]
+        L.oracle_sort_keys.restype = ctypes.c_int
         L.oracle_merge_runs.argtypes = [dp, up, ctypes.c_size_t, ctypes.c_size_t, dp, up]
         L.oracle_merge_runs.restype = ctypes.c_int
         _lib = L
@@ -105,6 +112,26 @@ def sort_target(keys: np.ndarray, vals: Optional[np.ndarray], target: str
         raise OracleNaNError("NaN key")
     if rc != 0:
         raise ValueError("oracle_sort_target failed")
+    return k, v
+
+
+KEY_TYPES = {"f64": 0, "i64": 1, "u64": 2}
+_KEY_DTYPES = {"f64": np.float64, "i64": np.int64, "u64": np.uint64}
+
+
+def sort_keys(keys: np.ndarray, vals: Optional[np.ndarray], key_type: str, target: str = "AscLeft"
+              ) -> Tuple[np.ndarray, Optional[np.ndarray]]:
+    """Stable sort of 8-byte keys of ``key_type`` (f64 / i64 / u64) for one of
+    the four targets; returns sorted copies (keys in their own dtype)."""
+    k = np.array(keys, dtype=_KEY_DTYPES[key_type], copy=True, order="C")
+    v = None if vals is None else np.array(vals, dtype=np.uint32, copy=True, order="C")
+    kp = k.view(np.uint64).ctypes.data_as(ctypes.POINTER(ctypes.c_uint64))
+    up = v.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32)) if v is not None else None
+    rc = lib().oracle_sort_keys(kp, up, k.size, KEY_TYPES[key_type], TARGETS[target])
+    if rc == 1:
+        raise OracleNaNError("NaN key")
+    if rc != 0:
+        raise ValueError("oracle_sort_keys failed")
     return k, v
 
 

@@ -30,6 +30,11 @@
  * precede the left run's head in the target order, ties included for the
  * *Right targets (ties in reverse input order).  (NEXT f3.)
  *
+ * oracle_sort_keys(): the same plain mergesort and per-target merge rule over
+ * 8-byte keys of one of three types, given as bit patterns: binary64 under
+ * IEEE < (kt 0; NaN rejected), two's-complement int64 (kt 1), uint64 (kt 2).
+ * (NEXT f3, key types.)
+ *
  * oracle_merge_runs(): one merge *level* of the same mergesort over runs of
  * length L ("per recursion-level one read-scan with comparisons ... and one
  * write-scan") — the definition a single GPU merge pass must
@@ -126,6 +131,78 @@ int oracle_sort_target(double *keys, uint32_t *vals, size_t n, int target)
     uint32_t *tv = vals ? (uint32_t *)malloc(n * sizeof(uint32_t)) : NULL;
     if (!tk || (vals && !tv)) { free(tk); free(tv); return 2; }
     msort_t(keys, vals, tk, tv, 0, n, target);
+    free(tk);
+    free(tv);
+    return 0;
+}
+
+/* ---- 8-byte key types (bit patterns) ------------------------------------ */
+/* -1 / 0 / +1 as a <, ==, > b in key type kt (0 f64, 1 i64, 2 u64). */
+static int key_cmp(int kt, uint64_t a, uint64_t b)
+{
+    if (kt == 1) {
+        int64_t x = (int64_t)a, y = (int64_t)b;
+        return x < y ? -1 : (x > y ? 1 : 0);
+    }
+    if (kt == 2) return a < b ? -1 : (a > b ? 1 : 0);
+    double x, y;
+    memcpy(&x, &a, 8);
+    memcpy(&y, &b, 8);
+    return x < y ? -1 : (x > y ? 1 : 0);
+}
+
+/* the right head r goes before the left head l in the target order */
+static int take_right_k(int kt, int target, uint64_t l, uint64_t r)
+{
+    int c = key_cmp(kt, r, l);
+    switch (target) {
+    case 1: return c <= 0;
+    case 2: return c > 0;
+    case 3: return c >= 0;
+    default: return c < 0;
+    }
+}
+
+static void msort_k(uint64_t *k, uint32_t *v, uint64_t *tk, uint32_t *tv, size_t lo, size_t hi, int kt, int target)
+{
+    if (hi - lo <= 1) return;
+    size_t mid = lo + (hi - lo) / 2;
+    msort_k(k, v, tk, tv, lo, mid, kt, target);
+    msort_k(k, v, tk, tv, mid, hi, kt, target);
+    size_t i = lo, j = mid, o = lo;
+    while (i < mid && j < hi) {
+        if (take_right_k(kt, target, k[i], k[j])) {
+            tk[o] = k[j];
+            if (v) tv[o] = v[j];
+            ++j;
+        } else {
+            tk[o] = k[i];
+            if (v) tv[o] = v[i];
+            ++i;
+        }
+        ++o;
+    }
+    while (i < mid) { tk[o] = k[i]; if (v) tv[o] = v[i]; ++i; ++o; }
+    while (j < hi) { tk[o] = k[j]; if (v) tv[o] = v[j]; ++j; ++o; }
+    memcpy(k + lo, tk + lo, (hi - lo) * sizeof(uint64_t));
+    if (v) memcpy(v + lo, tv + lo, (hi - lo) * sizeof(uint32_t));
+}
+
+/* Returns 0, 1 on a NaN f64 key, 2 on OOM, 3 on a bad kt/target. */
+int oracle_sort_keys(uint64_t *keys, uint32_t *vals, size_t n, int kt, int target)
+{
+    if (kt < 0 || kt > 2 || target < 0 || target > 3) return 3;
+    if (kt == 0)
+        for (size_t i = 0; i < n; ++i) {
+            double x;
+            memcpy(&x, &keys[i], 8);
+            if (x != x) return 1;
+        }
+    if (n < 2) return 0;
+    uint64_t *tk = (uint64_t *)malloc(n * sizeof(uint64_t));
+    uint32_t *tv = vals ? (uint32_t *)malloc(n * sizeof(uint32_t)) : NULL;
+    if (!tk || (vals && !tv)) { free(tk); free(tv); return 2; }
+    msort_k(keys, vals, tk, tv, 0, n, kt, target);
     free(tk);
     free(tv);
     return 0;

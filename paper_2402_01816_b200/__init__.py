@@ -63,6 +63,7 @@ _c = {
     "gns_sort_f64_ws": _sig("gns_sort_f64_ws", [_vp, _sz, _d, _vp, _sz, _vp]),
     "gns_sort_pairs_f64_u32_ws": _sig("gns_sort_pairs_f64_u32_ws", [_vp, _vp, _sz, _d, _vp, _sz, _vp]),
     "gns_sort_target_f64": _sig("gns_sort_target_f64", [_vp, _vp, _sz, _d, _i, _vp, _sz, _vp]),
+    "gns_sort_keys": _sig("gns_sort_keys", [_vp, _i, _vp, _sz, _d, _i, _vp, _sz, _vp]),
     "gns_plan": _sig("gns_plan", [_sz, _d, _i, ctypes.POINTER(gns_plan_info)]),
     "gns_tile_sort": _sig("gns_tile_sort", [_vp, _vp, _vp, _vp, _sz, _vp]),
     "gns_merge_workspace_bytes": _sig("gns_merge_workspace_bytes", [_sz], _sz),
@@ -119,6 +120,13 @@ TARGETS = {"AscLeft": 0, "AscRight": 1, "DescLeft": 2, "DescRight": 3}
 
 def gns_sort_target_f64(keys_ptr, vals_ptr, n, buffer_fraction, target, ws_ptr, ws_bytes, stream) -> int:
     return _c["gns_sort_target_f64"](keys_ptr, vals_ptr, n, buffer_fraction, target, ws_ptr, ws_bytes, stream)
+
+
+KEY_TYPES = {"f64": 0, "i64": 1, "u64": 2}
+
+
+def gns_sort_keys(keys_ptr, key_type, vals_ptr, n, buffer_fraction, target, ws_ptr, ws_bytes, stream) -> int:
+    return _c["gns_sort_keys"](keys_ptr, key_type, vals_ptr, n, buffer_fraction, target, ws_ptr, ws_bytes, stream)
 
 
 def gns_plan(n: int, buffer_fraction: float, with_vals: bool) -> gns_plan_info:
@@ -190,10 +198,22 @@ def _ptr(t) -> Optional[int]:
     return int(t.data_ptr())
 
 
-def _check_keys(keys, vals):
+def _key_type(keys) -> int:
     import torch
-    if keys.dtype != torch.float64 or not keys.is_cuda or not keys.is_contiguous():
+    kt = {torch.float64: 0, torch.int64: 1, torch.uint64: 2}.get(keys.dtype)
+    if kt is None:
+        raise TypeError("keys must be float64, int64 or uint64")
+    return kt
+
+
+def _check_keys(keys, vals, any_key_type: bool = False):
+    import torch
+    if any_key_type:
+        _key_type(keys)
+    elif keys.dtype != torch.float64:
         raise TypeError("keys must be a contiguous CUDA float64 tensor")
+    if not keys.is_cuda or not keys.is_contiguous():
+        raise TypeError("keys must be a contiguous CUDA tensor")
     if vals is not None:
         if vals.dtype != torch.uint32 or not vals.is_cuda or not vals.is_contiguous():
             raise TypeError("vals must be a contiguous CUDA uint32 tensor")
@@ -206,11 +226,18 @@ def sort_(keys, vals=None, buffer_fraction: float = 1.0, workspace=None, stream=
     with ties in input order unless ``target`` names another of the four API
     targets (AscLeft, AscRight, DescLeft, DescRight).
 
+    ``keys``: float64, int64 or uint64 (NEXT f3 key types, via gns_sort_keys).
     ``workspace``: optional uint8 CUDA tensor of >= workspace_bytes(...) bytes;
     without it the library allocates its buffer stream-ordered."""
-    _check_keys(keys, vals)
+    _check_keys(keys, vals, any_key_type=True)
     n = keys.numel()
     st = _stream_handle(stream)
+    kt = _key_type(keys)
+    if kt != 0:
+        wp = _ptr(workspace) if workspace is not None else None
+        wb = workspace.numel() * workspace.element_size() if workspace is not None else 0
+        _check(gns_sort_keys(_ptr(keys), kt, _ptr(vals), n, buffer_fraction, TARGETS[target], wp, wb, st), "sort_")
+        return keys, vals
     if target != "AscLeft":
         wp = _ptr(workspace) if workspace is not None else None
         wb = workspace.numel() * workspace.element_size() if workspace is not None else 0

@@ -115,6 +115,37 @@ size_t merge_ws(size_t n)
            align_up((nt + 1) * sizeof(unsigned), 256);
 }
 
+// Kernel instances by payload (hv) and order ORD = DESC | key type << 1
+// (ord_of): 3 key types x 2 directions.
+constexpr int NORD = 6;
+using TileK = decltype(&tile_sort2_kernel<false, 0>);
+using MergeK = decltype(&merge_tstore_kernel<false, 0>);
+using InplK = decltype(&merge_inplace_kernel<false, 0>);
+using PartK = decltype(&partition_kernel<0>);
+#define GNS_ORDS(K, HV) {&K<HV, 0>, &K<HV, 1>, &K<HV, 2>, &K<HV, 3>, &K<HV, 4>, &K<HV, 5>}
+TileK tile_kern(bool hv, int o)
+{
+    static const TileK t[2][NORD] = {GNS_ORDS(tile_sort2_kernel, false), GNS_ORDS(tile_sort2_kernel, true)};
+    return t[hv][o];
+}
+MergeK merge_kern(bool hv, int o)
+{
+    static const MergeK t[2][NORD] = {GNS_ORDS(merge_tstore_kernel, false), GNS_ORDS(merge_tstore_kernel, true)};
+    return t[hv][o];
+}
+InplK inplace_kern(bool hv, int o)
+{
+    static const InplK t[2][NORD] = {GNS_ORDS(merge_inplace_kernel, false), GNS_ORDS(merge_inplace_kernel, true)};
+    return t[hv][o];
+}
+PartK partition_kern(int o)
+{
+    static const PartK t[NORD] = {&partition_kernel<0>, &partition_kernel<1>, &partition_kernel<2>,
+                                  &partition_kernel<3>, &partition_kernel<4>, &partition_kernel<5>};
+    return t[o];
+}
+#undef GNS_ORDS
+
 // Per-device one-time kernel attributes (dynamic shared memory > 48 KB).
 std::mutex g_attr_mu;
 unsigned long long g_attr_done = 0;   // bit per device ordinal
@@ -129,20 +160,13 @@ gns_status ensure_attrs()
     if (g_attr_done & (1ull << dev)) return GNS_OK;
 #define GNS_ATTR(K, BYTES) \
     GNS_TRY(check(cudaFuncSetAttribute(K, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(BYTES)), "attr"))
-    GNS_ATTR((merge_tstore_kernel<true, false>), ts_smem(true));
-    GNS_ATTR((merge_tstore_kernel<false, false>), ts_smem(false));
-    GNS_ATTR((merge_tstore_kernel<true, true>), ts_smem(true));
-    GNS_ATTR((merge_tstore_kernel<false, true>), ts_smem(false));
-    GNS_ATTR((merge_tstore_kernel<false, false, 3>), ts_smem(false, 3));
-    GNS_ATTR((merge_tstore_kernel<false, true, 3>), ts_smem(false, 3));
-    GNS_ATTR((merge_inplace_kernel<true, false>), ts_smem(true));
-    GNS_ATTR((merge_inplace_kernel<false, false>), ts_smem(false));
-    GNS_ATTR((merge_inplace_kernel<true, true>), ts_smem(true));
-    GNS_ATTR((merge_inplace_kernel<false, true>), ts_smem(false));
-    GNS_ATTR((tile_sort2_kernel<true, false>), t1_smem(true));
-    GNS_ATTR((tile_sort2_kernel<false, false>), t1_smem(false));
-    GNS_ATTR((tile_sort2_kernel<true, true>), t1_smem(true));
-    GNS_ATTR((tile_sort2_kernel<false, true>), t1_smem(false));
+    for (int o = 0; o < NORD; ++o) {
+        for (int hv = 0; hv < 2; ++hv) {
+            GNS_ATTR(merge_kern(hv, o), ts_smem(hv));
+            GNS_ATTR(inplace_kern(hv, o), ts_smem(hv));
+            GNS_ATTR(tile_kern(hv, o), t1_smem(hv));
+        }
+    }
 #undef GNS_ATTR
     GNS_TRY(check(cudaDeviceGetAttribute(&g_num_sms[dev], cudaDevAttrMultiProcessorCount, dev), "sm count"));
     g_attr_done |= (1ull << dev);
@@ -207,16 +231,6 @@ bool pdl_enabled()
     return on;
 }
 
-// A/B knob for experiments: GNS_MERGE_STAGES=3 (key-only merge pass).
-int merge_stages()
-{
-    static const int v = [] {
-        const char *e = std::getenv("GNS_MERGE_STAGES");
-        return e ? std::atoi(e) : 2;
-    }();
-    return v;
-}
-
 // Launch timing (gns_timing_begin/end): one CUDA event on the launching stream
 // before the first launch and after every launch of the calling thread.
 struct Timing {
@@ -263,7 +277,7 @@ gns_status launch_pdl(const char *what, void (*kern)(KArgs...), dim3 grid, dim3 
 }
 
 // Row a2 (K1).
-gns_status launch_tile_sort(const double *sk, const uint32_t *sv, double *dk, uint32_t *dv, size_t n, bool desc,
+gns_status launch_tile_sort(const double *sk, const uint32_t *sv, double *dk, uint32_t *dv, size_t n, int ord,
                             cudaStream_t st, unsigned *unsorted = nullptr, double *smp = nullptr)
 {
     if (n == 0) return GNS_OK;
@@ -281,8 +295,7 @@ gns_status launch_tile_sort(const double *sk, const uint32_t *sv, double *dk, ui
     }
     const uint32_t *svv = hv ? sv : nullptr;
     uint32_t *dvv = hv ? dv : nullptr;
-    auto kern = hv ? (desc ? tile_sort2_kernel<true, true> : tile_sort2_kernel<true, false>)
-                   : (desc ? tile_sort2_kernel<false, true> : tile_sort2_kernel<false, false>);
+    auto kern = tile_kern(hv, ord);
     return launch_pdl("tile_sort2_kernel", kern, grid, NT1, t1_smem(hv), st, sk, svv, dk, dvv, (long long)n, m[0],
                       m[1], m[2], m[3], unsorted, smp);
 }
@@ -290,7 +303,7 @@ gns_status launch_tile_sort(const double *sk, const uint32_t *sv, double *dk, ui
 // Rows a3+a4 (fused K2+K3, persistent TMA pipeline) or, in place, a6 (K2 +
 // dependency ranges + K4 with the ticket/flag protocol).
 gns_status launch_merge(const MergeGeo &g, const double *lim_a, const double *lim_b, int *corank, int2 *deps,
-                        unsigned *flags, bool inplace, bool desc, cudaStream_t st, const unsigned *unsorted = nullptr,
+                        unsigned *flags, bool inplace, int ord, cudaStream_t st, const unsigned *unsorted = nullptr,
                         const double *copy_k = nullptr, const uint32_t *copy_v = nullptr)
 {
     const int ntiles = (int)ceil_div((size_t)g.n, MTILE);
@@ -305,21 +318,17 @@ gns_status launch_merge(const MergeGeo &g, const double *lim_a, const double *li
         const int ctas = std::min(ntiles, 2 * num_sms());
         const int per = (int)ceil_div(ntiles, ctas);
         const int grid = (int)ceil_div(ntiles, per);
-        const int ns = (!hv && merge_stages() == 3) ? 3 : 2;
-        auto kern = hv ? (desc ? merge_tstore_kernel<true, true> : merge_tstore_kernel<true, false>)
-                       : ns == 3 ? (desc ? merge_tstore_kernel<false, true, 3> : merge_tstore_kernel<false, false, 3>)
-                                 : (desc ? merge_tstore_kernel<false, true> : merge_tstore_kernel<false, false>);
-        return launch_pdl("merge_tstore_kernel", kern, grid, WS_THREADS, ts_smem(hv, ns), st, pg, ntiles, per, map,
+        auto kern = merge_kern(hv, ord);
+        return launch_pdl("merge_tstore_kernel", kern, grid, WS_THREADS, ts_smem(hv), st, pg, ntiles, per, map,
                           unsorted, copy_k, copy_v);
     }
-    GNS_TRY(launch_pdl("partition_kernel", desc ? partition_kernel<true> : partition_kernel<false>,
+    GNS_TRY(launch_pdl("partition_kernel", partition_kern(ord),
                        (unsigned)ceil_div((size_t)ntiles * 32, 256), 256, 0, st, g, ntiles, corank));
     GNS_TRY(launch_pdl("inplace_deps_kernel", inplace_deps_kernel, (unsigned)ceil_div(ntiles + 1, 256), 256, 0, st,
                        (const int *)corank, ntiles, g.L, g.n, deps, flags));
     unsigned *ticket = flags + ntiles;
     const int grid = std::min(ntiles, 2 * num_sms());
-    auto kern = hv ? (desc ? merge_inplace_kernel<true, true> : merge_inplace_kernel<true, false>)
-                   : (desc ? merge_inplace_kernel<false, true> : merge_inplace_kernel<false, false>);
+    auto kern = inplace_kern(hv, ord);
     return launch_pdl("merge_inplace_kernel", kern, grid, NT, ts_smem(hv), st, pg, ntiles, (const int *)corank,
                       (const int2 *)deps, flags, ticket, map);
 }
@@ -359,7 +368,7 @@ MergeGeo uniform_geo(const double *sk, const uint32_t *sv, double *dk, uint32_t 
 // no copy pass is ever needed (an odd number of merge levels starts from P).
 // smp: two sample arrays of >= len/SMP_G + 2 keys (R's and P's), or nullptr.
 gns_status sort_range(double *rk, uint32_t *rv, double *pk_, uint32_t *pv_, size_t len,
-                      bool final_in_partner, int *corank, bool desc, cudaStream_t st, unsigned *unsorted = nullptr,
+                      bool final_in_partner, int *corank, int ord, cudaStream_t st, unsigned *unsorted = nullptr,
                       double *smp_r = nullptr, double *smp_p = nullptr)
 {
     if (len == 0) return GNS_OK;
@@ -376,13 +385,13 @@ gns_status sort_range(double *rk, uint32_t *rv, double *pk_, uint32_t *pv_, size
     if (unsorted && M > 0) GNS_TRY(check(cudaMemsetAsync(unsorted, 0, sizeof(unsigned), st), "memset"));
     double *cs = tile_to_partner ? smp_p : smp_r;      // samples of the region holding the current runs
     double *os = tile_to_partner ? smp_r : smp_p;
-    GNS_TRY(launch_tile_sort(rk, rv, ck, cv, len, desc, st, M > 0 ? unsorted : nullptr, M > 0 ? cs : nullptr));
+    GNS_TRY(launch_tile_sort(rk, rv, ck, cv, len, ord, st, M > 0 ? unsorted : nullptr, M > 0 ? cs : nullptr));
     for (int p = 0; p < M; ++p) {
         const size_t L = (size_t)TILE << p;
         MergeGeo g = uniform_geo(ck, cv, ok, ov, len, L, cs, p + 1 < M ? os : nullptr);
         const bool last = p == M - 1;
         const bool need_copy = last && (tile_k != ok);   // presorted data must end where the sort ends
-        GNS_TRY(launch_merge(g, ck + len, ck + len, corank, nullptr, nullptr, false, desc, st, unsorted,
+        GNS_TRY(launch_merge(g, ck + len, ck + len, corank, nullptr, nullptr, false, ord, st, unsorted,
                              need_copy ? tile_k : nullptr, need_copy ? tile_v : nullptr));
         std::swap(ck, ok);
         std::swap(cv, ov);
@@ -424,7 +433,7 @@ gns_status validate_data(const double *keys, const uint32_t *vals, bool hv, size
 // Ordered in-place merge of A = buffer[0:nl) and B = data[lo+nl : lo+len)
 // into data[lo : lo+len) (row a6, K2 + deps + K4).
 gns_status top_merge(double *keys, uint32_t *vals, double *bk, uint32_t *bv, size_t lo, size_t len, size_t nl,
-                     int *corank, int2 *deps, unsigned *flags, bool desc, cudaStream_t st)
+                     int *corank, int2 *deps, unsigned *flags, int ord, cudaStream_t st)
 {
     const bool hv = vals != nullptr;
     MergeGeo g;
@@ -441,7 +450,7 @@ gns_status top_merge(double *keys, uint32_t *vals, double *bk, uint32_t *bv, siz
     g.tpp_log2 = 0;
     g.sa = nullptr;
     g.so = nullptr;
-    return launch_merge(g, bk + nl, keys + lo + len, corank, deps, flags, true, desc, st);
+    return launch_merge(g, bk + nl, keys + lo + len, corank, deps, flags, true, ord, st);
 }
 
 // One step of a limited-buffer sort, also used by gns_plan to count element passes.
@@ -465,7 +474,7 @@ void count_sort_range(size_t len, Sched *sc, size_t n)
 // data[lo+b : lo+len) is sorted first (recursively, same buffer), then the
 // left b elements are sorted into the buffer and merged in place.
 gns_status sort_limited(double *keys, uint32_t *vals, size_t lo, size_t len, size_t b, double *bk, uint32_t *bv,
-                        int *corank, int2 *deps, unsigned *flags, bool desc, cudaStream_t st, Sched *sc, size_t n,
+                        int *corank, int2 *deps, unsigned *flags, int ord, cudaStream_t st, Sched *sc, size_t n,
                         double *s0 = nullptr, double *s1 = nullptr)
 {
     const bool hv = vals != nullptr;
@@ -476,7 +485,7 @@ gns_status sort_limited(double *keys, uint32_t *vals, size_t lo, size_t len, siz
             count_sort_range(len, sc, n);
             return GNS_OK;
         }
-        return launch_tile_sort(dk, dv, dk, dv, len, desc, st);
+        return launch_tile_sort(dk, dv, dk, dv, len, ord, st);
     }
     const size_t nl = left_len(len);
     if (b >= nl) {
@@ -488,34 +497,35 @@ gns_status sort_limited(double *keys, uint32_t *vals, size_t lo, size_t len, siz
             sc->launches += 3;
             return GNS_OK;
         }
-        GNS_TRY(sort_range(dk, dv, bk, bv, nl, true, corank, desc, st, nullptr, s0, s1));
-        GNS_TRY(sort_range(dk + nl, hv ? dv + nl : nullptr, dk, dv, nr, false, corank, desc, st, nullptr, s0, s1));
-        return top_merge(keys, vals, bk, bv, lo, len, nl, corank, deps, flags, desc, st);
+        GNS_TRY(sort_range(dk, dv, bk, bv, nl, true, corank, ord, st, nullptr, s0, s1));
+        GNS_TRY(sort_range(dk + nl, hv ? dv + nl : nullptr, dk, dv, nr, false, corank, ord, st, nullptr, s0, s1));
+        return top_merge(keys, vals, bk, bv, lo, len, nl, corank, deps, flags, ord, st);
     }
-    GNS_TRY(sort_limited(keys, vals, lo + b, len - b, b, bk, bv, corank, deps, flags, desc, st, sc, n, s0, s1));
+    GNS_TRY(sort_limited(keys, vals, lo + b, len - b, b, bk, bv, corank, deps, flags, ord, st, sc, n, s0, s1));
     if (sc) {
         count_sort_range(b, sc, n);
         sc->elem_passes += (double)len / (double)n;
         sc->launches += 3;
         return GNS_OK;
     }
-    GNS_TRY(sort_range(dk, dv, bk, bv, b, true, corank, desc, st, nullptr, s0, s1));
-    return top_merge(keys, vals, bk, bv, lo, len, b, corank, deps, flags, desc, st);
+    GNS_TRY(sort_range(dk, dv, bk, bv, b, true, corank, ord, st, nullptr, s0, s1));
+    return top_merge(keys, vals, bk, bv, lo, len, b, corank, deps, flags, ord, st);
 }
 
 // The sort proper (rows a1..a7).  ws already validated and sized.
 // target: 0 AscLeft, 1 AscRight, 2 DescLeft, 3 DescRight (NEXT f3).
 // AscRight = reverse(DescLeft), DescRight = reverse(AscLeft).
-gns_status run_sort(double *keys, uint32_t *vals, size_t n, const Mode &m, unsigned char *ws, int target,
+// kt: key type (0 f64, 1 i64, 2 u64; NEXT f3).
+gns_status run_sort(double *keys, uint32_t *vals, size_t n, const Mode &m, unsigned char *ws, int target, int kt,
                     cudaStream_t st)
 {
     if (n <= 1) return GNS_OK;
     GNS_TRY(ensure_attrs());
     const bool hv = vals != nullptr;
     const bool right = target == 1 || target == 3;
-    const bool desc = (target == 2) || (target == 1);   // AscRight is reverse(DescLeft)
+    const int ord = ord_of((target == 2) || (target == 1), kt);   // AscRight is reverse(DescLeft)
     if (n <= (size_t)TILE) {   // one tile: in place, no buffer
-        GNS_TRY(launch_tile_sort(keys, vals, keys, vals, n, desc, st));
+        GNS_TRY(launch_tile_sort(keys, vals, keys, vals, n, ord, st));
     } else {
         const Layout Lo = layout(n, m, hv);
         double *bk = reinterpret_cast<double *>(ws + Lo.off_k);
@@ -524,11 +534,11 @@ gns_status run_sort(double *keys, uint32_t *vals, size_t n, const Mode &m, unsig
         double *smp = reinterpret_cast<double *>(ws + Lo.off_smp);
         if (!m.limited) {
             unsigned *unsorted = reinterpret_cast<unsigned *>(ws + Lo.off_adapt);
-            GNS_TRY(sort_range(keys, vals, bk, bv, n, false, corank, desc, st, unsorted, smp, smp + Lo.nsmp));
+            GNS_TRY(sort_range(keys, vals, bk, bv, n, false, corank, ord, st, unsorted, smp, smp + Lo.nsmp));
         } else {
             int2 *deps = reinterpret_cast<int2 *>(ws + Lo.off_deps);
             unsigned *flags = reinterpret_cast<unsigned *>(ws + Lo.off_flags);
-            GNS_TRY(sort_limited(keys, vals, 0, n, m.buf, bk, bv, corank, deps, flags, desc, st, nullptr, n, smp,
+            GNS_TRY(sort_limited(keys, vals, 0, n, m.buf, bk, bv, corank, deps, flags, ord, st, nullptr, n, smp,
                                  smp + Lo.nsmp));
         }
     }
@@ -536,7 +546,8 @@ gns_status run_sort(double *keys, uint32_t *vals, size_t n, const Mode &m, unsig
     return GNS_OK;
 }
 
-gns_status sort_alloc(double *keys, uint32_t *vals, bool hv, size_t n, double frac, int target, cudaStream_t st)
+gns_status sort_alloc(double *keys, uint32_t *vals, bool hv, size_t n, double frac, int target, cudaStream_t st,
+                      int kt = KT_F64)
 {
     Mode m;
     GNS_TRY(mode_for(frac, n, &m));
@@ -552,7 +563,7 @@ gns_status sort_alloc(double *keys, uint32_t *vals, bool hv, size_t n, double fr
             return check(e, "cudaMallocAsync");
         }
     }
-    gns_status s = run_sort(keys, hv ? vals : nullptr, n, m, ws, target, st);
+    gns_status s = run_sort(keys, hv ? vals : nullptr, n, m, ws, target, kt, st);
     if (ws) {
         gns_status f = check(cudaFreeAsync(ws, st), "cudaFreeAsync");
         if (s == GNS_OK) s = f;
@@ -561,7 +572,7 @@ gns_status sort_alloc(double *keys, uint32_t *vals, bool hv, size_t n, double fr
 }
 
 gns_status sort_ws(double *keys, uint32_t *vals, bool hv, size_t n, double frac, void *ws, size_t ws_bytes,
-                   int target, cudaStream_t st)
+                   int target, cudaStream_t st, int kt = KT_F64)
 {
     Mode m;
     GNS_TRY(mode_for(frac, n, &m));
@@ -572,7 +583,7 @@ gns_status sort_ws(double *keys, uint32_t *vals, bool hv, size_t n, double frac,
         if (!ws || ws_bytes < Lo.total) return fail(GNS_ERR_WORKSPACE_TOO_SMALL, "workspace too small");
         if (!is_aligned(ws, 32)) return fail(GNS_ERR_MISALIGNED, "ws must be 32-byte aligned");
     }
-    return run_sort(keys, hv ? vals : nullptr, n, m, (unsigned char *)ws, target, st);
+    return run_sort(keys, hv ? vals : nullptr, n, m, (unsigned char *)ws, target, kt, st);
 }
 
 }  // namespace
@@ -619,6 +630,18 @@ gns_status gns_sort_target_f64(double *keys, uint32_t *vals, size_t n, double bu
     return sort_alloc(keys, vals, vals != nullptr, n, buffer_fraction, (int)target, (cudaStream_t)stream);
 }
 
+gns_status gns_sort_keys(void *keys, gns_key_type key_type, uint32_t *vals, size_t n, double buffer_fraction,
+                         gns_target target, void *ws, size_t ws_bytes, gns_stream_t stream)
+{
+    if ((int)target < 0 || (int)target > 3) return fail(GNS_ERR_INVALID_ARGUMENT, "target must be 0..3");
+    if ((int)key_type < 0 || (int)key_type > 2) return fail(GNS_ERR_INVALID_ARGUMENT, "key_type must be 0..2");
+    double *k = (double *)keys;
+    if (ws) return sort_ws(k, vals, vals != nullptr, n, buffer_fraction, ws, ws_bytes, (int)target,
+                           (cudaStream_t)stream, (int)key_type);
+    return sort_alloc(k, vals, vals != nullptr, n, buffer_fraction, (int)target, (cudaStream_t)stream,
+                      (int)key_type);
+}
+
 gns_status gns_plan(size_t n, double buffer_fraction, int with_vals, gns_plan_info *out)
 {
     Mode m;
@@ -637,7 +660,7 @@ gns_status gns_plan(size_t n, double buffer_fraction, int with_vals, gns_plan_in
     } else if (n <= (size_t)TILE || !m.limited) {
         count_sort_range(n, &sc, n);
     } else {
-        sort_limited(nullptr, nullptr, 0, n, m.buf, nullptr, nullptr, nullptr, nullptr, nullptr, false, 0, &sc, n);
+        sort_limited(nullptr, nullptr, 0, n, m.buf, nullptr, nullptr, nullptr, nullptr, nullptr, 0, 0, &sc, n);
     }
     out->element_passes = sc.elem_passes;
     out->launches = sc.launches;
@@ -658,7 +681,7 @@ gns_status gns_tile_sort(const double *src_keys, const uint32_t *src_vals, doubl
     GNS_TRY(validate_data(dst_keys, dst_vals, hv, n));
     if (n == 0) return GNS_OK;
     GNS_TRY(ensure_attrs());
-    return launch_tile_sort(src_keys, src_vals, dst_keys, dst_vals, n, false, (cudaStream_t)stream);
+    return launch_tile_sort(src_keys, src_vals, dst_keys, dst_vals, n, 0, (cudaStream_t)stream);
 }
 
 size_t gns_merge_workspace_bytes(size_t n) { return merge_ws(n); }
@@ -677,7 +700,7 @@ gns_status gns_merge_pass(const double *src_keys, const uint32_t *src_vals, doub
     if (!ws || ws_bytes < merge_ws(n)) return fail(GNS_ERR_WORKSPACE_TOO_SMALL, "workspace too small");
     GNS_TRY(ensure_attrs());
     MergeGeo g = uniform_geo(src_keys, src_vals, dst_keys, dst_vals, n, run_len);
-    return launch_merge(g, src_keys + n, src_keys + n, (int *)ws, nullptr, nullptr, false, false, (cudaStream_t)stream);
+    return launch_merge(g, src_keys + n, src_keys + n, (int *)ws, nullptr, nullptr, false, 0, (cudaStream_t)stream);
 }
 
 gns_status gns_merge_inplace_top(double *keys, uint32_t *vals, const double *left_keys,
@@ -711,7 +734,7 @@ gns_status gns_merge_inplace_top(double *keys, uint32_t *vals, const double *lef
     g.tpp_log2 = 0;
     g.sa = nullptr;
     g.so = nullptr;
-    return launch_merge(g, left_keys + nl, keys + n, corank, deps, flags, true, false, (cudaStream_t)stream);
+    return launch_merge(g, left_keys + nl, keys + n, corank, deps, flags, true, 0, (cudaStream_t)stream);
 }
 
 #ifdef GNS_PROF

@@ -224,21 +224,52 @@ __device__ __forceinline__ void store_segment(double *ok, uint32_t *ov, long lon
 // Key order of the sort target: ascending (AscLeft) or
 // descending (DescLeft); ties always keep input order (the left run wins).
 // The *Right targets are the reversal of the opposite-direction Left target
-// (gns.cu).  before<DESC>(x, y): x must be output strictly before y.
-template <bool DESC>
-__device__ __forceinline__ bool before(double x, double y) { return DESC ? (x > y) : (x < y); }
+// (gns.cu).  before<ORD>(x, y): x must be output strictly before y.
+// ORD = DESC | (key type << 1): key types (NEXT f3) share the 8-byte layout;
+// keys travel as double bit patterns and are compared as binary64 (GNS_KEY_F64,
+// IEEE <: -0.0 == +0.0), two's-complement int64 (GNS_KEY_I64) or uint64
+// (GNS_KEY_U64).
+constexpr int KT_F64 = 0, KT_I64 = 1, KT_U64 = 2;
+constexpr int ord_of(bool desc, int kt) { return (desc ? 1 : 0) | (kt << 1); }
+template <int ORD>
+__device__ __forceinline__ bool before(double x, double y)
+{
+    constexpr bool DESC = ORD & 1;
+    constexpr int KT = ORD >> 1;
+    if (KT == KT_I64) {
+        const long long a = __double_as_longlong(x), b = __double_as_longlong(y);
+        return DESC ? (a > b) : (a < b);
+    } else if (KT == KT_U64) {
+        const unsigned long long a = (unsigned long long)__double_as_longlong(x);
+        const unsigned long long b = (unsigned long long)__double_as_longlong(y);
+        return DESC ? (a > b) : (a < b);
+    }
+    return DESC ? (x > y) : (x < y);
+}
+// A key no real key sorts after (ties with it keep real keys first because
+// pads are placed after every real key): +inf / -inf, INT64_MAX / MIN,
+// UINT64_MAX / 0.
+template <int ORD>
+__device__ __forceinline__ double pad_key()
+{
+    constexpr bool DESC = ORD & 1;
+    constexpr int KT = ORD >> 1;
+    if (KT == KT_I64) return __longlong_as_double(DESC ? (long long)0x8000000000000000ULL : 0x7FFFFFFFFFFFFFFFLL);
+    if (KT == KT_U64) return __longlong_as_double(DESC ? 0LL : (long long)0xFFFFFFFFFFFFFFFFULL);
+    return __longlong_as_double(DESC ? (long long)0xFFF0000000000000ULL : 0x7FF0000000000000LL);
+}
 
 // Stable co-rank (merge path) of diagonal d for sorted runs A[0:na), B[0:nb)
 // in shared memory: the number of A elements among the first d outputs of the
 // stable merge in which A (the left run) wins ties (Knuth's merge;
 // SPEC.md:290).  Predicate: A[m] <= B[d-1-m]  =>  the m-th A element precedes.
-template <bool DESC, class IX>
+template <int ORD, class IX>
 __device__ __forceinline__ int merge_path_smem(const double *s, int a0, int na, int b0, int nb, int d, IX ix)
 {
     int lo = max(0, d - nb), hi = min(d, na);
     while (lo < hi) {
         int m = (lo + hi) >> 1;
-        if (!before<DESC>(s[ix(b0 + d - 1 - m)], s[ix(a0 + m)])) lo = m + 1;
+        if (!before<ORD>(s[ix(b0 + d - 1 - m)], s[ix(a0 + m)])) lo = m + 1;
         else hi = m;
     }
     return lo;
@@ -248,7 +279,7 @@ __device__ __forceinline__ int merge_path_smem(const double *s, int a0, int na, 
 // index bi (ends aend/bend, exclusive).  B's head is taken only if strictly
 // smaller than A's (left wins ties).  Reads one slot past a run end at most
 // (the shared arrays carry spare slots; the value is never used).
-template <bool HV, bool DESC, class IK, class IV>
+template <bool HV, int ORD, class IK, class IV>
 __device__ __forceinline__ void serial_merge(const double *sk, const uint32_t *sv, int ai, int aend,
                                              int bi, int bend, double (&k)[VT], uint32_t (&v)[VT],
                                              IK ik, IV iv)
@@ -257,7 +288,7 @@ __device__ __forceinline__ void serial_merge(const double *sk, const uint32_t *s
     double ka = sk[ik(ai)], kb = sk[ik(bi)];
 #pragma unroll
     for (int x = 0; x < VT; ++x) {
-        const bool p = (bi < bend) && ((ai >= aend) || before<DESC>(kb, ka));
+        const bool p = (bi < bend) && ((ai >= aend) || before<ORD>(kb, ka));
         k[x] = p ? kb : ka;
         const int src = p ? bi : ai;
         if (HV) v[x] = sv[iv(src)];
@@ -325,7 +356,7 @@ __device__ __forceinline__ TileSpan tile_span(const MergeGeo &g, int t)
 // "parallelize over an arbitrary number of processes".
 // Warp-cooperative stable co-rank of tile t's first diagonal (all 32 lanes
 // return the result).
-template <bool DESC>
+template <int ORD>
 __device__ __forceinline__ int warp_corank(const MergeGeo &g, int t, int lane)
 {
     const TileSpan s = tile_span(g, t);
@@ -344,7 +375,7 @@ __device__ __forceinline__ int warp_corank(const MergeGeo &g, int t, int lane)
             nprobe = 32;
         }
         bool p = false;
-        if (lane < nprobe) p = !before<DESC>(B[d - 1 - m], A[m]);
+        if (lane < nprobe) p = !before<ORD>(B[d - 1 - m], A[m]);
         const unsigned bal = __ballot_sync(0xFFFFFFFFu, p);
         const int c = __popc(bal);
         const int m_prev = __shfl_sync(0xFFFFFFFFu, m, (c > 0 ? c - 1 : 0));
@@ -359,7 +390,7 @@ __device__ __forceinline__ int warp_corank(const MergeGeo &g, int t, int lane)
 
 // Co-rank search by a group of W lanes (W = 16: two independent searches per
 // warp, (W+1)-ary).  `gl` = lane within the group; `mask` = the group's lanes.
-template <int W, bool DESC>
+template <int W, int ORD>
 __device__ __forceinline__ int group_corank(const MergeGeo &g, int t, int gl, unsigned mask, int gbase)
 {
     const TileSpan s = tile_span(g, t);
@@ -380,7 +411,7 @@ __device__ __forceinline__ int group_corank(const MergeGeo &g, int t, int gl, un
             nprobe = W;
         }
         bool p = false;
-        if (gl < nprobe) p = !before<DESC>(B[d - 1 - m], A[m]);
+        if (gl < nprobe) p = !before<ORD>(B[d - 1 - m], A[m]);
         const unsigned bal = (__ballot_sync(mask, p) & mask) >> gbase;
         const int c = __popc(bal);
         const int m_prev = __shfl_sync(mask, m, gbase + (c > 0 ? c - 1 : 0));
@@ -440,7 +471,7 @@ __device__ __forceinline__ int group_count_true(int lo, int hi, int gl, unsigned
 
 // Stable co-rank of tile t's first diagonal by a group of W lanes, sample-guided
 // when the pass has samples (uniform passes), else over the whole range.
-template <int W, bool DESC>
+template <int W, int ORD>
 __device__ __forceinline__ int tile_corank(const MergeGeo &g, int t, int gl, unsigned mask, int gbase)
 {
     const TileSpan s = tile_span(g, t);
@@ -457,7 +488,7 @@ __device__ __forceinline__ int tile_corank(const MergeGeo &g, int t, int gl, uns
             const double *SB = g.sa + ((s.pbase + g.L) >> SMP_LOG2);
             const int cnt = group_count_true<W>(s_lo, s_hi, gl, mask, gbase, [&](int sx) {
                 const int yb = (d - 1 - (sx << SMP_LOG2)) >> SMP_LOG2;
-                return !before<DESC>(SB[yb], SA[sx]);
+                return !before<ORD>(SB[yb], SA[sx]);
             });
             if (cnt > 0) lo = max(lo, ((s_lo + cnt - 1) << SMP_LOG2) + 1);
             if (s_lo + cnt <= s_hi) hi = min(hi, ((s_lo + cnt) << SMP_LOG2) + SMP_G);
@@ -465,10 +496,10 @@ __device__ __forceinline__ int tile_corank(const MergeGeo &g, int t, int gl, uns
     }
     // exact: number of m in [lo, hi) with A[m] <= B[d-1-m]
     return lo + group_count_true<W>(lo, hi - 1, gl, mask, gbase,
-                                    [&](int m) { return !before<DESC>(B[d - 1 - m], A[m]); });
+                                    [&](int m) { return !before<ORD>(B[d - 1 - m], A[m]); });
 }
 
-template <bool DESC>
+template <int ORD>
 __global__ void __launch_bounds__(256)
 partition_kernel(MergeGeo g, int ntiles, int *__restrict__ corank)
 {
@@ -477,7 +508,7 @@ partition_kernel(MergeGeo g, int ntiles, int *__restrict__ corank)
     const int warp = (int)((blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5);
     const int lane = threadIdx.x & 31;
     if (warp >= ntiles) return;
-    const int c = warp_corank<DESC>(g, warp, lane);
+    const int c = warp_corank<ORD>(g, warp, lane);
     if (lane == 0) corank[warp] = c;
 }
 
@@ -668,7 +699,7 @@ constexpr int MERGE_WARPS = NT / 32;                 // 8
 constexpr int PRODUCER_WARP = MERGE_WARPS;           // 8
 constexpr int WS_THREADS = NT + 32 + 32 * SEARCH_WARPS;   // 352
 
-template <bool HV, bool DESC, int NS = 2>
+template <bool HV, int ORD, int NS = 2>
 __global__ void __launch_bounds__(WS_THREADS, 2)
 merge_tstore_kernel(PipeGeo pg, int ntiles, int per_cta, const __grid_constant__ CUtensorMap omap,
                     const unsigned *unsorted, const double *copy_k, const uint32_t *copy_v)
@@ -757,7 +788,7 @@ merge_tstore_kernel(PipeGeo pg, int ntiles, int per_cta, const __grid_constant__
             const int j = j0 + h;
             while (j0 + 1 - spl_used >= SPL_RING) { __nanosleep(64); }
             if (j < nspl) {
-                const int c = tile_corank<16, DESC>(pg.g, first + j, gl, mask, 16 * h);
+                const int c = tile_corank<16, ORD>(pg.g, first + j, gl, mask, 16 * h);
                 if (gl == 0) publish(j, c);
             }
             __syncwarp();
@@ -820,7 +851,7 @@ merge_tstore_kernel(PipeGeo pg, int ntiles, int per_cta, const __grid_constant__
 
     // ---------------------------------------------------- merge warps 0-7
     if (warp < init) {
-        const int c = tile_corank<32, DESC>(pg.g, first + warp, lane, 0xFFFFFFFFu, 0);
+        const int c = tile_corank<32, ORD>(pg.g, first + warp, lane, 0xFFFFFFFFu, 0);
         if (lane == 0) publish(warp, c);
     }
 #ifdef GNS_PROF
@@ -842,8 +873,8 @@ merge_tstore_kernel(PipeGeo pg, int ntiles, int per_cta, const __grid_constant__
         const uint32_t *sv = svb(st);
         double k[VT];
         uint32_t v[VT];
-        const int ii = merge_path_smem<DESC>(sk, mt.offa, mt.ca, mt.bslot, mt.cb, d, Lin());
-        serial_merge<HV, DESC>(sk, sv, mt.offa + ii, mt.offa + mt.ca, mt.bslot + d - ii, mt.bslot + mt.cb, k, v,
+        const int ii = merge_path_smem<ORD>(sk, mt.offa, mt.ca, mt.bslot, mt.cb, d, Lin());
+        serial_merge<HV, ORD>(sk, sv, mt.offa + ii, mt.offa + mt.ca, mt.bslot + d - ii, mt.bslot + mt.cb, k, v,
                                Lin(), Lin());
         const long long t = first + i;
         const long long row = t * (MTILE / 16) + tid;    // global row of this thread's 16 outputs
@@ -908,7 +939,7 @@ __device__ __forceinline__ uint32_t swa(uint32_t a) { return a ^ ((a >> 5) & 0x7
 __device__ __forceinline__ int swmv(int e) { return e ^ ((e >> 5) & 31); }
 struct SwM { __device__ __forceinline__ int operator()(int e) const { return swm(e); } };
 // merge_path_smem over the tile-sort layout (keys at swa(base + 8e)).
-template <bool DESC>
+template <int ORD>
 __device__ __forceinline__ int merge_path_tile(uint32_t base, int a0, int na, int b0, int nb, int d)
 {
     int lo = max(0, d - nb), hi = min(d, na);
@@ -916,7 +947,7 @@ __device__ __forceinline__ int merge_path_tile(uint32_t base, int a0, int na, in
         const int m = (lo + hi) >> 1;
         const double b = lds_f64(swa(base + 8u * (b0 + d - 1 - m)));
         const double a = lds_f64(swa(base + 8u * (a0 + m)));
-        if (!before<DESC>(b, a)) lo = m + 1;
+        if (!before<ORD>(b, a)) lo = m + 1;
         else hi = m;
     }
     return lo;
@@ -934,14 +965,14 @@ __device__ __forceinline__ int tv_slot(int e)     // u32, 32 per row
     return (r << 5) | ((((e >> 2) & 7) ^ (r & 7)) << 2) | (e & 3);
 }
 
-template <int O, bool HV, bool DESC>
+template <int O, bool HV, int ORD>
 __device__ __forceinline__ void transpose_sort16(double (&k)[VT1], uint32_t (&v)[VT1])
 {
 #pragma unroll
     for (int r = 0; r < 16; ++r) {
 #pragma unroll
         for (int i = r & 1; i + 1 < 16; i += 2) {
-            const bool p = before<DESC>(k[O + i + 1], k[O + i]);
+            const bool p = before<ORD>(k[O + i + 1], k[O + i]);
             const double lo = p ? k[O + i + 1] : k[O + i];
             const double hi = p ? k[O + i] : k[O + i + 1];
             k[O + i] = lo;
@@ -962,7 +993,7 @@ __device__ __forceinline__ void transpose_sort16(double (&k)[VT1], uint32_t (&v)
 // ties).  The next key of the consumed side is loaded straight into that
 // side's head register (predicated loads), so a step costs one compare, two
 // selects for the output, the index update and the swizzled address.
-template <bool HV, bool DESC>
+template <bool HV, int ORD>
 __device__ __forceinline__ void serial_merge32(const double *sk, const uint32_t *sv, int ai, int aend, int bi, int bend,
                                                double (&k)[VT1], uint32_t (&v)[VT1])
 {
@@ -974,7 +1005,7 @@ __device__ __forceinline__ void serial_merge32(const double *sk, const uint32_t 
     double ka = lds_f64(swa(pa)), kb = lds_f64(swa(pb));
 #pragma unroll
     for (int x = 0; x < VT1; ++x) {
-        const bool p = (pb < pbe) && ((pa >= pae) || before<DESC>(kb, ka));
+        const bool p = (pb < pbe) && ((pa >= pae) || before<ORD>(kb, ka));
         k[x] = p ? kb : ka;
         const uint32_t src = p ? pb : pa;
         if (HV) v[x] = sv[swmv((int)((src - base) >> 3))];
@@ -991,7 +1022,7 @@ __device__ __forceinline__ void serial_merge32(const double *sk, const uint32_t 
     }
 }
 
-template <bool HV, bool DESC>
+template <bool HV, int ORD>
 __global__ void __launch_bounds__(NT1, 512 / NT1)
 tile_sort2_kernel(const double *src_k, const uint32_t *src_v, double *dst_k, uint32_t *dst_v, long long n,
                   const __grid_constant__ CUtensorMap ksrc, const __grid_constant__ CUtensorMap vsrc,
@@ -1040,8 +1071,7 @@ tile_sort2_kernel(const double *src_k, const uint32_t *src_v, double *dst_k, uin
             const bool ok = e < cnt;
             // pads sort after every real key (+inf ascending, -inf descending;
             // real infinities come first among ties because pads are last)
-            k[x] = ok ? src_k[base + e] : __longlong_as_double(DESC ? (long long)0xFFF0000000000000ULL
-                                                                    : 0x7FF0000000000000LL);
+            k[x] = ok ? src_k[base + e] : pad_key<ORD>();
             if (HV) v[x] = ok ? src_v[base + e] : 0u;
         }
     }
@@ -1052,11 +1082,11 @@ tile_sort2_kernel(const double *src_k, const uint32_t *src_v, double *dst_k, uin
         // and the key after them (the next thread's first, or the next tile's).
         bool bad = false;
 #pragma unroll
-        for (int x = 0; x + 1 < VT1; ++x) bad |= before<DESC>(k[x + 1], k[x]);
+        for (int x = 0; x + 1 < VT1; ++x) bad |= before<ORD>(k[x + 1], k[x]);
         const long long nx = base + e0 + VT1;
         if (nx < n) {
             const double kn = (full && e0 + VT1 < TILE) ? sk[tk_slot(e0 + VT1)] : src_k[nx];
-            bad |= before<DESC>(kn, k[VT1 - 1]);
+            bad |= before<ORD>(kn, k[VT1 - 1]);
         }
         if (__syncthreads_or(bad) && tid == 0) atomicOr(unsorted, 1u);
     }
@@ -1064,8 +1094,8 @@ tile_sort2_kernel(const double *src_k, const uint32_t *src_v, double *dst_k, uin
 #define GNS_TS_EXP 0
 #endif
     if (GNS_TS_EXP != 1) {   // (timing experiments only: 1 = no register sort, 2 = no smem merge rounds)
-        transpose_sort16<0, HV, DESC>(k, v);
-        transpose_sort16<16, HV, DESC>(k, v);
+        transpose_sort16<0, HV, ORD>(k, v);
+        transpose_sort16<16, HV, ORD>(k, v);
     }
     __syncthreads();                       // the TMA-layout reads are done before the first spill
 #pragma unroll 1
@@ -1078,15 +1108,15 @@ tile_sort2_kernel(const double *src_k, const uint32_t *src_v, double *dst_k, uin
         }
         __syncthreads();
         if (coop == 1) {                   // merge the thread's own two sorted halves
-            serial_merge32<HV, DESC>(sk, sv, e0, e0 + 16, e0 + 16, e0 + 32, k, v);
+            serial_merge32<HV, ORD>(sk, sv, e0, e0 + 16, e0 + 16, e0 + 32, k, v);
         } else {
             const int local = tid & (coop - 1);
             const int a0 = (tid - local) * VT1;
             const int run = (coop >> 1) * VT1;
             const int b0 = a0 + run;
             const int d = local * VT1;
-            const int i = merge_path_tile<DESC>(smem_u32(sk), a0, run, b0, run, d);
-            serial_merge32<HV, DESC>(sk, sv, a0 + i, b0, b0 + d - i, b0 + run, k, v);
+            const int i = merge_path_tile<ORD>(smem_u32(sk), a0, run, b0, run, d);
+            serial_merge32<HV, ORD>(sk, sv, a0 + i, b0, b0 + d - i, b0 + run, k, v);
         }
         __syncthreads();
     }
@@ -1137,7 +1167,7 @@ tile_sort2_kernel(const double *src_k, const uint32_t *src_v, double *dst_k, uin
 // range intersects its write range (deps[], inplace_deps_kernel).  Later tiles
 // never intersect: k1(t) <= nl + j1(t) <= nl + j0(u) for u > t.  Deadlock-free:
 // the smallest tile in flight only depends on tiles whose loads have landed.
-template <bool HV, bool DESC>
+template <bool HV, int ORD>
 __global__ void __launch_bounds__(NT, 2)
 merge_inplace_kernel(PipeGeo pg, int ntiles, const int *__restrict__ corank, const int2 *__restrict__ deps,
                      unsigned *flags, unsigned *ticket, const __grid_constant__ CUtensorMap omap)
@@ -1192,8 +1222,8 @@ merge_inplace_kernel(PipeGeo pg, int ntiles, const int *__restrict__ corank, con
         const uint32_t *sv = svb(st);
         double k[VT];
         uint32_t v[VT];
-        const int ii = merge_path_smem<DESC>(sk, mt.offa, mt.ca, mt.bslot, mt.cb, d, Lin());
-        serial_merge<HV, DESC>(sk, sv, mt.offa + ii, mt.offa + mt.ca, mt.bslot + d - ii, mt.bslot + mt.cb, k, v,
+        const int ii = merge_path_smem<ORD>(sk, mt.offa, mt.ca, mt.bslot, mt.cb, d, Lin());
+        serial_merge<HV, ORD>(sk, sv, mt.offa + ii, mt.offa + mt.ca, mt.bslot + d - ii, mt.bslot + mt.cb, k, v,
                                Lin(), Lin());
         const long long row = (long long)tcur * (MTILE / 16) + tid;
         __syncthreads();                                       // stage st fully read

@@ -114,3 +114,14 @@ def test_argument_errors_before_any_cuda_call(gns):
     assert gns.gns_status_string(6) == "GNS_ERR_MISALIGNED"
     assert gns.gns_sort_f64(264, 10, 1.0, None) == 6
     assert "aligned" in gns.gns_last_error_string()
+
+
+def test_sort_keys_argument_errors(gns):
+    """gns_sort_keys (NEXT f3 key types): unknown key type / target rejected
+    before any CUDA call; the f64/i64/u64 paths share the alignment rules."""
+    assert gns.gns_sort_keys(256, 3, None, 10, 1.0, 0, None, 0, None) == 1
+    assert gns.gns_sort_keys(256, -1, None, 10, 1.0, 0, None, 0, None) == 1
+    assert gns.gns_sort_keys(256, 1, None, 10, 1.0, 4, None, 0, None) == 1
+    assert gns.gns_sort_keys(264, 2, None, 10, 1.0, 0, None, 0, None) == 6
+    assert gns.gns_sort_keys(256, 1, None, 10, 0.75, 0, None, 0, None) == 2
+    assert gns.gns_sort_keys(None, 2, None, 0, 1.0, 0, None, 0, None) == 0

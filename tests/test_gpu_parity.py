@@ -284,3 +284,55 @@ def test_nan_memory_safe(gns):
     for frac in (1.0, 0.5):
         gpu_sort(gns, k, v, frac)
     check_against_oracle(gns, synth.uniform(n, 4), v, 0.5, what="after NaN")
+
+
+def _int_keys(key_type, n, seed):
+    """Seeded 8-byte integer keys with ties and the type's extreme values."""
+    rng = np.random.default_rng(seed)
+    if key_type == "i64":
+        lo, hi = np.iinfo(np.int64).min, np.iinfo(np.int64).max
+        k = rng.integers(lo, hi, n, dtype=np.int64, endpoint=True)
+        k[::9] = rng.integers(-20, 20, k[::9].size)          # heavy ties around zero
+        ext = np.array([lo, hi, -1, 0, 1], dtype=np.int64)
+    else:
+        hi = np.iinfo(np.uint64).max
+        k = rng.integers(0, hi, n, dtype=np.uint64, endpoint=True)
+        k[::9] = rng.integers(0, 40, k[::9].size).astype(np.uint64)
+        ext = np.array([0, 1, 1 << 63, (1 << 63) - 1, hi], dtype=np.uint64)
+    k[::17] = ext[np.arange(k[::17].size) % ext.size]
+    return k
+
+
+@pytest.mark.parametrize("key_type", ["i64", "u64"])
+@pytest.mark.parametrize("target", ["AscLeft", "DescLeft", "AscRight", "DescRight"])
+@pytest.mark.parametrize("frac", [1.0, 0.5, 0.25])
+@pytest.mark.parametrize("n", [1, 777, T1, 3 * T1 + 5, 100003, (1 << 18) + 3])
+def test_int_key_types(gns, n, frac, target, key_type):
+    """NEXT f3: int64 / uint64 keys (gns_sort_keys) vs the oracle, bit-exact,
+    with payload and key-only, every target and buffer mode."""
+    k = _int_keys(key_type, n, 4000 + n)
+    v = synth.iota_u32(n)
+    ek, ev = oracle.sort_keys(k, v, key_type, target)
+    tk, tv = to_dev(k, v)
+    gns.sort_(tk, tv, frac, target=target)
+    torch.cuda.synchronize()
+    assert np.array_equal(tk.cpu().numpy(), ek), f"{key_type} {target} n={n} p={frac} keys"
+    assert np.array_equal(tv.cpu().numpy(), ev), f"{key_type} {target} n={n} p={frac} payload"
+    tk, _ = to_dev(k, None)
+    gns.sort_(tk, None, frac, target=target)
+    torch.cuda.synchronize()
+    assert np.array_equal(tk.cpu().numpy(), ek), f"{key_type} {target} n={n} p={frac} key-only"
+
+
+def test_key_type_f64_through_sort_keys(gns):
+    """gns_sort_keys with GNS_KEY_F64 is the f64 path (same result as sort_)."""
+    n = 3 * T1 + 11
+    k = synth.ties(n, 77, 50)
+    k[::5] *= -1.0
+    v = synth.iota_u32(n)
+    tk, tv = to_dev(k, v)
+    rc = gns.gns_sort_keys(tk.data_ptr(), 0, tv.data_ptr(), n, 1.0, 0, None, 0, 0)
+    assert rc == 0
+    torch.cuda.synchronize()
+    ek, ev = oracle.sort(k, v)
+    assert_bitexact(tk.cpu().numpy(), ek, tv.cpu().numpy(), ev)

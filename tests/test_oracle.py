@@ -248,3 +248,51 @@ def test_targets_relations_and_golden():
         gk, gt = oracle.sort_target(np.array(ex["keys"], dtype=np.float64),
                                     np.array(ex["tags"], dtype=np.uint32), ex["target"])
         assert list(gk) == ex["out_keys"] and list(gt) == ex["out_tags"], ex["cite"]
+
+
+# ------------------------------------------------- NEXT f3: 8-byte key types
+I64_EXTREMES = (np.iinfo(np.int64).min, -1, 0, 1, np.iinfo(np.int64).max)
+U64_EXTREMES = (0, 1, 1 << 63, (1 << 64) - 1)
+
+
+@pytest.mark.parametrize("key_type,alphabet", [("i64", I64_EXTREMES[:3] + I64_EXTREMES[4:]),
+                                               ("u64", U64_EXTREMES)])
+@pytest.mark.parametrize("target", ["AscLeft", "DescRight"])
+def test_int_keys_exhaustive_vs_brute_force(key_type, alphabet, target):
+    """Brute force over every sequence of length <= 5 drawn from values at the
+    ends of the type's range: treating u64 as i64 (or either as f64) puts
+    2^63 / 2^64-1 / INT64_MIN in the wrong place and fails here."""
+    dt = np.int64 if key_type == "i64" else np.uint64
+    for n in range(0, 6):
+        for seq in itertools.product(alphabet, repeat=n):
+            keys = np.array([int(x) for x in seq], dtype=dt)
+            tags = np.arange(n, dtype=np.uint32)
+            ek, et = brute_target([int(x) for x in keys], list(tags), target)   # Python ints: exact order
+            gk, gt = oracle.sort_keys(keys, tags, key_type, target)
+            assert [int(x) for x in gk] == ek and list(gt) == et, (key_type, target, seq)
+
+
+@pytest.mark.parametrize("key_type", ["f64", "i64", "u64"])
+def test_key_types_vs_numpy_stable(key_type):
+    rng = np.random.default_rng(11)
+    n = 20000
+    if key_type == "f64":
+        keys = rng.integers(-50, 50, n).astype(np.float64)
+    elif key_type == "i64":
+        keys = rng.integers(np.iinfo(np.int64).min, np.iinfo(np.int64).max, n, dtype=np.int64, endpoint=True)
+        keys[::7] = keys[3]                                     # ties
+    else:
+        keys = rng.integers(0, np.iinfo(np.uint64).max, n, dtype=np.uint64, endpoint=True)
+        keys[::5] = keys[2]
+    vals = np.arange(n, dtype=np.uint32)
+    order = np.argsort(keys, kind="stable")
+    gk, gv = oracle.sort_keys(keys, vals, key_type)
+    assert np.array_equal(gk, keys[order]) and np.array_equal(gv, vals[order])
+    # descending-left: stable sort by the reversed order, ties in input order
+    rk, rv = oracle.sort_keys(keys, vals, key_type, "DescLeft")
+    if key_type == "f64":
+        order_d = np.argsort(-keys, kind="stable")
+    else:
+        order_d = np.lexsort((np.arange(n), [-int(x) for x in keys])) if key_type == "u64" else \
+            np.argsort(-keys.astype(object), kind="stable")
+    assert [int(x) for x in rk] == [int(x) for x in keys[order_d]] and np.array_equal(rv, vals[order_d])
