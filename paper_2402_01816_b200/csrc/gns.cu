@@ -303,8 +303,7 @@ gns_status launch_tile_sort(const double *sk, const uint32_t *sv, double *dk, ui
 // Rows a3+a4 (fused K2+K3, persistent TMA pipeline) or, in place, a6 (K2 +
 // dependency ranges + K4 with the ticket/flag protocol).
 gns_status launch_merge(const MergeGeo &g, const double *lim_a, const double *lim_b, int *corank, int2 *deps,
-                        unsigned *flags, bool inplace, int ord, cudaStream_t st, const unsigned *unsorted = nullptr,
-                        const double *copy_k = nullptr, const uint32_t *copy_v = nullptr)
+                        unsigned *flags, bool inplace, int ord, cudaStream_t st, Adapt ad = Adapt{})
 {
     const int ntiles = (int)ceil_div((size_t)g.n, MTILE);
     const bool hv = g.av != nullptr;
@@ -319,8 +318,7 @@ gns_status launch_merge(const MergeGeo &g, const double *lim_a, const double *li
         const int per = (int)ceil_div(ntiles, ctas);
         const int grid = (int)ceil_div(ntiles, per);
         auto kern = merge_kern(hv, ord);
-        return launch_pdl("merge_tstore_kernel", kern, grid, WS_THREADS, ts_smem(hv), st, pg, ntiles, per, map,
-                          unsorted, copy_k, copy_v);
+        return launch_pdl("merge_tstore_kernel", kern, grid, WS_THREADS, ts_smem(hv), st, pg, ntiles, per, map, ad);
     }
     GNS_TRY(launch_pdl("partition_kernel", partition_kern(ord),
                        (unsigned)ceil_div((size_t)ntiles * 32, 256), 256, 0, st, g, ntiles, corank));
@@ -390,9 +388,33 @@ gns_status sort_range(double *rk, uint32_t *rv, double *pk_, uint32_t *pv_, size
         const size_t L = (size_t)TILE << p;
         MergeGeo g = uniform_geo(ck, cv, ok, ov, len, L, cs, p + 1 < M ? os : nullptr);
         const bool last = p == M - 1;
-        const bool need_copy = last && (tile_k != ok);   // presorted data must end where the sort ends
-        GNS_TRY(launch_merge(g, ck + len, ck + len, corank, nullptr, nullptr, false, ord, st, unsorted,
-                             need_copy ? tile_k : nullptr, need_copy ? tile_v : nullptr));
+        Adapt ad{};
+        ad.flag = unsorted;
+        if (unsorted) {
+            // ordered input: the tile sort's output must end where the sort ends
+            if (last && tile_k != ok) {
+                ad.pre_k = tile_k;
+                ad.pre_v = tile_v;
+            }
+            // strictly reversed input: tile-order reversal into the final
+            // array in the last pass, or (tile output already there, even M)
+            // reversal into the other array in pass M-2, then a copy back
+            const bool tile_final = tile_k == (final_in_partner ? pk_ : rk);
+            if (!tile_final && last) {
+                ad.rev_k = tile_k;
+                ad.rev_v = tile_v;
+                ad.rev_gather = 1;
+            } else if (tile_final && p == M - 2) {
+                ad.rev_k = tile_k;
+                ad.rev_v = tile_v;
+                ad.rev_gather = 1;
+            } else if (tile_final && last) {
+                ad.rev_k = ck;
+                ad.rev_v = cv;
+                ad.rev_gather = 0;
+            }
+        }
+        GNS_TRY(launch_merge(g, ck + len, ck + len, corank, nullptr, nullptr, false, ord, st, ad));
         std::swap(ck, ok);
         std::swap(cv, ov);
         std::swap(cs, os);

@@ -105,6 +105,7 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 
 // ---- mbarrier + TMA bulk copy (cp.async.bulk, SASS UBLKCP) helpers
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 __device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count)
 {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(bar)), "r"(count) : "memory");
@@ -697,12 +698,48 @@ constexpr size_t ts_stage_bytes(bool hv) { return TS_KEY_SLOTS * 8 + (hv ? TS_VA
 constexpr size_t ts_smem(bool hv, int ns = 2) { return ns * ts_stage_bytes(hv) + 1024; }
 constexpr int MERGE_WARPS = NT / 32;                 // 8
 constexpr int PRODUCER_WARP = MERGE_WARPS;           // 8
+// NEXT f2 adaptivity of the full-buffer sort, decided on the device from the
+// tile sort's flag word (bit 0: some descent, bit 1: some adjacent pair not
+// strictly reversed).  The host schedules, per merge pass, what an ordered or
+// strictly reversed input needs instead of the merge: a copy of the tile
+// sort's output into this pass's destination (pre_*) and, for a reversed
+// input, a tile-order reversal (gather) or a copy (rev_*).
+struct Adapt {
+    const unsigned *flag;         // nullptr: no adaptivity
+    const double *pre_k;          // ordered input: copy source, or nullptr
+    const uint32_t *pre_v;
+    const double *rev_k;          // strictly reversed input: source, or nullptr
+    const uint32_t *rev_v;
+    int rev_gather;               // 1: out[j] = tile-sorted src at 2tT + c_t - n + j; 0: plain copy
+};
+
+// The CTA's share of the output [lo, hi).  gather: the stable sort of a
+// strictly reversed input is its reversal; tile t of src holds input tile t
+// sorted (= reversed), so out[j] = src[2tT + c_t - n + j] with
+// t = (n-1-j) / T and c_t = min(T, n - tT) (contiguous within each tile).
+template <bool HV>
+__device__ void adapt_move(const MergeGeo &g, int per_cta, const double *sk, const uint32_t *sv, bool gather)
+{
+    const long long n = g.n;
+    const long long lo = (long long)blockIdx.x * per_cta * MTILE;
+    const long long hi = min(n, lo + (long long)per_cta * MTILE);
+    for (long long j = lo + threadIdx.x; j < hi; j += blockDim.x) {
+        long long s = j;
+        if (gather) {
+            const long long t = (n - 1 - j) >> TILE_LOG2;
+            const long long c = min((long long)TILE, n - (t << TILE_LOG2));
+            s = 2 * (t << TILE_LOG2) + c - n + j;
+        }
+        g.ok[j] = sk[s];
+        if (HV) g.ov[j] = sv[s];
+    }
+}
+
 constexpr int WS_THREADS = NT + 32 + 32 * SEARCH_WARPS;   // 352
 
 template <bool HV, int ORD, int NS = 2>
 __global__ void __launch_bounds__(WS_THREADS, 2)
-merge_tstore_kernel(PipeGeo pg, int ntiles, int per_cta, const __grid_constant__ CUtensorMap omap,
-                    const unsigned *unsorted, const double *copy_k, const uint32_t *copy_v)
+merge_tstore_kernel(PipeGeo pg, int ntiles, int per_cta, const __grid_constant__ CUtensorMap omap, Adapt ad)
 {
 #ifdef GNS_PROF
     unsigned long long acc[16] = {};
@@ -711,30 +748,20 @@ merge_tstore_kernel(PipeGeo pg, int ntiles, int per_cta, const __grid_constant__
 #endif
     pdl_wait();
     GNS_TL_START(tl_slot);
-    if (unsorted && *(volatile const unsigned *)unsorted == 0u) {
-        // NEXT f2: the whole input was already in order (tile sort found no
-        // descent), so every merge is an omission ("Omitsort").
-        // Only the last pass moves data, and only if the tile sort's output
-        // landed in the buffer (odd pass count): a plain copy back.
-        if (copy_k) {
-            const long long n = pg.g.n;
-            const long long lo = (long long)blockIdx.x * per_cta * MTILE;
-            const long long hi = min(n, lo + (long long)per_cta * MTILE);
-            for (long long i = lo + threadIdx.x * 4; i < hi; i += (long long)blockDim.x * 4) {
-                if (i + 4 <= hi) {
-                    const double4 x = *reinterpret_cast<const double4 *>(copy_k + i);
-                    *reinterpret_cast<double4 *>(pg.g.ok + i) = x;
-                    if (HV) *reinterpret_cast<uint4 *>(pg.g.ov + i) = *reinterpret_cast<const uint4 *>(copy_v + i);
-                } else {
-                    for (long long j = i; j < hi; ++j) {
-                        pg.g.ok[j] = copy_k[j];
-                        if (HV) pg.g.ov[j] = copy_v[j];
-                    }
-                }
-            }
+    if (ad.flag) {
+        const unsigned f = *(volatile const unsigned *)ad.flag;
+        if ((f & 1u) == 0u || (f & 2u) == 0u) {
+            // NEXT f2: the whole input was already in order (no descent: every
+            // merge is an omission, "Omitsort"), or strictly
+            // reversed (its stable sort is the reversal).
+            // Only the steps the host scheduled for this pass move data.
+            const bool pre = (f & 1u) == 0u;
+            const double *ck = pre ? ad.pre_k : ad.rev_k;
+            const uint32_t *cv = pre ? ad.pre_v : ad.rev_v;
+            if (ck) adapt_move<HV>(pg.g, per_cta, ck, cv, !pre && ad.rev_gather);
+            pdl_trigger();
+            return;
         }
-        pdl_trigger();
-        return;
     }
 #ifdef GNS_PROF
     const long long t_flag = clock64();
@@ -1036,8 +1063,10 @@ tile_sort2_kernel(const double *src_k, const uint32_t *src_v, double *dst_k, uin
     double *sk = reinterpret_cast<double *>(smem);
     uint32_t *sv = reinterpret_cast<uint32_t *>(smem + T1_KEY_BYTES);
     __shared__ __align__(8) uint64_t bar;
+    __shared__ unsigned s_flags;
     const int tid = threadIdx.x;
     const long long tile = blockIdx.x;
+    if (tid == 0) s_flags = 0;
     const long long base = tile * TILE;
     const int cnt = (int)min((long long)TILE, n - base);
     const bool full = cnt == TILE;
@@ -1065,6 +1094,7 @@ tile_sort2_kernel(const double *src_k, const uint32_t *src_v, double *dst_k, uin
             for (int c = 0; c < VT1 / 4; ++c) lds128u(sv + tv_slot(tid * VT1 + 4 * c), &v[4 * c]);
         }
     } else {
+        __syncthreads();                   // s_flags initialised (the full path has its own barrier)
 #pragma unroll
         for (int x = 0; x < VT1; ++x) {
             const int e = tid * VT1 + x;
@@ -1076,23 +1106,47 @@ tile_sort2_kernel(const double *src_k, const uint32_t *src_v, double *dst_k, uin
         }
     }
     const int e0 = tid * VT1;
-    if (unsorted) {
-        // NEXT f2 (Omitsort's presortedness test): does any key
-        // have to move before its predecessor?  Each thread checks its 32 keys
-        // and the key after them (the next thread's first, or the next tile's).
-        bool bad = false;
+    // NEXT f2 (Omitsort's omitted merges; Octosort's reversal of
+    // descending runs), per tile: is the tile already in
+    // order (no key must move before its predecessor), or strictly reversed
+    // (every key strictly before its predecessor; its stable sort is its
+    // reversal)?  Each thread checks its real keys and the key after them.
+    // The same tests across tile boundaries feed the whole-input flag word
+    // (bit 0: some descent, bit 1: some pair not strictly reversed).
+    int mode = 0;          // 0 sort, 1 tile in order (omit), 2 tile strictly reversed (reverse)
+    {
+        // one compare per adjacent pair: "descent" = next strictly before
+        // current; in order <=> no descent, strictly reversed <=> all descents
+        int pairs = 0, desc = 0;
 #pragma unroll
-        for (int x = 0; x + 1 < VT1; ++x) bad |= before<ORD>(k[x + 1], k[x]);
+        for (int x = 0; x + 1 < VT1; ++x) {
+            if (e0 + x + 1 < cnt) {
+                ++pairs;
+                desc += before<ORD>(k[x + 1], k[x]) ? 1 : 0;
+            }
+        }
+        unsigned fl = 0;       // bit 0/1: in-tile some descent / some non-descent; bit 2/3: across the tile end
         const long long nx = base + e0 + VT1;
         if (nx < n) {
             const double kn = (full && e0 + VT1 < TILE) ? sk[tk_slot(e0 + VT1)] : src_k[nx];
-            bad |= before<ORD>(kn, k[VT1 - 1]);
+            const bool d = before<ORD>(kn, k[VT1 - 1]);
+            fl |= (e0 + VT1 < cnt) ? (d ? 1u : 2u) : (d ? 4u : 8u);
         }
-        if (__syncthreads_or(bad) && tid == 0) atomicOr(unsorted, 1u);
+        fl |= (desc > 0 ? 1u : 0u) | (desc < pairs ? 2u : 0u);
+        fl = __reduce_or_sync(0xFFFFFFFFu, fl);
+        if (lane_id() == 0 && fl) atomicOr(&s_flags, fl);
+        __syncthreads();
+        fl = s_flags;
+        mode = !(fl & 1u) ? 1 : (!(fl & 2u) && full) ? 2 : 0;
+        if (unsorted && tid == 0) {
+            const unsigned g = ((fl | (fl >> 2)) & 3u);   // whole-input flag word (see merge_tstore_kernel)
+            if (g) atomicOr(unsorted, g);
+        }
     }
 #ifndef GNS_TS_EXP
 #define GNS_TS_EXP 0
 #endif
+    if (mode == 0) {
     if (GNS_TS_EXP != 1) {   // (timing experiments only: 1 = no register sort, 2 = no smem merge rounds)
         transpose_sort16<0, HV, ORD>(k, v);
         transpose_sort16<16, HV, ORD>(k, v);
@@ -1119,6 +1173,37 @@ tile_sort2_kernel(const double *src_k, const uint32_t *src_v, double *dst_k, uin
             serial_merge32<HV, ORD>(sk, sv, a0 + i, b0, b0 + d - i, b0 + run, k, v);
         }
         __syncthreads();
+    }
+    } else {
+        __syncthreads();                   // the TMA-layout reads are done before the staging writes
+    }
+    if (mode == 2) {
+        // full tile, strictly reversed: output position TILE-1-e gets input e
+#pragma unroll
+        for (int c = 0; c < VT1 / 2; ++c) sts128(sk + tk_slot(TILE - 2 - e0 - 2 * c), k[2 * c + 1], k[2 * c]);
+        if (HV) {
+#pragma unroll
+            for (int c = 0; c < VT1 / 4; ++c) {
+                const uint32_t r[4] = {v[4 * c + 3], v[4 * c + 2], v[4 * c + 1], v[4 * c]};
+                sts128u(sv + tv_slot(TILE - 4 - e0 - 4 * c), r);
+            }
+        }
+        fence_proxy_async();
+        __syncthreads();
+        if (smp != nullptr && (tid & (SMP_G / VT1 - 1)) == 0)
+            smp[(base + e0) >> SMP_LOG2] = sk[tk_slot(e0)];
+        if (tid == 0) {
+#pragma unroll
+            for (int b = 0; b < TILE / 4096; ++b) {
+                tma_store_2d(&kdst, sk + b * 4096, 0, (int)(tile * (TILE / 16) + b * 256));
+                if (HV && (b & 1) == 0) tma_store_2d(&vdst, sv + b * 4096, 0, (int)(tile * (TILE / 32) + (b / 2) * 256));
+            }
+            bulk_commit();
+            bulk_wait_read0();
+        }
+        GNS_TL_END(0);
+        pdl_trigger();
+        return;
     }
     if (smp != nullptr && e0 < cnt && (tid & (SMP_G / VT1 - 1)) == 0)
         smp[(base + e0) >> SMP_LOG2] = k[0];          // sample of output position base + e0

@@ -336,3 +336,88 @@ def test_key_type_f64_through_sort_keys(gns):
     torch.cuda.synchronize()
     ek, ev = oracle.sort(k, v)
     assert_bitexact(tk.cpu().numpy(), ek, tv.cpu().numpy(), ev)
+
+
+@pytest.mark.parametrize("target", ["AscLeft", "DescLeft", "AscRight", "DescRight"])
+@pytest.mark.parametrize("n", [T1 + 1, 3 * T1, 5 * T1 + 17, 16 * T1, 33 * T1 - 1, 100003])
+def test_reversed_fast_path(gns, n, target):
+    """NEXT f2 (Octosort's reversal): a strictly reversed
+    input is sorted by one tile-order reversal (odd merge-pass counts) or a
+    reversal + copy (even counts); a single tie or a single ordered pair must
+    take the full path.  Ragged last tiles included."""
+    desc = target in ("DescLeft", "AscRight")
+    base = synth.uniform(n, 66 + n)
+    base = np.unique(base)                             # distinct keys
+    while base.size < n:
+        base = np.unique(np.concatenate([base, synth.uniform(n, 67 + base.size)]))
+    base = np.sort(base[:n])[::-1].copy()              # strictly descending
+    if desc:
+        base = base[::-1].copy()                       # strictly ascending = reversed for Desc
+    v = synth.iota_u32(n)
+    cases = {"reversed": base}
+    k = base.copy()
+    k[n // 2] = k[n // 2 + 1]                          # one tie
+    cases["tie"] = k
+    k = base.copy()
+    k[T1 - 1], k[T1] = k[T1], k[T1 - 1]                # one ordered pair across a tile boundary
+    cases["swap"] = k
+    for name, k in cases.items():
+        tk, tv = to_dev(k, v)
+        gns.sort_(tk, tv, 1.0, target=target)
+        torch.cuda.synchronize()
+        ek, ev = oracle.sort_target(k, v, target)
+        assert_bitexact(tk.cpu().numpy(), ek, tv.cpu().numpy(), ev, what=f"{target} {name} n={n}")
+        tk, _ = to_dev(k, None)
+        gns.sort_(tk, None, 1.0, target=target)
+        torch.cuda.synchronize()
+        assert_bitexact(tk.cpu().numpy(), ek, what=f"{target} {name} key-only n={n}")
+
+
+@pytest.mark.parametrize("frac", [1.0, 0.5])
+@pytest.mark.parametrize("name", synth.PATTERNS)
+@pytest.mark.parametrize("n", [5 * T1 + 123, 40 * T1])
+def test_paper_patterns(gns, n, name, frac):
+    """The paper's eight input patterns incl. locally and
+    globally presorted / reversed ones, which exercise the per-tile omission
+    and reversal (NEXT f2) next to the full path, vs the oracle."""
+    k = synth.pattern(name, n, 500 + n)
+    v = synth.iota_u32(n)
+    tk, tv = to_dev(k, v)
+    gns.sort_(tk, tv, frac)
+    torch.cuda.synchronize()
+    ek, ev = oracle.sort(k, v)
+    assert_bitexact(tk.cpu().numpy(), ek, tv.cpu().numpy(), ev, what=f"{name} n={n} p={frac}")
+
+
+@pytest.mark.parametrize("target", ["AscLeft", "DescLeft"])
+def test_tile_local_order_mix(gns, target):
+    """Tiles that are in order, strictly reversed, reversed with a tie, and
+    random, side by side (per-tile mode decisions), plus the tile sort step."""
+    rng = np.random.default_rng(5)
+    parts = []
+    for i in range(12):
+        t = np.unique(rng.random(T1 + 64))[:T1]
+        kind = i % 4
+        if kind == 0:
+            t = np.sort(t)
+        elif kind == 1:
+            t = np.sort(t)[::-1].copy()
+        elif kind == 2:
+            t = np.sort(t)[::-1].copy()
+            t[100] = t[101]
+        parts.append(t)
+    k = np.concatenate(parts + [rng.random(777)])
+    v = synth.iota_u32(k.size)
+    tk, tv = to_dev(k, v)
+    gns.sort_(tk, tv, 1.0, target=target)
+    torch.cuda.synchronize()
+    ek, ev = oracle.sort_target(k, v, target)
+    assert_bitexact(tk.cpu().numpy(), ek, tv.cpu().numpy(), ev, what=target)
+    if target == "AscLeft":
+        sk_, sv_ = to_dev(k, v)
+        dk, dv = torch.empty_like(sk_), torch.empty_like(sv_)
+        gns.tile_sort(sk_, sv_, dk, dv)
+        torch.cuda.synchronize()
+        for t0 in range(0, k.size, T1):
+            ek, ev = oracle.sort(k[t0:t0 + T1], v[t0:t0 + T1])
+            assert_bitexact(dk.cpu().numpy()[t0:t0 + T1], ek, dv.cpu().numpy()[t0:t0 + T1], ev, what=f"tile {t0}")
