@@ -748,21 +748,9 @@ merge_tstore_kernel(PipeGeo pg, int ntiles, int per_cta, const __grid_constant__
 #endif
     pdl_wait();
     GNS_TL_START(tl_slot);
-    if (ad.flag) {
-        const unsigned f = *(volatile const unsigned *)ad.flag;
-        if ((f & 1u) == 0u || (f & 2u) == 0u) {
-            // NEXT f2: the whole input was already in order (no descent: every
-            // merge is an omission, "Omitsort"), or strictly
-            // reversed (its stable sort is the reversal).
-            // Only the steps the host scheduled for this pass move data.
-            const bool pre = (f & 1u) == 0u;
-            const double *ck = pre ? ad.pre_k : ad.rev_k;
-            const uint32_t *cv = pre ? ad.pre_v : ad.rev_v;
-            if (ck) adapt_move<HV>(pg.g, per_cta, ck, cv, !pre && ad.rev_gather);
-            pdl_trigger();
-            return;
-        }
-    }
+    // NEXT f2 flag word: loaded now, tested after the first split searches
+    // (which only read), so its latency hides behind them
+    const unsigned f_adapt = ad.flag ? *(volatile const unsigned *)ad.flag : 3u;
 #ifdef GNS_PROF
     const long long t_flag = clock64();
 #endif
@@ -798,13 +786,34 @@ merge_tstore_kernel(PipeGeo pg, int ntiles, int per_cta, const __grid_constant__
         spl_used = 0;
     }
     __syncthreads();
-    // the first splits: merge warps (idle until the first tile lands)
-    const int init = min(nspl, MERGE_WARPS);
     auto publish = [&](int j, int c) {
         spl[j % SPL_RING] = c;
         __threadfence_block();
         spl_tag[j % SPL_RING] = j;
     };
+    // the first splits: every warp computes one (32-lane sample-guided search)
+    const int init = min(nspl, WS_THREADS / 32);
+    if (warp < init) {
+        const int c = tile_corank<32, ORD>(pg.g, first + warp, lane, 0xFFFFFFFFu, 0);
+        if (lane == 0) publish(warp, c);
+    }
+#ifdef GNS_PROF
+    const long long t_split0 = clock64();
+    long long t_full0 = 0;
+#endif
+    if ((f_adapt & 1u) == 0u || (f_adapt & 2u) == 0u) {
+        // NEXT f2: the whole input was already in order (no descent: every
+        // merge is an omission, "Omitsort"), or strictly
+        // reversed (its stable sort is the reversal).
+        // Only the steps the host scheduled for this pass move data.
+        const bool pre = (f_adapt & 1u) == 0u;
+        const double *ck = pre ? ad.pre_k : ad.rev_k;
+        const uint32_t *cv = pre ? ad.pre_v : ad.rev_v;
+        if (ck) adapt_move<HV>(pg.g, per_cta, ck, cv, !pre && ad.rev_gather);
+        pdl_trigger();
+        return;
+    }
+    __syncthreads();      // the first splits are published
 
     if (warp > PRODUCER_WARP) {
         // ------------------------------------------------ search warps
@@ -877,14 +886,6 @@ merge_tstore_kernel(PipeGeo pg, int ntiles, int per_cta, const __grid_constant__
     }
 
     // ---------------------------------------------------- merge warps 0-7
-    if (warp < init) {
-        const int c = tile_corank<32, ORD>(pg.g, first + warp, lane, 0xFFFFFFFFu, 0);
-        if (lane == 0) publish(warp, c);
-    }
-#ifdef GNS_PROF
-    const long long t_split0 = clock64();
-    long long t_full0 = 0;
-#endif
     const long long n = pg.g.n;
     const long long full_rows = n >> 4;              // rows stored by TMA; a partial last row is stored by hand
     for (int i = 0; i < m; ++i) {
