@@ -129,6 +129,36 @@ typedef enum {
 gns_status gns_sort_keys(void *keys, gns_key_type key_type, uint32_t *vals, size_t n, double buffer_fraction,
                          gns_target target, void *ws, size_t ws_bytes, gns_stream_t stream);
 
+/* ---- NEXT f4: the steps of the distributed sort (paper_2402_01816_b200.dist,
+ * SURVEY.md §8(e); "parallelize over an arbitrary number of processes",
+ * PAPER.md:353).  Each rank sorts its shard (gns_sort_keys), the ranks agree
+ * on k-1 splitters (key, owner rank, position in the owner's sorted shard),
+ * cut their shards at them (gns_split_cuts), exchange the pieces (one NCCL
+ * all-to-all-v) and merge the k received sorted runs in rank order
+ * (gns_merge_two, a pairwise tree).  Global order: (key, rank, position),
+ * i.e. stable in the rank-major input order. */
+
+/* cuts[i] = number of keys of sorted_keys[0:n) (this rank's sorted shard,
+ * ascending in key_type order) that precede splitter i in the global order:
+ * my_rank < spl_rank[i]: keys <= spl_keys[i]; my_rank > spl_rank[i]:
+ * keys < spl_keys[i]; my_rank == spl_rank[i]: spl_pos[i] (clamped to [0, n]).
+ * All pointers are device pointers; spl_keys holds nsplit 8-byte keys.
+ * Asynchronous on `stream`; GNS_ERR_INVALID_ARGUMENT for NULL pointers,
+ * nsplit < 0 or an unknown key type. */
+gns_status gns_split_cuts(const void *sorted_keys, gns_key_type key_type, size_t n, const void *spl_keys,
+                          const int32_t *spl_rank, const int64_t *spl_pos, int nsplit, int my_rank, int64_t *cuts,
+                          gns_stream_t stream);
+
+/* Stable merge of two sorted runs a[0:la) and b[0:lb) (ascending in key_type
+ * order; a's keys win ties) into dst[0:la+lb), out of place.  a and b may
+ * live anywhere (8-byte aligned keys, 4-byte aligned vals, not overlapping
+ * dst); dst must be 32-byte aligned.  vals: dst_vals and the vals of every
+ * non-empty run, or none (an empty run's pointers may be NULL).  Row a3+a4's
+ * kernel in its two-run geometry; one launch, asynchronous. */
+gns_status gns_merge_two(const void *a_keys, const uint32_t *a_vals, size_t la, const void *b_keys,
+                         const uint32_t *b_vals, size_t lb, void *dst_keys, uint32_t *dst_vals, gns_key_type key_type,
+                         gns_stream_t stream);
+
 /* Pass schedule of a sort (host only, no CUDA call). */
 typedef struct {
     int tile;                   /* gns_tile_elems(): elements per tile-sort CTA          */
@@ -183,7 +213,7 @@ gns_status gns_merge_inplace_top(double *keys, uint32_t *vals, const double *lef
  * gns_timing_end(ms, kind, cap): waits for the last event, writes up to cap
  * per-launch durations (milliseconds) and kinds (1 tile sort, 2 merge pass,
  * 3 co-rank partition, 4 in-place dependency ranges, 5 in-place merge,
- * 6 reversal, 0 other) in launch order, turns timing off and returns the number
+ * 6 reversal, 7 splitter cuts, 0 other) in launch order, turns timing off and returns the number
  * of timed launches (-1 if timing was off or an event failed). */
 gns_status gns_timing_begin(int max_launches);
 int gns_timing_end(float *ms, int *kind, int cap);

@@ -64,6 +64,8 @@ _c = {
     "gns_sort_pairs_f64_u32_ws": _sig("gns_sort_pairs_f64_u32_ws", [_vp, _vp, _sz, _d, _vp, _sz, _vp]),
     "gns_sort_target_f64": _sig("gns_sort_target_f64", [_vp, _vp, _sz, _d, _i, _vp, _sz, _vp]),
     "gns_sort_keys": _sig("gns_sort_keys", [_vp, _i, _vp, _sz, _d, _i, _vp, _sz, _vp]),
+    "gns_split_cuts": _sig("gns_split_cuts", [_vp, _i, _sz, _vp, _vp, _vp, _i, _i, _vp, _vp]),
+    "gns_merge_two": _sig("gns_merge_two", [_vp, _vp, _sz, _vp, _vp, _sz, _vp, _vp, _i, _vp]),
     "gns_plan": _sig("gns_plan", [_sz, _d, _i, ctypes.POINTER(gns_plan_info)]),
     "gns_tile_sort": _sig("gns_tile_sort", [_vp, _vp, _vp, _vp, _sz, _vp]),
     "gns_merge_workspace_bytes": _sig("gns_merge_workspace_bytes", [_sz], _sz),
@@ -129,6 +131,14 @@ def gns_sort_keys(keys_ptr, key_type, vals_ptr, n, buffer_fraction, target, ws_p
     return _c["gns_sort_keys"](keys_ptr, key_type, vals_ptr, n, buffer_fraction, target, ws_ptr, ws_bytes, stream)
 
 
+def gns_split_cuts(keys_ptr, key_type, n, spl_keys, spl_rank, spl_pos, nsplit, my_rank, cuts, stream) -> int:
+    return _c["gns_split_cuts"](keys_ptr, key_type, n, spl_keys, spl_rank, spl_pos, nsplit, my_rank, cuts, stream)
+
+
+def gns_merge_two(a_k, a_v, la, b_k, b_v, lb, dst_k, dst_v, key_type, stream) -> int:
+    return _c["gns_merge_two"](a_k, a_v, la, b_k, b_v, lb, dst_k, dst_v, key_type, stream)
+
+
 def gns_plan(n: int, buffer_fraction: float, with_vals: bool) -> gns_plan_info:
     info = gns_plan_info()
     _check(_c["gns_plan"](n, buffer_fraction, int(bool(with_vals)), ctypes.byref(info)), "gns_plan")
@@ -165,7 +175,8 @@ def gns_timing_end(cap: int = 4096):
     return [(kind[i], ms[i]) for i in range(min(n, cap))]
 
 
-LAUNCH_KINDS = {1: "tile_sort", 2: "merge_pass", 3: "partition", 4: "inplace_deps", 5: "inplace_merge", 6: "reverse"}
+LAUNCH_KINDS = {1: "tile_sort", 2: "merge_pass", 3: "partition", 4: "inplace_deps", 5: "inplace_merge", 6: "reverse",
+                7: "split_cuts"}
 
 
 def gns_tile_elems() -> int:
@@ -257,6 +268,33 @@ def sort_(keys, vals=None, buffer_fraction: float = 1.0, workspace=None, stream=
             rc = gns_sort_pairs_f64_u32_ws(_ptr(keys), _ptr(vals), n, buffer_fraction, _ptr(workspace), wb, st)
     _check(rc, "sort_")
     return keys, vals
+
+
+def merge_two(a_k, a_v, b_k, b_v, stream=None):
+    """Stable merge of two sorted runs (a wins ties) into new tensors
+    (gns_merge_two).  Keys float64 / int64 / uint64; vals uint32 or None."""
+    import torch
+    kt = _key_type(a_k)
+    if b_k.dtype != a_k.dtype:
+        raise TypeError("a and b keys differ in dtype")
+    la, lb = a_k.numel(), b_k.numel()
+    out_k = torch.empty(la + lb, dtype=a_k.dtype, device=a_k.device)
+    out_v = None if a_v is None else torch.empty(la + lb, dtype=torch.uint32, device=a_k.device)
+    _check(gns_merge_two(_ptr(a_k), _ptr(a_v), la, _ptr(b_k), _ptr(b_v), lb, _ptr(out_k), _ptr(out_v), kt,
+                         _stream_handle(stream)), "merge_two")
+    return out_k, out_v
+
+
+def split_cuts(sorted_keys, spl_keys, spl_rank, spl_pos, my_rank: int, stream=None):
+    """gns_split_cuts: int64 tensor of cut positions of this rank's sorted
+    shard at the splitters (device tensors; spl_rank int32, spl_pos int64)."""
+    import torch
+    kt = _key_type(sorted_keys)
+    k = spl_keys.numel()
+    cuts = torch.empty(k, dtype=torch.int64, device=sorted_keys.device)
+    _check(gns_split_cuts(_ptr(sorted_keys), kt, sorted_keys.numel(), _ptr(spl_keys), _ptr(spl_rank),
+                          _ptr(spl_pos), k, my_rank, _ptr(cuts), _stream_handle(stream)), "split_cuts")
+    return cuts
 
 
 def workspace_bytes(n: int, buffer_fraction: float = 1.0, with_vals: bool = False) -> int:

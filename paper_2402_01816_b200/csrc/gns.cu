@@ -207,7 +207,8 @@ gns_status row_map(void *base, size_t n, bool f64, int box_rows, CUtensorMap *ma
     EncodeTiledFn fn = encode_fn();
     if (!fn) return fail(GNS_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
     const int per_row = f64 ? 16 : 32;
-    cuuint64_t dims[2] = {(cuuint64_t)per_row, (cuuint64_t)(n / per_row)};
+    // n < per_row: a 1-row map that no kernel stores through (they check n)
+    cuuint64_t dims[2] = {(cuuint64_t)per_row, (cuuint64_t)std::max<size_t>(1, n / per_row)};
     cuuint64_t strides[1] = {128};
     cuuint32_t box[2] = {(cuuint32_t)per_row, (cuuint32_t)box_rows};
     cuuint32_t estr[2] = {1, 1};
@@ -245,8 +246,9 @@ thread_local Timing g_timing;
 int launch_kind(const char *what)
 {
     static const char *names[] = {"tile_sort2_kernel", "merge_tstore_kernel", "partition_kernel",
-                                  "inplace_deps_kernel", "merge_inplace_kernel", "reverse_kernel"};
-    for (int i = 0; i < 6; ++i)
+                                  "inplace_deps_kernel", "merge_inplace_kernel", "reverse_kernel",
+                                  "split_cuts_kernel"};
+    for (int i = 0; i < 7; ++i)
         if (std::strcmp(what, names[i]) == 0) return i + 1;
     return 0;
 }
@@ -723,6 +725,76 @@ gns_status gns_merge_pass(const double *src_keys, const uint32_t *src_vals, doub
     GNS_TRY(ensure_attrs());
     MergeGeo g = uniform_geo(src_keys, src_vals, dst_keys, dst_vals, n, run_len);
     return launch_merge(g, src_keys + n, src_keys + n, (int *)ws, nullptr, nullptr, false, 0, (cudaStream_t)stream);
+}
+
+gns_status gns_merge_two(const void *a_keys, const uint32_t *a_vals, size_t la, const void *b_keys,
+                         const uint32_t *b_vals, size_t lb, void *dst_keys, uint32_t *dst_vals, gns_key_type key_type,
+                         gns_stream_t stream)
+{
+    const bool hv = dst_vals != nullptr;      // an empty run's vals may be NULL
+    if ((!hv && (a_vals || b_vals)) || (hv && ((la && !a_vals) || (lb && !b_vals))))
+        return fail(GNS_ERR_INVALID_ARGUMENT, "vals: dst_vals and the non-empty runs' vals, or none");
+    if ((int)key_type < 0 || (int)key_type > 2) return fail(GNS_ERR_INVALID_ARGUMENT, "key_type must be 0..2");
+    const size_t n = la + lb;
+    if (n > GNS_MAX_N) return fail(GNS_ERR_INVALID_ARGUMENT, "la + lb > GNS_MAX_N");
+    if (n == 0) return GNS_OK;
+    if ((la && !a_keys) || (lb && !b_keys) || !dst_keys)
+        return fail(GNS_ERR_INVALID_ARGUMENT, "NULL keys with a non-empty run");
+    if (!is_aligned(a_keys, 8) || !is_aligned(b_keys, 8) || !is_aligned(a_vals, 4) || !is_aligned(b_vals, 4))
+        return fail(GNS_ERR_MISALIGNED, "a/b keys must be 8-byte, vals 4-byte aligned");
+    GNS_TRY(validate_data((const double *)dst_keys, dst_vals, hv, n));
+    GNS_TRY(ensure_attrs());
+    cudaStream_t st = (cudaStream_t)stream;
+    if (la == 0 || lb == 0) {          // one run: a copy
+        const void *sk = la ? a_keys : b_keys;
+        const uint32_t *sv = la ? a_vals : b_vals;
+        GNS_TRY(check(cudaMemcpyAsync(dst_keys, sk, n * 8, cudaMemcpyDeviceToDevice, st), "copy"));
+        if (hv) GNS_TRY(check(cudaMemcpyAsync(dst_vals, sv, n * 4, cudaMemcpyDeviceToDevice, st), "copy"));
+        return GNS_OK;
+    }
+    MergeGeo g;
+    g.ak = (const double *)a_keys;
+    g.av = hv ? a_vals : nullptr;
+    g.bk = (const double *)b_keys;
+    g.bv = hv ? b_vals : nullptr;
+    g.ok = (double *)dst_keys;
+    g.ov = hv ? dst_vals : nullptr;
+    g.n = (long long)n;
+    g.L = (long long)la;
+    g.single = 1;
+    g.tpp = 1;
+    g.tpp_log2 = 0;
+    g.sa = nullptr;
+    g.so = nullptr;
+    const int ntiles = (int)ceil_div(n, MTILE);
+    PipeGeo pg;
+    pg.g = g;
+    pg.a_lim = g.ak + la;
+    pg.b_lim = g.bk + lb;
+    CUtensorMap map;
+    GNS_TRY(row_map(g.ok, n, true, MTILE / 16, &map));
+    const int ctas = std::min(ntiles, 2 * num_sms());
+    const int per = (int)ceil_div(ntiles, ctas);
+    const int grid = (int)ceil_div(ntiles, per);
+    auto kern = merge_kern(hv, ord_of(false, (int)key_type));
+    return launch_pdl("merge_tstore_kernel", kern, grid, WS_THREADS, ts_smem(hv), st, pg, ntiles, per, map, Adapt{});
+}
+
+gns_status gns_split_cuts(const void *sorted_keys, gns_key_type key_type, size_t n, const void *spl_keys,
+                          const int32_t *spl_rank, const int64_t *spl_pos, int nsplit, int my_rank, int64_t *cuts,
+                          gns_stream_t stream)
+{
+    if ((int)key_type < 0 || (int)key_type > 2) return fail(GNS_ERR_INVALID_ARGUMENT, "key_type must be 0..2");
+    if (nsplit < 0 || n > GNS_MAX_N) return fail(GNS_ERR_INVALID_ARGUMENT, "nsplit < 0 or n > GNS_MAX_N");
+    if (nsplit == 0) return GNS_OK;
+    if ((n && !sorted_keys) || !spl_keys || !spl_rank || !spl_pos || !cuts)
+        return fail(GNS_ERR_INVALID_ARGUMENT, "NULL pointer");
+    GNS_TRY(ensure_attrs());
+    static const decltype(&split_cuts_kernel<0>) tab[3] = {&split_cuts_kernel<0>, &split_cuts_kernel<2>,
+                                                          &split_cuts_kernel<4>};
+    return launch_pdl("split_cuts_kernel", tab[(int)key_type], (unsigned)ceil_div((size_t)nsplit, 128), 128, 0,
+                      (cudaStream_t)stream, (const double *)sorted_keys, (long long)n, (const double *)spl_keys,
+                      (const int *)spl_rank, (const long long *)spl_pos, nsplit, my_rank, (long long *)cuts);
 }
 
 gns_status gns_merge_inplace_top(double *keys, uint32_t *vals, const double *left_keys,

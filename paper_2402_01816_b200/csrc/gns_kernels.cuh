@@ -862,8 +862,10 @@ merge_tstore_kernel(PipeGeo pg, int ntiles, int per_cta, const __grid_constant__
             mbar_wait(&staged[st], (uint32_t)((i / NS) & 1));     // tile i staged by the 8 merge warps
             GNS_PT(p1);
             GNS_PADD(1, p1 - p0);
-            tma_store_2d(&omap, skb(st), 0, (int)((long long)(first + i) * (MTILE / 16)));
-            bulk_commit();
+            if (pg.g.n >= 16) {        // (n < 16: no full row; the merge warps stored the partial row)
+                tma_store_2d(&omap, skb(st), 0, (int)((long long)(first + i) * (MTILE / 16)));
+                bulk_commit();
+            }
             if (i + NS < m) {
                 bulk_wait_read0();                                 // stage st read out -> reusable
                 GNS_PT(p2);
@@ -1383,6 +1385,40 @@ reverse_kernel(double *k, uint32_t *v, long long n)
             v[i] = y;
             v[j] = x;
         }
+    }
+    pdl_trigger();
+}
+
+// ----------------------------------- NEXT f4: distributed sort, splitter cuts
+// For splitter i = (key, owner rank r_i, position p_i in r_i's sorted shard),
+// the number of this rank's sorted keys that precede it in the global stable
+// order (key, rank, position): ranks below r_i keep their ties first
+// (count of keys <= key), ranks above put theirs after (count of keys < key),
+// the owner cuts at p_i.  One thread per splitter, binary search.
+template <int ORD>
+__global__ void __launch_bounds__(128)
+split_cuts_kernel(const double *keys, long long n, const double *spl_key, const int *spl_rank,
+                  const long long *spl_pos, int nsplit, int my_rank, long long *cuts)
+{
+    pdl_wait();
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < nsplit) {
+        long long c;
+        if (spl_rank[i] == my_rank) {
+            c = min(max(spl_pos[i], 0LL), n);
+        } else {
+            const bool upper = my_rank < spl_rank[i];
+            const double x = spl_key[i];
+            long long lo = 0, hi = n;      // first position whose key does not precede x
+            while (lo < hi) {
+                const long long m = (lo + hi) >> 1;
+                const bool pre = upper ? !before<ORD>(x, keys[m]) : before<ORD>(keys[m], x);
+                if (pre) lo = m + 1;
+                else hi = m;
+            }
+            c = lo;
+        }
+        cuts[i] = c;
     }
     pdl_trigger();
 }

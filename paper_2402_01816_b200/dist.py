@@ -1,0 +1,195 @@
+"""NEXT f4: stable sort of an array sharded over the ranks of
+a ``torch.distributed`` group, one GPU per rank, with ONE data exchange.
+
+The paper parallelises its merges "over an arbitrary number of processes"
+(§Parallel sorting); across GPUs the natural form is
+sort -> split -> exchange -> merge:
+
+1. every rank stably sorts its shard with the single-GPU path
+   (``gns_sort_keys``);
+2. the ranks agree on k-1 splitters: each contributes ``samples`` regularly
+   spaced elements of its sorted shard as (key, rank, position) triples, the
+   triples are all-gathered in rank order and stably sorted by key -- which
+   orders them by (key, rank, position) -- and every (V/k)-th one is taken;
+3. each rank cuts its sorted shard at the splitters (``gns_split_cuts``:
+   elements preceding splitter i in the global order (key, rank, position));
+4. one all-to-all-v (NCCL over NVLink) sends piece j to rank j;
+5. each rank merges the k received sorted runs in rank order with a pairwise
+   tree of ``gns_merge_two`` launches (left run wins ties).
+
+Global order: (key, rank, position in the rank's shard) = stable in the
+rank-major input order, so the concatenation of the ranks' outputs is the
+unique stable sort of the concatenated shards (bit-exact, payload included).
+Output sizes vary per rank (splitter quality); a rank may receive nothing.
+
+Every step that touches the data runs in this package's CUDA kernels; the
+``ops`` argument exists so the orchestration can be exercised on CPU with the
+gloo backend in tests (tests/test_dist_sort.py passes oracle-based CPU ops);
+the default ops are the CUDA ones and fail loudly without the extension.
+"""
+from __future__ import annotations
+
+from typing import List, Optional, Tuple
+
+import paper_2402_01816_b200 as gns
+
+
+class CudaOps:
+    """The product steps: this package's kernels through the C-ABI."""
+
+    def sort(self, keys, vals):
+        gns.sort_(keys, vals)
+        return keys, vals
+
+    def cuts(self, sorted_keys, spl_keys, spl_rank, spl_pos, my_rank):
+        return gns.split_cuts(sorted_keys, spl_keys, spl_rank, spl_pos, my_rank)
+
+    def merge_two(self, a_k, a_v, b_k, b_v):
+        return gns.merge_two(a_k, a_v, b_k, b_v)
+
+
+def _sample_positions(n: int, s: int) -> List[int]:
+    """s regularly spaced positions of a shard of n elements (none if empty)."""
+    if n == 0:
+        return []
+    return [(j * n) // s for j in range(s)]
+
+
+def choose_splitters(torch, all_keys, all_rank, all_pos, k: int, ops):
+    """Splitters from the all-gathered samples (rank-major, positions
+    ascending within a rank): a stable key sort orders them by
+    (key, rank, position); every (V/k)-th triple is a splitter."""
+    V = all_keys.numel()
+    if k <= 1 or V == 0:
+        return all_keys[:0], all_rank[:0], all_pos[:0]
+    idx = torch.arange(V, dtype=torch.int64, device=all_keys.device).to(torch.uint32)
+    sk = all_keys.clone()
+    sk, idx = ops.sort(sk, idx)
+    pick = torch.tensor([(i * V) // k for i in range(1, k)], dtype=torch.int64, device=all_keys.device)
+    order = idx.to(torch.int64)[pick]
+    return sk[pick], all_rank[order], all_pos[order]
+
+
+def merge_runs(runs, ops):
+    """Pairwise tree merge of sorted runs given in rank order (left wins ties)."""
+    runs = [r for r in runs if r[0].numel() > 0] or runs[:1]
+    while len(runs) > 1:
+        nxt = []
+        for i in range(0, len(runs) - 1, 2):
+            (ak, av), (bk, bv) = runs[i], runs[i + 1]
+            nxt.append(ops.merge_two(ak, av, bk, bv))
+        if len(runs) % 2:
+            nxt.append(runs[-1])
+        runs = nxt
+    return runs[0]
+
+
+def sort_distributed(keys, vals=None, group=None, samples: int = 64, ops=None
+                     ) -> Tuple[object, Optional[object]]:
+    """Stable sort of the rank-major concatenation of every rank's
+    (keys, vals) shard.  Returns this rank's piece of the sorted array (new
+    tensors on the keys' device).  keys: float64 / int64 / uint64 (CUDA for
+    the default ops); vals: uint32 or None.  Collective: every rank of
+    ``group`` must call it."""
+    import torch
+    import torch.distributed as dist
+    ops = ops or CudaOps()
+    k = dist.get_world_size(group)
+    me = dist.get_rank(group)
+    dev = keys.device
+    keys = keys.clone()
+    vals = None if vals is None else vals.clone()
+    keys, vals = ops.sort(keys, vals)
+    if k == 1:
+        return keys, vals
+    n = keys.numel()
+    # 2. samples -> splitters (every rank contributes exactly `samples` slots;
+    # an empty shard marks its slots invalid)
+    pos = _sample_positions(n, samples)
+    valid = torch.zeros(samples, dtype=torch.int64, device=dev)
+    s_pos = torch.zeros(samples, dtype=torch.int64, device=dev)
+    s_key = torch.zeros(samples, dtype=keys.dtype, device=dev)
+    if pos:
+        p = torch.tensor(pos, dtype=torch.int64, device=dev)
+        valid[:] = 1
+        s_pos[:] = p
+        s_key[:] = keys[p]
+    g_key = [torch.empty_like(s_key) for _ in range(k)]
+    g_pos = [torch.empty_like(s_pos) for _ in range(k)]
+    g_val = [torch.empty_like(valid) for _ in range(k)]
+    dist.all_gather([g.view(torch.int64) for g in g_key], s_key.view(torch.int64), group=group)   # 8-byte patterns
+    dist.all_gather(g_pos, s_pos, group=group)
+    dist.all_gather(g_val, valid, group=group)
+    a_key = torch.cat(g_key)
+    a_pos = torch.cat(g_pos)
+    a_rank = torch.arange(k, dtype=torch.int32, device=dev).repeat_interleave(samples)
+    m = torch.cat(g_val).bool()
+    spl_key, spl_rank, spl_pos = choose_splitters(torch, a_key[m], a_rank[m], a_pos[m], k, ops)
+    # 3. cuts -> send counts
+    if spl_key.numel():
+        cuts = ops.cuts(keys, spl_key.contiguous(), spl_rank.contiguous(), spl_pos.contiguous(), me)
+    else:
+        cuts = torch.zeros(k - 1, dtype=torch.int64, device=dev)
+    edges = torch.cat([torch.zeros(1, dtype=torch.int64, device=dev), cuts.to(torch.int64),
+                       torch.full((1,), n, dtype=torch.int64, device=dev)])
+    send = (edges[1:] - edges[:-1]).contiguous()
+    recv = torch.empty_like(send)
+    dist.all_to_all_single(recv, send, group=group)
+    send_l = [int(x) for x in send.cpu()]
+    recv_l = [int(x) for x in recv.cpu()]
+    # 4. one all-to-all-v of keys (and vals)
+    out_k = torch.empty(sum(recv_l), dtype=keys.dtype, device=dev)
+    # (keys move as their 64-bit patterns: every key type is 8 bytes)
+    dist.all_to_all_single(out_k.view(torch.int64), keys.view(torch.int64), recv_l, send_l, group=group)
+    out_v = None
+    if vals is not None:
+        out_v = torch.empty(sum(recv_l), dtype=vals.dtype, device=dev)
+        # (uint32 is not an NCCL type: move the payload as int32 bits)
+        dist.all_to_all_single(out_v.view(torch.int32), vals.view(torch.int32), recv_l, send_l, group=group)
+    # 5. merge the k received runs in rank order
+    runs = []
+    o = 0
+    for c in recv_l:
+        runs.append((out_k[o:o + c], None if out_v is None else out_v[o:o + c]))
+        o += c
+    mk, mv = merge_runs(runs, ops)
+    return mk.contiguous(), (None if mv is None else mv.contiguous())
+
+
+def simulate(shards, samples: int = 64, ops=None):
+    """The same steps for k shards in ONE process (no collectives: the
+    all-gather and all-to-all are tensor concatenations / slices), for
+    validating the kernels of the distributed path on a single GPU.  Returns
+    the k output pieces."""
+    import torch
+    ops = ops or CudaOps()
+    k = len(shards)
+    srt = []
+    for kk, vv in shards:
+        kk = kk.clone()
+        vv = None if vv is None else vv.clone()
+        srt.append(ops.sort(kk, vv))
+    if k == 1:
+        return srt
+    dev = srt[0][0].device
+    a_key, a_pos, a_rank = [], [], []
+    for r, (kk, _) in enumerate(srt):
+        pos = _sample_positions(kk.numel(), samples)
+        if pos:
+            p = torch.tensor(pos, dtype=torch.int64, device=dev)
+            a_key.append(kk[p])
+            a_pos.append(p)
+            a_rank.append(torch.full((len(pos),), r, dtype=torch.int32, device=dev))
+    spl_key, spl_rank, spl_pos = choose_splitters(torch, torch.cat(a_key), torch.cat(a_rank), torch.cat(a_pos),
+                                                  k, ops)
+    pieces = []            # pieces[src][dst]
+    for r, (kk, vv) in enumerate(srt):
+        n = kk.numel()
+        cuts = ops.cuts(kk, spl_key.contiguous(), spl_rank.contiguous(), spl_pos.contiguous(), r)
+        e = [0] + [int(x) for x in cuts.cpu()] + [n]
+        pieces.append([(kk[e[j]:e[j + 1]], None if vv is None else vv[e[j]:e[j + 1]]) for j in range(k)])
+    out = []
+    for j in range(k):
+        runs = [pieces[r][j] for r in range(k)]
+        out.append(merge_runs(runs, ops))
+    return out

@@ -1,0 +1,140 @@
+"""NEXT f4: the distributed sort's orchestration
+(paper_2402_01816_b200.dist) on CPU with the gloo backend, world_size 2 and 3.
+
+The data steps (local sort, cuts, two-run merge) are the oracle's here
+(test-only CPU ops); the splitter choice, counts, all-to-all-v exchange and
+merge-tree order are the product code.  The concatenation of the ranks'
+outputs must equal the oracle's stable sort of the concatenated shards,
+bit-exact, payload included."""
+import os
+import socket
+import sys
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+KT = {torch.float64: "f64", torch.int64: "i64", torch.uint64: "u64"}
+
+
+class CpuOracleOps:
+    """Test-only CPU implementations of the three data steps (oracle /
+    numpy), so the orchestration runs without a GPU."""
+
+    def sort(self, keys, vals):
+        import oracle
+        kt = KT[keys.dtype]
+        k, v = oracle.sort_keys(keys.numpy(), None if vals is None else vals.numpy(), kt)
+        return torch.from_numpy(k), (None if v is None else torch.from_numpy(v))
+
+    def cuts(self, sorted_keys, spl_key, spl_rank, spl_pos, me):
+        a = sorted_keys.numpy()
+        out = []
+        for x, r, p in zip(spl_key.numpy(), spl_rank.numpy(), spl_pos.numpy()):
+            if r == me:
+                out.append(int(p))
+            else:
+                out.append(int(np.searchsorted(a, x, side="right" if me < r else "left")))
+        return torch.tensor(out, dtype=torch.int64)
+
+    def merge_two(self, a_k, a_v, b_k, b_v):
+        k = torch.cat([a_k, b_k])
+        v = None if a_v is None else torch.cat([a_v, b_v])
+        return self.sort(k, v)
+
+
+def make_shard(case, rank, world):
+    rng = np.random.default_rng(1000 * case + rank)
+    if case == 0:          # f64, heavy ties, signed zeros
+        n = 3000 + 700 * rank
+        k = rng.integers(-5, 6, n).astype(np.float64)
+        k[k == 0] = np.where(rng.random((k == 0).sum()) < 0.5, -0.0, 0.0)
+    elif case == 1:        # f64 distinct-ish, one empty shard
+        n = 0 if rank == world - 1 else 5000
+        k = rng.random(n)
+    elif case == 2:        # int64 extremes
+        n = 2000 + 13 * rank
+        k = rng.integers(np.iinfo(np.int64).min, np.iinfo(np.int64).max, n, dtype=np.int64, endpoint=True)
+        k[::3] = rng.integers(-3, 3, k[::3].size)
+    elif case == 3:        # uint64, all keys equal on every rank (stability across ranks)
+        n = 1500
+        k = np.full(n, 7, dtype=np.uint64)
+    else:                  # tiny shards (fewer elements than samples)
+        n = 5 + rank
+        k = rng.integers(0, 4, n).astype(np.float64)
+    return k
+
+
+CASES = (0, 1, 2, 3, 4)
+
+
+def _worker(rank, world, port, q):
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2402_01816_b200 import dist as gdist
+    for case in CASES:
+        k = make_shard(case, rank, world)
+        base = sum(make_shard(case, r, world).size for r in range(rank))
+        v = (np.arange(k.size) + base).astype(np.uint32)
+        ok, ov = gdist.sort_distributed(torch.from_numpy(k), torch.from_numpy(v), samples=16, ops=CpuOracleOps())
+        q.put((case, rank, ok.numpy(), ov.numpy()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_distributed_sort_gloo(world):
+    """All five shard patterns in one world_size-`world` gloo group."""
+    import oracle
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=240) for _ in range(world * len(CASES))]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for case in CASES:
+        got = sorted([r for r in res if r[0] == case], key=lambda x: x[1])
+        shards = [make_shard(case, r, world) for r in range(world)]
+        allk = np.concatenate(shards)
+        allv = np.arange(allk.size, dtype=np.uint32)
+        kt = {np.dtype(np.float64): "f64", np.dtype(np.int64): "i64", np.dtype(np.uint64): "u64"}[allk.dtype]
+        ek, ev = oracle.sort_keys(allk, allv, kt)
+        gk = np.concatenate([r[2] for r in got])
+        gv = np.concatenate([r[3] for r in got])
+        assert gk.view(np.uint64).tolist() == ek.view(np.uint64).tolist(), f"case {case} world {world}"
+        assert gv.tolist() == ev.tolist(), f"case {case} world {world}"
+
+
+def test_simulate_matches_collective_cpu():
+    """dist.simulate (one process, no collectives) == the oracle too."""
+    import oracle
+    from paper_2402_01816_b200 import dist as gdist
+    world = 4
+    shards = [make_shard(0, r, world) for r in range(world)]
+    base = np.cumsum([0] + [s.size for s in shards])
+    outs = gdist.simulate([(torch.from_numpy(s), torch.from_numpy((np.arange(s.size) + base[r]).astype(np.uint32)))
+                           for r, s in enumerate(shards)], samples=16, ops=CpuOracleOps())
+    allk = np.concatenate(shards)
+    ek, ev = oracle.sort_keys(allk, np.arange(allk.size, dtype=np.uint32), "f64")
+    assert np.concatenate([o[0].numpy() for o in outs]).view(np.uint64).tolist() == ek.view(np.uint64).tolist()
+    assert np.concatenate([o[1].numpy() for o in outs]).tolist() == ev.tolist()

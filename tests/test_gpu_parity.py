@@ -421,3 +421,113 @@ def test_tile_local_order_mix(gns, target):
         for t0 in range(0, k.size, T1):
             ek, ev = oracle.sort(k[t0:t0 + T1], v[t0:t0 + T1])
             assert_bitexact(dk.cpu().numpy()[t0:t0 + T1], ek, dv.cpu().numpy()[t0:t0 + T1], ev, what=f"tile {t0}")
+
+
+# ---------------------------------------------- NEXT f4: distributed sort steps
+@pytest.mark.parametrize("key_type", ["f64", "i64", "u64"])
+@pytest.mark.parametrize("la,lb", [(1, 1), (0, 5), (7, 0), (4095, 4097), (10000, 333), (333, 10000),
+                                   (3 * T1 + 5, 2 * T1 + 11), (1 << 18, (1 << 17) + 3)])
+def test_merge_two(gns, la, lb, key_type):
+    """gns_merge_two: two sorted runs of any lengths, at unaligned offsets,
+    stable (a wins ties) == the oracle's stable sort of a ++ b."""
+    rng = np.random.default_rng(la * 7 + lb)
+    if key_type == "f64":
+        k = rng.integers(-20, 20, la + lb).astype(np.float64)
+        k[k == 0] = -0.0
+    else:
+        k = _int_keys(key_type, la + lb, la + 3 * lb)
+        k[::4] = k[1]
+    a = oracle.sort_keys(k[:la], None, key_type)[0]
+    b = oracle.sort_keys(k[la:], None, key_type)[0]
+    cat = np.concatenate([a, b])
+    v = synth.iota_u32(la + lb)
+    ek, ev = oracle.sort_keys(cat, v, key_type)
+    # place a and b at odd element offsets of one buffer (8-byte, not 32-byte aligned)
+    pad = np.zeros(3, dtype=cat.dtype)
+    vpad = np.zeros(3, dtype=np.uint32)
+    buf = torch.from_numpy(np.concatenate([pad[:1], a, pad, b])).cuda()
+    vb = torch.from_numpy(np.concatenate([vpad[:1], v[:la], vpad, v[la:]])).cuda()
+    ak, av = buf[1:1 + la], vb[1:1 + la]
+    bk, bv = buf[4 + la:4 + la + lb], vb[4 + la:4 + la + lb]
+    gk, gv = gns.merge_two(ak, av, bk, bv)
+    torch.cuda.synchronize()
+    assert np.array_equal(gk.cpu().numpy().view(np.uint64), ek.view(np.uint64)), (la, lb, key_type)
+    assert np.array_equal(gv.cpu().numpy(), ev), (la, lb, key_type)
+    gk, _ = gns.merge_two(ak, None, bk, None)
+    torch.cuda.synchronize()
+    assert np.array_equal(gk.cpu().numpy().view(np.uint64), ek.view(np.uint64)), (la, lb, key_type, "key-only")
+
+
+@pytest.mark.parametrize("key_type", ["f64", "i64", "u64"])
+def test_split_cuts(gns, key_type):
+    """gns_split_cuts == the definition via numpy.searchsorted (upper bound for
+    lower ranks, lower bound for higher ranks, the position for the owner)."""
+    n = 50000
+    if key_type == "f64":
+        k = np.sort(np.random.default_rng(1).integers(-100, 100, n).astype(np.float64))
+        spl = np.array([-100.0, -3.0, 0.0, 7.5, 99.0, 1000.0])
+    else:
+        k = oracle.sort_keys(_int_keys(key_type, n, 2), None, key_type)[0]
+        spl = k[[0, 10, 20000, 20001, n - 1]]
+    for me in (0, 2, 4):
+        ranks = np.array([1, 2, 3, 2, 5, 0][:spl.size], dtype=np.int32)
+        pos = np.array([5, 17, 0, n, 123, 9][:spl.size], dtype=np.int64)
+        got = gns.split_cuts(torch.from_numpy(k).cuda(), torch.from_numpy(spl).cuda(), torch.from_numpy(ranks).cuda(),
+                             torch.from_numpy(pos).cuda(), me)
+        torch.cuda.synchronize()
+        want = [int(p) if r == me else int(np.searchsorted(k, x, side="right" if me < r else "left"))
+                for x, r, p in zip(spl, ranks, pos)]
+        assert got.cpu().tolist() == want, (key_type, me)
+
+
+@pytest.mark.parametrize("k", [2, 3, 4, 8])
+@pytest.mark.parametrize("pattern", ["uniform", "ties", "skewed"])
+def test_distributed_sort_simulated(gns, k, pattern):
+    """The f4 path's kernels end to end on one GPU: dist.simulate runs the k
+    ranks' steps in one process (exchange = slices, no collectives), vs the
+    oracle's stable sort of the rank-major concatenation."""
+    from paper_2402_01816_b200 import dist as gdist
+    rng = np.random.default_rng(k * 100 + len(pattern))
+    shards = []
+    for r in range(k):
+        n = int(rng.integers(0, 3 * T1)) if pattern == "skewed" else 2 * T1 + 37 * r
+        if pattern == "ties":
+            s = rng.integers(0, 5, n).astype(np.float64)
+        elif pattern == "skewed":
+            s = rng.random(n) + r          # rank r holds [r, r+1): no interleaving
+        else:
+            s = synth.uniform(n, 70 + r)
+        shards.append(s)
+    base = np.cumsum([0] + [s.size for s in shards])
+    ins = [(torch.from_numpy(s).cuda(), torch.from_numpy((np.arange(s.size) + base[r]).astype(np.uint32)).cuda())
+           for r, s in enumerate(shards)]
+    outs = gdist.simulate(ins, samples=32)
+    torch.cuda.synchronize()
+    allk = np.concatenate(shards)
+    ek, ev = oracle.sort(allk, np.arange(allk.size, dtype=np.uint32))
+    gk = np.concatenate([o[0].cpu().numpy() for o in outs])
+    gv = np.concatenate([o[1].cpu().numpy() for o in outs])
+    assert_bitexact(gk, ek, gv, ev, what=f"k={k} {pattern}")
+
+
+def test_distributed_sort_single_rank_nccl(gns):
+    """sort_distributed through a real NCCL process group (world size 1 on
+    this one-GPU box): the collective path's set-up and the local sort."""
+    import torch.distributed as dist
+    from paper_2402_01816_b200 import dist as gdist
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        k = synth.ties(3 * T1 + 5, 8, 30)
+        v = synth.iota_u32(k.size)
+        gk, gv = gdist.sort_distributed(torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda())
+        torch.cuda.synchronize()
+        ek, ev = oracle.sort(k, v)
+        assert_bitexact(gk.cpu().numpy(), ek, gv.cpu().numpy(), ev)
+    finally:
+        dist.destroy_process_group()
