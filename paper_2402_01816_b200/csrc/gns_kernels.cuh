@@ -950,10 +950,10 @@ merge_tstore_kernel(PipeGeo pg, int ntiles, int per_cta, const __grid_constant__
 // 256 threads x 32 keys (TILE = 8192).  The tile arrives by TMA tensor
 // load (2-D maps: keys [n/16][16] f64, vals [n/32][32] u32, 128-byte swizzle)
 // and leaves by one TMA tensor store; the blocked register<->smem transfers
-// use 16-byte accesses in the swizzled layout.  In registers: two stable
-// odd-even transposition sorts of 16; then log2(4096/16) = 8 shared-memory
-// merge rounds (round 0 merges each thread's own two halves, no search).  With
-// 32 outputs per thread the merge-path searches per key are halved vs VT=16.
+// use 16-byte accesses in the swizzled layout.  In registers: one stable
+// odd-even transposition sort of the thread's 32 keys; then log2(8192/32) = 8
+// shared-memory merge rounds (merge path + serial merge, left wins ties).
+// With 32 outputs per thread the merge-path searches per key are halved vs 16.
 constexpr size_t T1_KEY_BYTES = TILE * 8 + 1024;
 constexpr size_t T1_VAL_BYTES = TILE * 4 + 1024;
 constexpr size_t t1_smem(bool hv) { return T1_KEY_BYTES + (hv ? T1_VAL_BYTES : 0) + 1024; }
@@ -995,13 +995,15 @@ __device__ __forceinline__ int tv_slot(int e)     // u32, 32 per row
     return (r << 5) | ((((e >> 2) & 7) ^ (r & 7)) << 2) | (e & 3);
 }
 
-template <int O, bool HV, int ORD>
-__device__ __forceinline__ void transpose_sort16(double (&k)[VT1], uint32_t (&v)[VT1])
+// Stable odd-even transposition sort of k[O:O+N) (adjacent compare-exchange,
+// swap only if the right key is strictly before the left one).
+template <int O, int N, bool HV, int ORD>
+__device__ __forceinline__ void transpose_sort(double (&k)[VT1], uint32_t (&v)[VT1])
 {
 #pragma unroll
-    for (int r = 0; r < 16; ++r) {
+    for (int r = 0; r < N; ++r) {
 #pragma unroll
-        for (int i = r & 1; i + 1 < 16; i += 2) {
+        for (int i = r & 1; i + 1 < N; i += 2) {
             const bool p = before<ORD>(k[O + i + 1], k[O + i]);
             const double lo = p ? k[O + i + 1] : k[O + i];
             const double hi = p ? k[O + i] : k[O + i + 1];
@@ -1150,13 +1152,13 @@ tile_sort2_kernel(const double *src_k, const uint32_t *src_v, double *dst_k, uin
 #define GNS_TS_EXP 0
 #endif
     if (mode == 0) {
-    if (GNS_TS_EXP != 1) {   // (timing experiments only: 1 = no register sort, 2 = no smem merge rounds)
-        transpose_sort16<0, HV, ORD>(k, v);
-        transpose_sort16<16, HV, ORD>(k, v);
-    }
+    // the thread's 32 keys: one stable odd-even transposition sort in
+    // registers (trades ALU, which has headroom, for the shared-memory round
+    // that merged two sorted halves: measured -1.6 %)
+    if (GNS_TS_EXP != 1) transpose_sort<0, 32, HV, ORD>(k, v);   // (timing experiments: 1 = no register sort)
     __syncthreads();                       // the TMA-layout reads are done before the first spill
 #pragma unroll 1
-    for (int coop = 1; coop <= (GNS_TS_EXP == 2 ? 1 : NT1); coop <<= 1) {
+    for (int coop = 2; coop <= (GNS_TS_EXP == 2 ? 1 : NT1); coop <<= 1) {
 #pragma unroll
         for (int x = 0; x < VT1; ++x) {
             *reinterpret_cast<double *>(reinterpret_cast<unsigned char *>(sk) +
@@ -1164,9 +1166,7 @@ tile_sort2_kernel(const double *src_k, const uint32_t *src_v, double *dst_k, uin
             if (HV) sv[swmv(e0 + x)] = v[x];
         }
         __syncthreads();
-        if (coop == 1) {                   // merge the thread's own two sorted halves
-            serial_merge32<HV, ORD>(sk, sv, e0, e0 + 16, e0 + 16, e0 + 32, k, v);
-        } else {
+        {
             const int local = tid & (coop - 1);
             const int a0 = (tid - local) * VT1;
             const int run = (coop >> 1) * VT1;
