@@ -278,9 +278,11 @@ def main():
 
     footprint = None
     presorted = None
+    others = None
     if rank == 0 and world == 1 and not args.no_footprint and args.config == 2:
         footprint = footprint_cfg5(gns, torch, dev, stream, flush)
         presorted = config4(gns, torch, dev, stream, flush)
+        others = other_configs(gns, torch, dev, stream, flush)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -315,6 +317,8 @@ def main():
         line["footprint_cfg5"] = footprint
     if presorted:
         line["presorted_cfg4"] = presorted
+    if others:
+        line["other_configs"] = others
     if rank == 0:
         print(json.dumps(line), flush=True)
     if pg:
@@ -502,6 +506,38 @@ def config4(gns, torch, dev, stream, flush, reps=5):
         ok = bool((k[1:] >= k[:-1]).all().item())
         ms = float(np.median(ts))
         out[sub] = {"ms": ms, "keys_per_s": n / (ms / 1e3), "sorted": ok}
+    return out
+
+
+def other_configs(gns, torch, dev, stream, flush, reps=5):
+    """configs[0] (2^16 permutation + payload) and configs[2] (2^24 heavy
+    ties + payload), buffer 1.0: median ms and keys/s (same timing rules)."""
+    out = {}
+    for c in (1, 3):
+        case = synth.config(c)
+        n = case.keys.size
+        src = torch.from_numpy(case.keys).to(dev)
+        srcv = torch.from_numpy(case.vals).to(dev)
+        k, v = torch.empty_like(src), torch.empty_like(srcv)
+        ws = gns.alloc_workspace(n, 1.0, True, dev)
+        ts = []
+        for i in range(reps + 3):
+            k.copy_(src)
+            v.copy_(srcv)
+            flush.fill_(1)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            gns.sort_(k, v, 1.0, workspace=ws)
+            b.record(stream)
+            torch.cuda.synchronize()
+            if i >= 3:
+                ts.append(a.elapsed_time(b))
+        tie = k[1:] == k[:-1]
+        ok = bool((k[1:] >= k[:-1]).all().item()) and bool(
+            (v[1:].to(torch.int64)[tie] > v[:-1].to(torch.int64)[tie]).all().item())
+        ms = float(np.median(ts))
+        out[f"cfg{c}"] = {"workload": case.shape, "n": n, "payload": True, "ms": ms,
+                          "keys_per_s": n / (ms / 1e3), "sorted_stable": ok}
     return out
 
 

@@ -219,6 +219,19 @@ gns_status row_map(void *base, size_t n, bool f64, int box_rows, CUtensorMap *ma
     return GNS_OK;
 }
 
+// Key map of a merge input run for the stage loads: rows of 16 keys starting
+// at ptr rounded down to 16 bytes (idx0 = 0 or 1 keys before ptr), boxes of
+// krows(hv) rows, 128-byte swizzle; `rows` = full rows (the partial last row is
+// patched by the merge warps).
+gns_status key_map(const double *ptr, size_t count, bool hv, CUtensorMap *map, long long *idx0, long long *rows)
+{
+    const uintptr_t a = (uintptr_t)ptr;
+    const double *base = (const double *)(a & ~(uintptr_t)15);
+    *idx0 = (long long)(ptr - base);
+    *rows = (long long)((count + (size_t)*idx0) / 16);
+    return row_map((void *)base, (size_t)(*rows) * 16, true, krows(hv), map);
+}
+
 // Programmatic dependent launch: every kernel of a sort is launched with
 // programmatic stream serialization; it may be scheduled while its predecessor
 // drains and waits in griddepcontrol.wait until the predecessor's writes are
@@ -313,14 +326,18 @@ gns_status launch_merge(const MergeGeo &g, const double *lim_a, const double *li
     pg.g = g;
     pg.a_lim = lim_a;
     pg.b_lim = lim_b;
-    CUtensorMap map;
+    CUtensorMap map, amap, bmap;
     GNS_TRY(row_map(g.ok, (size_t)g.n, true, MTILE / 16, &map));
+    // (B may start past the array end when the last pair has no B run: empty map, never loaded)
+    GNS_TRY(key_map(g.ak, (size_t)std::max<long long>(0, lim_a - g.ak), hv, &amap, &pg.a_idx0, &pg.a_rows));
+    GNS_TRY(key_map(g.bk, (size_t)std::max<long long>(0, lim_b - g.bk), hv, &bmap, &pg.b_idx0, &pg.b_rows));
     if (!inplace) {
         const int ctas = std::min(ntiles, 2 * num_sms());
         const int per = (int)ceil_div(ntiles, ctas);
         const int grid = (int)ceil_div(ntiles, per);
         auto kern = merge_kern(hv, ord);
-        return launch_pdl("merge_tstore_kernel", kern, grid, WS_THREADS, ts_smem(hv), st, pg, ntiles, per, map, ad);
+        return launch_pdl("merge_tstore_kernel", kern, grid, WS_THREADS, ts_smem(hv), st, pg, ntiles, per, map, amap,
+                          bmap, ad);
     }
     GNS_TRY(launch_pdl("partition_kernel", partition_kern(ord),
                        (unsigned)ceil_div((size_t)ntiles * 32, 256), 256, 0, st, g, ntiles, corank));
@@ -330,7 +347,7 @@ gns_status launch_merge(const MergeGeo &g, const double *lim_a, const double *li
     const int grid = std::min(ntiles, 2 * num_sms());
     auto kern = inplace_kern(hv, ord);
     return launch_pdl("merge_inplace_kernel", kern, grid, NT, ts_smem(hv), st, pg, ntiles, (const int *)corank,
-                      (const int2 *)deps, flags, ticket, map);
+                      (const int2 *)deps, flags, ticket, map, amap, bmap);
 }
 
 gns_status launch_reverse(double *k, uint32_t *v, size_t n, cudaStream_t st)
@@ -771,13 +788,16 @@ gns_status gns_merge_two(const void *a_keys, const uint32_t *a_vals, size_t la, 
     pg.g = g;
     pg.a_lim = g.ak + la;
     pg.b_lim = g.bk + lb;
-    CUtensorMap map;
+    CUtensorMap map, amap, bmap;
     GNS_TRY(row_map(g.ok, n, true, MTILE / 16, &map));
+    GNS_TRY(key_map(g.ak, la, hv, &amap, &pg.a_idx0, &pg.a_rows));
+    GNS_TRY(key_map(g.bk, lb, hv, &bmap, &pg.b_idx0, &pg.b_rows));
     const int ctas = std::min(ntiles, 2 * num_sms());
     const int per = (int)ceil_div(ntiles, ctas);
     const int grid = (int)ceil_div(ntiles, per);
     auto kern = merge_kern(hv, ord_of(false, (int)key_type));
-    return launch_pdl("merge_tstore_kernel", kern, grid, WS_THREADS, ts_smem(hv), st, pg, ntiles, per, map, Adapt{});
+    return launch_pdl("merge_tstore_kernel", kern, grid, WS_THREADS, ts_smem(hv), st, pg, ntiles, per, map, amap, bmap,
+                      Adapt{});
 }
 
 gns_status gns_split_cuts(const void *sorted_keys, gns_key_type key_type, size_t n, const void *spl_keys,

@@ -157,6 +157,14 @@ __device__ __forceinline__ double lds_f64(uint32_t a)
     asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
     return v;
 }
+// the same with an L2 cache-policy hint (evict-first for data read once)
+__device__ __forceinline__ void tma_load_2d_hint(void *dst, const CUtensorMap *map, int c0, int c1, uint64_t *bar,
+                                                 uint64_t policy)
+{
+    asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+                 " [%0], [%1, {%2, %3}], [%4], %5;"
+                 :: "r"(smem_u32(dst)), "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(policy) : "memory");
+}
 __device__ __forceinline__ void lds128(const void *p, double &a, double &b)
 {
     asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(a), "=d"(b) : "r"(smem_u32(p)));
@@ -258,47 +266,6 @@ __device__ __forceinline__ double pad_key()
     if (KT == KT_I64) return __longlong_as_double(DESC ? (long long)0x8000000000000000ULL : 0x7FFFFFFFFFFFFFFFLL);
     if (KT == KT_U64) return __longlong_as_double(DESC ? 0LL : (long long)0xFFFFFFFFFFFFFFFFULL);
     return __longlong_as_double(DESC ? (long long)0xFFF0000000000000ULL : 0x7FF0000000000000LL);
-}
-
-// Stable co-rank (merge path) of diagonal d for sorted runs A[0:na), B[0:nb)
-// in shared memory: the number of A elements among the first d outputs of the
-// stable merge in which A (the left run) wins ties (Knuth's merge;
-// SPEC.md:290).  Predicate: A[m] <= B[d-1-m]  =>  the m-th A element precedes.
-template <int ORD, class IX>
-__device__ __forceinline__ int merge_path_smem(const double *s, int a0, int na, int b0, int nb, int d, IX ix)
-{
-    int lo = max(0, d - nb), hi = min(d, na);
-    while (lo < hi) {
-        int m = (lo + hi) >> 1;
-        if (!before<ORD>(s[ix(b0 + d - 1 - m)], s[ix(a0 + m)])) lo = m + 1;
-        else hi = m;
-    }
-    return lo;
-}
-
-// Serial merge of VT outputs from shared memory, starting at A index ai and B
-// index bi (ends aend/bend, exclusive).  B's head is taken only if strictly
-// smaller than A's (left wins ties).  Reads one slot past a run end at most
-// (the shared arrays carry spare slots; the value is never used).
-template <bool HV, int ORD, class IK, class IV>
-__device__ __forceinline__ void serial_merge(const double *sk, const uint32_t *sv, int ai, int aend,
-                                             int bi, int bend, double (&k)[VT], uint32_t (&v)[VT],
-                                             IK ik, IV iv)
-{
-    GNS_DASSERT(ai >= 0 && bi >= 0 && aend <= bend && bend <= MTILE + 128);
-    double ka = sk[ik(ai)], kb = sk[ik(bi)];
-#pragma unroll
-    for (int x = 0; x < VT; ++x) {
-        const bool p = (bi < bend) && ((ai >= aend) || before<ORD>(kb, ka));
-        k[x] = p ? kb : ka;
-        const int src = p ? bi : ai;
-        if (HV) v[x] = sv[iv(src)];
-        const int nxt = src + 1;
-        if (p) bi = nxt; else ai = nxt;
-        GNS_DASSERT(nxt >= 0 && nxt < MTILE + 128);
-        const double kn = sk[ik(nxt)];
-        if (p) kb = kn; else ka = kn;
-    }
 }
 
 // ----------------------------------------------------------- merge geometry
@@ -562,31 +529,57 @@ inplace_deps_kernel(const int *__restrict__ corank, int ntiles, long long L, lon
 // the TMA engine (cp.async.bulk, issued by one thread) streams the inputs of
 // tile i+1 -- exactly A[i0:i1) and B[j0:j1), from the co-ranks -- into the
 // other stage, so HBM reads run continuously under the merge arithmetic.
-// Keys and vals of global element g land in the same shared slot
-// (slot = base + (g mod 4) + ...), which keeps every bulk copy 16-byte
-// aligned for both 8-byte keys and 4-byte vals; at most one key / three vals
-// at an unaligned array end are read with plain loads instead.
-constexpr int PIPE_STAGES = 2;
-constexpr int PIPE_SLOTS = MTILE + 32;
-constexpr size_t pipe_stage_bytes(bool hv) { return PIPE_SLOTS * (sizeof(double) + (hv ? sizeof(uint32_t) : 0)); }
+// Keys arrive by TMA tensor loads of whole 128-byte rows (16 keys) in boxes of
+// KROWS rows, with the 128-byte swizzle (16-byte chunk c of stage row r at
+// chunk c ^ (r & 7)), so stride-16 reads (threads at neighbouring 16-output
+// segments of a copy-like tile: ties, presorted data) spread over the banks
+// instead of hitting one.  A's rows fill stage rows [0, RA), B's rows start at
+// row RA (a multiple of KROWS); key slot s = 16 * stage row + column.  Rows past
+// an array's last full row are out of the map (zero filled); their few real
+// keys are patched by the merge warps from global memory.  Vals keep 1-D bulk
+// copies into their own region (slot = base + (g mod 4) + ..., so every copy
+// is 16-byte aligned; at most three vals at an unaligned array end are read
+// with plain loads).
+// rows per key box: 32 (4 KB) key-only, 16 (2 KB) with payload (shared
+// memory for two CTAs per SM); fewer, larger boxes measured faster
+constexpr int krows(bool hv) { return hv ? 16 : 32; }
+// stage key rows: >= 4096/16 + 4 + 2 * (krows - 1), rounded up to a multiple of krows
+constexpr int stage_key_rows(bool hv) { return ((MTILE / 16 + 4 + 2 * (krows(hv) - 1)) + krows(hv) - 1) / krows(hv) * krows(hv); }
+constexpr int PIPE_VSLOTS = MTILE + 128;
+
+// key slot s of a stage whose 1 KiB-aligned base is `base` (shared address)
+__device__ __forceinline__ uint32_t stage_addr(uint32_t base, int s)
+{
+    const uint32_t b = 8u * (uint32_t)s;
+    return base + (b ^ ((b >> 3) & 0x70u));
+}
 
 struct PipeGeo {
     MergeGeo g;
     const double *a_lim;   // end of the array holding the A runs (keys)
     const double *b_lim;   // end of the array holding the B runs (keys)
+    long long a_idx0;      // element index of g.ak[0] in the A key map's array
+    long long b_idx0;      // element index of g.bk[0] in the B key map's array
+    long long a_rows;      // full 16-key rows of the A map (row a_rows is patched by hand)
+    long long b_rows;
 };
 
 struct PipeMeta {
-    int t, ca, cb, offa, bslot;
+    int t, ca, cb;
+    int offa, bslot;       // key slots of A[0], B[0]
+    int voffa, vbslot;     // val slots of A[0], B[0]
+    int pa_slot, pa_cnt;   // A keys at slots [pa_slot, +pa_cnt) to patch from pa_src
+    int pb_slot, pb_cnt;
+    const double *pa_src;
+    const double *pb_src;
 };
 
-// Thread-0 side: computes tile t's input slices and issues their bulk copies
-// into stage buffers sk/sv, completing on `bar`.  Leftover unaligned tail
-// elements are copied with plain loads (made visible by the caller's barrier).
+// Thread-0 side: computes tile t's input slices and issues their copies into
+// the stage (keys at sk, vals at sv), completing on `bar`.
 template <bool HV>
-__device__ __forceinline__ void pipe_issue(const PipeGeo &pg, int t, int i0, int i1next,
-                                           double *sk, uint32_t *sv, uint64_t *bar, PipeMeta *meta,
-                                           uint64_t policy)
+__device__ __forceinline__ void pipe_issue(const PipeGeo &pg, const CUtensorMap &amap, const CUtensorMap &bmap,
+                                           int t, int i0, int i1next, double *sk, uint32_t *sv, uint64_t *bar,
+                                           PipeMeta *meta, uint64_t policy)
 {
     const MergeGeo &g = pg.g;
     const TileSpan s = tile_span(g, t);
@@ -599,69 +592,137 @@ __device__ __forceinline__ void pipe_issue(const PipeGeo &pg, int t, int i0, int
     const double *Bk = g.bk + s.pbase + j0;
     const uint32_t *Av = HV ? g.av + s.pbase + i0 : nullptr;
     const uint32_t *Bv = HV ? g.bv + s.pbase + j0 : nullptr;
-    const int offa = (int)(((uintptr_t)Ak >> 3) & 3);
-    const int offb = (int)(((uintptr_t)Bk >> 3) & 3);
-    const int bbase = (offa + ca + 3) & ~3;
-    // one run: elements [0, c) of K/V, shared slot of element e = sbase + off + e
     GNS_DASSERT(i0 >= 0 && ca >= 0 && cb >= 0 && i0 + ca <= s.na && j0 >= 0 && j0 + cb <= s.nb);
-    auto run = [&](const double *K, const uint32_t *V, int c, int off, int sbase, const double *lim) {
-        if (c <= 0) return;
-        const long long avail = lim - K;       // elements readable from K
-        GNS_DASSERT(avail >= c && sbase + off + c + 4 <= PIPE_SLOTS + 96);
-        // keys: 16-byte chunks of 2
-        const int ks = -(off & 1);
-        int ke = ks + ((c - ks + 1) & ~1);
-        if (ke > avail) ke = ks + (int)((avail - ks) & ~1LL);
-        if (ke > ks) {
-            tma_load_1d(sk + sbase + off + ks, K + ks, (uint32_t)(ke - ks) * 8u, bar, policy);
-        }
-        for (int e = max(ke, 0); e < c; ++e) sk[sbase + off + e] = K[e];
-        if (HV) {
-            const int vs = -off;
-            int ve = vs + ((c - vs + 3) & ~3);
-            if (ve > avail) ve = vs + (int)((avail - vs) & ~3LL);
-            if (ve > vs) {
-                tma_load_1d(sv + sbase + off + vs, V + vs, (uint32_t)(ve - vs) * 4u, bar, policy);
-            }
-            for (int e = max(ve, 0); e < c; ++e) sv[sbase + off + e] = V[e];
+    // ---- keys: rows [r0, r1] of the slice, boxes of KROWS rows
+    const long long ga = pg.a_idx0 + s.pbase + i0, gb = pg.b_idx0 + s.pbase + j0;
+    constexpr int KROWS = krows(HV);
+    const int nba = ca > 0 ? (int)((((ga + ca - 1) >> 4) - (ga >> 4)) / KROWS) + 1 : 0;
+    const int nbb = cb > 0 ? (int)((((gb + cb - 1) >> 4) - (gb >> 4)) / KROWS) + 1 : 0;
+    const int rb0 = nba * KROWS;                                   // B's first stage row
+    GNS_DASSERT(rb0 + nbb * KROWS <= stage_key_rows(HV));
+    // ---- vals: 1-D bulk copies (16-byte chunks of 4) + plain loads at an unaligned end
+    const int voffa = HV ? (int)(((uintptr_t)Av >> 2) & 3) : 0;
+    const int voffb = HV ? (int)(((uintptr_t)Bv >> 2) & 3) : 0;
+    const int vbbase = (voffa + ca + 3) & ~3;
+    auto vrange = [&](const double *K, int c, int off, const double *lim, int &vs, int &ve) {
+        const long long avail = lim - K;           // elements readable
+        vs = -off;
+        ve = vs + ((c - vs + 3) & ~3);
+        if (ve > avail) ve = vs + (int)((avail - vs) & ~3LL);
+    };
+    uint32_t total = (uint32_t)(nba + nbb) * (KROWS * 128u);
+    int vsa = 0, vea = 0, vsb = 0, veb = 0;
+    if (HV) {
+        if (ca > 0) vrange(Ak, ca, voffa, pg.a_lim, vsa, vea);
+        if (cb > 0) vrange(Bk, cb, voffb, pg.b_lim, vsb, veb);
+        if (vea > vsa) total += (uint32_t)(vea - vsa) * 4u;
+        if (veb > vsb) total += (uint32_t)(veb - vsb) * 4u;
+    }
+    // Post the expected byte count first (no arrival yet), then issue.
+    mbar_expect_tx(bar, total);
+    for (int b = 0; b < nba; ++b)
+        tma_load_2d_hint(sk + b * KROWS * 16, &amap, 0, (int)((ga >> 4) + b * KROWS), bar, policy);
+    for (int b = 0; b < nbb; ++b)
+        tma_load_2d_hint(sk + (rb0 + b * KROWS) * 16, &bmap, 0, (int)((gb >> 4) + b * KROWS), bar, policy);
+    if (HV) {
+        if (vea > vsa) tma_load_1d(sv + voffa + vsa, Av + vsa, (uint32_t)(vea - vsa) * 4u, bar, policy);
+        for (int e = max(vea, 0); e < ca; ++e) sv[voffa + e] = Av[e];
+        if (veb > vsb) tma_load_1d(sv + vbbase + voffb + vsb, Bv + vsb, (uint32_t)(veb - vsb) * 4u, bar, policy);
+        for (int e = max(veb, 0); e < cb; ++e) sv[vbbase + voffb + e] = Bv[e];
+    }
+    PipeMeta mt;
+    mt.t = t;
+    mt.ca = ca;
+    mt.cb = cb;
+    mt.offa = (int)(ga & 15);
+    mt.bslot = rb0 * 16 + (int)(gb & 15);
+    mt.voffa = voffa;
+    mt.vbslot = vbbase + voffb;
+    // keys past the last full row of a map (out of the box, zero filled)
+    auto patch = [&](long long gi, int c, int slot0, long long rows, const double *src, int &pslot, int &pcnt,
+                     const double *&psrc) {
+        const long long lim = rows * 16;
+        pcnt = 0;
+        pslot = 0;
+        psrc = src;
+        if (c > 0 && gi + c > lim) {
+            const int e0 = (int)max(0LL, lim - gi);
+            pcnt = c - e0;
+            pslot = slot0 + e0;
+            psrc = src + e0;
         }
     };
-    // Post the expected byte count first (no arrival yet), then issue.
-    {
-        // dry run of the byte count (same arithmetic as run())
-        auto bytes = [&](const double *K, int c, int off, const double *lim) -> uint32_t {
-            if (c <= 0) return 0;
-            const long long avail = lim - K;
-            uint32_t b = 0;
-            const int ks = -(off & 1);
-            int ke = ks + ((c - ks + 1) & ~1);
-            if (ke > avail) ke = ks + (int)((avail - ks) & ~1LL);
-            if (ke > ks) b += (uint32_t)(ke - ks) * 8u;
-            if (HV) {
-                const int vs = -off;
-                int ve = vs + ((c - vs + 3) & ~3);
-                if (ve > avail) ve = vs + (int)((avail - vs) & ~3LL);
-                if (ve > vs) b += (uint32_t)(ve - vs) * 4u;
-            }
-            return b;
-        };
-        const uint32_t total = bytes(Ak, ca, offa, pg.a_lim) + bytes(Bk, cb, offb, pg.b_lim);
-        mbar_expect_tx(bar, total);
-    }
-    run(Ak, Av, ca, offa, 0, pg.a_lim);
-    run(Bk, Bv, cb, offb, bbase, pg.b_lim);
-    meta->t = t;
-    meta->ca = ca;
-    meta->cb = cb;
-    meta->offa = offa;
-    meta->bslot = bbase + offb;
+    patch(ga, ca, mt.offa, pg.a_rows, Ak, mt.pa_slot, mt.pa_cnt, mt.pa_src);
+    patch(gb, cb, mt.bslot, pg.b_rows, Bk, mt.pb_slot, mt.pb_cnt, mt.pb_src);
+    *meta = mt;
     // The stage's phase completes only after this arrive (the barrier expects
-    // one arrival) and the bulk-copy bytes: everything written above by this
-    // thread (meta, unaligned tail elements) is released to the waiters.
+    // one arrival) and the copies' bytes: everything written above by this
+    // thread (meta, unaligned tail vals) is released to the waiters.
     mbar_arrive(bar);
 }
 
-struct Lin { __device__ __forceinline__ int operator()(int e) const { return e; } };
+// Merge-warp side, after the stage's full barrier: copy the keys the TMA box
+// could not deliver (past a map's last full row; at most 15 per run, only at
+// an array end) into their swizzled slots, then sync the merge warps.
+__device__ __forceinline__ void stage_patch(uint32_t kbase, const PipeMeta &mt, int tid)
+{
+    if ((mt.pa_cnt | mt.pb_cnt) == 0) return;
+    if (tid < mt.pa_cnt)
+        asm volatile("st.shared.f64 [%0], %1;" :: "r"(stage_addr(kbase, mt.pa_slot + tid)), "d"(mt.pa_src[tid])
+                     : "memory");
+    if (tid < mt.pb_cnt)
+        asm volatile("st.shared.f64 [%0], %1;" :: "r"(stage_addr(kbase, mt.pb_slot + tid)), "d"(mt.pb_src[tid])
+                     : "memory");
+    asm volatile("bar.sync 1, %0;" :: "n"(NT) : "memory");
+}
+
+// Stable co-rank (merge path) of diagonal d for the stage's runs (key slots
+// A: a0.., B: b0..): the number of A keys among the first d outputs, A wins
+// ties.  Predicate: A[m] <= B[d-1-m].
+template <int ORD>
+__device__ __forceinline__ int merge_path_stage(uint32_t kbase, int a0, int na, int b0, int nb, int d)
+{
+    int lo = max(0, d - nb), hi = min(d, na);
+    while (lo < hi) {
+        const int m = (lo + hi) >> 1;
+        const double bk = lds_f64(stage_addr(kbase, b0 + d - 1 - m));
+        const double ak = lds_f64(stage_addr(kbase, a0 + m));
+        if (!before<ORD>(bk, ak)) lo = m + 1;
+        else hi = m;
+    }
+    return lo;
+}
+
+// Serial merge of VT outputs from the stage, starting at key slots ai (A) and
+// bi (B), run ends aend / bend (exclusive).  B's head is taken only if
+// strictly before A's (left wins ties).  The consumed side's next key is
+// loaded straight into its head register (predicated loads); reads at most
+// one slot past a run end (the value is never used).
+template <bool HV, int ORD>
+__device__ __forceinline__ void serial_merge_stage(uint32_t kbase, const uint32_t *sv, const PipeMeta &mt, int ai,
+                                                   int aend, int bi, int bend, double (&k)[VT], uint32_t (&v)[VT])
+{
+    GNS_DASSERT(ai >= 0 && bi >= 0 && aend <= bend && bend <= stage_key_rows(HV) * 16);
+    double ka = lds_f64(stage_addr(kbase, ai)), kb = lds_f64(stage_addr(kbase, bi));
+#pragma unroll
+    for (int x = 0; x < VT; ++x) {
+        const bool p = (bi < bend) && ((ai >= aend) || before<ORD>(kb, ka));
+        k[x] = p ? kb : ka;
+        const int src = p ? bi : ai;
+        if (HV) v[x] = sv[src < mt.bslot ? src - mt.offa + mt.voffa : src - mt.bslot + mt.vbslot];
+        const int nxt = src + 1;
+        GNS_DASSERT(nxt < stage_key_rows(HV) * 16);
+        const uint32_t a = stage_addr(kbase, nxt);
+        if (p) {
+            bi = nxt;
+            kb = lds_f64(a);
+        } else {
+            ai = nxt;
+            ka = lds_f64(a);
+        }
+    }
+}
+
 
 // ------------------------------- shared pieces of the fused merge kernels
 constexpr int SEARCH_WARPS = 2;
@@ -692,9 +753,9 @@ __device__ __forceinline__ void bar_merge_warps() { asm volatile("bar.sync 1, %0
 // with conflict-free st.shared.v2 into the 128-byte-swizzled layout; one
 // cp.async.bulk.tensor stores the 32 KB tile.  Vals (if any) are stored by the
 // merge threads with 256-bit stores.
-constexpr int TS_KEY_SLOTS = MTILE + 128;                       // 33,792 B = 33 KiB
-constexpr size_t TS_VAL_BYTES = ((MTILE + 128) * 4 + 1023) / 1024 * 1024;
-constexpr size_t ts_stage_bytes(bool hv) { return TS_KEY_SLOTS * 8 + (hv ? TS_VAL_BYTES : 0); }
+constexpr size_t ts_key_bytes(bool hv) { return (size_t)stage_key_rows(hv) * 128; }   // 43,008 / 38,912 B
+constexpr size_t TS_VAL_BYTES = ((size_t)PIPE_VSLOTS * 4 + 1023) / 1024 * 1024;
+constexpr size_t ts_stage_bytes(bool hv) { return ts_key_bytes(hv) + (hv ? TS_VAL_BYTES : 0); }
 constexpr size_t ts_smem(bool hv, int ns = 2) { return ns * ts_stage_bytes(hv) + 1024; }
 constexpr int MERGE_WARPS = NT / 32;                 // 8
 constexpr int PRODUCER_WARP = MERGE_WARPS;           // 8
@@ -739,7 +800,8 @@ constexpr int WS_THREADS = NT + 32 + 32 * SEARCH_WARPS;   // 352
 
 template <bool HV, int ORD, int NS = 2>
 __global__ void __launch_bounds__(WS_THREADS, 2)
-merge_tstore_kernel(PipeGeo pg, int ntiles, int per_cta, const __grid_constant__ CUtensorMap omap, Adapt ad)
+merge_tstore_kernel(PipeGeo pg, int ntiles, int per_cta, const __grid_constant__ CUtensorMap omap,
+                    const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap bmap, Adapt ad)
 {
 #ifdef GNS_PROF
     unsigned long long acc[16] = {};
@@ -766,7 +828,7 @@ merge_tstore_kernel(PipeGeo pg, int ntiles, int per_cta, const __grid_constant__
     __shared__ volatile int spl_used;
     auto skb = [&](int st) { return reinterpret_cast<double *>(smem_raw + st * ts_stage_bytes(HV)); };
     auto svb = [&](int st) {
-        return reinterpret_cast<uint32_t *>(smem_raw + st * ts_stage_bytes(HV) + TS_KEY_SLOTS * sizeof(double));
+        return reinterpret_cast<uint32_t *>(smem_raw + st * ts_stage_bytes(HV) + ts_key_bytes(HV));
     };
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
@@ -848,7 +910,7 @@ merge_tstore_kernel(PipeGeo pg, int ntiles, int per_cta, const __grid_constant__
         };
         auto issue = [&](int i) {
             const int st = i % NS;
-            pipe_issue<HV>(pg, first + i, get_split(i), (i + 1 < nspl) ? get_split(i + 1) : 0, skb(st), svb(st),
+            pipe_issue<HV>(pg, amap, bmap, first + i, get_split(i), (i + 1 < nspl) ? get_split(i + 1) : 0, skb(st), svb(st),
                            &full[st], &meta[st], policy);
             spl_used = i;
         };
@@ -901,11 +963,13 @@ merge_tstore_kernel(PipeGeo pg, int ntiles, int per_cta, const __grid_constant__
         const int d = min(tid * VT, cnt);
         double *sk = skb(st);
         const uint32_t *sv = svb(st);
+        const uint32_t kbase = smem_u32(sk);
+        stage_patch(kbase, mt, tid);
         double k[VT];
         uint32_t v[VT];
-        const int ii = merge_path_smem<ORD>(sk, mt.offa, mt.ca, mt.bslot, mt.cb, d, Lin());
-        serial_merge<HV, ORD>(sk, sv, mt.offa + ii, mt.offa + mt.ca, mt.bslot + d - ii, mt.bslot + mt.cb, k, v,
-                               Lin(), Lin());
+        const int ii = merge_path_stage<ORD>(kbase, mt.offa, mt.ca, mt.bslot, mt.cb, d);
+        serial_merge_stage<HV, ORD>(kbase, sv, mt, mt.offa + ii, mt.offa + mt.ca, mt.bslot + d - ii, mt.bslot + mt.cb, k,
+                                    v);
         const long long t = first + i;
         const long long row = t * (MTILE / 16) + tid;    // global row of this thread's 16 outputs
         if (pg.g.so != nullptr && (tid & (SMP_G / VT - 1)) == 0 && d < cnt)
@@ -968,7 +1032,7 @@ __device__ __forceinline__ int swm(int e) { return e ^ ((e >> 5) & 15); }
 __device__ __forceinline__ uint32_t swa(uint32_t a) { return a ^ ((a >> 5) & 0x78u); }
 __device__ __forceinline__ int swmv(int e) { return e ^ ((e >> 5) & 31); }
 struct SwM { __device__ __forceinline__ int operator()(int e) const { return swm(e); } };
-// merge_path_smem over the tile-sort layout (keys at swa(base + 8e)).
+// Stable co-rank over the tile-sort layout (keys at swa(base + 8e)); A wins ties.
 template <int ORD>
 __device__ __forceinline__ int merge_path_tile(uint32_t base, int a0, int na, int b0, int nb, int d)
 {
@@ -1148,17 +1212,14 @@ tile_sort2_kernel(const double *src_k, const uint32_t *src_v, double *dst_k, uin
             if (g) atomicOr(unsorted, g);
         }
     }
-#ifndef GNS_TS_EXP
-#define GNS_TS_EXP 0
-#endif
     if (mode == 0) {
     // the thread's 32 keys: one stable odd-even transposition sort in
     // registers (trades ALU, which has headroom, for the shared-memory round
     // that merged two sorted halves: measured -1.6 %)
-    if (GNS_TS_EXP != 1) transpose_sort<0, 32, HV, ORD>(k, v);   // (timing experiments: 1 = no register sort)
+    transpose_sort<0, 32, HV, ORD>(k, v);
     __syncthreads();                       // the TMA-layout reads are done before the first spill
 #pragma unroll 1
-    for (int coop = 2; coop <= (GNS_TS_EXP == 2 ? 1 : NT1); coop <<= 1) {
+    for (int coop = 2; coop <= NT1; coop <<= 1) {
 #pragma unroll
         for (int x = 0; x < VT1; ++x) {
             *reinterpret_cast<double *>(reinterpret_cast<unsigned char *>(sk) +
@@ -1258,7 +1319,8 @@ tile_sort2_kernel(const double *src_k, const uint32_t *src_v, double *dst_k, uin
 template <bool HV, int ORD>
 __global__ void __launch_bounds__(NT, 2)
 merge_inplace_kernel(PipeGeo pg, int ntiles, const int *__restrict__ corank, const int2 *__restrict__ deps,
-                     unsigned *flags, unsigned *ticket, const __grid_constant__ CUtensorMap omap)
+                     unsigned *flags, unsigned *ticket, const __grid_constant__ CUtensorMap omap,
+                     const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap bmap)
 {
     pdl_wait();
     extern __shared__ __align__(16) unsigned char smem_raw0[];
@@ -1268,7 +1330,7 @@ merge_inplace_kernel(PipeGeo pg, int ntiles, const int *__restrict__ corank, con
     __shared__ int s_next;
     auto skb = [&](int st) { return reinterpret_cast<double *>(smem_raw + st * ts_stage_bytes(HV)); };
     auto svb = [&](int st) {
-        return reinterpret_cast<uint32_t *>(smem_raw + st * ts_stage_bytes(HV) + TS_KEY_SLOTS * sizeof(double));
+        return reinterpret_cast<uint32_t *>(smem_raw + st * ts_stage_bytes(HV) + ts_key_bytes(HV));
     };
     const int tid = threadIdx.x;
     uint64_t policy = policy_evict_first();
@@ -1282,11 +1344,11 @@ merge_inplace_kernel(PipeGeo pg, int ntiles, const int *__restrict__ corank, con
     if (tid == 0) {
         const int a = (int)atomicAdd(ticket, 1u);
         if (a < ntiles) {
-            pipe_issue<HV>(pg, a, corank[a], a + 1 < ntiles ? corank[a + 1] : 0, skb(0), svb(0), &bars[0], &meta[0],
+            pipe_issue<HV>(pg, amap, bmap, a, corank[a], a + 1 < ntiles ? corank[a + 1] : 0, skb(0), svb(0), &bars[0], &meta[0],
                            policy);
             const int b = (int)atomicAdd(ticket, 1u);
             if (b < ntiles)
-                pipe_issue<HV>(pg, b, corank[b], b + 1 < ntiles ? corank[b + 1] : 0, skb(1), svb(1), &bars[1],
+                pipe_issue<HV>(pg, amap, bmap, b, corank[b], b + 1 < ntiles ? corank[b + 1] : 0, skb(1), svb(1), &bars[1],
                                &meta[1], policy);
             s_next = b;
         } else {
@@ -1308,11 +1370,13 @@ merge_inplace_kernel(PipeGeo pg, int ntiles, const int *__restrict__ corank, con
         const int d = min(tid * VT, cnt);
         double *sk = skb(st);
         const uint32_t *sv = svb(st);
+        const uint32_t kbase = smem_u32(sk);
+        stage_patch(kbase, mt, tid);
         double k[VT];
         uint32_t v[VT];
-        const int ii = merge_path_smem<ORD>(sk, mt.offa, mt.ca, mt.bslot, mt.cb, d, Lin());
-        serial_merge<HV, ORD>(sk, sv, mt.offa + ii, mt.offa + mt.ca, mt.bslot + d - ii, mt.bslot + mt.cb, k, v,
-                               Lin(), Lin());
+        const int ii = merge_path_stage<ORD>(kbase, mt.offa, mt.ca, mt.bslot, mt.cb, d);
+        serial_merge_stage<HV, ORD>(kbase, sv, mt, mt.offa + ii, mt.offa + mt.ca, mt.bslot + d - ii, mt.bslot + mt.cb, k,
+                                    v);
         const long long row = (long long)tcur * (MTILE / 16) + tid;
         __syncthreads();                                       // stage st fully read
         unsigned char *rowp = reinterpret_cast<unsigned char *>(sk) + tid * 128;
@@ -1350,7 +1414,7 @@ merge_inplace_kernel(PipeGeo pg, int ntiles, const int *__restrict__ corank, con
             if (tnext < ntiles) {
                 c = (int)atomicAdd(ticket, 1u);
                 if (c < ntiles)
-                    pipe_issue<HV>(pg, c, corank[c], c + 1 < ntiles ? corank[c + 1] : 0, skb(st), svb(st), &bars[st],
+                    pipe_issue<HV>(pg, amap, bmap, c, corank[c], c + 1 < ntiles ? corank[c + 1] : 0, skb(st), svb(st), &bars[st],
                                    &meta[st], policy);
             }
             s_next = c;

@@ -15,12 +15,13 @@ import synth  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--n", type=int, default=24)
+ap.add_argument("--ties", type=int, default=0, help="heavy ties: keys uniform integers in [0, T)")
 a = ap.parse_args()
 lib = gns._lib
 lib.gns_prof_read.argtypes = [ctypes.c_void_p]
 n = 1 << a.n
 T = gns.gns_tile_elems()
-src = torch.from_numpy(synth.uniform(n, 2000)).cuda()
+src = torch.from_numpy(synth.ties(n, 2000, a.ties) if a.ties else synth.uniform(n, 2000)).cuda()
 names = ["startup", "wait_load", "compute", "bar1", "staging+bar2", "store_read", "issue", "total", "split_spin"]
 cur = torch.empty_like(src)
 oth = torch.empty_like(src)
