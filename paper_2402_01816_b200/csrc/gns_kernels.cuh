@@ -1030,7 +1030,6 @@ __device__ __forceinline__ int swm(int e) { return e ^ ((e >> 5) & 15); }
 // row t) and stride-16 merge reads spread over the banks.  Working on byte
 // addresses saves the index->address shift in the merge steps.
 __device__ __forceinline__ uint32_t swa(uint32_t a) { return a ^ ((a >> 5) & 0x78u); }
-__device__ __forceinline__ int swmv(int e) { return e ^ ((e >> 5) & 31); }
 struct SwM { __device__ __forceinline__ int operator()(int e) const { return swm(e); } };
 // Stable co-rank over the tile-sort layout (keys at swa(base + 8e)); A wins ties.
 template <int ORD>
@@ -1046,7 +1045,6 @@ __device__ __forceinline__ int merge_path_tile(uint32_t base, int a0, int na, in
     }
     return lo;
 }
-struct SwMV { __device__ __forceinline__ int operator()(int e) const { return swmv(e); } };
 // TMA 128-byte swizzle layouts (16-byte chunk c of row r stored at chunk c ^ (r & 7))
 __device__ __forceinline__ int tk_slot(int e)     // doubles, 16 per row
 {
@@ -1104,7 +1102,9 @@ __device__ __forceinline__ void serial_merge32(const double *sk, const uint32_t 
         const bool p = (pb < pbe) && ((pa >= pae) || before<ORD>(kb, ka));
         k[x] = p ? kb : ka;
         const uint32_t src = p ? pb : pa;
-        if (HV) v[x] = sv[swmv((int)((src - base) >> 3))];
+        // vals sit at the keys' swizzled slot positions (4 bytes per slot):
+        // byte offset = (swizzled key byte offset) / 2
+        if (HV) v[x] = sv[(swa(src) - base) >> 3];
         const uint32_t nxt = src + 8u;
         GNS_DASSERT(nxt >= base && nxt <= base + 8u * TILE);
         const uint32_t a = swa(nxt);
@@ -1224,7 +1224,7 @@ tile_sort2_kernel(const double *src_k, const uint32_t *src_v, double *dst_k, uin
         for (int x = 0; x < VT1; ++x) {
             *reinterpret_cast<double *>(reinterpret_cast<unsigned char *>(sk) +
                                         (swa(smem_u32(sk) + 8u * (e0 + x)) - smem_u32(sk))) = k[x];
-            if (HV) sv[swmv(e0 + x)] = v[x];
+            if (HV) sv[(swa(smem_u32(sk) + 8u * (e0 + x)) - smem_u32(sk)) >> 3] = v[x];
         }
         __syncthreads();
         {
