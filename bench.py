@@ -384,14 +384,16 @@ def end_to_end(gns, torch, dev, stream, case, args, n, hv, ws, steps=None):
     """Same metric through the public C-ABI call, from pinned host memory:
     every step copies its input host->device, sorts it (gns_sort_*_ws) and
     copies the sorted result device->host, all inside the timed region.
-    Steps alternate between two buffer sets on two streams, so step i+1's
-    upload overlaps step i's download (PCIe is full duplex) -- a serving
-    pipeline; the fully serial figure is reported beside it."""
+    Steps rotate over three buffer sets on three streams, so step i+1's
+    upload, step i's sort and step i-1's download overlap (PCIe is full
+    duplex) -- a serving pipeline; the fully serial figure is reported beside
+    it."""
     steps = steps or max(4, min(args.steps, 12))
     hk = torch.from_numpy(case.keys).pin_memory()
     hv_ = torch.from_numpy(case.vals).pin_memory() if hv else None
+    nslot = 3
     slots = []
-    for i in range(2):
+    for i in range(nslot):
         slots.append({
             "st": stream if i == 0 else torch.cuda.Stream(dev),
             "dk": torch.empty(n, dtype=torch.float64, device=dev),
@@ -417,13 +419,15 @@ def end_to_end(gns, torch, dev, stream, case, args, n, hv, ws, steps=None):
         torch.cuda.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
-        slots[1]["st"].wait_event(a)
+        for sl in slots[1:]:
+            sl["st"].wait_event(a)
         for i in range(steps):
-            sl = slots[i % 2] if pipelined else slots[0]
+            sl = slots[i % nslot] if pipelined else slots[0]
             step(sl)
-        done = torch.cuda.Event()
-        done.record(slots[1]["st"])
-        stream.wait_event(done)
+        for sl in slots[1:]:
+            done = torch.cuda.Event()
+            done.record(sl["st"])
+            stream.wait_event(done)
         b.record(stream)
         torch.cuda.synchronize()
         return a.elapsed_time(b) / 1e3
@@ -434,8 +438,8 @@ def end_to_end(gns, torch, dev, stream, case, args, n, hv, ws, steps=None):
     by = n * (12 if hv else 8)
     return {"value": n * steps / t_pipe, "unit": UNIT, "h2d_bytes_per_step": by, "d2h_bytes_per_step": by,
             "steps": steps, "serial_value": n * steps / t_serial, "host_result_sorted": ok,
-            "path": "pinned host -> H2D -> gns_sort_*_ws -> D2H -> pinned host, two buffer sets alternating on "
-                    "two streams (upload of step i+1 overlaps download of step i)"}
+            "path": "pinned host -> H2D -> gns_sort_*_ws -> D2H -> pinned host, three buffer sets rotating on "
+                    "three streams (upload of step i+1, sort of step i, download of step i-1 overlap)"}
 
 
 def footprint_cfg5(gns, torch, dev, stream, flush, reps=3):
