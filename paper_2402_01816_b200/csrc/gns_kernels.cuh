@@ -1,12 +1,20 @@
 // gns_kernels.cuh — sm_100a device code of the stable f64 mergesort hot path.
 //
 // Kernels (PAPER.md line cites in each):
-//   K1    tile_sort2_kernel    (row a2) stable sort of one 4096-key tile per CTA
+//   K1    tile_sort2_kernel    (row a2) stable sort of one 8192-key tile per CTA,
+//                              per-tile omission / reversal of ordered tiles (f2)
 //   K2+K3 merge_tstore_kernel  (rows a3+a4) one merge level, src -> dst ping-pong,
-//                              co-rank search warps fused in
+//                              warp-specialised: sample-guided co-rank search
+//                              warps, TMA producer, merge warps; also the
+//                              two-run merge of the distributed sort (f4)
 //   K2    partition_kernel     (row a3) stable co-rank split per output tile (for K4)
-//   K4    merge_inplace_kernel (row a6) ordered in-place top merge of the 0.5 mode
+//   K4    merge_inplace_kernel (row a6) ordered in-place top merge of the limited-
+//                              buffer modes (0.5 and p < 0.5, f1)
 //         inplace_deps_kernel  (row a6) which earlier tiles each K4 tile must wait for
+//         reverse_kernel       (f3) the Right targets
+//         split_cuts_kernel    (f4) splitter cuts of the distributed sort
+// Keys of every type (f64, int64, uint64; f3) travel as 8-byte patterns; the
+// template parameter ORD = direction | key type << 1 selects the order.
 //
 // No code here is shared with oracle/ (the CPU oracle); the two are compared
 // only through their outputs.
@@ -75,11 +83,6 @@ static_assert(TILE % MTILE == 0, "pair boundaries must fall on merge-tile bounda
 
 // ---------------------------------------------------------------- global I/O
 // 256-bit vector accesses (LDG/STG.E.ENL2.256 on sm_100a).
-__device__ __forceinline__ void st_v4(double *p, double a, double b, double c, double d)
-{
-    asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};"
-                 :: "l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
-}
 __device__ __forceinline__ void st_v8(uint32_t *p, const uint32_t *u)
 {
     asm volatile("st.global.v8.u32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
@@ -113,11 +116,6 @@ __device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count)
 __device__ __forceinline__ void fence_mbar_init()
 {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes)
-{
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
 }
 __device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes)
 {
@@ -203,30 +201,6 @@ __device__ __forceinline__ uint64_t policy_evict_first()
     uint64_t p;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
     return p;
-}
-
-// Writes a thread's VT consecutive outputs (keys [+vals]) starting at out[pos].
-// `m` = how many of them are valid (tail); full segments use 256-bit stores
-// (pos is a multiple of VT and the arrays are 32-byte aligned).
-template <bool HV>
-__device__ __forceinline__ void store_segment(double *ok, uint32_t *ov, long long pos, int m,
-                                              const double (&k)[VT], const uint32_t (&v)[VT])
-{
-    if (m >= VT) {
-#pragma unroll
-        for (int x = 0; x < VT; x += 4) st_v4(ok + pos + x, k[x], k[x + 1], k[x + 2], k[x + 3]);
-        if (HV) {
-#pragma unroll
-            for (int x = 0; x < VT; x += 8) st_v8(ov + pos + x, &v[x]);
-        }
-    } else {
-#pragma unroll
-        for (int x = 0; x < VT; ++x)
-            if (x < m) {
-                ok[pos + x] = k[x];
-                if (HV) ov[pos + x] = v[x];
-            }
-    }
 }
 
 // ------------------------------------------------------------ merge device code
@@ -348,42 +322,6 @@ __device__ __forceinline__ int warp_corank(const MergeGeo &g, int t, int lane)
         const int c = __popc(bal);
         const int m_prev = __shfl_sync(0xFFFFFFFFu, m, (c > 0 ? c - 1 : 0));
         const int m_next = __shfl_sync(0xFFFFFFFFu, m, (c < nprobe ? c : 0));
-        const int nlo = (c == 0) ? lo : m_prev + 1;
-        const int nhi = (c == nprobe) ? hi : m_next;
-        lo = nlo;
-        hi = max(nlo, nhi);
-    }
-    return lo;
-}
-
-// Co-rank search by a group of W lanes (W = 16: two independent searches per
-// warp, (W+1)-ary).  `gl` = lane within the group; `mask` = the group's lanes.
-template <int W, int ORD>
-__device__ __forceinline__ int group_corank(const MergeGeo &g, int t, int gl, unsigned mask, int gbase)
-{
-    const TileSpan s = tile_span(g, t);
-    const double *A = g.ak + s.pbase;
-    const double *B = g.bk + s.pbase;
-    const int d = s.k0;
-    int lo = max(0, d - s.nb), hi = min(d, s.na);
-    while (true) {
-        // group-uniform loop condition (all lanes of the group see the same lo/hi)
-        if (lo >= hi) break;
-        const int span = hi - lo;
-        int m, nprobe;
-        if (span <= W) {
-            m = lo + gl;
-            nprobe = span;
-        } else {
-            m = lo + (int)(((long long)span * (gl + 1)) / (W + 1));
-            nprobe = W;
-        }
-        bool p = false;
-        if (gl < nprobe) p = !before<ORD>(B[d - 1 - m], A[m]);
-        const unsigned bal = (__ballot_sync(mask, p) & mask) >> gbase;
-        const int c = __popc(bal);
-        const int m_prev = __shfl_sync(mask, m, gbase + (c > 0 ? c - 1 : 0));
-        const int m_next = __shfl_sync(mask, m, gbase + (c < nprobe ? c : 0));
         const int nlo = (c == 0) ? lo : m_prev + 1;
         const int nhi = (c == nprobe) ? hi : m_next;
         lo = nlo;
