@@ -531,3 +531,36 @@ def test_distributed_sort_single_rank_nccl(gns):
         assert_bitexact(gk.cpu().numpy(), ek, gv.cpu().numpy(), ev)
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("n,frac", [((1 << 31) - 1, 1.0), ((1 << 30) + 12345, 0.5)])
+def test_max_size_properties(gns, n, frac):
+    """GNS_MAX_N-scale sorts (int32 tile/row/co-rank arithmetic at its limit),
+    checked by properties that together fix the stable sort uniquely
+    (SURVEY.md §8(c) I1-I3 plus the payload gather): output non-decreasing,
+    payload a permutation of 0..n-1 (the original indices), every output key
+    bit-identical to the input key its payload names, and equal keys in
+    ascending payload order.  Seeded device-side inputs with ties."""
+    free, _ = torch.cuda.mem_get_info()
+    need = n * (8 + 4) * 3 + n * 8
+    if free < need:
+        pytest.skip(f"needs {need / 2**30:.0f} GiB of device memory")
+    g = torch.Generator(device="cuda")
+    g.manual_seed(n)
+    keys = torch.randint(0, 1 << 20, (n,), device="cuda", generator=g).to(torch.float64)   # heavy ties
+    keys[::3] = torch.rand(keys[::3].shape, device="cuda", generator=g, dtype=torch.float64)
+    src = keys.clone()
+    vals = torch.arange(n, device="cuda", dtype=torch.int64).to(torch.uint32)
+    ws = gns.alloc_workspace(n, frac, True)
+    gns.sort_(keys, vals, frac, workspace=ws)
+    torch.cuda.synchronize()
+    del ws
+    assert bool((keys[1:] >= keys[:-1]).all())
+    idx = vals.to(torch.int64)
+    assert bool((src.view(torch.int64)[idx] == keys.view(torch.int64)).all())      # gather: bit-exact keys
+    seen = torch.zeros(n, dtype=torch.uint8, device="cuda")
+    seen[idx] = 1
+    assert int(seen.sum()) == n                                                       # a permutation
+    tie = keys[1:] == keys[:-1]
+    assert bool((idx[1:][tie] > idx[:-1][tie]).all())                                 # stable ties
