@@ -213,7 +213,7 @@ gns_status gns_merge_inplace_top(double *keys, uint32_t *vals, const double *lef
  * gns_timing_end(ms, kind, cap): waits for the last event, writes up to cap
  * per-launch durations (milliseconds) and kinds (1 tile sort, 2 merge pass,
  * 3 co-rank partition, 4 in-place dependency ranges, 5 in-place merge,
- * 6 reversal, 7 splitter cuts, 0 other) in launch order, turns timing off and returns the number
+ * 6 reversal, 7 splitter cuts, 8 sample gather, 0 other) in launch order, turns timing off and returns the number
  * of timed launches (-1 if timing was off or an event failed). */
 gns_status gns_timing_begin(int max_launches);
 int gns_timing_end(float *ms, int *kind, int cap);

@@ -260,8 +260,8 @@ int launch_kind(const char *what)
 {
     static const char *names[] = {"tile_sort2_kernel", "merge_tstore_kernel", "partition_kernel",
                                   "inplace_deps_kernel", "merge_inplace_kernel", "reverse_kernel",
-                                  "split_cuts_kernel"};
-    for (int i = 0; i < 7; ++i)
+                                  "split_cuts_kernel", "gather_samples_kernel"};
+    for (int i = 0; i < 8; ++i)
         if (std::strcmp(what, names[i]) == 0) return i + 1;
     return 0;
 }
@@ -376,6 +376,7 @@ MergeGeo uniform_geo(const double *sk, const uint32_t *sv, double *dk, uint32_t 
     g.tpp_log2 = (g.tpp & (g.tpp - 1)) ? -1 : __builtin_ctz((unsigned)g.tpp);
     g.sa = (L % SMP_G == 0) ? sa : nullptr;
     g.so = so;
+    g.sb = nullptr;
     return g;
 }
 
@@ -473,8 +474,11 @@ gns_status validate_data(const double *keys, const uint32_t *vals, bool hv, size
 
 // Ordered in-place merge of A = buffer[0:nl) and B = data[lo+nl : lo+len)
 // into data[lo : lo+len) (row a6, K2 + deps + K4).
+// s0, s1: two sample arrays (>= n/SMP_G + 2 keys each; free at this point),
+// or nullptr: the partition then searches without samples.
 gns_status top_merge(double *keys, uint32_t *vals, double *bk, uint32_t *bv, size_t lo, size_t len, size_t nl,
-                     int *corank, int2 *deps, unsigned *flags, int ord, cudaStream_t st)
+                     int *corank, int2 *deps, unsigned *flags, int ord, cudaStream_t st, double *s0 = nullptr,
+                     double *s1 = nullptr)
 {
     const bool hv = vals != nullptr;
     MergeGeo g;
@@ -491,6 +495,17 @@ gns_status top_merge(double *keys, uint32_t *vals, double *bk, uint32_t *bv, siz
     g.tpp_log2 = 0;
     g.sa = nullptr;
     g.so = nullptr;
+    g.sb = nullptr;
+    if (s0 && s1 && nl % SMP_G == 0) {
+        // every SMP_G-th key of both runs -> sample-guided partition
+        const long long nb = (long long)(len - nl);
+        const size_t cnt = ceil_div(nl, SMP_G) + ceil_div((size_t)nb, SMP_G);
+        GNS_TRY(launch_pdl("gather_samples_kernel", gather_samples_kernel,
+                           (unsigned)std::max<size_t>(1, std::min<size_t>(ceil_div(cnt, 256), 1024)), 256, 0, st,
+                           (const double *)bk, (long long)nl, s0, (const double *)g.bk, nb, s1));
+        g.sa = s0;
+        g.sb = s1;
+    }
     return launch_merge(g, bk + nl, keys + lo + len, corank, deps, flags, true, ord, st);
 }
 
@@ -535,22 +550,22 @@ gns_status sort_limited(double *keys, uint32_t *vals, size_t lo, size_t len, siz
             count_sort_range(nl, sc, n);
             count_sort_range(nr, sc, n);
             sc->elem_passes += (double)len / (double)n;
-            sc->launches += 3;
+            sc->launches += 3 + (nl % SMP_G == 0 ? 1 : 0);   // (+ sample gather)
             return GNS_OK;
         }
         GNS_TRY(sort_range(dk, dv, bk, bv, nl, true, corank, ord, st, nullptr, s0, s1));
         GNS_TRY(sort_range(dk + nl, hv ? dv + nl : nullptr, dk, dv, nr, false, corank, ord, st, nullptr, s0, s1));
-        return top_merge(keys, vals, bk, bv, lo, len, nl, corank, deps, flags, ord, st);
+        return top_merge(keys, vals, bk, bv, lo, len, nl, corank, deps, flags, ord, st, s0, s1);
     }
     GNS_TRY(sort_limited(keys, vals, lo + b, len - b, b, bk, bv, corank, deps, flags, ord, st, sc, n, s0, s1));
     if (sc) {
         count_sort_range(b, sc, n);
         sc->elem_passes += (double)len / (double)n;
-        sc->launches += 3;
+        sc->launches += 3 + (b % SMP_G == 0 ? 1 : 0);
         return GNS_OK;
     }
     GNS_TRY(sort_range(dk, dv, bk, bv, b, true, corank, ord, st, nullptr, s0, s1));
-    return top_merge(keys, vals, bk, bv, lo, len, b, corank, deps, flags, ord, st);
+    return top_merge(keys, vals, bk, bv, lo, len, b, corank, deps, flags, ord, st, s0, s1);
 }
 
 // The sort proper (rows a1..a7).  ws already validated and sized.
@@ -783,6 +798,7 @@ gns_status gns_merge_two(const void *a_keys, const uint32_t *a_vals, size_t la, 
     g.tpp_log2 = 0;
     g.sa = nullptr;
     g.so = nullptr;
+    g.sb = nullptr;
     const int ntiles = (int)ceil_div(n, MTILE);
     PipeGeo pg;
     pg.g = g;
@@ -848,6 +864,7 @@ gns_status gns_merge_inplace_top(double *keys, uint32_t *vals, const double *lef
     g.tpp_log2 = 0;
     g.sa = nullptr;
     g.so = nullptr;
+    g.sb = nullptr;
     return launch_merge(g, left_keys + nl, keys + n, corank, deps, flags, true, 0, (cudaStream_t)stream);
 }
 

@@ -262,6 +262,7 @@ struct MergeGeo {
     int tpp_log2;   // log2(tpp) if tpp is a power of two, else -1
     const double *sa;   // samples of the source region (key at every SMP_G-th position), or nullptr
     double *so;         // samples of the output region written by this pass, or nullptr
+    const double *sb;   // single (two-run) geometry: samples of B (every SMP_G-th key of bk), or nullptr
 };
 
 struct TileSpan {
@@ -386,12 +387,12 @@ __device__ __forceinline__ int tile_corank(const MergeGeo &g, int t, int gl, uns
     const int d = s.k0;
     int lo = max(0, d - s.nb), hi = min(d, s.na);
     if (lo >= hi) return lo;
-    if (g.sa != nullptr) {
+    if (g.sa != nullptr && (!g.single || g.sb != nullptr)) {
         const int s_lo = (lo + SMP_G - 1) >> SMP_LOG2;
         const int s_hi = (hi - 1) >> SMP_LOG2;
         if (s_lo <= s_hi) {
             const double *SA = g.sa + (s.pbase >> SMP_LOG2);
-            const double *SB = g.sa + ((s.pbase + g.L) >> SMP_LOG2);
+            const double *SB = g.single ? g.sb : g.sa + ((s.pbase + g.L) >> SMP_LOG2);
             const int cnt = group_count_true<W>(s_lo, s_hi, gl, mask, gbase, [&](int sx) {
                 const int yb = (d - 1 - (sx << SMP_LOG2)) >> SMP_LOG2;
                 return !before<ORD>(SB[yb], SA[sx]);
@@ -414,8 +415,22 @@ partition_kernel(MergeGeo g, int ntiles, int *__restrict__ corank)
     const int warp = (int)((blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5);
     const int lane = threadIdx.x & 31;
     if (warp >= ntiles) return;
-    const int c = warp_corank<ORD>(g, warp, lane);
+    const int c = tile_corank<32, ORD>(g, warp, lane, 0xFFFFFFFFu, 0);   // sample-guided if g has samples
     if (lane == 0) corank[warp] = c;
+}
+
+// Samples of the two runs of an in-place top merge (every SMP_G-th key of
+// each), so its partition can run the sample-guided split search.
+__global__ void __launch_bounds__(256)
+gather_samples_kernel(const double *a, long long na, double *sa, const double *b, long long nb, double *sb)
+{
+    pdl_wait();
+    pdl_trigger();
+    const long long ca = (na + SMP_G - 1) >> SMP_LOG2, cb = (nb + SMP_G - 1) >> SMP_LOG2;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < ca + cb; i += (long long)gridDim.x * blockDim.x) {
+        if (i < ca) sa[i] = a[i << SMP_LOG2];
+        else sb[i - ca] = b[(i - ca) << SMP_LOG2];
+    }
 }
 
 // ---------------------------------------------- K4 dependency ranges (row a6)
