@@ -346,7 +346,7 @@ gns_status launch_merge(const MergeGeo &g, const double *lim_a, const double *li
     unsigned *ticket = flags + ntiles;
     const int grid = std::min(ntiles, 2 * num_sms());
     auto kern = inplace_kern(hv, ord);
-    return launch_pdl("merge_inplace_kernel", kern, grid, NT, ts_smem(hv), st, pg, ntiles, (const int *)corank,
+    return launch_pdl("merge_inplace_kernel", kern, grid, NT + 32, ts_smem(hv), st, pg, ntiles, (const int *)corank,
                       (const int2 *)deps, flags, ticket, map, amap, bmap);
 }
 

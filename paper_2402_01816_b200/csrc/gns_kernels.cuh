@@ -1270,7 +1270,7 @@ tile_sort2_kernel(const double *src_k, const uint32_t *src_v, double *dst_k, uin
 // never intersect: k1(t) <= nl + j1(t) <= nl + j0(u) for u > t.  Deadlock-free:
 // the smallest tile in flight only depends on tiles whose loads have landed.
 template <bool HV, int ORD>
-__global__ void __launch_bounds__(NT, 2)
+__global__ void __launch_bounds__(NT + 32, 2)
 merge_inplace_kernel(PipeGeo pg, int ntiles, const int *__restrict__ corank, const int2 *__restrict__ deps,
                      unsigned *flags, unsigned *ticket, const __grid_constant__ CUtensorMap omap,
                      const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap bmap)
@@ -1278,47 +1278,76 @@ merge_inplace_kernel(PipeGeo pg, int ntiles, const int *__restrict__ corank, con
     pdl_wait();
     extern __shared__ __align__(16) unsigned char smem_raw0[];
     unsigned char *smem_raw = smem_raw0 + ((1024u - (smem_u32(smem_raw0) & 1023u)) & 1023u);
-    __shared__ __align__(8) uint64_t bars[2];
+    __shared__ __align__(8) uint64_t full[2];
+    __shared__ __align__(8) uint64_t staged[2];
     __shared__ PipeMeta meta[2];
-    __shared__ int s_next;
     auto skb = [&](int st) { return reinterpret_cast<double *>(smem_raw + st * ts_stage_bytes(HV)); };
     auto svb = [&](int st) {
         return reinterpret_cast<uint32_t *>(smem_raw + st * ts_stage_bytes(HV) + ts_key_bytes(HV));
     };
     const int tid = threadIdx.x;
-    uint64_t policy = policy_evict_first();
+    const int warp = tid >> 5, lane = tid & 31;
     if (tid == 0) {
-        mbar_init(&bars[0], 1);
-        mbar_init(&bars[1], 1);
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&full[b], 1);
+            mbar_init(&staged[b], MERGE_WARPS);
+        }
         fence_mbar_init();
     }
-    // claim the first two tiles
-    int tcur = -1, tnext = -1;
-    if (tid == 0) {
-        const int a = (int)atomicAdd(ticket, 1u);
-        if (a < ntiles) {
-            pipe_issue<HV>(pg, amap, bmap, a, corank[a], a + 1 < ntiles ? corank[a + 1] : 0, skb(0), svb(0), &bars[0], &meta[0],
-                           policy);
-            const int b = (int)atomicAdd(ticket, 1u);
-            if (b < ntiles)
-                pipe_issue<HV>(pg, amap, bmap, b, corank[b], b + 1 < ntiles ? corank[b + 1] : 0, skb(1), svb(1), &bars[1],
-                               &meta[1], policy);
-            s_next = b;
-        } else {
-            s_next = ntiles;
-        }
-        meta[0].t = a;   // (a >= ntiles: nothing to do)
-    }
     __syncthreads();
-    tcur = meta[0].t;
-    tnext = s_next;
+
+    if (warp == PRODUCER_WARP) {
+        // ---------------------------------------- producer (lane 0): tickets, loads, stores
+        if (lane != 0) return;
+        const uint64_t policy = policy_evict_first();
+        // claim a tile in ticket order and load it into stage st, or tell the
+        // merge warps there is none left (meta.t = ntiles, arrival without bytes)
+        auto claim = [&](int st) -> bool {
+            const int c = (int)atomicAdd(ticket, 1u);
+            if (c < ntiles) {
+                pipe_issue<HV>(pg, amap, bmap, c, corank[c], c + 1 < ntiles ? corank[c + 1] : 0, skb(st), svb(st),
+                               &full[st], &meta[st], policy);
+                return true;
+            }
+            meta[st].t = ntiles;
+            mbar_arrive(&full[st]);
+            return false;
+        };
+        bool more = claim(0) && claim(1);
+        for (int i = 0;; ++i) {
+            const int st = i & 1;
+            mbar_wait(&staged[st], (uint32_t)((i >> 1) & 1));    // merged, deps waited, staged
+            const int t = meta[st].t;
+            if (t >= ntiles) break;
+            fence_proxy_async_global();
+            tma_store_2d(&omap, skb(st), 0, t * (MTILE / 16));
+            bulk_commit();
+            bulk_wait_read0();                                    // stage st read out -> reusable
+            if (more) more = claim(st);
+            else {                                                // no tile for this stage: end marker
+                meta[st].t = ntiles;
+                mbar_arrive(&full[st]);
+            }
+        }
+        bulk_wait0();
+        pdl_trigger();
+        return;
+    }
+
+    // -------------------------------------------------------- merge warps 0-7
     const long long n = pg.g.n;
     const long long full_rows = n >> 4;
-    for (int i = 0; tcur < ntiles; ++i) {
+    for (int i = 0;; ++i) {
         const int st = i & 1;
-        mbar_wait(&bars[st], (uint32_t)((i >> 1) & 1));
-        if (tid == 0) st_release(flags + tcur, 1u);           // inputs of tile tcur are in shared memory
+        mbar_wait(&full[st], (uint32_t)((i >> 1) & 1));
         const PipeMeta mt = meta[st];
+        const int t = mt.t;
+        if (t >= ntiles) {                                      // end: let the producer see it too
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&staged[st]);
+            break;
+        }
+        if (tid == 0) st_release(flags + t, 1u);               // inputs of tile t are in shared memory
         const int cnt = mt.ca + mt.cb;
         const int d = min(tid * VT, cnt);
         double *sk = skb(st);
@@ -1330,17 +1359,18 @@ merge_inplace_kernel(PipeGeo pg, int ntiles, const int *__restrict__ corank, con
         const int ii = merge_path_stage<ORD>(kbase, mt.offa, mt.ca, mt.bslot, mt.cb, d);
         serial_merge_stage<HV, ORD>(kbase, sv, mt, mt.offa + ii, mt.offa + mt.ca, mt.bslot + d - ii, mt.bslot + mt.cb, k,
                                     v);
-        const long long row = (long long)tcur * (MTILE / 16) + tid;
-        __syncthreads();                                       // stage st fully read
+        const long long row = (long long)t * (MTILE / 16) + tid;
+        bar_merge_warps();                                     // stage st fully read
         unsigned char *rowp = reinterpret_cast<unsigned char *>(sk) + tid * 128;
 #pragma unroll
         for (int c = 0; c < 8; ++c) sts128(rowp + ((c ^ (tid & 7)) << 4), k[2 * c], k[2 * c + 1]);
         fence_proxy_async();
         // wait until every earlier tile that reads B slots we overwrite has loaded
-        const int2 dp = deps[tcur];
-        GNS_DASSERT(dp.x >= 0 && dp.y < tcur);
+        const int2 dp = deps[t];
+        GNS_DASSERT(dp.x >= 0 && dp.y < t);
         for (int u = dp.x + tid; u <= dp.y; u += NT)
             while (ld_acquire(flags + u) == 0u) { __nanosleep(32); }
+        bar_merge_warps();                                     // every dependency seen by some merge thread
         fence_proxy_async_global();
         if (HV) {
             const int mv = cnt - d;
@@ -1358,25 +1388,9 @@ merge_inplace_kernel(PipeGeo pg, int ntiles, const int *__restrict__ corank, con
             for (int x = 0; x < VT; ++x)
                 if (x < cnt - d) pg.g.ok[row * 16 + x] = k[x];
         }
-        __syncthreads();
-        if (tid == 0) {
-            tma_store_2d(&omap, sk, 0, tcur * (MTILE / 16));
-            bulk_commit();
-            bulk_wait_read0();
-            int c = ntiles;
-            if (tnext < ntiles) {
-                c = (int)atomicAdd(ticket, 1u);
-                if (c < ntiles)
-                    pipe_issue<HV>(pg, amap, bmap, c, corank[c], c + 1 < ntiles ? corank[c + 1] : 0, skb(st), svb(st), &bars[st],
-                                   &meta[st], policy);
-            }
-            s_next = c;
-        }
-        __syncthreads();
-        tcur = tnext;
-        tnext = s_next;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&staged[st]);
     }
-    if (tid == 0) bulk_wait0();
     pdl_trigger();
 }
 
