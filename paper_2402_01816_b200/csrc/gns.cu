@@ -266,6 +266,18 @@ int launch_kind(const char *what)
     return 0;
 }
 
+// Which kernel runs a uniform merge pass: the fused one (search warps) or
+// partition + ticket-scheduled merge.  GNS_MERGE_MODE=0/1 forces one (A/B).
+bool ticket_pass(bool hv, int ntiles)
+{
+    static const int forced = [] {
+        const char *e = std::getenv("GNS_MERGE_MODE");
+        return e ? std::atoi(e) : -1;
+    }();
+    if (forced == 0 || forced == 1) return forced == 1;
+    return hv && ntiles >= 8192;         // with payload, >= 2^25 elements
+}
+
 template <typename... KArgs, typename... Args>
 gns_status launch_pdl(const char *what, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
                       cudaStream_t st, Args... args)
@@ -331,6 +343,21 @@ gns_status launch_merge(const MergeGeo &g, const double *lim_a, const double *li
     // (B may start past the array end when the last pair has no B run: empty map, never loaded)
     GNS_TRY(key_map(g.ak, (size_t)std::max<long long>(0, lim_a - g.ak), hv, &amap, &pg.a_idx0, &pg.a_rows));
     GNS_TRY(key_map(g.bk, (size_t)std::max<long long>(0, lim_b - g.bk), hv, &bmap, &pg.b_idx0, &pg.b_rows));
+    if (!inplace && ticket_pass(hv, ntiles)) {
+        // Large passes with payload: a partition kernel (sample-guided splits
+        // of every tile) + the ticket-scheduled merge (K4's kernel without
+        // dependencies) beat the fused search warps (2^27 pairs: 10.3 vs
+        // 10.9 ms per sort); smaller or key-only passes keep the fused kernel.
+        unsigned *ticket = reinterpret_cast<unsigned *>(corank + ntiles);
+        GNS_TRY(check(cudaMemsetAsync(ticket, 0, sizeof(unsigned), st), "memset"));
+        GNS_TRY(launch_pdl("partition_kernel", partition_kern(ord),
+                           (unsigned)ceil_div((size_t)ntiles * 32, 256), 256, 0, st, g, ntiles, corank));
+        const int grid = std::min(ntiles, 2 * num_sms());
+        auto kern = inplace_kern(hv, ord);
+        return launch_pdl("merge_inplace_kernel", kern, grid, NT + 32, ts_smem(hv), st, pg, ntiles,
+                          (const int *)corank, (const int2 *)nullptr, (unsigned *)nullptr, ticket, map, amap, bmap,
+                          ad);
+    }
     if (!inplace) {
         const int ctas = std::min(ntiles, 2 * num_sms());
         const int per = (int)ceil_div(ntiles, ctas);
@@ -347,7 +374,7 @@ gns_status launch_merge(const MergeGeo &g, const double *lim_a, const double *li
     const int grid = std::min(ntiles, 2 * num_sms());
     auto kern = inplace_kern(hv, ord);
     return launch_pdl("merge_inplace_kernel", kern, grid, NT + 32, ts_smem(hv), st, pg, ntiles, (const int *)corank,
-                      (const int2 *)deps, flags, ticket, map, amap, bmap);
+                      (const int2 *)deps, flags, ticket, map, amap, bmap, Adapt{});
 }
 
 gns_status launch_reverse(double *k, uint32_t *v, size_t n, cudaStream_t st)
@@ -513,6 +540,7 @@ gns_status top_merge(double *keys, uint32_t *vals, double *bk, uint32_t *bv, siz
 struct Sched {
     double elem_passes = 0;     // sum over steps of (HBM passes of the step x elements) / n
     int launches = 0;
+    bool hv = false;
 };
 
 void count_sort_range(size_t len, Sched *sc, size_t n)
@@ -520,7 +548,8 @@ void count_sort_range(size_t len, Sched *sc, size_t n)
     if (!len) return;
     const int M = merge_passes_for(len);
     sc->elem_passes += (double)(1 + M) * (double)len / (double)n;
-    sc->launches += 1 + M;
+    // tile sort + per pass one fused launch, or partition + ticket merge
+    sc->launches += 1 + M * (ticket_pass(sc->hv, (int)ceil_div(len, MTILE)) ? 2 : 1);
 }
 
 // Limited-buffer sort of data[lo : lo+len) with a buffer of b elements
@@ -711,6 +740,7 @@ gns_status gns_plan(size_t n, double buffer_fraction, int with_vals, gns_plan_in
     out->merge_tile = MTILE;
     out->merge_passes = merge_passes_for(n);
     Sched sc;
+    sc.hv = with_vals != 0;
     if (n <= 1) {
         sc.elem_passes = 0;
     } else if (n <= (size_t)TILE || !m.limited) {

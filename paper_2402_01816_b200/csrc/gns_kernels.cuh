@@ -1273,9 +1273,22 @@ template <bool HV, int ORD>
 __global__ void __launch_bounds__(NT + 32, 2)
 merge_inplace_kernel(PipeGeo pg, int ntiles, const int *__restrict__ corank, const int2 *__restrict__ deps,
                      unsigned *flags, unsigned *ticket, const __grid_constant__ CUtensorMap omap,
-                     const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap bmap)
+                     const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap bmap, Adapt ad)
 {
     pdl_wait();
+    if (ad.flag) {
+        // NEXT f2 (as in merge_tstore_kernel): ordered or strictly reversed input
+        const unsigned f = *(volatile const unsigned *)ad.flag;
+        if ((f & 1u) == 0u || (f & 2u) == 0u) {
+            const bool pre = (f & 1u) == 0u;
+            const double *ck = pre ? ad.pre_k : ad.rev_k;
+            const uint32_t *cv = pre ? ad.pre_v : ad.rev_v;
+            const int per = (ntiles + gridDim.x - 1) / gridDim.x;
+            if (ck) adapt_move<HV>(pg.g, per, ck, cv, !pre && ad.rev_gather);
+            pdl_trigger();
+            return;
+        }
+    }
     extern __shared__ __align__(16) unsigned char smem_raw0[];
     unsigned char *smem_raw = smem_raw0 + ((1024u - (smem_u32(smem_raw0) & 1023u)) & 1023u);
     __shared__ __align__(8) uint64_t full[2];
@@ -1347,7 +1360,7 @@ merge_inplace_kernel(PipeGeo pg, int ntiles, const int *__restrict__ corank, con
             if (lane == 0) mbar_arrive(&staged[st]);
             break;
         }
-        if (tid == 0) st_release(flags + t, 1u);               // inputs of tile t are in shared memory
+        if (tid == 0 && flags) st_release(flags + t, 1u);      // inputs of tile t are in shared memory
         const int cnt = mt.ca + mt.cb;
         const int d = min(tid * VT, cnt);
         double *sk = skb(st);
@@ -1360,18 +1373,22 @@ merge_inplace_kernel(PipeGeo pg, int ntiles, const int *__restrict__ corank, con
         serial_merge_stage<HV, ORD>(kbase, sv, mt, mt.offa + ii, mt.offa + mt.ca, mt.bslot + d - ii, mt.bslot + mt.cb, k,
                                     v);
         const long long row = (long long)t * (MTILE / 16) + tid;
+        if (pg.g.so != nullptr && (tid & (SMP_G / VT - 1)) == 0 && d < cnt)
+            pg.g.so[(row * 16) >> SMP_LOG2] = k[0];             // sample of output position row*16
         bar_merge_warps();                                     // stage st fully read
         unsigned char *rowp = reinterpret_cast<unsigned char *>(sk) + tid * 128;
 #pragma unroll
         for (int c = 0; c < 8; ++c) sts128(rowp + ((c ^ (tid & 7)) << 4), k[2 * c], k[2 * c + 1]);
         fence_proxy_async();
-        // wait until every earlier tile that reads B slots we overwrite has loaded
-        const int2 dp = deps[t];
-        GNS_DASSERT(dp.x >= 0 && dp.y < t);
-        for (int u = dp.x + tid; u <= dp.y; u += NT)
-            while (ld_acquire(flags + u) == 0u) { __nanosleep(32); }
-        bar_merge_warps();                                     // every dependency seen by some merge thread
-        fence_proxy_async_global();
+        if (deps) {
+            // wait until every earlier tile that reads B slots we overwrite has loaded
+            const int2 dp = deps[t];
+            GNS_DASSERT(dp.x >= 0 && dp.y < t);
+            for (int u = dp.x + tid; u <= dp.y; u += NT)
+                while (ld_acquire(flags + u) == 0u) { __nanosleep(32); }
+            bar_merge_warps();                                 // every dependency seen by some merge thread
+            fence_proxy_async_global();
+        }
         if (HV) {
             const int mv = cnt - d;
             if (mv >= VT) {

@@ -564,3 +564,34 @@ def test_max_size_properties(gns, n, frac):
     assert int(seen.sum()) == n                                                       # a permutation
     tie = keys[1:] == keys[:-1]
     assert bool((idx[1:][tie] > idx[:-1][tie]).all())                                 # stable ties
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("pattern", ["uniform", "ties", "ascending", "reversed", "runs"])
+def test_ticket_merge_passes_large_pairs(gns, pattern):
+    """Passes of >= 8192 tiles with payload run as partition + ticket-scheduled
+    merge (gns.cu ticket_pass): 2^25 + ragged pairs, several patterns
+    (including the f2 ordered / reversed fast paths through that kernel), both
+    buffer modes and a descending target, vs the oracle."""
+    n = (1 << 25) + 777
+    if pattern == "uniform":
+        k = synth.uniform(n, 31)
+    elif pattern == "ties":
+        k = synth.ties(n, 32, 24)
+    elif pattern == "ascending":
+        k = np.arange(n, dtype=np.float64)
+    elif pattern == "reversed":
+        k = np.arange(n, 0, -1, dtype=np.float64)
+    else:
+        k = synth.runs(n, 33)
+    v = synth.iota_u32(n)
+    ek, ev = oracle.sort(k, v)
+    for frac in (1.0, 0.5):
+        gk, gv = gpu_sort(gns, k, v, frac, use_ws=True)
+        assert_bitexact(gk, ek, gv, ev, what=f"{pattern} frac={frac}")
+    if pattern in ("uniform", "ties"):
+        tk, tv = to_dev(k, v)
+        gns.sort_(tk, tv, 1.0, target="DescLeft")
+        torch.cuda.synchronize()
+        dk, dv = oracle.sort_target(k, v, "DescLeft")
+        assert_bitexact(tk.cpu().numpy(), dk, tv.cpu().numpy(), dv, what=f"{pattern} DescLeft")
