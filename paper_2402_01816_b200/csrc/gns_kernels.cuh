@@ -678,7 +678,10 @@ __device__ __forceinline__ void serial_merge_stage(uint32_t kbase, const uint32_
 
 
 // ------------------------------- shared pieces of the fused merge kernels
-constexpr int SEARCH_WARPS = 2;
+#ifndef GNS_SEARCH_WARPS
+#define GNS_SEARCH_WARPS 2
+#endif
+constexpr int SEARCH_WARPS = GNS_SEARCH_WARPS;
 constexpr int SPL_RING = 64;
 
 __device__ __forceinline__ void bar_merge_warps() { asm volatile("bar.sync 1, %0;" :: "n"(NT) : "memory"); }

@@ -595,3 +595,18 @@ def test_ticket_merge_passes_large_pairs(gns, pattern):
         torch.cuda.synchronize()
         dk, dv = oracle.sort_target(k, v, "DescLeft")
         assert_bitexact(tk.cpu().numpy(), dk, tv.cpu().numpy(), dv, what=f"{pattern} DescLeft")
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("key_type,target", [("u64", "AscLeft"), ("i64", "DescRight")])
+def test_ticket_merge_passes_int_keys(gns, key_type, target):
+    """The partition + ticket-merge passes (>= 8192 tiles with payload) with
+    64-bit integer keys and a Right target, vs the oracle."""
+    n = (1 << 25) + 33
+    k = _int_keys(key_type, n, 77)
+    v = synth.iota_u32(n)
+    ek, ev = oracle.sort_keys(k, v, key_type, target)
+    tk, tv = to_dev(k, v)
+    gns.sort_(tk, tv, 1.0, target=target)
+    torch.cuda.synchronize()
+    assert np.array_equal(tk.cpu().numpy(), ek) and np.array_equal(tv.cpu().numpy(), ev)
