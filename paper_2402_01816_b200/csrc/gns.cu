@@ -275,7 +275,7 @@ bool ticket_pass(bool hv, int ntiles)
         return e ? std::atoi(e) : -1;
     }();
     if (forced == 0 || forced == 1) return forced == 1;
-    return hv && ntiles >= 8192;         // with payload, >= 2^25 elements
+    return ntiles >= (hv ? 8192 : 32768);   // >= 2^25 elements with payload, >= 2^27 key-only (measured)
 }
 
 template <typename... KArgs, typename... Args>
@@ -344,10 +344,12 @@ gns_status launch_merge(const MergeGeo &g, const double *lim_a, const double *li
     GNS_TRY(key_map(g.ak, (size_t)std::max<long long>(0, lim_a - g.ak), hv, &amap, &pg.a_idx0, &pg.a_rows));
     GNS_TRY(key_map(g.bk, (size_t)std::max<long long>(0, lim_b - g.bk), hv, &bmap, &pg.b_idx0, &pg.b_rows));
     if (!inplace && ticket_pass(hv, ntiles)) {
-        // Large passes with payload: a partition kernel (sample-guided splits
-        // of every tile) + the ticket-scheduled merge (K4's kernel without
-        // dependencies) beat the fused search warps (2^27 pairs: 10.3 vs
-        // 10.9 ms per sort); smaller or key-only passes keep the fused kernel.
+        // Large passes: a partition kernel (sample-guided splits of every
+        // tile) + the ticket-scheduled merge (K4's kernel without
+        // dependencies; dynamic tile order balances the tail) beat the fused
+        // search warps (2^27 pairs 10.2 vs 10.8 ms, 2^27 keys 7.37 vs 7.60 ms
+        // per sort); smaller passes keep the fused kernel (the partition
+        // launch costs more than it saves).
         unsigned *ticket = reinterpret_cast<unsigned *>(corank + ntiles);
         GNS_TRY(check(cudaMemsetAsync(ticket, 0, sizeof(unsigned), st), "memset"));
         GNS_TRY(launch_pdl("partition_kernel", partition_kern(ord),

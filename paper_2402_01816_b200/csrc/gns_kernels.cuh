@@ -1318,11 +1318,23 @@ merge_inplace_kernel(PipeGeo pg, int ntiles, const int *__restrict__ corank, con
         const uint64_t policy = policy_evict_first();
         // claim a tile in ticket order and load it into stage st, or tell the
         // merge warps there is none left (meta.t = ntiles, arrival without bytes)
+        // the next ticket and its co-ranks are fetched one tile ahead, so the
+        // atomic and the two loads are off the stage-refill path (claiming a
+        // ticket before loading it keeps ticket order: every tile still only
+        // waits on smaller tickets, and the smallest unfinished tile has its
+        // dependencies' loads landed)
+        int pf = (int)atomicAdd(ticket, 1u);
+        int pf_i0 = pf < ntiles ? corank[pf] : 0;
+        int pf_i1 = pf + 1 < ntiles ? corank[pf + 1] : 0;
         auto claim = [&](int st) -> bool {
-            const int c = (int)atomicAdd(ticket, 1u);
+            const int c = pf;
             if (c < ntiles) {
-                pipe_issue<HV>(pg, amap, bmap, c, corank[c], c + 1 < ntiles ? corank[c + 1] : 0, skb(st), svb(st),
-                               &full[st], &meta[st], policy);
+                pipe_issue<HV>(pg, amap, bmap, c, pf_i0, pf_i1, skb(st), svb(st), &full[st], &meta[st], policy);
+                pf = (int)atomicAdd(ticket, 1u);
+                if (pf < ntiles) {
+                    pf_i0 = corank[pf];
+                    pf_i1 = pf + 1 < ntiles ? corank[pf + 1] : 0;
+                }
                 return true;
             }
             meta[st].t = ntiles;
