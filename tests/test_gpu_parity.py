@@ -610,3 +610,16 @@ def test_ticket_merge_passes_int_keys(gns, key_type, target):
     gns.sort_(tk, tv, 1.0, target=target)
     torch.cuda.synchronize()
     assert np.array_equal(tk.cpu().numpy(), ek) and np.array_equal(tv.cpu().numpy(), ev)
+
+
+@pytest.mark.slow
+def test_ticket_merge_passes_large_keys(gns):
+    """Key-only passes of >= 32768 tiles (2^27 + ragged keys) also run as
+    partition + ticket-scheduled merge; vs the oracle, both buffer modes."""
+    n = (1 << 27) + 5
+    k = synth.ties(n, 41, 1 << 20)
+    k[::5] = synth.uniform(k[::5].size, 42)
+    ek, _ = oracle.sort(k, None)
+    for frac in (1.0, 0.5):
+        gk, _ = gpu_sort(gns, k, None, frac, use_ws=True)
+        assert_bitexact(gk, ek, what=f"frac={frac}")
