@@ -75,9 +75,15 @@ constexpr int MTILE = NT * VT;     // K3/K4 output tile = 4096 elements
 #define GNS_NT1 256
 #endif
 constexpr int NT1 = GNS_NT1;       // K1 threads per CTA (two CTAs per SM)
-constexpr int VT1 = 32;            // K1 keys per thread
+#ifndef GNS_VT1
+#define GNS_VT1 32
+#endif
+#ifndef GNS_T1_MINB
+#define GNS_T1_MINB (512 / GNS_NT1)
+#endif
+constexpr int VT1 = GNS_VT1;       // K1 keys per thread
 constexpr int TILE = NT1 * VT1;    // K1 tile = 8192 elements (runs entering the merge passes)
-constexpr int TILE_LOG2 = NT1 == 512 ? 14 : NT1 == 256 ? 13 : 12;
+constexpr int TILE_LOG2 = TILE == 16384 ? 14 : TILE == 8192 ? 13 : 12;
 static_assert((1 << TILE_LOG2) == TILE, "TILE must be 4096, 8192 or 16384");
 static_assert(TILE % MTILE == 0, "pair boundaries must fall on merge-tile boundaries");
 
@@ -1075,7 +1081,7 @@ __device__ __forceinline__ void serial_merge32(const double *sk, const uint32_t 
 }
 
 template <bool HV, int ORD>
-__global__ void __launch_bounds__(NT1, 512 / NT1)
+__global__ void __launch_bounds__(NT1, GNS_T1_MINB)
 tile_sort2_kernel(const double *src_k, const uint32_t *src_v, double *dst_k, uint32_t *dst_v, long long n,
                   const __grid_constant__ CUtensorMap ksrc, const __grid_constant__ CUtensorMap vsrc,
                   const __grid_constant__ CUtensorMap kdst, const __grid_constant__ CUtensorMap vdst,
@@ -1172,7 +1178,7 @@ tile_sort2_kernel(const double *src_k, const uint32_t *src_v, double *dst_k, uin
     // the thread's 32 keys: one stable odd-even transposition sort in
     // registers (trades ALU, which has headroom, for the shared-memory round
     // that merged two sorted halves: measured -1.6 %)
-    transpose_sort<0, 32, HV, ORD>(k, v);
+    transpose_sort<0, VT1, HV, ORD>(k, v);
     __syncthreads();                       // the TMA-layout reads are done before the first spill
 #pragma unroll 1
     for (int coop = 2; coop <= NT1; coop <<= 1) {
