@@ -293,7 +293,8 @@ __device__ __forceinline__ TileSpan tile_span(const MergeGeo &g, int t)
         s.nb = (int)max(0LL, min(g.L, rem - g.L));
     }
     s.k0 = (int)(s.g0 - s.pbase);
-    s.k1 = min(s.k0 + MTILE, s.na + s.nb);
+    // (64-bit: the last tile of a 2^31 - 1 element pair starts at 2^31 - 4096)
+    s.k1 = (int)min((long long)s.k0 + MTILE, (long long)s.na + s.nb);
     return s;
 }
 
