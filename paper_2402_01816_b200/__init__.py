@@ -176,7 +176,7 @@ def gns_timing_end(cap: int = 4096):
 
 
 LAUNCH_KINDS = {1: "tile_sort", 2: "merge_pass", 3: "partition", 4: "inplace_deps", 5: "inplace_merge", 6: "reverse",
-                7: "split_cuts", 8: "gather_samples", 9: "split4", 10: "tile4", 11: "merge4"}
+                7: "split_cuts", 8: "gather_samples"}
 
 
 def gns_tile_elems() -> int:

@@ -65,20 +65,10 @@ size_t left_len(size_t n)
 
 bool is_aligned(const void *p, size_t a) { return ((uintptr_t)p % a) == 0; }
 
-// Scratch of the 4-way merge passes (key-only): per virtual sample its
-// 4-way split, per output tile its last sample and its splits, one ticket.
-size_t f4_bytes(size_t n)
-{
-    const size_t nq = n / SMP_G + 2, nt = ceil_div(n, MTILE) + 1;
-    return align_up(nq * sizeof(Split4), 256) + align_up(nt * sizeof(unsigned long long), 256) +
-           align_up(nt * sizeof(Tile4), 256) + 256;
-}
-
 // Workspace layout (one allocation = the whole bufferRAM of a call).
 struct Layout {
     size_t buf_elems = 0;   // buffer key(+val) slots
     size_t off_k = 0, off_v = 0, off_corank = 0, off_deps = 0, off_flags = 0, off_adapt = 0, off_smp = 0, total = 0;
-    size_t off_f4 = 0;      // 4-way passes: Split4[nsmp], tile_end u64[ntiles], Tile4[ntiles], ticket
     size_t nsmp = 0;        // keys per sample array (two arrays: data-side and buffer-side regions)
     int ntiles = 0;         // merge tiles over the whole array
 };
@@ -113,8 +103,6 @@ Layout layout(size_t n, const Mode &m, bool hv)
     L.off_smp = o;                     // split-search samples, every SMP_G-th key of each region
     L.nsmp = n / SMP_G + 2;
     o = align_up(o + 2 * L.nsmp * sizeof(double), 256);
-    L.off_f4 = o;
-    if (!hv) o = align_up(o + f4_bytes(n), 256);
     L.total = o;
     return L;
 }
@@ -157,20 +145,6 @@ PartK partition_kern(int o)
     return t[o];
 }
 #undef GNS_ORDS
-using Split4K = decltype(&split4_kernel<0>);
-using Merge4K = decltype(&merge4_kernel<0>);
-Split4K split4_kern(int o)
-{
-    static const Split4K t[NORD] = {&split4_kernel<0>, &split4_kernel<1>, &split4_kernel<2>,
-                                    &split4_kernel<3>, &split4_kernel<4>, &split4_kernel<5>};
-    return t[o];
-}
-Merge4K merge4_kern(int o)
-{
-    static const Merge4K t[NORD] = {&merge4_kernel<0>, &merge4_kernel<1>, &merge4_kernel<2>,
-                                    &merge4_kernel<3>, &merge4_kernel<4>, &merge4_kernel<5>};
-    return t[o];
-}
 
 // Per-device one-time kernel attributes (dynamic shared memory > 48 KB).
 std::mutex g_attr_mu;
@@ -192,7 +166,6 @@ gns_status ensure_attrs()
             GNS_ATTR(inplace_kern(hv, o), ts_smem(hv));
             GNS_ATTR(tile_kern(hv, o), t1_smem(hv));
         }
-        GNS_ATTR(merge4_kern(o), ts4_smem());
     }
 #undef GNS_ATTR
     GNS_TRY(check(cudaDeviceGetAttribute(&g_num_sms[dev], cudaDevAttrMultiProcessorCount, dev), "sm count"));
@@ -287,9 +260,8 @@ int launch_kind(const char *what)
 {
     static const char *names[] = {"tile_sort2_kernel", "merge_tstore_kernel", "partition_kernel",
                                   "inplace_deps_kernel", "merge_inplace_kernel", "reverse_kernel",
-                                  "split_cuts_kernel", "gather_samples_kernel", "split4_kernel", "tile4_kernel",
-                                  "merge4_kernel"};
-    for (int i = 0; i < 11; ++i)
+                                  "split_cuts_kernel", "gather_samples_kernel"};
+    for (int i = 0; i < 8; ++i)
         if (std::strcmp(what, names[i]) == 0) return i + 1;
     return 0;
 }
@@ -437,47 +409,6 @@ MergeGeo uniform_geo(const double *sk, const uint32_t *sv, double *dk, uint32_t 
     return g;
 }
 
-// GNS_FOURWAY=1: key-only sorts merge two levels per HBM pass (experiment).
-bool fourway_enabled()
-{
-    static const bool on = [] {
-        const char *e = std::getenv("GNS_FOURWAY");
-        return e && e[0] == '1';
-    }();
-    return on;
-}
-
-// One 4-way merge pass (runs of L -> 4L), key-only: split points from the
-// virtual samples (split4_kernel), per-tile splits (tile4_kernel), merge.
-gns_status launch_merge4(const double *src, double *dst, size_t n, size_t L, const double *smp_in, double *smp_out,
-                         unsigned char *f4, int ord, cudaStream_t st)
-{
-    const int nq = (int)ceil_div(n, SMP_G);
-    const int ntiles = (int)ceil_div(n, MTILE);
-    Split4 *spl = reinterpret_cast<Split4 *>(f4);
-    unsigned long long *tile_end =
-        reinterpret_cast<unsigned long long *>(f4 + align_up((n / SMP_G + 2) * sizeof(Split4), 256));
-    Tile4 *ts = reinterpret_cast<Tile4 *>(reinterpret_cast<unsigned char *>(tile_end) +
-                                          align_up((ceil_div(n, MTILE) + 1) * sizeof(unsigned long long), 256));
-    unsigned *ticket = reinterpret_cast<unsigned *>(reinterpret_cast<unsigned char *>(ts) +
-                                                    align_up((ceil_div(n, MTILE) + 1) * sizeof(Tile4), 256));
-    GNS_TRY(check(cudaMemsetAsync(tile_end, 0, (size_t)ntiles * sizeof(unsigned long long), st), "memset"));
-    GNS_TRY(check(cudaMemsetAsync(ticket, 0, sizeof(unsigned), st), "memset"));
-    GNS_TRY(launch_pdl("split4_kernel", split4_kern(ord), (unsigned)ceil_div((size_t)nq * Q4W, 256), 256, 0, st,
-                       src, smp_in, (long long)n, (long long)L, nq, spl, tile_end));
-    GNS_TRY(launch_pdl("tile4_kernel", tile4_kernel, (unsigned)ceil_div((size_t)ntiles, 256), 256, 0, st,
-                       (long long)n, (long long)L, ntiles, (const Split4 *)spl, (const unsigned long long *)tile_end,
-                       ts));
-    CUtensorMap kmap;
-    long long idx0 = 0, rows = 0;
-    GNS_TRY(key_map(src, n, false, &kmap, &idx0, &rows));   // (src is 32-byte aligned: idx0 = 0)
-    // (key_map's box is krows(false) = 32 rows; merge4 uses boxes of K4ROWS rows)
-    GNS_TRY(row_map((void *)src, (size_t)rows * 16, true, K4ROWS, &kmap));
-    const int grid = std::min(ntiles, num_sms());
-    return launch_pdl("merge4_kernel", merge4_kern(ord), grid, NT4 + 32, ts4_smem(), st, src, dst, (long long)n,
-                      (long long)L, ntiles, (const Tile4 *)ts, ticket, kmap, rows, smp_out);
-}
-
 // Sorts region R = (rk, rv)[0:len) using partner region P of >= len slots as
 // ping-pong buffer (Nocopy-Mergesort).  The result ends in P if
 // `final_in_partner`, else in R.  Parity picks the tile-sort destination so
@@ -485,15 +416,11 @@ gns_status launch_merge4(const double *src, double *dst, size_t n, size_t L, con
 // smp: two sample arrays of >= len/SMP_G + 2 keys (R's and P's), or nullptr.
 gns_status sort_range(double *rk, uint32_t *rv, double *pk_, uint32_t *pv_, size_t len,
                       bool final_in_partner, int *corank, int ord, cudaStream_t st, unsigned *unsorted = nullptr,
-                      double *smp_r = nullptr, double *smp_p = nullptr, unsigned char *f4 = nullptr)
+                      double *smp_r = nullptr, double *smp_p = nullptr)
 {
     if (len == 0) return GNS_OK;
     const int M = merge_passes_for(len);
-    // 4-way passes (key-only, with samples and scratch): two levels per HBM pass
-    const bool four = f4 != nullptr && rv == nullptr && smp_r != nullptr && M >= 2 && fourway_enabled();
-    if (four) unsorted = nullptr;                       // (adaptivity not in the 4-way kernels yet)
-    const int H = four ? M / 2 + (M & 1) : M;           // HBM merge passes
-    const bool tile_to_partner = final_in_partner ^ (bool)(H & 1);
+    const bool tile_to_partner = final_in_partner ^ (bool)(M & 1);
     double *ck = tile_to_partner ? pk_ : rk;
     uint32_t *cv = tile_to_partner ? pv_ : rv;
     double *ok = tile_to_partner ? rk : pk_;
@@ -506,23 +433,6 @@ gns_status sort_range(double *rk, uint32_t *rv, double *pk_, uint32_t *pv_, size
     double *cs = tile_to_partner ? smp_p : smp_r;      // samples of the region holding the current runs
     double *os = tile_to_partner ? smp_r : smp_p;
     GNS_TRY(launch_tile_sort(rk, rv, ck, cv, len, ord, st, M > 0 ? unsorted : nullptr, M > 0 ? cs : nullptr));
-    if (four) {
-        for (int p = 0; p < M;) {
-            const size_t L = (size_t)TILE << p;
-            if (M - p >= 2) {
-                GNS_TRY(launch_merge4(ck, ok, len, L, cs, p + 2 < M ? os : nullptr, f4, ord, st));
-                p += 2;
-            } else {
-                MergeGeo g = uniform_geo(ck, cv, ok, ov, len, L, cs, nullptr);
-                GNS_TRY(launch_merge(g, ck + len, ck + len, corank, nullptr, nullptr, false, ord, st, Adapt{}));
-                p += 1;
-            }
-            std::swap(ck, ok);
-            std::swap(cv, ov);
-            std::swap(cs, os);
-        }
-        return GNS_OK;
-    }
     for (int p = 0; p < M; ++p) {
         const size_t L = (size_t)TILE << p;
         MergeGeo g = uniform_geo(ck, cv, ok, ov, len, L, cs, p + 1 < M ? os : nullptr);
@@ -711,8 +621,7 @@ gns_status run_sort(double *keys, uint32_t *vals, size_t n, const Mode &m, unsig
         double *smp = reinterpret_cast<double *>(ws + Lo.off_smp);
         if (!m.limited) {
             unsigned *unsorted = reinterpret_cast<unsigned *>(ws + Lo.off_adapt);
-            GNS_TRY(sort_range(keys, vals, bk, bv, n, false, corank, ord, st, unsorted, smp, smp + Lo.nsmp,
-                               hv ? nullptr : ws + Lo.off_f4));
+            GNS_TRY(sort_range(keys, vals, bk, bv, n, false, corank, ord, st, unsorted, smp, smp + Lo.nsmp));
         } else {
             int2 *deps = reinterpret_cast<int2 *>(ws + Lo.off_deps);
             unsigned *flags = reinterpret_cast<unsigned *>(ws + Lo.off_flags);

@@ -383,20 +383,23 @@ __device__ __forceinline__ int group_count_true(int lo, int hi, int gl, unsigned
     return lo - lo0;
 }
 
-// Stable co-rank of diagonal d for sorted runs A[0:na) and B[0:nb) (A wins
-// ties) by a group of W lanes; sample-guided when both runs' samples SA, SB
-// (every SMP_G-th key from each run's start) are given and d is a multiple of
-// SMP_G, else over the whole range.
+// Stable co-rank of tile t's first diagonal by a group of W lanes, sample-guided
+// when the pass has samples (uniform passes), else over the whole range.
 template <int W, int ORD>
-__device__ __forceinline__ int corank_runs(const double *A, int na, const double *SA, const double *B, int nb,
-                                           const double *SB, int d, int gl, unsigned mask, int gbase)
+__device__ __forceinline__ int tile_corank(const MergeGeo &g, int t, int gl, unsigned mask, int gbase)
 {
-    int lo = max(0, d - nb), hi = min(d, na);
+    const TileSpan s = tile_span(g, t);
+    const double *A = g.ak + s.pbase;
+    const double *B = g.bk + s.pbase;
+    const int d = s.k0;
+    int lo = max(0, d - s.nb), hi = min(d, s.na);
     if (lo >= hi) return lo;
-    if (SA != nullptr && SB != nullptr) {
+    if (g.sa != nullptr && (!g.single || g.sb != nullptr)) {
         const int s_lo = (lo + SMP_G - 1) >> SMP_LOG2;
         const int s_hi = (hi - 1) >> SMP_LOG2;
         if (s_lo <= s_hi) {
+            const double *SA = g.sa + (s.pbase >> SMP_LOG2);
+            const double *SB = g.single ? g.sb : g.sa + ((s.pbase + g.L) >> SMP_LOG2);
             const int cnt = group_count_true<W>(s_lo, s_hi, gl, mask, gbase, [&](int sx) {
                 const int yb = (d - 1 - (sx << SMP_LOG2)) >> SMP_LOG2;
                 return !before<ORD>(SB[yb], SA[sx]);
@@ -408,37 +411,6 @@ __device__ __forceinline__ int corank_runs(const double *A, int na, const double
     // exact: number of m in [lo, hi) with A[m] <= B[d-1-m]
     return lo + group_count_true<W>(lo, hi - 1, gl, mask, gbase,
                                     [&](int m) { return !before<ORD>(B[d - 1 - m], A[m]); });
-}
-
-// Stable co-rank of tile t's first diagonal by a group of W lanes, sample-guided
-// when the pass has samples (uniform passes), else over the whole range.
-template <int W, int ORD>
-__device__ __forceinline__ int tile_corank(const MergeGeo &g, int t, int gl, unsigned mask, int gbase)
-{
-    const TileSpan s = tile_span(g, t);
-    const bool smp = g.sa != nullptr && (!g.single || g.sb != nullptr);
-    const double *SA = smp ? g.sa + (s.pbase >> SMP_LOG2) : nullptr;
-    const double *SB = smp ? (g.single ? g.sb : g.sa + ((s.pbase + g.L) >> SMP_LOG2)) : nullptr;
-    return corank_runs<W, ORD>(g.ak + s.pbase, s.na, SA, g.bk + s.pbase, s.nb, SB, s.k0, gl, mask, gbase);
-}
-
-// Number of keys of the sorted run R[0:nr) that precede key v: those strictly
-// before v (UPPER = false) or those not after v (UPPER = true, e <= v).
-// Sample-guided (SR = every SMP_G-th key of R) by a group of W lanes.
-template <int W, int ORD, bool UPPER>
-__device__ __forceinline__ int count_preceding(const double *R, int nr, const double *SR, double v, int gl,
-                                               unsigned mask, int gbase)
-{
-    auto pre = [&](double e) { return UPPER ? !before<ORD>(v, e) : before<ORD>(e, v); };
-    int lo = 0, hi = nr;              // answer in [lo, hi]
-    if (nr <= 0) return 0;
-    if (SR != nullptr) {
-        const int ns = (nr + SMP_G - 1) >> SMP_LOG2;
-        const int c = group_count_true<W>(0, ns - 1, gl, mask, gbase, [&](int sx) { return pre(SR[sx]); });
-        if (c > 0) lo = ((c - 1) << SMP_LOG2) + 1;
-        if (c < ns) hi = c << SMP_LOG2;
-    }
-    return lo + group_count_true<W>(lo, hi - 1, gl, mask, gbase, [&](int m) { return pre(R[m]); });
 }
 
 template <int ORD>
@@ -1461,395 +1433,6 @@ merge_inplace_kernel(PipeGeo pg, int ntiles, const int *__restrict__ corank, con
     pdl_trigger();
 }
 
-
-// ============================================================================
-// 4-way merge passes: two merge levels per HBM pass (runs of L -> 4L).
-//
-// A group is 4 runs R0..R3 of length L; X = R0 (+) R1 and Y = R2 (+) R3 are the
-// virtual results of the level in between (stable, left wins), and the output
-// is X (+) Y.  Instead of splitting the output at fixed positions (which needs
-// X and Y at arbitrary positions: nested searches), the output is split at
-// points whose 4-way split is found with plain searches:
-//   * X-sample at X position x = 512a: its 2-way split c in (R0, R1) and key
-//     v = X[x] (one co-rank search), then the number of Y keys before v
-//     (X wins ties: keys of R2, R3 strictly before v) -> 4-way position
-//     P = x + y and split (c, x - c, lb(R2, v), lb(R3, v));
-//   * Y-sample at Y position y = 512b: symmetric, counting X keys not after
-//     v (ub(R0, v), ub(R1, v), c, y - c).
-// Each is a prefix of the stable 4-way order.  Along the merge path the
-// samples are at most 1024 outputs apart, so every 4096-block of the output
-// holds one; output tile t ends at the block's last sample (variable tiles of
-// 3072..5120 outputs), the group's last tile at the group end.
-constexpr int T4_MAX = MTILE + 1024;            // largest 4-way output tile
-constexpr int NT4 = 512;                        // merge threads of merge4_kernel (16 warps, 1 CTA per SM)
-constexpr int MERGE_WARPS4 = NT4 / 32;
-constexpr int VT4 = 11;                         // outputs per merge thread (512 * 11 >= T4_MAX + 10)
-static_assert(NT4 * VT4 >= T4_MAX + VT4 - 1, "level-1 layout: X part padded to a multiple of VT4, then Y part");
-__device__ __forceinline__ void bar_merge4() { asm volatile("bar.sync 1, %0;" :: "n"(NT4) : "memory"); }
-
-struct Split4 {
-    int c[4];
-};
-
-// One group of Q4W lanes per virtual sample q (virtual position p = 512 q of
-// the level in between): split and 4-way position, and per output 4096-block
-// the sample with the largest position (tile_end[T] = (P + 1) << 32 | q, 0 =
-// none; zeroed beforehand).  Narrow groups: the fine searches probe the runs
-// at random (one 32-byte sector per probe), so fewer probes per round cost
-// less DRAM traffic than the extra rounds cost latency.
-constexpr int Q4W = 8;
-template <int ORD>
-__global__ void __launch_bounds__(256)
-split4_kernel(const double *src, const double *smp, long long n, long long L, int nq, Split4 *spl,
-              unsigned long long *tile_end)
-{
-    pdl_wait();
-    pdl_trigger();
-    const int q = (int)((blockIdx.x * (long long)blockDim.x + threadIdx.x) / Q4W);
-    const int lane = threadIdx.x & 31;
-    const int gl = lane % Q4W, gbase = lane - gl;
-    const unsigned mask = ((1u << Q4W) - 1u) << gbase;
-    if (q >= nq) return;
-    const long long p = (long long)q << SMP_LOG2;
-    const long long span = 4 * L;
-    const long long G0 = (p / span) * span;
-    const long long vp = p - G0;
-    const bool side_y = vp >= 2 * L;
-    const int o = (int)(vp - (side_y ? 2 * L : 0));
-    auto rlen = [&](int r) { return (int)max(0LL, min(L, n - (G0 + r * L))); };   // (no array: no local memory)
-    const int ra = side_y ? 2 : 0;                                  // this side's runs ra, ra+1
-    const int la = rlen(ra), lb = rlen(ra + 1);
-    if (o >= la + lb) return;
-    auto run = [&](int r) { return src + G0 + r * L; };
-    auto rsmp = [&](int r) { return smp + ((G0 + r * L) >> SMP_LOG2); };
-    const int c = corank_runs<Q4W, ORD>(run(ra), la, rsmp(ra), run(ra + 1), lb, rsmp(ra + 1), o, gl, mask, gbase);
-    const double *A = run(ra), *B = run(ra + 1);
-    const bool takeA = c < la && (o - c >= lb || !before<ORD>(B[o - c], A[c]));
-    const double v = takeA ? A[c] : B[o - c];
-    // the other side's two runs
-    const int rb = side_y ? 0 : 2;
-    int cnt0, cnt1;
-    if (side_y) {
-        cnt0 = count_preceding<Q4W, ORD, true>(run(rb), rlen(rb), rsmp(rb), v, gl, mask, gbase);
-        cnt1 = count_preceding<Q4W, ORD, true>(run(rb + 1), rlen(rb + 1), rsmp(rb + 1), v, gl, mask, gbase);
-    } else {
-        cnt0 = count_preceding<Q4W, ORD, false>(run(rb), rlen(rb), rsmp(rb), v, gl, mask, gbase);
-        cnt1 = count_preceding<Q4W, ORD, false>(run(rb + 1), rlen(rb + 1), rsmp(rb + 1), v, gl, mask, gbase);
-    }
-    if (gl == 0) {
-        Split4 sp;
-        if (side_y) {
-            sp.c[0] = cnt0; sp.c[1] = cnt1; sp.c[2] = c; sp.c[3] = o - c;
-        } else {
-            sp.c[0] = c; sp.c[1] = o - c; sp.c[2] = cnt0; sp.c[3] = cnt1;
-        }
-        spl[q] = sp;
-        const long long P = (long long)o + cnt0 + cnt1;               // 4-way position within the group
-        atomicMax(tile_end + ((G0 + P) >> 12), ((unsigned long long)(P + 1) << 32) | (unsigned)q);
-    }
-}
-
-// Per output tile t (4096-block of the output): its start and end 4-way splits
-// and group-relative output positions.  ts[t] = {P0, P1, s0..s3, e0..e3}.
-struct Tile4 {
-    int p0, p1;
-    int s[4], e[4];
-};
-
-__global__ void __launch_bounds__(256)
-tile4_kernel(long long n, long long L, int ntiles, const Split4 *spl, const unsigned long long *tile_end,
-             Tile4 *ts)
-{
-    pdl_wait();
-    pdl_trigger();
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= ntiles) return;
-    const long long span = 4 * L;
-    const long long g0 = (long long)t * MTILE;
-    const long long G0 = (g0 / span) * span;
-    int len[4];
-    long long gs = 0;
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-        len[r] = (int)max(0LL, min(L, n - (G0 + r * L)));
-        gs += len[r];
-    }
-    const int t_first = (int)(G0 / MTILE);
-    const int t_last = (int)((G0 + gs - 1) / MTILE);
-    Tile4 o;
-    if (t == t_first) {
-        o.p0 = 0;
-#pragma unroll
-        for (int r = 0; r < 4; ++r) o.s[r] = 0;
-    } else {
-        const unsigned long long key = tile_end[t - 1];
-        const Split4 sp = spl[(unsigned)key];
-        o.p0 = (int)((key >> 32) - 1);
-#pragma unroll
-        for (int r = 0; r < 4; ++r) o.s[r] = sp.c[r];
-    }
-    if (t == t_last) {
-        o.p1 = (int)gs;
-#pragma unroll
-        for (int r = 0; r < 4; ++r) o.e[r] = len[r];
-    } else {
-        const unsigned long long key = tile_end[t];
-        const Split4 sp = spl[(unsigned)key];
-        o.p1 = (int)((key >> 32) - 1);
-#pragma unroll
-        for (int r = 0; r < 4; ++r) o.e[r] = sp.c[r];
-    }
-    GNS_DASSERT(tile_end[t] != 0ull || t == t_last);
-    GNS_DASSERT(o.p1 > o.p0 && o.p1 - o.p0 <= T4_MAX);
-    ts[t] = o;
-}
-
-// Stage of a 4-way tile: the four runs' key rows by TMA boxes (128-byte
-// swizzle), run r at stage rows [rr[r], rr[r+1]).
-constexpr int K4ROWS = 16;
-constexpr int STAGE4_ROWS = ((T4_MAX / 16 + 8 + 4 * (K4ROWS - 1)) + K4ROWS - 1) / K4ROWS * K4ROWS;   // 400
-constexpr size_t TS4_BYTES = (size_t)STAGE4_ROWS * 128;                                              // 51,200
-constexpr int NST4 = 3;                                                                               // stages
-constexpr size_t L1BUF_BYTES = (size_t)T4_MAX * 8;                                                    // 40,960
-static_assert(L1BUF_BYTES % 1024 == 0, "level-1 buffer keeps the 128-byte swizzle period");
-constexpr size_t ts4_smem() { return NST4 * TS4_BYTES + L1BUF_BYTES + 1024; }
-
-struct Meta4 {
-    int t, p0, cnt;                 // tile, group-relative start, outputs
-    long long out0;                 // global output index of the tile's first output
-    int slot[4], len[4];            // key slot of each run's first key, keys per run
-    int pslot[4], pcnt[4];          // keys past the map's last full row, patched from psrc
-    const double *psrc[4];
-};
-
-// Serial merge of up to VT4 outputs from key slots (A: ai..aend, B: bi..bend)
-// of a swizzled stage, left wins ties; outputs beyond `cnt` are not used.
-template <int ORD>
-__device__ __forceinline__ void serial_merge4(uint32_t kbase, int ai, int aend, int bi, int bend,
-                                              double (&k)[VT4])
-{
-    double ka = lds_f64(stage_addr(kbase, ai)), kb = lds_f64(stage_addr(kbase, bi));
-#pragma unroll
-    for (int x = 0; x < VT4; ++x) {
-        const bool p = (bi < bend) && ((ai >= aend) || before<ORD>(kb, ka));
-        k[x] = p ? kb : ka;
-        const int src = p ? bi : ai;
-        const int nxt = src + 1;
-        GNS_DASSERT(nxt < STAGE4_ROWS * 16);
-        const uint32_t a = stage_addr(kbase, nxt);
-        if (p) {
-            bi = nxt;
-            kb = lds_f64(a);
-        } else {
-            ai = nxt;
-            ka = lds_f64(a);
-        }
-    }
-}
-
-// The 4-way merge (key-only): ticket-scheduled, warp-specialised like
-// merge_inplace_kernel, one CTA per SM (16 merge warps + a producer warp, 3
-// stages).  Merge warps: level 1 (R0 (+) R1 -> X part, R2 (+) R3 -> Y part;
-// thread t takes outputs [VT4 t, VT4 t + VT4) of the X part padded to a
-// multiple of VT4 followed by the Y part) into the level-1 buffer; level 2
-// (X part (+) Y part) into registers, written linearly into the (consumed)
-// stage for one 1-D bulk store of the tile (the unaligned first / last key by
-// hand).
-template <int ORD>
-__global__ void __launch_bounds__(NT4 + 32, 1)
-merge4_kernel(const double *src, double *dst, long long n, long long L, int ntiles, const Tile4 *ts,
-              unsigned *ticket, const __grid_constant__ CUtensorMap kmap, long long krows, double *so)
-{
-    pdl_wait();
-    extern __shared__ __align__(16) unsigned char smem_raw0[];
-    unsigned char *smem_raw = smem_raw0 + ((1024u - (smem_u32(smem_raw0) & 1023u)) & 1023u);
-    __shared__ __align__(8) uint64_t full[NST4];
-    __shared__ __align__(8) uint64_t staged[NST4];
-    __shared__ Meta4 meta[NST4];
-    auto skb = [&](int st) { return reinterpret_cast<double *>(smem_raw + st * TS4_BYTES); };
-    const uint32_t bbase = smem_u32(smem_raw + NST4 * TS4_BYTES);     // level-1 buffer
-    const int tid = threadIdx.x;
-    const int warp = tid >> 5, lane = tid & 31;
-    if (tid == 0) {
-        for (int b = 0; b < NST4; ++b) {
-            mbar_init(&full[b], 1);
-            mbar_init(&staged[b], MERGE_WARPS4);
-        }
-        fence_mbar_init();
-    }
-    __syncthreads();
-    const long long span = 4 * L;
-
-    if (warp == MERGE_WARPS4) {
-        if (lane != 0) return;
-        const uint64_t policy = policy_evict_first();
-        int pf = (int)atomicAdd(ticket, 1u);
-        Tile4 pft;
-        if (pf < ntiles) pft = ts[pf];
-        auto claim = [&](int st) -> bool {
-            const int t = pf;
-            if (t >= ntiles) {
-                meta[st].t = ntiles;
-                mbar_arrive(&full[st]);
-                return false;
-            }
-            const Tile4 tl = pft;
-            pf = (int)atomicAdd(ticket, 1u);
-            if (pf < ntiles) pft = ts[pf];
-            const long long G0 = ((long long)t * MTILE / span) * span;
-            Meta4 m;
-            m.t = t;
-            m.p0 = tl.p0;
-            m.cnt = tl.p1 - tl.p0;
-            m.out0 = G0 + tl.p0;
-            int nb[4], row = 0;
-            long long gi[4];
-            uint32_t bytes = 0;
-#pragma unroll
-            for (int r = 0; r < 4; ++r) {
-                const int c = tl.e[r] - tl.s[r];
-                gi[r] = G0 + r * L + tl.s[r];
-                nb[r] = c > 0 ? (int)((((gi[r] + c - 1) >> 4) - (gi[r] >> 4)) / K4ROWS) + 1 : 0;
-                m.len[r] = c;
-                m.slot[r] = row * 16 + (int)(gi[r] & 15);
-                m.pcnt[r] = 0;
-                m.pslot[r] = 0;
-                m.psrc[r] = src + gi[r];
-                if (c > 0 && gi[r] + c > krows * 16) {              // past the map's last full row
-                    const int e0 = (int)max(0LL, krows * 16 - gi[r]);
-                    m.pcnt[r] = c - e0;
-                    m.pslot[r] = m.slot[r] + e0;
-                    m.psrc[r] = src + gi[r] + e0;
-                }
-                row += nb[r] * K4ROWS;
-                bytes += (uint32_t)nb[r] * (K4ROWS * 128u);
-            }
-            GNS_DASSERT(row <= STAGE4_ROWS && m.cnt > 0 && m.cnt <= T4_MAX);
-            mbar_expect_tx(&full[st], bytes);
-            double *sk = skb(st);
-#pragma unroll
-            for (int r = 0; r < 4; ++r) {
-                const int r0 = m.slot[r] >> 4;
-                for (int b = 0; b < nb[r]; ++b)
-                    tma_load_2d_hint(sk + (r0 + b * K4ROWS) * 16, &kmap, 0, (int)((gi[r] >> 4) + b * K4ROWS),
-                                     &full[st], policy);
-            }
-            meta[st] = m;
-            mbar_arrive(&full[st]);
-            return true;
-        };
-        bool more = true;
-        for (int st = 0; st < NST4 && more; ++st) more = claim(st);   // (the merge warps stop at the first end marker)
-        for (int i = 0;; ++i) {
-            const int st = i % NST4;
-            mbar_wait(&staged[st], (uint32_t)((i / NST4) & 1));
-            const Meta4 m = meta[st];
-            if (m.t >= ntiles) break;
-            // outputs [out0, out0 + cnt) sit at stage slots [out0 & 1, ...): the
-            // 16-byte aligned middle by one bulk store (the merge warps stored
-            // an unaligned first / last key by hand)
-            const long long a0 = (m.out0 + 1) & ~1LL, a1 = (m.out0 + m.cnt) & ~1LL;
-            if (a1 > a0) {
-                const unsigned char *sbase = reinterpret_cast<const unsigned char *>(skb(st));
-                const uint32_t soff = (uint32_t)((a0 - m.out0 + (m.out0 & 1)) * 8);
-                asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
-                             :: "l"(dst + a0), "r"(smem_u32(sbase + soff)), "r"((uint32_t)((a1 - a0) * 8))
-                             : "memory");
-                bulk_commit();
-            }
-            bulk_wait_read0();
-            if (more) more = claim(st);
-            else {
-                meta[st].t = ntiles;
-                mbar_arrive(&full[st]);
-            }
-        }
-        bulk_wait0();
-        pdl_trigger();
-        return;
-    }
-
-    // ------------------------------------------------------------ merge warps
-    for (int i = 0;; ++i) {
-        const int st = i % NST4;
-        mbar_wait(&full[st], (uint32_t)((i / NST4) & 1));
-        const Meta4 &m = meta[st];             // (read in place: the producer rewrites it only after `staged`)
-        if (m.t >= ntiles) {
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&staged[st]);
-            break;
-        }
-        double *sk = skb(st);
-        const uint32_t kbase = smem_u32(sk);
-        // keys the TMA box could not deliver (array end)
-        if ((m.pcnt[0] | m.pcnt[1] | m.pcnt[2] | m.pcnt[3]) != 0) {
-#pragma unroll
-            for (int r = 0; r < 4; ++r)
-                for (int e = tid; e < m.pcnt[r]; e += NT4)
-                    asm volatile("st.shared.f64 [%0], %1;" :: "r"(stage_addr(kbase, m.pslot[r] + e)),
-                                 "d"(m.psrc[r][e]) : "memory");
-            bar_merge4();
-        }
-        // ---- level 1: X part = R0 (+) R1, Y part = R2 (+) R3
-        const int sx = m.len[0] + m.len[1], sy = m.len[2] + m.len[3];
-        const int xend = (sx + VT4 - 1) / VT4 * VT4;             // Y part starts at a thread boundary
-        double k[VT4];
-        int q0 = tid * VT4, cnt1 = 0, side = -1;
-        if (q0 < sx) {
-            side = 0;
-            cnt1 = min(VT4, sx - q0);
-        } else if (q0 >= xend && q0 < xend + sy) {
-            side = 1;
-            q0 -= xend;
-            cnt1 = min(VT4, sy - q0);
-        }
-        if (side >= 0) {
-            const int ra = 2 * side;
-            const int a0 = m.slot[ra], na = m.len[ra], b0 = m.slot[ra + 1], nb = m.len[ra + 1];
-            const int ii = merge_path_stage<ORD>(kbase, a0, na, b0, nb, q0);
-            serial_merge4<ORD>(kbase, a0 + ii, a0 + na, b0 + q0 - ii, b0 + nb, k);
-        }
-        bar_merge4();                         // the previous tile's level 2 is done with the buffer
-        // X part at buffer slots [0, sx), Y part at [sx, sx + sy)
-        if (side >= 0) {
-            const int base = side ? sx + q0 : q0;
-#pragma unroll
-            for (int x = 0; x < VT4; ++x)
-                if (x < cnt1)
-                    asm volatile("st.shared.f64 [%0], %1;" :: "r"(stage_addr(bbase, base + x)), "d"(k[x]) : "memory");
-        }
-        bar_merge4();
-        // ---- level 2: X part (+) Y part, X wins ties
-        const int cnt = m.cnt;
-        const int d = min(tid * VT4, cnt);
-        const int c2 = min(VT4, cnt - d);
-        if (c2 > 0) {
-            const int ii = merge_path_stage<ORD>(bbase, 0, sx, sx, sy, d);
-            serial_merge4<ORD>(bbase, ii, sx, sx + d - ii, sx + sy, k);
-        }
-        // linear staging (the stage's input was consumed before the last
-        // barrier): output j at stage byte (j + (out0 & 1)) * 8, unswizzled
-        const int sh = (int)(m.out0 & 1);
-#pragma unroll
-        for (int x = 0; x < VT4; ++x)
-            if (x < c2) sk[sh + d + x] = k[x];
-        // unaligned first / last output by hand; samples of the output
-        const long long o0 = m.out0;
-        if (tid == 0 && (o0 & 1)) dst[o0] = k[0];
-        // (read back from the thread's own staging writes, not k[variable]: a
-        // dynamic index would move k to local memory)
-        if (c2 > 0 && d + c2 == cnt && ((o0 + cnt) & 1)) dst[o0 + cnt - 1] = sk[sh + cnt - 1];
-        if (so != nullptr && c2 > 0) {
-            const long long g = o0 + d;
-            const long long mult = (g + SMP_G - 1) & ~(long long)(SMP_G - 1);
-            if (mult < g + c2) so[mult >> SMP_LOG2] = sk[sh + (int)(mult - o0)];
-        }
-        fence_proxy_async();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&staged[st]);
-    }
-    pdl_trigger();
-}
 
 // ------------------------------------- target reversal (NEXT f3, AscRight/DescRight)
 // AscRight = reverse(DescLeft), DescRight = reverse(AscLeft) (PAPER.md:137-142:
