@@ -129,6 +129,23 @@ typedef enum {
 gns_status gns_sort_keys(void *keys, gns_key_type key_type, uint32_t *vals, size_t n, double buffer_fraction,
                          gns_target target, void *ws, size_t ws_bytes, gns_stream_t stream);
 
+/* NEXT f2: Omitsort (§Full adaptivity) on the full buffer
+ * (%RAM 2.0; workspace = gns_workspace_bytes(n, 1.0, vals != NULL)).  Same
+ * result as gns_sort_keys (the unique stable sort), different schedule: every
+ * sorted run carries its location (data or buffer); a pair of runs in
+ * different regions first moves the buffer-resident run to the data region
+ * (the paper's "copies one to the data region"); a pair whose runs do not
+ * overlap (B's first key not before A's last) is not merged at all ("omitted",
+ * zero moves); others are merged into the other region.  The tile sort works
+ * in place and does not write back tiles already in order.  A run that ends in
+ * the buffer is copied back once.  Presorted input moves no key; partially
+ * presorted input (long ascending runs) moves only where runs overlap; random
+ * input costs one copy pass more than gns_sort_keys when the number of merge
+ * levels is odd, plus ~10 us of planning per level.  Arguments, alignment and
+ * errors as gns_sort_keys (ws may be NULL: allocated stream-ordered). */
+gns_status gns_sort_omit(void *keys, gns_key_type key_type, uint32_t *vals, size_t n, gns_target target, void *ws,
+                         size_t ws_bytes, gns_stream_t stream);
+
 /* ---- NEXT f4: the steps of the distributed sort (paper_2402_01816_b200.dist,
  * SURVEY.md §8(e); "parallelize over an arbitrary number of processes",
  * PAPER.md:353).  Each rank sorts its shard (gns_sort_keys), the ranks agree
@@ -213,7 +230,8 @@ gns_status gns_merge_inplace_top(double *keys, uint32_t *vals, const double *lef
  * gns_timing_end(ms, kind, cap): waits for the last event, writes up to cap
  * per-launch durations (milliseconds) and kinds (1 tile sort, 2 merge pass,
  * 3 co-rank partition, 4 in-place dependency ranges, 5 in-place merge,
- * 6 reversal, 7 splitter cuts, 8 sample gather, 0 other) in launch order, turns timing off and returns the number
+ * 6 reversal, 7 splitter cuts, 8 sample gather, 9 Omitsort plan, 10 Omitsort
+ * tile list + copies, 11 Omitsort final copy, 0 other) in launch order, turns timing off and returns the number
  * of timed launches (-1 if timing was off or an event failed). */
 gns_status gns_timing_begin(int max_launches);
 int gns_timing_end(float *ms, int *kind, int cap);

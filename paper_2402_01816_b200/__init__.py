@@ -64,6 +64,7 @@ _c = {
     "gns_sort_pairs_f64_u32_ws": _sig("gns_sort_pairs_f64_u32_ws", [_vp, _vp, _sz, _d, _vp, _sz, _vp]),
     "gns_sort_target_f64": _sig("gns_sort_target_f64", [_vp, _vp, _sz, _d, _i, _vp, _sz, _vp]),
     "gns_sort_keys": _sig("gns_sort_keys", [_vp, _i, _vp, _sz, _d, _i, _vp, _sz, _vp]),
+    "gns_sort_omit": _sig("gns_sort_omit", [_vp, _i, _vp, _sz, _i, _vp, _sz, _vp]),
     "gns_split_cuts": _sig("gns_split_cuts", [_vp, _i, _sz, _vp, _vp, _vp, _i, _i, _vp, _vp]),
     "gns_merge_two": _sig("gns_merge_two", [_vp, _vp, _sz, _vp, _vp, _sz, _vp, _vp, _i, _vp]),
     "gns_plan": _sig("gns_plan", [_sz, _d, _i, ctypes.POINTER(gns_plan_info)]),
@@ -131,6 +132,10 @@ def gns_sort_keys(keys_ptr, key_type, vals_ptr, n, buffer_fraction, target, ws_p
     return _c["gns_sort_keys"](keys_ptr, key_type, vals_ptr, n, buffer_fraction, target, ws_ptr, ws_bytes, stream)
 
 
+def gns_sort_omit(keys_ptr, key_type, vals_ptr, n, target, ws_ptr, ws_bytes, stream) -> int:
+    return _c["gns_sort_omit"](keys_ptr, key_type, vals_ptr, n, target, ws_ptr, ws_bytes, stream)
+
+
 def gns_split_cuts(keys_ptr, key_type, n, spl_keys, spl_rank, spl_pos, nsplit, my_rank, cuts, stream) -> int:
     return _c["gns_split_cuts"](keys_ptr, key_type, n, spl_keys, spl_rank, spl_pos, nsplit, my_rank, cuts, stream)
 
@@ -176,7 +181,7 @@ def gns_timing_end(cap: int = 4096):
 
 
 LAUNCH_KINDS = {1: "tile_sort", 2: "merge_pass", 3: "partition", 4: "inplace_deps", 5: "inplace_merge", 6: "reverse",
-                7: "split_cuts", 8: "gather_samples"}
+                7: "split_cuts", 8: "gather_samples", 9: "omit_plan", 10: "omit_prep", 11: "omit_final"}
 
 
 def gns_tile_elems() -> int:
@@ -230,6 +235,21 @@ def _check_keys(keys, vals, any_key_type: bool = False):
             raise TypeError("vals must be a contiguous CUDA uint32 tensor")
         if vals.numel() != keys.numel():
             raise ValueError("keys and vals differ in length")
+
+
+def sort_omit_(keys, vals=None, workspace=None, stream=None, target: str = "AscLeft"):
+    """NEXT f2 Omitsort schedule (gns_sort_omit): the same stable sort as
+    ``sort_`` with the full buffer, but runs carry their location, merges of
+    non-overlapping runs are omitted and presorted input moves no key.
+    ``workspace``: optional uint8 CUDA tensor of >= workspace_bytes(n, 1.0,
+    vals is not None) bytes."""
+    _check_keys(keys, vals, any_key_type=True)
+    n = keys.numel()
+    wp = _ptr(workspace) if workspace is not None else None
+    wb = workspace.numel() * workspace.element_size() if workspace is not None else 0
+    _check(gns_sort_omit(_ptr(keys), _key_type(keys), _ptr(vals), n, TARGETS[target], wp, wb,
+                         _stream_handle(stream)), "sort_omit_")
+    return keys, vals
 
 
 def sort_(keys, vals=None, buffer_fraction: float = 1.0, workspace=None, stream=None, target: str = "AscLeft"):

@@ -71,6 +71,11 @@ struct Layout {
     size_t off_k = 0, off_v = 0, off_corank = 0, off_deps = 0, off_flags = 0, off_adapt = 0, off_smp = 0, total = 0;
     size_t nsmp = 0;        // keys per sample array (two arrays: data-side and buffer-side regions)
     int ntiles = 0;         // merge tiles over the whole array
+    // NEXT f2 Omitsort (full buffer only): run state of two levels (location,
+    // first and last key), per level and pair the copy flag, per level the
+    // merge tile list and its length (+ the sorted run's region)
+    size_t off_loc = 0, off_fl = 0, off_fix = 0, off_pre = 0, off_list = 0, off_cnt = 0;
+    size_t nruns = 0, npairs = 0;
 };
 
 // Buffer mode (row a5 and NEXT f1): FULL = 100 % buffer (ping-pong with the
@@ -79,6 +84,7 @@ struct Layout {
 struct Mode {
     bool limited = false;
     size_t buf = 0;
+    bool omit = false;      // NEXT f2: Omitsort schedule (full buffer; gns_sort_omit)
 };
 
 Layout layout(size_t n, const Mode &m, bool hv)
@@ -103,6 +109,23 @@ Layout layout(size_t n, const Mode &m, bool hv)
     L.off_smp = o;                     // split-search samples, every SMP_G-th key of each region
     L.nsmp = n / SMP_G + 2;
     o = align_up(o + 2 * L.nsmp * sizeof(double), 256);
+    if (!m.limited) {
+        L.nruns = ceil_div(n, TILE);
+        L.npairs = ceil_div(n, 2 * (size_t)TILE);
+        const size_t M = (size_t)merge_passes_for(n);
+        L.off_loc = o;
+        o = align_up(o + 2 * L.nruns, 256);
+        L.off_fl = o;
+        o = align_up(o + 4 * L.nruns * sizeof(double), 256);
+        L.off_fix = o;                                      // action bytes, all levels' pairs (<= nruns + M)
+        o = align_up(o + L.nruns + M, 256);
+        L.off_pre = o;                                      // merge-tile prefixes, all levels' pairs
+        o = align_up(o + (L.nruns + M) * sizeof(int), 256);
+        L.off_list = o;                                     // one level's merge-tile list
+        o = align_up(o + (size_t)L.ntiles * sizeof(int), 256);
+        L.off_cnt = o;
+        o = align_up(o + (M + 1) * sizeof(int), 256);
+    }
     L.total = o;
     return L;
 }
@@ -120,6 +143,8 @@ size_t merge_ws(size_t n)
 constexpr int NORD = 6;
 using TileK = decltype(&tile_sort2_kernel<false, 0>);
 using MergeK = decltype(&merge_tstore_kernel<false, 0>);
+using MergeOLK = decltype(&merge_tstore_kernel<false, 0, 2, true>);
+using OmitPlanK = decltype(&omit_plan_kernel<0>);
 using InplK = decltype(&merge_inplace_kernel<false, 0>);
 using PartK = decltype(&partition_kernel<0>);
 #define GNS_ORDS(K, HV) {&K<HV, 0>, &K<HV, 1>, &K<HV, 2>, &K<HV, 3>, &K<HV, 4>, &K<HV, 5>}
@@ -132,6 +157,21 @@ MergeK merge_kern(bool hv, int o)
 {
     static const MergeK t[2][NORD] = {GNS_ORDS(merge_tstore_kernel, false), GNS_ORDS(merge_tstore_kernel, true)};
     return t[hv][o];
+}
+#define GNS_ORDS_OL(K, HV) {&K<HV, 0, 2, true>, &K<HV, 1, 2, true>, &K<HV, 2, 2, true>, \
+                           &K<HV, 3, 2, true>, &K<HV, 4, 2, true>, &K<HV, 5, 2, true>}
+MergeOLK merge_kern_ol(bool hv, int o)
+{
+    static const MergeOLK t[2][NORD] = {GNS_ORDS_OL(merge_tstore_kernel, false),
+                                        GNS_ORDS_OL(merge_tstore_kernel, true)};
+    return t[hv][o];
+}
+#undef GNS_ORDS_OL
+OmitPlanK omit_plan_kern(int o)
+{
+    static const OmitPlanK t[NORD] = {&omit_plan_kernel<0>, &omit_plan_kernel<1>, &omit_plan_kernel<2>,
+                                      &omit_plan_kernel<3>, &omit_plan_kernel<4>, &omit_plan_kernel<5>};
+    return t[o];
 }
 InplK inplace_kern(bool hv, int o)
 {
@@ -163,6 +203,8 @@ gns_status ensure_attrs()
     for (int o = 0; o < NORD; ++o) {
         for (int hv = 0; hv < 2; ++hv) {
             GNS_ATTR(merge_kern(hv, o), ts_smem(hv));
+            GNS_ATTR(merge_kern_ol(hv, o), ts_smem(hv));
+            if (!hv) GNS_ATTR(omit_plan_kern(o), OMIT_SMEM);
             GNS_ATTR(inplace_kern(hv, o), ts_smem(hv));
             GNS_ATTR(tile_kern(hv, o), t1_smem(hv));
         }
@@ -260,8 +302,9 @@ int launch_kind(const char *what)
 {
     static const char *names[] = {"tile_sort2_kernel", "merge_tstore_kernel", "partition_kernel",
                                   "inplace_deps_kernel", "merge_inplace_kernel", "reverse_kernel",
-                                  "split_cuts_kernel", "gather_samples_kernel"};
-    for (int i = 0; i < 8; ++i)
+                                  "split_cuts_kernel", "gather_samples_kernel", "omit_plan_kernel",
+                                  "omit_prep_kernel", "omit_final_kernel"};
+    for (int i = 0; i < 11; ++i)
         if (std::strcmp(what, names[i]) == 0) return i + 1;
     return 0;
 }
@@ -366,7 +409,7 @@ gns_status launch_merge(const MergeGeo &g, const double *lim_a, const double *li
         const int grid = (int)ceil_div(ntiles, per);
         auto kern = merge_kern(hv, ord);
         return launch_pdl("merge_tstore_kernel", kern, grid, WS_THREADS, ts_smem(hv), st, pg, ntiles, per, map, amap,
-                          bmap, ad);
+                          bmap, ad, OmitList{}, map, amap, bmap);
     }
     GNS_TRY(launch_pdl("partition_kernel", partition_kern(ord),
                        (unsigned)ceil_div((size_t)ntiles * 32, 256), 256, 0, st, g, ntiles, corank));
@@ -469,6 +512,90 @@ gns_status sort_range(double *rk, uint32_t *rv, double *pk_, uint32_t *pv_, size
         std::swap(cs, os);
     }
     return GNS_OK;
+}
+
+// One list-driven merge launch (Omitsort): the listed tiles, data -> buffer
+// (g0) or buffer -> data (g1) per the entry's direction bit.
+gns_status launch_merge_list(const MergeGeo &g0, const MergeGeo &g1, const int *list, const int *count, int ord,
+                             cudaStream_t st)
+{
+    const int ntiles = (int)ceil_div((size_t)g0.n, MTILE);
+    const bool hv = g0.av != nullptr;
+    PipeGeo pg[2];
+    CUtensorMap map[2], amap[2], bmap[2];
+    const MergeGeo *gs[2] = {&g0, &g1};
+    for (int d = 0; d < 2; ++d) {
+        const MergeGeo &g = *gs[d];
+        const double *lim = g.ak + g.n;
+        pg[d].g = g;
+        pg[d].a_lim = lim;
+        pg[d].b_lim = lim;
+        GNS_TRY(row_map(g.ok, (size_t)g.n, true, MTILE / 16, &map[d]));
+        GNS_TRY(key_map(g.ak, (size_t)g.n, hv, &amap[d], &pg[d].a_idx0, &pg[d].a_rows));
+        GNS_TRY(key_map(g.bk, (size_t)std::max<long long>(0, lim - g.bk), hv, &bmap[d], &pg[d].b_idx0,
+                        &pg[d].b_rows));
+    }
+    OmitList ol{list, count, pg[1]};
+    const int grid = std::min(ntiles, 2 * num_sms());
+    return launch_pdl("merge_tstore_kernel", merge_kern_ol(hv, ord), grid, WS_THREADS, ts_smem(hv), st, pg[0], ntiles,
+                      0, map[0], amap[0], bmap[0], Adapt{}, ol, map[1], amap[1], bmap[1]);
+}
+
+// NEXT f2: Omitsort on the full buffer.  The tile sort works
+// in place (a tile already in order is not written back); one plan launch
+// decides every level; per level the copies and one list-driven merge
+// launch; a final copy if the sorted run ends in the buffer.  Presorted
+// input: no key moves.
+gns_status sort_omit(double *keys, uint32_t *vals, size_t n, unsigned char *ws, const Layout &Lo, int ord,
+                     cudaStream_t st)
+{
+    const bool hv = vals != nullptr;
+    double *bk = reinterpret_cast<double *>(ws + Lo.off_k);
+    uint32_t *bv = hv ? reinterpret_cast<uint32_t *>(ws + Lo.off_v) : nullptr;
+    double *smp_d = reinterpret_cast<double *>(ws + Lo.off_smp);
+    double *smp_b = smp_d + Lo.nsmp;
+    OmitState S;
+    S.loc[0] = ws + Lo.off_loc;
+    S.loc[1] = S.loc[0] + Lo.nruns;
+    double *fl = reinterpret_cast<double *>(ws + Lo.off_fl);
+    S.first[0] = fl;
+    S.first[1] = fl + Lo.nruns;
+    S.last[0] = fl + 2 * Lo.nruns;
+    S.last[1] = fl + 3 * Lo.nruns;
+    unsigned char *act = ws + Lo.off_fix;
+    int *pre = reinterpret_cast<int *>(ws + Lo.off_pre);
+    int *list = reinterpret_cast<int *>(ws + Lo.off_list);
+    int *cnt = reinterpret_cast<int *>(ws + Lo.off_cnt);
+    const int M = merge_passes_for(n);
+    GNS_TRY(launch_tile_sort(keys, vals, keys, vals, n, ord, st, nullptr, smp_d));
+    GNS_TRY(launch_pdl("omit_plan_kernel", omit_plan_kern(ord), 1, OMIT_THREADS,
+                       Lo.nruns <= (size_t)OMIT_SMEM_RUNS ? OMIT_SMEM : 0, st, (const double *)keys, (long long)n, M,
+                       S, act, pre, cnt));
+    const unsigned cgrid = (unsigned)std::min<size_t>(ceil_div(n, MTILE), (size_t)num_sms() * 4);
+    size_t off = 0;
+    for (int p = 0; p < M; ++p) {
+        const size_t L = (size_t)TILE << p;
+        const unsigned char *ap = act + off;
+        const int *pp = pre + off;
+        off += ceil_div(n, 2 * L);
+        if (hv)
+            GNS_TRY(launch_pdl("omit_prep_kernel", omit_prep_kernel<true>, cgrid, 256, 0, st, keys, vals,
+                               (const double *)bk, (const uint32_t *)bv, smp_d, (const double *)smp_b, (long long)n,
+                               TILE_LOG2 + p, ap, pp, list));
+        else
+            GNS_TRY(launch_pdl("omit_prep_kernel", omit_prep_kernel<false>, cgrid, 256, 0, st, keys,
+                               (uint32_t *)nullptr, (const double *)bk, (const uint32_t *)nullptr, smp_d,
+                               (const double *)smp_b, (long long)n, TILE_LOG2 + p, ap, pp, list));
+        MergeGeo g0 = uniform_geo(keys, vals, bk, bv, n, L, smp_d, smp_b);
+        MergeGeo g1 = uniform_geo(bk, bv, keys, vals, n, L, smp_b, smp_d);
+        GNS_TRY(launch_merge_list(g0, g1, list, cnt + p, ord, st));
+    }
+    const unsigned grid = (unsigned)std::min<size_t>(ceil_div(n, 2 * 256), (size_t)num_sms() * 8);
+    if (hv)
+        return launch_pdl("omit_final_kernel", omit_final_kernel<true>, grid, 256, 0, st, keys, vals,
+                          (const double *)bk, (const uint32_t *)bv, (long long)n, (const int *)(cnt + M));
+    return launch_pdl("omit_final_kernel", omit_final_kernel<false>, grid, 256, 0, st, keys, (uint32_t *)nullptr,
+                      (const double *)bk, (const uint32_t *)nullptr, (long long)n, (const int *)(cnt + M));
 }
 
 constexpr double GNS_MIN_FRACTION = 1.0 / 64.0;
@@ -619,7 +746,9 @@ gns_status run_sort(double *keys, uint32_t *vals, size_t n, const Mode &m, unsig
         uint32_t *bv = hv ? reinterpret_cast<uint32_t *>(ws + Lo.off_v) : nullptr;
         int *corank = reinterpret_cast<int *>(ws + Lo.off_corank);
         double *smp = reinterpret_cast<double *>(ws + Lo.off_smp);
-        if (!m.limited) {
+        if (m.omit) {
+            GNS_TRY(sort_omit(keys, vals, n, ws, Lo, ord, st));
+        } else if (!m.limited) {
             unsigned *unsorted = reinterpret_cast<unsigned *>(ws + Lo.off_adapt);
             GNS_TRY(sort_range(keys, vals, bk, bv, n, false, corank, ord, st, unsorted, smp, smp + Lo.nsmp));
         } else {
@@ -634,10 +763,11 @@ gns_status run_sort(double *keys, uint32_t *vals, size_t n, const Mode &m, unsig
 }
 
 gns_status sort_alloc(double *keys, uint32_t *vals, bool hv, size_t n, double frac, int target, cudaStream_t st,
-                      int kt = KT_F64)
+                      int kt = KT_F64, bool omit = false)
 {
     Mode m;
     GNS_TRY(mode_for(frac, n, &m));
+    m.omit = omit && !m.limited;
     GNS_TRY(validate_data(keys, vals, hv, n));
     if (n <= 1) return GNS_OK;
     const Layout Lo = layout(n, m, hv);
@@ -659,10 +789,11 @@ gns_status sort_alloc(double *keys, uint32_t *vals, bool hv, size_t n, double fr
 }
 
 gns_status sort_ws(double *keys, uint32_t *vals, bool hv, size_t n, double frac, void *ws, size_t ws_bytes,
-                   int target, cudaStream_t st, int kt = KT_F64)
+                   int target, cudaStream_t st, int kt = KT_F64, bool omit = false)
 {
     Mode m;
     GNS_TRY(mode_for(frac, n, &m));
+    m.omit = omit && !m.limited;
     GNS_TRY(validate_data(keys, vals, hv, n));
     if (n <= 1) return GNS_OK;
     const Layout Lo = layout(n, m, hv);
@@ -727,6 +858,17 @@ gns_status gns_sort_keys(void *keys, gns_key_type key_type, uint32_t *vals, size
                            (cudaStream_t)stream, (int)key_type);
     return sort_alloc(k, vals, vals != nullptr, n, buffer_fraction, (int)target, (cudaStream_t)stream,
                       (int)key_type);
+}
+
+gns_status gns_sort_omit(void *keys, gns_key_type key_type, uint32_t *vals, size_t n, gns_target target, void *ws,
+                         size_t ws_bytes, gns_stream_t stream)
+{
+    if ((int)target < 0 || (int)target > 3) return fail(GNS_ERR_INVALID_ARGUMENT, "target must be 0..3");
+    if ((int)key_type < 0 || (int)key_type > 2) return fail(GNS_ERR_INVALID_ARGUMENT, "key_type must be 0..2");
+    double *k = (double *)keys;
+    if (ws) return sort_ws(k, vals, vals != nullptr, n, 1.0, ws, ws_bytes, (int)target, (cudaStream_t)stream,
+                           (int)key_type, true);
+    return sort_alloc(k, vals, vals != nullptr, n, 1.0, (int)target, (cudaStream_t)stream, (int)key_type, true);
 }
 
 gns_status gns_plan(size_t n, double buffer_fraction, int with_vals, gns_plan_info *out)
@@ -845,7 +987,7 @@ gns_status gns_merge_two(const void *a_keys, const uint32_t *a_vals, size_t la, 
     const int grid = (int)ceil_div(ntiles, per);
     auto kern = merge_kern(hv, ord_of(false, (int)key_type));
     return launch_pdl("merge_tstore_kernel", kern, grid, WS_THREADS, ts_smem(hv), st, pg, ntiles, per, map, amap, bmap,
-                      Adapt{});
+                      Adapt{}, OmitList{}, map, amap, bmap);
 }
 
 gns_status gns_split_cuts(const void *sorted_keys, gns_key_type key_type, size_t n, const void *spl_keys,

@@ -71,6 +71,8 @@ __device__ __forceinline__ unsigned long long gtimer()
 constexpr int NT = 256;            // merge threads per CTA
 constexpr int VT = 16;             // outputs per merge thread
 constexpr int MTILE = NT * VT;     // K3/K4 output tile = 4096 elements
+constexpr int MTILE_LOG2 = 12;
+static_assert((1 << MTILE_LOG2) == MTILE, "MTILE_LOG2");
 #ifndef GNS_NT1
 #define GNS_NT1 256
 #endif
@@ -761,10 +763,24 @@ __device__ void adapt_move(const MergeGeo &g, int per_cta, const double *sk, con
 
 constexpr int WS_THREADS = NT + 32 + 32 * SEARCH_WARPS;   // 352
 
-template <bool HV, int ORD, int NS = 2>
+// NEXT f2 Omitsort (OL = true): the pass merges only the tiles listed in
+// ol.tiles[0:*ol.count) (ascending; every tile of a listed pair), split
+// evenly over the grid on the device.  Bit 31 (OMIT_DIR) of an entry selects the
+// direction: 0 = pg (data -> buffer) with omap/amap/bmap, 1 = ol.pg1 (buffer
+// -> data) with omap1/amap1/bmap1.
+constexpr unsigned OMIT_DIR = 1u << 31;        // list-entry bit: buffer -> data
+struct OmitList {
+    const int *tiles;
+    const int *count;
+    PipeGeo pg1;
+};
+
+template <bool HV, int ORD, int NS = 2, bool OL = false>
 __global__ void __launch_bounds__(WS_THREADS, 2)
 merge_tstore_kernel(PipeGeo pg, int ntiles, int per_cta, const __grid_constant__ CUtensorMap omap,
-                    const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap bmap, Adapt ad)
+                    const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap bmap, Adapt ad,
+                    const OmitList ol, const __grid_constant__ CUtensorMap omap1,
+                    const __grid_constant__ CUtensorMap amap1, const __grid_constant__ CUtensorMap bmap1)
 {
 #ifdef GNS_PROF
     unsigned long long acc[16] = {};
@@ -795,11 +811,26 @@ merge_tstore_kernel(PipeGeo pg, int ntiles, int per_cta, const __grid_constant__
     };
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
+    int nlist = ntiles;
+    if (OL) {
+        nlist = *ol.count;
+        per_cta = (nlist + (int)gridDim.x - 1) / (int)gridDim.x;
+    }
     const int first = blockIdx.x * per_cta;
-    const int last = min(first + per_cta, ntiles);
+    const int last = min(first + per_cta, nlist);
     const int m = last - first;
     if (m <= 0) return;
-    const int nspl = (last < ntiles) ? m + 1 : m;
+    // the CTA's j-th tile; j = m: the tile after its last one (its split ends the last tile)
+    auto entry = [&](int j) -> int { return ol.tiles[first + min(j, m - 1)]; };
+    auto tile_of = [&](int j) -> int {
+        if (!OL) return first + j;
+        const int e = (int)((unsigned)entry(j) & ~OMIT_DIR);
+        return j < m ? e : e + 1;
+    };
+    // direction of the CTA's j-th tile (j = m: the last tile's)
+    auto rev = [&](int j) -> bool { return OL && ((unsigned)entry(j) & OMIT_DIR) != 0u; };
+    auto geo = [&](int j) -> const PipeGeo & { return rev(j) ? ol.pg1 : pg; };
+    const int nspl = (tile_of(m - 1) + 1 < ntiles) ? m + 1 : m;
     for (int j = tid; j < SPL_RING; j += WS_THREADS) spl_tag[j] = -1;
     if (tid == 0) {
 #pragma unroll
@@ -819,7 +850,7 @@ merge_tstore_kernel(PipeGeo pg, int ntiles, int per_cta, const __grid_constant__
     // the first splits: every warp computes one (32-lane sample-guided search)
     const int init = min(nspl, WS_THREADS / 32);
     if (warp < init) {
-        const int c = tile_corank<32, ORD>(pg.g, first + warp, lane, 0xFFFFFFFFu, 0);
+        const int c = tile_corank<32, ORD>(geo(warp).g, tile_of(warp), lane, 0xFFFFFFFFu, 0);
         if (lane == 0) publish(warp, c);
     }
 #ifdef GNS_PROF
@@ -849,7 +880,7 @@ merge_tstore_kernel(PipeGeo pg, int ntiles, int per_cta, const __grid_constant__
             const int j = j0 + h;
             while (j0 + 1 - spl_used >= SPL_RING) { __nanosleep(64); }
             if (j < nspl) {
-                const int c = tile_corank<16, ORD>(pg.g, first + j, gl, mask, 16 * h);
+                const int c = tile_corank<16, ORD>(geo(j).g, tile_of(j), gl, mask, 16 * h);
                 if (gl == 0) publish(j, c);
             }
             __syncwarp();
@@ -873,7 +904,9 @@ merge_tstore_kernel(PipeGeo pg, int ntiles, int per_cta, const __grid_constant__
         };
         auto issue = [&](int i) {
             const int st = i % NS;
-            pipe_issue<HV>(pg, amap, bmap, first + i, get_split(i), (i + 1 < nspl) ? get_split(i + 1) : 0, skb(st), svb(st),
+            const bool r = rev(i);
+            pipe_issue<HV>(geo(i), r ? amap1 : amap, r ? bmap1 : bmap, tile_of(i), get_split(i),
+                           (i + 1 < nspl) ? get_split(i + 1) : 0, skb(st), svb(st),
                            &full[st], &meta[st], policy);
             spl_used = i;
         };
@@ -888,7 +921,7 @@ merge_tstore_kernel(PipeGeo pg, int ntiles, int per_cta, const __grid_constant__
             GNS_PT(p1);
             GNS_PADD(1, p1 - p0);
             if (pg.g.n >= 16) {        // (n < 16: no full row; the merge warps stored the partial row)
-                tma_store_2d(&omap, skb(st), 0, (int)((long long)(first + i) * (MTILE / 16)));
+                tma_store_2d(rev(i) ? &omap1 : &omap, skb(st), 0, (int)((long long)tile_of(i) * (MTILE / 16)));
                 bulk_commit();
             }
             if (i + NS < m) {
@@ -933,10 +966,11 @@ merge_tstore_kernel(PipeGeo pg, int ntiles, int per_cta, const __grid_constant__
         const int ii = merge_path_stage<ORD>(kbase, mt.offa, mt.ca, mt.bslot, mt.cb, d);
         serial_merge_stage<HV, ORD>(kbase, sv, mt, mt.offa + ii, mt.offa + mt.ca, mt.bslot + d - ii, mt.bslot + mt.cb, k,
                                     v);
-        const long long t = first + i;
+        const long long t = tile_of(i);
+        const MergeGeo &G = geo(i).g;
         const long long row = t * (MTILE / 16) + tid;    // global row of this thread's 16 outputs
-        if (pg.g.so != nullptr && (tid & (SMP_G / VT - 1)) == 0 && d < cnt)
-            pg.g.so[(row * 16) >> SMP_LOG2] = k[0];      // sample of output position row*16
+        if (G.so != nullptr && (tid & (SMP_G / VT - 1)) == 0 && d < cnt)
+            G.so[(row * 16) >> SMP_LOG2] = k[0];      // sample of output position row*16
         bar_merge_warps();                               // stage st fully read
         unsigned char *rowp = reinterpret_cast<unsigned char *>(sk) + tid * 128;
 #pragma unroll
@@ -946,17 +980,17 @@ merge_tstore_kernel(PipeGeo pg, int ntiles, int per_cta, const __grid_constant__
             const int mv = cnt - d;
             if (mv >= VT) {
 #pragma unroll
-                for (int x = 0; x < VT; x += 8) st_v8(pg.g.ov + row * 16 + x, &v[x]);
+                for (int x = 0; x < VT; x += 8) st_v8(G.ov + row * 16 + x, &v[x]);
             } else {
 #pragma unroll
                 for (int x = 0; x < VT; ++x)
-                    if (x < mv) pg.g.ov[row * 16 + x] = v[x];
+                    if (x < mv) G.ov[row * 16 + x] = v[x];
             }
         }
         if (row == full_rows && d < cnt) {                  // the partial last row (n % 16 != 0)
 #pragma unroll
             for (int x = 0; x < VT; ++x)
-                if (x < cnt - d) pg.g.ok[row * 16 + x] = k[x];
+                if (x < cnt - d) G.ok[row * 16 + x] = k[x];
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&staged[st]);
@@ -1234,6 +1268,11 @@ tile_sort2_kernel(const double *src_k, const uint32_t *src_v, double *dst_k, uin
     }
     if (smp != nullptr && e0 < cnt && (tid & (SMP_G / VT1 - 1)) == 0)
         smp[(base + e0) >> SMP_LOG2] = k[0];          // sample of output position base + e0
+    if (mode == 1 && dst_k == src_k) {                // in place and in order: nothing moves (Omitsort)
+        GNS_TL_END(0);
+        pdl_trigger();
+        return;
+    }
     if (full) {
 #pragma unroll
         for (int c = 0; c < VT1 / 2; ++c) sts128(sk + tk_slot(e0 + 2 * c), k[2 * c], k[2 * c + 1]);
@@ -1433,6 +1472,202 @@ merge_inplace_kernel(PipeGeo pg, int ntiles, const int *__restrict__ corank, con
     pdl_trigger();
 }
 
+
+// ------------------------------ NEXT f2: Omitsort with run-location tracking
+// PAPER.md:228 (§Full adaptivity): "the merge function simply returns the
+// location of the data and the sort function checks whether after its two
+// merges the data are in the same memory region, if not, it copies one to the
+// data region ... diagnosing presortedness as non-overlap of the two input
+// sequences".  Level-p runs (L = TILE << p keys, the last one shorter) each
+// live in the data (0) or the buffer (1) region.  Pair q = runs 2q, 2q+1:
+//   * no B run: the run is carried, location kept (no move);
+//   * locations differ: the buffer-resident run is copied to the data region;
+//   * B[0] not before A[L-1] (non-overlap): the merge is omitted, location
+//     kept; else both runs are merged into the other region.
+// Every decision depends only on the run boundaries: a merged run starts with
+// the smaller and ends with the larger of its runs' first / last keys (only
+// comparisons are made, so which of two equal keys is irrelevant).  So one
+// CTA plans all levels right after the tile sort (omit_plan_kernel): per level
+// p and pair q an action byte act[p][q] (OMIT_COPY_A / OMIT_COPY_B: move that
+// run from the buffer to the data region; OMIT_MERGE: merge the pair, from the
+// buffer to the data region if OMIT_REV, else the other way) and the
+// exclusive prefix pre[p][q] of merge tiles over the level's pairs, plus each
+// level's merge-tile count.  Per level, omit_prep_kernel (all SMs) writes the
+// merge-tile list (ascending, OMIT_DIR = buffer -> data) and does the copies;
+// one list-driven merge launch follows.
+constexpr int OMIT_THREADS = 1024;
+constexpr int OMIT_SMEM_RUNS = 2048;            // run state in shared memory up to 2048 level-0 runs (2^24 keys)
+constexpr size_t OMIT_SMEM = 34 * OMIT_SMEM_RUNS;
+constexpr unsigned OMIT_COPY_A = 1u, OMIT_COPY_B = 2u, OMIT_MERGE = 4u, OMIT_REV = 8u;
+struct OmitState {                  // per-run state of two levels (ping-pong), scratch
+    unsigned char *loc[2];
+    double *first[2];
+    double *last[2];
+};
+template <int ORD>
+__global__ void __launch_bounds__(OMIT_THREADS)
+omit_plan_kernel(const double *dk, long long n, int levels, OmitState S, unsigned char *act, int *pre, int *counts)
+{
+    pdl_wait();
+    __shared__ int wsum[OMIT_THREADS / 32];
+    __shared__ int carry;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const unsigned un = (unsigned)n;            // n < 2^31: positions fit 32 bits (unsigned: a0 + 2L < 2^32)
+    // level 0: the tile-sorted runs, all in the data region
+    const int nr0 = (int)((n + TILE - 1) / TILE);
+    extern __shared__ __align__(16) unsigned char omit_smem[];
+    if (nr0 <= OMIT_SMEM_RUNS) {            // small sorts: the run state in shared memory
+        double *f = reinterpret_cast<double *>(omit_smem);
+        S.first[0] = f;
+        S.first[1] = f + OMIT_SMEM_RUNS;
+        S.last[0] = f + 2 * OMIT_SMEM_RUNS;
+        S.last[1] = f + 3 * OMIT_SMEM_RUNS;
+        S.loc[0] = omit_smem + 32 * OMIT_SMEM_RUNS;
+        S.loc[1] = S.loc[0] + OMIT_SMEM_RUNS;
+    }
+    for (int r = tid; r < nr0; r += OMIT_THREADS) {
+        S.loc[0][r] = 0;
+        S.first[0][r] = dk[(long long)r * TILE];
+        S.last[0][r] = dk[min(n, (long long)(r + 1) * TILE) - 1];
+    }
+    __syncthreads();
+    int off = 0, cur = 0;
+    for (int p = 0; p < levels; ++p) {
+        const unsigned L = (unsigned)TILE << p;
+        const int npairs = (int)((n + 2 * (long long)L - 1) / (2 * (long long)L));
+        const unsigned tpp = 2 * L / MTILE;     // merge tiles per full pair
+        if (tid == 0) carry = 0;
+        __syncthreads();
+        for (int c0 = 0; c0 < npairs; c0 += OMIT_THREADS) {
+            const int q = c0 + tid;
+            int nt = 0;
+            unsigned a = 0;
+            if (q < npairs) {
+                const unsigned a0 = 2u * (unsigned)q * L, b0 = a0 + L;
+                unsigned la = S.loc[cur][2 * q];
+                unsigned lo = la;
+                double fst = S.first[cur][2 * q], lst = S.last[cur][2 * q];
+                if (b0 < un) {
+                    const unsigned lb = S.loc[cur][2 * q + 1];
+                    const double bf = S.first[cur][2 * q + 1], bl = S.last[cur][2 * q + 1];
+                    if (la != lb) {      // copy the buffer-resident run to the data region
+                        a = la ? OMIT_COPY_A : OMIT_COPY_B;
+                        la = 0;
+                    }
+                    if (before<ORD>(bf, lst)) {             // overlap: merge into the other region
+                        lo = la ^ 1u;
+                        a |= OMIT_MERGE | (la ? OMIT_REV : 0u);
+                        nt = (int)min(tpp, (un - a0 + MTILE - 1) / MTILE);
+                    } else {
+                        lo = la;                            // omitted (0 moves)
+                    }
+                    if (before<ORD>(bf, fst)) fst = bf;
+                    if (!before<ORD>(bl, lst)) lst = bl;
+                }
+                S.loc[cur ^ 1][q] = (unsigned char)lo;
+                S.first[cur ^ 1][q] = fst;
+                S.last[cur ^ 1][q] = lst;
+                act[off + q] = (unsigned char)a;
+            }
+            int x = nt;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+                if (lane >= o) x += y;
+            }
+            if (lane == 31) wsum[warp] = x;
+            __syncthreads();
+            if (warp == 0) {
+                int w = wsum[lane];
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int y = __shfl_up_sync(0xFFFFFFFFu, w, o);
+                    if (lane >= o) w += y;
+                }
+                wsum[lane] = w;
+            }
+            __syncthreads();
+            if (q < npairs) pre[off + q] = carry + x - nt + (warp ? wsum[warp - 1] : 0);
+            __syncthreads();
+            if (tid == 0) carry += wsum[OMIT_THREADS / 32 - 1];
+            __syncthreads();
+        }
+        if (tid == 0) counts[p] = carry;
+        off += npairs;
+        cur ^= 1;
+        __syncthreads();                        // the level's state is complete
+    }
+    if (tid == 0) counts[levels] = S.loc[cur][0];  // the sorted run's region
+    pdl_trigger();
+}
+
+// Per level (run length L = 1 << lg), one pass over the merge tiles on all
+// SMs: tile t of a merging pair q goes to list[pre[q] + t - first tile of q]
+// (with OMIT_DIR for buffer -> data), and a tile of a run to be moved is
+// copied from the buffer to the data region (keys, vals and the run's
+// split-search samples).
+template <bool HV>
+__global__ void __launch_bounds__(256)
+omit_prep_kernel(double *dk, uint32_t *dv, const double *bk, const uint32_t *bv, double *smp_d, const double *smp_b,
+                 long long n, int lg, const unsigned char *act, const int *pre, int *list)
+{
+    pdl_trigger();          // (the merge launch may become resident early; it waits for this grid to finish)
+    pdl_wait();
+    const int ntiles = (int)((n + MTILE - 1) / MTILE);
+    const int tq_log2 = lg + 1 - MTILE_LOG2;                       // tiles per pair = 1 << tq_log2
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < ntiles; t += gridDim.x * blockDim.x) {
+        const int q = t >> tq_log2;
+        const unsigned a = act[q];
+        if (a & OMIT_MERGE)
+            list[pre[q] + (t & ((1 << tq_log2) - 1))] = (int)((unsigned)t | ((a & OMIT_REV) ? OMIT_DIR : 0u));
+    }
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const long long s0 = (long long)t * MTILE;
+        const unsigned a = act[t >> tq_log2];
+        const bool in_a = ((s0 >> lg) & 1) == 0;
+        if (!((a & OMIT_COPY_A) && in_a) && !((a & OMIT_COPY_B) && !in_a)) continue;
+        const long long e = min(n, s0 + MTILE);
+        if (e - s0 == MTILE) {             // full tile: 16-byte vectors (regions are 32-byte aligned)
+            const double2 *src = reinterpret_cast<const double2 *>(bk + s0);
+            double2 *dst = reinterpret_cast<double2 *>(dk + s0);
+            for (int i = threadIdx.x; i < MTILE / 2; i += blockDim.x) dst[i] = src[i];
+            if (HV) {
+                const uint4 *vs = reinterpret_cast<const uint4 *>(bv + s0);
+                uint4 *vd = reinterpret_cast<uint4 *>(dv + s0);
+                for (int i = threadIdx.x; i < MTILE / 4; i += blockDim.x) vd[i] = vs[i];
+            }
+        } else {
+            for (long long i = s0 + threadIdx.x; i < e; i += blockDim.x) {
+                dk[i] = bk[i];
+                if (HV) dv[i] = bv[i];
+            }
+        }
+        for (long long i = ((s0 + SMP_G - 1) >> SMP_LOG2) + threadIdx.x; (i << SMP_LOG2) < e; i += blockDim.x)
+            smp_d[i] = smp_b[i];
+    }
+}
+
+// The sorted run ends in the buffer (odd number of region changes): copy it
+// back to the data region.  `loc` = the top-level run's location.
+template <bool HV>
+__global__ void __launch_bounds__(256)
+omit_final_kernel(double *dk, uint32_t *dv, const double *bk, const uint32_t *bv, long long n,
+                  const int *loc)
+{
+    pdl_wait();
+    if (*loc != 0) {
+        const long long n2 = n >> 1;
+        const double2 *src = reinterpret_cast<const double2 *>(bk);
+        double2 *dst = reinterpret_cast<double2 *>(dk);
+        const long long stride = (long long)gridDim.x * blockDim.x;
+        for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n2; i += stride) dst[i] = src[i];
+        if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) dk[n - 1] = bk[n - 1];
+        if (HV) {
+            for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += stride) dv[i] = bv[i];
+        }
+    }
+    pdl_trigger();
+}
 
 // ------------------------------------- target reversal (NEXT f3, AscRight/DescRight)
 // AscRight = reverse(DescLeft), DescRight = reverse(AscLeft) (PAPER.md:137-142:

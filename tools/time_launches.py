@@ -15,9 +15,11 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--n", type=int, default=27)
 ap.add_argument("--pairs", action="store_true")
 ap.add_argument("--frac", type=float, default=0.5)
+ap.add_argument("--omit", action="store_true")
+ap.add_argument("--input", default="uniform")
 a = ap.parse_args()
 n = 1 << a.n
-src = torch.from_numpy(synth.uniform(n, 9)).cuda()
+src = torch.from_numpy(synth.uniform(n, 9) if a.input == "uniform" else synth.config(4, a.input, n).keys).cuda()
 srcv = torch.from_numpy(synth.iota_u32(n)).cuda() if a.pairs else None
 k = torch.empty_like(src)
 v = torch.empty_like(srcv) if a.pairs else None
@@ -28,7 +30,10 @@ for i in range(3):
     if a.pairs:
         v.copy_(srcv)
     assert gns.gns_timing_begin(512) == 0
-    gns.sort_(k, v, a.frac, workspace=ws)
+    if a.omit:
+        gns.sort_omit_(k, v, workspace=ws)
+    else:
+        gns.sort_(k, v, a.frac, workspace=ws)
     per.append(gns.gns_timing_end())
 kinds = [gns.LAUNCH_KINDS.get(kd, "?") for kd, _ in per[-1]]
 med = [float(np.median([r[j][1] for r in per[1:]])) for j in range(len(kinds))]
