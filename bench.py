@@ -487,29 +487,39 @@ def footprint_cfg5(gns, torch, dev, stream, flush, reps=3):
 
 
 def config4(gns, torch, dev, stream, flush, reps=5):
-    """configs[3]: n = 2^24 presorted patterns, key-only, buffer 1.0.  Fully
-    ordered input takes the NEXT-f2 omission path (no merge pass moves data);
-    the others sort normally."""
+    """configs[3]: n = 2^24 presorted patterns, key-only, buffer 1.0, through
+    the default schedule (``sort_``: a fully ordered or strictly reversed
+    input skips the merge passes on the device) and through the Omitsort
+    schedule (``sort_omit_``, NEXT f2: per-pair omission with run-location
+    tracking)."""
     out = {}
     n = 1 << 24
     ws = gns.alloc_workspace(n, 1.0, False, dev)
     for sub in synth.CONFIG4_SUBS:
         src = torch.from_numpy(synth.config(4, sub).keys).to(dev)
         k = torch.empty_like(src)
-        ts = []
-        for i in range(reps + 1):
-            k.copy_(src)
-            flush.fill_(1)
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            gns.sort_(k, None, 1.0, workspace=ws)
-            b.record(stream)
-            torch.cuda.synchronize()
-            if i:
-                ts.append(a.elapsed_time(b))
-        ok = bool((k[1:] >= k[:-1]).all().item())
-        ms = float(np.median(ts))
-        out[sub] = {"ms": ms, "keys_per_s": n / (ms / 1e3), "sorted": ok}
+        for sched in ("default", "omit"):
+            ts = []
+            for i in range(reps + 1):
+                k.copy_(src)
+                flush.fill_(1)
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                if sched == "omit":
+                    gns.sort_omit_(k, None, workspace=ws)
+                else:
+                    gns.sort_(k, None, 1.0, workspace=ws)
+                b.record(stream)
+                torch.cuda.synchronize()
+                if i:
+                    ts.append(a.elapsed_time(b))
+            ok = bool((k[1:] >= k[:-1]).all().item())
+            ms = float(np.median(ts))
+            r = {"ms": ms, "keys_per_s": n / (ms / 1e3), "sorted": ok}
+            if sched == "omit":
+                out[sub]["omit"] = r
+            else:
+                out[sub] = r
     return out
 
 
