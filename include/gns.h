@@ -142,7 +142,11 @@ gns_status gns_sort_keys(void *keys, gns_key_type key_type, uint32_t *vals, size
  * presorted input (long ascending runs) moves only where runs overlap; random
  * input costs one copy pass more than gns_sort_keys when the number of merge
  * levels is odd, plus ~10 us of planning per level.  Arguments, alignment and
- * errors as gns_sort_keys (ws may be NULL: allocated stream-ordered). */
+ * errors as gns_sort_keys (ws may be NULL: allocated stream-ordered).
+ * Octosort in the same schedule: a strictly reversed tile is
+ * kept as a descending run, disjoint descending runs stay descending, a
+ * descending run meeting anything else is reversed once; a descending result
+ * is reversed at the end (strictly reversed input: one reversal pass). */
 gns_status gns_sort_omit(void *keys, gns_key_type key_type, uint32_t *vals, size_t n, gns_target target, void *ws,
                          size_t ws_bytes, gns_stream_t stream);
 

@@ -74,7 +74,7 @@ struct Layout {
     // NEXT f2 Omitsort (full buffer only): run state of two levels (location,
     // first and last key), per level and pair the copy flag, per level the
     // merge tile list and its length (+ the sorted run's region)
-    size_t off_loc = 0, off_fl = 0, off_fix = 0, off_pre = 0, off_list = 0, off_cnt = 0;
+    size_t off_loc = 0, off_fl = 0, off_fix = 0, off_pre = 0, off_list = 0, off_cnt = 0, off_tdesc = 0;
     size_t nruns = 0, npairs = 0;
 };
 
@@ -113,6 +113,8 @@ Layout layout(size_t n, const Mode &m, bool hv)
         L.nruns = ceil_div(n, TILE);
         L.npairs = ceil_div(n, 2 * (size_t)TILE);
         const size_t M = (size_t)merge_passes_for(n);
+        L.off_tdesc = o;                                    // per tile: kept as a descending run (Octosort)
+        o = align_up(o + L.nruns, 256);
         L.off_loc = o;
         o = align_up(o + 2 * L.nruns, 256);
         L.off_fl = o;
@@ -348,7 +350,8 @@ gns_status launch_pdl(const char *what, void (*kern)(KArgs...), dim3 grid, dim3 
 
 // Row a2 (K1).
 gns_status launch_tile_sort(const double *sk, const uint32_t *sv, double *dk, uint32_t *dv, size_t n, int ord,
-                            cudaStream_t st, unsigned *unsorted = nullptr, double *smp = nullptr)
+                            cudaStream_t st, unsigned *unsorted = nullptr, double *smp = nullptr,
+                            unsigned char *tdesc = nullptr)
 {
     if (n == 0) return GNS_OK;
     const unsigned grid = (unsigned)ceil_div(n, TILE);
@@ -367,7 +370,7 @@ gns_status launch_tile_sort(const double *sk, const uint32_t *sv, double *dk, ui
     uint32_t *dvv = hv ? dv : nullptr;
     auto kern = tile_kern(hv, ord);
     return launch_pdl("tile_sort2_kernel", kern, grid, NT1, t1_smem(hv), st, sk, svv, dk, dvv, (long long)n, m[0],
-                      m[1], m[2], m[3], unsorted, smp);
+                      m[1], m[2], m[3], unsorted, smp, tdesc);
 }
 
 // Rows a3+a4 (fused K2+K3, persistent TMA pipeline) or, in place, a6 (K2 +
@@ -555,22 +558,23 @@ gns_status sort_omit(double *keys, uint32_t *vals, size_t n, unsigned char *ws, 
     double *smp_d = reinterpret_cast<double *>(ws + Lo.off_smp);
     double *smp_b = smp_d + Lo.nsmp;
     OmitState S;
-    S.loc[0] = ws + Lo.off_loc;
-    S.loc[1] = S.loc[0] + Lo.nruns;
+    S.st[0] = ws + Lo.off_loc;
+    S.st[1] = S.st[0] + Lo.nruns;
     double *fl = reinterpret_cast<double *>(ws + Lo.off_fl);
-    S.first[0] = fl;
-    S.first[1] = fl + Lo.nruns;
-    S.last[0] = fl + 2 * Lo.nruns;
-    S.last[1] = fl + 3 * Lo.nruns;
+    S.lo[0] = fl;
+    S.lo[1] = fl + Lo.nruns;
+    S.hi[0] = fl + 2 * Lo.nruns;
+    S.hi[1] = fl + 3 * Lo.nruns;
+    unsigned char *tdesc = ws + Lo.off_tdesc;
     unsigned char *act = ws + Lo.off_fix;
     int *pre = reinterpret_cast<int *>(ws + Lo.off_pre);
     int *list = reinterpret_cast<int *>(ws + Lo.off_list);
     int *cnt = reinterpret_cast<int *>(ws + Lo.off_cnt);
     const int M = merge_passes_for(n);
-    GNS_TRY(launch_tile_sort(keys, vals, keys, vals, n, ord, st, nullptr, smp_d));
+    GNS_TRY(launch_tile_sort(keys, vals, keys, vals, n, ord, st, nullptr, smp_d, tdesc));
     GNS_TRY(launch_pdl("omit_plan_kernel", omit_plan_kern(ord), 1, OMIT_THREADS,
-                       Lo.nruns <= (size_t)OMIT_SMEM_RUNS ? OMIT_SMEM : 0, st, (const double *)keys, (long long)n, M,
-                       S, act, pre, cnt));
+                       Lo.nruns <= (size_t)OMIT_SMEM_RUNS ? OMIT_SMEM : 0, st, (const double *)keys,
+                       (const unsigned char *)tdesc, (long long)n, M, S, act, pre, cnt));
     const unsigned cgrid = (unsigned)std::min<size_t>(ceil_div(n, MTILE), (size_t)num_sms() * 4);
     size_t off = 0;
     for (int p = 0; p < M; ++p) {
@@ -579,13 +583,12 @@ gns_status sort_omit(double *keys, uint32_t *vals, size_t n, unsigned char *ws, 
         const int *pp = pre + off;
         off += ceil_div(n, 2 * L);
         if (hv)
-            GNS_TRY(launch_pdl("omit_prep_kernel", omit_prep_kernel<true>, cgrid, 256, 0, st, keys, vals,
-                               (const double *)bk, (const uint32_t *)bv, smp_d, (const double *)smp_b, (long long)n,
-                               TILE_LOG2 + p, ap, pp, list));
+            GNS_TRY(launch_pdl("omit_prep_kernel", omit_prep_kernel<true>, cgrid, 256, 0, st, keys, vals, bk, bv,
+                               smp_d, smp_b, (long long)n, TILE_LOG2 + p, ap, pp, list));
         else
             GNS_TRY(launch_pdl("omit_prep_kernel", omit_prep_kernel<false>, cgrid, 256, 0, st, keys,
-                               (uint32_t *)nullptr, (const double *)bk, (const uint32_t *)nullptr, smp_d,
-                               (const double *)smp_b, (long long)n, TILE_LOG2 + p, ap, pp, list));
+                               (uint32_t *)nullptr, bk, (uint32_t *)nullptr, smp_d, smp_b, (long long)n,
+                               TILE_LOG2 + p, ap, pp, list));
         MergeGeo g0 = uniform_geo(keys, vals, bk, bv, n, L, smp_d, smp_b);
         MergeGeo g1 = uniform_geo(bk, bv, keys, vals, n, L, smp_b, smp_d);
         GNS_TRY(launch_merge_list(g0, g1, list, cnt + p, ord, st));

@@ -1120,7 +1120,7 @@ __global__ void __launch_bounds__(NT1, GNS_T1_MINB)
 tile_sort2_kernel(const double *src_k, const uint32_t *src_v, double *dst_k, uint32_t *dst_v, long long n,
                   const __grid_constant__ CUtensorMap ksrc, const __grid_constant__ CUtensorMap vsrc,
                   const __grid_constant__ CUtensorMap kdst, const __grid_constant__ CUtensorMap vdst,
-                  unsigned *unsorted, double *smp)
+                  unsigned *unsorted, double *smp, unsigned char *tdesc)
 {
     pdl_wait();
     GNS_TL_START(0);
@@ -1237,6 +1237,15 @@ tile_sort2_kernel(const double *src_k, const uint32_t *src_v, double *dst_k, uin
     }
     } else {
         __syncthreads();                   // the TMA-layout reads are done before the staging writes
+    }
+    if (tdesc != nullptr && tid == 0) tdesc[tile] = (mode == 2) ? 1 : 0;
+    if (mode == 2 && tdesc != nullptr && dst_k == src_k) {
+        // Octosort (NEXT f2): the strictly reversed tile
+        // stays as it is, a descending run (its reversal is its stable sort)
+        if (smp != nullptr && (tid & (SMP_G / VT1 - 1)) == 0) smp[(base + e0) >> SMP_LOG2] = k[0];
+        GNS_TL_END(0);
+        pdl_trigger();
+        return;
     }
     if (mode == 2) {
         // full tile, strictly reversed: output position TILE-1-e gets input e
@@ -1484,29 +1493,43 @@ merge_inplace_kernel(PipeGeo pg, int ntiles, const int *__restrict__ corank, con
 //   * locations differ: the buffer-resident run is copied to the data region;
 //   * B[0] not before A[L-1] (non-overlap): the merge is omitted, location
 //     kept; else both runs are merged into the other region.
-// Every decision depends only on the run boundaries: a merged run starts with
-// the smaller and ends with the larger of its runs' first / last keys (only
-// comparisons are made, so which of two equal keys is irrelevant).  So one
-// CTA plans all levels right after the tile sort (omit_plan_kernel): per level
-// p and pair q an action byte act[p][q] (OMIT_COPY_A / OMIT_COPY_B: move that
-// run from the buffer to the data region; OMIT_MERGE: merge the pair, from the
-// buffer to the data region if OMIT_REV, else the other way) and the
-// exclusive prefix pre[p][q] of merge tiles over the level's pairs, plus each
-// level's merge-tile count.  Per level, omit_prep_kernel (all SMs) writes the
-// merge-tile list (ascending, OMIT_DIR = buffer -> data) and does the copies;
-// one list-driven merge launch follows.
+// Every decision depends only on the run boundaries: a merged run's smallest
+// and largest key are the smaller / larger of its runs' (only comparisons are
+// made, so which of two equal keys is irrelevant).  So one CTA plans all
+// levels right after the tile sort (omit_plan_kernel).  Run state: region
+// (data / buffer), direction (ascending, or strictly descending = Octosort's
+// lazily kept reversed run: its reversal is its stable sort),
+// smallest and largest key.  Pair (A, B):
+//   * no B run: carried unchanged;
+//   * both descending and every key of B strictly before every key of A:
+//     A ++ B is strictly descending -- omitted as a descending run (after
+//     copying the buffer-resident one to the data region if they differ);
+//   * else each descending run is reversed (in place, or while it is copied),
+//     the buffer-resident run is copied to the data region if the regions
+//     differ, then the pair is omitted if B's smallest key is not
+//     before A's largest, else merged into the other region.
+// Per level p and pair q: an action byte act[p][q] and the exclusive prefix
+// pre[p][q] of merge tiles over the level's pairs; per level the merge-tile
+// count; at the end the sorted run's state.  Per level, omit_prep_kernel (all
+// SMs) writes the merge-tile list (ascending, OMIT_DIR = buffer -> data),
+// reverses and copies runs; one list-driven merge launch follows.
 constexpr int OMIT_THREADS = 1024;
 constexpr int OMIT_SMEM_RUNS = 2048;            // run state in shared memory up to 2048 level-0 runs (2^24 keys)
 constexpr size_t OMIT_SMEM = 34 * OMIT_SMEM_RUNS;
-constexpr unsigned OMIT_COPY_A = 1u, OMIT_COPY_B = 2u, OMIT_MERGE = 4u, OMIT_REV = 8u;
+// action byte: copy A / B from the buffer to the data region, merge (buffer ->
+// data if OMIT_REV), reverse A / B, A / B currently in the buffer
+constexpr unsigned OMIT_COPY_A = 1u, OMIT_COPY_B = 2u, OMIT_MERGE = 4u, OMIT_REV = 8u, OMIT_FLIP_A = 16u,
+                   OMIT_FLIP_B = 32u, OMIT_BUF_A = 64u, OMIT_BUF_B = 128u;
+constexpr unsigned OMIT_ST_BUF = 1u, OMIT_ST_DESC = 2u;   // run state bits
 struct OmitState {                  // per-run state of two levels (ping-pong), scratch
-    unsigned char *loc[2];
-    double *first[2];
-    double *last[2];
+    unsigned char *st[2];           // OMIT_ST_BUF | OMIT_ST_DESC
+    double *lo[2];                  // smallest key (target order)
+    double *hi[2];                  // largest key
 };
 template <int ORD>
 __global__ void __launch_bounds__(OMIT_THREADS)
-omit_plan_kernel(const double *dk, long long n, int levels, OmitState S, unsigned char *act, int *pre, int *counts)
+omit_plan_kernel(const double *dk, const unsigned char *tdesc, long long n, int levels, OmitState S,
+                 unsigned char *act, int *pre, int *counts)
 {
     pdl_wait();
     __shared__ int wsum[OMIT_THREADS / 32];
@@ -1518,17 +1541,19 @@ omit_plan_kernel(const double *dk, long long n, int levels, OmitState S, unsigne
     extern __shared__ __align__(16) unsigned char omit_smem[];
     if (nr0 <= OMIT_SMEM_RUNS) {            // small sorts: the run state in shared memory
         double *f = reinterpret_cast<double *>(omit_smem);
-        S.first[0] = f;
-        S.first[1] = f + OMIT_SMEM_RUNS;
-        S.last[0] = f + 2 * OMIT_SMEM_RUNS;
-        S.last[1] = f + 3 * OMIT_SMEM_RUNS;
-        S.loc[0] = omit_smem + 32 * OMIT_SMEM_RUNS;
-        S.loc[1] = S.loc[0] + OMIT_SMEM_RUNS;
+        S.lo[0] = f;
+        S.lo[1] = f + OMIT_SMEM_RUNS;
+        S.hi[0] = f + 2 * OMIT_SMEM_RUNS;
+        S.hi[1] = f + 3 * OMIT_SMEM_RUNS;
+        S.st[0] = omit_smem + 32 * OMIT_SMEM_RUNS;
+        S.st[1] = S.st[0] + OMIT_SMEM_RUNS;
     }
     for (int r = tid; r < nr0; r += OMIT_THREADS) {
-        S.loc[0][r] = 0;
-        S.first[0][r] = dk[(long long)r * TILE];
-        S.last[0][r] = dk[min(n, (long long)(r + 1) * TILE) - 1];
+        const unsigned d = tdesc[r] ? OMIT_ST_DESC : 0u;
+        const double f = dk[(long long)r * TILE], l = dk[min(n, (long long)(r + 1) * TILE) - 1];
+        S.st[0][r] = (unsigned char)d;
+        S.lo[0][r] = d ? l : f;
+        S.hi[0][r] = d ? f : l;
     }
     __syncthreads();
     int off = 0, cur = 0;
@@ -1544,29 +1569,38 @@ omit_plan_kernel(const double *dk, long long n, int levels, OmitState S, unsigne
             unsigned a = 0;
             if (q < npairs) {
                 const unsigned a0 = 2u * (unsigned)q * L, b0 = a0 + L;
-                unsigned la = S.loc[cur][2 * q];
-                unsigned lo = la;
-                double fst = S.first[cur][2 * q], lst = S.last[cur][2 * q];
+                unsigned sa = S.st[cur][2 * q];
+                double lo = S.lo[cur][2 * q], hi = S.hi[cur][2 * q];
+                unsigned so = sa;
                 if (b0 < un) {
-                    const unsigned lb = S.loc[cur][2 * q + 1];
-                    const double bf = S.first[cur][2 * q + 1], bl = S.last[cur][2 * q + 1];
-                    if (la != lb) {      // copy the buffer-resident run to the data region
-                        a = la ? OMIT_COPY_A : OMIT_COPY_B;
-                        la = 0;
+                    const unsigned sb = S.st[cur][2 * q + 1];
+                    const double blo = S.lo[cur][2 * q + 1], bhi = S.hi[cur][2 * q + 1];
+                    a = ((sa & OMIT_ST_BUF) ? OMIT_BUF_A : 0u) | ((sb & OMIT_ST_BUF) ? OMIT_BUF_B : 0u);
+                    unsigned ra = sa & OMIT_ST_BUF, rb = sb & OMIT_ST_BUF;
+                    const bool desc_omit = (sa & sb & OMIT_ST_DESC) && before<ORD>(bhi, lo);
+                    if (!desc_omit) {
+                        if (sa & OMIT_ST_DESC) a |= OMIT_FLIP_A;
+                        if (sb & OMIT_ST_DESC) a |= OMIT_FLIP_B;
                     }
-                    if (before<ORD>(bf, lst)) {             // overlap: merge into the other region
-                        lo = la ^ 1u;
-                        a |= OMIT_MERGE | (la ? OMIT_REV : 0u);
+                    if (ra != rb) {      // copy the buffer-resident run to the data region
+                        a |= ra ? OMIT_COPY_A : OMIT_COPY_B;
+                        ra = 0;
+                    }
+                    if (desc_omit) {
+                        so = ra | OMIT_ST_DESC;                 // omitted, still descending
+                    } else if (before<ORD>(blo, hi)) {          // overlap: merge into the other region
+                        so = ra ^ 1u;
+                        a |= OMIT_MERGE | (ra ? OMIT_REV : 0u);
                         nt = (int)min(tpp, (un - a0 + MTILE - 1) / MTILE);
                     } else {
-                        lo = la;                            // omitted (0 moves)
+                        so = ra;                                // omitted (0 moves)
                     }
-                    if (before<ORD>(bf, fst)) fst = bf;
-                    if (!before<ORD>(bl, lst)) lst = bl;
+                    if (before<ORD>(blo, lo)) lo = blo;
+                    if (!before<ORD>(bhi, hi)) hi = bhi;
                 }
-                S.loc[cur ^ 1][q] = (unsigned char)lo;
-                S.first[cur ^ 1][q] = fst;
-                S.last[cur ^ 1][q] = lst;
+                S.st[cur ^ 1][q] = (unsigned char)so;
+                S.lo[cur ^ 1][q] = lo;
+                S.hi[cur ^ 1][q] = hi;
                 act[off + q] = (unsigned char)a;
             }
             int x = nt;
@@ -1597,19 +1631,21 @@ omit_plan_kernel(const double *dk, long long n, int levels, OmitState S, unsigne
         cur ^= 1;
         __syncthreads();                        // the level's state is complete
     }
-    if (tid == 0) counts[levels] = S.loc[cur][0];  // the sorted run's region
+    if (tid == 0) counts[levels] = S.st[cur][0];   // the sorted run's state (region, direction)
     pdl_trigger();
 }
 
 // Per level (run length L = 1 << lg), one pass over the merge tiles on all
 // SMs: tile t of a merging pair q goes to list[pre[q] + t - first tile of q]
-// (with OMIT_DIR for buffer -> data), and a tile of a run to be moved is
-// copied from the buffer to the data region (keys, vals and the run's
-// split-search samples).
+// (with OMIT_DIR for buffer -> data); a tile of a run to be moved and / or
+// reversed is processed by one CTA: plain copy buffer -> data, reversed copy
+// buffer -> data, or (first half of the run only) in-place swaps with the
+// mirrored positions in the run's region -- keys, vals and the split-search
+// samples of the touched positions.
 template <bool HV>
 __global__ void __launch_bounds__(256)
-omit_prep_kernel(double *dk, uint32_t *dv, const double *bk, const uint32_t *bv, double *smp_d, const double *smp_b,
-                 long long n, int lg, const unsigned char *act, const int *pre, int *list)
+omit_prep_kernel(double *dk, uint32_t *dv, double *bk, uint32_t *bv, double *smp_d, double *smp_b, long long n, int lg,
+                 const unsigned char *act, const int *pre, int *list)
 {
     pdl_trigger();          // (the merge launch may become resident early; it waits for this grid to finish)
     pdl_wait();
@@ -1625,45 +1661,94 @@ omit_prep_kernel(double *dk, uint32_t *dv, const double *bk, const uint32_t *bv,
         const long long s0 = (long long)t * MTILE;
         const unsigned a = act[t >> tq_log2];
         const bool in_a = ((s0 >> lg) & 1) == 0;
-        if (!((a & OMIT_COPY_A) && in_a) && !((a & OMIT_COPY_B) && !in_a)) continue;
+        const bool copy = (a & (in_a ? OMIT_COPY_A : OMIT_COPY_B)) != 0;
+        const bool flip = (a & (in_a ? OMIT_FLIP_A : OMIT_FLIP_B)) != 0;
+        if (!copy && !flip) continue;
         const long long e = min(n, s0 + MTILE);
-        if (e - s0 == MTILE) {             // full tile: 16-byte vectors (regions are 32-byte aligned)
-            const double2 *src = reinterpret_cast<const double2 *>(bk + s0);
-            double2 *dst = reinterpret_cast<double2 *>(dk + s0);
-            for (int i = threadIdx.x; i < MTILE / 2; i += blockDim.x) dst[i] = src[i];
-            if (HV) {
-                const uint4 *vs = reinterpret_cast<const uint4 *>(bv + s0);
-                uint4 *vd = reinterpret_cast<uint4 *>(dv + s0);
-                for (int i = threadIdx.x; i < MTILE / 4; i += blockDim.x) vd[i] = vs[i];
+        const long long rs = (s0 >> lg) << lg;                     // the run [rs, rs + len)
+        const long long len = min((long long)1 << lg, n - rs);
+        const long long mir = 2 * rs + len - 1;                     // position i <-> mir - i
+        if (copy && !flip) {
+            if (e - s0 == MTILE) {         // full tile: 16-byte vectors (regions are 32-byte aligned)
+                const double2 *src = reinterpret_cast<const double2 *>(bk + s0);
+                double2 *dst = reinterpret_cast<double2 *>(dk + s0);
+                for (int i = threadIdx.x; i < MTILE / 2; i += blockDim.x) dst[i] = src[i];
+                if (HV) {
+                    const uint4 *vs = reinterpret_cast<const uint4 *>(bv + s0);
+                    uint4 *vd = reinterpret_cast<uint4 *>(dv + s0);
+                    for (int i = threadIdx.x; i < MTILE / 4; i += blockDim.x) vd[i] = vs[i];
+                }
+            } else {
+                for (long long i = s0 + threadIdx.x; i < e; i += blockDim.x) {
+                    dk[i] = bk[i];
+                    if (HV) dv[i] = bv[i];
+                }
             }
-        } else {
+            for (long long i = ((s0 + SMP_G - 1) >> SMP_LOG2) + threadIdx.x; (i << SMP_LOG2) < e; i += blockDim.x)
+                smp_d[i] = smp_b[i];
+        } else if (copy) {                 // reversed copy, buffer -> data
             for (long long i = s0 + threadIdx.x; i < e; i += blockDim.x) {
-                dk[i] = bk[i];
-                if (HV) dv[i] = bv[i];
+                const double x = bk[mir - i];
+                dk[i] = x;
+                if (HV) dv[i] = bv[mir - i];
+                if ((i & (SMP_G - 1)) == 0) smp_d[i >> SMP_LOG2] = x;
+            }
+        } else {                           // in place, in the run's region; the first half swaps
+            const bool buf = (a & (in_a ? OMIT_BUF_A : OMIT_BUF_B)) != 0;
+            double *K = buf ? bk : dk;
+            uint32_t *V = buf ? bv : dv;
+            double *Sm = buf ? smp_b : smp_d;
+            const long long half = rs + len / 2;
+            for (long long i = s0 + threadIdx.x; i < min(e, half); i += blockDim.x) {
+                const long long j = mir - i;
+                const double x = K[i], y = K[j];
+                K[i] = y;
+                K[j] = x;
+                if (HV) {
+                    const uint32_t u = V[i], w = V[j];
+                    V[i] = w;
+                    V[j] = u;
+                }
+                if ((i & (SMP_G - 1)) == 0) Sm[i >> SMP_LOG2] = y;
+                if ((j & (SMP_G - 1)) == 0) Sm[j >> SMP_LOG2] = x;
             }
         }
-        for (long long i = ((s0 + SMP_G - 1) >> SMP_LOG2) + threadIdx.x; (i << SMP_LOG2) < e; i += blockDim.x)
-            smp_d[i] = smp_b[i];
     }
 }
 
-// The sorted run ends in the buffer (odd number of region changes): copy it
-// back to the data region.  `loc` = the top-level run's location.
+// The sorted run's state `st` (OMIT_ST_BUF, OMIT_ST_DESC): copy it back to the
+// data region, reverse it in place, or both (reversed copy); nothing if it is
+// an ascending run in the data region.
 template <bool HV>
 __global__ void __launch_bounds__(256)
-omit_final_kernel(double *dk, uint32_t *dv, const double *bk, const uint32_t *bv, long long n,
-                  const int *loc)
+omit_final_kernel(double *dk, uint32_t *dv, const double *bk, const uint32_t *bv, long long n, const int *st)
 {
     pdl_wait();
-    if (*loc != 0) {
-        const long long n2 = n >> 1;
+    const unsigned s = (unsigned)*st;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    const long long i0 = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (s == OMIT_ST_BUF) {
         const double2 *src = reinterpret_cast<const double2 *>(bk);
         double2 *dst = reinterpret_cast<double2 *>(dk);
-        const long long stride = (long long)gridDim.x * blockDim.x;
-        for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n2; i += stride) dst[i] = src[i];
-        if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) dk[n - 1] = bk[n - 1];
-        if (HV) {
-            for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += stride) dv[i] = bv[i];
+        for (long long i = i0; i < (n >> 1); i += stride) dst[i] = src[i];
+        if ((n & 1) && i0 == 0) dk[n - 1] = bk[n - 1];
+        if (HV) for (long long i = i0; i < n; i += stride) dv[i] = bv[i];
+    } else if (s == (OMIT_ST_BUF | OMIT_ST_DESC)) {
+        for (long long i = i0; i < n; i += stride) {
+            dk[i] = bk[n - 1 - i];
+            if (HV) dv[i] = bv[n - 1 - i];
+        }
+    } else if (s == OMIT_ST_DESC) {
+        for (long long i = i0; i < (n >> 1); i += stride) {
+            const long long j = n - 1 - i;
+            const double x = dk[i], y = dk[j];
+            dk[i] = y;
+            dk[j] = x;
+            if (HV) {
+                const uint32_t u = dv[i], w = dv[j];
+                dv[i] = w;
+                dv[j] = u;
+            }
         }
     }
     pdl_trigger();

@@ -168,3 +168,60 @@ def test_omit_errors(gns):
         gns.sort_omit_(tk, None, workspace=small)
     torch.cuda.synchronize()
     assert np.array_equal(tk.cpu().numpy(), k)
+
+
+def dir_blocks(n, seed, block, kinds):
+    """Blocks of distinct keys, each ascending, strictly descending, or
+    descending with one tie ('a', 'd', 't' cycling through `kinds`), in a
+    seeded block order: descending runs are kept lazily (Octosort), merged
+    with each other when disjoint, reversed when they meet an ascending run
+    or overlap."""
+    rng = np.random.default_rng(seed)
+    base = np.arange(n, dtype=np.float64) * 2.0
+    nb = (n + block - 1) // block
+    order = rng.permutation(nb) if seed % 2 else np.arange(nb)[::-1]
+    parts = []
+    for j, b in enumerate(order):
+        x = base[b * block:(b + 1) * block].copy()
+        kind = kinds[j % len(kinds)]
+        if kind != "a":
+            x = x[::-1].copy()
+        if kind == "t" and x.size > 3:
+            x[1] = x[2]
+        parts.append(x)
+    return np.concatenate(parts)
+
+
+@pytest.mark.parametrize("kinds", ["d", "dt", "ad", "dda", "t"])
+@pytest.mark.parametrize("block", [T1, 2 * T1, 5 * T1 + 3])
+@pytest.mark.parametrize("n", [33 * T1 + 17, 64 * T1])
+def test_omit_descending_runs(gns, n, block, kinds):
+    """Octosort inside the Omitsort schedule: strictly
+    reversed tiles stay descending runs, disjoint descending pairs are omitted
+    as descending, the rest is reversed (in place or while copied) before
+    merging; a descending result is reversed once at the end."""
+    k = dir_blocks(n, n + block + len(kinds), block, kinds)
+    v = synth.iota_u32(n)
+    gk, gv = omit_sort(gns, k, v, use_ws=True)
+    ek, ev = oracle.sort(k, v)
+    assert_bitexact(gk, ek, gv, ev, what=f"kinds={kinds} block={block} n={n}")
+    gk, _ = omit_sort(gns, k, None)
+    assert_bitexact(gk, ek, what=f"kinds={kinds} block={block} n={n} key-only")
+
+
+@pytest.mark.parametrize("target", ["AscLeft", "DescLeft", "AscRight", "DescRight"])
+@pytest.mark.parametrize("n", [T1 + 1, 4 * T1, 9 * T1 + 5, (1 << 20) + 3])
+def test_omit_strictly_reversed(gns, n, target):
+    """A strictly reversed input (for the target's direction): one final
+    reversal (or reversed copy); with one tie it must take merges."""
+    k = np.arange(n, dtype=np.float64)
+    if target in ("AscLeft", "AscRight"):
+        k = k[::-1].copy()
+    v = synth.iota_u32(n)
+    for name in ("strict", "tie"):
+        x = k.copy()
+        if name == "tie":
+            x[n // 2] = x[n // 2 + 1]
+        gk, gv = omit_sort(gns, x, v, target=target)
+        ek, ev = oracle.sort_target(x, v, target)
+        assert_bitexact(gk, ek, gv, ev, what=f"{target} {name} n={n}")
