@@ -80,8 +80,13 @@ constexpr int NT1 = GNS_NT1;       // K1 threads per CTA (two CTAs per SM)
 #ifndef GNS_VT1
 #define GNS_VT1 32
 #endif
+// K1 CTAs per SM: key-only 3 (80 registers, 3 x 67.5 KB shared: 2^24 keys
+// tile sort 272 -> 249 us), with payload 2 (its 100 KB of shared memory)
 #ifndef GNS_T1_MINB
 #define GNS_T1_MINB (512 / GNS_NT1)
+#endif
+#ifndef GNS_T1_MINB_KEYS
+#define GNS_T1_MINB_KEYS (768 / GNS_NT1)
 #endif
 constexpr int VT1 = GNS_VT1;       // K1 keys per thread
 constexpr int TILE = NT1 * VT1;    // K1 tile = 8192 elements (runs entering the merge passes)
@@ -1116,7 +1121,7 @@ __device__ __forceinline__ void serial_merge32(const double *sk, const uint32_t 
 }
 
 template <bool HV, int ORD>
-__global__ void __launch_bounds__(NT1, GNS_T1_MINB)
+__global__ void __launch_bounds__(NT1, HV ? GNS_T1_MINB : GNS_T1_MINB_KEYS)
 tile_sort2_kernel(const double *src_k, const uint32_t *src_v, double *dst_k, uint32_t *dst_v, long long n,
                   const __grid_constant__ CUtensorMap ksrc, const __grid_constant__ CUtensorMap vsrc,
                   const __grid_constant__ CUtensorMap kdst, const __grid_constant__ CUtensorMap vdst,
