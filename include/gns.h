@@ -36,7 +36,9 @@
  *     in gns_last_error_string() (thread-local).
  *   - NaN keys are a precondition violation: the contents of keys/vals after
  *     the call are then unspecified, but every access stays inside
- *     keys/vals/the buffer and the call terminates.
+ *     keys/vals/the buffer and the call terminates.  With the environment
+ *     variable GNS_DEBUG=1 the sorts of f64 keys first count NaNs (one pass
+ *     and a host sync) and return GNS_ERR_INVALID_ARGUMENT, data untouched.
  *   - n in {0, 1} returns GNS_OK with no launch; pointers may be NULL if n == 0.
  *   - Reentrant: no global mutable state; concurrent calls on different streams
  *     with disjoint buffers are allowed.

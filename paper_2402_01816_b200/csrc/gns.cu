@@ -765,6 +765,29 @@ gns_status run_sort(double *keys, uint32_t *vals, size_t n, const Mode &m, unsig
     return GNS_OK;
 }
 
+// GNS_DEBUG=1: reject NaN keys (a precondition, R1) with
+// GNS_ERR_INVALID_ARGUMENT before sorting; costs one pass and a host sync.
+gns_status nan_guard(const double *keys, size_t n, int kt, cudaStream_t st)
+{
+    const char *e = std::getenv("GNS_DEBUG");
+    if (kt != KT_F64 || n == 0 || !e || e[0] != '1') return GNS_OK;
+    unsigned *dcnt = nullptr;
+    GNS_TRY(check(cudaMallocAsync((void **)&dcnt, sizeof(unsigned), st), "cudaMallocAsync"));
+    unsigned hcnt = 0;
+    gns_status r = check(cudaMemsetAsync(dcnt, 0, sizeof(unsigned), st), "memset");
+    if (r == GNS_OK) {
+        const unsigned grid = (unsigned)std::min<size_t>(ceil_div(n, 256), (size_t)num_sms() * 8);
+        nan_count_kernel<<<grid, 256, 0, st>>>(keys, (long long)n, dcnt);
+        r = check(cudaGetLastError(), "nan_count_kernel");
+    }
+    if (r == GNS_OK) r = check(cudaMemcpyAsync(&hcnt, dcnt, sizeof(unsigned), cudaMemcpyDeviceToHost, st), "memcpy");
+    if (r == GNS_OK) r = check(cudaStreamSynchronize(st), "sync");
+    cudaFreeAsync(dcnt, st);
+    if (r != GNS_OK) return r;
+    if (hcnt) return fail(GNS_ERR_INVALID_ARGUMENT, "NaN key (GNS_DEBUG=1 pre-scan)");
+    return GNS_OK;
+}
+
 gns_status sort_alloc(double *keys, uint32_t *vals, bool hv, size_t n, double frac, int target, cudaStream_t st,
                       int kt = KT_F64, bool omit = false)
 {
@@ -773,6 +796,8 @@ gns_status sort_alloc(double *keys, uint32_t *vals, bool hv, size_t n, double fr
     m.omit = omit && !m.limited;
     GNS_TRY(validate_data(keys, vals, hv, n));
     if (n <= 1) return GNS_OK;
+    GNS_TRY(ensure_attrs());
+    GNS_TRY(nan_guard(keys, n, kt, st));
     const Layout Lo = layout(n, m, hv);
     unsigned char *ws = nullptr;
     if (Lo.total) {
@@ -804,6 +829,8 @@ gns_status sort_ws(double *keys, uint32_t *vals, bool hv, size_t n, double frac,
         if (!ws || ws_bytes < Lo.total) return fail(GNS_ERR_WORKSPACE_TOO_SMALL, "workspace too small");
         if (!is_aligned(ws, 32)) return fail(GNS_ERR_MISALIGNED, "ws must be 32-byte aligned");
     }
+    GNS_TRY(ensure_attrs());
+    GNS_TRY(nan_guard(keys, n, kt, st));
     return run_sort(keys, hv ? vals : nullptr, n, m, (unsigned char *)ws, target, kt, st);
 }
 

@@ -1759,6 +1759,16 @@ omit_final_kernel(double *dk, uint32_t *dv, const double *bk, const uint32_t *bv
     pdl_trigger();
 }
 
+// GNS_DEBUG=1 pre-scan (R1): number of NaN keys (f64 only).
+__global__ void __launch_bounds__(256) nan_count_kernel(const double *k, long long n, unsigned *cnt)
+{
+    unsigned c = 0;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        c += (k[i] != k[i]) ? 1u : 0u;
+    c = __reduce_add_sync(0xFFFFFFFFu, c);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(cnt, c);
+}
+
 // ------------------------------------- target reversal (NEXT f3, AscRight/DescRight)
 // AscRight = reverse(DescLeft), DescRight = reverse(AscLeft) (PAPER.md:137-142:
 // the Right targets are the Left targets read from the other end of memory).

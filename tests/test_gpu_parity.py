@@ -286,6 +286,29 @@ def test_nan_memory_safe(gns):
     check_against_oracle(gns, synth.uniform(n, 4), v, 0.5, what="after NaN")
 
 
+def test_nan_rejected_with_gns_debug(gns, monkeypatch):
+    """GNS_DEBUG=1: a NaN key makes every f64 sort return
+    GNS_ERR_INVALID_ARGUMENT before anything moves (pre-scan, header R1);
+    NaN-free input still sorts bit-exact."""
+    monkeypatch.setenv("GNS_DEBUG", "1")
+    n = 5 * T + 3
+    k = synth.uniform(n, 8)
+    k[n // 2] = np.nan
+    v = synth.iota_u32(n)
+    for frac in (1.0, 0.5):
+        tk, tv = to_dev(k, v)
+        with pytest.raises(gns.GnsError) as ei:
+            gns.sort_(tk, tv, frac)
+        assert ei.value.status == 1
+        torch.cuda.synchronize()
+        assert np.array_equal(tk.cpu().numpy().view(np.uint64), k.view(np.uint64))
+        assert np.array_equal(tv.cpu().numpy(), v)
+    tk, _ = to_dev(k, None)
+    with pytest.raises(gns.GnsError):
+        gns.sort_omit_(tk, None)
+    check_against_oracle(gns, synth.uniform(n, 9), v, 1.0, what="GNS_DEBUG=1, no NaN")
+
+
 def _int_keys(key_type, n, seed):
     """Seeded 8-byte integer keys with ties and the type's extreme values."""
     rng = np.random.default_rng(seed)
