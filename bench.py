@@ -167,7 +167,8 @@ def run_reference(args, rank, world):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": config_json(case, args.frac),
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample,
+                         "host": host_cpu()},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -253,7 +254,8 @@ def main():
         torch.cuda.synchronize()
     if pg:
         pg.barrier()
-    t_ms = sum(a.elapsed_time(b) for a, b in ev)
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    t_ms = sum(step_ms)
     t_max, value = aggregate(torch, pg, t_ms, n, args.steps, world, dev)
     ms_per_step = t_max / args.steps
 
@@ -292,7 +294,9 @@ def main():
     ram = 1.0 + plan["workspace_bytes"] / (n * s)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms_per_step,
+        "step_ms_rank0": {"median": float(np.median(step_ms)), "min": float(min(step_ms))},
+        "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded SplitMix64, see DESIGN.md §3)",
         "config": dict(config_json(case, args.frac), parallelism=f"replicas{world}" if world > 1 else "single"),
         "roofline": {"bound": "hbm", "kernel": "merge pass (merge_tstore_kernel: K2 co-rank search warps + K3 TMA-pipelined merge, one launch per pass), avg over "
@@ -303,7 +307,8 @@ def main():
                      "whole_sort": {"bytes_lower_bound": plan["bytes_lower_bound"],
                                     "element_passes": plan["element_passes"],
                                     "achieved": plan["bytes_lower_bound"] / (ms_per_step / 1e3) / 1e9,
-                                    "frac": plan["bytes_lower_bound"] / (ms_per_step / 1e3) / 1e9 / peak},
+                                    "frac": plan["bytes_lower_bound"] / (ms_per_step / 1e3) / 1e9 / peak,
+                                    "frac_vs_nominal_8tbs": plan["bytes_lower_bound"] / (ms_per_step / 1e3) / 8e12},
                      "per_kernel_ms": roof["per_kernel_ms"]},
         "e2e": e2e,
         "gpu_launches": launches_per_step * args.steps,
@@ -555,6 +560,20 @@ def other_configs(gns, torch, dev, stream, flush, reps=5):
     return out
 
 
+def host_cpu():
+    """The host CPU model and core count (report them beside the oracle)."""
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return f"{model}, {os.cpu_count()} logical cores"
+
+
 def cpu_baseline(case):
     """The oracle, as it stands, on the host: the full workload sorted 3x on 1
     core (~10 s)."""
@@ -566,7 +585,7 @@ def cpu_baseline(case):
     for _ in range(reps):
         oracle.sort(keys, vals)
     t = time.perf_counter() - t0
-    return {"value": keys.size * reps / t, "unit": UNIT, "cores": 1, "kind": "oracle",
+    return {"value": keys.size * reps / t, "unit": UNIT, "cores": 1, "kind": "oracle", "host": host_cpu(),
             "sample": f"{case.name}, full n={keys.size}, sorted {reps}x by the single-threaded oracle "
                       f"(host has {os.cpu_count()} cores)"}
 
