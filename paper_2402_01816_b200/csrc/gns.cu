@@ -180,11 +180,27 @@ InplK inplace_kern(bool hv, int o)
     static const InplK t[2][NORD] = {GNS_ORDS(merge_inplace_kernel, false), GNS_ORDS(merge_inplace_kernel, true)};
     return t[hv][o];
 }
+// Lanes per tile of the partition search: 4 (eight tiles per warp; 2^27
+// pairs 10.22 -> 9.81 ms, keys 7.14 -> 6.72 ms against one warp per tile,
+// 8 lanes 9.90 / 6.80: the searches are latency-bound, fewer waves of warps
+// win over fewer search rounds).  GNS_PART_W = 32 / 16 / 8 / 4 (A/B).
+int part_w()
+{
+    static const int w = [] {
+        const char *e = std::getenv("GNS_PART_W");
+        const int v = e ? std::atoi(e) : 4;
+        return (v == 8 || v == 16 || v == 32) ? v : 4;
+    }();
+    return w;
+}
 PartK partition_kern(int o)
 {
-    static const PartK t[NORD] = {&partition_kernel<0>, &partition_kernel<1>, &partition_kernel<2>,
-                                  &partition_kernel<3>, &partition_kernel<4>, &partition_kernel<5>};
-    return t[o];
+#define GNS_PW(W) {&partition_kernel<0, W>, &partition_kernel<1, W>, &partition_kernel<2, W>, \
+                   &partition_kernel<3, W>, &partition_kernel<4, W>, &partition_kernel<5, W>}
+    static const PartK t[4][NORD] = {GNS_PW(32), GNS_PW(16), GNS_PW(8), GNS_PW(4)};
+#undef GNS_PW
+    const int w = part_w();
+    return t[w == 32 ? 0 : w == 16 ? 1 : w == 8 ? 2 : 3][o];
 }
 #undef GNS_ORDS
 
@@ -399,7 +415,7 @@ gns_status launch_merge(const MergeGeo &g, const double *lim_a, const double *li
         unsigned *ticket = reinterpret_cast<unsigned *>(corank + ntiles);
         GNS_TRY(check(cudaMemsetAsync(ticket, 0, sizeof(unsigned), st), "memset"));
         GNS_TRY(launch_pdl("partition_kernel", partition_kern(ord),
-                           (unsigned)ceil_div((size_t)ntiles * 32, 256), 256, 0, st, g, ntiles, corank));
+                           (unsigned)ceil_div((size_t)ntiles * part_w(), 256), 256, 0, st, g, ntiles, corank));
         const int grid = std::min(ntiles, 2 * num_sms());
         auto kern = inplace_kern(hv, ord);
         return launch_pdl("merge_inplace_kernel", kern, grid, NT + 32, ts_smem(hv), st, pg, ntiles,
@@ -415,7 +431,7 @@ gns_status launch_merge(const MergeGeo &g, const double *lim_a, const double *li
                           bmap, ad, OmitList{}, map, amap, bmap);
     }
     GNS_TRY(launch_pdl("partition_kernel", partition_kern(ord),
-                       (unsigned)ceil_div((size_t)ntiles * 32, 256), 256, 0, st, g, ntiles, corank));
+                       (unsigned)ceil_div((size_t)ntiles * part_w(), 256), 256, 0, st, g, ntiles, corank));
     GNS_TRY(launch_pdl("inplace_deps_kernel", inplace_deps_kernel, (unsigned)ceil_div(ntiles + 1, 256), 256, 0, st,
                        (const int *)corank, ntiles, g.L, g.n, deps, flags));
     unsigned *ticket = flags + ntiles;

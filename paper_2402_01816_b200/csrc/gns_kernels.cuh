@@ -420,17 +420,21 @@ __device__ __forceinline__ int tile_corank(const MergeGeo &g, int t, int gl, uns
                                     [&](int m) { return !before<ORD>(B[d - 1 - m], A[m]); });
 }
 
-template <int ORD>
+// One group of PW lanes per tile (PW = 32: one warp; 16 / 8: two / four tiles
+// per warp, fewer waves of latency-bound searches).
+template <int ORD, int PW = 32>
 __global__ void __launch_bounds__(256)
 partition_kernel(MergeGeo g, int ntiles, int *__restrict__ corank)
 {
     pdl_wait();
     pdl_trigger();
-    const int warp = (int)((blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5);
+    const int t = (int)((blockIdx.x * (long long)blockDim.x + threadIdx.x) / PW);
     const int lane = threadIdx.x & 31;
-    if (warp >= ntiles) return;
-    const int c = tile_corank<32, ORD>(g, warp, lane, 0xFFFFFFFFu, 0);   // sample-guided if g has samples
-    if (lane == 0) corank[warp] = c;
+    const int gl = lane % PW, gbase = lane - gl;
+    const unsigned mask = PW == 32 ? 0xFFFFFFFFu : ((1u << PW) - 1u) << gbase;
+    if (t >= ntiles) return;
+    const int c = tile_corank<PW, ORD>(g, t, gl, mask, gbase);   // sample-guided if g has samples
+    if (gl == 0) corank[t] = c;
 }
 
 // Samples of the two runs of an in-place top merge (every SMP_G-th key of
