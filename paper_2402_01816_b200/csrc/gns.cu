@@ -336,7 +336,7 @@ bool ticket_pass(bool hv, int ntiles)
         return e ? std::atoi(e) : -1;
     }();
     if (forced == 0 || forced == 1) return forced == 1;
-    return ntiles >= (hv ? 8192 : 32768);   // >= 2^25 elements with payload, >= 2^27 key-only (measured)
+    return ntiles >= (hv ? 8192 : 16384);   // >= 2^25 elements with payload, >= 2^26 key-only (measured)
 }
 
 template <typename... KArgs, typename... Args>
