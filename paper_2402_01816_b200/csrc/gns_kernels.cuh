@@ -13,6 +13,10 @@
 //         inplace_deps_kernel  (row a6) which earlier tiles each K4 tile must wait for
 //         reverse_kernel       (f3) the Right targets
 //         split_cuts_kernel    (f4) splitter cuts of the distributed sort
+//         omit_plan_kernel, omit_prep_kernel, omit_final_kernel and the
+//         list-driven merge_tstore_kernel<.., OL = true>
+//                              (f2) the Omitsort / Octosort schedule
+//         nan_count_kernel     GNS_DEBUG=1 pre-scan (R1)
 // Keys of every type (f64, int64, uint64; f3) travel as 8-byte patterns; the
 // template parameter ORD = direction | key type << 1 selects the order.
 //
@@ -76,7 +80,7 @@ static_assert((1 << MTILE_LOG2) == MTILE, "MTILE_LOG2");
 #ifndef GNS_NT1
 #define GNS_NT1 256
 #endif
-constexpr int NT1 = GNS_NT1;       // K1 threads per CTA (two CTAs per SM)
+constexpr int NT1 = GNS_NT1;       // K1 threads per CTA (three CTAs per SM key-only, two with payload)
 #ifndef GNS_VT1
 #define GNS_VT1 32
 #endif
