@@ -225,3 +225,49 @@ def test_omit_strictly_reversed(gns, n, target):
         gk, gv = omit_sort(gns, x, v, target=target)
         ek, ev = oracle.sort_target(x, v, target)
         assert_bitexact(gk, ek, gv, ev, what=f"{target} {name} n={n}")
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("pattern", ["runs", "ties"])
+def test_omit_max_size_properties(gns, pattern):
+    """GNS_MAX_N-scale Omitsort schedule (32-bit positions in the plan at
+    their limit), checked by properties that fix the stable sort uniquely:
+    non-decreasing keys, payload a permutation of the original indices, every
+    output key bit-identical to the input key its payload names, ties in
+    ascending payload order.  Seeded device-side inputs: 64 shuffled
+    ascending runs with a descending one (omitted, copied, reversed and
+    merged pairs), or heavy ties."""
+    n = (1 << 31) - 1
+    torch.cuda.empty_cache()                  # (blocks cached by earlier tests count as used)
+    free, _ = torch.cuda.mem_get_info()
+    need = n * (8 + 4) * 3 + n * 8
+    if free < need:
+        pytest.skip(f"needs {need / 2**30:.0f} GiB of device memory")
+    g = torch.Generator(device="cuda")
+    g.manual_seed(n + len(pattern))
+    if pattern == "runs":
+        base = torch.arange(n, device="cuda", dtype=torch.float64)
+        blk = (n + 63) // 64
+        perm = torch.randperm(64, device="cuda", generator=g)
+        keys = torch.empty_like(base)
+        for i in range(64):
+            a, b = i * blk, min(n, (i + 1) * blk)
+            c = int(perm[i]) * blk
+            keys[a:b] = base[c:c + (b - a)] if c + (b - a) <= n else base[n - (b - a):]
+        keys[:blk] = keys[:blk].flip(0)                       # one strictly descending run
+    else:
+        keys = torch.randint(0, 1 << 20, (n,), device="cuda", generator=g).to(torch.float64)
+    src = keys.clone()
+    vals = torch.arange(n, device="cuda", dtype=torch.int64).to(torch.uint32)
+    ws = gns.alloc_workspace(n, 1.0, True)
+    gns.sort_omit_(keys, vals, workspace=ws)
+    torch.cuda.synchronize()
+    del ws
+    assert bool((keys[1:] >= keys[:-1]).all())
+    idx = vals.to(torch.int64)
+    assert bool((src.view(torch.int64)[idx] == keys.view(torch.int64)).all())
+    seen = torch.zeros(n, dtype=torch.uint8, device="cuda")
+    seen[idx] = 1
+    assert int(seen.sum()) == n
+    tie = keys[1:] == keys[:-1]
+    assert bool((idx[1:][tie] > idx[:-1][tie]).all())

@@ -565,6 +565,7 @@ def test_max_size_properties(gns, n, frac):
     payload a permutation of 0..n-1 (the original indices), every output key
     bit-identical to the input key its payload names, and equal keys in
     ascending payload order.  Seeded device-side inputs with ties."""
+    torch.cuda.empty_cache()                  # (blocks cached by earlier tests count as used)
     free, _ = torch.cuda.mem_get_info()
     need = n * (8 + 4) * 3 + n * 8
     if free < need:
