@@ -17,10 +17,24 @@ sort -> split -> exchange -> merge:
 5. each rank merges the k received sorted runs in rank order with a pairwise
    tree of ``gns_merge_two`` launches (left run wins ties).
 
+With ``balanced=True`` (default) steps 2-3 are exact instead (SURVEY.md
+§8(e) step 2, "the k co-ranks across the k sorted shards"): rank g receives
+exactly the elements of global stable rank [g N / k, (g+1) N / k).  For every
+target rank R each rank keeps a window [lo, hi] of its cut; per round every
+rank proposes ``samples`` elements evenly spaced in its window, all ranks
+count (``gns_split_cuts``) how many of their elements precede each proposal,
+one all-reduce sums the counts C(x), and each rank narrows its window:
+C(x) < R puts x among the first R (lo >= its count, +1 on the owner),
+C(x) >= R keeps it out (hi <= its count).  A rank's own proposals split its
+window into ``samples`` + 1 parts, so about log_{samples+1}(n) rounds; the
+cuts are exact when the windows' lower ends sum to R.
+
 Global order: (key, rank, position in the rank's shard) = stable in the
 rank-major input order, so the concatenation of the ranks' outputs is the
 unique stable sort of the concatenated shards (bit-exact, payload included).
-Output sizes vary per rank (splitter quality); a rank may receive nothing.
+With sample splitters (``balanced=False``) output sizes vary per rank
+(splitter quality) and a rank may receive nothing; with exact co-ranks
+(default) they are the balanced shares.
 
 Every step that touches the data runs in this package's CUDA kernels; the
 ``ops`` argument exists so the orchestration can be exercised on CPU with the
@@ -84,13 +98,93 @@ def merge_runs(runs, ops):
     return runs[0]
 
 
-def sort_distributed(keys, vals=None, group=None, samples: int = 64, ops=None
+def _proposals(torch, keys, lo, hi, s):
+    """s positions evenly spaced in each window [lo_g, hi_g) of this rank's
+    sorted keys (positions past an empty window are marked invalid)."""
+    dev = keys.device
+    j = torch.arange(1, s + 1, dtype=torch.int64, device=dev)
+    span = (hi - lo).clamp(min=0)
+    pos = lo[:, None] + (span[:, None] * j[None, :]) // (s + 1)
+    valid = (span[:, None] > 0) & (pos < hi[:, None])
+    pos = torch.where(valid, pos, torch.zeros_like(pos))
+    key = keys[pos.clamp(max=max(keys.numel() - 1, 0))] if keys.numel() else torch.zeros(pos.shape, dtype=keys.dtype,
+                                                                                            device=dev)
+    return pos, key, valid
+
+
+def _narrow(torch, lo, hi, R, cand_rank, cand_pos, valid, mine, C, me):
+    """Window update of this rank from the global counts C of every proposal
+    (targets x proposals): x with C(x) < R is among the first R elements (cut
+    >= its count here, +1 if this rank owns it), else the cut <= its count."""
+    inside = valid & (C < R[:, None])
+    own = (cand_rank == me).to(torch.int64)
+    big = torch.iinfo(torch.int64).max
+    lo_new = torch.where(inside, mine + own * inside.to(torch.int64), torch.full_like(mine, -1)).amax(dim=1)
+    hi_new = torch.where(valid & ~inside, mine, torch.full_like(mine, big)).amin(dim=1)
+    return torch.maximum(lo, lo_new), torch.minimum(hi, hi_new)
+
+
+def _count(torch, ops, keys, ck, cr, cp, cv, me):
+    """This rank's count of elements preceding every valid proposal (0 for
+    invalid ones); ck holds the proposals' keys as int64 bit patterns."""
+    flat = cv.reshape(-1)
+    mine = torch.zeros(ck.numel(), dtype=torch.int64, device=keys.device)
+    if bool(flat.any()):
+        c = ops.cuts(keys, ck.reshape(-1)[flat].contiguous().view(keys.dtype), cr.reshape(-1)[flat].contiguous(),
+                     cp.reshape(-1)[flat].contiguous(), me)
+        mine[flat] = c.to(torch.int64)
+    return mine.reshape(ck.shape)
+
+
+def exact_cuts(keys, k, me, group, samples, ops):
+    """Cuts of this rank's sorted shard at global stable ranks g N / k,
+    g = 1..k-1 (collective over ``group``)."""
+    import torch
+    import torch.distributed as dist
+    dev = keys.device
+    n = keys.numel()
+    nt = torch.tensor([n], dtype=torch.int64, device=dev)
+    dist.all_reduce(nt, group=group)
+    N = int(nt.item())
+    R = torch.tensor([(g * N) // k for g in range(1, k)], dtype=torch.int64, device=dev)
+    lo = torch.zeros(k - 1, dtype=torch.int64, device=dev)
+    hi = torch.full((k - 1,), n, dtype=torch.int64, device=dev)
+    s = max(1, samples)
+    for _ in range(64):
+        pos, key, valid = _proposals(torch, keys, lo, hi, s)
+        # every rank's proposals: (key bits, position, valid) gathered in rank order
+        kb = key.contiguous().view(torch.int64)                    # 8-byte patterns of any key type
+        gk = [torch.empty_like(kb) for _ in range(k)]
+        gp = [torch.empty_like(pos) for _ in range(k)]
+        gvl = [torch.empty_like(pos) for _ in range(k)]
+        dist.all_gather(gk, kb, group=group)
+        dist.all_gather(gp, pos.contiguous(), group=group)
+        dist.all_gather(gvl, valid.to(torch.int64).contiguous(), group=group)
+        ck = torch.stack(gk, dim=1).reshape(k - 1, k * s)          # target x (rank, j)
+        cp = torch.stack(gp, dim=1).reshape(k - 1, k * s)
+        cv = torch.stack(gvl, dim=1).reshape(k - 1, k * s).bool()
+        cr = torch.arange(k, dtype=torch.int32, device=dev).repeat_interleave(s).repeat(k - 1, 1)
+        mine = _count(torch, ops, keys, ck, cr, cp, cv, me)
+        # global counts of every proposal, plus the windows' lower ends
+        red = torch.cat([mine.reshape(-1), lo])
+        dist.all_reduce(red, group=group)
+        C = red[:mine.numel()].reshape(k - 1, k * s)
+        if bool((red[mine.numel():] == R).all()):
+            break
+        lo, hi = _narrow(torch, lo, hi, R, cr, cp, cv, mine, C, me)
+    else:
+        raise RuntimeError("exact_cuts did not converge")
+    return lo
+
+
+def sort_distributed(keys, vals=None, group=None, samples: int = 64, ops=None, balanced: bool = True
                      ) -> Tuple[object, Optional[object]]:
     """Stable sort of the rank-major concatenation of every rank's
     (keys, vals) shard.  Returns this rank's piece of the sorted array (new
-    tensors on the keys' device).  keys: float64 / int64 / uint64 (CUDA for
-    the default ops); vals: uint32 or None.  Collective: every rank of
-    ``group`` must call it."""
+    tensors on the keys' device): with ``balanced`` exactly global ranks
+    [g N / k, (g+1) N / k) on rank g, else the piece between sample
+    splitters.  keys: float64 / int64 / uint64 (CUDA for the default ops);
+    vals: uint32 or None.  Collective: every rank of ``group`` must call it."""
     import torch
     import torch.distributed as dist
     ops = ops or CudaOps()
@@ -103,6 +197,9 @@ def sort_distributed(keys, vals=None, group=None, samples: int = 64, ops=None
     if k == 1:
         return keys, vals
     n = keys.numel()
+    if balanced:
+        cuts = exact_cuts(keys, k, me, group, samples, ops)
+        return _exchange_and_merge(torch, dist, keys, vals, cuts, n, k, group, ops)
     # 2. samples -> splitters (every rank contributes exactly `samples` slots;
     # an empty shard marks its slots invalid)
     pos = _sample_positions(n, samples)
@@ -130,6 +227,13 @@ def sort_distributed(keys, vals=None, group=None, samples: int = 64, ops=None
         cuts = ops.cuts(keys, spl_key.contiguous(), spl_rank.contiguous(), spl_pos.contiguous(), me)
     else:
         cuts = torch.zeros(k - 1, dtype=torch.int64, device=dev)
+    return _exchange_and_merge(torch, dist, keys, vals, cuts, n, k, group, ops)
+
+
+def _exchange_and_merge(torch, dist, keys, vals, cuts, n, k, group, ops):
+    """Steps 4-5: one all-to-all-v of the pieces between the cuts, then the
+    merge of the k received runs in rank order."""
+    dev = keys.device
     edges = torch.cat([torch.zeros(1, dtype=torch.int64, device=dev), cuts.to(torch.int64),
                        torch.full((1,), n, dtype=torch.int64, device=dev)])
     send = (edges[1:] - edges[:-1]).contiguous()
@@ -156,7 +260,34 @@ def sort_distributed(keys, vals=None, group=None, samples: int = 64, ops=None
     return mk.contiguous(), (None if mv is None else mv.contiguous())
 
 
-def simulate(shards, samples: int = 64, ops=None):
+def simulate_exact_cuts(torch, keys_list, samples, ops):
+    """exact_cuts for k shards in one process (the all-gather and all-reduce
+    are concatenations and sums): every shard's k-1 cuts."""
+    k = len(keys_list)
+    dev = keys_list[0].device
+    N = sum(x.numel() for x in keys_list)
+    R = torch.tensor([(g * N) // k for g in range(1, k)], dtype=torch.int64, device=dev)
+    lo = [torch.zeros(k - 1, dtype=torch.int64, device=dev) for _ in range(k)]
+    hi = [torch.full((k - 1,), x.numel(), dtype=torch.int64, device=dev) for x in keys_list]
+    s = max(1, samples)
+    for _ in range(64):
+        props = [_proposals(torch, keys_list[r], lo[r], hi[r], s) for r in range(k)]
+        ck = torch.stack([p[1].contiguous().view(torch.int64) for p in props], dim=1).reshape(k - 1, k * s)
+        cp = torch.stack([p[0] for p in props], dim=1).reshape(k - 1, k * s)
+        cv = torch.stack([p[2] for p in props], dim=1).reshape(k - 1, k * s)
+        cr = torch.arange(k, dtype=torch.int32, device=dev).repeat_interleave(s).repeat(k - 1, 1)
+        mine = [_count(torch, ops, keys_list[r], ck, cr, cp, cv, r) for r in range(k)]
+        C = sum(mine)
+        if bool((sum(lo) == R).all()):
+            break
+        for r in range(k):
+            lo[r], hi[r] = _narrow(torch, lo[r], hi[r], R, cr, cp, cv, mine[r], C, r)
+    else:
+        raise RuntimeError("exact_cuts did not converge")
+    return lo
+
+
+def simulate(shards, samples: int = 64, ops=None, balanced: bool = True):
     """The same steps for k shards in ONE process (no collectives: the
     all-gather and all-to-all are tensor concatenations / slices), for
     validating the kernels of the distributed path on a single GPU.  Returns
@@ -172,6 +303,13 @@ def simulate(shards, samples: int = 64, ops=None):
     if k == 1:
         return srt
     dev = srt[0][0].device
+    if balanced:
+        cuts = simulate_exact_cuts(torch, [kk for kk, _ in srt], samples, ops)
+        pieces = []
+        for r, (kk, vv) in enumerate(srt):
+            e = [0] + [int(x) for x in cuts[r].cpu()] + [kk.numel()]
+            pieces.append([(kk[e[j]:e[j + 1]], None if vv is None else vv[e[j]:e[j + 1]]) for j in range(k)])
+        return [merge_runs([pieces[r][j] for r in range(k)], ops) for j in range(k)]
     a_key, a_pos, a_rank = [], [], []
     for r, (kk, _) in enumerate(srt):
         pos = _sample_positions(kk.numel(), samples)

@@ -92,8 +92,10 @@ def _worker(rank, world, port, q):
         k = make_shard(case, rank, world)
         base = sum(make_shard(case, r, world).size for r in range(rank))
         v = (np.arange(k.size) + base).astype(np.uint32)
-        ok, ov = gdist.sort_distributed(torch.from_numpy(k), torch.from_numpy(v), samples=16, ops=CpuOracleOps())
-        q.put((case, rank, ok.numpy(), ov.numpy()))
+        for bal in (True, False):
+            ok, ov = gdist.sort_distributed(torch.from_numpy(k), torch.from_numpy(v), samples=16, ops=CpuOracleOps(),
+                                            balanced=bal)
+            q.put((case, bal, rank, ok.numpy(), ov.numpy()))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -108,33 +110,46 @@ def test_distributed_sort_gloo(world):
     procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
-    res = [q.get(timeout=240) for _ in range(world * len(CASES))]
+    res = [q.get(timeout=240) for _ in range(world * len(CASES) * 2)]
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
     for case in CASES:
-        got = sorted([r for r in res if r[0] == case], key=lambda x: x[1])
         shards = [make_shard(case, r, world) for r in range(world)]
         allk = np.concatenate(shards)
         allv = np.arange(allk.size, dtype=np.uint32)
         kt = {np.dtype(np.float64): "f64", np.dtype(np.int64): "i64", np.dtype(np.uint64): "u64"}[allk.dtype]
         ek, ev = oracle.sort_keys(allk, allv, kt)
-        gk = np.concatenate([r[2] for r in got])
-        gv = np.concatenate([r[3] for r in got])
-        assert gk.view(np.uint64).tolist() == ek.view(np.uint64).tolist(), f"case {case} world {world}"
-        assert gv.tolist() == ev.tolist(), f"case {case} world {world}"
+        N = allk.size
+        for bal in (True, False):
+            got = sorted([r for r in res if r[0] == case and r[1] == bal], key=lambda x: x[2])
+            gk = np.concatenate([r[3] for r in got])
+            gv = np.concatenate([r[4] for r in got])
+            what = f"case {case} world {world} balanced={bal}"
+            assert gk.view(np.uint64).tolist() == ek.view(np.uint64).tolist(), what
+            assert gv.tolist() == ev.tolist(), what
+            if bal:   # exact co-ranks: rank g holds global ranks [g N / k, (g+1) N / k)
+                assert [r[3].size for r in got] == [((g + 1) * N) // world - (g * N) // world
+                                                    for g in range(world)], what
 
 
-def test_simulate_matches_collective_cpu():
-    """dist.simulate (one process, no collectives) == the oracle too."""
+@pytest.mark.parametrize("balanced", [True, False])
+@pytest.mark.parametrize("case", CASES)
+def test_simulate_matches_collective_cpu(case, balanced):
+    """dist.simulate (one process, no collectives) == the oracle too; with
+    exact co-ranks every piece has its balanced size."""
     import oracle
     from paper_2402_01816_b200 import dist as gdist
     world = 4
-    shards = [make_shard(0, r, world) for r in range(world)]
+    shards = [make_shard(case, r, world) for r in range(world)]
     base = np.cumsum([0] + [s.size for s in shards])
     outs = gdist.simulate([(torch.from_numpy(s), torch.from_numpy((np.arange(s.size) + base[r]).astype(np.uint32)))
-                           for r, s in enumerate(shards)], samples=16, ops=CpuOracleOps())
+                           for r, s in enumerate(shards)], samples=16, ops=CpuOracleOps(), balanced=balanced)
     allk = np.concatenate(shards)
-    ek, ev = oracle.sort_keys(allk, np.arange(allk.size, dtype=np.uint32), "f64")
+    kt = {np.dtype(np.float64): "f64", np.dtype(np.int64): "i64", np.dtype(np.uint64): "u64"}[allk.dtype]
+    ek, ev = oracle.sort_keys(allk, np.arange(allk.size, dtype=np.uint32), kt)
     assert np.concatenate([o[0].numpy() for o in outs]).view(np.uint64).tolist() == ek.view(np.uint64).tolist()
     assert np.concatenate([o[1].numpy() for o in outs]).tolist() == ev.tolist()
+    if balanced:
+        N = allk.size
+        assert [o[0].numel() for o in outs] == [((g + 1) * N) // world - (g * N) // world for g in range(world)]

@@ -503,12 +503,14 @@ def test_split_cuts(gns, key_type):
         assert got.cpu().tolist() == want, (key_type, me)
 
 
+@pytest.mark.parametrize("balanced", [True, False])
 @pytest.mark.parametrize("k", [2, 3, 4, 8])
 @pytest.mark.parametrize("pattern", ["uniform", "ties", "skewed"])
-def test_distributed_sort_simulated(gns, k, pattern):
+def test_distributed_sort_simulated(gns, k, pattern, balanced):
     """The f4 path's kernels end to end on one GPU: dist.simulate runs the k
     ranks' steps in one process (exchange = slices, no collectives), vs the
-    oracle's stable sort of the rank-major concatenation."""
+    oracle's stable sort of the rank-major concatenation; with exact co-ranks
+    (balanced) every piece has exactly its share of the N keys."""
     from paper_2402_01816_b200 import dist as gdist
     rng = np.random.default_rng(k * 100 + len(pattern))
     shards = []
@@ -524,13 +526,16 @@ def test_distributed_sort_simulated(gns, k, pattern):
     base = np.cumsum([0] + [s.size for s in shards])
     ins = [(torch.from_numpy(s).cuda(), torch.from_numpy((np.arange(s.size) + base[r]).astype(np.uint32)).cuda())
            for r, s in enumerate(shards)]
-    outs = gdist.simulate(ins, samples=32)
+    outs = gdist.simulate(ins, samples=32, balanced=balanced)
     torch.cuda.synchronize()
     allk = np.concatenate(shards)
     ek, ev = oracle.sort(allk, np.arange(allk.size, dtype=np.uint32))
     gk = np.concatenate([o[0].cpu().numpy() for o in outs])
     gv = np.concatenate([o[1].cpu().numpy() for o in outs])
     assert_bitexact(gk, ek, gv, ev, what=f"k={k} {pattern}")
+    if balanced:
+        N = allk.size
+        assert [o[0].numel() for o in outs] == [((g + 1) * N) // k - (g * N) // k for g in range(k)]
 
 
 def test_distributed_sort_single_rank_nccl(gns):
