@@ -652,3 +652,42 @@ def test_ticket_merge_passes_large_keys(gns):
     for frac in (1.0, 0.5):
         gk, _ = gpu_sort(gns, k, None, frac, use_ws=True)
         assert_bitexact(gk, ek, what=f"frac={frac}")
+
+
+def test_concurrent_streams_and_threads(gns):
+    """Reentrancy (header): sorts enqueued on different streams from two host
+    threads at once, each with its own workspace (and one stream-ordered
+    allocation), all bit-exact."""
+    import threading
+    cases = []
+    for i, (n, frac, hv) in enumerate([(5 * T1 + 17, 1.0, True), (7 * T1 + 3, 0.5, False),
+                                       (3 * T1 + 1, 0.25, True), (9 * T1, 1.0, False)]):
+        k = synth.ties(n, 300 + i, 50) if i % 2 else synth.uniform(n, 300 + i)
+        v = synth.iota_u32(n) if hv else None
+        cases.append((k, v, frac))
+    results = [None] * len(cases)
+    errors = []
+
+    def run(idx):
+        try:
+            k, v, frac = cases[idx]
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                tk, tv = to_dev(k, v)
+                ws = gns.alloc_workspace(k.size, frac, v is not None) if idx % 2 == 0 else None
+                for _ in range(3):                     # re-sorting sorted data is a no-op, result unchanged
+                    gns.sort_(tk, tv, frac, workspace=ws, stream=s)
+            s.synchronize()
+            results[idx] = (tk.cpu().numpy(), None if tv is None else tv.cpu().numpy())
+        except Exception as e:  # noqa: BLE001
+            errors.append(e)
+
+    threads = [threading.Thread(target=run, args=(i,)) for i in range(len(cases))]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
+    for (k, v, frac), (gk, gv) in zip(cases, results):
+        ek, ev = oracle.sort(k, v)
+        assert_bitexact(gk, ek, gv, ev, what=f"n={k.size} frac={frac}")
