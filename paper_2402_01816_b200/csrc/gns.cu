@@ -367,7 +367,7 @@ gns_status launch_pdl(const char *what, void (*kern)(KArgs...), dim3 grid, dim3 
 // Row a2 (K1).
 gns_status launch_tile_sort(const double *sk, const uint32_t *sv, double *dk, uint32_t *dv, size_t n, int ord,
                             cudaStream_t st, unsigned *unsorted = nullptr, double *smp = nullptr,
-                            unsigned char *tdesc = nullptr)
+                            unsigned char *tdesc = nullptr, double *smp_src = nullptr)
 {
     if (n == 0) return GNS_OK;
     const unsigned grid = (unsigned)ceil_div(n, TILE);
@@ -386,7 +386,7 @@ gns_status launch_tile_sort(const double *sk, const uint32_t *sv, double *dk, ui
     uint32_t *dvv = hv ? dv : nullptr;
     auto kern = tile_kern(hv, ord);
     return launch_pdl("tile_sort2_kernel", kern, grid, NT1, t1_smem(hv), st, sk, svv, dk, dvv, (long long)n, m[0],
-                      m[1], m[2], m[3], unsorted, smp, tdesc);
+                      m[1], m[2], m[3], unsorted, smp, tdesc, smp_src);
 }
 
 // Rows a3+a4 (fused K2+K3, persistent TMA pipeline) or, in place, a6 (K2 +
@@ -560,11 +560,12 @@ gns_status launch_merge_list(const MergeGeo &g0, const MergeGeo &g1, const int *
                       0, map[0], amap[0], bmap[0], Adapt{}, ol, map[1], amap[1], bmap[1]);
 }
 
-// NEXT f2: Omitsort on the full buffer.  The tile sort works
-// in place (a tile already in order is not written back); one plan launch
-// decides every level; per level the copies and one list-driven merge
-// launch; a final copy if the sorted run ends in the buffer.  Presorted
-// input: no key moves.
+// NEXT f2: Omitsort on the full buffer.  The tile sort leaves
+// tiles in order (and strictly reversed ones, Octosort) where they are and
+// writes the others to the region that makes an all-merging input end in
+// the data array; one plan launch decides every level; per level the copies
+// and one list-driven merge launch; a final copy if the sorted run ends in
+// the buffer.  Presorted input: no key moves.
 gns_status sort_omit(double *keys, uint32_t *vals, size_t n, unsigned char *ws, const Layout &Lo, int ord,
                      cudaStream_t st)
 {
@@ -587,10 +588,15 @@ gns_status sort_omit(double *keys, uint32_t *vals, size_t n, unsigned char *ws, 
     int *list = reinterpret_cast<int *>(ws + Lo.off_list);
     int *cnt = reinterpret_cast<int *>(ws + Lo.off_cnt);
     const int M = merge_passes_for(n);
-    GNS_TRY(launch_tile_sort(keys, vals, keys, vals, n, ord, st, nullptr, smp_d, tdesc));
+    // Tiles that need sorting go to the buffer when the number of merge
+    // levels is odd (random input then ends in the data region with no copy
+    // back); tiles in order or strictly reversed stay in place either way.
+    const bool to_buf = (M & 1) != 0;
+    GNS_TRY(launch_tile_sort(keys, vals, to_buf ? bk : keys, to_buf ? bv : vals, n, ord, st, nullptr,
+                             to_buf ? smp_b : smp_d, tdesc, smp_d));
     GNS_TRY(launch_pdl("omit_plan_kernel", omit_plan_kern(ord), 1, OMIT_THREADS,
                        Lo.nruns <= (size_t)OMIT_SMEM_RUNS ? OMIT_SMEM : 0, st, (const double *)keys,
-                       (const unsigned char *)tdesc, (long long)n, M, S, act, pre, cnt));
+                       (const double *)bk, (const unsigned char *)tdesc, (long long)n, M, S, act, pre, cnt));
     const unsigned cgrid = (unsigned)std::min<size_t>(ceil_div(n, MTILE), (size_t)num_sms() * 4);
     size_t off = 0;
     for (int p = 0; p < M; ++p) {

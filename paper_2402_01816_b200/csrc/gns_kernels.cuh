@@ -1133,7 +1133,7 @@ __global__ void __launch_bounds__(NT1, HV ? GNS_T1_MINB : GNS_T1_MINB_KEYS)
 tile_sort2_kernel(const double *src_k, const uint32_t *src_v, double *dst_k, uint32_t *dst_v, long long n,
                   const __grid_constant__ CUtensorMap ksrc, const __grid_constant__ CUtensorMap vsrc,
                   const __grid_constant__ CUtensorMap kdst, const __grid_constant__ CUtensorMap vdst,
-                  unsigned *unsorted, double *smp, unsigned char *tdesc)
+                  unsigned *unsorted, double *smp, unsigned char *tdesc, double *smp_src)
 {
     pdl_wait();
     GNS_TL_START(0);
@@ -1251,11 +1251,16 @@ tile_sort2_kernel(const double *src_k, const uint32_t *src_v, double *dst_k, uin
     } else {
         __syncthreads();                   // the TMA-layout reads are done before the staging writes
     }
-    if (tdesc != nullptr && tid == 0) tdesc[tile] = (mode == 2) ? 1 : 0;
-    if (mode == 2 && tdesc != nullptr && dst_k == src_k) {
-        // Octosort (NEXT f2): the strictly reversed tile
-        // stays as it is, a descending run (its reversal is its stable sort)
-        if (smp != nullptr && (tid & (SMP_G / VT1 - 1)) == 0) smp[(base + e0) >> SMP_LOG2] = k[0];
+    // Omitsort schedule (tdesc != nullptr): per tile bit 0 = kept as a
+    // descending run, bit 1 = written to dst (not in src's region)
+    if (tdesc != nullptr && tid == 0)
+        tdesc[tile] = (unsigned char)((mode == 2 ? 1 : 0) | ((mode == 0 && dst_k != src_k) ? 2 : 0));
+    if (tdesc != nullptr && mode != 0) {
+        // Omitsort / Octosort (NEXT f2): a tile in order,
+        // or strictly reversed (a descending run: its reversal is its stable
+        // sort), stays where it is; only its samples are written
+        if (smp_src != nullptr && e0 < cnt && (tid & (SMP_G / VT1 - 1)) == 0)
+            smp_src[(base + e0) >> SMP_LOG2] = k[0];
         GNS_TL_END(0);
         pdl_trigger();
         return;
@@ -1541,7 +1546,7 @@ struct OmitState {                  // per-run state of two levels (ping-pong), 
 };
 template <int ORD>
 __global__ void __launch_bounds__(OMIT_THREADS)
-omit_plan_kernel(const double *dk, const unsigned char *tdesc, long long n, int levels, OmitState S,
+omit_plan_kernel(const double *dk, const double *bk, const unsigned char *tdesc, long long n, int levels, OmitState S,
                  unsigned char *act, int *pre, int *counts)
 {
     pdl_wait();
@@ -1562,9 +1567,11 @@ omit_plan_kernel(const double *dk, const unsigned char *tdesc, long long n, int 
         S.st[1] = S.st[0] + OMIT_SMEM_RUNS;
     }
     for (int r = tid; r < nr0; r += OMIT_THREADS) {
-        const unsigned d = tdesc[r] ? OMIT_ST_DESC : 0u;
-        const double f = dk[(long long)r * TILE], l = dk[min(n, (long long)(r + 1) * TILE) - 1];
-        S.st[0][r] = (unsigned char)d;
+        const unsigned d = (tdesc[r] & 1) ? OMIT_ST_DESC : 0u;
+        const unsigned b = (tdesc[r] & 2) ? OMIT_ST_BUF : 0u;
+        const double *R = b ? bk : dk;
+        const double f = R[(long long)r * TILE], l = R[min(n, (long long)(r + 1) * TILE) - 1];
+        S.st[0][r] = (unsigned char)(d | b);
         S.lo[0][r] = d ? l : f;
         S.hi[0][r] = d ? f : l;
     }
