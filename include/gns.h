@@ -131,6 +131,18 @@ typedef enum {
 gns_status gns_sort_keys(void *keys, gns_key_type key_type, uint32_t *vals, size_t n, double buffer_fraction,
                          gns_target target, void *ws, size_t ws_bytes, gns_stream_t stream);
 
+/* NEXT f3: 64-bit payloads.  keys (any gns_key_type) are sorted as by
+ * gns_sort_keys with the full buffer and any target; vals[n] (uint64_t, e.g.
+ * a 64-bit index or pointer) moves with its key.  The payload rides through
+ * the sort as a u32 index (the pairs path), then is gathered once (random
+ * 8-byte reads) into the free pairs buffer and copied back: %RAM = 2.0 of
+ * the 16-byte elements, about one extra HBM pass over the payload.
+ * ws: NULL (allocated stream-ordered) or gns_workspace_bytes_u64(n) bytes,
+ * 32-byte aligned.  Errors as gns_sort_keys. */
+size_t gns_workspace_bytes_u64(size_t n);
+gns_status gns_sort_keys_u64(void *keys, gns_key_type key_type, uint64_t *vals, size_t n, gns_target target,
+                             void *ws, size_t ws_bytes, gns_stream_t stream);
+
 /* NEXT f2: Omitsort (§Full adaptivity) on the full buffer
  * (%RAM 2.0; workspace = gns_workspace_bytes(n, 1.0, vals != NULL)).  Same
  * result as gns_sort_keys (the unique stable sort), different schedule: every
@@ -238,7 +250,8 @@ gns_status gns_merge_inplace_top(double *keys, uint32_t *vals, const double *lef
  * per-launch durations (milliseconds) and kinds (1 tile sort, 2 merge pass,
  * 3 co-rank partition, 4 in-place dependency ranges, 5 in-place merge,
  * 6 reversal, 7 splitter cuts, 8 sample gather, 9 Omitsort plan, 10 Omitsort
- * tile list + copies, 11 Omitsort final copy, 0 other) in launch order, turns timing off and returns the number
+ * tile list + copies, 11 Omitsort final copy, 12 / 13 index and gather of
+ * gns_sort_keys_u64, 0 other) in launch order, turns timing off and returns the number
  * of timed launches (-1 if timing was off or an event failed). */
 gns_status gns_timing_begin(int max_launches);
 int gns_timing_end(float *ms, int *kind, int cap);

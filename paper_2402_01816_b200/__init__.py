@@ -65,6 +65,8 @@ _c = {
     "gns_sort_target_f64": _sig("gns_sort_target_f64", [_vp, _vp, _sz, _d, _i, _vp, _sz, _vp]),
     "gns_sort_keys": _sig("gns_sort_keys", [_vp, _i, _vp, _sz, _d, _i, _vp, _sz, _vp]),
     "gns_sort_omit": _sig("gns_sort_omit", [_vp, _i, _vp, _sz, _i, _vp, _sz, _vp]),
+    "gns_sort_keys_u64": _sig("gns_sort_keys_u64", [_vp, _i, _vp, _sz, _i, _vp, _sz, _vp]),
+    "gns_workspace_bytes_u64": _sig("gns_workspace_bytes_u64", [_sz], _sz),
     "gns_split_cuts": _sig("gns_split_cuts", [_vp, _i, _sz, _vp, _vp, _vp, _i, _i, _vp, _vp]),
     "gns_merge_two": _sig("gns_merge_two", [_vp, _vp, _sz, _vp, _vp, _sz, _vp, _vp, _i, _vp]),
     "gns_plan": _sig("gns_plan", [_sz, _d, _i, ctypes.POINTER(gns_plan_info)]),
@@ -132,6 +134,14 @@ def gns_sort_keys(keys_ptr, key_type, vals_ptr, n, buffer_fraction, target, ws_p
     return _c["gns_sort_keys"](keys_ptr, key_type, vals_ptr, n, buffer_fraction, target, ws_ptr, ws_bytes, stream)
 
 
+def gns_sort_keys_u64(keys_ptr, key_type, vals_ptr, n, target, ws_ptr, ws_bytes, stream) -> int:
+    return _c["gns_sort_keys_u64"](keys_ptr, key_type, vals_ptr, n, target, ws_ptr, ws_bytes, stream)
+
+
+def gns_workspace_bytes_u64(n) -> int:
+    return _c["gns_workspace_bytes_u64"](n)
+
+
 def gns_sort_omit(keys_ptr, key_type, vals_ptr, n, target, ws_ptr, ws_bytes, stream) -> int:
     return _c["gns_sort_omit"](keys_ptr, key_type, vals_ptr, n, target, ws_ptr, ws_bytes, stream)
 
@@ -181,7 +191,8 @@ def gns_timing_end(cap: int = 4096):
 
 
 LAUNCH_KINDS = {1: "tile_sort", 2: "merge_pass", 3: "partition", 4: "inplace_deps", 5: "inplace_merge", 6: "reverse",
-                7: "split_cuts", 8: "gather_samples", 9: "omit_plan", 10: "omit_prep", 11: "omit_final"}
+                7: "split_cuts", 8: "gather_samples", 9: "omit_plan", 10: "omit_prep", 11: "omit_final",
+                12: "iota", 13: "gather_u64"}
 
 
 def gns_tile_elems() -> int:
@@ -235,6 +246,29 @@ def _check_keys(keys, vals, any_key_type: bool = False):
             raise TypeError("vals must be a contiguous CUDA uint32 tensor")
         if vals.numel() != keys.numel():
             raise ValueError("keys and vals differ in length")
+
+
+def sort_u64_(keys, vals, workspace=None, stream=None, target: str = "AscLeft"):
+    """NEXT f3: stable sort of ``keys`` (float64 / int64 / uint64) moving a
+    64-bit payload ``vals`` (uint64 or int64, contiguous CUDA) with each key
+    (gns_sort_keys_u64, full buffer).  ``workspace``: optional uint8 CUDA
+    tensor of >= workspace_bytes_u64(n) bytes."""
+    _check_keys(keys, None, any_key_type=True)
+    import torch
+    if vals.dtype not in (torch.uint64, torch.int64) or not vals.is_cuda or not vals.is_contiguous():
+        raise TypeError("vals must be a contiguous CUDA uint64/int64 tensor")
+    if vals.numel() != keys.numel():
+        raise ValueError("keys and vals differ in length")
+    n = keys.numel()
+    wp = _ptr(workspace) if workspace is not None else None
+    wb = workspace.numel() * workspace.element_size() if workspace is not None else 0
+    _check(gns_sort_keys_u64(_ptr(keys), _key_type(keys), _ptr(vals), n, TARGETS[target], wp, wb,
+                             _stream_handle(stream)), "sort_u64_")
+    return keys, vals
+
+
+def workspace_bytes_u64(n: int) -> int:
+    return gns_workspace_bytes_u64(n)
 
 
 def sort_omit_(keys, vals=None, workspace=None, stream=None, target: str = "AscLeft"):

@@ -321,8 +321,8 @@ int launch_kind(const char *what)
     static const char *names[] = {"tile_sort2_kernel", "merge_tstore_kernel", "partition_kernel",
                                   "inplace_deps_kernel", "merge_inplace_kernel", "reverse_kernel",
                                   "split_cuts_kernel", "gather_samples_kernel", "omit_plan_kernel",
-                                  "omit_prep_kernel", "omit_final_kernel"};
-    for (int i = 0; i < 11; ++i)
+                                  "omit_prep_kernel", "omit_final_kernel", "iota_u32_kernel", "gather_u64_kernel"};
+    for (int i = 0; i < 13; ++i)
         if (std::strcmp(what, names[i]) == 0) return i + 1;
     return 0;
 }
@@ -910,6 +910,64 @@ gns_status gns_sort_keys(void *keys, gns_key_type key_type, uint32_t *vals, size
                            (cudaStream_t)stream, (int)key_type);
     return sort_alloc(k, vals, vals != nullptr, n, buffer_fraction, (int)target, (cudaStream_t)stream,
                       (int)key_type);
+}
+
+size_t gns_workspace_bytes_u64(size_t n)
+{
+    Mode m;
+    if (mode_for(1.0, n, &m) != GNS_OK || n > GNS_MAX_N) return 0;
+    if (n <= 1) return 0;
+    return align_up(n * sizeof(uint32_t), 256) +
+           std::max(layout(n, m, true).total, align_up(n * sizeof(uint64_t), 256));
+}
+
+gns_status gns_sort_keys_u64(void *keys, gns_key_type key_type, uint64_t *vals, size_t n, gns_target target,
+                             void *ws, size_t ws_bytes, gns_stream_t stream)
+{
+    if ((int)target < 0 || (int)target > 3) return fail(GNS_ERR_INVALID_ARGUMENT, "target must be 0..3");
+    if ((int)key_type < 0 || (int)key_type > 2) return fail(GNS_ERR_INVALID_ARGUMENT, "key_type must be 0..2");
+    double *k = (double *)keys;
+    if (n > GNS_MAX_N) return fail(GNS_ERR_INVALID_ARGUMENT, "n > GNS_MAX_N");
+    if (n && (!keys || !vals)) return fail(GNS_ERR_INVALID_ARGUMENT, "NULL keys/vals with n > 0");
+    if (n && (!is_aligned(keys, 32) || !is_aligned(vals, 32)))
+        return fail(GNS_ERR_MISALIGNED, "keys/vals must be 32-byte aligned");
+    if (n <= 1) return GNS_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t need = gns_workspace_bytes_u64(n);
+    unsigned char *w = (unsigned char *)ws;
+    if (w) {
+        if (ws_bytes < need) return fail(GNS_ERR_WORKSPACE_TOO_SMALL, "workspace too small");
+        if (!is_aligned(w, 32)) return fail(GNS_ERR_MISALIGNED, "ws must be 32-byte aligned");
+    }
+    GNS_TRY(ensure_attrs());
+    GNS_TRY(nan_guard(k, n, (int)key_type, st));
+    bool own = false;
+    if (!w) {
+        cudaError_t e = cudaMallocAsync((void **)&w, need, st);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            if (e == cudaErrorMemoryAllocation) return fail(GNS_ERR_OUT_OF_MEMORY, "cudaMallocAsync: out of memory");
+            return check(e, "cudaMallocAsync");
+        }
+        own = true;
+    }
+    uint32_t *idx = reinterpret_cast<uint32_t *>(w);
+    unsigned char *rest = w + align_up(n * sizeof(uint32_t), 256);     // pairs workspace, then the gather buffer
+    Mode m;
+    gns_status r = mode_for(1.0, n, &m);
+    const unsigned grid = (unsigned)std::min<size_t>(ceil_div(n, 256), (size_t)num_sms() * 8);
+    if (r == GNS_OK) r = launch_pdl("iota_u32_kernel", iota_u32_kernel, grid, 256, 0, st, idx, (long long)n);
+    if (r == GNS_OK) r = run_sort(k, idx, n, m, rest, (int)target, (int)key_type, st);
+    uint64_t *tmp = reinterpret_cast<uint64_t *>(rest);
+    if (r == GNS_OK)
+        r = launch_pdl("gather_u64_kernel", gather_u64_kernel, grid, 256, 0, st, tmp, (const uint64_t *)vals,
+                       (const uint32_t *)idx, (long long)n);
+    if (r == GNS_OK) r = check(cudaMemcpyAsync(vals, tmp, n * sizeof(uint64_t), cudaMemcpyDeviceToDevice, st), "copy");
+    if (own) {
+        gns_status f = check(cudaFreeAsync(w, st), "cudaFreeAsync");
+        if (r == GNS_OK) r = f;
+    }
+    return r;
 }
 
 gns_status gns_sort_omit(void *keys, gns_key_type key_type, uint32_t *vals, size_t n, gns_target target, void *ws,

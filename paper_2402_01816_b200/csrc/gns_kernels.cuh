@@ -1774,6 +1774,25 @@ omit_final_kernel(double *dk, uint32_t *dv, const double *bk, const uint32_t *bv
     pdl_trigger();
 }
 
+// NEXT f3: 64-bit payloads (gns_sort_keys_u64) ride as a u32 index through
+// the pairs sort, then are gathered: idx[i] = i before, tmp[i] = vals[idx[i]]
+// after (random 8-byte reads, coalesced writes).
+__global__ void __launch_bounds__(256) iota_u32_kernel(uint32_t *idx, long long n)
+{
+    pdl_wait();
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        idx[i] = (uint32_t)i;
+    pdl_trigger();
+}
+__global__ void __launch_bounds__(256) gather_u64_kernel(uint64_t *out, const uint64_t *vals, const uint32_t *idx,
+                                                          long long n)
+{
+    pdl_wait();
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        out[i] = vals[idx[i]];
+    pdl_trigger();
+}
+
 // GNS_DEBUG=1 pre-scan (R1): number of NaN keys (f64 only).
 __global__ void __launch_bounds__(256) nan_count_kernel(const double *k, long long n, unsigned *cnt)
 {

@@ -691,3 +691,50 @@ def test_concurrent_streams_and_threads(gns):
     for (k, v, frac), (gk, gv) in zip(cases, results):
         ek, ev = oracle.sort(k, v)
         assert_bitexact(gk, ek, gv, ev, what=f"n={k.size} frac={frac}")
+
+
+@pytest.mark.parametrize("key_type", ["f64", "i64", "u64"])
+@pytest.mark.parametrize("target", ["AscLeft", "DescLeft", "AscRight", "DescRight"])
+@pytest.mark.parametrize("n", [0, 1, 2, 777, T1, T1 + 1, 3 * T1 + 5, 100003, (1 << 20) + 3])
+def test_u64_payload(gns, n, target, key_type):
+    """NEXT f3: 64-bit payloads (gns_sort_keys_u64) vs the oracle: keys
+    bit-exact, payload[i] = the input payload of the key's stable position
+    (the oracle's index permutation), every target and key type; with and
+    without a caller workspace."""
+    rng = np.random.default_rng(n + len(target) + len(key_type))
+    if key_type == "f64":
+        k = synth.ties(n, 600 + n, 40)
+        k[::5] *= -1.0
+    else:
+        k = _int_keys(key_type, n, 600 + n)
+    pay = rng.integers(0, 1 << 64, n, dtype=np.uint64, endpoint=False)
+    ek, ev = oracle.sort_keys(k, synth.iota_u32(n), key_type, target)
+    for use_ws in (False, True):
+        tk = torch.from_numpy(k.copy()).cuda()
+        tp = torch.from_numpy(pay.copy()).cuda()
+        ws = (torch.empty(max(1, gns.workspace_bytes_u64(n)), dtype=torch.uint8, device="cuda") if use_ws else None)
+        gns.sort_u64_(tk, tp, workspace=ws, target=target)
+        torch.cuda.synchronize()
+        assert np.array_equal(tk.cpu().numpy().view(np.uint64), ek.view(np.uint64)), f"keys n={n} {target}"
+        assert np.array_equal(tp.cpu().numpy(), pay[ev.astype(np.int64)]), f"payload n={n} {target} ws={use_ws}"
+
+
+def test_u64_payload_full_size_and_errors(gns):
+    """BASELINE config 2 keys with a 64-bit payload at full size; argument
+    errors leave the data untouched."""
+    k = synth.config(2).keys
+    n = k.size
+    pay = np.arange(n, dtype=np.uint64) * np.uint64(0x9E3779B97F4A7C15)
+    ek, ev = oracle.sort(k, synth.iota_u32(n))
+    tk, tp = torch.from_numpy(k.copy()).cuda(), torch.from_numpy(pay).cuda()
+    gns.sort_u64_(tk, tp)
+    torch.cuda.synchronize()
+    assert np.array_equal(tk.cpu().numpy().view(np.uint64), ek.view(np.uint64))
+    assert np.array_equal(tp.cpu().numpy(), pay[ev.astype(np.int64)])
+    small = torch.empty(64, dtype=torch.uint8, device="cuda")
+    tk2, tp2 = torch.from_numpy(k[:3 * T1].copy()).cuda(), torch.from_numpy(pay[:3 * T1].copy()).cuda()
+    with pytest.raises(gns.GnsError) as ei:
+        gns.sort_u64_(tk2, tp2, workspace=small)
+    assert ei.value.status == 5
+    torch.cuda.synchronize()
+    assert np.array_equal(tk2.cpu().numpy(), k[:3 * T1]) and np.array_equal(tp2.cpu().numpy(), pay[:3 * T1])
