@@ -1788,7 +1788,22 @@ __global__ void __launch_bounds__(256) gather_u64_kernel(uint64_t *out, const ui
                                                           long long n)
 {
     pdl_wait();
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    // 8 outputs per thread and step: 8 independent random loads in flight
+    // (the gather is latency-bound), 16-byte index loads and stores
+    const long long n8 = n >> 3;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < n8; g += stride) {
+        const uint4 a = reinterpret_cast<const uint4 *>(idx)[2 * g];
+        const uint4 b = reinterpret_cast<const uint4 *>(idx)[2 * g + 1];
+        const uint64_t v0 = __ldg(vals + a.x), v1 = __ldg(vals + a.y), v2 = __ldg(vals + a.z), v3 = __ldg(vals + a.w);
+        const uint64_t v4 = __ldg(vals + b.x), v5 = __ldg(vals + b.y), v6 = __ldg(vals + b.z), v7 = __ldg(vals + b.w);
+        ulonglong2 *o = reinterpret_cast<ulonglong2 *>(out + 8 * g);
+        o[0] = make_ulonglong2(v0, v1);
+        o[1] = make_ulonglong2(v2, v3);
+        o[2] = make_ulonglong2(v4, v5);
+        o[3] = make_ulonglong2(v6, v7);
+    }
+    for (long long i = 8 * n8 + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += stride)
         out[i] = vals[idx[i]];
     pdl_trigger();
 }
