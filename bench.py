@@ -301,7 +301,8 @@ def main():
         "config": dict(config_json(case, args.frac), parallelism=f"replicas{world}" if world > 1 else "single"),
         "roofline": {"bound": "hbm", "kernel": "merge pass (merge_tstore_kernel: K2 co-rank search warps + K3 TMA-pipelined merge, one launch per pass), avg over "
                      f"{plan['merge_passes']} passes", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                     "frac": achieved / peak, "frac_vs_nominal_8tbs": achieved / 8000.0, "traffic": traffic,
+                     "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": 2 * n * s,
                      "share_of_step": roof["merge_share"],
                      "whole_sort": {"bytes_lower_bound": plan["bytes_lower_bound"],
