@@ -156,8 +156,9 @@ gns_status gns_sort_keys_u64(void *keys, gns_key_type key_type, uint64_t *vals, 
  * input whose every pair merges ends in the data array.  A run that ends in
  * the buffer is copied back once.  Presorted input moves no key; partially
  * presorted input (long ascending runs) moves only where runs overlap; random
- * input costs ~25 us of planning plus ~5 us per level over gns_sort_keys.  Arguments, alignment and
- * errors as gns_sort_keys (ws may be NULL: allocated stream-ordered).
+ * input costs ~25 us of planning plus ~5 us per level over gns_sort_keys.
+ * Arguments, alignment and errors as gns_sort_keys (ws may be NULL: allocated
+ * stream-ordered).
  * Octosort in the same schedule: a strictly reversed tile is
  * kept as a descending run, disjoint descending runs stay descending, a
  * descending run meeting anything else is reversed once; a descending result
@@ -167,12 +168,14 @@ gns_status gns_sort_omit(void *keys, gns_key_type key_type, uint32_t *vals, size
 
 /* ---- NEXT f4: the steps of the distributed sort (paper_2402_01816_b200.dist,
  * SURVEY.md §8(e); "parallelize over an arbitrary number of processes",
- * PAPER.md:353).  Each rank sorts its shard (gns_sort_keys), the ranks agree
- * on k-1 splitters (key, owner rank, position in the owner's sorted shard),
- * cut their shards at them (gns_split_cuts), exchange the pieces (one NCCL
- * all-to-all-v) and merge the k received sorted runs in rank order
- * (gns_merge_two, a pairwise tree).  Global order: (key, rank, position),
- * i.e. stable in the rank-major input order. */
+ * PAPER.md:353).  Each rank sorts its shard (gns_sort_keys), the ranks find
+ * the exact cuts at global ranks g N / k by rounds of proposals (key, owner
+ * rank, position in the owner's sorted shard) counted with gns_split_cuts and
+ * summed by one all-reduce (or, faster but unbalanced, cut at sample
+ * splitters), exchange the pieces (one NCCL all-to-all-v) and merge the k
+ * received sorted runs in rank order (gns_merge_two, a pairwise tree).
+ * Global order: (key, rank, position), i.e. stable in the rank-major input
+ * order. */
 
 /* cuts[i] = number of keys of sorted_keys[0:n) (this rank's sorted shard,
  * ascending in key_type order) that precede splitter i in the global order:
@@ -251,8 +254,8 @@ gns_status gns_merge_inplace_top(double *keys, uint32_t *vals, const double *lef
  * 3 co-rank partition, 4 in-place dependency ranges, 5 in-place merge,
  * 6 reversal, 7 splitter cuts, 8 sample gather, 9 Omitsort plan, 10 Omitsort
  * tile list + copies, 11 Omitsort final copy, 12 / 13 index and gather of
- * gns_sort_keys_u64, 0 other) in launch order, turns timing off and returns the number
- * of timed launches (-1 if timing was off or an event failed). */
+ * gns_sort_keys_u64, 0 other) in launch order, turns timing off and returns
+ * the number of timed launches (-1 if timing was off or an event failed). */
 gns_status gns_timing_begin(int max_launches);
 int gns_timing_end(float *ms, int *kind, int cap);
 
