@@ -133,9 +133,10 @@ def test_distributed_sort_gloo(world):
                                                     for g in range(world)], what
 
 
+@pytest.mark.parametrize("samples", [1, 16])
 @pytest.mark.parametrize("balanced", [True, False])
 @pytest.mark.parametrize("case", CASES)
-def test_simulate_matches_collective_cpu(case, balanced):
+def test_simulate_matches_collective_cpu(case, balanced, samples):
     """dist.simulate (one process, no collectives) == the oracle too; with
     exact co-ranks every piece has its balanced size."""
     import oracle
@@ -144,7 +145,7 @@ def test_simulate_matches_collective_cpu(case, balanced):
     shards = [make_shard(case, r, world) for r in range(world)]
     base = np.cumsum([0] + [s.size for s in shards])
     outs = gdist.simulate([(torch.from_numpy(s), torch.from_numpy((np.arange(s.size) + base[r]).astype(np.uint32)))
-                           for r, s in enumerate(shards)], samples=16, ops=CpuOracleOps(), balanced=balanced)
+                           for r, s in enumerate(shards)], samples=samples, ops=CpuOracleOps(), balanced=balanced)
     allk = np.concatenate(shards)
     kt = {np.dtype(np.float64): "f64", np.dtype(np.int64): "i64", np.dtype(np.uint64): "u64"}[allk.dtype]
     ek, ev = oracle.sort_keys(allk, np.arange(allk.size, dtype=np.uint32), kt)
