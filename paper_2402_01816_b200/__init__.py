@@ -67,6 +67,8 @@ _c = {
     "gns_sort_omit": _sig("gns_sort_omit", [_vp, _i, _vp, _sz, _i, _vp, _sz, _vp]),
     "gns_sort_keys_u64": _sig("gns_sort_keys_u64", [_vp, _i, _vp, _sz, _i, _vp, _sz, _vp]),
     "gns_workspace_bytes_u64": _sig("gns_workspace_bytes_u64", [_sz], _sz),
+    "gns_sort_f32": _sig("gns_sort_f32", [_vp, _vp, _sz, _i, _vp, _sz, _vp]),
+    "gns_workspace_bytes_f32": _sig("gns_workspace_bytes_f32", [_sz], _sz),
     "gns_split_cuts": _sig("gns_split_cuts", [_vp, _i, _sz, _vp, _vp, _vp, _i, _i, _vp, _vp]),
     "gns_merge_two": _sig("gns_merge_two", [_vp, _vp, _sz, _vp, _vp, _sz, _vp, _vp, _i, _vp]),
     "gns_plan": _sig("gns_plan", [_sz, _d, _i, ctypes.POINTER(gns_plan_info)]),
@@ -142,6 +144,14 @@ def gns_workspace_bytes_u64(n) -> int:
     return _c["gns_workspace_bytes_u64"](n)
 
 
+def gns_sort_f32(keys_ptr, vals_ptr, n, target, ws_ptr, ws_bytes, stream) -> int:
+    return _c["gns_sort_f32"](keys_ptr, vals_ptr, n, target, ws_ptr, ws_bytes, stream)
+
+
+def gns_workspace_bytes_f32(n) -> int:
+    return _c["gns_workspace_bytes_f32"](n)
+
+
 def gns_sort_omit(keys_ptr, key_type, vals_ptr, n, target, ws_ptr, ws_bytes, stream) -> int:
     return _c["gns_sort_omit"](keys_ptr, key_type, vals_ptr, n, target, ws_ptr, ws_bytes, stream)
 
@@ -192,7 +202,7 @@ def gns_timing_end(cap: int = 4096):
 
 LAUNCH_KINDS = {1: "tile_sort", 2: "merge_pass", 3: "partition", 4: "inplace_deps", 5: "inplace_merge", 6: "reverse",
                 7: "split_cuts", 8: "gather_samples", 9: "omit_plan", 10: "omit_prep", 11: "omit_final",
-                12: "iota", 13: "gather_u64"}
+                12: "iota", 13: "gather_u64", 14: "f32_pack", 15: "f32_gather"}
 
 
 def gns_tile_elems() -> int:
@@ -269,6 +279,30 @@ def sort_u64_(keys, vals, workspace=None, stream=None, target: str = "AscLeft"):
 
 def workspace_bytes_u64(n: int) -> int:
     return gns_workspace_bytes_u64(n)
+
+
+def sort_f32_(keys, vals=None, workspace=None, stream=None, target: str = "AscLeft"):
+    """NEXT f3: stable sort of float32 ``keys`` (and uint32 ``vals``) on the
+    GPU (gns_sort_f32; packed 64-bit words through the uint64 key path, %RAM
+    5.0 key-only / 3.0 with vals).  ``workspace``: optional uint8 CUDA tensor
+    of >= workspace_bytes_f32(n) bytes."""
+    import torch
+    if keys.dtype != torch.float32 or not keys.is_cuda or not keys.is_contiguous():
+        raise TypeError("keys must be a contiguous CUDA float32 tensor")
+    if vals is not None:
+        if vals.dtype != torch.uint32 or not vals.is_cuda or not vals.is_contiguous():
+            raise TypeError("vals must be a contiguous CUDA uint32 tensor")
+        if vals.numel() != keys.numel():
+            raise ValueError("keys and vals differ in length")
+    n = keys.numel()
+    wp = _ptr(workspace) if workspace is not None else None
+    wb = workspace.numel() * workspace.element_size() if workspace is not None else 0
+    _check(gns_sort_f32(_ptr(keys), _ptr(vals), n, TARGETS[target], wp, wb, _stream_handle(stream)), "sort_f32_")
+    return keys, vals
+
+
+def workspace_bytes_f32(n: int) -> int:
+    return gns_workspace_bytes_f32(n)
 
 
 def sort_omit_(keys, vals=None, workspace=None, stream=None, target: str = "AscLeft"):

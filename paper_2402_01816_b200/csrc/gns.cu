@@ -321,8 +321,9 @@ int launch_kind(const char *what)
     static const char *names[] = {"tile_sort2_kernel", "merge_tstore_kernel", "partition_kernel",
                                   "inplace_deps_kernel", "merge_inplace_kernel", "reverse_kernel",
                                   "split_cuts_kernel", "gather_samples_kernel", "omit_plan_kernel",
-                                  "omit_prep_kernel", "omit_final_kernel", "iota_u32_kernel", "gather_u64_kernel"};
-    for (int i = 0; i < 13; ++i)
+                                  "omit_prep_kernel", "omit_final_kernel", "iota_u32_kernel", "gather_u64_kernel",
+                                  "f32_pack_kernel", "f32_gather_kernel"};
+    for (int i = 0; i < 15; ++i)
         if (std::strcmp(what, names[i]) == 0) return i + 1;
     return 0;
 }
@@ -963,6 +964,69 @@ gns_status gns_sort_keys_u64(void *keys, gns_key_type key_type, uint64_t *vals, 
         r = launch_pdl("gather_u64_kernel", gather_u64_kernel, grid, 256, 0, st, tmp, (const uint64_t *)vals,
                        (const uint32_t *)idx, (long long)n);
     if (r == GNS_OK) r = check(cudaMemcpyAsync(vals, tmp, n * sizeof(uint64_t), cudaMemcpyDeviceToDevice, st), "copy");
+    if (own) {
+        gns_status f = check(cudaFreeAsync(w, st), "cudaFreeAsync");
+        if (r == GNS_OK) r = f;
+    }
+    return r;
+}
+
+size_t gns_workspace_bytes_f32(size_t n)
+{
+    Mode m;
+    if (mode_for(1.0, n, &m) != GNS_OK || n > GNS_MAX_N) return 0;
+    if (n <= 1) return 0;
+    // the words, then the u64 sort's workspace (>= 2 x 4n for the gathered keys and vals)
+    return align_up(n * sizeof(uint64_t), 256) +
+           std::max(layout(n, m, false).total, 2 * align_up(n * sizeof(uint32_t), 256));
+}
+
+gns_status gns_sort_f32(float *keys, uint32_t *vals, size_t n, gns_target target, void *ws, size_t ws_bytes,
+                        gns_stream_t stream)
+{
+    if ((int)target < 0 || (int)target > 3) return fail(GNS_ERR_INVALID_ARGUMENT, "target must be 0..3");
+    if (n > GNS_MAX_N) return fail(GNS_ERR_INVALID_ARGUMENT, "n > GNS_MAX_N");
+    if (n && !keys) return fail(GNS_ERR_INVALID_ARGUMENT, "NULL keys with n > 0");
+    if (n && (!is_aligned(keys, 32) || (vals && !is_aligned(vals, 32))))
+        return fail(GNS_ERR_MISALIGNED, "keys/vals must be 32-byte aligned");
+    if (n <= 1) return GNS_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t need = gns_workspace_bytes_f32(n);
+    unsigned char *w = (unsigned char *)ws;
+    if (w) {
+        if (ws_bytes < need) return fail(GNS_ERR_WORKSPACE_TOO_SMALL, "workspace too small");
+        if (!is_aligned(w, 32)) return fail(GNS_ERR_MISALIGNED, "ws must be 32-byte aligned");
+    }
+    GNS_TRY(ensure_attrs());
+    bool own = false;
+    if (!w) {
+        cudaError_t e = cudaMallocAsync((void **)&w, need, st);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            if (e == cudaErrorMemoryAllocation) return fail(GNS_ERR_OUT_OF_MEMORY, "cudaMallocAsync: out of memory");
+            return check(e, "cudaMallocAsync");
+        }
+        own = true;
+    }
+    unsigned long long *words = reinterpret_cast<unsigned long long *>(w);
+    unsigned char *rest = w + align_up(n * sizeof(uint64_t), 256);     // the u64 sort's workspace, then the gather
+    const int desc = (target == 2 || target == 3) ? 1 : 0;
+    const int right = (target == 1 || target == 3) ? 1 : 0;
+    Mode m;
+    gns_status r = mode_for(1.0, n, &m);
+    const unsigned grid = (unsigned)std::min<size_t>(ceil_div(n, 256), (size_t)num_sms() * 8);
+    if (r == GNS_OK)
+        r = launch_pdl("f32_pack_kernel", f32_pack_kernel, grid, 256, 0, st, (const uint32_t *)keys, words,
+                       (long long)n, desc, right);
+    if (r == GNS_OK) r = run_sort(reinterpret_cast<double *>(words), nullptr, n, m, rest, 0, KT_U64, st);
+    uint32_t *tk = reinterpret_cast<uint32_t *>(rest);
+    uint32_t *tv = reinterpret_cast<uint32_t *>(rest + align_up(n * sizeof(uint32_t), 256));
+    if (r == GNS_OK)
+        r = launch_pdl("f32_gather_kernel", f32_gather_kernel, grid, 256, 0, st, (const unsigned long long *)words,
+                       (const uint32_t *)keys, (const uint32_t *)vals, tk, vals ? tv : (uint32_t *)nullptr,
+                       (long long)n, right);
+    if (r == GNS_OK) r = check(cudaMemcpyAsync(keys, tk, n * 4, cudaMemcpyDeviceToDevice, st), "copy");
+    if (r == GNS_OK && vals) r = check(cudaMemcpyAsync(vals, tv, n * 4, cudaMemcpyDeviceToDevice, st), "copy");
     if (own) {
         gns_status f = check(cudaFreeAsync(w, st), "cudaFreeAsync");
         if (r == GNS_OK) r = f;

@@ -738,3 +738,50 @@ def test_u64_payload_full_size_and_errors(gns):
     assert ei.value.status == 5
     torch.cuda.synchronize()
     assert np.array_equal(tk2.cpu().numpy(), k[:3 * T1]) and np.array_equal(tp2.cpu().numpy(), pay[:3 * T1])
+
+
+def _f32_keys(n, seed):
+    """Seeded binary32 keys with ties, signed zeros, infinities, subnormals."""
+    rng = np.random.default_rng(seed)
+    k = (rng.standard_normal(n) * 1e3).astype(np.float32)
+    k[::7] = rng.integers(-20, 20, k[::7].size).astype(np.float32)          # ties
+    ext = np.array([0.0, -0.0, np.inf, -np.inf, 1e-45, -1e-45, 3.4e38, -3.4e38], dtype=np.float32)
+    k[::13] = ext[np.arange(k[::13].size) % ext.size]
+    return k
+
+
+@pytest.mark.parametrize("payload", [False, True])
+@pytest.mark.parametrize("target", ["AscLeft", "DescLeft", "AscRight", "DescRight"])
+@pytest.mark.parametrize("n", [0, 1, 2, 777, T1, T1 + 1, 3 * T1 + 5, 100003, (1 << 20) + 3])
+def test_f32_keys(gns, n, target, payload):
+    """NEXT f3: binary32 keys (gns_sort_f32) vs the oracle: the oracle sorts
+    the exactly widened keys (same IEEE order, -0.0 == +0.0) with the index as
+    payload; the expected output is the input permuted by that stable order,
+    bit-exact (signed zeros keep their bits)."""
+    k = _f32_keys(n, 900 + n + len(target))
+    v = synth.iota_u32(n)[::-1].copy() if payload else None
+    _, ev = oracle.sort_target(k.astype(np.float64), synth.iota_u32(n), target)
+    perm = ev.astype(np.int64)
+    for use_ws in (False, True):
+        tk = torch.from_numpy(k.copy()).cuda()
+        tv = None if v is None else torch.from_numpy(v.copy()).cuda()
+        ws = (torch.empty(max(1, gns.workspace_bytes_f32(n)), dtype=torch.uint8, device="cuda") if use_ws else None)
+        gns.sort_f32_(tk, tv, workspace=ws, target=target)
+        torch.cuda.synchronize()
+        assert np.array_equal(tk.cpu().numpy().view(np.uint32), k[perm].view(np.uint32)), f"keys n={n} {target}"
+        if v is not None:
+            assert np.array_equal(tv.cpu().numpy(), v[perm]), f"vals n={n} {target}"
+
+
+def test_f32_keys_full_size(gns):
+    """2^24 binary32 keys with payload at full size, vs the oracle."""
+    n = 1 << 24
+    k = _f32_keys(n, 4242)
+    v = synth.iota_u32(n)
+    _, ev = oracle.sort(k.astype(np.float64), v)
+    tk, tv = torch.from_numpy(k.copy()).cuda(), torch.from_numpy(v.copy()).cuda()
+    gns.sort_f32_(tk, tv)
+    torch.cuda.synchronize()
+    perm = ev.astype(np.int64)
+    assert np.array_equal(tk.cpu().numpy().view(np.uint32), k[perm].view(np.uint32))
+    assert np.array_equal(tv.cpu().numpy(), v[perm])
