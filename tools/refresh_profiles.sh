@@ -15,3 +15,4 @@ PY
 cp gpurun_out/launches.csv profiles/r1_launches.csv
 (tail -3 gpurun_out/pytest_gpu.log; echo "--- bounds-asserting build (GNS_LIB=libgns_debug.so):"; tail -1 gpurun_out/pytest_gpu_debug.log) > profiles/r1_pytest_gpu.txt
 echo refreshed
+python tools/sass_evidence.py > /dev/null

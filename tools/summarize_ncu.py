@@ -119,7 +119,7 @@ def main():
                 f"{g('smsp__issue_active.avg.pct_of_peak_sustained_active')} | {g('launch__registers_per_thread')} | "
                 f"{g('sm__warps_active.avg.per_cycle_active')} | "
                 f"{g('l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum')} / "
-                f"{g('l1tex__data_pipe_lsu_wavefronts_mem_shared.sum')} | see SASS |")
+                f"{g('l1tex__data_pipe_lsu_wavefronts_mem_shared.sum')} | profiles/r1_sass_tma.txt |")
     except Exception as e:  # noqa: BLE001
         lines.append(f"(full capture unavailable: {e})")
     open(os.path.join(PROF, f"{TAG}_ncu_summary.md"), "w").write("\n".join(lines) + "\n")
