@@ -145,17 +145,13 @@ gns_status gns_sort_keys_u64(void *keys, gns_key_type key_type, uint64_t *vals, 
 
 /* NEXT f3: binary32 keys.  keys[n] (float) are replaced by their stable sort
  * for `target` (IEEE order, -0.0 == +0.0 with stability fixing their order,
- * every key keeps its bits); vals[n] (u32, or NULL) move with them.  Each key
- * and its input index are packed into one 64-bit word whose unsigned order
- * is the target order of (key, index) -- ties broken by the index, ascending
- * for the Left targets and descending for the Right ones -- the words are
- * sorted by the uint64 key path (full buffer), and keys and vals are gathered
- * back by the index.  Not footprint-native: workspace = 8n + max(the uint64
- * sort's buffer 8n, 8n) bytes, %RAM 5.0 key-only / 3.0 with vals (a 4-byte
- * key kernel set would give 2.0; next).  ws: NULL (allocated
- * stream-ordered) or gns_workspace_bytes_f32(n) bytes, 32-byte aligned.
- * NaN keys: precondition violation (sorted after +inf in the ascending
- * order, but unspecified).  Errors as gns_sort_keys. */
+ * every key keeps its bits); vals[n] (u32, or NULL) move with them.  Its own
+ * 4-byte kernels (csrc/gns_f32.cuh): the same schedule as the f64 full-buffer
+ * sort -- one tile-sort pass (8192-key tiles, every level on chip), then one
+ * HBM merge pass per level, ping-pong with a buffer of n keys (+ n vals):
+ * %RAM 2.0.  ws: NULL (allocated stream-ordered) or gns_workspace_bytes_f32(n)
+ * bytes (0 for n <= 8192), 32-byte aligned.  NaN keys: precondition
+ * violation.  Errors as gns_sort_keys. */
 size_t gns_workspace_bytes_f32(size_t n);
 gns_status gns_sort_f32(float *keys, uint32_t *vals, size_t n, gns_target target, void *ws, size_t ws_bytes,
                         gns_stream_t stream);
@@ -271,7 +267,7 @@ gns_status gns_merge_inplace_top(double *keys, uint32_t *vals, const double *lef
  * 3 co-rank partition, 4 in-place dependency ranges, 5 in-place merge,
  * 6 reversal, 7 splitter cuts, 8 sample gather, 9 Omitsort plan, 10 Omitsort
  * tile list + copies, 11 Omitsort final copy, 12 / 13 index and gather of
- * gns_sort_keys_u64, 14 / 15 pack and gather of gns_sort_f32, 0 other) in
+ * gns_sort_keys_u64, 0 other -- incl. the binary32 kernels) in
  * launch order, turns timing off and returns the number of timed launches
  * (-1 if timing was off or an event failed). */
 gns_status gns_timing_begin(int max_launches);

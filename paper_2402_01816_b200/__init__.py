@@ -202,7 +202,7 @@ def gns_timing_end(cap: int = 4096):
 
 LAUNCH_KINDS = {1: "tile_sort", 2: "merge_pass", 3: "partition", 4: "inplace_deps", 5: "inplace_merge", 6: "reverse",
                 7: "split_cuts", 8: "gather_samples", 9: "omit_plan", 10: "omit_prep", 11: "omit_final",
-                12: "iota", 13: "gather_u64", 14: "f32_pack", 15: "f32_gather"}
+                12: "iota", 13: "gather_u64"}
 
 
 def gns_tile_elems() -> int:
@@ -283,9 +283,9 @@ def workspace_bytes_u64(n: int) -> int:
 
 def sort_f32_(keys, vals=None, workspace=None, stream=None, target: str = "AscLeft"):
     """NEXT f3: stable sort of float32 ``keys`` (and uint32 ``vals``) on the
-    GPU (gns_sort_f32; packed 64-bit words through the uint64 key path, %RAM
-    5.0 key-only / 3.0 with vals).  ``workspace``: optional uint8 CUDA tensor
-    of >= workspace_bytes_f32(n) bytes."""
+    GPU (gns_sort_f32: the 4-byte kernel set, full buffer, %RAM 2.0).
+    ``workspace``: optional uint8 CUDA tensor of >= workspace_bytes_f32(n)
+    bytes."""
     import torch
     if keys.dtype != torch.float32 or not keys.is_cuda or not keys.is_contiguous():
         raise TypeError("keys must be a contiguous CUDA float32 tensor")

@@ -7,6 +7,7 @@
 // calls into the oracle or any CPU sort.
 #include "../../include/gns.h"
 #include "gns_kernels.cuh"
+#include "gns_f32.cuh"
 
 #include <cuda_runtime.h>
 #include <cstdio>
@@ -175,6 +176,20 @@ OmitPlanK omit_plan_kern(int o)
                                       &omit_plan_kernel<3>, &omit_plan_kernel<4>, &omit_plan_kernel<5>};
     return t[o];
 }
+using F32TileK = decltype(&f32_tile_sort_kernel<false, false>);
+using F32MergeK = decltype(&f32_merge_kernel<false, false>);
+F32TileK f32_tile_kern(bool hv, int desc)
+{
+    static const F32TileK t[2][2] = {{&f32_tile_sort_kernel<false, false>, &f32_tile_sort_kernel<false, true>},
+                                     {&f32_tile_sort_kernel<true, false>, &f32_tile_sort_kernel<true, true>}};
+    return t[hv][desc];
+}
+F32MergeK f32_merge_kern(bool hv, int desc)
+{
+    static const F32MergeK t[2][2] = {{&f32_merge_kernel<false, false>, &f32_merge_kernel<false, true>},
+                                      {&f32_merge_kernel<true, false>, &f32_merge_kernel<true, true>}};
+    return t[hv][desc];
+}
 InplK inplace_kern(bool hv, int o)
 {
     static const InplK t[2][NORD] = {GNS_ORDS(merge_inplace_kernel, false), GNS_ORDS(merge_inplace_kernel, true)};
@@ -222,6 +237,7 @@ gns_status ensure_attrs()
         for (int hv = 0; hv < 2; ++hv) {
             GNS_ATTR(merge_kern(hv, o), ts_smem(hv));
             GNS_ATTR(merge_kern_ol(hv, o), ts_smem(hv));
+            if (o < 2) GNS_ATTR(f32_tile_kern(hv, o), f_tile_smem(hv));
             if (!hv) GNS_ATTR(omit_plan_kern(o), OMIT_SMEM);
             GNS_ATTR(inplace_kern(hv, o), ts_smem(hv));
             GNS_ATTR(tile_kern(hv, o), t1_smem(hv));
@@ -322,8 +338,8 @@ int launch_kind(const char *what)
                                   "inplace_deps_kernel", "merge_inplace_kernel", "reverse_kernel",
                                   "split_cuts_kernel", "gather_samples_kernel", "omit_plan_kernel",
                                   "omit_prep_kernel", "omit_final_kernel", "iota_u32_kernel", "gather_u64_kernel",
-                                  "f32_pack_kernel", "f32_gather_kernel"};
-    for (int i = 0; i < 15; ++i)
+                                  "f32_tile_sort_kernel", "f32_merge_kernel", "f32_reverse_kernel"};
+    for (int i = 0; i < 16; ++i)
         if (std::strcmp(what, names[i]) == 0) return i + 1;
     return 0;
 }
@@ -973,12 +989,9 @@ gns_status gns_sort_keys_u64(void *keys, gns_key_type key_type, uint64_t *vals, 
 
 size_t gns_workspace_bytes_f32(size_t n)
 {
-    Mode m;
-    if (mode_for(1.0, n, &m) != GNS_OK || n > GNS_MAX_N) return 0;
-    if (n <= 1) return 0;
-    // the words, then the u64 sort's workspace (>= 2 x 4n for the gathered keys and vals)
-    return align_up(n * sizeof(uint64_t), 256) +
-           std::max(layout(n, m, false).total, 2 * align_up(n * sizeof(uint32_t), 256));
+    // the buffer: n keys + n vals (enough with or without payload); none for one tile
+    if (n > GNS_MAX_N || n <= (size_t)F_TILE) return 0;
+    return 2 * align_up(n * sizeof(float), 256);
 }
 
 gns_status gns_sort_f32(float *keys, uint32_t *vals, size_t n, gns_target target, void *ws, size_t ws_bytes,
@@ -993,13 +1006,13 @@ gns_status gns_sort_f32(float *keys, uint32_t *vals, size_t n, gns_target target
     cudaStream_t st = (cudaStream_t)stream;
     const size_t need = gns_workspace_bytes_f32(n);
     unsigned char *w = (unsigned char *)ws;
-    if (w) {
+    if (need && w) {
         if (ws_bytes < need) return fail(GNS_ERR_WORKSPACE_TOO_SMALL, "workspace too small");
         if (!is_aligned(w, 32)) return fail(GNS_ERR_MISALIGNED, "ws must be 32-byte aligned");
     }
     GNS_TRY(ensure_attrs());
     bool own = false;
-    if (!w) {
+    if (need && !w) {
         cudaError_t e = cudaMallocAsync((void **)&w, need, st);
         if (e != cudaSuccess) {
             cudaGetLastError();
@@ -1008,25 +1021,31 @@ gns_status gns_sort_f32(float *keys, uint32_t *vals, size_t n, gns_target target
         }
         own = true;
     }
-    unsigned long long *words = reinterpret_cast<unsigned long long *>(w);
-    unsigned char *rest = w + align_up(n * sizeof(uint64_t), 256);     // the u64 sort's workspace, then the gather
-    const int desc = (target == 2 || target == 3) ? 1 : 0;
-    const int right = (target == 1 || target == 3) ? 1 : 0;
-    Mode m;
-    gns_status r = mode_for(1.0, n, &m);
-    const unsigned grid = (unsigned)std::min<size_t>(ceil_div(n, 256), (size_t)num_sms() * 8);
-    if (r == GNS_OK)
-        r = launch_pdl("f32_pack_kernel", f32_pack_kernel, grid, 256, 0, st, (const uint32_t *)keys, words,
-                       (long long)n, desc, right);
-    if (r == GNS_OK) r = run_sort(reinterpret_cast<double *>(words), nullptr, n, m, rest, 0, KT_U64, st);
-    uint32_t *tk = reinterpret_cast<uint32_t *>(rest);
-    uint32_t *tv = reinterpret_cast<uint32_t *>(rest + align_up(n * sizeof(uint32_t), 256));
-    if (r == GNS_OK)
-        r = launch_pdl("f32_gather_kernel", f32_gather_kernel, grid, 256, 0, st, (const unsigned long long *)words,
-                       (const uint32_t *)keys, (const uint32_t *)vals, tk, vals ? tv : (uint32_t *)nullptr,
-                       (long long)n, right);
-    if (r == GNS_OK) r = check(cudaMemcpyAsync(keys, tk, n * 4, cudaMemcpyDeviceToDevice, st), "copy");
-    if (r == GNS_OK && vals) r = check(cudaMemcpyAsync(vals, tv, n * 4, cudaMemcpyDeviceToDevice, st), "copy");
+    const bool hv = vals != nullptr;
+    const bool right = target == 1 || target == 3;
+    const int desc = (target == 2 || target == 1) ? 1 : 0;      // AscRight = reverse(DescLeft)
+    float *bk = reinterpret_cast<float *>(w);
+    uint32_t *bv = hv ? reinterpret_cast<uint32_t *>(w + align_up(n * sizeof(float), 256)) : nullptr;
+    const int M = merge_passes_for(n);                // (F_TILE == TILE: the same level count)
+    // the tile sort's destination by the parity of the merge levels: the last pass lands in keys
+    float *ck = (M & 1) ? bk : keys, *ok = (M & 1) ? keys : bk;
+    uint32_t *cv = (M & 1) ? bv : vals, *ov = (M & 1) ? vals : bv;
+    gns_status r = launch_pdl("f32_tile_sort_kernel", f32_tile_kern(hv, desc), (unsigned)ceil_div(n, F_TILE), F_NT,
+                              f_tile_smem(hv), st, (const float *)keys, (const uint32_t *)vals, ck, cv, (long long)n);
+    for (int p = 0; p < M && r == GNS_OK; ++p) {
+        const long long L = (long long)F_TILE << p;
+        r = launch_pdl("f32_merge_kernel", f32_merge_kern(hv, desc), (unsigned)ceil_div(n, F_MTILE), F_NT, 0, st,
+                       (const float *)ck, (const uint32_t *)cv, ok, ov, (long long)n, L);
+        std::swap(ck, ok);
+        std::swap(cv, ov);
+    }
+    if (r == GNS_OK && right) {
+        const unsigned grid = (unsigned)std::min<size_t>(ceil_div(n / 2, 256), (size_t)num_sms() * 8);
+        r = hv ? launch_pdl("f32_reverse_kernel", f32_reverse_kernel<true>, std::max(1u, grid), 256, 0, st, keys,
+                            vals, (long long)n)
+               : launch_pdl("f32_reverse_kernel", f32_reverse_kernel<false>, std::max(1u, grid), 256, 0, st, keys,
+                            (uint32_t *)nullptr, (long long)n);
+    }
     if (own) {
         gns_status f = check(cudaFreeAsync(w, st), "cudaFreeAsync");
         if (r == GNS_OK) r = f;

@@ -1,0 +1,239 @@
+// gns_f32.cuh — NEXT f3: the binary32 key path on its own 4-byte kernels
+// (footprint-native: buffer n keys (+ n u32 vals), %RAM 2.0 like the f64
+// path).  Same method as the f64 path (PAPER.md:150/219/221: one tile-sort
+// pass with every level on chip, then one HBM pass per merge level, ping-pong
+// between the data and the buffer, the left run winning ties), simpler
+// kernels: no TMA, one CTA per output tile, the tile's splits searched in
+// global memory by 32-lane groups.
+//   F1  f32_tile_sort_kernel  stable sort of 8192-key tiles (registers + smem)
+//   F2  f32_merge_kernel      one merge level, 4096 outputs per CTA
+// DESC selects the descending key order; ties always keep input order.
+#pragma once
+
+namespace gns {
+
+constexpr int F_NT = 256;                 // threads per CTA
+constexpr int F_VT = 32;                  // keys per thread in the tile sort
+constexpr int F_TILE = F_NT * F_VT;       // 8192 keys per tile (level-0 run)
+constexpr int F_MVT = 16;                 // outputs per thread in a merge pass
+constexpr int F_MTILE = F_NT * F_MVT;     // 4096 outputs per merge CTA
+constexpr size_t f_tile_smem(bool hv) { return (size_t)F_TILE * (hv ? 8 : 4); }
+static_assert(F_TILE % F_MTILE == 0, "pair boundaries on merge-tile boundaries");
+static_assert(F_TILE == TILE, "the f32 path shares the f64 path's level count (merge_passes_for)");
+
+template <bool DESC>
+__device__ __forceinline__ bool fbefore(float a, float b) { return DESC ? (a > b) : (a < b); }
+
+// key pads after every real key (the stable sort keeps real infinities first)
+template <bool DESC>
+__device__ __forceinline__ float fpad() { return DESC ? -__int_as_float(0x7f800000) : __int_as_float(0x7f800000); }
+
+// shared-memory slot of tile element e: the 32-element row index XORed into
+// the column, so the blocked accesses (thread t, element 32t + x) and the
+// stride-16 merge reads spread over the 32 banks
+__device__ __forceinline__ int fswz(int e) { return e ^ ((e >> 5) & 31); }
+
+// ------------------------------------------------------------------ F1
+template <bool HV, bool DESC>
+__global__ void __launch_bounds__(F_NT, HV ? 2 : 3)
+f32_tile_sort_kernel(const float *src_k, const uint32_t *src_v, float *dst_k, uint32_t *dst_v, long long n)
+{
+    pdl_wait();
+    extern __shared__ __align__(16) unsigned char f_smem[];      // keys [8192] (+ vals [8192])
+    float *sk = reinterpret_cast<float *>(f_smem);
+    uint32_t *sv = reinterpret_cast<uint32_t *>(f_smem + F_TILE * sizeof(float));
+    const int tid = threadIdx.x;
+    const long long base = (long long)blockIdx.x * F_TILE;
+    const int cnt = (int)min((long long)F_TILE, n - base);
+    for (int e = tid; e < F_TILE; e += F_NT) {          // coalesced loads
+        sk[fswz(e)] = e < cnt ? src_k[base + e] : fpad<DESC>();
+        if (HV) sv[fswz(e)] = e < cnt ? src_v[base + e] : 0u;
+    }
+    __syncthreads();
+    const int e0 = tid * F_VT;
+    float k[F_VT];
+    uint32_t v[F_VT];
+#pragma unroll
+    for (int x = 0; x < F_VT; ++x) {
+        k[x] = sk[fswz(e0 + x)];
+        if (HV) v[x] = sv[fswz(e0 + x)];
+    }
+    // stable odd-even transposition sort of the thread's 32 keys
+#pragma unroll
+    for (int r = 0; r < F_VT; ++r) {
+#pragma unroll
+        for (int i = r & 1; i + 1 < F_VT; i += 2) {
+            const bool p = fbefore<DESC>(k[i + 1], k[i]);
+            const float lo = p ? k[i + 1] : k[i], hi = p ? k[i] : k[i + 1];
+            k[i] = lo;
+            k[i + 1] = hi;
+            if (HV) {
+                const uint32_t vl = p ? v[i + 1] : v[i], vh = p ? v[i] : v[i + 1];
+                v[i] = vl;
+                v[i + 1] = vh;
+            }
+        }
+    }
+    // shared-memory merge rounds: runs of 32 -> 8192 (merge path + serial merge)
+#pragma unroll 1
+    for (int coop = 2; coop <= F_NT; coop <<= 1) {
+        __syncthreads();
+#pragma unroll
+        for (int x = 0; x < F_VT; ++x) {
+            sk[fswz(e0 + x)] = k[x];
+            if (HV) sv[fswz(e0 + x)] = v[x];
+        }
+        __syncthreads();
+        const int local = tid & (coop - 1);
+        const int a0 = (tid - local) * F_VT;
+        const int run = (coop >> 1) * F_VT;
+        const int b0 = a0 + run;
+        const int d = local * F_VT;
+        int lo = max(0, d - run), hi = min(d, run);
+        while (lo < hi) {                                // co-rank: A[m] <= B[d-1-m]
+            const int m = (lo + hi) >> 1;
+            if (!fbefore<DESC>(sk[fswz(b0 + d - 1 - m)], sk[fswz(a0 + m)])) lo = m + 1;
+            else hi = m;
+        }
+        int ai = a0 + lo, bi = b0 + d - lo;
+        const int aend = a0 + run, bend = b0 + run;
+#pragma unroll
+        for (int x = 0; x < F_VT; ++x) {
+            const float ka = ai < aend ? sk[fswz(ai)] : 0.f, kb = bi < bend ? sk[fswz(bi)] : 0.f;
+            const bool p = (bi < bend) && ((ai >= aend) || fbefore<DESC>(kb, ka));
+            k[x] = p ? kb : ka;
+            if (HV) v[x] = sv[fswz(p ? bi : ai)];
+            if (p) ++bi;
+            else ++ai;
+        }
+    }
+    // the thread's 32 outputs are elements e0.. of the sorted tile
+    if (cnt == F_TILE) {
+        float4 *dk = reinterpret_cast<float4 *>(dst_k + base + e0);
+#pragma unroll
+        for (int c = 0; c < F_VT / 4; ++c) dk[c] = make_float4(k[4 * c], k[4 * c + 1], k[4 * c + 2], k[4 * c + 3]);
+        if (HV) {
+            uint4 *dv = reinterpret_cast<uint4 *>(dst_v + base + e0);
+#pragma unroll
+            for (int c = 0; c < F_VT / 4; ++c) dv[c] = make_uint4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+        }
+    } else {
+#pragma unroll
+        for (int x = 0; x < F_VT; ++x)
+            if (e0 + x < cnt) {
+                dst_k[base + e0 + x] = k[x];
+                if (HV) dst_v[base + e0 + x] = v[x];
+            }
+    }
+    pdl_trigger();
+}
+
+// Stable co-rank of output position d of the merge of A[0:na) and B[0:nb)
+// (A wins ties) by the 32 lanes of a warp, in global memory.
+template <bool DESC>
+__device__ __forceinline__ int f32_corank(const float *A, int na, const float *B, int nb, int d, int lane)
+{
+    const int lo = max(0, d - nb), hi = min(d, na);
+    if (lo >= hi) return lo;
+    return lo + group_count_true<32>(lo, hi - 1, lane, 0xFFFFFFFFu, 0,
+                                     [&](int m) { return !fbefore<DESC>(B[d - 1 - m], A[m]); });
+}
+
+// ------------------------------------------------------------------ F2
+// One merge level: pair q = runs [2qL, 2qL+L) and [2qL+L, 2qL+2L) of src
+// (clipped to n) into the same range of dst; CTA t writes outputs
+// [4096 t, 4096 t + 4096).
+template <bool HV, bool DESC>
+__global__ void __launch_bounds__(F_NT)
+f32_merge_kernel(const float *src_k, const uint32_t *src_v, float *dst_k, uint32_t *dst_v, long long n, long long L)
+{
+    pdl_wait();
+    __shared__ float sa[F_MTILE + 1];
+    __shared__ uint32_t va[HV ? F_MTILE + 1 : 1];
+    __shared__ int s_split[2];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const long long t0 = (long long)blockIdx.x * F_MTILE;
+    const long long pb = (t0 / (2 * L)) * (2 * L);          // the pair's first element
+    const int na = (int)min(L, n - pb);
+    const int nb = (int)max(0LL, min(L, n - pb - L));
+    const int k0 = (int)(t0 - pb);
+    const int k1 = (int)min((long long)k0 + F_MTILE, (long long)na + nb);
+    const float *A = src_k + pb, *B = src_k + pb + L;
+    if (warp < 2) {
+        const int d = warp == 0 ? k0 : k1;
+        const int c = f32_corank<DESC>(A, na, B, nb, d, lane);
+        if (lane == 0) s_split[warp] = c;
+    }
+    __syncthreads();
+    const int i0 = s_split[0], i1 = s_split[1];
+    const int j0 = k0 - i0, j1 = k1 - i1;
+    const int ca = i1 - i0, cb = j1 - j0, cnt = ca + cb;
+    // the tile's inputs: A[i0:i1) at [0, ca), B[j0:j1) at [ca, cnt)
+    for (int e = tid; e < cnt; e += F_NT) {
+        const bool fa = e < ca;
+        sa[e] = fa ? A[i0 + e] : B[j0 + e - ca];
+        if (HV) va[e] = fa ? src_v[pb + i0 + e] : src_v[pb + L + j0 + e - ca];
+    }
+    __syncthreads();
+    const int d = tid * F_MVT;
+    if (d < cnt) {
+        int lo = max(0, d - cb), hi = min(d, ca);
+        while (lo < hi) {
+            const int m = (lo + hi) >> 1;
+            if (!fbefore<DESC>(sa[ca + d - 1 - m], sa[m])) lo = m + 1;
+            else hi = m;
+        }
+        int ai = lo, bi = ca + d - lo;
+        float k[F_MVT];
+        uint32_t v[F_MVT];
+#pragma unroll
+        for (int x = 0; x < F_MVT; ++x) {
+            const float ka = ai < ca ? sa[ai] : 0.f, kb = bi < cnt ? sa[bi] : 0.f;
+            const bool p = (bi < cnt) && ((ai >= ca) || fbefore<DESC>(kb, ka));
+            k[x] = p ? kb : ka;
+            if (HV) v[x] = va[p ? bi : ai];
+            if (p) ++bi;
+            else ++ai;
+        }
+        const long long o = t0 + d;
+        if (d + F_MVT <= cnt && (o & 3) == 0) {
+            float4 *ok = reinterpret_cast<float4 *>(dst_k + o);
+#pragma unroll
+            for (int c = 0; c < F_MVT / 4; ++c) ok[c] = make_float4(k[4 * c], k[4 * c + 1], k[4 * c + 2], k[4 * c + 3]);
+            if (HV) {
+                uint4 *ov = reinterpret_cast<uint4 *>(dst_v + o);
+#pragma unroll
+                for (int c = 0; c < F_MVT / 4; ++c) ov[c] = make_uint4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+            }
+        } else {
+#pragma unroll
+            for (int x = 0; x < F_MVT; ++x)
+                if (d + x < cnt) {
+                    dst_k[o + x] = k[x];
+                    if (HV) dst_v[o + x] = v[x];
+                }
+        }
+    }
+    pdl_trigger();
+}
+
+// reversal of a binary32 array (+ vals) in place (the Right targets)
+template <bool HV>
+__global__ void __launch_bounds__(256) f32_reverse_kernel(float *k, uint32_t *v, long long n)
+{
+    pdl_wait();
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n / 2; i += (long long)gridDim.x * blockDim.x) {
+        const long long j = n - 1 - i;
+        const float a = k[i], b = k[j];
+        k[i] = b;
+        k[j] = a;
+        if (HV) {
+            const uint32_t x = v[i], y = v[j];
+            v[i] = y;
+            v[j] = x;
+        }
+    }
+    pdl_trigger();
+}
+
+}  // namespace gns

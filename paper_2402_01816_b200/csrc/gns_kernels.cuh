@@ -1808,46 +1808,6 @@ __global__ void __launch_bounds__(256) gather_u64_kernel(uint64_t *out, const ui
     pdl_trigger();
 }
 
-// NEXT f3: binary32 keys (gns_sort_f32).  Each key becomes one 64-bit word
-// whose unsigned order is the target order of (key, input index): high half
-// = the key's bits mapped monotonically to u32 (sign-magnitude -> offset; -0.0
-// and +0.0 both to 0x80000000, so they tie), complemented for the descending
-// targets; low half = the input index, complemented for the Right targets
-// (ties in reverse input order).  The words are sorted as uint64 keys by the
-// product path; the output keys (original bits, signed zeros kept) and
-// payload are then gathered by the index.
-__device__ __forceinline__ uint32_t f32_order_bits(uint32_t b)
-{
-    if ((b & 0x7FFFFFFFu) == 0u) return 0x80000000u;           // -0.0 == +0.0
-    return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
-}
-__global__ void __launch_bounds__(256) f32_pack_kernel(const uint32_t *keys, unsigned long long *words, long long n,
-                                                        int desc, int right)
-{
-    pdl_wait();
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-        uint32_t hi = f32_order_bits(keys[i]);
-        if (desc) hi = ~hi;
-        const uint32_t lo = right ? ~(uint32_t)i : (uint32_t)i;
-        words[i] = ((unsigned long long)hi << 32) | lo;
-    }
-    pdl_trigger();
-}
-// tmp_k[i] = keys[idx_i], tmp_v[i] = vals[idx_i] (idx_i from the sorted word)
-__global__ void __launch_bounds__(256) f32_gather_kernel(const unsigned long long *words, const uint32_t *keys,
-                                                          const uint32_t *vals, uint32_t *tmp_k, uint32_t *tmp_v,
-                                                          long long n, int right)
-{
-    pdl_wait();
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-        uint32_t j = (uint32_t)words[i];
-        if (right) j = ~j;
-        tmp_k[i] = keys[j];
-        if (vals) tmp_v[i] = vals[j];
-    }
-    pdl_trigger();
-}
-
 // GNS_DEBUG=1 pre-scan (R1): number of NaN keys (f64 only).
 __global__ void __launch_bounds__(256) nan_count_kernel(const double *k, long long n, unsigned *cnt)
 {
