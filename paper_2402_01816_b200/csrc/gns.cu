@@ -184,6 +184,12 @@ F32TileK f32_tile_kern(bool hv, int desc)
                                      {&f32_tile_sort_kernel<true, false>, &f32_tile_sort_kernel<true, true>}};
     return t[hv][desc];
 }
+using F32PartK = decltype(&f32_partition_kernel<false>);
+F32PartK f32_part_kern(int desc)
+{
+    static const F32PartK t[2] = {&f32_partition_kernel<false>, &f32_partition_kernel<true>};
+    return t[desc];
+}
 F32MergeK f32_merge_kern(bool hv, int desc)
 {
     static const F32MergeK t[2][2] = {{&f32_merge_kernel<false, false>, &f32_merge_kernel<false, true>},
@@ -338,8 +344,9 @@ int launch_kind(const char *what)
                                   "inplace_deps_kernel", "merge_inplace_kernel", "reverse_kernel",
                                   "split_cuts_kernel", "gather_samples_kernel", "omit_plan_kernel",
                                   "omit_prep_kernel", "omit_final_kernel", "iota_u32_kernel", "gather_u64_kernel",
-                                  "f32_tile_sort_kernel", "f32_merge_kernel", "f32_reverse_kernel"};
-    for (int i = 0; i < 16; ++i)
+                                  "f32_tile_sort_kernel", "f32_merge_kernel", "f32_reverse_kernel",
+                                  "f32_partition_kernel"};
+    for (int i = 0; i < 17; ++i)
         if (std::strcmp(what, names[i]) == 0) return i + 1;
     return 0;
 }
@@ -989,9 +996,10 @@ gns_status gns_sort_keys_u64(void *keys, gns_key_type key_type, uint64_t *vals, 
 
 size_t gns_workspace_bytes_f32(size_t n)
 {
-    // the buffer: n keys + n vals (enough with or without payload); none for one tile
+    // the buffer: n keys + n vals (enough with or without payload), the
+    // merge tiles' splits; none for one tile
     if (n > GNS_MAX_N || n <= (size_t)F_TILE) return 0;
-    return 2 * align_up(n * sizeof(float), 256);
+    return 2 * align_up(n * sizeof(float), 256) + align_up((ceil_div(n, F_MTILE) + 1) * sizeof(int), 256);
 }
 
 gns_status gns_sort_f32(float *keys, uint32_t *vals, size_t n, gns_target target, void *ws, size_t ws_bytes,
@@ -1032,10 +1040,15 @@ gns_status gns_sort_f32(float *keys, uint32_t *vals, size_t n, gns_target target
     uint32_t *cv = (M & 1) ? bv : vals, *ov = (M & 1) ? vals : bv;
     gns_status r = launch_pdl("f32_tile_sort_kernel", f32_tile_kern(hv, desc), (unsigned)ceil_div(n, F_TILE), F_NT,
                               f_tile_smem(hv), st, (const float *)keys, (const uint32_t *)vals, ck, cv, (long long)n);
+    int *corank = reinterpret_cast<int *>(w + 2 * align_up(n * sizeof(float), 256));
+    const int ntiles = (int)ceil_div(n, F_MTILE);
     for (int p = 0; p < M && r == GNS_OK; ++p) {
         const long long L = (long long)F_TILE << p;
-        r = launch_pdl("f32_merge_kernel", f32_merge_kern(hv, desc), (unsigned)ceil_div(n, F_MTILE), F_NT, 0, st,
-                       (const float *)ck, (const uint32_t *)cv, ok, ov, (long long)n, L);
+        r = launch_pdl("f32_partition_kernel", f32_part_kern(desc), (unsigned)ceil_div((size_t)ntiles * 32, 256), 256,
+                       0, st, (const float *)ck, (long long)n, L, ntiles, corank);
+        if (r == GNS_OK)
+            r = launch_pdl("f32_merge_kernel", f32_merge_kern(hv, desc), (unsigned)ntiles, F_NT, 0, st,
+                           (const float *)ck, (const uint32_t *)cv, ok, ov, (long long)n, L, (const int *)corank);
         std::swap(ck, ok);
         std::swap(cv, ov);
     }

@@ -45,14 +45,23 @@ f32_tile_sort_kernel(const float *src_k, const uint32_t *src_v, float *dst_k, ui
     const int tid = threadIdx.x;
     const long long base = (long long)blockIdx.x * F_TILE;
     const int cnt = (int)min((long long)F_TILE, n - base);
-    for (int e = tid; e < F_TILE; e += F_NT) {          // coalesced loads
-        sk[fswz(e)] = e < cnt ? src_k[base + e] : fpad<DESC>();
-        if (HV) sv[fswz(e)] = e < cnt ? src_v[base + e] : 0u;
-    }
-    __syncthreads();
     const int e0 = tid * F_VT;
     float k[F_VT];
     uint32_t v[F_VT];
+    // coalesced loads, all issued before the shared stores
+#pragma unroll
+    for (int u = 0; u < F_VT; ++u) {
+        const int e = tid + u * F_NT;
+        k[u] = e < cnt ? src_k[base + e] : fpad<DESC>();
+        if (HV) v[u] = e < cnt ? src_v[base + e] : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < F_VT; ++u) {
+        const int e = tid + u * F_NT;
+        sk[fswz(e)] = k[u];
+        if (HV) sv[fswz(e)] = v[u];
+    }
+    __syncthreads();
 #pragma unroll
     for (int x = 0; x < F_VT; ++x) {
         k[x] = sk[fswz(e0 + x)];
@@ -139,19 +148,39 @@ __device__ __forceinline__ int f32_corank(const float *A, int na, const float *B
                                      [&](int m) { return !fbefore<DESC>(B[d - 1 - m], A[m]); });
 }
 
+// F2a: the split (A keys among the pair's first k0 outputs) of every merge
+// tile's first output, one warp per tile (all tiles in one wave: the
+// latency-bound searches overlap).
+template <bool DESC>
+__global__ void __launch_bounds__(256)
+f32_partition_kernel(const float *src_k, long long n, long long L, int ntiles, int *corank)
+{
+    pdl_wait();
+    pdl_trigger();
+    const int t = (int)((blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5);
+    const int lane = threadIdx.x & 31;
+    if (t >= ntiles) return;
+    const long long t0 = (long long)t * F_MTILE;
+    const long long pb = (t0 / (2 * L)) * (2 * L);
+    const int na = (int)min(L, n - pb);
+    const int nb = (int)max(0LL, min(L, n - pb - L));
+    const int c = f32_corank<DESC>(src_k + pb, na, src_k + pb + L, nb, (int)(t0 - pb), lane);
+    if (lane == 0) corank[t] = c;
+}
+
 // ------------------------------------------------------------------ F2
 // One merge level: pair q = runs [2qL, 2qL+L) and [2qL+L, 2qL+2L) of src
 // (clipped to n) into the same range of dst; CTA t writes outputs
-// [4096 t, 4096 t + 4096).
+// [4096 t, 4096 t + 4096), its splits from the partition.
 template <bool HV, bool DESC>
 __global__ void __launch_bounds__(F_NT)
-f32_merge_kernel(const float *src_k, const uint32_t *src_v, float *dst_k, uint32_t *dst_v, long long n, long long L)
+f32_merge_kernel(const float *src_k, const uint32_t *src_v, float *dst_k, uint32_t *dst_v, long long n, long long L,
+                 const int *corank)
 {
     pdl_wait();
     __shared__ float sa[F_MTILE + 1];
     __shared__ uint32_t va[HV ? F_MTILE + 1 : 1];
-    __shared__ int s_split[2];
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int tid = threadIdx.x;
     const long long t0 = (long long)blockIdx.x * F_MTILE;
     const long long pb = (t0 / (2 * L)) * (2 * L);          // the pair's first element
     const int na = (int)min(L, n - pb);
@@ -159,20 +188,32 @@ f32_merge_kernel(const float *src_k, const uint32_t *src_v, float *dst_k, uint32
     const int k0 = (int)(t0 - pb);
     const int k1 = (int)min((long long)k0 + F_MTILE, (long long)na + nb);
     const float *A = src_k + pb, *B = src_k + pb + L;
-    if (warp < 2) {
-        const int d = warp == 0 ? k0 : k1;
-        const int c = f32_corank<DESC>(A, na, B, nb, d, lane);
-        if (lane == 0) s_split[warp] = c;
-    }
-    __syncthreads();
-    const int i0 = s_split[0], i1 = s_split[1];
+    const int i0 = corank[blockIdx.x];
+    const int i1 = (k1 == na + nb) ? na : corank[blockIdx.x + 1];   // (the pair's last tile ends at na)
     const int j0 = k0 - i0, j1 = k1 - i1;
     const int ca = i1 - i0, cb = j1 - j0, cnt = ca + cb;
-    // the tile's inputs: A[i0:i1) at [0, ca), B[j0:j1) at [ca, cnt)
-    for (int e = tid; e < cnt; e += F_NT) {
-        const bool fa = e < ca;
-        sa[e] = fa ? A[i0 + e] : B[j0 + e - ca];
-        if (HV) va[e] = fa ? src_v[pb + i0 + e] : src_v[pb + L + j0 + e - ca];
+    // the tile's inputs: A[i0:i1) at [0, ca), B[j0:j1) at [ca, cnt); all of a
+    // thread's loads are issued before its shared stores (memory-level parallelism)
+    {
+        float tk[F_MVT];
+        uint32_t tv[F_MVT];
+#pragma unroll
+        for (int u = 0; u < F_MVT; ++u) {
+            const int e = tid + u * F_NT;
+            if (e < cnt) {
+                const bool fa = e < ca;
+                tk[u] = fa ? A[i0 + e] : B[j0 + e - ca];
+                if (HV) tv[u] = fa ? src_v[pb + i0 + e] : src_v[pb + L + j0 + e - ca];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < F_MVT; ++u) {
+            const int e = tid + u * F_NT;
+            if (e < cnt) {
+                sa[e] = tk[u];
+                if (HV) va[e] = tv[u];
+            }
+        }
     }
     __syncthreads();
     const int d = tid * F_MVT;
