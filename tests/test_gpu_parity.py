@@ -785,3 +785,33 @@ def test_f32_keys_full_size(gns):
     perm = ev.astype(np.int64)
     assert np.array_equal(tk.cpu().numpy().view(np.uint32), k[perm].view(np.uint32))
     assert np.array_equal(tv.cpu().numpy(), v[perm])
+
+
+@pytest.mark.slow
+def test_f32_max_size_properties(gns):
+    """binary32 keys at GNS_MAX_N with payload = index (int32 offsets of the
+    4-byte kernels at their limit), by the properties that fix the stable
+    sort: non-decreasing, payload a permutation, every key bit-identical to
+    the input key its payload names, ties in ascending payload order."""
+    n = (1 << 31) - 1
+    torch.cuda.empty_cache()
+    free, _ = torch.cuda.mem_get_info()
+    need = n * (4 + 4) * 3 + n * 8
+    if free < need:
+        pytest.skip(f"needs {need / 2**30:.0f} GiB of device memory")
+    g = torch.Generator(device="cuda")
+    g.manual_seed(31)
+    keys = torch.randint(0, 1 << 20, (n,), device="cuda", generator=g).to(torch.float32)   # heavy ties
+    keys[::3] = torch.rand(keys[::3].shape, device="cuda", generator=g, dtype=torch.float32)
+    src = keys.clone()
+    vals = torch.arange(n, device="cuda", dtype=torch.int64).to(torch.uint32)
+    gns.sort_f32_(keys, vals)
+    torch.cuda.synchronize()
+    assert bool((keys[1:] >= keys[:-1]).all())
+    idx = vals.to(torch.int64)
+    assert bool((src.view(torch.int32)[idx] == keys.view(torch.int32)).all())
+    seen = torch.zeros(n, dtype=torch.uint8, device="cuda")
+    seen[idx] = 1
+    assert int(seen.sum()) == n
+    tie = keys[1:] == keys[:-1]
+    assert bool((idx[1:][tie] > idx[:-1][tie]).all())
