@@ -815,3 +815,30 @@ def test_f32_max_size_properties(gns):
     assert int(seen.sum()) == n
     tie = keys[1:] == keys[:-1]
     assert bool((idx[1:][tie] > idx[:-1][tie]).all())
+
+
+@pytest.mark.slow
+def test_u64_payload_max_size_properties(gns):
+    """64-bit payloads at GNS_MAX_N: keys non-decreasing, each payload (the
+    input index as uint64) names the input key its key equals bit-exactly,
+    ties in ascending payload order."""
+    n = (1 << 31) - 1
+    torch.cuda.empty_cache()
+    free, _ = torch.cuda.mem_get_info()
+    need = n * (8 + 8) * 3 + n * 8
+    if free < need:
+        pytest.skip(f"needs {need / 2**30:.0f} GiB of device memory")
+    g = torch.Generator(device="cuda")
+    g.manual_seed(64)
+    keys = torch.randint(0, 1 << 20, (n,), device="cuda", generator=g).to(torch.float64)
+    src = keys.clone()
+    vals = torch.arange(n, device="cuda", dtype=torch.int64)
+    gns.sort_u64_(keys, vals)
+    torch.cuda.synchronize()
+    assert bool((keys[1:] >= keys[:-1]).all())
+    assert bool((src.view(torch.int64)[vals] == keys.view(torch.int64)).all())
+    tie = keys[1:] == keys[:-1]
+    assert bool((vals[1:][tie] > vals[:-1][tie]).all())
+    seen = torch.zeros(n, dtype=torch.uint8, device="cuda")
+    seen[vals] = 1
+    assert int(seen.sum()) == n
