@@ -281,10 +281,12 @@ def main():
     footprint = None
     presorted = None
     others = None
+    keytypes = None
     if rank == 0 and world == 1 and not args.no_footprint and args.config == 2:
         footprint = footprint_cfg5(gns, torch, dev, stream, flush)
         presorted = config4(gns, torch, dev, stream, flush)
         others = other_configs(gns, torch, dev, stream, flush)
+        keytypes = key_types(gns, torch, dev, stream, flush)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -325,6 +327,8 @@ def main():
         line["presorted_cfg4"] = presorted
     if others:
         line["other_configs"] = others
+    if keytypes:
+        line["key_types_f3"] = keytypes
     if rank == 0:
         print(json.dumps(line), flush=True)
     if pg:
@@ -526,6 +530,55 @@ def config4(gns, torch, dev, stream, flush, reps=5):
                 out[sub]["omit"] = r
             else:
                 out[sub] = r
+    return out
+
+
+def key_types(gns, torch, dev, stream, flush, reps=5):
+    """NEXT f3 at n = 2^24 (same timing rules): int64 keys (the 8-byte path),
+    binary32 keys key-only and with a u32 payload (the 4-byte kernels), f64
+    keys with a 64-bit payload (index sort + gather); median ms, keys/s,
+    %RAM."""
+    n = 1 << 24
+    g = torch.Generator(device=dev)
+    g.manual_seed(3)
+    cases = {
+        "i64": (torch.randint(-(1 << 62), 1 << 62, (n,), device=dev, generator=g), None),
+        "f32": (torch.rand(n, device=dev, generator=g, dtype=torch.float32), None),
+        "f32_u32": (torch.rand(n, device=dev, generator=g, dtype=torch.float32),
+                    torch.arange(n, device=dev, dtype=torch.int64).to(torch.uint32)),
+        "f64_u64": (torch.rand(n, device=dev, generator=g, dtype=torch.float64),
+                    torch.arange(n, device=dev, dtype=torch.int64)),
+    }
+    out = {}
+    for name, (src, srcv) in cases.items():
+        if name.startswith("f32"):
+            ws = torch.empty(max(1, gns.workspace_bytes_f32(n, srcv is not None)), dtype=torch.uint8, device=dev)
+            run = lambda k, v: gns.sort_f32_(k, v, workspace=ws, stream=stream)
+            data = n * (4 + (4 if srcv is not None else 0))
+        elif name == "f64_u64":
+            ws = torch.empty(gns.workspace_bytes_u64(n), dtype=torch.uint8, device=dev)
+            run = lambda k, v: gns.sort_u64_(k, v, workspace=ws, stream=stream)
+            data = n * 16
+        else:
+            ws = gns.alloc_workspace(n, 1.0, False, dev)
+            run = lambda k, v: gns.sort_(k, v, 1.0, workspace=ws, stream=stream)
+            data = n * 8
+        ts = []
+        for i in range(reps + 1):
+            k = src.clone()
+            v = None if srcv is None else srcv.clone()
+            flush.fill_(1)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            run(k, v)
+            b.record(stream)
+            torch.cuda.synchronize()
+            if i:
+                ts.append(a.elapsed_time(b))
+        ms = float(np.median(ts))
+        out[name] = {"ms": ms, "keys_per_s": n / (ms / 1e3), "sorted": bool((k[1:] >= k[:-1]).all().item()),
+                     "ram_pct": 1.0 + ws.numel() / data}
+        del ws
     return out
 
 

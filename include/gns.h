@@ -149,10 +149,11 @@ gns_status gns_sort_keys_u64(void *keys, gns_key_type key_type, uint64_t *vals, 
  * 4-byte kernels (csrc/gns_f32.cuh): the same schedule as the f64 full-buffer
  * sort -- one tile-sort pass (8192-key tiles, every level on chip), then one
  * HBM merge pass per level, ping-pong with a buffer of n keys (+ n vals):
- * %RAM 2.0.  ws: NULL (allocated stream-ordered) or gns_workspace_bytes_f32(n)
- * bytes (0 for n <= 8192), 32-byte aligned.  NaN keys: precondition
+ * %RAM 2.0.  ws: NULL (allocated stream-ordered) or
+ * gns_workspace_bytes_f32(n, vals != NULL) bytes (0 for n <= 8192), 32-byte
+ * aligned.  NaN keys: precondition
  * violation.  Errors as gns_sort_keys. */
-size_t gns_workspace_bytes_f32(size_t n);
+size_t gns_workspace_bytes_f32(size_t n, int with_vals);
 gns_status gns_sort_f32(float *keys, uint32_t *vals, size_t n, gns_target target, void *ws, size_t ws_bytes,
                         gns_stream_t stream);
 

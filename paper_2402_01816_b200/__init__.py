@@ -68,7 +68,7 @@ _c = {
     "gns_sort_keys_u64": _sig("gns_sort_keys_u64", [_vp, _i, _vp, _sz, _i, _vp, _sz, _vp]),
     "gns_workspace_bytes_u64": _sig("gns_workspace_bytes_u64", [_sz], _sz),
     "gns_sort_f32": _sig("gns_sort_f32", [_vp, _vp, _sz, _i, _vp, _sz, _vp]),
-    "gns_workspace_bytes_f32": _sig("gns_workspace_bytes_f32", [_sz], _sz),
+    "gns_workspace_bytes_f32": _sig("gns_workspace_bytes_f32", [_sz, _i], _sz),
     "gns_split_cuts": _sig("gns_split_cuts", [_vp, _i, _sz, _vp, _vp, _vp, _i, _i, _vp, _vp]),
     "gns_merge_two": _sig("gns_merge_two", [_vp, _vp, _sz, _vp, _vp, _sz, _vp, _vp, _i, _vp]),
     "gns_plan": _sig("gns_plan", [_sz, _d, _i, ctypes.POINTER(gns_plan_info)]),
@@ -148,8 +148,8 @@ def gns_sort_f32(keys_ptr, vals_ptr, n, target, ws_ptr, ws_bytes, stream) -> int
     return _c["gns_sort_f32"](keys_ptr, vals_ptr, n, target, ws_ptr, ws_bytes, stream)
 
 
-def gns_workspace_bytes_f32(n) -> int:
-    return _c["gns_workspace_bytes_f32"](n)
+def gns_workspace_bytes_f32(n, with_vals) -> int:
+    return _c["gns_workspace_bytes_f32"](n, with_vals)
 
 
 def gns_sort_omit(keys_ptr, key_type, vals_ptr, n, target, ws_ptr, ws_bytes, stream) -> int:
@@ -285,8 +285,8 @@ def workspace_bytes_u64(n: int) -> int:
 def sort_f32_(keys, vals=None, workspace=None, stream=None, target: str = "AscLeft"):
     """NEXT f3: stable sort of float32 ``keys`` (and uint32 ``vals``) on the
     GPU (gns_sort_f32: the 4-byte kernel set, full buffer, %RAM 2.0).
-    ``workspace``: optional uint8 CUDA tensor of >= workspace_bytes_f32(n)
-    bytes."""
+    ``workspace``: optional uint8 CUDA tensor of >= workspace_bytes_f32(n,
+    vals is not None) bytes."""
     import torch
     if keys.dtype != torch.float32 or not keys.is_cuda or not keys.is_contiguous():
         raise TypeError("keys must be a contiguous CUDA float32 tensor")
@@ -302,8 +302,8 @@ def sort_f32_(keys, vals=None, workspace=None, stream=None, target: str = "AscLe
     return keys, vals
 
 
-def workspace_bytes_f32(n: int) -> int:
-    return gns_workspace_bytes_f32(n)
+def workspace_bytes_f32(n: int, with_vals: bool = False) -> int:
+    return gns_workspace_bytes_f32(n, 1 if with_vals else 0)
 
 
 def sort_omit_(keys, vals=None, workspace=None, stream=None, target: str = "AscLeft"):

@@ -994,12 +994,12 @@ gns_status gns_sort_keys_u64(void *keys, gns_key_type key_type, uint64_t *vals, 
     return r;
 }
 
-size_t gns_workspace_bytes_f32(size_t n)
+size_t gns_workspace_bytes_f32(size_t n, int with_vals)
 {
-    // the buffer: n keys + n vals (enough with or without payload), the
-    // merge tiles' splits; none for one tile
+    // the buffer: n keys (+ n vals), the merge tiles' splits; none for one tile
     if (n > GNS_MAX_N || n <= (size_t)F_TILE) return 0;
-    return 2 * align_up(n * sizeof(float), 256) + align_up((ceil_div(n, F_MTILE) + 1) * sizeof(int), 256);
+    return (with_vals ? 2 : 1) * align_up(n * sizeof(float), 256) +
+           align_up((ceil_div(n, F_MTILE) + 1) * sizeof(int), 256);
 }
 
 gns_status gns_sort_f32(float *keys, uint32_t *vals, size_t n, gns_target target, void *ws, size_t ws_bytes,
@@ -1012,7 +1012,8 @@ gns_status gns_sort_f32(float *keys, uint32_t *vals, size_t n, gns_target target
         return fail(GNS_ERR_MISALIGNED, "keys/vals must be 32-byte aligned");
     if (n <= 1) return GNS_OK;
     cudaStream_t st = (cudaStream_t)stream;
-    const size_t need = gns_workspace_bytes_f32(n);
+    const bool hv = vals != nullptr;
+    const size_t need = gns_workspace_bytes_f32(n, hv ? 1 : 0);
     unsigned char *w = (unsigned char *)ws;
     if (need && w) {
         if (ws_bytes < need) return fail(GNS_ERR_WORKSPACE_TOO_SMALL, "workspace too small");
@@ -1029,7 +1030,6 @@ gns_status gns_sort_f32(float *keys, uint32_t *vals, size_t n, gns_target target
         }
         own = true;
     }
-    const bool hv = vals != nullptr;
     const bool right = target == 1 || target == 3;
     const int desc = (target == 2 || target == 1) ? 1 : 0;      // AscRight = reverse(DescLeft)
     float *bk = reinterpret_cast<float *>(w);
@@ -1040,7 +1040,7 @@ gns_status gns_sort_f32(float *keys, uint32_t *vals, size_t n, gns_target target
     uint32_t *cv = (M & 1) ? bv : vals, *ov = (M & 1) ? vals : bv;
     gns_status r = launch_pdl("f32_tile_sort_kernel", f32_tile_kern(hv, desc), (unsigned)ceil_div(n, F_TILE), F_NT,
                               f_tile_smem(hv), st, (const float *)keys, (const uint32_t *)vals, ck, cv, (long long)n);
-    int *corank = reinterpret_cast<int *>(w + 2 * align_up(n * sizeof(float), 256));
+    int *corank = reinterpret_cast<int *>(w + (hv ? 2 : 1) * align_up(n * sizeof(float), 256));
     const int ntiles = (int)ceil_div(n, F_MTILE);
     for (int p = 0; p < M && r == GNS_OK; ++p) {
         const long long L = (long long)F_TILE << p;

@@ -765,7 +765,7 @@ def test_f32_keys(gns, n, target, payload):
     for use_ws in (False, True):
         tk = torch.from_numpy(k.copy()).cuda()
         tv = None if v is None else torch.from_numpy(v.copy()).cuda()
-        ws = (torch.empty(max(1, gns.workspace_bytes_f32(n)), dtype=torch.uint8, device="cuda") if use_ws else None)
+        ws = (torch.empty(max(1, gns.workspace_bytes_f32(n, v is not None)), dtype=torch.uint8, device="cuda") if use_ws else None)
         gns.sort_f32_(tk, tv, workspace=ws, target=target)
         torch.cuda.synchronize()
         assert np.array_equal(tk.cpu().numpy().view(np.uint32), k[perm].view(np.uint32)), f"keys n={n} {target}"

@@ -17,7 +17,7 @@ a = ap.parse_args()
 n = 1 << a.n
 k = torch.rand(n, device="cuda", dtype=torch.float32)
 v = torch.arange(n, device="cuda", dtype=torch.int64).to(torch.uint32) if a.pairs else None
-ws = torch.empty(gns.workspace_bytes_f32(n), dtype=torch.uint8, device="cuda")
+ws = torch.empty(gns.workspace_bytes_f32(n, True), dtype=torch.uint8, device="cuda")
 gns.sort_f32_(k.clone(), None if v is None else v.clone(), workspace=ws)
 torch.cuda.synchronize()
 kk, vv = k.clone(), (None if v is None else v.clone())

@@ -19,7 +19,7 @@ g.manual_seed(1)
 src = torch.rand(n, device="cuda", generator=g, dtype=torch.float32)
 pay = torch.arange(n, device="cuda", dtype=torch.int64).to(torch.uint32)
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-ws = torch.empty(gns.workspace_bytes_f32(n), dtype=torch.uint8, device="cuda")
+ws = torch.empty(gns.workspace_bytes_f32(n, True), dtype=torch.uint8, device="cuda")
 for hv in (False, True):
     ts = []
     for i in range(13):
