@@ -244,6 +244,7 @@ gns_status ensure_attrs()
             GNS_ATTR(merge_kern(hv, o), ts_smem(hv));
             GNS_ATTR(merge_kern_ol(hv, o), ts_smem(hv));
             if (o < 2) GNS_ATTR(f32_tile_kern(hv, o), f_tile_smem(hv));
+            if (o < 2) GNS_ATTR(f32_merge_kern(hv, o), f_merge_smem(hv));
             if (!hv) GNS_ATTR(omit_plan_kern(o), OMIT_SMEM);
             GNS_ATTR(inplace_kern(hv, o), ts_smem(hv));
             GNS_ATTR(tile_kern(hv, o), t1_smem(hv));
@@ -1047,7 +1048,7 @@ gns_status gns_sort_f32(float *keys, uint32_t *vals, size_t n, gns_target target
         r = launch_pdl("f32_partition_kernel", f32_part_kern(desc), (unsigned)ceil_div((size_t)ntiles * 32, 256), 256,
                        0, st, (const float *)ck, (long long)n, L, ntiles, corank);
         if (r == GNS_OK)
-            r = launch_pdl("f32_merge_kernel", f32_merge_kern(hv, desc), (unsigned)ntiles, F_NT, 0, st,
+            r = launch_pdl("f32_merge_kernel", f32_merge_kern(hv, desc), (unsigned)ntiles, F_NT, f_merge_smem(hv), st,
                            (const float *)ck, (const uint32_t *)cv, ok, ov, (long long)n, L, (const int *)corank);
         std::swap(ck, ok);
         std::swap(cv, ov);

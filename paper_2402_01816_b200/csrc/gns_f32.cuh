@@ -172,14 +172,23 @@ f32_partition_kernel(const float *src_k, long long n, long long L, int ntiles, i
 // One merge level: pair q = runs [2qL, 2qL+L) and [2qL+L, 2qL+2L) of src
 // (clipped to n) into the same range of dst; CTA t writes outputs
 // [4096 t, 4096 t + 4096), its splits from the partition.
+// merge stage: A slots [0, F_SEG), B slots [F_SEG, 2 F_SEG) (+ vals alike);
+// each part arrives by one 16-byte aligned 1-D bulk copy, `off` elements in
+constexpr int F_SEG = F_MTILE + 8;
+constexpr size_t f_merge_smem(bool hv) { return (size_t)2 * F_SEG * 4 * (hv ? 2 : 1); }
+
 template <bool HV, bool DESC>
 __global__ void __launch_bounds__(F_NT)
 f32_merge_kernel(const float *src_k, const uint32_t *src_v, float *dst_k, uint32_t *dst_v, long long n, long long L,
                  const int *corank)
 {
     pdl_wait();
-    __shared__ float sa[F_MTILE + 1];
-    __shared__ uint32_t va[HV ? F_MTILE + 1 : 1];
+    extern __shared__ __align__(16) unsigned char fm_smem[];
+    float *SA = reinterpret_cast<float *>(fm_smem);
+    float *SB = SA + F_SEG;
+    uint32_t *VA = reinterpret_cast<uint32_t *>(fm_smem + 2 * F_SEG * 4);
+    uint32_t *VB = VA + F_SEG;
+    __shared__ __align__(8) uint64_t bar;
     const int tid = threadIdx.x;
     const long long t0 = (long long)blockIdx.x * F_MTILE;
     const long long pb = (t0 / (2 * L)) * (2 * L);          // the pair's first element
@@ -187,32 +196,52 @@ f32_merge_kernel(const float *src_k, const uint32_t *src_v, float *dst_k, uint32
     const int nb = (int)max(0LL, min(L, n - pb - L));
     const int k0 = (int)(t0 - pb);
     const int k1 = (int)min((long long)k0 + F_MTILE, (long long)na + nb);
-    const float *A = src_k + pb, *B = src_k + pb + L;
     const int i0 = corank[blockIdx.x];
     const int i1 = (k1 == na + nb) ? na : corank[blockIdx.x + 1];   // (the pair's last tile ends at na)
     const int j0 = k0 - i0, j1 = k1 - i1;
     const int ca = i1 - i0, cb = j1 - j0, cnt = ca + cb;
-    // the tile's inputs: A[i0:i1) at [0, ca), B[j0:j1) at [ca, cnt); all of a
-    // thread's loads are issued before its shared stores (memory-level parallelism)
-    {
-        float tk[F_MVT];
-        uint32_t tv[F_MVT];
-#pragma unroll
-        for (int u = 0; u < F_MVT; ++u) {
-            const int e = tid + u * F_NT;
-            if (e < cnt) {
-                const bool fa = e < ca;
-                tk[u] = fa ? A[i0 + e] : B[j0 + e - ca];
-                if (HV) tv[u] = fa ? src_v[pb + i0 + e] : src_v[pb + L + j0 + e - ca];
-            }
+    // global element ranges of the two parts, the 16-byte aligned bulk range
+    // inside [0, n & ~3), and the elements past it (at most 3, loaded by hand)
+    const long long ga = pb + i0, gb = pb + L + j0;
+    const long long nal = n & ~3LL;
+    auto span = [&](long long g, int c, long long &s0, long long &s1) {
+        s0 = g & ~3LL;
+        s1 = min((g + c + 3) & ~3LL, nal);
+        if (s1 < s0) s1 = s0;
+    };
+    long long sa0, sa1, sb0, sb1;
+    span(ga, ca, sa0, sa1);
+    span(gb, cb, sb0, sb1);
+    if (ca == 0) sa1 = sa0;                                  // (nothing to copy: no bytes expected)
+    if (cb == 0) sb1 = sb0;
+    const int oa = (int)(ga - sa0), ob = (int)(gb - sb0);
+    if (tid == 0) {
+        mbar_init(&bar, 1);
+        fence_mbar_init();
+        const uint32_t bytes = (uint32_t)((sa1 - sa0) + (sb1 - sb0)) * 4u * (HV ? 2u : 1u);
+        mbar_expect_tx(&bar, bytes);
+        const uint64_t pol = policy_evict_first();
+        if (sa1 > sa0) {
+            tma_load_1d(SA, src_k + sa0, (uint32_t)(sa1 - sa0) * 4u, &bar, pol);
+            if (HV) tma_load_1d(VA, src_v + sa0, (uint32_t)(sa1 - sa0) * 4u, &bar, pol);
         }
-#pragma unroll
-        for (int u = 0; u < F_MVT; ++u) {
-            const int e = tid + u * F_NT;
-            if (e < cnt) {
-                sa[e] = tk[u];
-                if (HV) va[e] = tv[u];
-            }
+        if (sb1 > sb0) {
+            tma_load_1d(SB, src_k + sb0, (uint32_t)(sb1 - sb0) * 4u, &bar, pol);
+            if (HV) tma_load_1d(VB, src_v + sb0, (uint32_t)(sb1 - sb0) * 4u, &bar, pol);
+        }
+        mbar_arrive(&bar);
+    }
+    __syncthreads();
+    mbar_wait(&bar, 0);
+    // the tails past the last aligned group of the array (only at its end)
+    if (tid < 8) {
+        const bool fa = tid < 4;
+        const long long g = (fa ? sa1 : sb1) + (tid & 3);
+        const long long gend = fa ? ga + ca : gb + cb;
+        if (g < gend) {
+            const int slot = (int)(g - (fa ? sa0 : sb0));
+            (fa ? SA : SB)[slot] = src_k[g];
+            if (HV) (fa ? VA : VB)[slot] = src_v[g];
         }
     }
     __syncthreads();
@@ -221,19 +250,19 @@ f32_merge_kernel(const float *src_k, const uint32_t *src_v, float *dst_k, uint32
         int lo = max(0, d - cb), hi = min(d, ca);
         while (lo < hi) {
             const int m = (lo + hi) >> 1;
-            if (!fbefore<DESC>(sa[ca + d - 1 - m], sa[m])) lo = m + 1;
+            if (!fbefore<DESC>(SB[ob + d - 1 - m], SA[oa + m])) lo = m + 1;
             else hi = m;
         }
-        int ai = lo, bi = ca + d - lo;
+        int ai = lo, bj = d - lo;
         float k[F_MVT];
         uint32_t v[F_MVT];
 #pragma unroll
         for (int x = 0; x < F_MVT; ++x) {
-            const float ka = ai < ca ? sa[ai] : 0.f, kb = bi < cnt ? sa[bi] : 0.f;
-            const bool p = (bi < cnt) && ((ai >= ca) || fbefore<DESC>(kb, ka));
+            const float ka = ai < ca ? SA[oa + ai] : 0.f, kb = bj < cb ? SB[ob + bj] : 0.f;
+            const bool p = (bj < cb) && ((ai >= ca) || fbefore<DESC>(kb, ka));
             k[x] = p ? kb : ka;
-            if (HV) v[x] = va[p ? bi : ai];
-            if (p) ++bi;
+            if (HV) v[x] = p ? VB[ob + bj] : VA[oa + ai];
+            if (p) ++bj;
             else ++ai;
         }
         const long long o = t0 + d;
