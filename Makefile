@@ -4,7 +4,7 @@ ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC,-O3 -shared --expt-relaxed-constexpr
 PKG := paper_2402_01816_b200
 LIB := $(PKG)/libgns.so
-SRCS := $(PKG)/csrc/gns.cu $(PKG)/csrc/gns_kernels.cuh $(PKG)/csrc/gns_f32.cuh include/gns.h
+SRCS := $(PKG)/csrc/gns.cu $(wildcard $(PKG)/csrc/*.cuh) include/gns.h
 
 all: $(LIB) oracle/liboracle.so synth/libsynth.so
 

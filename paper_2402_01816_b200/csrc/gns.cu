@@ -8,6 +8,7 @@
 #include "../../include/gns.h"
 #include "gns_kernels.cuh"
 #include "gns_f32.cuh"
+#include "gns_tile64.cuh"
 
 #include <cuda_runtime.h>
 #include <cstdio>
@@ -156,6 +157,23 @@ TileK tile_kern(bool hv, int o)
     static const TileK t[2][NORD] = {GNS_ORDS(tile_sort2_kernel, false), GNS_ORDS(tile_sort2_kernel, true)};
     return t[hv][o];
 }
+using Tile3K = decltype(&tile_sort3_kernel<0>);
+Tile3K tile3_kern(int o)
+{
+    static const Tile3K t[NORD] = {&tile_sort3_kernel<0>, &tile_sort3_kernel<1>, &tile_sort3_kernel<2>,
+                                   &tile_sort3_kernel<3>, &tile_sort3_kernel<4>, &tile_sort3_kernel<5>};
+    return t[o];
+}
+// Key-only K1: the 128 x 64 kernel (tile_sort3_kernel) unless GNS_K1=2
+// forces the 256 x 32 one (A/B).
+bool k1_v3()
+{
+    static const bool on = [] {
+        const char *e = std::getenv("GNS_K1");
+        return !(e && e[0] == '2');
+    }();
+    return on;
+}
 MergeK merge_kern(bool hv, int o)
 {
     static const MergeK t[2][NORD] = {GNS_ORDS(merge_tstore_kernel, false), GNS_ORDS(merge_tstore_kernel, true)};
@@ -248,6 +266,7 @@ gns_status ensure_attrs()
             if (!hv) GNS_ATTR(omit_plan_kern(o), OMIT_SMEM);
             GNS_ATTR(inplace_kern(hv, o), ts_smem(hv));
             GNS_ATTR(tile_kern(hv, o), t1_smem(hv));
+            if (!hv) GNS_ATTR(tile3_kern(o), T3_SMEM);
         }
     }
 #undef GNS_ATTR
@@ -397,6 +416,9 @@ gns_status launch_tile_sort(const double *sk, const uint32_t *sv, double *dk, ui
     if (n == 0) return GNS_OK;
     const unsigned grid = (unsigned)ceil_div(n, TILE);
     const bool hv = sv != nullptr;
+    if (!hv && k1_v3())
+        return launch_pdl("tile_sort2_kernel", tile3_kern(ord), grid, NT3, T3_SMEM, st, sk, dk, (long long)n, unsorted,
+                          smp, tdesc, smp_src);
     CUtensorMap m[4];
     std::memset(m, 0, sizeof(m));
     if (n >= (size_t)TILE) {          // full tiles move by TMA tensor copies; a ragged last tile by plain loads

@@ -196,10 +196,16 @@ f32_merge_kernel(const float *src_k, const uint32_t *src_v, float *dst_k, uint32
     const int nb = (int)max(0LL, min(L, n - pb - L));
     const int k0 = (int)(t0 - pb);
     const int k1 = (int)min((long long)k0 + F_MTILE, (long long)na + nb);
-    const int i0 = corank[blockIdx.x];
-    const int i1 = (k1 == na + nb) ? na : corank[blockIdx.x + 1];   // (the pair's last tile ends at na)
+    // Split points clamped to the feasible co-ranks: with NaN keys (a
+    // precondition violation, R1) the searches may return
+    // non-monotone splits; clamping keeps 0 <= ca, cb and ca + cb = k1 - k0
+    // <= F_MTILE, so every copy stays inside its F_SEG slots.
+    const int i0 = min(max(corank[blockIdx.x], max(0, k0 - nb)), min(k0, na));
+    int i1 = (k1 == na + nb) ? na : corank[blockIdx.x + 1];         // (the pair's last tile ends at na)
+    i1 = min(max(max(i1, i0), k1 - nb), min(i0 + (k1 - k0), na));
     const int j0 = k0 - i0, j1 = k1 - i1;
     const int ca = i1 - i0, cb = j1 - j0, cnt = ca + cb;
+    GNS_DASSERT(ca >= 0 && cb >= 0 && cnt == k1 - k0 && cnt <= F_MTILE);
     // global element ranges of the two parts, the 16-byte aligned bulk range
     // inside [0, n & ~3), and the elements past it (at most 3, loaded by hand)
     const long long ga = pb + i0, gb = pb + L + j0;
@@ -215,6 +221,7 @@ f32_merge_kernel(const float *src_k, const uint32_t *src_v, float *dst_k, uint32
     if (ca == 0) sa1 = sa0;                                  // (nothing to copy: no bytes expected)
     if (cb == 0) sb1 = sb0;
     const int oa = (int)(ga - sa0), ob = (int)(gb - sb0);
+    GNS_DASSERT(oa + ca <= F_SEG && ob + cb <= F_SEG && (sa1 - sa0) <= F_SEG && (sb1 - sb0) <= F_SEG);
     if (tid == 0) {
         mbar_init(&bar, 1);
         fence_mbar_init();

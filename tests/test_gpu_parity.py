@@ -842,3 +842,45 @@ def test_u64_payload_max_size_properties(gns):
     seen = torch.zeros(n, dtype=torch.uint8, device="cuda")
     seen[vals] = 1
     assert int(seen.sum()) == n
+
+
+@pytest.mark.parametrize("payload", [False, True])
+def test_f32_nan_memory_safe(gns, payload):
+    """binary32 keys with NaN (a precondition violation, R1): the
+    merge pass must clamp non-monotone split points so its bulk
+    copies stay inside their shared slots.  Crafted inputs: a tile of zeros
+    with NaNs (at every position a search can probe, and sparse), followed by
+    a tile of -1.0; plus random NaNs over several passes.  The call must
+    terminate without a fault and the context must still sort correctly."""
+    t = T1
+    cases = []
+    a = np.zeros(2 * t, np.float32)
+    a[:t:7] = np.nan
+    a[t:] = -1.0
+    cases.append(a)
+    b = np.zeros(2 * t, np.float32)
+    b[:t][np.arange(0, t, 1)[::2]] = np.nan
+    b[t:] = -1.0
+    cases.append(b)
+    c = np.zeros(4 * t + 5, np.float32)
+    c[::3] = np.nan
+    c[2 * t:] = -2.0
+    cases.append(c)
+    r = synth.uniform(9 * t + 3, 77).astype(np.float32)
+    r[::5] = np.nan
+    cases.append(r)
+    for k in cases:
+        n = k.size
+        tk = torch.from_numpy(k.copy()).cuda()
+        tv = torch.from_numpy(synth.iota_u32(n)).cuda() if payload else None
+        gns.sort_f32_(tk, tv)
+        torch.cuda.synchronize()
+    n = 3 * t + 11
+    k = _f32_keys(n, 31337)
+    v = synth.iota_u32(n)
+    _, ev = oracle.sort(k.astype(np.float64), v)
+    tk, tv = torch.from_numpy(k.copy()).cuda(), torch.from_numpy(v.copy()).cuda()
+    gns.sort_f32_(tk, tv)
+    torch.cuda.synchronize()
+    perm = ev.astype(np.int64)
+    assert np.array_equal(tk.cpu().numpy().view(np.uint32), k[perm].view(np.uint32)), "after NaN"
