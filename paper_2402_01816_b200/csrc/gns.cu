@@ -9,6 +9,7 @@
 #include "gns_kernels.cuh"
 #include "gns_f32.cuh"
 #include "gns_tile64.cuh"
+#include "gns_multipass.cuh"
 
 #include <cuda_runtime.h>
 #include <cstdio>
@@ -89,6 +90,11 @@ struct Mode {
     bool omit = false;      // NEXT f2: Omitsort schedule (full buffer; gns_sort_omit)
 };
 
+// words of the multi-pass launch: [0] flag (NEXT f2), [1] ticket, then the
+// per-region completion counters of all passes (<= ntiles/4 + passes) or the
+// per-chunk counters of a two-phase reversal (ntiles)
+size_t mp_words(int ntiles) { return 2 + (size_t)ntiles + 64; }
+
 Layout layout(size_t n, const Mode &m, bool hv)
 {
     Layout L;
@@ -106,8 +112,9 @@ Layout layout(size_t n, const Mode &m, bool hv)
     if (m.limited) o = align_up(o + (size_t)L.ntiles * sizeof(int2), 256);
     L.off_flags = o;
     if (m.limited) o = align_up(o + (size_t)(L.ntiles + 1) * sizeof(unsigned), 256);
-    L.off_adapt = o;                   // the "input not presorted" word (NEXT f2)
-    o = align_up(o + sizeof(unsigned), 256);
+    L.off_adapt = o;                   // the "input not presorted" word (NEXT f2); full buffer: + the
+                                       // multi-pass ticket and completion counters (mp_words)
+    o = align_up(o + (m.limited ? 1 : mp_words(L.ntiles)) * sizeof(unsigned), 256);
     L.off_smp = o;                     // split-search samples, every SMP_G-th key of each region
     L.nsmp = n / SMP_G + 2;
     o = align_up(o + 2 * L.nsmp * sizeof(double), 256);
@@ -156,6 +163,28 @@ TileK tile_kern(bool hv, int o)
 {
     static const TileK t[2][NORD] = {GNS_ORDS(tile_sort2_kernel, false), GNS_ORDS(tile_sort2_kernel, true)};
     return t[hv][o];
+}
+using MultiK = decltype(&merge_multi_kernel<false, 0>);
+MultiK multi_kern(bool hv, int o)
+{
+    static const MultiK t[2][NORD] = {
+        {&merge_multi_kernel<false, 0>, &merge_multi_kernel<false, 1>, &merge_multi_kernel<false, 2>,
+         &merge_multi_kernel<false, 3>, &merge_multi_kernel<false, 4>, &merge_multi_kernel<false, 5>},
+        {&merge_multi_kernel<true, 0>, &merge_multi_kernel<true, 1>, &merge_multi_kernel<true, 2>,
+         &merge_multi_kernel<true, 3>, &merge_multi_kernel<true, 4>, &merge_multi_kernel<true, 5>}};
+    return t[hv][o];
+}
+// Full-buffer merge passes: one launch per level (merge_tstore_kernel), or,
+// with GNS_MULTI=1, one pipelined launch for all levels (merge_multi_kernel;
+// measured slower at 2^24 keys: dependency stalls of the
+// whole-array regions of the last passes).
+bool multi_on()
+{
+    static const bool on = [] {
+        const char *e = std::getenv("GNS_MULTI");
+        return e && e[0] == '1';
+    }();
+    return on;
 }
 using Tile3K = decltype(&tile_sort3_kernel<0>);
 Tile3K tile3_kern(int o)
@@ -267,6 +296,7 @@ gns_status ensure_attrs()
             GNS_ATTR(inplace_kern(hv, o), ts_smem(hv));
             GNS_ATTR(tile_kern(hv, o), t1_smem(hv));
             if (!hv) GNS_ATTR(tile3_kern(o), T3_SMEM);
+            GNS_ATTR(multi_kern(hv, o), ts_smem(hv));
         }
     }
 #undef GNS_ATTR
@@ -365,8 +395,8 @@ int launch_kind(const char *what)
                                   "split_cuts_kernel", "gather_samples_kernel", "omit_plan_kernel",
                                   "omit_prep_kernel", "omit_final_kernel", "iota_u32_kernel", "gather_u64_kernel",
                                   "f32_tile_sort_kernel", "f32_merge_kernel", "f32_reverse_kernel",
-                                  "f32_partition_kernel"};
-    for (int i = 0; i < 17; ++i)
+                                  "f32_partition_kernel", "merge_multi_kernel"};
+    for (int i = 0; i < 18; ++i)
         if (std::strcmp(what, names[i]) == 0) return i + 1;
     return 0;
 }
@@ -523,9 +553,60 @@ MergeGeo uniform_geo(const double *sk, const uint32_t *sv, double *dk, uint32_t 
 // `final_in_partner`, else in R.  Parity picks the tile-sort destination so
 // no copy pass is ever needed (an odd number of merge levels starts from P).
 // smp: two sample arrays of >= len/SMP_G + 2 keys (R's and P's), or nullptr.
+// All M merge passes of a full-buffer sort as one pipelined launch
+// (merge_multi_kernel): X = the tile sort's output, Y = the other region;
+// words = mp_words(ntiles) zeroed words ([0] = the NEXT f2 flag, written by
+// the tile sort).  `fin` = where the sort must end (X or Y).
+gns_status launch_multi(double *xk, uint32_t *xv, double *yk, uint32_t *yv, double *xs, double *ys, size_t n, int M,
+                        unsigned *words, double *fin, int ord, cudaStream_t st)
+{
+    const bool hv = xv != nullptr;
+    const int ntiles = (int)ceil_div(n, MTILE);
+    MultiGeo G;
+    std::memset(&G, 0, sizeof(G));
+    G.xk = xk;
+    G.xv = xv;
+    G.yk = yk;
+    G.yv = yv;
+    G.xs = xs;
+    G.ys = ys;
+    G.n = (long long)n;
+    G.passes = M;
+    G.ntiles = ntiles;
+    G.flag = words;
+    G.ticket = words + 1;
+    G.done = words + 2;
+    CUtensorMap xl, yl, xs_map, ys_map;
+    GNS_TRY(key_map(xk, n, hv, &xl, &G.x_idx0, &G.x_rows));
+    GNS_TRY(key_map(yk, n, hv, &yl, &G.y_idx0, &G.y_rows));
+    GNS_TRY(row_map(xk, n, true, MTILE / 16, &xs_map));
+    GNS_TRY(row_map(yk, n, true, MTILE / 16, &ys_map));
+    // NEXT f2: the moves of an ordered / strictly reversed input
+    const bool fin_x = fin == xk;
+    if (!fin_x) {
+        G.ord_src = xk;
+        G.ord_srcv = xv;
+        G.ord_dst = yk;
+        G.ord_dstv = yv;
+    }
+    G.rev_src = xk;
+    G.rev_srcv = xv;
+    G.rev_dst = yk;
+    G.rev_dstv = yv;
+    if (fin_x) {                 // reversal into Y, then back to X
+        G.rev2_src = yk;
+        G.rev2_srcv = yv;
+        G.rev2_dst = xk;
+        G.rev2_dstv = xv;
+    }
+    const int grid = (int)std::min<long long>((long long)M * ntiles, 2LL * num_sms());
+    return launch_pdl("merge_multi_kernel", multi_kern(hv, ord), std::max(grid, 1), MP_THREADS, ts_smem(hv), st, G, xl,
+                      yl, xs_map, ys_map);
+}
+
 gns_status sort_range(double *rk, uint32_t *rv, double *pk_, uint32_t *pv_, size_t len,
                       bool final_in_partner, int *corank, int ord, cudaStream_t st, unsigned *unsorted = nullptr,
-                      double *smp_r = nullptr, double *smp_p = nullptr)
+                      double *smp_r = nullptr, double *smp_p = nullptr, unsigned *mpw = nullptr)
 {
     if (len == 0) return GNS_OK;
     const int M = merge_passes_for(len);
@@ -536,11 +617,17 @@ gns_status sort_range(double *rk, uint32_t *rv, double *pk_, uint32_t *pv_, size
     uint32_t *ov = tile_to_partner ? rv : pv_;
     double *tile_k = ck;
     uint32_t *tile_v = cv;
+    double *cs = tile_to_partner ? smp_p : smp_r;      // samples of the region holding the current runs
+    double *os = tile_to_partner ? smp_r : smp_p;
+    if (mpw && unsorted == mpw && M > 0 && multi_on() && smp_r && smp_p) {
+        // one pipelined launch for all merge levels (flag word + counters zeroed together)
+        GNS_TRY(check(cudaMemsetAsync(mpw, 0, mp_words((int)ceil_div(len, MTILE)) * sizeof(unsigned), st), "memset"));
+        GNS_TRY(launch_tile_sort(rk, rv, ck, cv, len, ord, st, unsorted, cs));
+        return launch_multi(ck, cv, ok, ov, cs, os, len, M, mpw, final_in_partner ? pk_ : rk, ord, st);
+    }
     // NEXT f2: with `unsorted` the tile sort also tests whether the input is
     // already in order; if it is, every merge pass is omitted on the device.
     if (unsorted && M > 0) GNS_TRY(check(cudaMemsetAsync(unsorted, 0, sizeof(unsigned), st), "memset"));
-    double *cs = tile_to_partner ? smp_p : smp_r;      // samples of the region holding the current runs
-    double *os = tile_to_partner ? smp_r : smp_p;
     GNS_TRY(launch_tile_sort(rk, rv, ck, cv, len, ord, st, M > 0 ? unsorted : nullptr, M > 0 ? cs : nullptr));
     for (int p = 0; p < M; ++p) {
         const size_t L = (size_t)TILE << p;
@@ -822,7 +909,7 @@ gns_status run_sort(double *keys, uint32_t *vals, size_t n, const Mode &m, unsig
             GNS_TRY(sort_omit(keys, vals, n, ws, Lo, ord, st));
         } else if (!m.limited) {
             unsigned *unsorted = reinterpret_cast<unsigned *>(ws + Lo.off_adapt);
-            GNS_TRY(sort_range(keys, vals, bk, bv, n, false, corank, ord, st, unsorted, smp, smp + Lo.nsmp));
+            GNS_TRY(sort_range(keys, vals, bk, bv, n, false, corank, ord, st, unsorted, smp, smp + Lo.nsmp, unsorted));
         } else {
             int2 *deps = reinterpret_cast<int2 *>(ws + Lo.off_deps);
             unsigned *flags = reinterpret_cast<unsigned *>(ws + Lo.off_flags);

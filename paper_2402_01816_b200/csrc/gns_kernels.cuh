@@ -213,10 +213,19 @@ __device__ __forceinline__ void tma_load_1d(void *dst, const void *src, uint32_t
                  " [%0], [%1], %2, [%3], %4;"
                  :: "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy) : "memory");
 }
+#ifndef GNS_LOAD_POLICY
+#define GNS_LOAD_POLICY 0
+#endif
 __device__ __forceinline__ uint64_t policy_evict_first()
 {
     uint64_t p;
+#if GNS_LOAD_POLICY == 1
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+#elif GNS_LOAD_POLICY == 2
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+#else
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+#endif
     return p;
 }
 
