@@ -25,8 +25,19 @@
  *   - Pointers named keys/vals/src/dst/ws are DEVICE pointers.  The caller owns
  *     them; they must stay valid and untouched until the enqueued work on
  *     `stream` completes.
- *   - keys and vals must be 32-byte aligned (cudaMalloc / torch give >= 256 B);
- *     otherwise GNS_ERR_MISALIGNED.
+ *   - Alignment: the sorts (gns_sort_f64, _pairs_, _target_,
+ *     gns_sort_keys, gns_sort_omit and their _ws forms) need natural alignment
+ *     only -- keys 8-byte, vals 4-byte aligned (any view t[i:j] of a torch
+ *     tensor).  32-byte aligned arrays take the fast path directly; other
+ *     arrays peel the <= 7 head elements before the first 32-byte boundary,
+ *     sort the aligned rest and merge the head in place (one extra read +
+ *     write pass, gns_peel.cuh).  Keys and vals with no common 32-byte
+ *     boundary (e.g. keys[1:] with vals[2:]) route the vals through a
+ *     stream-ordered temporary of 4n bytes (the only case that exceeds the
+ *     workspace).  The per-step entry points (gns_tile_sort, gns_merge_pass,
+ *     gns_merge_inplace_top, gns_merge_two's dst), gns_sort_keys_u64,
+ *     gns_sort_f32 and every ws need 32-byte alignment.  Below these:
+ *     GNS_ERR_MISALIGNED, data untouched.
  *   - Every call is asynchronous on `stream` (0 = legacy default stream): a
  *     return of GNS_OK means the kernels are enqueued.  No host sync, except
  *     that the non-_ws sorts allocate their buffer stream-ordered
@@ -62,7 +73,7 @@ typedef enum {
     GNS_ERR_OUT_OF_MEMORY = 3,         /* buffer allocation failed; input untouched            */
     GNS_ERR_CUDA = 4,                  /* CUDA launch/runtime error                             */
     GNS_ERR_WORKSPACE_TOO_SMALL = 5,   /* ws NULL or ws_bytes < gns_workspace_bytes(...)        */
-    GNS_ERR_MISALIGNED = 6             /* keys/vals/ws not 32-byte aligned                      */
+    GNS_ERR_MISALIGNED = 6             /* below the required alignment (see Conventions)        */
 } gns_status;
 
 #define GNS_MAX_N ((size_t)0x7FFFFFFF)   /* 2^31 - 1 elements */

@@ -10,6 +10,7 @@
 #include "gns_f32.cuh"
 #include "gns_tile64.cuh"
 #include "gns_multipass.cuh"
+#include "gns_peel.cuh"
 
 #include <cuda_runtime.h>
 #include <cstdio>
@@ -162,6 +163,26 @@ using PartK = decltype(&partition_kernel<0>);
 TileK tile_kern(bool hv, int o)
 {
     static const TileK t[2][NORD] = {GNS_ORDS(tile_sort2_kernel, false), GNS_ORDS(tile_sort2_kernel, true)};
+    return t[hv][o];
+}
+using PeelK = decltype(&peel_merge_kernel<false, 0>);
+PeelK peel_kern(bool hv, int o)
+{
+    static const PeelK t[2][NORD] = {
+        {&peel_merge_kernel<false, 0>, &peel_merge_kernel<false, 1>, &peel_merge_kernel<false, 2>,
+         &peel_merge_kernel<false, 3>, &peel_merge_kernel<false, 4>, &peel_merge_kernel<false, 5>},
+        {&peel_merge_kernel<true, 0>, &peel_merge_kernel<true, 1>, &peel_merge_kernel<true, 2>,
+         &peel_merge_kernel<true, 3>, &peel_merge_kernel<true, 4>, &peel_merge_kernel<true, 5>}};
+    return t[hv][o];
+}
+using PeelHK = decltype(&peel_head_kernel<false, 0>);
+PeelHK peel_head_kern(bool hv, int o)
+{
+    static const PeelHK t[2][NORD] = {
+        {&peel_head_kernel<false, 0>, &peel_head_kernel<false, 1>, &peel_head_kernel<false, 2>,
+         &peel_head_kernel<false, 3>, &peel_head_kernel<false, 4>, &peel_head_kernel<false, 5>},
+        {&peel_head_kernel<true, 0>, &peel_head_kernel<true, 1>, &peel_head_kernel<true, 2>,
+         &peel_head_kernel<true, 3>, &peel_head_kernel<true, 4>, &peel_head_kernel<true, 5>}};
     return t[hv][o];
 }
 using MultiK = decltype(&merge_multi_kernel<false, 0>);
@@ -395,8 +416,9 @@ int launch_kind(const char *what)
                                   "split_cuts_kernel", "gather_samples_kernel", "omit_plan_kernel",
                                   "omit_prep_kernel", "omit_final_kernel", "iota_u32_kernel", "gather_u64_kernel",
                                   "f32_tile_sort_kernel", "f32_merge_kernel", "f32_reverse_kernel",
-                                  "f32_partition_kernel", "merge_multi_kernel"};
-    for (int i = 0; i < 18; ++i)
+                                  "f32_partition_kernel", "merge_multi_kernel", "peel_head_kernel",
+                                  "peel_merge_kernel"};
+    for (int i = 0; i < 20; ++i)
         if (std::strcmp(what, names[i]) == 0) return i + 1;
     return 0;
 }
@@ -777,13 +799,17 @@ gns_status mode_for(double f, size_t n, Mode *m)
     return GNS_OK;
 }
 
-gns_status validate_data(const double *keys, const uint32_t *vals, bool hv, size_t n)
+gns_status validate_data(const double *keys, const uint32_t *vals, bool hv, size_t n, bool strict = false)
 {
     if (n > GNS_MAX_N) return fail(GNS_ERR_INVALID_ARGUMENT, "n > GNS_MAX_N");
     if (n == 0) return GNS_OK;
     if (!keys || (hv && !vals)) return fail(GNS_ERR_INVALID_ARGUMENT, "NULL keys/vals with n > 0");
-    if (!is_aligned(keys, 32) || (hv && !is_aligned(vals, 32)))
-        return fail(GNS_ERR_MISALIGNED, "keys/vals must be 32-byte aligned");
+    // the per-step entry points launch the 32-byte kernels directly
+    if (strict && (!is_aligned(keys, 32) || (hv && !is_aligned(vals, 32))))
+        return fail(GNS_ERR_MISALIGNED, "keys/vals of the per-step entry points must be 32-byte aligned");
+    // natural alignment; other 8-byte / 4-byte alignments take the peel path (run_sort)
+    if (!is_aligned(keys, 8) || (hv && !is_aligned(vals, 4)))
+        return fail(GNS_ERR_MISALIGNED, "keys must be 8-byte and vals 4-byte aligned");
     return GNS_OK;
 }
 
@@ -889,8 +915,8 @@ gns_status sort_limited(double *keys, uint32_t *vals, size_t lo, size_t len, siz
 // target: 0 AscLeft, 1 AscRight, 2 DescLeft, 3 DescRight (NEXT f3).
 // AscRight = reverse(DescLeft), DescRight = reverse(AscLeft).
 // kt: key type (0 f64, 1 i64, 2 u64; NEXT f3).
-gns_status run_sort(double *keys, uint32_t *vals, size_t n, const Mode &m, unsigned char *ws, int target, int kt,
-                    cudaStream_t st)
+gns_status run_sort_aligned(double *keys, uint32_t *vals, size_t n, const Mode &m, unsigned char *ws, int target, int kt,
+                    cudaStream_t st, bool reverse_right = true)
 {
     if (n <= 1) return GNS_OK;
     GNS_TRY(ensure_attrs());
@@ -916,6 +942,92 @@ gns_status run_sort(double *keys, uint32_t *vals, size_t n, const Mode &m, unsig
             GNS_TRY(sort_limited(keys, vals, 0, n, m.buf, bk, bv, corank, deps, flags, ord, st, nullptr, n, smp,
                                  smp + Lo.nsmp));
         }
+    }
+    if (right && reverse_right) GNS_TRY(launch_reverse(keys, vals, n, st));
+    return GNS_OK;
+}
+
+// Natural alignment: head elements before the first
+// 32-byte boundary of keys (and vals) -- 0..7 -- or -1 if keys and vals
+// are misaligned relative to each other (no common boundary).
+int peel_count(const double *keys, const uint32_t *vals)
+{
+    const int hk = (int)((4 - (((uintptr_t)keys >> 3) & 3)) & 3);
+    if (!vals) return hk;
+    const int hv = (int)((8 - (((uintptr_t)vals >> 2) & 7)) & 7);
+    return (hv & 3) == hk ? hv : -1;
+}
+
+// The sort of keys[0:n) (+ vals) whatever their natural alignment: 32-byte
+// aligned arrays go straight to run_sort_aligned; otherwise the aligned
+// middle is sorted and the <= 7 head elements are merged in (gns_peel.cuh).
+gns_status run_sort(double *keys, uint32_t *vals, size_t n, const Mode &m, unsigned char *ws, int target, int kt,
+                    cudaStream_t st)
+{
+    if (n <= 1) return GNS_OK;
+    const int h = peel_count(keys, vals);
+    if (h == 0) return run_sort_aligned(keys, vals, n, m, ws, target, kt, st);
+    GNS_TRY(ensure_attrs());
+    const bool hv = vals != nullptr;
+    if (h < 0) {
+        // keys and vals with no common 32-byte boundary: the vals go through
+        // a temporary placed so that it shares the keys' boundary (4n extra
+        // bytes for the call)
+        uint32_t *tbase = nullptr;
+        cudaError_t e = cudaMallocAsync((void **)&tbase, (n + 8) * sizeof(uint32_t), st);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            return e == cudaErrorMemoryAllocation ? fail(GNS_ERR_OUT_OF_MEMORY, "cudaMallocAsync: out of memory")
+                                                  : check(e, "cudaMallocAsync");
+        }
+        const int hk = peel_count(keys, nullptr);
+        uint32_t *tv = tbase + ((8 - hk) & 7);          // peel_count(keys, tv) == hk
+        gns_status r = check(cudaMemcpyAsync(tv, vals, n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st), "copy");
+        if (r == GNS_OK) r = run_sort(keys, tv, n, m, ws, target, kt, st);
+        if (r == GNS_OK)
+            r = check(cudaMemcpyAsync(vals, tv, n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st), "copy");
+        const gns_status f = check(cudaFreeAsync(tbase, st), "cudaFreeAsync");
+        return r != GNS_OK ? r : f;
+    }
+    const bool right = target == 1 || target == 3;
+    const int ord = ord_of((target == 2) || (target == 1), kt);
+    const size_t hh = std::min<size_t>((size_t)h, n);
+    if (n > hh) {
+        // the middle in the target's merge order (a Right target is the
+        // reversal of the opposite-direction Left one: the whole array is
+        // reversed at the end, not the middle)
+        GNS_TRY(run_sort_aligned(keys + hh, hv ? vals + hh : nullptr, n - hh, m, ws, target, kt, st, false));
+    }
+    const Layout Lo = layout(n, m, hv);
+    if (n <= (size_t)PEEL_CHUNK * 2 || Lo.total == 0) {
+        // one CTA merges in order (no flags; the head sorted by the kernel)
+        if (hv)
+            GNS_TRY(launch_pdl("peel_merge_kernel", peel_kern(true, ord), 1, PEEL_NT, 0, st, keys, vals, (long long)n,
+                               (int)hh, (const double *)nullptr, (const uint32_t *)nullptr, (unsigned *)nullptr,
+                               (unsigned *)nullptr));
+        else
+            GNS_TRY(launch_pdl("peel_merge_kernel", peel_kern(false, ord), 1, PEEL_NT, 0, st, keys, (uint32_t *)nullptr,
+                               (long long)n, (int)hh, (const double *)nullptr, (const uint32_t *)nullptr,
+                               (unsigned *)nullptr, (unsigned *)nullptr));
+    } else {
+        // free workspace regions after the middle's sort: the co-rank array
+        // (>= n / 4096 + 1 words) holds the chunk flags and the ticket, the
+        // sample region the sorted head
+        unsigned *flags = reinterpret_cast<unsigned *>(ws + Lo.off_corank);
+        const size_t nch = ceil_div(n, PEEL_CHUNK);
+        double *hk = reinterpret_cast<double *>(ws + Lo.off_smp);
+        uint32_t *hvp = reinterpret_cast<uint32_t *>(hk + 8);
+        GNS_TRY(check(cudaMemsetAsync(flags, 0, (nch + 1) * sizeof(unsigned), st), "memset"));
+        if (hv)
+            GNS_TRY(launch_pdl("peel_head_kernel", peel_head_kern(true, ord), 1, 32, 0, st, (const double *)keys,
+                               (const uint32_t *)vals, (int)hh, hk, hvp));
+        else
+            GNS_TRY(launch_pdl("peel_head_kernel", peel_head_kern(false, ord), 1, 32, 0, st, (const double *)keys,
+                               (const uint32_t *)nullptr, (int)hh, hk, (uint32_t *)nullptr));
+        const int grid = (int)std::min<size_t>(nch, (size_t)num_sms() * 4);
+        GNS_TRY(launch_pdl("peel_merge_kernel", peel_kern(hv, ord), grid, PEEL_NT, 0, st, keys,
+                           hv ? vals : (uint32_t *)nullptr, (long long)n, (int)hh, (const double *)hk,
+                           (const uint32_t *)(hv ? hvp : nullptr), flags, flags + nch));
     }
     if (right) GNS_TRY(launch_reverse(keys, vals, n, st));
     return GNS_OK;
@@ -1223,8 +1335,8 @@ gns_status gns_tile_sort(const double *src_keys, const uint32_t *src_vals, doubl
 {
     const bool hv = src_vals != nullptr || dst_vals != nullptr;
     if (hv && (!src_vals || !dst_vals)) return fail(GNS_ERR_INVALID_ARGUMENT, "src_vals/dst_vals: both or neither");
-    GNS_TRY(validate_data(src_keys, src_vals, hv, n));
-    GNS_TRY(validate_data(dst_keys, dst_vals, hv, n));
+    GNS_TRY(validate_data(src_keys, src_vals, hv, n, true));
+    GNS_TRY(validate_data(dst_keys, dst_vals, hv, n, true));
     if (n == 0) return GNS_OK;
     GNS_TRY(ensure_attrs());
     return launch_tile_sort(src_keys, src_vals, dst_keys, dst_vals, n, 0, (cudaStream_t)stream);
@@ -1238,8 +1350,8 @@ gns_status gns_merge_pass(const double *src_keys, const uint32_t *src_vals, doub
 {
     const bool hv = src_vals != nullptr || dst_vals != nullptr;
     if (hv && (!src_vals || !dst_vals)) return fail(GNS_ERR_INVALID_ARGUMENT, "src_vals/dst_vals: both or neither");
-    GNS_TRY(validate_data(src_keys, src_vals, hv, n));
-    GNS_TRY(validate_data(dst_keys, dst_vals, hv, n));
+    GNS_TRY(validate_data(src_keys, src_vals, hv, n, true));
+    GNS_TRY(validate_data(dst_keys, dst_vals, hv, n, true));
     if (run_len == 0 || run_len % (MTILE / 2) != 0 || run_len > (size_t)1 << 30)
         return fail(GNS_ERR_INVALID_ARGUMENT, "run_len must be a positive multiple of gns_merge_tile_elems()/2, <= 2^30");
     if (n == 0) return GNS_OK;
@@ -1264,7 +1376,7 @@ gns_status gns_merge_two(const void *a_keys, const uint32_t *a_vals, size_t la, 
         return fail(GNS_ERR_INVALID_ARGUMENT, "NULL keys with a non-empty run");
     if (!is_aligned(a_keys, 8) || !is_aligned(b_keys, 8) || !is_aligned(a_vals, 4) || !is_aligned(b_vals, 4))
         return fail(GNS_ERR_MISALIGNED, "a/b keys must be 8-byte, vals 4-byte aligned");
-    GNS_TRY(validate_data((const double *)dst_keys, dst_vals, hv, n));
+    GNS_TRY(validate_data((const double *)dst_keys, dst_vals, hv, n, true));
     GNS_TRY(ensure_attrs());
     cudaStream_t st = (cudaStream_t)stream;
     if (la == 0 || lb == 0) {          // one run: a copy
@@ -1329,8 +1441,8 @@ gns_status gns_merge_inplace_top(double *keys, uint32_t *vals, const double *lef
 {
     const bool hv = vals != nullptr || left_vals != nullptr;
     if (hv && (!vals || !left_vals)) return fail(GNS_ERR_INVALID_ARGUMENT, "vals/left_vals: both or neither");
-    GNS_TRY(validate_data(keys, vals, hv, n));
-    GNS_TRY(validate_data(left_keys, left_vals, hv, nl));
+    GNS_TRY(validate_data(keys, vals, hv, n, true));
+    GNS_TRY(validate_data(left_keys, left_vals, hv, nl, true));
     if (nl > n || nl % 32 != 0 || nl == 0)
         return fail(GNS_ERR_INVALID_ARGUMENT, "need 0 < nl <= n, nl % 32 == 0");
     if (!ws || ws_bytes < merge_ws(n)) return fail(GNS_ERR_WORKSPACE_TOO_SMALL, "workspace too small");

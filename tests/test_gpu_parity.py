@@ -267,7 +267,7 @@ def test_error_paths_leave_data_untouched(gns):
     tk, _ = to_dev(k, None)
     before = tk.clone()
     assert gns.gns_sort_f64(int(tk.data_ptr()), n, 0.7, 0) == 2
-    assert gns.gns_sort_f64(int(tk.data_ptr()) + 8, n - 1, 1.0, 0) == 6
+    assert gns.gns_sort_f64(int(tk.data_ptr()) + 4, n - 1, 1.0, 0) == 6      # below natural alignment
     assert gns.gns_sort_f64_ws(int(tk.data_ptr()), n, 1.0, 0, 0, 0) == 5
     assert gns.gns_sort_f64_ws(int(tk.data_ptr()), n, 1.0, 256, 64, 0) == 5
     torch.cuda.synchronize()
@@ -884,3 +884,89 @@ def test_f32_nan_memory_safe(gns, payload):
     torch.cuda.synchronize()
     perm = ev.astype(np.int64)
     assert np.array_equal(tk.cpu().numpy().view(np.uint32), k[perm].view(np.uint32)), "after NaN"
+
+
+# ---------------------------------------------------------------- row b: natural alignment
+# keys need only 8-byte, vals 4-byte alignment; the sort of a
+# sliced view (not 32-byte aligned) takes the peel path (gns_peel.cuh) and is
+# bit-exact like any other (sorting applies to any contiguous
+# sequence).
+VIEW_SIZES = [1, 2, 5, 7, 9, 100, T1 - 3, T1 + 9, 3 * T1 + 77, 2 * 4096 * 3 + 5, (1 << 20) + 13]
+
+
+@pytest.mark.parametrize("payload", [False, True])
+@pytest.mark.parametrize("frac", [1.0, 0.5, 0.25])
+@pytest.mark.parametrize("view", [(1, 0), (3, 0), (5, 7), (2, 1), (7, 0)])
+@pytest.mark.parametrize("n", VIEW_SIZES)
+def test_sliced_views(gns, n, view, frac, payload):
+    lo, hi = view
+    full = n + lo + hi
+    k = synth.ties(full, 4100 + n + lo, 50)
+    k[::11] *= -1.0
+    v = synth.iota_u32(full)[::-1].copy() if payload else None
+    ek, ev = oracle.sort(k[lo:full - hi], None if v is None else v[lo:full - hi])
+    for use_ws in (False, True):
+        tk, tv = to_dev(k, v)
+        sk = tk[lo:full - hi]
+        sv = None if tv is None else tv[lo:full - hi]
+        ws = gns.alloc_workspace(n, frac, payload) if use_ws else None
+        gns.sort_(sk, sv, frac, workspace=ws)
+        torch.cuda.synchronize()
+        gk = tk.cpu().numpy()
+        assert_bitexact(gk[lo:full - hi], ek, None if tv is None else tv.cpu().numpy()[lo:full - hi], ev,
+                        what=f"view {view} n={n} frac={frac}")
+        # nothing outside the view moved
+        assert np.array_equal(gk[:lo].view(np.uint64), k[:lo].view(np.uint64))
+        assert np.array_equal(gk[full - hi:].view(np.uint64), k[full - hi:].view(np.uint64))
+
+
+@pytest.mark.parametrize("target", ["AscLeft", "DescLeft", "AscRight", "DescRight"])
+@pytest.mark.parametrize("key_type", ["f64", "i64", "u64"])
+@pytest.mark.parametrize("frac", [1.0, 0.5])
+def test_sliced_views_targets_key_types(gns, target, key_type, frac):
+    """Views of every key type and target (the peel merge runs in the
+    target's direction; Right targets reverse the whole view at the end)."""
+    n = 5 * T1 + 3
+    if key_type == "f64":
+        k = synth.ties(n + 3, 4200, 30)
+        k[::7] *= -1.0
+    else:
+        k = _int_keys(key_type, n + 3, 4201)
+    v = synth.iota_u32(n + 3)
+    kk, vv = k[3:], v[3:]
+    if key_type == "f64":
+        ek, ev = oracle.sort_target(kk, vv, target)
+    else:
+        ek, ev = oracle.sort_keys(kk, vv, key_type, target)
+    tk, tv = to_dev(k, v)
+    gns.sort_(tk[3:], tv[3:], frac, target=target)
+    torch.cuda.synchronize()
+    assert np.array_equal(tk.cpu().numpy()[3:].view(np.uint64), ek.view(np.uint64)), f"{key_type} {target}"
+    assert np.array_equal(tv.cpu().numpy()[3:], ev), f"{key_type} {target}"
+
+
+def test_sliced_view_ticket_passes(gns):
+    """A view at a size whose merge passes use the ticket-scheduled kernel
+    (>= 2^25 pairs), both buffer modes."""
+    n = (1 << 25) + 3
+    k = synth.uniform(n + 1, 4300)
+    v = synth.iota_u32(n + 1)
+    ek, ev = oracle.sort(k[1:], v[1:])
+    for frac in (1.0, 0.5):
+        tk, tv = to_dev(k, v)
+        gns.sort_(tk[1:], tv[1:], frac)
+        torch.cuda.synchronize()
+        assert_bitexact(tk.cpu().numpy()[1:], ek, tv.cpu().numpy()[1:], ev, what=f"frac={frac}")
+
+
+def test_sliced_views_incompatible_offsets(gns):
+    """keys and vals with no common 32-byte boundary (keys[1:] with vals[2:]):
+    vals go through an aligned temporary; still bit-exact."""
+    n = 3 * T1 + 5
+    k = synth.ties(n + 2, 4400, 20)
+    v = synth.iota_u32(n + 2)
+    ek, ev = oracle.sort(k[1:n + 1], v[2:n + 2])
+    tk, tv = to_dev(k, v)
+    gns.sort_(tk[1:n + 1], tv[2:n + 2], 1.0)
+    torch.cuda.synchronize()
+    assert_bitexact(tk.cpu().numpy()[1:n + 1], ek, tv.cpu().numpy()[2:n + 2], ev, what="incompatible")
