@@ -101,7 +101,9 @@ def test_argument_errors_before_any_cuda_call(gns):
     # all of these must return before touching CUDA (there is no GPU here)
     assert gns.gns_sort_f64(None, 10, 1.0, None) == 1
     assert gns.gns_sort_f64(256, 10, 0.75, None) == 2
-    assert gns.gns_sort_f64(264, 10, 1.0, None) == 6            # 8-byte but not 32-byte aligned
+    assert gns.gns_sort_f64(260, 10, 1.0, None) == 6            # below natural (8-byte) alignment
+    assert gns.gns_sort_pairs_f64_u32(256, 258, 10, 1.0, None) == 6   # vals below 4-byte alignment
+    assert gns.gns_tile_sort(264, None, 512, None, 10, None) == 6     # per-step entry points: 32-byte
     assert gns.gns_sort_pairs_f64_u32(256, None, 10, 1.0, None) == 1
     assert gns.gns_sort_f64(256, (1 << 31), 1.0, None) == 1
     assert gns.gns_sort_f64_ws(256, 1 << 20, 1.0, None, 0, None) == 5
@@ -112,7 +114,7 @@ def test_argument_errors_before_any_cuda_call(gns):
     assert gns.gns_sort_f64(None, 0, 1.0, None) == 0
     assert gns.gns_sort_f64(256, 1, 0.5, None) == 0
     assert gns.gns_status_string(6) == "GNS_ERR_MISALIGNED"
-    assert gns.gns_sort_f64(264, 10, 1.0, None) == 6
+    assert gns.gns_sort_f64(260, 10, 1.0, None) == 6
     assert "aligned" in gns.gns_last_error_string()
 
 
