@@ -124,6 +124,6 @@ def test_sort_keys_argument_errors(gns):
     assert gns.gns_sort_keys(256, 3, None, 10, 1.0, 0, None, 0, None) == 1
     assert gns.gns_sort_keys(256, -1, None, 10, 1.0, 0, None, 0, None) == 1
     assert gns.gns_sort_keys(256, 1, None, 10, 1.0, 4, None, 0, None) == 1
-    assert gns.gns_sort_keys(264, 2, None, 10, 1.0, 0, None, 0, None) == 6
+    assert gns.gns_sort_keys(260, 2, None, 10, 1.0, 0, None, 0, None) == 6
     assert gns.gns_sort_keys(256, 1, None, 10, 0.75, 0, None, 0, None) == 2
     assert gns.gns_sort_keys(None, 2, None, 0, 1.0, 0, None, 0, None) == 0
