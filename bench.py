@@ -149,19 +149,18 @@ def run_reference(args, rank, world):
     import oracle
     case = synth.config(args.config, args.sub)
     n = case.keys.size
-    sample_n = min(n, 1 << 22)
-    keys = case.keys[:sample_n].copy()
-    vals = None if case.vals is None else case.vals[:sample_n].copy()
-    for _ in range(args.warmup if args.warmup < 2 else 1):
+    keys = case.keys
+    vals = case.vals
+    for _ in range(min(args.warmup, 1)):
         oracle.sort(keys, vals)
     t = 0.0
     for _ in range(args.steps):
         t0 = time.perf_counter()
         oracle.sort(keys, vals)
         t += time.perf_counter() - t0
-    v = sample_n * args.steps / t
-    sample = (f"each step: oracle stable mergesort of the first 2^{sample_n.bit_length() - 1} keys of "
-              f"{case.name} on 1 host core (warm-up {min(args.warmup, 1)} step)")
+    v = n * args.steps / t
+    sample = (f"each step: the oracle's stable mergesort of the full workload ({case.name}, n=2^{n.bit_length() - 1}) "
+              f"on 1 host core (warm-up {min(args.warmup, 1)} step)")
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
@@ -282,15 +281,30 @@ def main():
     presorted = None
     others = None
     keytypes = None
+    half = None
     if rank == 0 and world == 1 and not args.no_footprint and args.config == 2:
+        half = half_buffer(gns, torch, dev, stream, flush, src_k, k, n, s)
         footprint = footprint_cfg5(gns, torch, dev, stream, flush)
         presorted = config4(gns, torch, dev, stream, flush)
         others = other_configs(gns, torch, dev, stream, flush)
         keytypes = key_types(gns, torch, dev, stream, flush)
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(case)
+    bitexact = None
+    if rank == 0 and not args.no_cpu_baseline:
+        # (rank 0's input is the BASELINE workload itself; other ranks' replicas
+        # are checked by the GPU-side properties above)
+        cpu, (ek, ev) = cpu_baseline(case)
+        gk = k.cpu().numpy()
+        bitexact = bool(np.array_equal(gk.view(np.uint64), ek.view(np.uint64)))
+        if hv:
+            bitexact = bitexact and bool(np.array_equal(v.cpu().numpy(), ev))
+        if world > 1:
+            cpu = None          # (cpu_baseline: rank 0 at N=1 only)
+
+    # ------------------- the allocating C-ABI call (buffer allocated per call)
+    alloc = allocating_api(gns, torch, dev, stream, src_k, src_v, k, v, n, hv, s, args.frac, restore,
+                           max(3, min(args.steps, 10)))
 
     launches_per_step = launches(plan, args.frac, n)
     ram = 1.0 + plan["workspace_bytes"] / (n * s)
@@ -317,10 +331,15 @@ def main():
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clk.summary(),
         "ram_pct": ram, "tfootprint_ms": ram * ms_per_step,
-        "valid": {"sorted": ok_sorted, "same_multiset_and_stable_ties": ok_perm},
+        "bitexact": bitexact,
+        "valid": {"sorted": ok_sorted, "same_multiset_and_stable_ties": ok_perm,
+                  "bitexact_vs_oracle": bitexact},
+        "allocating_api": alloc,
     }
     if cpu:
         line["cpu_baseline"] = cpu
+    if half:
+        line["buffer_0.5_same_config"] = half
     if footprint:
         line["footprint_cfg5"] = footprint
     if presorted:
@@ -450,6 +469,56 @@ def end_to_end(gns, torch, dev, stream, case, args, n, hv, ws, steps=None):
             "steps": steps, "serial_value": n * steps / t_serial, "host_result_sorted": ok,
             "path": "pinned host -> H2D -> gns_sort_*_ws -> D2H -> pinned host, three buffer sets rotating on "
                     "three streams (upload of step i+1, sort of step i, download of step i-1 overlap)"}
+
+
+def allocating_api(gns, torch, dev, stream, src_k, src_v, k, v, n, hv, s, frac, restore, reps):
+    """The plain C-ABI call (gns_sort_f64 / gns_sort_pairs_f64_u32: the buffer
+    is allocated and freed stream-ordered inside the call, SURVEY §8(a) a7,
+    reading A8) timed like the headline (L2 flushed, input restored untimed),
+    and the measured %RAM: the high-water mark of the device's default memory
+    pool (the one the call allocates from) during the call."""
+    ts = []
+    hw = None
+    for i in range(reps + 1):
+        restore()
+        torch.cuda.synchronize()
+        gns.gns_pool_high_water(1)          # (torch's caching allocator is a separate pool)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        gns.sort_(k, v, frac, stream=stream)
+        b.record(stream)
+        torch.cuda.synchronize()
+        if i:
+            ts.append(a.elapsed_time(b))
+        hw = gns.gns_pool_high_water(0)
+    ms = float(np.median(ts))
+    data = n * s
+    return {"ms": ms, "keys_per_s": n / (ms / 1e3), "pool_high_water_bytes": hw,
+            "ram_pct_measured": 1.0 + hw / data if hw is not None and hw != (1 << 64) - 1 else None,
+            "ram_pct_nominal": 1.0 + gns.workspace_bytes(n, frac, hv) / data,
+            "note": "cudaMallocAsync/cudaFreeAsync of the whole buffer inside every timed call"}
+
+
+def half_buffer(gns, torch, dev, stream, flush, src_k, k, n, s, reps=10):
+    """The headline workload at buffer fraction 0.5 (%RAM 1.5): runtime and
+    tFootprint beside the 1.0 line."""
+    ws = gns.alloc_workspace(n, 0.5, False, dev)
+    ts = []
+    for i in range(reps + 2):
+        k.copy_(src_k)
+        flush.fill_(1)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        gns.sort_(k, None, 0.5, workspace=ws)
+        b.record(stream)
+        torch.cuda.synchronize()
+        if i >= 2:
+            ts.append(a.elapsed_time(b))
+    ms = float(np.median(ts))
+    ram = 1.0 + ws.numel() / (n * s)
+    return {"ms": ms, "keys_per_s": n / (ms / 1e3), "ram_pct": ram, "tfootprint_ms": ram * ms,
+            "sorted": bool((k[1:] >= k[:-1]).all().item()),
+            "element_passes": gns.plan(n, 0.5, False)["element_passes"]}
 
 
 def footprint_cfg5(gns, torch, dev, stream, flush, reps=3):
@@ -630,18 +699,20 @@ def host_cpu():
 
 def cpu_baseline(case):
     """The oracle, as it stands, on the host: the full workload sorted 3x on 1
-    core (~10 s)."""
+    core (~10 s).  Also returns its output, which the timed GPU output is
+    compared with bit for bit."""
     import oracle
     keys = case.keys
     vals = case.vals
     reps = 3
+    out = None
     t0 = time.perf_counter()
     for _ in range(reps):
-        oracle.sort(keys, vals)
+        out = oracle.sort(keys, vals)
     t = time.perf_counter() - t0
-    return {"value": keys.size * reps / t, "unit": UNIT, "cores": 1, "kind": "oracle", "host": host_cpu(),
-            "sample": f"{case.name}, full n={keys.size}, sorted {reps}x by the single-threaded oracle "
-                      f"(host has {os.cpu_count()} cores)"}
+    return ({"value": keys.size * reps / t, "unit": UNIT, "cores": 1, "kind": "oracle", "host": host_cpu(),
+             "sample": f"{case.name}, full n={keys.size}, sorted {reps}x by the single-threaded oracle "
+                       f"(host has {os.cpu_count()} cores)"}, out)
 
 
 if __name__ == "__main__":

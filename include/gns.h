@@ -282,6 +282,14 @@ gns_status gns_merge_inplace_top(double *keys, uint32_t *vals, const double *lef
  * gns_sort_keys_u64, 0 other -- incl. the binary32 kernels) in
  * launch order, turns timing off and returns the number of timed launches
  * (-1 if timing was off or an event failed). */
+
+/* Measurement helper (bench.py, SURVEY §8(a) row a7 "measured %RAM"): the
+ * high-water mark in bytes of the current device's default memory pool --
+ * the pool the non-_ws sorts allocate their buffer from (cudaMallocAsync) --
+ * since the last reset.  reset != 0 resets it to the current usage first and
+ * returns 0.  Returns (size_t)-1 on a CUDA error.  Synchronous (no stream
+ * work); call it outside timed regions. */
+size_t gns_pool_high_water(int reset);
 gns_status gns_timing_begin(int max_launches);
 int gns_timing_end(float *ms, int *kind, int cap);
 

@@ -77,6 +77,7 @@ _c = {
     "gns_merge_pass": _sig("gns_merge_pass", [_vp, _vp, _vp, _vp, _sz, _sz, _vp, _sz, _vp]),
     "gns_merge_inplace_top": _sig("gns_merge_inplace_top", [_vp, _vp, _vp, _vp, _sz, _sz, _vp, _sz, _vp]),
     "gns_timing_begin": _sig("gns_timing_begin", [_i]),
+    "gns_pool_high_water": _sig("gns_pool_high_water", [_i], _sz),
     "gns_timing_end": _sig("gns_timing_end", [ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_int), _i]),
     "gns_tile_elems": _sig("gns_tile_elems", []),
     "gns_merge_tile_elems": _sig("gns_merge_tile_elems", []),
@@ -184,6 +185,10 @@ def gns_merge_pass(src_k, src_v, dst_k, dst_v, n, run_len, ws, ws_bytes, stream)
 
 def gns_merge_inplace_top(keys, vals, left_k, left_v, nl, n, ws, ws_bytes, stream) -> int:
     return _c["gns_merge_inplace_top"](keys, vals, left_k, left_v, nl, n, ws, ws_bytes, stream)
+
+
+def gns_pool_high_water(reset: int) -> int:
+    return _c["gns_pool_high_water"](reset)
 
 
 def gns_timing_begin(max_launches: int) -> int:

@@ -1492,6 +1492,21 @@ void gns_prof_read(unsigned long long *out)
 }
 #endif
 
+size_t gns_pool_high_water(int reset)
+{
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetDefaultMemPool(&pool, dev) != cudaSuccess)
+        return (size_t)-1;
+    cuuint64_t v = 0;
+    if (reset) {
+        if (cudaMemPoolSetAttribute(pool, cudaMemPoolAttrUsedMemHigh, &v) != cudaSuccess) return (size_t)-1;
+        return 0;
+    }
+    if (cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemHigh, &v) != cudaSuccess) return (size_t)-1;
+    return (size_t)v;
+}
+
 gns_status gns_timing_begin(int max_launches)
 {
     Timing &T = g_timing;

@@ -215,7 +215,8 @@ def test_inplace_top_merge_hazards(gns, layout):
     the unused buffer tail are poisoned with NaN, so a read-after-overwrite
     shows up as a wrong output.  Repeated to give races a chance."""
     rng = np.random.default_rng(123)
-    for rep, (n, nl) in enumerate([(64 * T, 32 * T), (64 * T + 40, 32 * T + 32), (20 * T + 7, 10 * T + 32)] * 4):
+    # 100 repetitions per layout (SURVEY §4 T4), the three geometries in turn
+    for rep, (n, nl) in enumerate(([(64 * T, 32 * T), (64 * T + 40, 32 * T + 32), (20 * T + 7, 10 * T + 32)] * 34)[:100]):
         a, b = _inplace_case(layout, n, nl, rng)
         va = np.arange(nl, dtype=np.uint32)
         vb = np.arange(nl, n, dtype=np.uint32)
@@ -245,15 +246,16 @@ def test_baseline_configs_full_size(gns, c, sub):
     case = synth.config(c, sub)
     k, v = case.keys, case.vals
     n = k.size
+    ek, ev = oracle.sort(k, v)
     if c in (1, 4):
-        # closed form (permutations of 0..n-1): keys -> i, payload -> inverse permutation
-        ek = np.arange(n, dtype=np.float64)
-        ev = None
+        # also the closed form (permutations of 0..n-1): keys -> i, payload ->
+        # inverse permutation -- an expectation independent of the oracle
+        ck = np.arange(n, dtype=np.float64)
+        assert_bitexact(ek, ck, what=f"{case.name} oracle vs closed form")
         if v is not None:
-            ev = np.empty(n, dtype=np.uint32)
-            ev[k.astype(np.int64)] = v
-    else:
-        ek, ev = oracle.sort(k, v)
+            cv = np.empty(n, dtype=np.uint32)
+            cv[k.astype(np.int64)] = v
+            assert np.array_equal(ev, cv), f"{case.name} oracle payload vs closed form"
     for frac in case.fractions + ([0.5] if c in (2, 3) else []):
         gk, gv = gpu_sort(gns, k, v, frac, use_ws=True)
         assert_bitexact(gk, ek, gv, ev, what=f"{case.name} frac={frac}")
@@ -970,3 +972,49 @@ def test_sliced_views_incompatible_offsets(gns):
     gns.sort_(tk[1:n + 1], tv[2:n + 2], 1.0)
     torch.cuda.synchronize()
     assert_bitexact(tk.cpu().numpy()[1:n + 1], ek, tv.cpu().numpy()[2:n + 2], ev, what="incompatible")
+
+
+# ------------------------------------------------- all-equal keys through the merges
+@pytest.mark.parametrize("frac", [1.0, 0.5, 0.125])
+@pytest.mark.parametrize("n", [3 * T1 + 5, 20 * T1 + 1, (1 << 20) + 7])
+@pytest.mark.parametrize("sched", ["default", "omit"])
+def test_all_equal_keys_defeat_shortcut(gns, n, frac, sched):
+    """All keys equal except a smaller LAST key: the whole-input "in order"
+    shortcut does not fire (one descent), so every tie goes through the tile
+    sort, every merge pass and (limited buffer) the in-place top merge; the
+    payload (= index) must come out as n-1 followed by 0..n-2 (stability).
+    Same with the Omitsort schedule (full buffer)."""
+    if sched == "omit" and frac != 1.0:
+        pytest.skip("the Omitsort schedule runs with the full buffer")
+    k = np.full(n, 7.0)
+    k[-1] = 3.0
+    v = synth.iota_u32(n)
+    ek, ev = oracle.sort(k, v)
+    assert ev[0] == n - 1 and np.array_equal(ev[1:], np.arange(n - 1, dtype=np.uint32))
+    tk, tv = to_dev(k, v)
+    if sched == "omit":
+        gns.sort_omit_(tk, tv)
+    else:
+        gns.sort_(tk, tv, frac)
+    torch.cuda.synchronize()
+    assert_bitexact(tk.cpu().numpy(), ek, tv.cpu().numpy(), ev, what=f"all-equal n={n} frac={frac} {sched}")
+    # signed zeros: all +-0.0 (equal under IEEE <) but one -1.0 at the end:
+    # the zeros' bit patterns must keep their input order
+    z = np.where(np.arange(n) % 3 == 0, -0.0, 0.0)
+    z[-1] = -1.0
+    ek, ev = oracle.sort(z, v)
+    tk, tv = to_dev(z, v)
+    if sched == "omit":
+        gns.sort_omit_(tk, tv)
+    else:
+        gns.sort_(tk, tv, frac)
+    torch.cuda.synchronize()
+    assert_bitexact(tk.cpu().numpy(), ek, tv.cpu().numpy(), ev, what=f"zeros n={n} frac={frac} {sched}")
+    # key-only (the 64-key network path with its zero-sign fix-up)
+    tk, _ = to_dev(z, None)
+    if sched == "omit":
+        gns.sort_omit_(tk, None)
+    else:
+        gns.sort_(tk, None, frac)
+    torch.cuda.synchronize()
+    assert_bitexact(tk.cpu().numpy(), ek, what=f"zeros key-only n={n} frac={frac} {sched}")
