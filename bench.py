@@ -8,9 +8,11 @@ key-only, buffer fraction 1.0) and its HBM-roofline fraction; tFootprint =
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                     [--config 2] [--frac 1.0] [--no-footprint]
 
-One process per GPU (torchrun for N > 1).  The sort does not shard without an
-exchange step: N > 1 runs N independent replicas, one per GPU,
-"scaling": "weak".  Timing: W untimed warm-up steps; each timed step restores
+One process per GPU (torchrun for N > 1).  N > 1 (default): the sharded sort
+(NEXT f4, dist.sort_distributed) of ONE array of N x 2^24 keys, rank r holding
+the r-th 2^24-key shard (rank 0's = BASELINE config 2): local sort, exact
+co-ranks, one NCCL all-to-all-v, merge of the received runs; "scaling":
+"weak"; per-rank %RAM reported.  --replicas: N independent single-GPU sorts.  Timing: W untimed warm-up steps; each timed step restores
 the unsorted input (untimed D2D copy) and flushes L2 (untimed 256 MiB write),
 then CUDA events on the sort's stream bracket exactly one sort; the K step
 times are summed; barrier + synchronize on both sides; max over ranks.
@@ -52,6 +54,8 @@ def parse():
     ap.add_argument("--no-footprint", action="store_true",
                     help="skip the config-5 tFootprint comparison (1.0 vs 0.5)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N > 1: independent replicas instead of the sharded sort")
     ap.add_argument("--profile-only", action="store_true",
                     help="one warm-up + one sort, no timing loops (for ncu)")
     return ap.parse_args()
@@ -195,13 +199,24 @@ def main():
 
     if not torch.cuda.is_available():
         raise SystemExit("bench.py needs a CUDA GPU (no CPU fallback)")
+    # (GNS_BENCH_BACKEND=gloo: ranks may share GPUs -- a functional check of
+    # the N > 1 paths on a one-GPU box; timings of shared GPUs mean nothing)
+    backend = os.environ.get("GNS_BENCH_BACKEND", "nccl")
+    local = local % torch.cuda.device_count() if backend == "gloo" else local
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     pg = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "gloo":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
         pg = dist
+
+    if world > 1 and not args.replicas:
+        run_sharded(args, rank, world, local, dev, pg)
+        return
 
     case = workload(args.config, args.sub, args.frac, rank)
     n = case.keys.size
@@ -255,7 +270,8 @@ def main():
         pg.barrier()
     step_ms = [a.elapsed_time(b) for a, b in ev]
     t_ms = sum(step_ms)
-    t_max, value = aggregate(torch, pg, t_ms, n, args.steps, world, dev)
+    cdev = torch.device("cpu") if os.environ.get("GNS_BENCH_BACKEND") == "gloo" else dev
+    t_max, value = aggregate(torch, pg, t_ms, n, args.steps, world, cdev)
     ms_per_step = t_max / args.steps
 
     # validity of the last output: GPU-side properties only (the oracle is not
@@ -353,6 +369,83 @@ def main():
     if pg:
         pg.barrier()
         pg.destroy_process_group()
+
+
+def run_sharded(args, rank, world, local, dev, pg):
+    """N > 1: the distributed stable sort of one array (NEXT f4), weak
+    scaling (2^24 keys per rank).  Device-timed per step with CUDA events on
+    the sort's stream (collectives included), max over ranks."""
+    import torch
+    import paper_2402_01816_b200 as gns
+    from paper_2402_01816_b200 import dist as gdist
+    n = 1 << 24
+    keys = synth.uniform(n, 1000 * 2 + (7919 * rank if rank else 0))       # rank 0: BASELINE config 2
+    src = torch.from_numpy(keys).to(dev)
+    k = torch.empty_like(src)
+    ws = gns.alloc_workspace(n, args.frac, False, dev)
+    stream = torch.cuda.current_stream(dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    info = {}
+    out = None
+
+    def step():
+        nonlocal out
+        k.copy_(src)
+        flush.fill_(1)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        out = gdist.sort_distributed(k, None, samples=64, buffer_fraction=args.frac, workspace=ws, info=info)
+        b.record(stream)
+        return a, b
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    pg.barrier()
+    evs = []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            evs.append(step())
+        torch.cuda.synchronize()
+    pg.barrier()
+    t_ms = sum(a.elapsed_time(b) for a, b in evs)
+    cdev = torch.device("cpu") if os.environ.get("GNS_BENCH_BACKEND") == "gloo" else dev   # (gloo: host tensors)
+    t_max, value = aggregate(torch, pg, t_ms, n, args.steps, world, cdev)
+    ok_k = out[0]
+    # validity: every piece sorted, pieces in rank order (last key <= next first), balanced sizes
+    ends = torch.tensor([ok_k[0].item() if ok_k.numel() else 0.0, ok_k[-1].item() if ok_k.numel() else 0.0,
+                         float(ok_k.numel()), float(bool((ok_k[1:] >= ok_k[:-1]).all().item()))],
+                        dtype=torch.float64, device=cdev)
+    allends = [torch.empty_like(ends) for _ in range(world)]
+    pg.all_gather(allends, ends)
+    e = torch.stack(allends).cpu().numpy()
+    ok = bool(all(e[:, 3] == 1.0) and all(e[i, 1] <= e[i + 1, 0] for i in range(world - 1))
+              and all(e[:, 2] == n))
+    ram = torch.tensor([info.get("ram_pct_peak", 0.0), info.get("ram_pct_sort", 0.0),
+                        info.get("ram_pct_exchange", 0.0)], dtype=torch.float64, device=cdev)
+    pg.all_reduce(ram, op=pg.ReduceOp.MAX)
+    ms = t_max / args.steps
+    if rank == 0:
+        plan = gns.plan(n, args.frac, False)
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded SplitMix64 U(0,1), see DESIGN.md §3)",
+            "config": {"workload": f"sharded stable sort of one array of {world} x 2^24 f64 U(0,1) keys "
+                                   f"(rank r holds shard r; rank 0's is BASELINE config 2), buffer fraction {args.frac}",
+                       "n_per_rank": n, "parallelism": f"sharded{world} (local sort, exact co-ranks, one NCCL "
+                                                       f"all-to-all-v, merge tree of the received runs)",
+                       "l2": "flushed (256 MiB write) before every timed step"},
+            "gpu_launches": args.steps * (plan["launches"] + world),
+            "clocks": clk.summary(),
+            "ram_pct": float(ram[0]), "ram_pct_local_sort": float(ram[1]), "ram_pct_exchange": float(ram[2]),
+            "tfootprint_ms": float(ram[0]) * ms,
+            "valid": {"pieces_sorted_in_rank_order_balanced": ok},
+            "e2e": None,
+        }
+        print(json.dumps(line), flush=True)
+    pg.barrier()
+    pg.destroy_process_group()
 
 
 def aggregate(torch, pg, t_ms, n, steps, world, device):

@@ -364,16 +364,23 @@ def sort_(keys, vals=None, buffer_fraction: float = 1.0, workspace=None, stream=
     return keys, vals
 
 
-def merge_two(a_k, a_v, b_k, b_v, stream=None):
-    """Stable merge of two sorted runs (a wins ties) into new tensors
-    (gns_merge_two).  Keys float64 / int64 / uint64; vals uint32 or None."""
+def merge_two(a_k, a_v, b_k, b_v, stream=None, out=None):
+    """Stable merge of two sorted runs (a wins ties) (gns_merge_two) into new
+    tensors, or into ``out`` = (keys, vals-or-None) views of la + lb elements
+    at natural alignment (the distributed sort's ping-pong tree).  Keys
+    float64 / int64 / uint64; vals uint32 or None."""
     import torch
     kt = _key_type(a_k)
     if b_k.dtype != a_k.dtype:
         raise TypeError("a and b keys differ in dtype")
     la, lb = a_k.numel(), b_k.numel()
-    out_k = torch.empty(la + lb, dtype=a_k.dtype, device=a_k.device)
-    out_v = None if a_v is None else torch.empty(la + lb, dtype=torch.uint32, device=a_k.device)
+    if out is None:
+        out_k = torch.empty(la + lb, dtype=a_k.dtype, device=a_k.device)
+        out_v = None if a_v is None else torch.empty(la + lb, dtype=torch.uint32, device=a_k.device)
+    else:
+        out_k, out_v = out
+        if out_k.numel() != la + lb or out_k.dtype != a_k.dtype or not out_k.is_contiguous():
+            raise ValueError("out keys: a contiguous tensor of la + lb keys of the same dtype")
     _check(gns_merge_two(_ptr(a_k), _ptr(a_v), la, _ptr(b_k), _ptr(b_v), lb, _ptr(out_k), _ptr(out_v), kt,
                          _stream_handle(stream)), "merge_two")
     return out_k, out_v

@@ -165,6 +165,16 @@ TileK tile_kern(bool hv, int o)
     static const TileK t[2][NORD] = {GNS_ORDS(tile_sort2_kernel, false), GNS_ORDS(tile_sort2_kernel, true)};
     return t[hv][o];
 }
+using MHeadK = decltype(&merge_head_kernel<false, 0>);
+MHeadK mhead_kern(bool hv, int o)
+{
+    static const MHeadK t[2][NORD] = {
+        {&merge_head_kernel<false, 0>, &merge_head_kernel<false, 1>, &merge_head_kernel<false, 2>,
+         &merge_head_kernel<false, 3>, &merge_head_kernel<false, 4>, &merge_head_kernel<false, 5>},
+        {&merge_head_kernel<true, 0>, &merge_head_kernel<true, 1>, &merge_head_kernel<true, 2>,
+         &merge_head_kernel<true, 3>, &merge_head_kernel<true, 4>, &merge_head_kernel<true, 5>}};
+    return t[hv][o];
+}
 using PeelK = decltype(&peel_merge_kernel<false, 0>);
 PeelK peel_kern(bool hv, int o)
 {
@@ -1376,7 +1386,18 @@ gns_status gns_merge_two(const void *a_keys, const uint32_t *a_vals, size_t la, 
         return fail(GNS_ERR_INVALID_ARGUMENT, "NULL keys with a non-empty run");
     if (!is_aligned(a_keys, 8) || !is_aligned(b_keys, 8) || !is_aligned(a_vals, 4) || !is_aligned(b_vals, 4))
         return fail(GNS_ERR_MISALIGNED, "a/b keys must be 8-byte, vals 4-byte aligned");
-    GNS_TRY(validate_data((const double *)dst_keys, dst_vals, hv, n, true));
+    GNS_TRY(validate_data((const double *)dst_keys, dst_vals, hv, n));
+    // dst at natural alignment: the first `off` outputs go through a one-thread
+    // head kernel so that the pipelined merge stores from a 16-byte aligned
+    // key row / 32-byte aligned vals (the distributed sort merges runs at any
+    // element offset)
+    int off = (int)(((uintptr_t)dst_keys >> 3) & 1);
+    if (hv) {
+        off = (int)((8 - (((uintptr_t)dst_vals >> 2) & 7)) & 7);
+        if (((((uintptr_t)dst_keys >> 3) + off) & 1) != 0)
+            return fail(GNS_ERR_MISALIGNED, "dst keys and vals have no common aligned element");
+    }
+    off = (int)std::min<size_t>((size_t)off, n);
     GNS_TRY(ensure_attrs());
     cudaStream_t st = (cudaStream_t)stream;
     if (la == 0 || lb == 0) {          // one run: a copy
@@ -1386,13 +1407,26 @@ gns_status gns_merge_two(const void *a_keys, const uint32_t *a_vals, size_t la, 
         if (hv) GNS_TRY(check(cudaMemcpyAsync(dst_vals, sv, n * 4, cudaMemcpyDeviceToDevice, st), "copy"));
         return GNS_OK;
     }
+    const int ordm = ord_of(false, (int)key_type);
+    if (off > 0) {
+        if (hv)
+            GNS_TRY(launch_pdl("merge_head_kernel", mhead_kern(true, ordm), 1, 32, 0, st, (const double *)a_keys, a_vals,
+                               (long long)la, (const double *)b_keys, b_vals, (long long)lb, (double *)dst_keys,
+                               dst_vals, off));
+        else
+            GNS_TRY(launch_pdl("merge_head_kernel", mhead_kern(false, ordm), 1, 32, 0, st, (const double *)a_keys,
+                               (const uint32_t *)nullptr, (long long)la, (const double *)b_keys,
+                               (const uint32_t *)nullptr, (long long)lb, (double *)dst_keys, (uint32_t *)nullptr,
+                               off));
+        if ((size_t)off == n) return GNS_OK;
+    }
     MergeGeo g;
     g.ak = (const double *)a_keys;
     g.av = hv ? a_vals : nullptr;
     g.bk = (const double *)b_keys;
     g.bv = hv ? b_vals : nullptr;
-    g.ok = (double *)dst_keys;
-    g.ov = hv ? dst_vals : nullptr;
+    g.ok = (double *)dst_keys + off;
+    g.ov = hv ? dst_vals + off : nullptr;
     g.n = (long long)n;
     g.L = (long long)la;
     g.single = 1;
@@ -1401,19 +1435,20 @@ gns_status gns_merge_two(const void *a_keys, const uint32_t *a_vals, size_t la, 
     g.sa = nullptr;
     g.so = nullptr;
     g.sb = nullptr;
-    const int ntiles = (int)ceil_div(n, MTILE);
+    g.off = off;
+    const int ntiles = (int)ceil_div(n - off, MTILE);
     PipeGeo pg;
     pg.g = g;
     pg.a_lim = g.ak + la;
     pg.b_lim = g.bk + lb;
     CUtensorMap map, amap, bmap;
-    GNS_TRY(row_map(g.ok, n, true, MTILE / 16, &map));
+    GNS_TRY(row_map(g.ok, n - off, true, MTILE / 16, &map));
     GNS_TRY(key_map(g.ak, la, hv, &amap, &pg.a_idx0, &pg.a_rows));
     GNS_TRY(key_map(g.bk, lb, hv, &bmap, &pg.b_idx0, &pg.b_rows));
     const int ctas = std::min(ntiles, 2 * num_sms());
     const int per = (int)ceil_div(ntiles, ctas);
     const int grid = (int)ceil_div(ntiles, per);
-    auto kern = merge_kern(hv, ord_of(false, (int)key_type));
+    auto kern = merge_kern(hv, ordm);
     return launch_pdl("merge_tstore_kernel", kern, grid, WS_THREADS, ts_smem(hv), st, pg, ntiles, per, map, amap, bmap,
                       Adapt{}, OmitList{}, map, amap, bmap);
 }

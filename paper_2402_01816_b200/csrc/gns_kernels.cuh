@@ -289,6 +289,7 @@ struct MergeGeo {
     const double *sa;   // samples of the source region (key at every SMP_G-th position), or nullptr
     double *so;         // samples of the output region written by this pass, or nullptr
     const double *sb;   // single (two-run) geometry: samples of B (every SMP_G-th key of bk), or nullptr
+    long long off = 0;  // single geometry: outputs [off, n) only; ok = the output of merge position off
 };
 
 struct TileSpan {
@@ -312,10 +313,31 @@ __device__ __forceinline__ TileSpan tile_span(const MergeGeo &g, int t)
         s.na = (int)min(g.L, rem);
         s.nb = (int)max(0LL, min(g.L, rem - g.L));
     }
-    s.k0 = (int)(s.g0 - s.pbase);
+    s.k0 = (int)(s.g0 - s.pbase + (g.single ? g.off : 0));
     // (64-bit: the last tile of a 2^31 - 1 element pair starts at 2^31 - 4096)
     s.k1 = (int)min((long long)s.k0 + MTILE, (long long)s.na + s.nb);
     return s;
+}
+
+// gns_merge_two into a destination that is not 32-byte aligned: the first
+// `off` (<= 7) outputs of the stable merge (A first, left wins ties,
+// PAPER.md:221), one thread; the pipelined merge writes the rest from dst + off.
+template <bool HV, int ORD>
+__global__ void merge_head_kernel(const double *A, const uint32_t *AV, long long la, const double *B,
+                                  const uint32_t *BV, long long lb, double *dst, uint32_t *dv, int off)
+{
+    pdl_wait();
+    if (threadIdx.x == 0) {
+        long long i = 0, j = 0;
+        for (int x = 0; x < off; ++x) {
+            const bool tb = j < lb && (i >= la || before<ORD>(B[j], A[i]));
+            dst[x] = tb ? B[j] : A[i];
+            if (HV) dv[x] = tb ? BV[j] : AV[i];
+            if (tb) ++j;
+            else ++i;
+        }
+    }
+    pdl_trigger();
 }
 
 // ---------------------------------------------------------- K2 partition
@@ -942,7 +964,7 @@ merge_tstore_kernel(PipeGeo pg, int ntiles, int per_cta, const __grid_constant__
             mbar_wait(&staged[st], (uint32_t)((i / NS) & 1));     // tile i staged by the 8 merge warps
             GNS_PT(p1);
             GNS_PADD(1, p1 - p0);
-            if (pg.g.n >= 16) {        // (n < 16: no full row; the merge warps stored the partial row)
+            if (pg.g.n - pg.g.off >= 16) {   // (< 16 outputs: no full row; the merge warps stored the partial row)
                 tma_store_2d(rev(i) ? &omap1 : &omap, skb(st), 0, (int)((long long)tile_of(i) * (MTILE / 16)));
                 bulk_commit();
             }
@@ -968,7 +990,7 @@ merge_tstore_kernel(PipeGeo pg, int ntiles, int per_cta, const __grid_constant__
     }
 
     // ---------------------------------------------------- merge warps 0-7
-    const long long n = pg.g.n;
+    const long long n = pg.g.n - pg.g.off;           // outputs of this launch (from ok)
     const long long full_rows = n >> 4;              // rows stored by TMA; a partial last row is stored by hand
     for (int i = 0; i < m; ++i) {
         const int st = i % NS;

@@ -58,6 +58,30 @@ class CpuOracleOps:
         return self.sort(k, v)
 
 
+class CpuFootprintOps(CpuOracleOps):
+    """The same CPU data steps plus the footprint-aware interface of the
+    product ops: sort with a buffer fraction and workspace (sized by the
+    library's own gns_workspace_bytes), and merge_into (the ping-pong tree
+    writes into given views instead of allocating)."""
+
+    def sort(self, keys, vals, buffer_fraction=1.0, workspace=None):
+        k, v = CpuOracleOps.sort(self, keys, vals)
+        keys.copy_(k)                         # in place, like the CUDA op
+        if vals is not None:
+            vals.copy_(v)
+        return keys, vals
+
+    def workspace_bytes(self, n, buffer_fraction, with_vals):
+        import paper_2402_01816_b200 as gns
+        return gns.workspace_bytes(n, buffer_fraction, with_vals)
+
+    def merge_into(self, a_k, a_v, b_k, b_v, d_k, d_v):
+        k, v = self.merge_two(a_k, a_v, b_k, b_v)
+        d_k.copy_(k)
+        if d_v is not None:
+            d_v.copy_(v)
+
+
 def make_shard(case, rank, world):
     rng = np.random.default_rng(1000 * case + rank)
     if case == 0:          # f64, heavy ties, signed zeros
@@ -154,3 +178,53 @@ def test_simulate_matches_collective_cpu(case, balanced, samples):
     if balanced:
         N = allk.size
         assert [o[0].numel() for o in outs] == [((g + 1) * N) // world - (g * N) // world for g in range(world)]
+
+
+def _fp_worker(rank, world, port, q):
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2402_01816_b200 import dist as gdist
+    n = 40000                                   # equal shards: balanced pieces fit the shard's memory
+    rng = np.random.default_rng(77 + rank)
+    k = rng.integers(0, 50, n).astype(np.float64)
+    v = (np.arange(n) + rank * n).astype(np.uint32)
+    for frac in (1.0, 0.5):
+        info = {}
+        tk, tv = torch.from_numpy(k.copy()), torch.from_numpy(v.copy())
+        ok, ov = gdist.sort_distributed(tk, tv, samples=8, ops=CpuFootprintOps(), buffer_fraction=frac, info=info)
+        q.put((frac, rank, ok.numpy().copy(), ov.numpy().copy(), info))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_distributed_sort_footprint_gloo(world):
+    """f4 footprint: the shard sorted in place with the caller's buffer
+    fraction, one receive buffer, the ping-pong merge tree inside the
+    shard's memory: per-rank peak %RAM <= 2.0 (1.0 + p for the local sort,
+    2.0 for the exchange of balanced equal shards), output bit-exact."""
+    import oracle
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_fp_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=240) for _ in range(world * 2)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    n = 40000
+    allk = np.concatenate([np.random.default_rng(77 + r).integers(0, 50, n).astype(np.float64) for r in range(world)])
+    ek, ev = oracle.sort(allk, np.arange(allk.size, dtype=np.uint32))
+    for frac in (1.0, 0.5):
+        got = sorted([r for r in res if r[0] == frac], key=lambda x: x[1])
+        assert np.concatenate([g[2] for g in got]).view(np.uint64).tolist() == ek.view(np.uint64).tolist()
+        assert np.concatenate([g[3] for g in got]).tolist() == ev.tolist()
+        for g in got:
+            info = g[4]
+            assert info["partner_bytes"] == 0                       # the tree ping-pongs in the shard's memory
+            assert info["ram_pct_sort"] <= 1.0 + frac + 0.02
+            assert info["ram_pct_exchange"] <= 2.0 + 1e-9
+            assert info["ram_pct_peak"] <= 2.0 + 0.02

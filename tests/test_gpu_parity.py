@@ -1018,3 +1018,25 @@ def test_all_equal_keys_defeat_shortcut(gns, n, frac, sched):
         gns.sort_(tk, None, frac)
     torch.cuda.synchronize()
     assert_bitexact(tk.cpu().numpy(), ek, what=f"zeros key-only n={n} frac={frac} {sched}")
+
+
+@pytest.mark.parametrize("off", [1, 2, 3, 5, 7])
+@pytest.mark.parametrize("la,lb", [(1, 1), (3, 9), (T + 5, 2 * T + 1), (5 * T1 + 3, 17)])
+def test_merge_two_into_unaligned_views(gns, la, lb, off):
+    """gns_merge_two writing into a view at any element offset (natural
+    alignment; the first outputs by the head kernel), keys and vals."""
+    a = np.sort(synth.ties(la, 31 + la, 20), kind="stable")
+    b = np.sort(synth.ties(lb, 32 + lb, 20), kind="stable")
+    va = np.arange(la, dtype=np.uint32)
+    vb = np.arange(la, la + lb, dtype=np.uint32)
+    # the stable merge of two sorted runs = the stable sort of their concatenation
+    ek, ev = oracle.sort(np.concatenate([a, b]), np.concatenate([va, vb]))
+    dk = torch.full((la + lb + 16,), np.nan, dtype=torch.float64, device="cuda")
+    dv = torch.full((la + lb + 16,), 7, dtype=torch.int64, device="cuda").to(torch.uint32)
+    ta, tva = to_dev(a, va)
+    tb, tvb = to_dev(b, vb)
+    gns.merge_two(ta, tva, tb, tvb, out=(dk[off:off + la + lb], dv[off:off + la + lb]))
+    torch.cuda.synchronize()
+    assert_bitexact(dk.cpu().numpy()[off:off + la + lb], ek, dv.cpu().numpy()[off:off + la + lb], ev,
+                    what=f"off={off} la={la} lb={lb}")
+    assert np.isnan(dk.cpu().numpy()[:off]).all() and np.isnan(dk.cpu().numpy()[off + la + lb:]).all()
