@@ -14,5 +14,8 @@ python bench.py --profile-only --warmup 1 > gpurun_out/plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
     --log-file gpurun_out/launches.csv python bench.py --profile-only --warmup 1 > gpurun_out/ncu_list.log 2>&1; echo "ncu_list_rc=$?"
 python bench.py --profile-only --warmup 1 > gpurun_out/plain2.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:"merge_tstore|tile_sort2" -s 2 -c 2 \
+ncu --set full --clock-control none --import-source on -k regex:"merge_tstore|tile_sort3" -s 12 -c 2 \
     -o gpurun_out/prof_full python bench.py --profile-only --warmup 1 > gpurun_out/ncu_full.log 2>&1; echo "ncu_full_rc=$?"
+python tools/f32_once.py > gpurun_out/plain_f32.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:"f32_merge" -s 11 -c 1 \
+    -o gpurun_out/prof_f32 python tools/f32_once.py > gpurun_out/ncu_f32.log 2>&1; echo "ncu_f32_rc=$?"

@@ -1,6 +1,6 @@
 """Counts the Blackwell data-movement instructions in the SASS of each kernel
 of libgns.so (TMA tensor loads/stores UTMALDG/UTMASTG, bulk copies UBLKCP,
-mbarrier ops SYNCS, programmatic-launch control) -> profiles/r1_sass_tma.txt.
+mbarrier ops SYNCS, programmatic-launch control) -> profiles/r2_sass_tma.txt.
 usage: python tools/sass_evidence.py"""
 import os
 import re
@@ -27,7 +27,7 @@ for line in sass.splitlines():
         for o in OPS:
             if op == o or op.startswith(o + "."):
                 per[cur][o] += 1
-out = ["# SASS evidence (r1): data-movement instructions per kernel of libgns.so (sm_100a)", "",
+out = ["# SASS evidence (r2): data-movement instructions per kernel of libgns.so (sm_100a)", "",
        "UTMALDG / UTMASTG = TMA tensor load / store, UBLKCP = TMA 1-D bulk copy, SYNCS = mbarrier ops,",
        "ACQBULK = griddepcontrol.wait (programmatic dependent launch).  `python tools/sass_evidence.py`.", "",
        "| kernel (mangled, ORD 0 instances) | " + " | ".join(OPS) + " |", "|---|" + "---|" * len(OPS)]
@@ -35,5 +35,5 @@ for f, c in per.items():
     if not re.search(r"ILi0E|ILb0ELi0E|ILb1ELi0E|Kernel[^I]*$|nan_count|iota|gather|f32_|reverse|split_cuts|inplace_deps", f):
         continue
     out.append(f"| `{f[:90]}` | " + " | ".join(str(c[o]) for o in OPS) + " |")
-open(os.path.join(ROOT, "profiles", "r1_sass_tma.txt"), "w").write("\n".join(out) + "\n")
+open(os.path.join(ROOT, "profiles", "r2_sass_tma.txt"), "w").write("\n".join(out) + "\n")
 print("\n".join(out[:40]))

@@ -9,7 +9,7 @@ from collections import OrderedDict
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 D = sys.argv[1] if len(sys.argv) > 1 else os.path.join(ROOT, "gpurun_out")
-TAG = sys.argv[2] if len(sys.argv) > 2 else "r1"
+TAG = sys.argv[2] if len(sys.argv) > 2 else "r2"
 N, S = 1 << 27, 12
 PEAK = 6533.5      # MEASURED_PEAKS.json hbm_gbs (copy read + write)
 OURS = ("tile_sort2", "merge_tstore", "merge_inplace", "partition", "inplace_deps", "gather_samples", "reverse")
@@ -40,7 +40,7 @@ def launches(path):
     return per
 
 
-out = [f"# ncu launch lists (r1) — BASELINE config 5: n = 2^27 f64 U(0,1) + u32 index, one sort per mode",
+out = [f"# ncu launch lists ({TAG}) — BASELINE config 5: n = 2^27 f64 U(0,1) + u32 index, one sort per mode",
        "", "`tools/ncu_cfg5.sh` (`--metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum "
        "--clock-control none`; cold-cache serialised replay: compare shares and bytes, not absolutes).", ""]
 for f in ("1.0", "0.5"):

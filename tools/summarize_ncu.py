@@ -18,7 +18,7 @@ from collections import OrderedDict
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 D = sys.argv[1] if len(sys.argv) > 1 else os.path.join(ROOT, "gpurun_out")
-TAG = sys.argv[2] if len(sys.argv) > 2 else "r1"
+TAG = sys.argv[2] if len(sys.argv) > 2 else "r2"
 PROF = os.path.join(ROOT, "profiles")
 os.makedirs(PROF, exist_ok=True)
 
@@ -119,7 +119,7 @@ def main():
                 f"{g('smsp__issue_active.avg.pct_of_peak_sustained_active')} | {g('launch__registers_per_thread')} | "
                 f"{g('sm__warps_active.avg.per_cycle_active')} | "
                 f"{g('l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum')} / "
-                f"{g('l1tex__data_pipe_lsu_wavefronts_mem_shared.sum')} | profiles/r1_sass_tma.txt |")
+                f"{g('l1tex__data_pipe_lsu_wavefronts_mem_shared.sum')} | profiles/r2_sass_tma.txt |")
     except Exception as e:  # noqa: BLE001
         lines.append(f"(full capture unavailable: {e})")
     open(os.path.join(PROF, f"{TAG}_ncu_summary.md"), "w").write("\n".join(lines) + "\n")
