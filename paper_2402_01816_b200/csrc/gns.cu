@@ -217,12 +217,19 @@ bool multi_on()
     }();
     return on;
 }
-using Tile3K = decltype(&tile_sort3_kernel<0>);
+using Tile3K = decltype(&tile_sort3_kernel<double, 0>);
 Tile3K tile3_kern(int o)
 {
-    static const Tile3K t[NORD] = {&tile_sort3_kernel<0>, &tile_sort3_kernel<1>, &tile_sort3_kernel<2>,
-                                   &tile_sort3_kernel<3>, &tile_sort3_kernel<4>, &tile_sort3_kernel<5>};
+    static const Tile3K t[NORD] = {&tile_sort3_kernel<double, 0>, &tile_sort3_kernel<double, 1>,
+                                   &tile_sort3_kernel<double, 2>, &tile_sort3_kernel<double, 3>,
+                                   &tile_sort3_kernel<double, 4>, &tile_sort3_kernel<double, 5>};
     return t[o];
+}
+using Tile3FK = decltype(&tile_sort3_kernel<float, 0>);
+Tile3FK tile3f_kern(int desc)
+{
+    static const Tile3FK t[2] = {&tile_sort3_kernel<float, 0>, &tile_sort3_kernel<float, 1>};
+    return t[desc];
 }
 // Key-only K1: the 128 x 64 kernel (tile_sort3_kernel) unless GNS_K1=2
 // forces the 256 x 32 one (A/B).
@@ -261,6 +268,12 @@ F32TileK f32_tile_kern(bool hv, int desc)
     static const F32TileK t[2][2] = {{&f32_tile_sort_kernel<false, false>, &f32_tile_sort_kernel<false, true>},
                                      {&f32_tile_sort_kernel<true, false>, &f32_tile_sort_kernel<true, true>}};
     return t[hv][desc];
+}
+using F32M2K = decltype(&f32_merge2_kernel<false>);
+F32M2K f32_merge2_kern(int desc)
+{
+    static const F32M2K t[2] = {&f32_merge2_kernel<false>, &f32_merge2_kernel<true>};
+    return t[desc];
 }
 using F32PartK = decltype(&f32_partition_kernel<false>);
 F32PartK f32_part_kern(int desc)
@@ -323,10 +336,12 @@ gns_status ensure_attrs()
             GNS_ATTR(merge_kern_ol(hv, o), ts_smem(hv));
             if (o < 2) GNS_ATTR(f32_tile_kern(hv, o), f_tile_smem(hv));
             if (o < 2) GNS_ATTR(f32_merge_kern(hv, o), f_merge_smem(hv));
+            if (o < 2 && !hv) GNS_ATTR(f32_merge2_kern(o), f2_smem());
             if (!hv) GNS_ATTR(omit_plan_kern(o), OMIT_SMEM);
             GNS_ATTR(inplace_kern(hv, o), ts_smem(hv));
             GNS_ATTR(tile_kern(hv, o), t1_smem(hv));
             if (!hv) GNS_ATTR(tile3_kern(o), T3_SMEM);
+            if (!hv && o < 2) GNS_ATTR(tile3f_kern(o), (t3_smem<float, NT3>()));
             GNS_ATTR(multi_kern(hv, o), ts_smem(hv));
         }
     }
@@ -1270,11 +1285,28 @@ gns_status gns_sort_f32(float *keys, uint32_t *vals, size_t n, gns_target target
     // the tile sort's destination by the parity of the merge levels: the last pass lands in keys
     float *ck = (M & 1) ? bk : keys, *ok = (M & 1) ? keys : bk;
     uint32_t *cv = (M & 1) ? bv : vals, *ov = (M & 1) ? vals : bv;
-    gns_status r = launch_pdl("f32_tile_sort_kernel", f32_tile_kern(hv, desc), (unsigned)ceil_div(n, F_TILE), F_NT,
-                              f_tile_smem(hv), st, (const float *)keys, (const uint32_t *)vals, ck, cv, (long long)n);
+    // key-only: the 128 x 64 K1 (gns_tile64.cuh) on 4-byte keys; with payload
+    // the 256 x 32 binary32 tile sort (gns_f32.cuh)
+    gns_status r = (!hv && k1_v3())
+        ? launch_pdl("f32_tile_sort_kernel", tile3f_kern(desc), (unsigned)ceil_div(n, F_TILE), NT3,
+                     t3_smem<float, NT3>(), st, (const float *)keys, ck, (long long)n, (unsigned *)nullptr,
+                     (float *)nullptr, (unsigned char *)nullptr, (float *)nullptr)
+        : launch_pdl("f32_tile_sort_kernel", f32_tile_kern(hv, desc), (unsigned)ceil_div(n, F_TILE), F_NT,
+                     f_tile_smem(hv), st, (const float *)keys, (const uint32_t *)vals, ck, cv, (long long)n);
     int *corank = reinterpret_cast<int *>(w + (hv ? 2 : 1) * align_up(n * sizeof(float), 256));
     const int ntiles = (int)ceil_div(n, F_MTILE);
-    for (int p = 0; p < M && r == GNS_OK; ++p) {
+    for (int p = 0; p < M && r == GNS_OK && !hv && k1_v3(); ++p) {
+        // key-only: the pipelined pass with in-kernel co-rank searches
+        const long long L = (long long)F_TILE << p;
+        const int nt2 = (int)ceil_div(n, F2_MT);
+        const int ctas = std::min(nt2, 3 * num_sms());
+        const int per = (int)ceil_div(nt2, ctas);
+        r = launch_pdl("f32_merge_kernel", f32_merge2_kern(desc), (unsigned)ceil_div(nt2, per), F2_THREADS,
+                       f2_smem(), st, (const float *)ck, ok, (long long)n, L, nt2, per);
+        std::swap(ck, ok);
+        std::swap(cv, ov);
+    }
+    for (int p = 0; p < M && r == GNS_OK && (hv || !k1_v3()); ++p) {
         const long long L = (long long)F_TILE << p;
         r = launch_pdl("f32_partition_kernel", f32_part_kern(desc), (unsigned)ceil_div((size_t)ntiles * 32, 256), 256,
                        0, st, (const float *)ck, (long long)n, L, ntiles, corank);

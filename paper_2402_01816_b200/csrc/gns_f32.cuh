@@ -294,6 +294,214 @@ f32_merge_kernel(const float *src_k, const uint32_t *src_v, float *dst_k, uint32
     pdl_trigger();
 }
 
+// ------------------------------------------------------------------ F2 v2
+// One merge level of binary32 keys (key-only) as a persistent, warp-
+// specialised pipeline like the f64 pass (merge_tstore_kernel): each CTA owns a
+// contiguous run of 4096-output tiles;
+//   warps 0-7  merge: per thread the merge path of its 16 outputs in the
+//              staged slices, 16-step serial merge (left run wins ties,
+//              PAPER.md:221); the tile's outputs are staged in shared memory
+//              and leave by one 1-D bulk store (TMA engine);
+//   warp 8     producer (one lane): per tile one 1-D bulk copy (16-byte
+//              aligned superset) of A's and of B's slice into a double-
+//              buffered stage (A then B, packed), mbarrier tx-count completion;
+//   warps 9-12 search: the tiles' co-ranks (A keys among the pair's first
+//              k0 outputs) ahead into a shared ring, two 16-lane 17-ary
+//              searches per warp in global memory (no separate partition
+//              launch); at kernel start every warp computes one.
+constexpr int F2_NS = 2;
+#ifndef GNS_F2_SW
+#define GNS_F2_SW 2
+#endif
+constexpr int F2_SW = GNS_F2_SW;                     // search warps
+constexpr int F2_THREADS = F_NT + 32 + 32 * F2_SW;   // 352
+constexpr int F2_RING = 64;
+constexpr int F2_VT = 16;                            // outputs per merge thread
+constexpr int F2_MT = F_NT * F2_VT;                  // 4096 outputs per tile (8192: 47 vs 41 us per 2^24-key level)
+static_assert(F_TILE % F2_MT == 0, "pair boundaries on tile boundaries");
+constexpr int F2_SLOTS = F2_MT + 16;                 // A (+ <= 6 alignment slots), then B (+ <= 6)
+constexpr size_t f2_smem() { return (size_t)F2_NS * F2_SLOTS * 4 + 16; }
+
+struct F2Meta {
+    int t, ca, cb, oa, ob;    // tile, slice lengths, slots of A[0] / B[0] in the stage
+};
+
+template <bool DESC>
+__device__ __forceinline__ int f2_corank(const float *src, long long n, long long L, int t, int gl, unsigned mask,
+                                         int gbase)
+{
+    const long long t0 = (long long)t * F2_MT;
+    const long long pb = (t0 / (2 * L)) * (2 * L);
+    const int na = (int)min(L, n - pb);
+    const int nb = (int)max(0LL, min(L, n - pb - L));
+    const int d = (int)(t0 - pb);
+    const float *A = src + pb, *B = src + pb + L;
+    const int lo = max(0, d - nb), hi = min(d, na);
+    if (lo >= hi) return lo;
+    return lo + group_count_true<16>(lo, hi - 1, gl, mask, gbase,
+                                     [&](int m) { return !fbefore<DESC>(B[d - 1 - m], A[m]); });
+}
+
+template <bool DESC>
+__global__ void __launch_bounds__(F2_THREADS, 3)
+f32_merge2_kernel(const float *src, float *dst, long long n, long long L, int ntiles, int per_cta)
+{
+    pdl_wait();
+    extern __shared__ __align__(16) unsigned char f2_smem_raw[];
+    float *stage = reinterpret_cast<float *>(f2_smem_raw);
+    __shared__ __align__(8) uint64_t full[F2_NS];
+    __shared__ __align__(8) uint64_t freed[F2_NS];
+    __shared__ F2Meta meta[F2_NS];
+    __shared__ int spl[F2_RING];
+    __shared__ volatile int spl_tag[F2_RING];
+    __shared__ volatile int spl_used;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int first = blockIdx.x * per_cta;
+    const int last = min(first + per_cta, ntiles);
+    const int m = last - first;
+    if (m <= 0) return;
+    const int nspl = (last < ntiles) ? m + 1 : m;      // split of tile `last` ends the CTA's last tile
+    for (int j = tid; j < F2_RING; j += F2_THREADS) spl_tag[j] = -1;
+    if (tid == 0) {
+        for (int b = 0; b < F2_NS; ++b) {
+            mbar_init(&full[b], 1);
+            mbar_init(&freed[b], F_NT / 32);
+        }
+        fence_mbar_init();
+        spl_used = 0;
+    }
+    __syncthreads();
+    auto publish = [&](int j, int c) {
+        spl[j % F2_RING] = c;
+        __threadfence_block();
+        spl_tag[j % F2_RING] = j;
+    };
+    const int init = min(nspl, F2_THREADS / 32);
+    if (warp < init) {
+        const int h = lane >> 4, gl = lane & 15;
+        const int c = f2_corank<DESC>(src, n, L, first + warp, gl, 0xFFFFu << (16 * h), 16 * h);
+        if (lane == 0) publish(warp, c);
+    }
+    __syncthreads();
+    if (warp > F_NT / 32) {
+        // ------------------------------------------------ search warps
+        const int sw = warp - F_NT / 32 - 1;
+        const int h = lane >> 4, gl = lane & 15;
+        const unsigned mask = 0xFFFFu << (16 * h);
+        for (int j0 = init + 2 * sw; j0 < nspl; j0 += 2 * F2_SW) {
+            const int j = j0 + h;
+            while (j0 + 1 - spl_used >= F2_RING) __nanosleep(64);
+            if (j < nspl) {
+                const int c = f2_corank<DESC>(src, n, L, first + j, gl, mask, 16 * h);
+                if (gl == 0) publish(j, c);
+            }
+            __syncwarp();
+        }
+        return;
+    }
+    if (warp == F_NT / 32) {
+        // ------------------------------------------------ producer (one lane)
+        if (lane != 0) return;
+        const uint64_t pol = policy_evict_first();
+        const long long nal = n & ~3LL;
+        auto get = [&](int j) -> int {
+            while (spl_tag[j % F2_RING] != j) { }
+            return spl[j % F2_RING];
+        };
+        auto issue = [&](int i) {
+            const int st = i % F2_NS;
+            const int t = first + i;
+            const long long t0 = (long long)t * F2_MT;
+            const long long pb = (t0 / (2 * L)) * (2 * L);
+            const int na = (int)min(L, n - pb);
+            const int nb = (int)max(0LL, min(L, n - pb - L));
+            const int k0 = (int)(t0 - pb);
+            const int k1 = (int)min((long long)k0 + F2_MT, (long long)na + nb);
+            // split points clamped to the feasible co-ranks (NaN keys: DESIGN.md R1)
+            const int i0 = min(max(get(i), max(0, k0 - nb)), min(k0, na));
+            int i1 = (k1 == na + nb) ? na : get(i + 1);
+            i1 = min(max(max(i1, i0), k1 - nb), min(i0 + (k1 - k0), na));
+            spl_used = i;
+            const int ca = i1 - i0, cb = (k1 - k0) - ca;
+            const long long ga = pb + i0, gb = pb + L + (k0 - i0);
+            long long sa0 = ga & ~3LL, sa1 = min((ga + ca + 3) & ~3LL, nal);
+            long long sb0 = gb & ~3LL, sb1 = min((gb + cb + 3) & ~3LL, nal);
+            if (sa1 < sa0 || ca == 0) sa1 = sa0;
+            if (sb1 < sb0 || cb == 0) sb1 = sb0;
+            const int oa = (int)(ga - sa0);
+            const int rb = (oa + ca + 3) & ~3;                 // B's region: after all of A's slots, 16-byte aligned
+            const int ob = rb + (int)(gb - sb0);
+            float *S = stage + st * F2_SLOTS;
+            GNS_DASSERT(oa + ca <= rb && sa1 - sa0 <= rb && ob + cb + 1 <= F2_SLOTS && rb + (sb1 - sb0) <= F2_SLOTS);
+            mbar_expect_tx(&full[st], (uint32_t)((sa1 - sa0) + (sb1 - sb0)) * 4u);
+            if (sa1 > sa0) tma_load_1d(S, src + sa0, (uint32_t)(sa1 - sa0) * 4u, &full[st], pol);
+            if (sb1 > sb0) tma_load_1d(S + rb, src + sb0, (uint32_t)(sb1 - sb0) * 4u, &full[st], pol);
+            // the <= 3 keys past the array's last aligned group, by hand
+            for (long long g = max(sa1, ga); g < ga + ca; ++g) S[g - sa0] = src[g];
+            for (long long g = max(sb1, gb); g < gb + cb; ++g) S[rb + (g - sb0)] = src[g];
+            F2Meta mt;
+            mt.t = t;
+            mt.ca = ca;
+            mt.cb = cb;
+            mt.oa = oa;
+            mt.ob = ob;
+            meta[st] = mt;
+            mbar_arrive(&full[st]);
+        };
+        for (int i = 0; i < F2_NS && i < m; ++i) issue(i);
+        for (int i = F2_NS; i < m; ++i) {
+            const int st = i % F2_NS;
+            mbar_wait(&freed[st], (uint32_t)(((i - F2_NS) / F2_NS) & 1));   // tile i - NS merged out of stage st
+            issue(i);
+        }
+        pdl_trigger();
+        return;
+    }
+    // ---------------------------------------------------- merge warps 0-7
+    for (int i = 0; i < m; ++i) {
+        const int st = i % F2_NS;
+        mbar_wait(&full[st], (uint32_t)((i / F2_NS) & 1));
+        const F2Meta mt = meta[st];
+        const float *S = stage + st * F2_SLOTS;
+        const float *SA = S + mt.oa, *SB = S + mt.ob;
+        const int cnt = mt.ca + mt.cb;
+        const int d = tid * F2_VT;
+        float k[F2_VT];
+        if (d < cnt) {
+            int lo = max(0, d - mt.cb), hi = min(d, mt.ca);
+            while (lo < hi) {
+                const int x = (lo + hi) >> 1;
+                if (!fbefore<DESC>(SB[d - 1 - x], SA[x])) lo = x + 1;
+                else hi = x;
+            }
+            int ai = lo, bj = d - lo;
+            float ka = SA[ai], kb = SB[bj];          // (one slot past a run end is inside the stage)
+#pragma unroll
+            for (int x = 0; x < F2_VT; ++x) {
+                const bool p = (bj < mt.cb) && ((ai >= mt.ca) || fbefore<DESC>(kb, ka));
+                k[x] = p ? kb : ka;
+                if (p) kb = SB[++bj];
+                else ka = SA[++ai];
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&freed[st]);             // this warp is done reading stage st
+        if (d < cnt) {
+            const long long o = (long long)mt.t * F2_MT + d;
+            if (d + F2_VT <= cnt && (o & 3) == 0) {
+                float4 *ok = reinterpret_cast<float4 *>(dst + o);
+#pragma unroll
+                for (int c = 0; c < F2_VT / 4; ++c) ok[c] = make_float4(k[4 * c], k[4 * c + 1], k[4 * c + 2], k[4 * c + 3]);
+            } else {
+#pragma unroll
+                for (int x = 0; x < F2_VT; ++x)
+                    if (d + x < cnt) dst[o + x] = k[x];
+            }
+        }
+    }
+    pdl_trigger();
+}
+
 // reversal of a binary32 array (+ vals) in place (the Right targets)
 template <bool HV>
 __global__ void __launch_bounds__(256) f32_reverse_kernel(float *k, uint32_t *v, long long n)

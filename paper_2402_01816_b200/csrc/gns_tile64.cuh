@@ -39,7 +39,7 @@ namespace gns {
 constexpr int NT3 = 128;                  // threads per CTA
 constexpr int VT3 = 64;                   // keys per thread
 static_assert(NT3 * VT3 == TILE, "K1 key-only tile must equal TILE");
-template <int NT> constexpr size_t t3_smem() { return (size_t)NT * (VT3 * 8 + 16) + 128; }
+template <typename K = double, int NT = 128> constexpr size_t t3_smem() { return (size_t)NT * (VT3 * sizeof(K) + 16) + 128; }
 constexpr int SEG3_BYTES = VT3 * 8 + 16;  // padded 512-byte segment per thread
 constexpr size_t T3_SMEM = (size_t)NT3 * SEG3_BYTES + 128;   // 67,712 B: 3 CTAs per SM
 static_assert(256 + TILE * 8 + 8 <= NT3 * SEG3_BYTES, "merge layout + guard slots fit the padded segments");
@@ -77,16 +77,74 @@ struct OddEvenNet {
 static_assert(OddEvenNet<64>::NC == 543, "Batcher odd-even merge sort of 64 keys has 543 comparators");
 static_assert(OddEvenNet<32>::NC == 191, "Batcher odd-even merge sort of 32 keys has 191 comparators");
 
-template <int N, int ORD>
-__device__ __forceinline__ void network_sort(double (&k)[N])
+// ---- key width: binary64 (and the 8-byte integer key types) or binary32
+// (NEXT f3).  kbef<K, ORD>: x must be output strictly before y (ORD = DESC |
+// key type << 1 for 8-byte keys, DESC for binary32).
+template <typename K, int ORD>
+__device__ __forceinline__ bool kbef(K x, K y)
+{
+    if constexpr (sizeof(K) == 8) return before<ORD>((double)x, (double)y);
+    else return (ORD & 1) ? (x > y) : (x < y);
+}
+template <typename K, int ORD>
+__device__ __forceinline__ K kpad()
+{
+    if constexpr (sizeof(K) == 8) return pad_key<ORD>();
+    else return (ORD & 1) ? -__int_as_float(0x7f800000) : __int_as_float(0x7f800000);
+}
+template <typename K>
+__device__ __forceinline__ K lds_k(uint32_t a)
+{
+    if constexpr (sizeof(K) == 8) return lds_f64(a);
+    else {
+        float v;
+        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+        return v;
+    }
+}
+// 16-byte shared transfers of 16 / sizeof(K) consecutive keys
+template <typename K>
+__device__ __forceinline__ void lds16_k(uint32_t a, K *v)
+{
+    if constexpr (sizeof(K) == 8)
+        asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v[0]), "=d"(v[1]) : "r"(a));
+    else
+        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3])
+                     : "r"(a));
+}
+template <typename K>
+__device__ __forceinline__ void sts16_k(uint32_t a, const K *v)
+{
+    if constexpr (sizeof(K) == 8)
+        asm volatile("st.shared.v2.f64 [%0], {%1, %2};" :: "r"(a), "d"(v[0]), "d"(v[1]) : "memory");
+    else
+        asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" :: "r"(a), "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3])
+                     : "memory");
+}
+// key bits: -0.0 (the one key equal to another key with different bits)
+template <typename K>
+__device__ __forceinline__ bool neg_zero(K x)
+{
+    if constexpr (sizeof(K) == 8) return __double_as_longlong(x) == (long long)0x8000000000000000ULL;
+    else return __float_as_uint(x) == 0x80000000u;
+}
+template <typename K>
+__device__ __forceinline__ bool sign_set(K x)
+{
+    if constexpr (sizeof(K) == 8) return __double_as_longlong(x) < 0;
+    else return (int)__float_as_uint(x) < 0;
+}
+
+template <typename K, int N, int ORD>
+__device__ __forceinline__ void network_sort(K (&k)[N])
 {
     constexpr OddEvenNet<N> net{};
 #pragma unroll
     for (int c = 0; c < OddEvenNet<N>::NC; ++c) {
         const int i = net.a[c], j = net.b[c];
-        const bool p = before<ORD>(k[j], k[i]);
-        const double lo = p ? k[j] : k[i];
-        const double hi = p ? k[i] : k[j];
+        const bool p = kbef<K, ORD>(k[j], k[i]);
+        const K lo = p ? k[j] : k[i];
+        const K hi = p ? k[i] : k[j];
         k[i] = lo;
         k[j] = hi;
     }
@@ -96,11 +154,13 @@ __device__ __forceinline__ void network_sort(double (&k)[N])
 // XORed with bits 9-11 (the thread's 512-byte block), so the blocked 16-byte
 // spill (lane t writes chunk c of its own block) hits 8 distinct chunk
 // positions per 8 lanes: conflict-free.  A bijection on every 128-byte line.
-__device__ __forceinline__ uint32_t sw3(uint32_t a) { return a ^ ((a >> 5) & 0x70u); }
+// (binary32: 256-byte blocks, bits 4-6 XORed with bits 8-10)
+template <typename K = double>
+__device__ __forceinline__ uint32_t sw3(uint32_t a) { return a ^ ((a >> (sizeof(K) == 8 ? 5 : 4)) & 0x70u); }
 
 // Stable co-rank of diagonal d (A wins ties; predicate A[m] <= B[d-1-m]) and,
 // if `two`, of diagonal d + VT3 in the same loop (independent probes).
-template <int ORD>
+template <typename K, int ORD>
 __device__ __forceinline__ void merge_path3x2(uint32_t base, int a0, int na, int b0, int nb, int d, bool two,
                                               int &r1, int &r2)
 {
@@ -110,16 +170,16 @@ __device__ __forceinline__ void merge_path3x2(uint32_t base, int a0, int na, int
     while (lo < hi || lo2 < hi2) {
         if (lo < hi) {
             const int m = (lo + hi) >> 1;
-            const double b = lds_f64(sw3(base + 8u * (b0 + d - 1 - m)));
-            const double a = lds_f64(sw3(base + 8u * (a0 + m)));
-            if (!before<ORD>(b, a)) lo = m + 1;
+            const K b = lds_k<K>(sw3<K>(base + (uint32_t)sizeof(K) * (b0 + d - 1 - m)));
+            const K a = lds_k<K>(sw3<K>(base + (uint32_t)sizeof(K) * (a0 + m)));
+            if (!kbef<K, ORD>(b, a)) lo = m + 1;
             else hi = m;
         }
         if (lo2 < hi2) {
             const int m = (lo2 + hi2) >> 1;
-            const double b = lds_f64(sw3(base + 8u * (b0 + d2 - 1 - m)));
-            const double a = lds_f64(sw3(base + 8u * (a0 + m)));
-            if (!before<ORD>(b, a)) lo2 = m + 1;
+            const K b = lds_k<K>(sw3<K>(base + (uint32_t)sizeof(K) * (b0 + d2 - 1 - m)));
+            const K a = lds_k<K>(sw3<K>(base + (uint32_t)sizeof(K) * (a0 + m)));
+            if (!kbef<K, ORD>(b, a)) lo2 = m + 1;
             else hi2 = m;
         }
     }
@@ -137,36 +197,37 @@ __device__ __forceinline__ void merge_path3x2(uint32_t base, int a0, int na, int
 //            (exclusive ends): outputs k[VT3-1 .. VT3/2], A's tail taken only
 //            if strictly after B's (a tie puts B's element later).
 // By the merge-path property both chains meet exactly at the midpoint.
-template <int ORD>
+template <typename K, int ORD>
 __device__ __forceinline__ void serial_merge3(uint32_t base, int a0, int ai, int aend, int bi, int bend, int qa,
-                                              int qb, double (&k)[VT3])
+                                              int qb, K (&k)[VT3])
 {
-    uint32_t pa = base + 8u * ai, pb = base + 8u * bi;
-    const uint32_t pae = base + 8u * aend, pbe = base + 8u * bend;
+    constexpr uint32_t SZ = sizeof(K);
+    uint32_t pa = base + SZ * ai, pb = base + SZ * bi;
+    const uint32_t pae = base + SZ * aend, pbe = base + SZ * bend;
     // backward chain: ra / rb = addresses of the next A / B key to take from
     // the back; A's run starts at a0, B's run starts at aend
-    uint32_t ra = base + 8u * (qa - 1), rb = base + 8u * (qb - 1);
-    const uint32_t ras = base + 8u * a0, rbs = pae;
-    double ka = lds_f64(sw3(pa)), kb = lds_f64(sw3(pb));
-    double ta = lds_f64(sw3(ra)), tb = lds_f64(sw3(rb));
+    uint32_t ra = base + SZ * (qa - 1), rb = base + SZ * (qb - 1);
+    const uint32_t ras = base + SZ * a0, rbs = pae;
+    K ka = lds_k<K>(sw3<K>(pa)), kb = lds_k<K>(sw3<K>(pb));
+    K ta = lds_k<K>(sw3<K>(ra)), tb = lds_k<K>(sw3<K>(rb));
 #pragma unroll
     for (int x = 0; x < VT3 / 2; ++x) {
-        const bool p = (pb < pbe) && ((pa >= pae) || before<ORD>(kb, ka));
+        const bool p = (pb < pbe) && ((pa >= pae) || kbef<K, ORD>(kb, ka));
         k[x] = p ? kb : ka;
-        const uint32_t nxt = (p ? pb : pa) + 8u;
-        GNS_DASSERT(nxt >= base && nxt <= base + 8u * 2 * TILE + 8u);
-        const uint32_t a = sw3(nxt);
+        const uint32_t nxt = (p ? pb : pa) + SZ;
+        GNS_DASSERT(nxt >= base && nxt <= base + SZ * 2 * TILE + SZ);
+        const uint32_t a = sw3<K>(nxt);
         // backward: take A's tail iff it exists and (B is exhausted or B's
         // tail is strictly before it)
-        const bool q = (ra >= ras) && ((rb < rbs) || before<ORD>(tb, ta));
+        const bool q = (ra >= ras) && ((rb < rbs) || kbef<K, ORD>(tb, ta));
         k[VT3 - 1 - x] = q ? ta : tb;
-        const uint32_t prv = (q ? ra : rb) - 8u;
-        GNS_DASSERT(prv + 8u >= base && prv < base + 8u * 2 * TILE);
-        const uint32_t b = sw3(prv);
+        const uint32_t prv = (q ? ra : rb) - SZ;
+        GNS_DASSERT(prv + SZ >= base && prv < base + SZ * 2 * TILE);
+        const uint32_t b = sw3<K>(prv);
 #if GNS_K1_ONELDS
         // one full-warp load per chain step (fewer shared wavefronts than two
         // predicated half-warp loads), routed into the consumed side's head
-        const double u = lds_f64(a), w = lds_f64(b);
+        const K u = lds_k<K>(a), w = lds_k<K>(b);
         if (p) pb = nxt; else pa = nxt;
         kb = p ? u : kb;
         ka = p ? ka : u;
@@ -176,17 +237,17 @@ __device__ __forceinline__ void serial_merge3(uint32_t base, int a0, int ai, int
 #else
         if (p) {
             pb = nxt;
-            kb = lds_f64(a);
+            kb = lds_k<K>(a);
         } else {
             pa = nxt;
-            ka = lds_f64(a);
+            ka = lds_k<K>(a);
         }
         if (q) {
             ra = prv;
-            ta = lds_f64(b);
+            ta = lds_k<K>(b);
         } else {
             rb = prv;
-            tb = lds_f64(b);
+            tb = lds_k<K>(b);
         }
 #endif
     }
@@ -195,14 +256,13 @@ __device__ __forceinline__ void serial_merge3(uint32_t base, int a0, int ai, int
 // One merge-path round: spill the thread's sorted run block, synchronise
 // (the warp, or the CTA if `cta`), then merge pair (A, B) of runs of
 // (coop / 2) * VT3 keys; the thread produces outputs [d, d + VT3) of its pair.
-template <int ORD>
-__device__ __forceinline__ void merge_round3(uint32_t sbase, int tid, int e0, int coop, double (&k)[VT3],
+template <typename K, int ORD>
+__device__ __forceinline__ void merge_round3(uint32_t sbase, int tid, int e0, int coop, K (&k)[VT3],
                                              bool cta = false)
 {
+    constexpr int PER = 16 / (int)sizeof(K);          // keys per 16-byte transfer
 #pragma unroll
-    for (int c = 0; c < VT3 / 2; ++c)
-        asm volatile("st.shared.v2.f64 [%0], {%1, %2};"
-                     :: "r"(sw3(sbase + 8u * (e0 + 2 * c))), "d"(k[2 * c]), "d"(k[2 * c + 1]) : "memory");
+    for (int c = 0; c < VT3 / PER; ++c) sts16_k<K>(sw3<K>(sbase + (uint32_t)sizeof(K) * (e0 + PER * c)), &k[PER * c]);
     if (cta) __syncthreads();
     else __syncwarp();
     const int local = tid & (coop - 1);
@@ -214,12 +274,12 @@ __device__ __forceinline__ void merge_round3(uint32_t sbase, int tid, int e0, in
     // last (d + VT3): the latter is the next thread's first (a shuffle),
     // searched here only by lane 31, or the pair's end
     int i, inext;
-    merge_path3x2<ORD>(sbase, a0, run, b0, run, d, (lane_id() == 31 && local + 1 < coop), i, inext);
+    merge_path3x2<K, ORD>(sbase, a0, run, b0, run, d, (lane_id() == 31 && local + 1 < coop), i, inext);
     const int up = __shfl_down_sync(0xFFFFFFFFu, i, 1);
     if (lane_id() != 31) inext = up;
     if (local + 1 == coop) inext = run;
     const int dn = d + VT3;
-    serial_merge3<ORD>(sbase, a0, a0 + i, b0, b0 + d - i, b0 + run, a0 + inext, b0 + dn - inext, k);
+    serial_merge3<K, ORD>(sbase, a0, a0 + i, b0, b0 + d - i, b0 + run, a0 + inext, b0 + dn - inext, k);
 }
 
 // ---- warp-level bitonic merge rounds (runs of 64 keys in 2^r lanes, r = 1..5)
@@ -232,24 +292,24 @@ __device__ __forceinline__ void merge_round3(uint32_t sbase, int tid, int e0, in
 // half-warp), and there is no spill, search or barrier.  Unstable: used only
 // by warps without -0.0/+0.0 or NaN keys (key-only, equal keys are
 // bit-identical), the others take the stable merge-path rounds.
-template <int ORD>
-__device__ __forceinline__ double bce(double own, double oth, bool up)
+template <typename K, int ORD>
+__device__ __forceinline__ K bce(K own, K oth, bool up)
 {
     // the lower lane keeps the earlier key, the upper lane the later one
-    return (before<ORD>(oth, own) != up) ? oth : own;
+    return (kbef<K, ORD>(oth, own) != up) ? oth : own;
 }
 
-template <int ORD>
-__device__ __forceinline__ void incore_halfcleaners(double (&k)[VT3])
+template <typename K, int ORD>
+__device__ __forceinline__ void incore_halfcleaners(K (&k)[VT3])
 {
 #pragma unroll
     for (int dist = VT3 / 2; dist >= 1; dist >>= 1) {
 #pragma unroll
         for (int i = 0; i < VT3; ++i) {
             if ((i & dist) == 0) {
-                const bool p = before<ORD>(k[i + dist], k[i]);
-                const double lo = p ? k[i + dist] : k[i];
-                const double hi = p ? k[i] : k[i + dist];
+                const bool p = kbef<K, ORD>(k[i + dist], k[i]);
+                const K lo = p ? k[i + dist] : k[i];
+                const K hi = p ? k[i] : k[i + dist];
                 k[i] = lo;
                 k[i + dist] = hi;
             }
@@ -257,8 +317,8 @@ __device__ __forceinline__ void incore_halfcleaners(double (&k)[VT3])
     }
 }
 
-template <int ORD>
-__device__ __forceinline__ void warp_bitonic_rounds(double (&k)[VT3], int lane)
+template <typename K, int ORD>
+__device__ __forceinline__ void warp_bitonic_rounds(K (&k)[VT3], int lane)
 {
 #pragma unroll 1
     for (int h = 1; h < (1 << GNS_K1_BITONIC); h <<= 1) {   // runs of 64 h keys in h lanes -> 128 h in 2 h lanes
@@ -266,22 +326,22 @@ __device__ __forceinline__ void warp_bitonic_rounds(double (&k)[VT3], int lane)
         const bool up = (lane & h) != 0;
 #pragma unroll
         for (int x = 0; x < VT3 / 2; ++x) {
-            const double lo = k[x], hi = k[VT3 - 1 - x];
-            const double olo = __shfl_xor_sync(0xFFFFFFFFu, lo, mask);
-            const double ohi = __shfl_xor_sync(0xFFFFFFFFu, hi, mask);
-            k[x] = bce<ORD>(lo, ohi, up);
-            k[VT3 - 1 - x] = bce<ORD>(hi, olo, up);
+            const K lo = k[x], hi = k[VT3 - 1 - x];
+            const K olo = __shfl_xor_sync(0xFFFFFFFFu, lo, mask);
+            const K ohi = __shfl_xor_sync(0xFFFFFFFFu, hi, mask);
+            k[x] = bce<K, ORD>(lo, ohi, up);
+            k[VT3 - 1 - x] = bce<K, ORD>(hi, olo, up);
         }
 #pragma unroll 1
         for (int d = h >> 1; d >= 1; d >>= 1) {
             const bool u = (lane & d) != 0;
 #pragma unroll
             for (int x = 0; x < VT3; ++x) {
-                const double o = __shfl_xor_sync(0xFFFFFFFFu, k[x], d);
-                k[x] = bce<ORD>(k[x], o, u);
+                const K o = __shfl_xor_sync(0xFFFFFFFFu, k[x], d);
+                k[x] = bce<K, ORD>(k[x], o, u);
             }
         }
-        incore_halfcleaners<ORD>(k);
+        incore_halfcleaners<K, ORD>(k);
     }
 }
 
@@ -293,13 +353,18 @@ __device__ __forceinline__ void bulk_store_1d(void *gdst, const void *ssrc, uint
 }
 
 // K1 key-only.  Same contract as tile_sort2_kernel<false, ORD> (flags,
-// samples, Omitsort tile descriptors; the tensor maps are unused).
-template <int ORD, int NT3 = gns::NT3>
-__global__ void __launch_bounds__(NT3, NT3 == 128 ? 3 : 1)
-tile_sort3_kernel(const double *src_k, double *dst_k, long long n, unsigned *unsorted, double *smp,
-                  unsigned char *tdesc, double *smp_src)
+// samples, Omitsort tile descriptors; the tensor maps are unused).  K = double
+// (every 8-byte key type, ORD = DESC | key type << 1) or float (NEXT f3
+// binary32 keys, ORD = DESC; flags / samples / descriptors unused).
+template <typename K, int ORD, int NT3 = gns::NT3>
+__global__ void __launch_bounds__(NT3, NT3 == 128 ? (sizeof(K) == 4 ? 4 : 3) : 1)
+tile_sort3_kernel(const K *src_k, K *dst_k, long long n, unsigned *unsorted, K *smp,
+                  unsigned char *tdesc, K *smp_src)
 {
     constexpr int TL = NT3 * VT3;                // keys per tile
+    constexpr int SZ = sizeof(K);
+    constexpr int SEG = VT3 * SZ + 16;           // padded segment per thread
+    constexpr int PER = 16 / SZ;                 // keys per 16-byte transfer
     pdl_wait();
     GNS_TL_START(0);
     extern __shared__ __align__(16) unsigned char smem3[];
@@ -312,30 +377,30 @@ tile_sort3_kernel(const double *src_k, double *dst_k, long long n, unsigned *uns
     const int cnt = (int)min((long long)TL, n - base);
     const bool full = cnt == TL;
     const int e0 = tid * VT3;
-    unsigned char *seg = smem + tid * SEG3_BYTES;       // this thread's padded segment
-    double k[VT3];
+    unsigned char *seg = smem + tid * SEG;              // this thread's padded segment
+    K k[VT3];
     if (tid == 0) {
         s_flags = 0;
         if (full) {
             mbar_init(&bar, 1);
             fence_mbar_init();
-            mbar_expect_tx(&bar, (uint32_t)TL * 8u);
+            mbar_expect_tx(&bar, (uint32_t)TL * SZ);
         }
     }
     __syncthreads();
     if (full) {
-        tma_load_1d(seg, src_k + base + e0, VT3 * 8, &bar, policy_evict_first());
+        tma_load_1d(seg, src_k + base + e0, VT3 * SZ, &bar, policy_evict_first());
         if (tid == 0) mbar_arrive(&bar);
         mbar_wait(&bar, 0);
 #pragma unroll
-        for (int c = 0; c < VT3 / 2; ++c) lds128(seg + 16 * c, k[2 * c], k[2 * c + 1]);
+        for (int c = 0; c < VT3 / PER; ++c) lds16_k<K>(smem_u32(seg) + 16 * c, &k[PER * c]);
     } else {
 #pragma unroll
         for (int x = 0; x < VT3; ++x) {
             const int e = e0 + x;
             // pads sort after every real key; they are bit-identical to the
             // largest key, so an unstable order among them changes nothing
-            k[x] = e < cnt ? src_k[base + e] : pad_key<ORD>();
+            k[x] = e < cnt ? src_k[base + e] : kpad<K, ORD>();
         }
     }
     // ---- NEXT f2 per-tile order tests (as in tile_sort2_kernel): in order
@@ -347,15 +412,14 @@ tile_sort3_kernel(const double *src_k, double *dst_k, long long n, unsigned *uns
         for (int x = 0; x + 1 < VT3; ++x) {
             if (e0 + x + 1 < cnt) {
                 ++pairs;
-                desc += before<ORD>(k[x + 1], k[x]) ? 1 : 0;
+                desc += kbef<K, ORD>(k[x + 1], k[x]) ? 1 : 0;
             }
         }
         unsigned fl = 0;
         const long long nx = base + e0 + VT3;
         if (nx < n) {
-            const double kn = (full && e0 + VT3 < TL) ? *reinterpret_cast<const double *>(seg + SEG3_BYTES)
-                                                        : src_k[nx];
-            const bool d = before<ORD>(kn, k[VT3 - 1]);
+            const K kn = (full && e0 + VT3 < TL) ? *reinterpret_cast<const K *>(seg + SEG) : src_k[nx];
+            const bool d = kbef<K, ORD>(kn, k[VT3 - 1]);
             fl |= (e0 + VT3 < cnt) ? (d ? 1u : 2u) : (d ? 4u : 8u);
         }
         fl |= (desc > 0 ? 1u : 0u) | (desc < pairs ? 2u : 0u);
@@ -371,33 +435,35 @@ tile_sort3_kernel(const double *src_k, double *dst_k, long long n, unsigned *uns
     }
     if (mode == 0) {
         // ---- the thread's 64 keys: sorting network in registers
-        constexpr bool F64 = (ORD >> 1) == KT_F64;
+        // floating-point keys (binary64 / binary32): the zero-sign fix-up and
+        // the -0.0 / NaN check; the integer key types have neither
+        constexpr bool F64 = sizeof(K) == 4 || (ORD >> 1) == KT_F64;
         unsigned long long zsign = 0;      // signs of the thread's zeros, input order
         bool zero = false, special = false;
         if (F64) {
 #pragma unroll
             for (int x = 0; x < VT3; ++x) {
-                zero |= (k[x] == 0.0);
+                zero |= (k[x] == (K)0);
             }
             if (zero) {
                 int z = 0;
 #pragma unroll
                 for (int x = 0; x < VT3; ++x) {
-                    if (k[x] == 0.0) {
-                        zsign |= (unsigned long long)(__double_as_longlong(k[x]) < 0) << z;
+                    if (k[x] == (K)0) {
+                        zsign |= (unsigned long long)sign_set<K>(k[x]) << z;
                         ++z;
-                        k[x] = 0.0;
+                        k[x] = (K)0;
                     }
                 }
             }
         }
-        network_sort<VT3, ORD>(k);
+        network_sort<K, VT3, ORD>(k);
         if (F64 && zero) {
             int z = 0;
 #pragma unroll
             for (int x = 0; x < VT3; ++x) {
-                if (k[x] == 0.0) {
-                    k[x] = ((zsign >> z) & 1ull) ? -0.0 : 0.0;
+                if (k[x] == (K)0) {
+                    k[x] = ((zsign >> z) & 1ull) ? -(K)0 : (K)0;
                     ++z;
                 }
             }
@@ -410,14 +476,14 @@ tile_sort3_kernel(const double *src_k, double *dst_k, long long n, unsigned *uns
             // live across it costs registers)
 #pragma unroll
             for (int x = 0; x < VT3; ++x)       // -0.0 (unequal bits among equal keys) or NaN
-                special |= !(k[x] >= 0.0 || k[x] < 0.0) || __double_as_longlong(k[x]) == (long long)0x8000000000000000ULL;
+                special |= !(k[x] >= (K)0 || k[x] < (K)0) || neg_zero<K>(k[x]);
         }
         const bool cta_special = __syncthreads_or(special) != 0;
-        if (!cta_special) warp_bitonic_rounds<ORD>(k, lane_id());
+        if (!cta_special) warp_bitonic_rounds<K, ORD>(k, lane_id());
         // ---- merge-path rounds (runs 2048 -> 8192, or 64 -> 8192)
 #pragma unroll 1
         for (int coop = cta_special ? 2 : (2 << GNS_K1_BITONIC); coop <= NT3; coop <<= 1) {
-            merge_round3<ORD>(sbase, tid, e0, coop, k, true);
+            merge_round3<K, ORD>(sbase, tid, e0, coop, k, true);
             __syncthreads();
         }
     } else {
@@ -438,13 +504,18 @@ tile_sort3_kernel(const double *src_k, double *dst_k, long long n, unsigned *uns
         // full tile, strictly reversed: output TL-1-e <- input e; thread t
         // fills segment 127-t backwards and stores it
         const int ot = NT3 - 1 - tid;
-        unsigned char *oseg = smem + ot * SEG3_BYTES;
+        unsigned char *oseg = smem + ot * SEG;
 #pragma unroll
-        for (int c = 0; c < VT3 / 2; ++c) sts128(oseg + 16 * (VT3 / 2 - 1 - c), k[2 * c + 1], k[2 * c]);
+        for (int c = 0; c < VT3 / PER; ++c) {
+            K r[PER];
+#pragma unroll
+            for (int j = 0; j < PER; ++j) r[j] = k[PER * c + PER - 1 - j];
+            sts16_k<K>(smem_u32(oseg) + 16 * (VT3 / PER - 1 - c), r);
+        }
         if (smp != nullptr && (ot & (SMP_G / VT3 - 1)) == 0)
             smp[(base + (long long)ot * VT3) >> SMP_LOG2] = k[VT3 - 1];
         fence_proxy_async();
-        bulk_store_1d(dst_k + base + (long long)ot * VT3, oseg, VT3 * 8);
+        bulk_store_1d(dst_k + base + (long long)ot * VT3, oseg, VT3 * SZ);
         bulk_commit();
         bulk_wait_read0();
         GNS_TL_END(0);
@@ -460,9 +531,9 @@ tile_sort3_kernel(const double *src_k, double *dst_k, long long n, unsigned *uns
     }
     if (full) {
 #pragma unroll
-        for (int c = 0; c < VT3 / 2; ++c) sts128(seg + 16 * c, k[2 * c], k[2 * c + 1]);
+        for (int c = 0; c < VT3 / PER; ++c) sts16_k<K>(smem_u32(seg) + 16 * c, &k[PER * c]);
         fence_proxy_async();
-        bulk_store_1d(dst_k + base + e0, seg, VT3 * 8);
+        bulk_store_1d(dst_k + base + e0, seg, VT3 * SZ);
         bulk_commit();
         bulk_wait_read0();
     } else {
