@@ -708,7 +708,9 @@ template <bool HV, int ORD>
 __device__ __forceinline__ void serial_merge_stage(uint32_t kbase, const uint32_t *sv, const PipeMeta &mt, int ai,
                                                    int aend, int bi, int bend, double (&k)[VT], uint32_t (&v)[VT])
 {
-    GNS_DASSERT(ai >= 0 && bi >= 0 && aend <= bend && bend <= stage_key_rows(HV) * 16);
+    // (A's slots precede B's when A is non-empty; an empty A may sit anywhere)
+    GNS_DASSERT(ai >= 0 && bi >= 0 && (ai >= aend || aend <= bend) && bend <= stage_key_rows(HV) * 16 &&
+                aend <= stage_key_rows(HV) * 16);
     double ka = lds_f64(stage_addr(kbase, ai)), kb = lds_f64(stage_addr(kbase, bi));
 #pragma unroll
     for (int x = 0; x < VT; ++x) {
