@@ -217,6 +217,17 @@ bool multi_on()
     }();
     return on;
 }
+// Chained uniform passes (no griddepcontrol.wait between merge levels, region
+// counters instead) only with GNS_CHAIN=1: measured 809 vs 798 us per 2^24-key
+// sort, bit-exact either way.
+bool chain_on()
+{
+    static const bool on = [] {
+        const char *e = std::getenv("GNS_CHAIN");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
 using Tile3K = decltype(&tile_sort3_kernel<double, 0>);
 Tile3K tile3_kern(int o)
 {
@@ -516,7 +527,8 @@ gns_status launch_tile_sort(const double *sk, const uint32_t *sv, double *dk, ui
 // Rows a3+a4 (fused K2+K3, persistent TMA pipeline) or, in place, a6 (K2 +
 // dependency ranges + K4 with the ticket/flag protocol).
 gns_status launch_merge(const MergeGeo &g, const double *lim_a, const double *lim_b, int *corank, int2 *deps,
-                        unsigned *flags, bool inplace, int ord, cudaStream_t st, Adapt ad = Adapt{})
+                        unsigned *flags, bool inplace, int ord, cudaStream_t st, Adapt ad = Adapt{},
+                        Chain chain = Chain{nullptr, nullptr})
 {
     const int ntiles = (int)ceil_div((size_t)g.n, MTILE);
     const bool hv = g.av != nullptr;
@@ -552,7 +564,7 @@ gns_status launch_merge(const MergeGeo &g, const double *lim_a, const double *li
         const int grid = (int)ceil_div(ntiles, per);
         auto kern = merge_kern(hv, ord);
         return launch_pdl("merge_tstore_kernel", kern, grid, WS_THREADS, ts_smem(hv), st, pg, ntiles, per, map, amap,
-                          bmap, ad, OmitList{}, map, amap, bmap);
+                          bmap, ad, OmitList{}, map, amap, bmap, chain);
     }
     GNS_TRY(launch_pdl("partition_kernel", partition_kern(ord),
                        (unsigned)ceil_div((size_t)ntiles * part_w(), 256), 256, 0, st, g, ntiles, corank));
@@ -672,9 +684,18 @@ gns_status sort_range(double *rk, uint32_t *rv, double *pk_, uint32_t *pv_, size
         GNS_TRY(launch_tile_sort(rk, rv, ck, cv, len, ord, st, unsorted, cs));
         return launch_multi(ck, cv, ok, ov, cs, os, len, M, mpw, final_in_partner ? pk_ : rk, ord, st);
     }
+    // Chained passes (Chain, gns_kernels.cuh): every uniform pass after the
+    // first starts as the previous one drains, tile by tile on region
+    // counters (mp_words: [0] flag, [1] spare, then the counters of every
+    // pass).  Only when every pass is the fused kernel (no ticket passes).
+    const int ntl = (int)ceil_div(len, MTILE);
+    const bool chain = mpw && unsorted == mpw && M > 1 && chain_on() && !ticket_pass(rv != nullptr, ntl);
     // NEXT f2: with `unsorted` the tile sort also tests whether the input is
     // already in order; if it is, every merge pass is omitted on the device.
-    if (unsorted && M > 0) GNS_TRY(check(cudaMemsetAsync(unsorted, 0, sizeof(unsigned), st), "memset"));
+    if (chain) GNS_TRY(check(cudaMemsetAsync(mpw, 0, mp_words(ntl) * sizeof(unsigned), st), "memset"));
+    else if (unsorted && M > 0) GNS_TRY(check(cudaMemsetAsync(unsorted, 0, sizeof(unsigned), st), "memset"));
+    unsigned *cnt_prev = nullptr;
+    unsigned *cnt_next = chain ? mpw + 2 : nullptr;
     GNS_TRY(launch_tile_sort(rk, rv, ck, cv, len, ord, st, M > 0 ? unsorted : nullptr, M > 0 ? cs : nullptr));
     for (int p = 0; p < M; ++p) {
         const size_t L = (size_t)TILE << p;
@@ -706,7 +727,14 @@ gns_status sort_range(double *rk, uint32_t *rv, double *pk_, uint32_t *pv_, size
                 ad.rev_gather = 0;
             }
         }
-        GNS_TRY(launch_merge(g, ck + len, ck + len, corank, nullptr, nullptr, false, ord, st, ad));
+        Chain chn{nullptr, nullptr};
+        if (chain) {
+            chn.dep = cnt_prev;                        // (pass 0: griddepcontrol.wait on the tile sort)
+            chn.sig = last ? nullptr : cnt_next;
+            cnt_prev = cnt_next;
+            cnt_next += ceil_div(len, 4 * L);          // next-pass regions of this pass
+        }
+        GNS_TRY(launch_merge(g, ck + len, ck + len, corank, nullptr, nullptr, false, ord, st, ad, chn));
         std::swap(ck, ok);
         std::swap(cv, ov);
         std::swap(cs, os);
@@ -738,7 +766,7 @@ gns_status launch_merge_list(const MergeGeo &g0, const MergeGeo &g1, const int *
     OmitList ol{list, count, pg[1]};
     const int grid = std::min(ntiles, 2 * num_sms());
     return launch_pdl("merge_tstore_kernel", merge_kern_ol(hv, ord), grid, WS_THREADS, ts_smem(hv), st, pg[0], ntiles,
-                      0, map[0], amap[0], bmap[0], Adapt{}, ol, map[1], amap[1], bmap[1]);
+                      0, map[0], amap[0], bmap[0], Adapt{}, ol, map[1], amap[1], bmap[1], Chain{nullptr, nullptr});
 }
 
 // NEXT f2: Omitsort on the full buffer.  The tile sort leaves
@@ -1482,7 +1510,7 @@ gns_status gns_merge_two(const void *a_keys, const uint32_t *a_vals, size_t la, 
     const int grid = (int)ceil_div(ntiles, per);
     auto kern = merge_kern(hv, ordm);
     return launch_pdl("merge_tstore_kernel", kern, grid, WS_THREADS, ts_smem(hv), st, pg, ntiles, per, map, amap, bmap,
-                      Adapt{}, OmitList{}, map, amap, bmap);
+                      Adapt{}, OmitList{}, map, amap, bmap, Chain{nullptr, nullptr});
 }
 
 gns_status gns_split_cuts(const void *sorted_keys, gns_key_type key_type, size_t n, const void *spl_keys,

@@ -821,19 +821,49 @@ struct OmitList {
     PipeGeo pg1;
 };
 
+// Chained uniform passes of a full-buffer sort (no griddepcontrol.wait): the
+// pass triggers its dependent launch at start, its CTAs start as the previous
+// pass's CTAs exit, and every tile waits -- before its co-rank search reads
+// anything -- until the previous pass has stored its pair region
+// [q 2L, (q+1) 2L) (dep[q] counts the stored previous-pass tiles there; it
+// also covers the write-after-read hazard on this pass's output, which the
+// previous pass read within the same region).  At exit the producer adds
+// the CTA's tiles to this pass's counters, per next-pass region of 4L
+// (sig), after its last store completed.  Deadlock-free: a pass launches
+// only once every CTA of the previous one has started (PDL trigger at start),
+// so every region it waits on belongs to resident CTAs.
+struct Chain {
+    const unsigned *dep;     // previous pass's region counters, or nullptr (griddepcontrol.wait)
+    unsigned *sig;           // this pass's region counters, or nullptr (last pass)
+};
+__device__ __forceinline__ void red_release_add(unsigned *p, unsigned v)
+{
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void chain_wait(const Chain &ch, const MergeGeo &g, int t)
+{
+    const long long span = 2 * g.L;
+    const long long q = ((long long)t * MTILE) / span;
+    const long long lo = q * span, hi = min(g.n, lo + span);
+    const unsigned want = (unsigned)((hi - lo + MTILE - 1) / MTILE);
+    while (ld_acquire(ch.dep + q) < want) __nanosleep(64);
+}
+
 template <bool HV, int ORD, int NS = 2, bool OL = false>
 __global__ void __launch_bounds__(WS_THREADS, 2)
 merge_tstore_kernel(PipeGeo pg, int ntiles, int per_cta, const __grid_constant__ CUtensorMap omap,
                     const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap bmap, Adapt ad,
                     const OmitList ol, const __grid_constant__ CUtensorMap omap1,
-                    const __grid_constant__ CUtensorMap amap1, const __grid_constant__ CUtensorMap bmap1)
+                    const __grid_constant__ CUtensorMap amap1, const __grid_constant__ CUtensorMap bmap1, Chain ch)
 {
 #ifdef GNS_PROF
     unsigned long long acc[16] = {};
     const long long t_entry = clock64();
     const int tl_slot = min(31, 1 + (63 - __clzll(pg.g.L)) - TILE_LOG2);
 #endif
-    pdl_wait();
+    const bool chained = !OL && ch.dep != nullptr;
+    if (chained) pdl_trigger();          // (the next pass may launch once every CTA of this one started)
+    else pdl_wait();
     GNS_TL_START(tl_slot);
     // NEXT f2 flag word: loaded now, tested after the first split searches
     // (which only read), so its latency hides behind them
@@ -895,7 +925,12 @@ merge_tstore_kernel(PipeGeo pg, int ntiles, int per_cta, const __grid_constant__
     };
     // the first splits: every warp computes one (32-lane sample-guided search)
     const int init = min(nspl, WS_THREADS / 32);
-    if (warp < init) {
+    const bool adapt = (f_adapt & 1u) == 0u || (f_adapt & 2u) == 0u;
+    if (warp < init && !(chained && adapt)) {
+        if (chained) {
+            if (lane == 0) chain_wait(ch, geo(warp).g, tile_of(warp));
+            __syncwarp();
+        }
         const int c = tile_corank<32, ORD>(geo(warp).g, tile_of(warp), lane, 0xFFFFFFFFu, 0);
         if (lane == 0) publish(warp, c);
     }
@@ -911,6 +946,7 @@ merge_tstore_kernel(PipeGeo pg, int ntiles, int per_cta, const __grid_constant__
         const bool pre = (f_adapt & 1u) == 0u;
         const double *ck = pre ? ad.pre_k : ad.rev_k;
         const uint32_t *cv = pre ? ad.pre_v : ad.rev_v;
+        if (chained) pdl_wait();          // (the moves read the previous pass's moves: full completion)
         if (ck) adapt_move<HV>(pg.g, per_cta, ck, cv, !pre && ad.rev_gather);
         pdl_trigger();
         return;
@@ -926,6 +962,10 @@ merge_tstore_kernel(PipeGeo pg, int ntiles, int per_cta, const __grid_constant__
             const int j = j0 + h;
             while (j0 + 1 - spl_used >= SPL_RING) { __nanosleep(64); }
             if (j < nspl) {
+                if (chained) {
+                    if (gl == 0) chain_wait(ch, geo(j).g, tile_of(j));
+                    __syncwarp(mask);
+                }
                 const int c = tile_corank<16, ORD>(geo(j).g, tile_of(j), gl, mask, 16 * h);
                 if (gl == 0) publish(j, c);
             }
@@ -951,8 +991,10 @@ merge_tstore_kernel(PipeGeo pg, int ntiles, int per_cta, const __grid_constant__
         auto issue = [&](int i) {
             const int st = i % NS;
             const bool r = rev(i);
-            pipe_issue<HV>(geo(i), r ? amap1 : amap, r ? bmap1 : bmap, tile_of(i), get_split(i),
-                           (i + 1 < nspl) ? get_split(i + 1) : 0, skb(st), svb(st),
+            const int s0 = get_split(i);
+            const int s1 = (i + 1 < nspl) ? get_split(i + 1) : 0;
+            if (chained) fence_proxy_async_global();   // the region's stores (acquired by a search lane) before our loads
+            pipe_issue<HV>(geo(i), r ? amap1 : amap, r ? bmap1 : bmap, tile_of(i), s0, s1, skb(st), svb(st),
                            &full[st], &meta[st], policy);
             spl_used = i;
         };
@@ -980,6 +1022,18 @@ merge_tstore_kernel(PipeGeo pg, int ntiles, int per_cta, const __grid_constant__
             }
         }
         bulk_wait0();
+        if (!OL && ch.sig != nullptr) {
+            // this CTA's stored tiles, per next-pass region of 4L
+            __threadfence();
+            const long long span = 4 * pg.g.L;
+            long long t = first;
+            while (t < last) {
+                const long long r = (t * MTILE) / span;
+                const long long tend = min((long long)last, ((r + 1) * span + MTILE - 1) / MTILE);
+                red_release_add(ch.sig + r, (unsigned)(tend - t));
+                t = tend;
+            }
+        }
 #ifdef GNS_PROF
         atomicMax(&g_tl[tl_slot][1], gtimer());
         acc[7] = clock64() - t_entry;

@@ -135,10 +135,6 @@ __device__ __forceinline__ unsigned mp_target(const MultiGeo &G, int p, long lon
     const long long lo = q * span, hi = min(G.n, lo + span);
     return (unsigned)((hi - lo + MTILE - 1) / MTILE);
 }
-__device__ __forceinline__ void red_release_add(unsigned *p, unsigned v)
-{
-    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
-}
 // stored tiles whose completion is signalled once their bulk group is done:
 // at most MP_PEND groups stay in flight, so the producer never waits for a
 // store's global write except when it has nothing else to do
