@@ -1,0 +1,53 @@
+"""The A/B code paths selected by environment knobs (read once per process,
+so each runs in a subprocess): GNS_MULTI=1 (all merge levels in one
+persistent launch), GNS_CHAIN=1 (chained passes on region counters),
+GNS_K1=2 (the 256 x 32 key-only tile sort), GNS_MERGE_MODE=1 (ticket passes
+for every size).  Each sorts a few seeded inputs through the C-ABI and
+compares bit-exactly with the oracle."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, ROOT_DIR)
+import oracle, synth, paper_2402_01816_b200 as gns
+bad = 0
+for n, seed, pay in ((3 * 8192 + 77, 1, True), (1 << 20, 2, False), ((1 << 21) + 5, 3, True), (40000, 4, False)):
+    k = synth.ties(n, seed, 1000) if seed % 2 else synth.uniform(n, seed)
+    v = synth.iota_u32(n) if pay else None
+    ek, ev = oracle.sort(k, v)
+    for frac in (1.0, 0.5):
+        tk = torch.from_numpy(k.copy()).cuda()
+        tv = None if v is None else torch.from_numpy(v.copy()).cuda()
+        gns.sort_(tk, tv, frac)
+        torch.cuda.synchronize()
+        ok = np.array_equal(tk.cpu().numpy().view(np.uint64), ek.view(np.uint64))
+        ok = ok and (v is None or np.array_equal(tv.cpu().numpy(), ev))
+        if not ok:
+            bad += 1
+            print("FAIL", n, frac, pay)
+# ordered / strictly reversed inputs (the adaptive shortcuts inside the variant)
+for k in (np.arange(3 * 8192 + 5, dtype=np.float64), np.arange(5 * 8192, 0, -1).astype(np.float64)):
+    tk = torch.from_numpy(k.copy()).cuda()
+    gns.sort_(tk, None, 1.0)
+    torch.cuda.synchronize()
+    if not np.array_equal(tk.cpu().numpy(), np.sort(k)):
+        bad += 1
+        print("FAIL presorted", k.size)
+print("bad", bad)
+sys.exit(1 if bad else 0)
+"""
+
+
+@pytest.mark.parametrize("env", [{"GNS_MULTI": "1"}, {"GNS_CHAIN": "1"}, {"GNS_K1": "2"}, {"GNS_MERGE_MODE": "1"},
+                                 {"GNS_MERGE_MODE": "0"}])
+def test_env_variant_bitexact(env):
+    e = dict(os.environ, **env)
+    r = subprocess.run([sys.executable, "-c", SCRIPT.replace("ROOT_DIR", repr(ROOT))], capture_output=True, text=True, env=e, timeout=600)
+    assert r.returncode == 0, (env, r.stdout[-2000:], r.stderr[-2000:])

@@ -1,8 +1,9 @@
 """Randomised parity fuzzing of every sort entry point against the oracle
 (run under gpurun).  Each case draws: size (log-uniform, ragged), input shape
 (uniform, heavy ties, presorted / reversed runs, blocks, specials), key type,
-target, payload, buffer fraction and entry point (sort_, sort_omit_,
-sort_u64_, sort_f32_), then compares bit-exactly.
+target, payload, buffer fraction, entry point (sort_, sort_omit_,
+sort_u64_, sort_f32_) and, for sort_ / sort_omit_, a view offset (0..7 head
+and tail elements: the natural-alignment path), then compares bit-exactly.
 usage: python tools/fuzz.py [--seconds 600] [--max-log2 22] [--seed 1]"""
 import argparse
 import os
@@ -91,8 +92,14 @@ def one():
         return ok, (entry, kt, n, target)
     v = synth.iota_u32(n)[::-1].copy() if payload else None
     ek, ev = oracle.sort_keys(k, v, kt, target)
-    tk = torch.from_numpy(k.copy()).cuda()
-    tv = None if v is None else torch.from_numpy(v.copy()).cuda()
+    lo = int(rng.integers(0, 8)) if rng.random() < 0.4 else 0          # view t[lo:lo+n]
+    hi = int(rng.integers(0, 8)) if lo else 0
+    kk = np.concatenate([np.zeros(lo, k.dtype), k, np.zeros(hi, k.dtype)])
+    tkf = torch.from_numpy(kk).cuda()
+    tk = tkf[lo:lo + n]
+    tvf = None if v is None else torch.from_numpy(np.concatenate([np.zeros(lo, np.uint32), v,
+                                                                   np.zeros(hi, np.uint32)])).cuda()
+    tv = None if tvf is None else tvf[lo:lo + n]
     frac = 1.0
     if entry == "omit":
         gns.sort_omit_(tk, tv, target=target)
@@ -102,7 +109,7 @@ def one():
     torch.cuda.synchronize()
     ok = np.array_equal(tk.cpu().numpy().view(np.uint64), ek.view(np.uint64))
     ok = ok and (v is None or np.array_equal(tv.cpu().numpy(), ev))
-    return ok, (entry, kt, n, target, payload, frac)
+    return ok, (entry, kt, n, target, payload, frac, lo)
 
 
 t_end = time.time() + a.seconds
