@@ -11,6 +11,7 @@
 #include "gns_tile64.cuh"
 #include "gns_multipass.cuh"
 #include "gns_peel.cuh"
+#include "gns_small.cuh"
 
 #include <cuda_runtime.h>
 #include <cstdio>
@@ -96,10 +97,13 @@ struct Mode {
 // per-chunk counters of a two-phase reversal (ntiles)
 size_t mp_words(int ntiles) { return 2 + (size_t)ntiles + 64; }
 
+bool small_on();
+
 Layout layout(size_t n, const Mode &m, bool hv)
 {
     Layout L;
     if (n <= (size_t)TILE) return L;   // one tile, sorted in place, no buffer
+    if (n <= (size_t)SMALL_MAX_N && small_on()) return L;   // one cluster, on chip, no buffer
     L.buf_elems = m.limited ? m.buf : n;
     L.ntiles = (int)ceil_div(n, MTILE);
     size_t o = 0;
@@ -164,6 +168,26 @@ TileK tile_kern(bool hv, int o)
 {
     static const TileK t[2][NORD] = {GNS_ORDS(tile_sort2_kernel, false), GNS_ORDS(tile_sort2_kernel, true)};
     return t[hv][o];
+}
+using SmallK = decltype(&small_sort_kernel<false, 0>);
+SmallK small_kern(bool hv, int o)
+{
+    static const SmallK t[2][NORD] = {
+        {&small_sort_kernel<false, 0>, &small_sort_kernel<false, 1>, &small_sort_kernel<false, 2>,
+         &small_sort_kernel<false, 3>, &small_sort_kernel<false, 4>, &small_sort_kernel<false, 5>},
+        {&small_sort_kernel<true, 0>, &small_sort_kernel<true, 1>, &small_sort_kernel<true, 2>,
+         &small_sort_kernel<true, 3>, &small_sort_kernel<true, 4>, &small_sort_kernel<true, 5>}};
+    return t[hv][o];
+}
+// Small arrays (n <= SMALL_MAX_N) on one thread-block cluster (gns_small.cuh)
+// unless GNS_SMALL=0 (A/B).
+bool small_on()
+{
+    static const bool on = [] {
+        const char *e = std::getenv("GNS_SMALL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
 }
 using MHeadK = decltype(&merge_head_kernel<false, 0>);
 MHeadK mhead_kern(bool hv, int o)
@@ -354,6 +378,9 @@ gns_status ensure_attrs()
             if (!hv) GNS_ATTR(tile3_kern(o), T3_SMEM);
             if (!hv && o < 2) GNS_ATTR(tile3f_kern(o), (t3_smem<float, NT3>()));
             GNS_ATTR(multi_kern(hv, o), ts_smem(hv));
+            GNS_ATTR(small_kern(hv, o), sm_smem(hv));
+            GNS_TRY(check(cudaFuncSetAttribute(small_kern(hv, o), cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
+                          "attr"));
         }
     }
 #undef GNS_ATTR
@@ -453,8 +480,8 @@ int launch_kind(const char *what)
                                   "omit_prep_kernel", "omit_final_kernel", "iota_u32_kernel", "gather_u64_kernel",
                                   "f32_tile_sort_kernel", "f32_merge_kernel", "f32_reverse_kernel",
                                   "f32_partition_kernel", "merge_multi_kernel", "peel_head_kernel",
-                                  "peel_merge_kernel"};
-    for (int i = 0; i < 20; ++i)
+                                  "peel_merge_kernel", "small_sort_kernel"};
+    for (int i = 0; i < 21; ++i)
         if (std::strcmp(what, names[i]) == 0) return i + 1;
     return 0;
 }
@@ -968,6 +995,35 @@ gns_status sort_limited(double *keys, uint32_t *vals, size_t lo, size_t len, siz
 // target: 0 AscLeft, 1 AscRight, 2 DescLeft, 3 DescRight (NEXT f3).
 // AscRight = reverse(DescLeft), DescRight = reverse(AscLeft).
 // kt: key type (0 f64, 1 i64, 2 u64; NEXT f3).
+// One cluster of C CTAs (cluster dimension C, non-portable above 8).
+gns_status launch_small(double *keys, uint32_t *vals, size_t n, int ord, int C, cudaStream_t st)
+{
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)C);
+    cfg.blockDim = dim3(SM_NT);
+    cfg.dynamicSmemBytes = sm_smem(vals != nullptr);
+    cfg.stream = st;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)C;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
+    Timing &T = g_timing;
+    const bool timed = T.on && T.used + 2 <= T.cap;
+    if (timed && T.used == 0) cudaEventRecord(T.ev[T.used++], st);
+    const gns_status r = check(cudaLaunchKernelEx(&cfg, small_kern(vals != nullptr, ord), keys, vals, (long long)n),
+                               "small_sort_kernel");
+    if (timed && r == GNS_OK) {
+        T.kind[T.used - 1] = launch_kind("small_sort_kernel");
+        cudaEventRecord(T.ev[T.used++], st);
+    }
+    return r;
+}
+
 gns_status run_sort_aligned(double *keys, uint32_t *vals, size_t n, const Mode &m, unsigned char *ws, int target, int kt,
                     cudaStream_t st, bool reverse_right = true)
 {
@@ -976,7 +1032,12 @@ gns_status run_sort_aligned(double *keys, uint32_t *vals, size_t n, const Mode &
     const bool hv = vals != nullptr;
     const bool right = target == 1 || target == 3;
     const int ord = ord_of((target == 2) || (target == 1), kt);   // AscRight is reverse(DescLeft)
-    if (n <= (size_t)TILE) {   // one tile: in place, no buffer
+    if (small_on() && n <= (size_t)SMALL_MAX_N) {
+        // on one thread-block cluster, no buffer (gns_small.cuh)
+        int C = 1;
+        while ((size_t)C * SM_TILE < n) C <<= 1;
+        GNS_TRY(launch_small(keys, vals, n, ord, C, st));
+    } else if (n <= (size_t)TILE) {   // one tile: in place, no buffer
         GNS_TRY(launch_tile_sort(keys, vals, keys, vals, n, ord, st));
     } else {
         const Layout Lo = layout(n, m, hv);
@@ -1385,6 +1446,10 @@ gns_status gns_plan(size_t n, double buffer_fraction, int with_vals, gns_plan_in
     sc.hv = with_vals != 0;
     if (n <= 1) {
         sc.elem_passes = 0;
+    } else if (n <= (size_t)SMALL_MAX_N && small_on()) {
+        sc.elem_passes = 1;                           // one read + one write, every level on chip
+        sc.launches = 1;
+        out->merge_passes = 0;
     } else if (n <= (size_t)TILE || !m.limited) {
         count_sort_range(n, &sc, n);
     } else {

@@ -62,8 +62,14 @@ def test_geometry_and_plan(gns):
     assert p["bytes_lower_bound"] == p["hbm_passes"] * 2 * (1 << 27) * 12
     p = gns.plan(T, 0.5, True)
     assert p["workspace_bytes"] == 0 and p["hbm_passes"] == 1
-    p = gns.plan(T + 1, 1.0, False)
-    assert p["merge_passes"] == 1
+    # up to 16 x 4096 keys: one thread-block cluster sorts on chip (no buffer,
+    # one read + one write, no merge pass)
+    small = 16 * 4096
+    for n in (T + 1, small):
+        p = gns.plan(n, 1.0, True)
+        assert p["merge_passes"] == 0 and p["hbm_passes"] == 1 and p["workspace_bytes"] == 0
+    p = gns.plan(small + 1, 1.0, False)
+    assert p["merge_passes"] == passes(small + 1) and p["workspace_bytes"] > 0
     assert gns.plan(0, 1.0, False)["hbm_passes"] == 0
 
 

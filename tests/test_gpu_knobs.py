@@ -2,7 +2,7 @@
 so each runs in a subprocess): GNS_MULTI=1 (all merge levels in one
 persistent launch), GNS_CHAIN=1 (chained passes on region counters),
 GNS_K1=2 (the 256 x 32 key-only tile sort), GNS_MERGE_MODE=1 (ticket passes
-for every size).  Each sorts a few seeded inputs through the C-ABI and
+for every size), GNS_SMALL=0 (tile sort + merge passes for n <= 65536).  Each sorts a few seeded inputs through the C-ABI and
 compares bit-exactly with the oracle."""
 import os
 import subprocess
@@ -18,7 +18,8 @@ import sys, numpy as np, torch
 sys.path.insert(0, ROOT_DIR)
 import oracle, synth, paper_2402_01816_b200 as gns
 bad = 0
-for n, seed, pay in ((3 * 8192 + 77, 1, True), (1 << 20, 2, False), ((1 << 21) + 5, 3, True), (40000, 4, False)):
+for n, seed, pay in ((3 * 8192 + 77, 1, True), (1 << 20, 2, False), ((1 << 21) + 5, 3, True), (40000, 4, False),
+                     (65536, 5, True), (9000, 6, False)):
     k = synth.ties(n, seed, 1000) if seed % 2 else synth.uniform(n, seed)
     v = synth.iota_u32(n) if pay else None
     ek, ev = oracle.sort(k, v)
@@ -45,7 +46,7 @@ sys.exit(1 if bad else 0)
 """
 
 
-@pytest.mark.parametrize("env", [{"GNS_MULTI": "1"}, {"GNS_CHAIN": "1"}, {"GNS_K1": "2"}, {"GNS_MERGE_MODE": "1"},
+@pytest.mark.parametrize("env", [{"GNS_MULTI": "1"}, {"GNS_CHAIN": "1"}, {"GNS_K1": "2"}, {"GNS_MERGE_MODE": "1"}, {"GNS_SMALL": "0"},
                                  {"GNS_MERGE_MODE": "0"}])
 def test_env_variant_bitexact(env):
     e = dict(os.environ, **env)

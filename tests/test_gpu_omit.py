@@ -159,7 +159,7 @@ def test_omit_uniform_full_size(gns):
 
 def test_omit_errors(gns):
     """Argument errors as gns_sort_keys; the input stays untouched."""
-    k = synth.uniform(3 * T1, 1)
+    k = synth.uniform(9 * T1, 1)              # (above the on-chip small sort: a workspace is needed)
     tk, _ = to_dev(k, None)
     with pytest.raises(Exception):
         gns.sort_omit_(tk, None, target="Sideways")

@@ -264,7 +264,7 @@ def test_baseline_configs_full_size(gns, c, sub):
 
 
 def test_error_paths_leave_data_untouched(gns):
-    n = 3 * gns.gns_tile_elems() + 5          # > one tile, so a workspace is required
+    n = 16 * 4096 + 5                         # > the on-chip small sort, so a workspace is required
     k = synth.uniform(n, 1)
     tk, _ = to_dev(k, None)
     before = tk.clone()

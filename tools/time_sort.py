@@ -20,6 +20,7 @@ ap.add_argument("--reps", type=int, default=20)
 ap.add_argument("--tag", default="")
 ap.add_argument("--omit", action="store_true", help="gns_sort_omit (Omitsort schedule)")
 ap.add_argument("--input", default="uniform")
+ap.add_argument("--no-flush", action="store_true", help="keep L2 warm between reps (code + data)")
 a = ap.parse_args()
 n = 1 << a.n
 src = torch.from_numpy(synth.uniform(n, 2000) if a.input == "uniform" else synth.config(4, a.input, n).keys).cuda()
@@ -33,7 +34,8 @@ for i in range(a.reps + 3):
     k.copy_(src)
     if a.pairs:
         v.copy_(srcv)
-    flush.fill_(1)
+    if not a.no_flush:
+        flush.fill_(1)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     if a.omit:
