@@ -304,11 +304,12 @@ F32TileK f32_tile_kern(bool hv, int desc)
                                      {&f32_tile_sort_kernel<true, false>, &f32_tile_sort_kernel<true, true>}};
     return t[hv][desc];
 }
-using F32M2K = decltype(&f32_merge2_kernel<false>);
-F32M2K f32_merge2_kern(int desc)
+using F32M2K = decltype(&f32_merge2_kernel<false, false>);
+F32M2K f32_merge2_kern(bool hv, int desc)
 {
-    static const F32M2K t[2] = {&f32_merge2_kernel<false>, &f32_merge2_kernel<true>};
-    return t[desc];
+    static const F32M2K t[2][2] = {{&f32_merge2_kernel<false, false>, &f32_merge2_kernel<false, true>},
+                                   {&f32_merge2_kernel<true, false>, &f32_merge2_kernel<true, true>}};
+    return t[hv][desc];
 }
 using F32PartK = decltype(&f32_partition_kernel<false>);
 F32PartK f32_part_kern(int desc)
@@ -371,7 +372,7 @@ gns_status ensure_attrs()
             GNS_ATTR(merge_kern_ol(hv, o), ts_smem(hv));
             if (o < 2) GNS_ATTR(f32_tile_kern(hv, o), f_tile_smem(hv));
             if (o < 2) GNS_ATTR(f32_merge_kern(hv, o), f_merge_smem(hv));
-            if (o < 2 && !hv) GNS_ATTR(f32_merge2_kern(o), f2_smem());
+            if (o < 2) GNS_ATTR(f32_merge2_kern(hv, o), f2_smem(hv));
             if (!hv) GNS_ATTR(omit_plan_kern(o), OMIT_SMEM);
             GNS_ATTR(inplace_kern(hv, o), ts_smem(hv));
             GNS_ATTR(tile_kern(hv, o), t1_smem(hv));
@@ -1384,18 +1385,18 @@ gns_status gns_sort_f32(float *keys, uint32_t *vals, size_t n, gns_target target
                      f_tile_smem(hv), st, (const float *)keys, (const uint32_t *)vals, ck, cv, (long long)n);
     int *corank = reinterpret_cast<int *>(w + (hv ? 2 : 1) * align_up(n * sizeof(float), 256));
     const int ntiles = (int)ceil_div(n, F_MTILE);
-    for (int p = 0; p < M && r == GNS_OK && !hv && k1_v3(); ++p) {
-        // key-only: the pipelined pass with in-kernel co-rank searches
+    for (int p = 0; p < M && r == GNS_OK && k1_v3(); ++p) {
+        // the pipelined pass with in-kernel co-rank searches (with payload: 2 CTAs per SM)
         const long long L = (long long)F_TILE << p;
         const int nt2 = (int)ceil_div(n, F2_MT);
-        const int ctas = std::min(nt2, 3 * num_sms());
+        const int ctas = std::min(nt2, (hv ? 2 : 3) * num_sms());
         const int per = (int)ceil_div(nt2, ctas);
-        r = launch_pdl("f32_merge_kernel", f32_merge2_kern(desc), (unsigned)ceil_div(nt2, per), F2_THREADS,
-                       f2_smem(), st, (const float *)ck, ok, (long long)n, L, nt2, per);
+        r = launch_pdl("f32_merge_kernel", f32_merge2_kern(hv, desc), (unsigned)ceil_div(nt2, per), F2_THREADS,
+                       f2_smem(hv), st, (const float *)ck, (const uint32_t *)cv, ok, ov, (long long)n, L, nt2, per);
         std::swap(ck, ok);
         std::swap(cv, ov);
     }
-    for (int p = 0; p < M && r == GNS_OK && (hv || !k1_v3()); ++p) {
+    for (int p = 0; p < M && r == GNS_OK && !k1_v3(); ++p) {
         const long long L = (long long)F_TILE << p;
         r = launch_pdl("f32_partition_kernel", f32_part_kern(desc), (unsigned)ceil_div((size_t)ntiles * 32, 256), 256,
                        0, st, (const float *)ck, (long long)n, L, ntiles, corank);

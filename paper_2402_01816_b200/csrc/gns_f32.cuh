@@ -320,7 +320,7 @@ constexpr int F2_VT = 16;                            // outputs per merge thread
 constexpr int F2_MT = F_NT * F2_VT;                  // 4096 outputs per tile (8192: 47 vs 41 us per 2^24-key level)
 static_assert(F_TILE % F2_MT == 0, "pair boundaries on tile boundaries");
 constexpr int F2_SLOTS = F2_MT + 16;                 // A (+ <= 6 alignment slots), then B (+ <= 6)
-constexpr size_t f2_smem() { return (size_t)F2_NS * F2_SLOTS * 4 + 16; }
+constexpr size_t f2_smem(bool hv = false) { return (size_t)F2_NS * F2_SLOTS * 4 * (hv ? 2 : 1) + 16; }
 
 struct F2Meta {
     int t, ca, cb, oa, ob;    // tile, slice lengths, slots of A[0] / B[0] in the stage
@@ -342,13 +342,17 @@ __device__ __forceinline__ int f2_corank(const float *src, long long n, long lon
                                      [&](int m) { return !fbefore<DESC>(B[d - 1 - m], A[m]); });
 }
 
-template <bool DESC>
-__global__ void __launch_bounds__(F2_THREADS, 3)
-f32_merge2_kernel(const float *src, float *dst, long long n, long long L, int ntiles, int per_cta)
+// HV: u32 payload staged at the same slots as its key (vals stage after the
+// key stages), carried through the merge, stored with 16-byte stores.
+template <bool HV, bool DESC>
+__global__ void __launch_bounds__(F2_THREADS, HV ? 2 : 3)
+f32_merge2_kernel(const float *src, const uint32_t *srcv, float *dst, uint32_t *dstv, long long n, long long L,
+                  int ntiles, int per_cta)
 {
     pdl_wait();
     extern __shared__ __align__(16) unsigned char f2_smem_raw[];
     float *stage = reinterpret_cast<float *>(f2_smem_raw);
+    uint32_t *vstage = reinterpret_cast<uint32_t *>(stage + F2_NS * F2_SLOTS);
     __shared__ __align__(8) uint64_t full[F2_NS];
     __shared__ __align__(8) uint64_t freed[F2_NS];
     __shared__ F2Meta meta[F2_NS];
@@ -433,12 +437,25 @@ f32_merge2_kernel(const float *src, float *dst, long long n, long long L, int nt
             const int ob = rb + (int)(gb - sb0);
             float *S = stage + st * F2_SLOTS;
             GNS_DASSERT(oa + ca <= rb && sa1 - sa0 <= rb && ob + cb + 1 <= F2_SLOTS && rb + (sb1 - sb0) <= F2_SLOTS);
-            mbar_expect_tx(&full[st], (uint32_t)((sa1 - sa0) + (sb1 - sb0)) * 4u);
-            if (sa1 > sa0) tma_load_1d(S, src + sa0, (uint32_t)(sa1 - sa0) * 4u, &full[st], pol);
-            if (sb1 > sb0) tma_load_1d(S + rb, src + sb0, (uint32_t)(sb1 - sb0) * 4u, &full[st], pol);
+            uint32_t *V = vstage + st * F2_SLOTS;
+            mbar_expect_tx(&full[st], (uint32_t)((sa1 - sa0) + (sb1 - sb0)) * 4u * (HV ? 2u : 1u));
+            if (sa1 > sa0) {
+                tma_load_1d(S, src + sa0, (uint32_t)(sa1 - sa0) * 4u, &full[st], pol);
+                if (HV) tma_load_1d(V, srcv + sa0, (uint32_t)(sa1 - sa0) * 4u, &full[st], pol);
+            }
+            if (sb1 > sb0) {
+                tma_load_1d(S + rb, src + sb0, (uint32_t)(sb1 - sb0) * 4u, &full[st], pol);
+                if (HV) tma_load_1d(V + rb, srcv + sb0, (uint32_t)(sb1 - sb0) * 4u, &full[st], pol);
+            }
             // the <= 3 keys past the array's last aligned group, by hand
-            for (long long g = max(sa1, ga); g < ga + ca; ++g) S[g - sa0] = src[g];
-            for (long long g = max(sb1, gb); g < gb + cb; ++g) S[rb + (g - sb0)] = src[g];
+            for (long long g = max(sa1, ga); g < ga + ca; ++g) {
+                S[g - sa0] = src[g];
+                if (HV) V[g - sa0] = srcv[g];
+            }
+            for (long long g = max(sb1, gb); g < gb + cb; ++g) {
+                S[rb + (g - sb0)] = src[g];
+                if (HV) V[rb + (g - sb0)] = srcv[g];
+            }
             F2Meta mt;
             mt.t = t;
             mt.ca = ca;
@@ -464,9 +481,11 @@ f32_merge2_kernel(const float *src, float *dst, long long n, long long L, int nt
         const F2Meta mt = meta[st];
         const float *S = stage + st * F2_SLOTS;
         const float *SA = S + mt.oa, *SB = S + mt.ob;
+        const uint32_t *VA = vstage + st * F2_SLOTS + mt.oa, *VB = vstage + st * F2_SLOTS + mt.ob;
         const int cnt = mt.ca + mt.cb;
         const int d = tid * F2_VT;
         float k[F2_VT];
+        uint32_t v[F2_VT];
         if (d < cnt) {
             int lo = max(0, d - mt.cb), hi = min(d, mt.ca);
             while (lo < hi) {
@@ -480,6 +499,7 @@ f32_merge2_kernel(const float *src, float *dst, long long n, long long L, int nt
             for (int x = 0; x < F2_VT; ++x) {
                 const bool p = (bj < mt.cb) && ((ai >= mt.ca) || fbefore<DESC>(kb, ka));
                 k[x] = p ? kb : ka;
+                if (HV) v[x] = p ? VB[bj] : VA[ai];
                 if (p) kb = SB[++bj];
                 else ka = SA[++ai];
             }
@@ -492,10 +512,18 @@ f32_merge2_kernel(const float *src, float *dst, long long n, long long L, int nt
                 float4 *ok = reinterpret_cast<float4 *>(dst + o);
 #pragma unroll
                 for (int c = 0; c < F2_VT / 4; ++c) ok[c] = make_float4(k[4 * c], k[4 * c + 1], k[4 * c + 2], k[4 * c + 3]);
+                if (HV) {
+                    uint4 *ov = reinterpret_cast<uint4 *>(dstv + o);
+#pragma unroll
+                    for (int c = 0; c < F2_VT / 4; ++c) ov[c] = make_uint4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+                }
             } else {
 #pragma unroll
                 for (int x = 0; x < F2_VT; ++x)
-                    if (d + x < cnt) dst[o + x] = k[x];
+                    if (d + x < cnt) {
+                        dst[o + x] = k[x];
+                        if (HV) dstv[o + x] = v[x];
+                    }
             }
         }
     }
