@@ -51,14 +51,38 @@ gns_status check(cudaError_t e, const char *where)
 inline size_t ceil_div(size_t a, size_t b) { return (a + b - 1) / b; }
 inline size_t align_up(size_t a, size_t b) { return ceil_div(a, b) * b; }
 
-int merge_passes_for(size_t n)
+int merge_passes_for(size_t n, size_t run = TILE)
 {
-    if (n <= (size_t)TILE) return 0;
-    size_t runs = ceil_div(n, TILE);
+    if (n <= run) return 0;
+    size_t runs = ceil_div(n, run);
     int p = 0;
     while (((size_t)1 << p) < runs) ++p;
     return p;
 }
+
+bool k1_v3();
+bool multi_on();
+bool chain_on();
+// K1 cluster size C (key-only, 8-byte keys): the tile sort merges the C tiles
+// of a thread-block cluster on chip (cluster_levels, gns_tile64.cuh), so the
+// merge passes start at runs of C x TILE keys.  GNS_K1_CL = 1, 2, 4, 8, 16;
+// default 1: measured slower at every C (2^24 keys 0.80 / 0.83 / 0.87 / 0.96
+// / 1.09 ms for C = 1 / 2 / 4 / 8 / 16, DESIGN.md 8b -- a distributed
+// shared memory merge level costs more than the HBM pass it saves).  1 for
+// pairs, the A/B kernels and arrays of at most one tile.
+int k1_cluster(size_t len, bool hv)
+{
+    static const int cl = [] {
+        const char *e = std::getenv("GNS_K1_CL");
+        const int v = e ? std::atoi(e) : 1;
+        return (v == 1 || v == 2 || v == 4 || v == 8 || v == 16) ? v : 1;
+    }();
+    if (hv || !k1_v3() || multi_on() || chain_on() || len <= (size_t)TILE) return 1;
+    int c = 1;
+    while (c < cl && (size_t)c * TILE < len) c <<= 1;
+    return c;
+}
+size_t k1_run(size_t len, bool hv) { return (size_t)TILE * k1_cluster(len, hv); }
 
 // 0.5 mode split: the left (larger) half goes to the buffer.  Rounded up to 32
 // elements so that data + nl stays 256-byte (keys) / 128-byte (vals) aligned.
@@ -261,6 +285,14 @@ Tile3K tile3_kern(int o)
     return t[o];
 }
 using Tile3FK = decltype(&tile_sort3_kernel<float, 0>);
+Tile3K tile3c_kern(int o)
+{
+    static const Tile3K t[NORD] = {
+        &tile_sort3_kernel<double, 0, NT3, true>, &tile_sort3_kernel<double, 1, NT3, true>,
+        &tile_sort3_kernel<double, 2, NT3, true>, &tile_sort3_kernel<double, 3, NT3, true>,
+        &tile_sort3_kernel<double, 4, NT3, true>, &tile_sort3_kernel<double, 5, NT3, true>};
+    return t[o];
+}
 Tile3FK tile3f_kern(int desc)
 {
     static const Tile3FK t[2] = {&tile_sort3_kernel<float, 0>, &tile_sort3_kernel<float, 1>};
@@ -377,6 +409,11 @@ gns_status ensure_attrs()
             GNS_ATTR(inplace_kern(hv, o), ts_smem(hv));
             GNS_ATTR(tile_kern(hv, o), t1_smem(hv));
             if (!hv) GNS_ATTR(tile3_kern(o), T3_SMEM);
+            if (!hv) {
+                GNS_ATTR(tile3c_kern(o), T3_SMEM);
+                GNS_TRY(check(cudaFuncSetAttribute(tile3c_kern(o), cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
+                              "cudaFuncSetAttribute"));
+            }
             if (!hv && o < 2) GNS_ATTR(tile3f_kern(o), (t3_smem<float, NT3>()));
             GNS_ATTR(multi_kern(hv, o), ts_smem(hv));
             GNS_ATTR(small_kern(hv, o), sm_smem(hv));
@@ -527,11 +564,40 @@ gns_status launch_pdl(const char *what, void (*kern)(KArgs...), dim3 grid, dim3 
 // Row a2 (K1).
 gns_status launch_tile_sort(const double *sk, const uint32_t *sv, double *dk, uint32_t *dv, size_t n, int ord,
                             cudaStream_t st, unsigned *unsorted = nullptr, double *smp = nullptr,
-                            unsigned char *tdesc = nullptr, double *smp_src = nullptr)
+                            unsigned char *tdesc = nullptr, double *smp_src = nullptr, int cl = 1)
 {
     if (n == 0) return GNS_OK;
     const unsigned grid = (unsigned)ceil_div(n, TILE);
     const bool hv = sv != nullptr;
+    if (!hv && k1_v3() && cl > 1) {
+        // thread-block clusters of cl CTAs (the grid padded to whole clusters;
+        // CTAs past the array hold pads only)
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)align_up(grid, (size_t)cl));
+        cfg.blockDim = dim3(NT3);
+        cfg.dynamicSmemBytes = T3_SMEM;
+        cfg.stream = st;
+        cudaLaunchAttribute at[2];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = (unsigned)cl;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[1].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = pdl_enabled() ? 2 : 1;
+        Timing &T = g_timing;
+        const bool timed = T.on && T.used + 2 <= T.cap;
+        if (timed && T.used == 0) cudaEventRecord(T.ev[T.used++], st);
+        const gns_status r = check(cudaLaunchKernelEx(&cfg, tile3c_kern(ord), sk, dk, (long long)n, unsorted, smp,
+                                                      (unsigned char *)nullptr, (double *)nullptr),
+                                   "tile_sort2_kernel");
+        if (timed && r == GNS_OK) {
+            T.kind[T.used - 1] = launch_kind("tile_sort2_kernel");
+            cudaEventRecord(T.ev[T.used++], st);
+        }
+        return r;
+    }
     if (!hv && k1_v3())
         return launch_pdl("tile_sort2_kernel", tile3_kern(ord), grid, NT3, T3_SMEM, st, sk, dk, (long long)n, unsorted,
                           smp, tdesc, smp_src);
@@ -696,7 +762,9 @@ gns_status sort_range(double *rk, uint32_t *rv, double *pk_, uint32_t *pv_, size
                       double *smp_r = nullptr, double *smp_p = nullptr, unsigned *mpw = nullptr)
 {
     if (len == 0) return GNS_OK;
-    const int M = merge_passes_for(len);
+    const int cl = k1_cluster(len, rv != nullptr);
+    const size_t R = (size_t)TILE * cl;                 // run length after K1
+    const int M = merge_passes_for(len, R);
     const bool tile_to_partner = final_in_partner ^ (bool)(M & 1);
     double *ck = tile_to_partner ? pk_ : rk;
     uint32_t *cv = tile_to_partner ? pv_ : rv;
@@ -724,13 +792,15 @@ gns_status sort_range(double *rk, uint32_t *rv, double *pk_, uint32_t *pv_, size
     else if (unsorted && M > 0) GNS_TRY(check(cudaMemsetAsync(unsorted, 0, sizeof(unsigned), st), "memset"));
     unsigned *cnt_prev = nullptr;
     unsigned *cnt_next = chain ? mpw + 2 : nullptr;
-    GNS_TRY(launch_tile_sort(rk, rv, ck, cv, len, ord, st, M > 0 ? unsorted : nullptr, M > 0 ? cs : nullptr));
+    GNS_TRY(launch_tile_sort(rk, rv, ck, cv, len, ord, st, M > 0 ? unsorted : nullptr, M > 0 ? cs : nullptr,
+                             nullptr, nullptr, cl));
     for (int p = 0; p < M; ++p) {
-        const size_t L = (size_t)TILE << p;
+        const size_t L = R << p;
         MergeGeo g = uniform_geo(ck, cv, ok, ov, len, L, cs, p + 1 < M ? os : nullptr);
         const bool last = p == M - 1;
         Adapt ad{};
         ad.flag = unsorted;
+        ad.run_log2 = TILE_LOG2 + __builtin_ctz((unsigned)cl);
         if (unsorted) {
             // ordered input: the tile sort's output must end where the sort ends
             if (last && tile_k != ok) {
@@ -941,7 +1011,7 @@ struct Sched {
 void count_sort_range(size_t len, Sched *sc, size_t n)
 {
     if (!len) return;
-    const int M = merge_passes_for(len);
+    const int M = merge_passes_for(len, k1_run(len, sc->hv));
     sc->elem_passes += (double)(1 + M) * (double)len / (double)n;
     // tile sort + per pass one fused launch, or partition + ticket merge
     sc->launches += 1 + M * (ticket_pass(sc->hv, (int)ceil_div(len, MTILE)) ? 2 : 1);
@@ -1442,7 +1512,7 @@ gns_status gns_plan(size_t n, double buffer_fraction, int with_vals, gns_plan_in
     std::memset(out, 0, sizeof(*out));
     out->tile = TILE;
     out->merge_tile = MTILE;
-    out->merge_passes = merge_passes_for(n);
+    out->merge_passes = merge_passes_for(n, k1_run(n, with_vals != 0));
     Sched sc;
     sc.hv = with_vals != 0;
     if (n <= 1) {

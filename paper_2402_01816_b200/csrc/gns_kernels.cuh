@@ -783,6 +783,7 @@ struct Adapt {
     const double *rev_k;          // strictly reversed input: source, or nullptr
     const uint32_t *rev_v;
     int rev_gather;               // 1: out[j] = tile-sorted src at 2tT + c_t - n + j; 0: plain copy
+    int run_log2 = TILE_LOG2;     // log2 T: the tile sort's run length (TILE, or a K1 cluster's C x TILE)
 };
 
 // The CTA's share of the output [lo, hi).  gather: the stable sort of a
@@ -790,7 +791,8 @@ struct Adapt {
 // sorted (= reversed), so out[j] = src[2tT + c_t - n + j] with
 // t = (n-1-j) / T and c_t = min(T, n - tT) (contiguous within each tile).
 template <bool HV>
-__device__ void adapt_move(const MergeGeo &g, int per_cta, const double *sk, const uint32_t *sv, bool gather)
+__device__ void adapt_move(const MergeGeo &g, int per_cta, const double *sk, const uint32_t *sv, bool gather,
+                           int rl)
 {
     const long long n = g.n;
     const long long lo = (long long)blockIdx.x * per_cta * MTILE;
@@ -798,9 +800,9 @@ __device__ void adapt_move(const MergeGeo &g, int per_cta, const double *sk, con
     for (long long j = lo + threadIdx.x; j < hi; j += blockDim.x) {
         long long s = j;
         if (gather) {
-            const long long t = (n - 1 - j) >> TILE_LOG2;
-            const long long c = min((long long)TILE, n - (t << TILE_LOG2));
-            s = 2 * (t << TILE_LOG2) + c - n + j;
+            const long long t = (n - 1 - j) >> rl;
+            const long long c = min(1LL << rl, n - (t << rl));
+            s = 2 * (t << rl) + c - n + j;
         }
         g.ok[j] = sk[s];
         if (HV) g.ov[j] = sv[s];
@@ -947,7 +949,7 @@ merge_tstore_kernel(PipeGeo pg, int ntiles, int per_cta, const __grid_constant__
         const double *ck = pre ? ad.pre_k : ad.rev_k;
         const uint32_t *cv = pre ? ad.pre_v : ad.rev_v;
         if (chained) pdl_wait();          // (the moves read the previous pass's moves: full completion)
-        if (ck) adapt_move<HV>(pg.g, per_cta, ck, cv, !pre && ad.rev_gather);
+        if (ck) adapt_move<HV>(pg.g, per_cta, ck, cv, !pre && ad.rev_gather, ad.run_log2);
         pdl_trigger();
         return;
     }
@@ -1447,7 +1449,7 @@ merge_inplace_kernel(PipeGeo pg, int ntiles, const int *__restrict__ corank, con
             const double *ck = pre ? ad.pre_k : ad.rev_k;
             const uint32_t *cv = pre ? ad.pre_v : ad.rev_v;
             const int per = (ntiles + gridDim.x - 1) / gridDim.x;
-            if (ck) adapt_move<HV>(pg.g, per, ck, cv, !pre && ad.rev_gather);
+            if (ck) adapt_move<HV>(pg.g, per, ck, cv, !pre && ad.rev_gather, ad.run_log2);
             pdl_trigger();
             return;
         }

@@ -352,11 +352,136 @@ __device__ __forceinline__ void bulk_store_1d(void *gdst, const void *ssrc, uint
                  :: "l"(gdst), "r"(smem_u32(ssrc)), "r"(bytes) : "memory");
 }
 
+// ---- distributed shared memory (thread-block cluster) access
+__device__ __forceinline__ uint32_t cl_rank()
+{
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint32_t cl_size()
+{
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cl_sync()
+{
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// shared::cta address a of this CTA -> the same offset in cluster CTA `rank`
+__device__ __forceinline__ uint32_t cl_map(uint32_t a, uint32_t rank)
+{
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+    return r;
+}
+template <typename K>
+__device__ __forceinline__ void sts_k(uint32_t a, K v)
+{
+    if constexpr (sizeof(K) == 8) asm volatile("st.shared.f64 [%0], %1;" :: "r"(a), "d"(v) : "memory");
+    else asm volatile("st.shared.f32 [%0], %1;" :: "r"(a), "f"(v) : "memory");
+}
+template <typename K>
+__device__ __forceinline__ K ldc_k(uint32_t a)
+{
+    if constexpr (sizeof(K) == 8) {
+        double v;
+        asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(a) : "memory");
+        return v;
+    } else {
+        float v;
+        asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(a) : "memory");
+        return v;
+    }
+}
+
+// Cluster extension of K1 (CLU): the C CTAs of a thread-block cluster hold
+// their sorted tiles in shared memory (linear sw3 layout at sbase, identical
+// addresses in every CTA) and merge them on chip into one run of C x TL keys
+// in log2(C) levels: at level G (groups of G CTAs, runs of G/2 tiles), CTA c
+// produces outputs [(c - g0) TL, +TL) of its group's pair (A = the first G/2
+// tiles, B = the rest): warps 0 / 1 find the co-ranks of its first and
+// one-past-last output by 33-ary searches over the remote keys (left run
+// wins ties), every thread loads 64 of the TL inputs A[i0:i1),
+// B[j0:j1) from the remote CTAs into registers, a cluster barrier ends the
+// remote reads, the inputs go to the CTA's own shared memory and one
+// merge-path round (merge_path3x2 + serial_merge3) merges them.  Pads (the
+// order's largest key) of a ragged or empty last tile stay behind every real
+// key.  No HBM traffic; the merge passes that follow start at C x TL keys.
+template <typename K, int ORD, int NT3>
+__device__ __forceinline__ void cluster_levels(uint32_t sbase, int tid, K (&k)[VT3])
+{
+    constexpr int TL = NT3 * VT3;
+    constexpr int PER = 16 / (int)sizeof(K);
+    constexpr uint32_t SZ = sizeof(K);
+    __shared__ int s_co[2];
+    const int C = (int)cl_size(), c = (int)cl_rank();
+    const int e0 = tid * VT3;
+    const int warp = tid >> 5, lane = tid & 31;
+#pragma unroll 1
+    for (int G = 2; G <= C; G <<= 1) {
+        __syncthreads();                              // (the previous merge's reads of the staging are done)
+#pragma unroll
+        for (int q = 0; q < VT3 / PER; ++q) sts16_k<K>(sw3<K>(sbase + SZ * (e0 + PER * q)), &k[PER * q]);
+        cl_sync();                                    // every CTA's run is in its shared memory
+        const int g0 = c & ~(G - 1), half = G >> 1;
+        const int run = half * TL;
+        const int d0 = (c - g0) * TL;
+        auto A = [&](int m) -> K {
+            return ldc_k<K>(cl_map(sw3<K>(sbase + SZ * (uint32_t)(m & (TL - 1))), (uint32_t)(g0 + m / TL)));
+        };
+        auto B = [&](int m) -> K {
+            return ldc_k<K>(cl_map(sw3<K>(sbase + SZ * (uint32_t)(m & (TL - 1))), (uint32_t)(g0 + half + m / TL)));
+        };
+        if (warp < 2) {
+            const int d = d0 + warp * TL;
+            const int lo = max(0, d - run), hi = min(d, run);
+            int r = lo;
+            if (lo < hi)
+                r = lo + group_count_true<32>(lo, hi - 1, lane, 0xFFFFFFFFu, 0,
+                                              [&](int m) { return !kbef<K, ORD>(B(d - 1 - m), A(m)); });
+            if (lane == 0) s_co[warp] = r;
+        }
+        __syncthreads();
+        const int i0 = s_co[0], i1 = s_co[1];
+        const int j0 = d0 - i0;
+        const int ca = i1 - i0, cb = TL - ca;
+        // the TL inputs [A slice, B slice]: element e = x NT3 + tid (consecutive
+        // lanes, consecutive remote slots), all loads issued before any use
+#pragma unroll
+        for (int x = 0; x < VT3; ++x) {
+            const int e = x * NT3 + tid;
+            const bool fa = e < ca;
+            const int m = fa ? i0 + e : j0 + (e - ca);
+            const int r = (fa ? g0 : g0 + half) + m / TL;
+            k[x] = ldc_k<K>(cl_map(sw3<K>(sbase + SZ * (uint32_t)(m & (TL - 1))), (uint32_t)r));
+        }
+        cl_sync();                                    // every remote read of this level is done
+#pragma unroll
+        for (int x = 0; x < VT3; ++x) {
+            const int e = x * NT3 + tid;
+            sts_k<K>(sw3<K>(sbase + SZ * e), k[x]);
+        }
+        __syncthreads();
+        int i, inext;
+        merge_path3x2<K, ORD>(sbase, 0, ca, ca, cb, e0, (lane == 31 && tid + 1 < NT3), i, inext);
+        const int up = __shfl_down_sync(0xFFFFFFFFu, i, 1);
+        if (lane != 31) inext = up;
+        if (tid + 1 == NT3) inext = ca;
+        const int dn = e0 + VT3;
+        serial_merge3<K, ORD>(sbase, 0, i, ca, ca + e0 - i, TL, inext, ca + dn - inext, k);
+    }
+    __syncthreads();                                  // (the caller reuses the shared memory)
+}
+
 // K1 key-only.  Same contract as tile_sort2_kernel<false, ORD> (flags,
 // samples, Omitsort tile descriptors; the tensor maps are unused).  K = double
 // (every 8-byte key type, ORD = DESC | key type << 1) or float (NEXT f3
 // binary32 keys, ORD = DESC; flags / samples / descriptors unused).
-template <typename K, int ORD, int NT3 = gns::NT3>
+// CLU: launched in thread-block clusters of C CTAs, the output runs are
+// C x TL keys (cluster_levels); no Omitsort descriptors (tdesc == nullptr).
+template <typename K, int ORD, int NT3 = gns::NT3, bool CLU = false>
 __global__ void __launch_bounds__(NT3, NT3 == 128 ? (sizeof(K) == 4 ? 4 : 3) : 1)
 tile_sort3_kernel(const K *src_k, K *dst_k, long long n, unsigned *unsorted, K *smp,
                   unsigned char *tdesc, K *smp_src)
@@ -500,7 +625,26 @@ tile_sort3_kernel(const K *src_k, K *dst_k, long long n, unsigned *unsorted, K *
         pdl_trigger();
         return;
     }
-    if (mode == 2) {
+    if (CLU) {
+        const uint32_t sbase = smem_u32(smem) + 256u;
+        if (mode == 2) {
+            // strictly reversed full tile: sorted order = the reversal (thread
+            // t's keys go to the other end), through shared memory
+            __syncthreads();
+#pragma unroll
+            for (int c = 0; c < VT3 / PER; ++c) {
+                K r[PER];
+#pragma unroll
+                for (int j = 0; j < PER; ++j) r[j] = k[PER * c + PER - 1 - j];
+                sts16_k<K>(sw3<K>(sbase + (uint32_t)SZ * (TL - e0 - PER * (c + 1))), r);
+            }
+            __syncthreads();
+#pragma unroll
+            for (int c = 0; c < VT3 / PER; ++c) lds16_k<K>(sw3<K>(sbase + (uint32_t)SZ * (e0 + PER * c)), &k[PER * c]);
+        }
+        cluster_levels<K, ORD, NT3>(sbase, tid, k);
+    }
+    if (!CLU && mode == 2) {
         // full tile, strictly reversed: output TL-1-e <- input e; thread t
         // fills segment 127-t backwards and stores it
         const int ot = NT3 - 1 - tid;
@@ -524,7 +668,7 @@ tile_sort3_kernel(const K *src_k, K *dst_k, long long n, unsigned *unsorted, K *
     }
     if (smp != nullptr && e0 < cnt && (tid & (SMP_G / VT3 - 1)) == 0)
         smp[(base + e0) >> SMP_LOG2] = k[0];
-    if (mode == 1 && dst_k == src_k) {
+    if (!CLU && mode == 1 && dst_k == src_k) {
         GNS_TL_END(0);
         pdl_trigger();
         return;

@@ -1,8 +1,10 @@
 """The A/B code paths selected by environment knobs (read once per process,
 so each runs in a subprocess): GNS_MULTI=1 (all merge levels in one
 persistent launch), GNS_CHAIN=1 (chained passes on region counters),
-GNS_K1=2 (the 256 x 32 key-only tile sort), GNS_MERGE_MODE=1 (ticket passes
-for every size), GNS_SMALL=0 (tile sort + merge passes for n <= 65536).  Each sorts a few seeded inputs through the C-ABI and
+GNS_K1=2 (the 256 x 32 key-only tile sort), GNS_K1_CL=8 / 16 (the key-only
+tile sort merging a thread-block cluster's tiles on chip), GNS_MERGE_MODE=1
+(ticket passes for every size), GNS_SMALL=0 (tile sort + merge passes for
+n <= 65536).  Each sorts a few seeded inputs through the C-ABI and
 compares bit-exactly with the oracle."""
 import os
 import subprocess
@@ -34,7 +36,8 @@ for n, seed, pay in ((3 * 8192 + 77, 1, True), (1 << 20, 2, False), ((1 << 21) +
             bad += 1
             print("FAIL", n, frac, pay)
 # ordered / strictly reversed inputs (the adaptive shortcuts inside the variant)
-for k in (np.arange(3 * 8192 + 5, dtype=np.float64), np.arange(5 * 8192, 0, -1).astype(np.float64)):
+for k in (np.arange(3 * 8192 + 5, dtype=np.float64), np.arange(5 * 8192, 0, -1).astype(np.float64),
+          np.arange(20 * 8192, 0, -1).astype(np.float64), np.arange(37 * 8192 + 11, dtype=np.float64)):
     tk = torch.from_numpy(k.copy()).cuda()
     gns.sort_(tk, None, 1.0)
     torch.cuda.synchronize()
@@ -47,7 +50,7 @@ sys.exit(1 if bad else 0)
 
 
 @pytest.mark.parametrize("env", [{"GNS_MULTI": "1"}, {"GNS_CHAIN": "1"}, {"GNS_K1": "2"}, {"GNS_MERGE_MODE": "1"}, {"GNS_SMALL": "0"},
-                                 {"GNS_MERGE_MODE": "0"}])
+                                 {"GNS_MERGE_MODE": "0"}, {"GNS_K1_CL": "8"}, {"GNS_K1_CL": "16"}])
 def test_env_variant_bitexact(env):
     e = dict(os.environ, **env)
     r = subprocess.run([sys.executable, "-c", SCRIPT.replace("ROOT_DIR", repr(ROOT))], capture_output=True, text=True, env=e, timeout=600)
