@@ -208,7 +208,8 @@ def gns_timing_end(cap: int = 4096):
 LAUNCH_KINDS = {1: "tile_sort", 2: "merge_pass", 3: "partition", 4: "inplace_deps", 5: "inplace_merge", 6: "reverse",
                 7: "split_cuts", 8: "gather_samples", 9: "omit_plan", 10: "omit_prep", 11: "omit_final",
                 12: "iota", 13: "gather_u64", 14: "f32_tile_sort", 15: "f32_merge", 16: "f32_reverse",
-                17: "f32_partition", 18: "merge_multi", 19: "peel_head", 20: "peel_merge", 21: "small_sort"}
+                17: "f32_partition", 18: "merge_multi", 19: "peel_head", 20: "peel_merge", 21: "small_sort",
+                22: "rank4", 23: "merge4"}
 
 
 def gns_tile_elems() -> int:

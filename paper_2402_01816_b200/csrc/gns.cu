@@ -10,6 +10,7 @@
 #include "gns_f32.cuh"
 #include "gns_tile64.cuh"
 #include "gns_multipass.cuh"
+#include "gns_merge4.cuh"
 #include "gns_peel.cuh"
 #include "gns_small.cuh"
 
@@ -99,6 +100,7 @@ struct Layout {
     size_t buf_elems = 0;   // buffer key(+val) slots
     size_t off_k = 0, off_v = 0, off_corank = 0, off_deps = 0, off_flags = 0, off_adapt = 0, off_smp = 0, total = 0;
     size_t nsmp = 0;        // keys per sample array (two arrays: data-side and buffer-side regions)
+    size_t off_piv = 0;     // 4-way passes: approximate pivot positions + chunk split vectors, or none
     int ntiles = 0;         // merge tiles over the whole array
     // NEXT f2 Omitsort (full buffer only): run state of two levels (location,
     // first and last key), per level and pair the copy flag, per level the
@@ -122,6 +124,7 @@ struct Mode {
 size_t mp_words(int ntiles) { return 2 + (size_t)ntiles + 64; }
 
 bool small_on();
+bool four_on();
 
 Layout layout(size_t n, const Mode &m, bool hv)
 {
@@ -144,9 +147,17 @@ Layout layout(size_t n, const Mode &m, bool hv)
     L.off_adapt = o;                   // the "input not presorted" word (NEXT f2); full buffer: + the
                                        // multi-pass ticket and completion counters (mp_words)
     o = align_up(o + (m.limited ? 1 : mp_words(L.ntiles)) * sizeof(unsigned), 256);
-    L.off_smp = o;                     // split-search samples, every SMP_G-th key of each region
-    L.nsmp = n / SMP_G + 2;
+    // split-search samples of each region: every SMP_G-th key, or every FS-th
+    // (fine samples) when 4-way passes run (gns_merge4.cuh)
+    const bool four = !hv && four_on();
+    L.off_smp = o;
+    L.nsmp = n / (four ? FS : SMP_G) + 2;
     o = align_up(o + 2 * L.nsmp * sizeof(double), 256);
+    if (four) {
+        L.off_piv = o;                 // 4-way passes: per fine sample its approximate position, per chunk its split vector
+        o = align_up(o + (ceil_div(n, FS) + 2) * sizeof(int), 256);
+        o = align_up(o + (3 * ceil_div(n, T4) + 8) * sizeof(int4), 256);
+    }
     if (!m.limited) {
         L.nruns = ceil_div(n, TILE);
         L.npairs = ceil_div(n, 2 * (size_t)TILE);
@@ -193,6 +204,27 @@ TileK tile_kern(bool hv, int o)
     static const TileK t[2][NORD] = {GNS_ORDS(tile_sort2_kernel, false), GNS_ORDS(tile_sort2_kernel, true)};
     return t[hv][o];
 }
+using Rank4K = decltype(&rank4_kernel<0>);
+using Merge4K = decltype(&merge4_kernel<0>);
+Rank4K rank4_kern(int o)
+{
+    static const Rank4K t[NORD] = {&rank4_kernel<0>, &rank4_kernel<1>, &rank4_kernel<2>,
+                                   &rank4_kernel<3>, &rank4_kernel<4>, &rank4_kernel<5>};
+    return t[o];
+}
+using Chunk4K = decltype(&chunk4_kernel<0>);
+Chunk4K chunk4_kern(int o)
+{
+    static const Chunk4K t[NORD] = {&chunk4_kernel<0>, &chunk4_kernel<1>, &chunk4_kernel<2>,
+                                    &chunk4_kernel<3>, &chunk4_kernel<4>, &chunk4_kernel<5>};
+    return t[o];
+}
+Merge4K merge4_kern(int o)
+{
+    static const Merge4K t[NORD] = {&merge4_kernel<0>, &merge4_kernel<1>, &merge4_kernel<2>,
+                                    &merge4_kernel<3>, &merge4_kernel<4>, &merge4_kernel<5>};
+    return t[o];
+}
 using SmallK = decltype(&small_sort_kernel<false, 0>);
 SmallK small_kern(bool hv, int o)
 {
@@ -212,6 +244,23 @@ bool small_on()
         return !(e && e[0] == '0');
     }();
     return on;
+}
+// 4-way merge passes (gns_merge4.cuh) for key-only sorts only with GNS_FOUR=1:
+// bit-exact, but measured slower at 2^23 .. 2^27 keys (2^24: 0.92 vs 0.80 ms,
+// the on-chip merge is bound by shared-memory wavefronts, so a
+// 4-way pass costs about two 2-way passes, plus the pivot ranking).
+bool four_on()
+{
+    static const bool on = [] {
+        const char *e = std::getenv("GNS_FOUR");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
+// whether a range of len keys (runs of R after K1) merges by 4-way passes
+bool use_four(bool hv, size_t len, size_t R)
+{
+    return !hv && four_on() && !multi_on() && !chain_on() && merge_passes_for(len, R) >= 2;
 }
 using MHeadK = decltype(&merge_head_kernel<false, 0>);
 MHeadK mhead_kern(bool hv, int o)
@@ -416,6 +465,7 @@ gns_status ensure_attrs()
             }
             if (!hv && o < 2) GNS_ATTR(tile3f_kern(o), (t3_smem<float, NT3>()));
             GNS_ATTR(multi_kern(hv, o), ts_smem(hv));
+            if (!hv) GNS_ATTR(merge4_kern(o), M4_SMEM);
             GNS_ATTR(small_kern(hv, o), sm_smem(hv));
             GNS_TRY(check(cudaFuncSetAttribute(small_kern(hv, o), cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
                           "attr"));
@@ -518,8 +568,8 @@ int launch_kind(const char *what)
                                   "omit_prep_kernel", "omit_final_kernel", "iota_u32_kernel", "gather_u64_kernel",
                                   "f32_tile_sort_kernel", "f32_merge_kernel", "f32_reverse_kernel",
                                   "f32_partition_kernel", "merge_multi_kernel", "peel_head_kernel",
-                                  "peel_merge_kernel", "small_sort_kernel"};
-    for (int i = 0; i < 21; ++i)
+                                  "peel_merge_kernel", "small_sort_kernel", "rank4_kernel", "merge4_kernel", "chunk4_kernel"};
+    for (int i = 0; i < 24; ++i)
         if (std::strcmp(what, names[i]) == 0) return i + 1;
     return 0;
 }
@@ -564,7 +614,8 @@ gns_status launch_pdl(const char *what, void (*kern)(KArgs...), dim3 grid, dim3 
 // Row a2 (K1).
 gns_status launch_tile_sort(const double *sk, const uint32_t *sv, double *dk, uint32_t *dv, size_t n, int ord,
                             cudaStream_t st, unsigned *unsorted = nullptr, double *smp = nullptr,
-                            unsigned char *tdesc = nullptr, double *smp_src = nullptr, int cl = 1)
+                            unsigned char *tdesc = nullptr, double *smp_src = nullptr, int cl = 1,
+                            int smp_log2 = SMP_LOG2)
 {
     if (n == 0) return GNS_OK;
     const unsigned grid = (unsigned)ceil_div(n, TILE);
@@ -590,7 +641,7 @@ gns_status launch_tile_sort(const double *sk, const uint32_t *sv, double *dk, ui
         const bool timed = T.on && T.used + 2 <= T.cap;
         if (timed && T.used == 0) cudaEventRecord(T.ev[T.used++], st);
         const gns_status r = check(cudaLaunchKernelEx(&cfg, tile3c_kern(ord), sk, dk, (long long)n, unsorted, smp,
-                                                      (unsigned char *)nullptr, (double *)nullptr),
+                                                      (unsigned char *)nullptr, (double *)nullptr, smp_log2),
                                    "tile_sort2_kernel");
         if (timed && r == GNS_OK) {
             T.kind[T.used - 1] = launch_kind("tile_sort2_kernel");
@@ -600,7 +651,7 @@ gns_status launch_tile_sort(const double *sk, const uint32_t *sv, double *dk, ui
     }
     if (!hv && k1_v3())
         return launch_pdl("tile_sort2_kernel", tile3_kern(ord), grid, NT3, T3_SMEM, st, sk, dk, (long long)n, unsorted,
-                          smp, tdesc, smp_src);
+                          smp, tdesc, smp_src, smp_log2);
     CUtensorMap m[4];
     std::memset(m, 0, sizeof(m));
     if (n >= (size_t)TILE) {          // full tiles move by TMA tensor copies; a ragged last tile by plain loads
@@ -701,6 +752,34 @@ MergeGeo uniform_geo(const double *sk, const uint32_t *sv, double *dk, uint32_t 
     return g;
 }
 
+// One 4-way merge pass (gns_merge4.cuh): the pivots' split vectors
+// (rank4_kernel), then the persistent merge of the chunks (merge4_kernel).
+gns_status launch_merge4(const double *src, double *dst, size_t n, size_t L, const double *fsmp, double *smp_out,
+                         int so_log2, unsigned char *wsp, int ord, cudaStream_t st, const Adapt &ad)
+{
+    Geo4 g;
+    g.src = src;
+    g.dst = dst;
+    g.n = (long long)n;
+    g.L = (long long)L;
+    g.fsmp = fsmp;
+    g.smp_out = smp_out;
+    g.so_log2 = so_log2;
+    g.apx = reinterpret_cast<int *>(wsp);
+    g.vec = reinterpret_cast<int4 *>(wsp + align_up((ceil_div(n, FS) + 2) * sizeof(int), 256));
+    g.cpg = (long long)ceil_div(4 * L, T4);
+    const size_t ng = ceil_div(n, 4 * L);
+    const size_t last_len = n - (ng - 1) * 4 * L;
+    g.nchunks = (long long)((ng - 1) * (size_t)g.cpg + ceil_div(last_len, T4));
+    const size_t np = ceil_div(n, FS);
+    const unsigned rgrid = (unsigned)std::max<size_t>(1, std::min<size_t>(ceil_div(np, 256), (size_t)num_sms() * 8));
+    GNS_TRY(launch_pdl("rank4_kernel", rank4_kern(ord), rgrid, 256, 0, st, g, ad.flag));
+    GNS_TRY(launch_pdl("chunk4_kernel", chunk4_kern(ord), (unsigned)ceil_div((size_t)g.nchunks * 32, 256), 256, 0, st,
+                       g, ad.flag));
+    const int grid = (int)std::min<long long>(g.nchunks, (long long)GNS_M4_CTAS * num_sms());
+    return launch_pdl("merge4_kernel", merge4_kern(ord), std::max(grid, 1), M4_THREADS, M4_SMEM, st, g, ad);
+}
+
 // Sorts region R = (rk, rv)[0:len) using partner region P of >= len slots as
 // ping-pong buffer (Nocopy-Mergesort).  The result ends in P if
 // `final_in_partner`, else in R.  Parity picks the tile-sort destination so
@@ -726,6 +805,10 @@ gns_status launch_multi(double *xk, uint32_t *xv, double *yk, uint32_t *yv, doub
     G.n = (long long)n;
     G.passes = M;
     G.ntiles = ntiles;
+    {
+        const char *e = std::getenv("GNS_MP_BLK");
+        G.blk = e ? std::atoi(e) : 0;
+    }
     G.flag = words;
     G.ticket = words + 1;
     G.done = words + 2;
@@ -759,13 +842,19 @@ gns_status launch_multi(double *xk, uint32_t *xv, double *yk, uint32_t *yv, doub
 
 gns_status sort_range(double *rk, uint32_t *rv, double *pk_, uint32_t *pv_, size_t len,
                       bool final_in_partner, int *corank, int ord, cudaStream_t st, unsigned *unsorted = nullptr,
-                      double *smp_r = nullptr, double *smp_p = nullptr, unsigned *mpw = nullptr)
+                      double *smp_r = nullptr, double *smp_p = nullptr, unsigned *mpw = nullptr,
+                      unsigned char *piv = nullptr)
 {
     if (len == 0) return GNS_OK;
     const int cl = k1_cluster(len, rv != nullptr);
     const size_t R = (size_t)TILE * cl;                 // run length after K1
     const int M = merge_passes_for(len, R);
-    const bool tile_to_partner = final_in_partner ^ (bool)(M & 1);
+    // 4-way passes (gns_merge4.cuh): two merge levels per HBM pass; an odd
+    // level count starts with one 2-way pass.  P = HBM passes after K1.
+    const bool four = use_four(rv != nullptr, len, R) && piv && smp_r && smp_p && !multi_on() && !chain_on();
+    const int two_first = four ? (M & 1) : M;          // leading 2-way passes
+    const int P = four ? two_first + M / 2 : M;
+    const bool tile_to_partner = final_in_partner ^ (bool)(P & 1);
     double *ck = tile_to_partner ? pk_ : rk;
     uint32_t *cv = tile_to_partner ? pv_ : rv;
     double *ok = tile_to_partner ? rk : pk_;
@@ -792,12 +881,18 @@ gns_status sort_range(double *rk, uint32_t *rv, double *pk_, uint32_t *pv_, size
     else if (unsorted && M > 0) GNS_TRY(check(cudaMemsetAsync(unsorted, 0, sizeof(unsigned), st), "memset"));
     unsigned *cnt_prev = nullptr;
     unsigned *cnt_next = chain ? mpw + 2 : nullptr;
+    // samples of each pass's output for the next pass: fine (every FS-th key) before a 4-way pass
+    auto smp_log2_before = [&](int p) { return (four && p >= two_first) ? FS_LOG2 : SMP_LOG2; };
     GNS_TRY(launch_tile_sort(rk, rv, ck, cv, len, ord, st, M > 0 ? unsorted : nullptr, M > 0 ? cs : nullptr,
-                             nullptr, nullptr, cl));
-    for (int p = 0; p < M; ++p) {
-        const size_t L = R << p;
-        MergeGeo g = uniform_geo(ck, cv, ok, ov, len, L, cs, p + 1 < M ? os : nullptr);
-        const bool last = p == M - 1;
+                             nullptr, nullptr, cl, smp_log2_before(0)));
+    int lvl = 0;                                       // merge levels done
+    for (int p = 0; p < P; ++p) {
+        const size_t L = R << lvl;
+        const bool last = p == P - 1;
+        const bool four_pass = four && p >= two_first;
+        lvl += four_pass ? 2 : 1;
+        MergeGeo g = uniform_geo(ck, cv, ok, ov, len, L, cs, last ? nullptr : os);
+        g.so_log2 = smp_log2_before(p + 1);
         Adapt ad{};
         ad.flag = unsorted;
         ad.run_log2 = TILE_LOG2 + __builtin_ctz((unsigned)cl);
@@ -815,7 +910,7 @@ gns_status sort_range(double *rk, uint32_t *rv, double *pk_, uint32_t *pv_, size
                 ad.rev_k = tile_k;
                 ad.rev_v = tile_v;
                 ad.rev_gather = 1;
-            } else if (tile_final && p == M - 2) {
+            } else if (tile_final && p == P - 2) {
                 ad.rev_k = tile_k;
                 ad.rev_v = tile_v;
                 ad.rev_gather = 1;
@@ -832,7 +927,9 @@ gns_status sort_range(double *rk, uint32_t *rv, double *pk_, uint32_t *pv_, size
             cnt_prev = cnt_next;
             cnt_next += ceil_div(len, 4 * L);          // next-pass regions of this pass
         }
-        GNS_TRY(launch_merge(g, ck + len, ck + len, corank, nullptr, nullptr, false, ord, st, ad, chn));
+        if (four_pass)
+            GNS_TRY(launch_merge4(ck, ok, len, L, cs, last ? nullptr : os, smp_log2_before(p + 1), piv, ord, st, ad));
+        else GNS_TRY(launch_merge(g, ck + len, ck + len, corank, nullptr, nullptr, false, ord, st, ad, chn));
         std::swap(ck, ok);
         std::swap(cv, ov);
         std::swap(cs, os);
@@ -1011,7 +1108,15 @@ struct Sched {
 void count_sort_range(size_t len, Sched *sc, size_t n)
 {
     if (!len) return;
-    const int M = merge_passes_for(len, k1_run(len, sc->hv));
+    const size_t R = k1_run(len, sc->hv);
+    const int M = merge_passes_for(len, R);
+    if (use_four(sc->hv, len, R)) {
+        // 4-way passes (two levels each, rank + merge launch), an odd level count starts 2-way
+        const int P = (M & 1) + M / 2;
+        sc->elem_passes += (double)(1 + P) * (double)len / (double)n;
+        sc->launches += 1 + (M & 1) * (ticket_pass(false, (int)ceil_div(len, MTILE)) ? 2 : 1) + 2 * (M / 2);
+        return;
+    }
     sc->elem_passes += (double)(1 + M) * (double)len / (double)n;
     // tile sort + per pass one fused launch, or partition + ticket merge
     sc->launches += 1 + M * (ticket_pass(sc->hv, (int)ceil_div(len, MTILE)) ? 2 : 1);
@@ -1025,7 +1130,7 @@ void count_sort_range(size_t len, Sched *sc, size_t n)
 // left b elements are sorted into the buffer and merged in place.
 gns_status sort_limited(double *keys, uint32_t *vals, size_t lo, size_t len, size_t b, double *bk, uint32_t *bv,
                         int *corank, int2 *deps, unsigned *flags, int ord, cudaStream_t st, Sched *sc, size_t n,
-                        double *s0 = nullptr, double *s1 = nullptr)
+                        double *s0 = nullptr, double *s1 = nullptr, unsigned char *piv = nullptr)
 {
     const bool hv = vals != nullptr;
     double *dk = keys + lo;
@@ -1047,18 +1152,19 @@ gns_status sort_limited(double *keys, uint32_t *vals, size_t lo, size_t len, siz
             sc->launches += 3 + (nl % SMP_G == 0 ? 1 : 0);   // (+ sample gather)
             return GNS_OK;
         }
-        GNS_TRY(sort_range(dk, dv, bk, bv, nl, true, corank, ord, st, nullptr, s0, s1));
-        GNS_TRY(sort_range(dk + nl, hv ? dv + nl : nullptr, dk, dv, nr, false, corank, ord, st, nullptr, s0, s1));
+        GNS_TRY(sort_range(dk, dv, bk, bv, nl, true, corank, ord, st, nullptr, s0, s1, nullptr, piv));
+        GNS_TRY(sort_range(dk + nl, hv ? dv + nl : nullptr, dk, dv, nr, false, corank, ord, st, nullptr, s0, s1, nullptr,
+                           piv));
         return top_merge(keys, vals, bk, bv, lo, len, nl, corank, deps, flags, ord, st, s0, s1);
     }
-    GNS_TRY(sort_limited(keys, vals, lo + b, len - b, b, bk, bv, corank, deps, flags, ord, st, sc, n, s0, s1));
+    GNS_TRY(sort_limited(keys, vals, lo + b, len - b, b, bk, bv, corank, deps, flags, ord, st, sc, n, s0, s1, piv));
     if (sc) {
         count_sort_range(b, sc, n);
         sc->elem_passes += (double)len / (double)n;
         sc->launches += 3 + (b % SMP_G == 0 ? 1 : 0);
         return GNS_OK;
     }
-    GNS_TRY(sort_range(dk, dv, bk, bv, b, true, corank, ord, st, nullptr, s0, s1));
+    GNS_TRY(sort_range(dk, dv, bk, bv, b, true, corank, ord, st, nullptr, s0, s1, nullptr, piv));
     return top_merge(keys, vals, bk, bv, lo, len, b, corank, deps, flags, ord, st, s0, s1);
 }
 
@@ -1116,16 +1222,18 @@ gns_status run_sort_aligned(double *keys, uint32_t *vals, size_t n, const Mode &
         uint32_t *bv = hv ? reinterpret_cast<uint32_t *>(ws + Lo.off_v) : nullptr;
         int *corank = reinterpret_cast<int *>(ws + Lo.off_corank);
         double *smp = reinterpret_cast<double *>(ws + Lo.off_smp);
+        unsigned char *piv = Lo.off_piv ? ws + Lo.off_piv : nullptr;
         if (m.omit) {
             GNS_TRY(sort_omit(keys, vals, n, ws, Lo, ord, st));
         } else if (!m.limited) {
             unsigned *unsorted = reinterpret_cast<unsigned *>(ws + Lo.off_adapt);
-            GNS_TRY(sort_range(keys, vals, bk, bv, n, false, corank, ord, st, unsorted, smp, smp + Lo.nsmp, unsorted));
+            GNS_TRY(sort_range(keys, vals, bk, bv, n, false, corank, ord, st, unsorted, smp, smp + Lo.nsmp, unsorted,
+                               piv));
         } else {
             int2 *deps = reinterpret_cast<int2 *>(ws + Lo.off_deps);
             unsigned *flags = reinterpret_cast<unsigned *>(ws + Lo.off_flags);
             GNS_TRY(sort_limited(keys, vals, 0, n, m.buf, bk, bv, corank, deps, flags, ord, st, nullptr, n, smp,
-                                 smp + Lo.nsmp));
+                                 smp + Lo.nsmp, piv));
         }
     }
     if (right && reverse_right) GNS_TRY(launch_reverse(keys, vals, n, st));
@@ -1450,7 +1558,7 @@ gns_status gns_sort_f32(float *keys, uint32_t *vals, size_t n, gns_target target
     gns_status r = (!hv && k1_v3())
         ? launch_pdl("f32_tile_sort_kernel", tile3f_kern(desc), (unsigned)ceil_div(n, F_TILE), NT3,
                      t3_smem<float, NT3>(), st, (const float *)keys, ck, (long long)n, (unsigned *)nullptr,
-                     (float *)nullptr, (unsigned char *)nullptr, (float *)nullptr)
+                     (float *)nullptr, (unsigned char *)nullptr, (float *)nullptr, (int)SMP_LOG2)
         : launch_pdl("f32_tile_sort_kernel", f32_tile_kern(hv, desc), (unsigned)ceil_div(n, F_TILE), F_NT,
                      f_tile_smem(hv), st, (const float *)keys, (const uint32_t *)vals, ck, cv, (long long)n);
     int *corank = reinterpret_cast<int *>(w + (hv ? 2 : 1) * align_up(n * sizeof(float), 256));

@@ -274,6 +274,7 @@ __device__ __forceinline__ double pad_key()
 //   uniform pass : ak = src, bk = src + L, out = dst
 //   in-place top merge (single = 1): ak = buffer, bk = data + nl, L = nl,
 //                  out = data, one pair with na = nl, nb = n - nl
+constexpr int SMP_LOG2_DEF = 9;   // = SMP_LOG2 (below): split-search sample spacing 512
 struct MergeGeo {
     const double *ak;
     const uint32_t *av;
@@ -290,6 +291,7 @@ struct MergeGeo {
     double *so;         // samples of the output region written by this pass, or nullptr
     const double *sb;   // single (two-run) geometry: samples of B (every SMP_G-th key of bk), or nullptr
     long long off = 0;  // single geometry: outputs [off, n) only; ok = the output of merge position off
+    int so_log2 = SMP_LOG2_DEF;   // spacing of the output samples `so` (6 before a 4-way pass, gns_merge4.cuh)
 };
 
 struct TileSpan {
@@ -390,7 +392,7 @@ __device__ __forceinline__ int warp_corank(const MergeGeo &g, int t, int lane)
 //        Q(x) false => B[d-1-x-G] <= B[y_lo(x)] < A[x] <= A[x+G] => c <= x + G.
 // Then the exact search runs in that window (2 rounds of 33-ary probes),
 // instead of ~5 rounds spread over the whole run.
-constexpr int SMP_LOG2 = 9;
+constexpr int SMP_LOG2 = SMP_LOG2_DEF;
 constexpr int SMP_G = 1 << SMP_LOG2;   // 512
 
 // (W+1)-ary search of the last true of a monotone predicate over [lo, hi]
@@ -1071,8 +1073,8 @@ merge_tstore_kernel(PipeGeo pg, int ntiles, int per_cta, const __grid_constant__
         const long long t = tile_of(i);
         const MergeGeo &G = geo(i).g;
         const long long row = t * (MTILE / 16) + tid;    // global row of this thread's 16 outputs
-        if (G.so != nullptr && (tid & (SMP_G / VT - 1)) == 0 && d < cnt)
-            G.so[(row * 16) >> SMP_LOG2] = k[0];      // sample of output position row*16
+        if (G.so != nullptr && (tid & ((1 << (G.so_log2 - 4)) - 1)) == 0 && d < cnt)
+            G.so[(row * 16) >> G.so_log2] = k[0];     // sample of output position row*16
         bar_merge_warps();                               // stage st fully read
         unsigned char *rowp = reinterpret_cast<unsigned char *>(sk) + tid * 128;
 #pragma unroll
@@ -1550,8 +1552,8 @@ merge_inplace_kernel(PipeGeo pg, int ntiles, const int *__restrict__ corank, con
         serial_merge_stage<HV, ORD>(kbase, sv, mt, mt.offa + ii, mt.offa + mt.ca, mt.bslot + d - ii, mt.bslot + mt.cb, k,
                                     v);
         const long long row = (long long)t * (MTILE / 16) + tid;
-        if (pg.g.so != nullptr && (tid & (SMP_G / VT - 1)) == 0 && d < cnt)
-            pg.g.so[(row * 16) >> SMP_LOG2] = k[0];             // sample of output position row*16
+        if (pg.g.so != nullptr && (tid & ((1 << (pg.g.so_log2 - 4)) - 1)) == 0 && d < cnt)
+            pg.g.so[(row * 16) >> pg.g.so_log2] = k[0];         // sample of output position row*16
         bar_merge_warps();                                     // stage st fully read
         unsigned char *rowp = reinterpret_cast<unsigned char *>(sk) + tid * 128;
 #pragma unroll

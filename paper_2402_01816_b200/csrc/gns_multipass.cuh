@@ -61,6 +61,7 @@ struct MultiGeo {
     long long n;
     int passes;            // merge passes M (>= 1)
     int ntiles;            // merge tiles per pass
+    int blk;               // the first `blk` passes run block-major (blocks of TILE << blk keys: L2-resident), 0: pass-major
     unsigned *ticket;      // [0] work ticket (zeroed by the host)
     unsigned *done;        // completion counters (zeroed by the host)
     long long x_idx0, y_idx0;   // element index of xk[0] / yk[0] in its load map (0 or 1)
@@ -148,6 +149,42 @@ __device__ __forceinline__ bool mbar_test(uint64_t *bar, uint32_t parity)
                  "selp.u32 %0, 1, 0, p;\n}"
                  : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
     return ok != 0;
+}
+
+// Ticket order.  Pass-major: ticket tk = p * cpp + chunk.  With G.blk > 0 the
+// first blk passes are claimed block by block (all blk passes of block b, a
+// block = TILE << blk keys, before block b+1), so a block's intermediate runs
+// stay in L2 between its passes; the remaining passes follow pass-major.
+// Every chunk still depends only on smaller tickets (its pair region of the
+// previous pass): deadlock-free.
+__device__ __forceinline__ void mp_item(const MultiGeo &G, int cpp, int tk, int &p, int &c)
+{
+    const int blk = min(G.blk, G.passes);
+    if (blk > 0) {
+        const int cpb = (int)(((long long)TILE << blk) / (MP_CHUNK * MTILE));   // chunks per block and pass
+        const int nb = (cpp + cpb - 1) / cpb;
+        const int tb = blk * cpp;
+        if (tk < tb) {
+            const int b = tk / (blk * cpb);
+            if (b < nb - 1) {
+                const int r = tk - b * blk * cpb;
+                p = r / cpb;
+                c = b * cpb + r % cpb;
+            } else {
+                const int lc = cpp - (nb - 1) * cpb;                    // chunks of the last (partial) block
+                const int r = tk - (nb - 1) * blk * cpb;
+                p = r / lc;
+                c = (nb - 1) * cpb + r % lc;
+            }
+            return;
+        }
+        tk -= tb;
+        p = blk + tk / cpp;
+        c = tk % cpp;
+        return;
+    }
+    p = tk / cpp;
+    c = tk % cpp;
 }
 
 struct MpEntry {
@@ -335,8 +372,9 @@ merge_multi_kernel(MultiGeo G, const __grid_constant__ CUtensorMap xload, const 
                 }
                 break;
             }
-            const int p = tk / cpp;
-            const int t0 = (tk % cpp) * MP_CHUNK;
+            int p, cidx;
+            mp_item(G, cpp, tk, p, cidx);
+            const int t0 = cidx * MP_CHUNK;
             const int nt = min(MP_CHUNK, G.ntiles - t0);
             const MergeGeo g = mp_geo(G, p);
 #ifdef GNS_PROF

@@ -37,7 +37,7 @@ namespace gns {
 #define GNS_K1_ONELDS 0
 #endif
 constexpr int NT3 = 128;                  // threads per CTA
-constexpr int VT3 = 64;                   // keys per thread
+constexpr int VT3 = 64;                   // keys per thread (2^6: the finest sample spacing of K1)
 static_assert(NT3 * VT3 == TILE, "K1 key-only tile must equal TILE");
 template <typename K = double, int NT = 128> constexpr size_t t3_smem() { return (size_t)NT * (VT3 * sizeof(K) + 16) + 128; }
 constexpr int SEG3_BYTES = VT3 * 8 + 16;  // padded 512-byte segment per thread
@@ -484,7 +484,7 @@ __device__ __forceinline__ void cluster_levels(uint32_t sbase, int tid, K (&k)[V
 template <typename K, int ORD, int NT3 = gns::NT3, bool CLU = false>
 __global__ void __launch_bounds__(NT3, NT3 == 128 ? (sizeof(K) == 4 ? 4 : 3) : 1)
 tile_sort3_kernel(const K *src_k, K *dst_k, long long n, unsigned *unsorted, K *smp,
-                  unsigned char *tdesc, K *smp_src)
+                  unsigned char *tdesc, K *smp_src, int smp_log2)
 {
     constexpr int TL = NT3 * VT3;                // keys per tile
     constexpr int SZ = sizeof(K);
@@ -656,8 +656,9 @@ tile_sort3_kernel(const K *src_k, K *dst_k, long long n, unsigned *unsorted, K *
             for (int j = 0; j < PER; ++j) r[j] = k[PER * c + PER - 1 - j];
             sts16_k<K>(smem_u32(oseg) + 16 * (VT3 / PER - 1 - c), r);
         }
-        if (smp != nullptr && (ot & (SMP_G / VT3 - 1)) == 0)
-            smp[(base + (long long)ot * VT3) >> SMP_LOG2] = k[VT3 - 1];
+        // (samples of dst every 1 << smp_log2 keys, smp_log2 >= log2(VT3); 6 for 4-way passes)
+        if (smp != nullptr && (ot & ((1 << (smp_log2 - 6)) - 1)) == 0)
+            smp[(base + (long long)ot * VT3) >> smp_log2] = k[VT3 - 1];
         fence_proxy_async();
         bulk_store_1d(dst_k + base + (long long)ot * VT3, oseg, VT3 * SZ);
         bulk_commit();
@@ -666,8 +667,8 @@ tile_sort3_kernel(const K *src_k, K *dst_k, long long n, unsigned *unsorted, K *
         pdl_trigger();
         return;
     }
-    if (smp != nullptr && e0 < cnt && (tid & (SMP_G / VT3 - 1)) == 0)
-        smp[(base + e0) >> SMP_LOG2] = k[0];
+    if (smp != nullptr && e0 < cnt && (tid & ((1 << (smp_log2 - 6)) - 1)) == 0)
+        smp[(base + e0) >> smp_log2] = k[0];
     if (!CLU && mode == 1 && dst_k == src_k) {
         GNS_TL_END(0);
         pdl_trigger();

@@ -4,7 +4,7 @@ persistent launch), GNS_CHAIN=1 (chained passes on region counters),
 GNS_K1=2 (the 256 x 32 key-only tile sort), GNS_K1_CL=8 / 16 (the key-only
 tile sort merging a thread-block cluster's tiles on chip), GNS_MERGE_MODE=1
 (ticket passes for every size), GNS_SMALL=0 (tile sort + merge passes for
-n <= 65536).  Each sorts a few seeded inputs through the C-ABI and
+n <= 65536), GNS_FOUR=1 (key-only 4-way merge passes, gns_merge4.cuh).  Each sorts a few seeded inputs through the C-ABI and
 compares bit-exactly with the oracle."""
 import os
 import subprocess
@@ -50,8 +50,74 @@ sys.exit(1 if bad else 0)
 
 
 @pytest.mark.parametrize("env", [{"GNS_MULTI": "1"}, {"GNS_CHAIN": "1"}, {"GNS_K1": "2"}, {"GNS_MERGE_MODE": "1"}, {"GNS_SMALL": "0"},
-                                 {"GNS_MERGE_MODE": "0"}, {"GNS_K1_CL": "8"}, {"GNS_K1_CL": "16"}])
+                                 {"GNS_MERGE_MODE": "0"}, {"GNS_K1_CL": "8"}, {"GNS_K1_CL": "16"}, {"GNS_FOUR": "1"},
+                                 {"GNS_FOUR": "1", "GNS_MERGE_MODE": "1"}])
 def test_env_variant_bitexact(env):
     e = dict(os.environ, **env)
     r = subprocess.run([sys.executable, "-c", SCRIPT.replace("ROOT_DIR", repr(ROOT))], capture_output=True, text=True, env=e, timeout=600)
     assert r.returncode == 0, (env, r.stdout[-2000:], r.stderr[-2000:])
+
+
+# The 4-way passes (GNS_FOUR=1) on what only they see: an even level count
+# (every pass 4-way, the tile sort writes the fine samples), partial last
+# groups (1, 2 or 3 runs), heavy ties and signed zeros across the runs (the
+# pivot tie rule), both directions and the integer key types, both buffer modes.
+SCRIPT4 = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, ROOT_DIR)
+import oracle, synth, paper_2402_01816_b200 as gns
+T1 = 8192
+bad = 0
+sizes = [4 * T1, 4 * T1 + 1, 6 * T1 + 333, 7 * T1 - 3, 16 * T1, 17 * T1 + 9, (1 << 19) + 1, 1 << 20, 3 * (1 << 18) + 77]
+for n in sizes:
+    for kind in ("uniform", "ties3", "zeros", "runs"):
+        if kind == "uniform":
+            k = synth.uniform(n, n)
+        elif kind == "ties3":
+            k = synth.ties(n, n + 1, 3)
+        elif kind == "zeros":
+            k = synth.ties(n, n + 2, 3) - 1.0
+            k[::5] = -0.0
+            k[1::7] = 0.0
+        else:
+            k = synth.config(4, "runs16", n).keys
+        for frac in (1.0, 0.5):
+            tk = torch.from_numpy(k.copy()).cuda()
+            gns.sort_(tk, None, frac)
+            torch.cuda.synchronize()
+            ek, _ = oracle.sort(k, None)
+            if not np.array_equal(tk.cpu().numpy().view(np.uint64), ek.view(np.uint64)):
+                bad += 1
+                print("FAIL", n, kind, frac)
+# the four targets and the integer key types (gns_sort_keys), with payload-free keys
+n = 9 * T1 + 5
+rng = np.random.default_rng(7)
+for target in ("AscLeft", "AscRight", "DescLeft", "DescRight"):
+    k = synth.ties(n, 11, 50)
+    tk = torch.from_numpy(k.copy()).cuda()
+    gns.sort_(tk, None, 1.0, target=target)
+    torch.cuda.synchronize()
+    ek, _ = oracle.sort_target(k, None, target)
+    if not np.array_equal(tk.cpu().numpy().view(np.uint64), ek.view(np.uint64)):
+        bad += 1
+        print("FAIL target", target)
+for kt, dt in (("i64", np.int64), ("u64", np.uint64)):
+    k = rng.integers(0, 1000, n).astype(dt)
+    k[::3] = np.iinfo(dt).max
+    tk = torch.from_numpy(k.copy()).cuda()
+    gns.sort_(tk, None, 1.0, target="DescLeft")
+    torch.cuda.synchronize()
+    ek, _ = oracle.sort_keys(k, None, kt, "DescLeft")
+    if not np.array_equal(tk.cpu().numpy(), ek):
+        bad += 1
+        print("FAIL key type", kt)
+print("bad", bad)
+sys.exit(1 if bad else 0)
+"""
+
+
+def test_four_way_passes_bitexact():
+    e = dict(os.environ, GNS_FOUR="1")
+    r = subprocess.run([sys.executable, "-c", SCRIPT4.replace("ROOT_DIR", repr(ROOT))], capture_output=True, text=True, env=e,
+                       timeout=900)
+    assert r.returncode == 0, (r.stdout[-2000:], r.stderr[-2000:])

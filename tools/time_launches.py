@@ -46,3 +46,4 @@ for kd, t in sorted(agg.items(), key=lambda x: -x[1]):
     print(f"  {kd:14s} {t:.3f} ms ({100 * t / tot:.1f}%)  launches {kinds.count(kd)}")
 big = [(kd, t) for kd, t in zip(kinds, med) if kd in ("inplace_merge", "partition", "inplace_deps")]
 print("  in-place steps:", " ".join(f"{kd}:{t*1e3:.0f}us" for kd, t in big))
+print("  per launch:", " ".join(f"{kd}:{t*1e3:.1f}" for kd, t in zip(kinds, med)))
