@@ -17,6 +17,7 @@ ap.add_argument("--pairs", action="store_true")
 ap.add_argument("--frac", type=float, default=0.5)
 ap.add_argument("--omit", action="store_true")
 ap.add_argument("--input", default="uniform")
+ap.add_argument("--u64", action="store_true", help="gns_sort_keys_u64 (64-bit payload)")
 a = ap.parse_args()
 n = 1 << a.n
 src = torch.from_numpy(synth.uniform(n, 9) if a.input == "uniform" else synth.config(4, a.input, n).keys).cuda()
@@ -24,13 +25,18 @@ srcv = torch.from_numpy(synth.iota_u32(n)).cuda() if a.pairs else None
 k = torch.empty_like(src)
 v = torch.empty_like(srcv) if a.pairs else None
 ws = gns.alloc_workspace(n, a.frac, a.pairs)
+if a.u64:
+    v64 = torch.arange(n, device="cuda", dtype=torch.int64)
+    ws64 = torch.empty(gns.workspace_bytes_u64(n), dtype=torch.uint8, device="cuda")
 per = []
 for i in range(3):
     k.copy_(src)
     if a.pairs:
         v.copy_(srcv)
     assert gns.gns_timing_begin(512) == 0
-    if a.omit:
+    if a.u64:
+        gns.sort_u64_(k, v64, workspace=ws64)
+    elif a.omit:
         gns.sort_omit_(k, v, workspace=ws)
     else:
         gns.sort_(k, v, a.frac, workspace=ws)
