@@ -1,46 +1,66 @@
 // gns_tile64.cuh — K1 for key-only sorts: the stable
-// sort of one 8192-key tile per CTA with 128 threads x 64 keys.
+// sort of one 8192-key tile per CTA with NT3 threads x VT3 keys (default
+// 256 x 32, three CTAs per SM; GNS_VT3=64 gives round 2's 128 x 64).
 //
-// Why a second K1 for key-only: the 256 x 32 kernel (tile_sort2_kernel) is
-// bound by shared-memory wavefronts (ncu: l1tex 91 % busy, 3.7 wavefronts per
-// key, half of them bank conflicts of the data-dependent merge reads) and
-// spends ~77 instructions per key on its 32-key transposition sort.  Here:
-//   * one 64-key sorting network per thread in registers (Batcher's odd-even
-//     merge sort: 543 compare-exchanges instead of 2016 for a 64-key
-//     transposition sort) -- unstable, which is harmless for key-only input
-//     because equal keys are bit-identical, except -0.0 / +0.0 (equal under
-//     IEEE <, different bits): a thread holding a zero records the signs of its
-//     zeros in input order, sorts canonical +0.0 and writes the signs back in
-//     that order, which is exactly the stable order (R2);
-//   * 3 warp-level bitonic merge rounds in registers + shuffles (runs 64 ->
-//     512) unless the CTA holds a -0.0 or NaN key, then 4 shared-memory
-//     merge-path rounds (runs 512 -> 8192; all 7 in the -0.0 / NaN case), each
-//     thread producing 64 outputs as two independent chains (merge path +
-//     serial merge, left run wins ties);
-//   * the tile arrives by 128 one-dimensional bulk copies (one 512-byte
-//     segment per thread, TMA engine, one mbarrier) into a padded layout whose
-//     16-byte register transfers are conflict-free, and leaves the same way.
-// Measured (B200, 2^24 f64 U(0,1), event-timed): 246 -> 223 us; ncu: 61.5 M ->
-// ~31 M shared wavefronts, 154 M -> ~120 M instructions (DESIGN.md 8b lists
-// the variants tried: one-load merge steps, 16384-key tiles, 0-5 bitonic rounds).
-// One read-scan and one write-scan of HBM per tile; the 13
-// merge levels inside the tile cost no HBM traffic.
+// Why a second K1 for key-only: the 256 x 32 kernel with payload
+// (tile_sort2_kernel) is bound by shared-memory wavefronts (ncu: l1tex 91 %
+// busy, 3.7 wavefronts per key, half of them bank conflicts of the
+// data-dependent merge reads) and spends ~77 instructions per key on its
+// 32-key transposition sort.  Here:
+//   * one VT3-key sorting network per thread in registers (Batcher's odd-even
+//     merge sort: 191 compare-exchanges for 32 keys, 543 for 64, instead of
+//     496 / 2016 for a transposition sort) -- unstable, which is harmless for
+//     key-only input because equal keys are bit-identical, except -0.0 / +0.0
+//     (equal under IEEE <, different bits): a thread holding a zero records
+//     the signs of its zeros in input order, sorts canonical +0.0 and writes
+//     the signs back in that order, which is exactly the stable order
+//     (R2);
+//   * GNS_K1_BITONIC warp-level bitonic merge rounds in registers + shuffles
+//     (default 2: runs 32 -> 128) unless the CTA holds a -0.0 or NaN key, then
+//     shared-memory merge-path rounds up to 8192 (all of them in the -0.0 /
+//     NaN case), each thread producing VT3 outputs as two independent chains
+//     (merge path + serial merge, left run wins ties);
+//   * the tile arrives by one-dimensional bulk copies (one VT3-key segment
+//     per thread, TMA engine, one mbarrier) into a padded layout whose 16-byte
+//     register transfers are conflict-free, and leaves the same way.
+// Measured (B200, 2^24 f64, event-timed): 128 x 64: 246 -> 223-229 us (ncu:
+// 61.5 M -> ~31 M shared wavefronts, 154 M -> ~120 M instructions); 256 x 32
+// (24 warps per SM instead of 12): whole sort 0.807 -> 0.794 ms, 24 tie
+// values 0.783 -> 0.752 ms (DESIGN.md 8b lists the variants tried: one-load
+// merge steps, 16384-key tiles, 0-5 bitonic rounds, 16 keys per thread,
+// four chains).  One read-scan and one write-scan of HBM per tile
+// (PAPER.md:150); the 13 merge levels inside the tile cost no HBM traffic.
 #pragma once
 
 namespace gns {
 
 // warp-level bitonic merge rounds before the merge-path rounds (0..5)
 #ifndef GNS_K1_BITONIC
-#define GNS_K1_BITONIC 3
+#define GNS_K1_BITONIC 2
 #endif
 #ifndef GNS_K1_ONELDS
 #define GNS_K1_ONELDS 0
 #endif
-constexpr int NT3 = 128;                  // threads per CTA
-constexpr int VT3 = 64;                   // keys per thread (2^6: the finest sample spacing of K1)
+// keys per thread: 32 (256 threads, 3 CTAs per SM = 24 warps, Batcher's
+// 191-comparator network of 32 keys) -- measured against 64 (128 threads,
+// 12 warps, 543 comparators): 2^24 keys 0.794 vs 0.804 ms, 24 heavy-tie
+// values 0.750 vs 0.780 ms
+#ifndef GNS_VT3
+#define GNS_VT3 32
+#endif
+constexpr int VT3 = GNS_VT3;              // keys per thread (64: 2^6, the finest sample spacing of K1)
+constexpr int NT3 = TILE / VT3;           // threads per CTA (128)
+constexpr int VT3_LOG2 = VT3 == 64 ? 6 : VT3 == 32 ? 5 : 4;
+static_assert((1 << VT3_LOG2) == VT3, "VT3_LOG2");
+#ifndef GNS_T3_MINB
+#define GNS_T3_MINB 3             // CTAs per SM (shared memory allows three 8192-key tiles)
+#endif
+#ifndef GNS_T3F_MINB
+#define GNS_T3F_MINB 4            // binary32 keys: four (half the shared memory per tile)
+#endif
 static_assert(NT3 * VT3 == TILE, "K1 key-only tile must equal TILE");
 template <typename K = double, int NT = 128> constexpr size_t t3_smem() { return (size_t)NT * (VT3 * sizeof(K) + 16) + 128; }
-constexpr int SEG3_BYTES = VT3 * 8 + 16;  // padded 512-byte segment per thread
+constexpr int SEG3_BYTES = VT3 * 8 + 16;  // padded 512-byte segment per thread (+16)
 constexpr size_t T3_SMEM = (size_t)NT3 * SEG3_BYTES + 128;   // 67,712 B: 3 CTAs per SM
 static_assert(256 + TILE * 8 + 8 <= NT3 * SEG3_BYTES, "merge layout + guard slots fit the padded segments");
 
@@ -156,7 +176,12 @@ __device__ __forceinline__ void network_sort(K (&k)[N])
 // positions per 8 lanes: conflict-free.  A bijection on every 128-byte line.
 // (binary32: 256-byte blocks, bits 4-6 XORed with bits 8-10)
 template <typename K = double>
-__device__ __forceinline__ uint32_t sw3(uint32_t a) { return a ^ ((a >> (sizeof(K) == 8 ? 5 : 4)) & 0x70u); }
+__device__ __forceinline__ uint32_t sw3(uint32_t a)
+{
+    // bits 4-6 XOR the thread-block index bits: block = VT3 * sizeof(K) bytes
+    constexpr int SH = (VT3 * (int)sizeof(K) == 512) ? 5 : (VT3 * (int)sizeof(K) == 256) ? 4 : 3;
+    return a ^ ((a >> SH) & 0x70u);
+}
 
 // Stable co-rank of diagonal d (A wins ties; predicate A[m] <= B[d-1-m]) and,
 // if `two`, of diagonal d + VT3 in the same loop (independent probes).
@@ -482,7 +507,7 @@ __device__ __forceinline__ void cluster_levels(uint32_t sbase, int tid, K (&k)[V
 // CLU: launched in thread-block clusters of C CTAs, the output runs are
 // C x TL keys (cluster_levels); no Omitsort descriptors (tdesc == nullptr).
 template <typename K, int ORD, int NT3 = gns::NT3, bool CLU = false>
-__global__ void __launch_bounds__(NT3, NT3 == 128 ? (sizeof(K) == 4 ? 4 : 3) : 1)
+__global__ void __launch_bounds__(NT3, NT3 == gns::NT3 ? (sizeof(K) == 4 ? GNS_T3F_MINB : GNS_T3_MINB) : 1)
 tile_sort3_kernel(const K *src_k, K *dst_k, long long n, unsigned *unsorted, K *smp,
                   unsigned char *tdesc, K *smp_src, int smp_log2)
 {
@@ -656,8 +681,8 @@ tile_sort3_kernel(const K *src_k, K *dst_k, long long n, unsigned *unsorted, K *
             for (int j = 0; j < PER; ++j) r[j] = k[PER * c + PER - 1 - j];
             sts16_k<K>(smem_u32(oseg) + 16 * (VT3 / PER - 1 - c), r);
         }
-        // (samples of dst every 1 << smp_log2 keys, smp_log2 >= log2(VT3); 6 for 4-way passes)
-        if (smp != nullptr && (ot & ((1 << (smp_log2 - 6)) - 1)) == 0)
+        // (samples of dst every 1 << smp_log2 keys, smp_log2 >= log2(VT3); 6 before 4-way passes)
+        if (smp != nullptr && (ot & ((1 << (smp_log2 - VT3_LOG2)) - 1)) == 0)
             smp[(base + (long long)ot * VT3) >> smp_log2] = k[VT3 - 1];
         fence_proxy_async();
         bulk_store_1d(dst_k + base + (long long)ot * VT3, oseg, VT3 * SZ);
@@ -667,7 +692,7 @@ tile_sort3_kernel(const K *src_k, K *dst_k, long long n, unsigned *unsorted, K *
         pdl_trigger();
         return;
     }
-    if (smp != nullptr && e0 < cnt && (tid & ((1 << (smp_log2 - 6)) - 1)) == 0)
+    if (smp != nullptr && e0 < cnt && (tid & ((1 << (smp_log2 - VT3_LOG2)) - 1)) == 0)
         smp[(base + e0) >> smp_log2] = k[0];
     if (!CLU && mode == 1 && dst_k == src_k) {
         GNS_TL_END(0);
