@@ -325,6 +325,16 @@ bool chain_on()
     }();
     return on;
 }
+// The merge pass's producer warp issues a tile's TMA boxes one per lane
+// (PipeGeo::coop) instead of all from one lane.  GNS_COOP=0: one lane (A/B).
+bool coop_on()
+{
+    static const bool on = [] {
+        const char *e = std::getenv("GNS_COOP");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
 using Tile3K = decltype(&tile_sort3_kernel<double, 0>);
 Tile3K tile3_kern(int o)
 {
@@ -681,6 +691,7 @@ gns_status launch_merge(const MergeGeo &g, const double *lim_a, const double *li
     pg.g = g;
     pg.a_lim = lim_a;
     pg.b_lim = lim_b;
+    pg.coop = coop_on();
     CUtensorMap map, amap, bmap;
     GNS_TRY(row_map(g.ok, (size_t)g.n, true, MTILE / 16, &map));
     // (B may start past the array end when the last pair has no B run: empty map, never loaded)

@@ -570,6 +570,8 @@ struct PipeGeo {
     long long b_idx0;      // element index of g.bk[0] in the B key map's array
     long long a_rows;      // full 16-key rows of the A map (row a_rows is patched by hand)
     long long b_rows;
+    int coop = 0;          // merge_tstore_kernel: 1 = the whole producer warp issues a tile's TMA boxes
+                           // (one box per lane), 0 = one lane issues them all
 };
 
 struct PipeMeta {
@@ -587,8 +589,12 @@ struct PipeMeta {
 template <bool HV>
 __device__ __forceinline__ void pipe_issue(const PipeGeo &pg, const CUtensorMap &amap, const CUtensorMap &bmap,
                                            int t, int i0, int i1next, double *sk, uint32_t *sv, uint64_t *bar,
-                                           PipeMeta *meta, uint64_t policy)
+                                           PipeMeta *meta, uint64_t policy, int ln = -1)
 {
+    // ln >= 0: called by all 32 lanes of a warp (lane ln); lane 0 posts the
+    // byte count, writes the meta and arrives, lane b issues key box b.
+    const bool coop = ln >= 0;
+    const bool lead = !coop || ln == 0;
     const MergeGeo &g = pg.g;
     const TileSpan s = tile_span(g, t);
     const int cnt = s.k1 - s.k0;
@@ -627,11 +633,22 @@ __device__ __forceinline__ void pipe_issue(const PipeGeo &pg, const CUtensorMap 
         if (veb > vsb) total += (uint32_t)(veb - vsb) * 4u;
     }
     // Post the expected byte count first (no arrival yet), then issue.
-    mbar_expect_tx(bar, total);
-    for (int b = 0; b < nba; ++b)
-        tma_load_2d_hint(sk + b * KROWS * 16, &amap, 0, (int)((ga >> 4) + b * KROWS), bar, policy);
-    for (int b = 0; b < nbb; ++b)
-        tma_load_2d_hint(sk + (rb0 + b * KROWS) * 16, &bmap, 0, (int)((gb >> 4) + b * KROWS), bar, policy);
+    if (lead) mbar_expect_tx(bar, total);
+    if (coop) {
+        GNS_DASSERT(nba + nbb <= 32);
+        __syncwarp();
+        if (ln < nba)
+            tma_load_2d_hint(sk + ln * KROWS * 16, &amap, 0, (int)((ga >> 4) + ln * KROWS), bar, policy);
+        else if (ln - nba < nbb)
+            tma_load_2d_hint(sk + (rb0 + (ln - nba) * KROWS) * 16, &bmap, 0, (int)((gb >> 4) + (ln - nba) * KROWS),
+                             bar, policy);
+        if (!lead) return;
+    } else {
+        for (int b = 0; b < nba; ++b)
+            tma_load_2d_hint(sk + b * KROWS * 16, &amap, 0, (int)((ga >> 4) + b * KROWS), bar, policy);
+        for (int b = 0; b < nbb; ++b)
+            tma_load_2d_hint(sk + (rb0 + b * KROWS) * 16, &bmap, 0, (int)((gb >> 4) + b * KROWS), bar, policy);
+    }
     if (HV) {
         if (vea > vsa) tma_load_1d(sv + voffa + vsa, Av + vsa, (uint32_t)(vea - vsa) * 4u, bar, policy);
         for (int e = max(vea, 0); e < ca; ++e) sv[voffa + e] = Av[e];
@@ -979,8 +996,10 @@ merge_tstore_kernel(PipeGeo pg, int ntiles, int per_cta, const __grid_constant__
     }
 
     if (warp == PRODUCER_WARP) {
-        // ------------------------------------------------ producer (one lane)
-        if (lane != 0) return;
+        // ------------------------------------------------ producer (one lane, or the
+        // whole warp issuing the loads with pg.coop; stores and their waits stay on lane 0)
+        if (!pg.coop && lane != 0) return;
+        const int pln = pg.coop ? lane : -1;
         const uint64_t policy = policy_evict_first();
         auto get_split = [&](int j) -> int {
 #ifdef GNS_PROF
@@ -999,8 +1018,8 @@ merge_tstore_kernel(PipeGeo pg, int ntiles, int per_cta, const __grid_constant__
             const int s1 = (i + 1 < nspl) ? get_split(i + 1) : 0;
             if (chained) fence_proxy_async_global();   // the region's stores (acquired by a search lane) before our loads
             pipe_issue<HV>(geo(i), r ? amap1 : amap, r ? bmap1 : bmap, tile_of(i), s0, s1, skb(st), svb(st),
-                           &full[st], &meta[st], policy);
-            spl_used = i;
+                           &full[st], &meta[st], policy, pln);
+            if (lane == 0) spl_used = i;
         };
         for (int i = 0; i < NS && i < m; ++i) issue(i);
 #ifdef GNS_PROF
@@ -1012,12 +1031,13 @@ merge_tstore_kernel(PipeGeo pg, int ntiles, int per_cta, const __grid_constant__
             mbar_wait(&staged[st], (uint32_t)((i / NS) & 1));     // tile i staged by the 8 merge warps
             GNS_PT(p1);
             GNS_PADD(1, p1 - p0);
-            if (pg.g.n - pg.g.off >= 16) {   // (< 16 outputs: no full row; the merge warps stored the partial row)
+            if (pg.g.n - pg.g.off >= 16 && lane == 0) {   // (< 16 outputs: no full row; the merge warps stored the partial row)
                 tma_store_2d(rev(i) ? &omap1 : &omap, skb(st), 0, (int)((long long)tile_of(i) * (MTILE / 16)));
                 bulk_commit();
             }
             if (i + NS < m) {
-                bulk_wait_read0();                                 // stage st read out -> reusable
+                if (lane == 0) bulk_wait_read0();                  // stage st read out -> reusable
+                if (pg.coop) __syncwarp();
                 GNS_PT(p2);
                 GNS_PADD(5, p2 - p1);
                 issue(i + NS);
@@ -1025,8 +1045,8 @@ merge_tstore_kernel(PipeGeo pg, int ntiles, int per_cta, const __grid_constant__
                 GNS_PADD(6, p3 - p2);
             }
         }
-        bulk_wait0();
-        if (!OL && ch.sig != nullptr) {
+        if (lane == 0) bulk_wait0();
+        if (!OL && ch.sig != nullptr && lane == 0) {
             // this CTA's stored tiles, per next-pass region of 4L
             __threadfence();
             const long long span = 4 * pg.g.L;
@@ -1043,7 +1063,8 @@ merge_tstore_kernel(PipeGeo pg, int ntiles, int per_cta, const __grid_constant__
         acc[7] = clock64() - t_entry;
         acc[9] = m;
         acc[10] = 1;
-        for (int q = 0; q < 11; ++q) atomicAdd(&g_prof[q], acc[q]);
+        if (lane == 0)
+            for (int q = 0; q < 11; ++q) atomicAdd(&g_prof[q], acc[q]);
 #endif
         pdl_trigger();
         return;

@@ -8,15 +8,17 @@
 // holds the array in shared memory, 4096 elements per CTA:
 //   1. each CTA loads its 4096 keys (+ vals; the last CTA padded with the
 //      order's maximum key, placed after every real key) and sorts them
-//      stably: a 16-key transposition sort per thread, then 8 shared-memory
-//      merge-path rounds (runs 16 -> 4096, left run wins ties);
+//      stably: an SM_VT-key transposition sort per thread (512 threads x 8
+//      keys; 256 x 16 measured 4 % slower at 2^16 pairs, 1024 x 4 8 % slower),
+//      then log2(SM_NT) shared-memory merge-path rounds (runs 8 -> 4096, left
+//      run wins ties);
 //   2. log2(C) merge levels across the cluster through distributed shared
 //      memory: CTA c produces outputs [4096 (c - g0), +4096) of its group's
 //      two runs (A = the group's first half of CTAs, B = the second): two
 //      warps find the co-ranks of the first and the one-past-last output by
 //      33-ary searches over the remote keys, all threads copy A[i0:i1) and
 //      B[j0:j1) from the remote CTAs into local staging, then a local merge
-//      path + 16-step serial merge per thread; cluster barriers separate the
+//      path + SM_VT-step serial merge per thread; cluster barriers separate the
 //      remote reads from the overwrite of each CTA's buffer;
 //   3. each CTA writes its first real outputs back.
 // One read and one write of the data in HBM; no buffer (%RAM 1.0).
@@ -27,8 +29,14 @@ namespace gns {
 
 namespace cg = cooperative_groups;
 
-constexpr int SM_NT = 256;                   // threads per CTA
-constexpr int SM_VT = 16;                    // elements per thread
+#ifndef GNS_SM_NT
+#define GNS_SM_NT 512
+#endif
+#ifndef GNS_SM_VT
+#define GNS_SM_VT 8
+#endif
+constexpr int SM_NT = GNS_SM_NT;             // threads per CTA
+constexpr int SM_VT = GNS_SM_VT;             // elements per thread
 constexpr int SM_TILE = SM_NT * SM_VT;       // 4096 elements per CTA
 constexpr int SM_MAXC = 16;                  // CTAs per cluster (non-portable above 8)
 constexpr long long SMALL_MAX_N = (long long)SM_MAXC * SM_TILE;   // 65536

@@ -4,7 +4,8 @@ persistent launch), GNS_CHAIN=1 (chained passes on region counters),
 GNS_K1=2 (the 256 x 32 key-only tile sort), GNS_K1_CL=8 / 16 (the key-only
 tile sort merging a thread-block cluster's tiles on chip), GNS_MERGE_MODE=1
 (ticket passes for every size), GNS_SMALL=0 (tile sort + merge passes for
-n <= 65536), GNS_FOUR=1 (key-only 4-way merge passes, gns_merge4.cuh).  Each sorts a few seeded inputs through the C-ABI and
+n <= 65536), GNS_FOUR=1 (key-only 4-way merge passes, gns_merge4.cuh),
+GNS_COOP=0 (the merge pass's TMA boxes issued by one producer lane).  Each sorts a few seeded inputs through the C-ABI and
 compares bit-exactly with the oracle."""
 import os
 import subprocess
@@ -51,7 +52,7 @@ sys.exit(1 if bad else 0)
 
 @pytest.mark.parametrize("env", [{"GNS_MULTI": "1"}, {"GNS_CHAIN": "1"}, {"GNS_K1": "2"}, {"GNS_MERGE_MODE": "1"}, {"GNS_SMALL": "0"},
                                  {"GNS_MERGE_MODE": "0"}, {"GNS_K1_CL": "8"}, {"GNS_K1_CL": "16"}, {"GNS_FOUR": "1"},
-                                 {"GNS_FOUR": "1", "GNS_MERGE_MODE": "1"}])
+                                 {"GNS_FOUR": "1", "GNS_MERGE_MODE": "1"}, {"GNS_COOP": "0"}])
 def test_env_variant_bitexact(env):
     e = dict(os.environ, **env)
     r = subprocess.run([sys.executable, "-c", SCRIPT.replace("ROOT_DIR", repr(ROOT))], capture_output=True, text=True, env=e, timeout=600)
