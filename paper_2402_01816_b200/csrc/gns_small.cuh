@@ -106,7 +106,15 @@ template <bool HV, int ORD>
 __global__ void __launch_bounds__(SM_NT, 1)
 small_sort_kernel(double *keys, uint32_t *vals, long long n)
 {
+#ifdef GNS_PROF
+    // phase clocks of CTA 0 (tools/prof_small.py): g_prof[0..8]
+    const long long pt0 = clock64();
+#define SM_PT(q) do { if (threadIdx.x == 0 && blockIdx.x == 0) atomicAdd(&g_prof[q], (unsigned long long)(clock64() - pt0)); } while (0)
+#else
+#define SM_PT(q) do {} while (0)
+#endif
     pdl_wait();
+    SM_PT(0);
     cg::cluster_group cluster = cg::this_cluster();
     const int C = (int)cluster.num_blocks();
     const int c = (int)cluster.block_rank();
@@ -139,7 +147,9 @@ small_sort_kernel(double *keys, uint32_t *vals, long long n)
         k[x] = sk[swz16(tid * SM_VT + x)];
         if (HV) v[x] = sv[swz16(tid * SM_VT + x)];
     }
+    SM_PT(1);
     sm_transpose16<ORD>(k, v, HV);
+    SM_PT(2);
 #pragma unroll 1
     for (int coop = 2; coop <= SM_NT; coop <<= 1) {
         __syncthreads();
@@ -162,12 +172,14 @@ small_sort_kernel(double *keys, uint32_t *vals, long long n)
         rk[swz16(tid * SM_VT + x)] = k[x];
         if (HV) rv[swz16(tid * SM_VT + x)] = v[x];
     }
+    SM_PT(3);
     // ---- 2. merge levels across the cluster
     __shared__ int s_co[2];
     const int warp = tid >> 5, lane = tid & 31;
 #pragma unroll 1
     for (int G = 2; G <= C; G <<= 1) {
         cluster.sync();                                  // every CTA's run is written (and readable remotely)
+        if (G == 2) SM_PT(4);
         const int g0 = c & ~(G - 1), half = G >> 1;
         const int la = half * SM_TILE, lb = half * SM_TILE;
         auto A = [&](int m) -> double {
@@ -186,6 +198,7 @@ small_sort_kernel(double *keys, uint32_t *vals, long long n)
             if (lane == 0) s_co[warp] = r;
         }
         __syncthreads();
+        if (G == 2) SM_PT(5);
         const int d0 = (c - g0) * SM_TILE;
         const int i0 = s_co[0], i1 = s_co[1];
         const int j0 = d0 - i0, j1 = d0 + SM_TILE - i1;
@@ -216,6 +229,7 @@ small_sort_kernel(double *keys, uint32_t *vals, long long n)
             sk[swz16(ob + cb)] = pad_key<ORD>();
         }
         __syncthreads();
+        if (G == 2) SM_PT(6);
         const int d = tid * SM_VT;
         const int i = sm_corank_local<ORD>(sk, 0, ca, ob, cb, d);
         sm_serial<HV, ORD>(sk, sv, 0, ca, ob, cb, i, d - i, k, v);
@@ -228,6 +242,7 @@ small_sort_kernel(double *keys, uint32_t *vals, long long n)
     }
     // ---- 3. the CTA's real outputs back to HBM (coalesced)
     __syncthreads();
+    SM_PT(7);
     for (int e = tid; e < SM_TILE; e += SM_NT) {
         const long long g = base + e;
         if (g < n) {
@@ -235,7 +250,9 @@ small_sort_kernel(double *keys, uint32_t *vals, long long n)
             if (HV) vals[g] = rv[swz16(e)];
         }
     }
+    SM_PT(8);
     pdl_trigger();
+#undef SM_PT
 }
 
 }  // namespace gns
