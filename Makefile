@@ -23,6 +23,13 @@ debug: $(PKG)/libgns_debug.so
 $(PKG)/libgns_debug.so: $(SRCS)
 	$(NVCC) $(NVFLAGS) -DGNS_DEBUG_BOUNDS -o $@ $(PKG)/csrc/gns.cu
 
+# A/B build with the register network merges on (binary32 merge pass, K1 merge-path
+# rounds of both key widths; measured no faster); tests/test_gpu_knobs.py
+net: $(PKG)/libgns_net.so
+
+$(PKG)/libgns_net.so: $(SRCS)
+	$(NVCC) $(NVFLAGS) -DGNS_F2_NET=1 -DGNS_K1_NET=3 -o $@ $(PKG)/csrc/gns.cu
+
 # phase-timing build for experiments (GNS_LIB=libgns_prof.so, tools/prof_merge.py)
 prof: $(PKG)/libgns_prof.so
 
@@ -38,4 +45,4 @@ sass: $(LIB)
 clean:
 	rm -f $(LIB) oracle/liboracle.so synth/libsynth.so
 
-.PHONY: all debug prof ptxas sass clean
+.PHONY: all debug net prof ptxas sass clean

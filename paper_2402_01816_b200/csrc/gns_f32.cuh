@@ -319,6 +319,10 @@ constexpr int F2_RING = 64;
 constexpr int F2_VT = 16;                            // outputs per merge thread
 constexpr int F2_MT = F_NT * F2_VT;                  // 4096 outputs per tile (8192: 47 vs 41 us per 2^24-key level)
 static_assert(F_TILE % F2_MT == 0, "pair boundaries on tile boundaries");
+#ifndef GNS_F2_NET
+#define GNS_F2_NET 0
+#endif
+constexpr bool F2_NET = GNS_F2_NET != 0;             // key-only: register bitonic merge of a thread's outputs
 constexpr int F2_SLOTS = F2_MT + 16;                 // A (+ <= 6 alignment slots), then B (+ <= 6)
 constexpr size_t f2_smem(bool hv = false) { return (size_t)F2_NS * F2_SLOTS * 4 * (hv ? 2 : 1) + 16; }
 
@@ -326,7 +330,7 @@ struct F2Meta {
     int t, ca, cb, oa, ob;    // tile, slice lengths, slots of A[0] / B[0] in the stage
 };
 
-template <bool DESC>
+template <bool DESC, int W = 16>
 __device__ __forceinline__ int f2_corank(const float *src, long long n, long long L, int t, int gl, unsigned mask,
                                          int gbase)
 {
@@ -338,8 +342,8 @@ __device__ __forceinline__ int f2_corank(const float *src, long long n, long lon
     const float *A = src + pb, *B = src + pb + L;
     const int lo = max(0, d - nb), hi = min(d, na);
     if (lo >= hi) return lo;
-    return lo + group_count_true<16>(lo, hi - 1, gl, mask, gbase,
-                                     [&](int m) { return !fbefore<DESC>(B[d - 1 - m], A[m]); });
+    return lo + group_count_true<W>(lo, hi - 1, gl, mask, gbase,
+                                    [&](int m) { return !fbefore<DESC>(B[d - 1 - m], A[m]); });
 }
 
 // HV: u32 payload staged at the same slots as its key (vals stage after the
@@ -382,8 +386,8 @@ f32_merge2_kernel(const float *src, const uint32_t *srcv, float *dst, uint32_t *
     };
     const int init = min(nspl, F2_THREADS / 32);
     if (warp < init) {
-        const int h = lane >> 4, gl = lane & 15;
-        const int c = f2_corank<DESC>(src, n, L, first + warp, gl, 0xFFFFu << (16 * h), 16 * h);
+        // (the start-up splits by whole warps: one 33-ary round fewer than a 16-lane group)
+        const int c = f2_corank<DESC, 32>(src, n, L, first + warp, lane, 0xFFFFFFFFu, 0);
         if (lane == 0) publish(warp, c);
     }
     __syncthreads();
@@ -486,12 +490,81 @@ f32_merge2_kernel(const float *src, const uint32_t *srcv, float *dst, uint32_t *
         const int d = tid * F2_VT;
         float k[F2_VT];
         uint32_t v[F2_VT];
-        if (d < cnt) {
-            int lo = max(0, d - mt.cb), hi = min(d, mt.ca);
+        bool merged = false;
+        int lo = 0;
+        if (!HV && F2_NET) {
+            // Key-only: the thread's 16 outputs merged by a bitonic network in
+            // registers instead of 16 dependent shared-memory steps.  Its A
+            // count is the next thread's co-rank minus its own (lane 31: the
+            // warp's end co-rank, searched by all 32 lanes together); the A
+            // keys ascending followed by the B keys descending are a bitonic
+            // sequence, which 4 stages of fmin / fmax sort.  Keys that compare
+            // equal are bit-identical unless they are zeros of both signs, so
+            // the result equals the stable merge's whenever the
+            // warp's inputs hold no -0.0; a warp that sees one (or a partial
+            // tile) takes the serial merge below.
+            const int dd = min(d, cnt);
+            // the warp's last diagonal by a 33-ary search of all 32 lanes
+            // (three rounds for 4096 keys); it bounds every lane's own range
+            const int de = min((warp + 1) * 32 * F2_VT, cnt);
+            int ce;
+            {
+                const int l0 = max(0, de - mt.cb), h0 = min(de, mt.ca);
+                ce = l0;
+                if (l0 < h0)
+                    ce = l0 + group_count_true<32>(l0, h0 - 1, lane, 0xffffffffu, 0,
+                                                   [&](int x) { return !fbefore<DESC>(SB[de - 1 - x], SA[x]); });
+            }
+            // co-rank(d) <= co-rank(de) and d - co-rank(d) <= de - co-rank(de)
+            int hi = min(min(dd, mt.ca), ce);
+            lo = min(max(max(0, dd - mt.cb), ce - (de - dd)), hi);
             while (lo < hi) {
                 const int x = (lo + hi) >> 1;
-                if (!fbefore<DESC>(SB[d - 1 - x], SA[x])) lo = x + 1;
+                if (!fbefore<DESC>(SB[dd - 1 - x], SA[x])) lo = x + 1;
                 else hi = x;
+            }
+            int nlo = __shfl_down_sync(0xffffffffu, lo, 1);
+            if (lane == 31) nlo = ce;
+            const bool fullt = d + F2_VT <= cnt;
+            // A count, clamped to what both slices hold (a no-op unless NaN
+            // keys made the searches inconsistent: DESIGN.md R1)
+            const int ai = lo, bj = dd - lo;
+            int an = min(max(nlo - lo, 0), F2_VT);
+            an = max(min(an, mt.ca - ai), F2_VT - (mt.cb - bj));
+            bool zero = false;
+            if (fullt) {
+                GNS_DASSERT(an >= 0 && an <= F2_VT && ai + an <= mt.ca && bj + (F2_VT - an) <= mt.cb);
+                const float *pa = SA + ai, *pb = SB + bj + (F2_VT - 1);
+#pragma unroll
+                for (int x = 0; x < F2_VT; ++x) {
+                    k[x] = *(x < an ? pa + x : pb - x);
+                    zero |= (__float_as_uint(k[x]) == 0x80000000u);     // -0.0
+                }
+            }
+            if (__all_sync(0xffffffffu, fullt && !zero)) {
+#pragma unroll
+                for (int s = F2_VT / 2; s > 0; s >>= 1) {
+#pragma unroll
+                    for (int x = 0; x < F2_VT; ++x) {
+                        if ((x & s) == 0) {
+                            const float a = k[x], b = k[x + s];
+                            k[x] = DESC ? fmaxf(a, b) : fminf(a, b);
+                            k[x + s] = DESC ? fminf(a, b) : fmaxf(a, b);
+                        }
+                    }
+                }
+                merged = true;
+            }
+        }
+        if (!merged && d < cnt) {
+            if (HV || !F2_NET) {
+                int hi = min(d, mt.ca);
+                lo = max(0, d - mt.cb);
+                while (lo < hi) {
+                    const int x = (lo + hi) >> 1;
+                    if (!fbefore<DESC>(SB[d - 1 - x], SA[x])) lo = x + 1;
+                    else hi = x;
+                }
             }
             int ai = lo, bj = d - lo;
             float ka = SA[ai], kb = SB[bj];          // (one slot past a run end is inside the stage)

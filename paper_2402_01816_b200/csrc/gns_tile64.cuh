@@ -278,12 +278,57 @@ __device__ __forceinline__ void serial_merge3(uint32_t base, int a0, int ai, int
     }
 }
 
+// Network merge of the thread's VT3 outputs (no dependent shared-memory
+// chain): its an A keys ascending followed by its VT3 - an B keys descending
+// are a bitonic sequence, sorted by log2(VT3) half-cleaner stages in
+// registers (binary32: fmin / fmax).  Unstable, so only used when no key of
+// the CTA is -0.0 or NaN (equal keys are then bit-identical and the result is
+// the stable merge's) -- the same condition as the warp-level
+// bitonic rounds.  GNS_K1_NET: bit 0 = binary32 keys, bit 1 = 8-byte keys.
+#ifndef GNS_K1_NET
+#define GNS_K1_NET 0
+#endif
+// merge-path rounds over more than one warp: the warp's end co-rank by a
+// 33-ary search of the whole warp (1) or by lane 31's second search (0)
+#ifndef GNS_K1_WSYNC
+#define GNS_K1_WSYNC 0
+#endif
+#ifndef GNS_K1_COOPEND
+#define GNS_K1_COOPEND 1
+#endif
+template <typename K, int ORD>
+__device__ __forceinline__ void net_merge3(uint32_t base, int ai, int an, int bi, K (&k)[VT3])
+{
+    constexpr uint32_t SZ = sizeof(K);
+    GNS_DASSERT(an >= 0 && an <= VT3 && ai >= 0 && bi >= 0 && ai + an <= TILE && bi + (VT3 - an) <= TILE + VT3);
+    const uint32_t pa = base + SZ * ai, pb = base + SZ * (bi + VT3 - 1);
+#pragma unroll
+    for (int x = 0; x < VT3; ++x) k[x] = lds_k<K>(sw3<K>(x < an ? pa + SZ * x : pb - SZ * x));
+#pragma unroll
+    for (int s = VT3 / 2; s > 0; s >>= 1) {
+#pragma unroll
+        for (int x = 0; x < VT3; ++x) {
+            if ((x & s) == 0) {
+                const K a = k[x], b = k[x + s];
+                if constexpr (sizeof(K) == 4) {
+                    k[x] = (ORD & 1) ? fmaxf(a, b) : fminf(a, b);
+                    k[x + s] = (ORD & 1) ? fminf(a, b) : fmaxf(a, b);
+                } else {
+                    const bool p = kbef<K, ORD>(b, a);
+                    k[x] = p ? b : a;
+                    k[x + s] = p ? a : b;
+                }
+            }
+        }
+    }
+}
+
 // One merge-path round: spill the thread's sorted run block, synchronise
 // (the warp, or the CTA if `cta`), then merge pair (A, B) of runs of
 // (coop / 2) * VT3 keys; the thread produces outputs [d, d + VT3) of its pair.
 template <typename K, int ORD>
 __device__ __forceinline__ void merge_round3(uint32_t sbase, int tid, int e0, int coop, K (&k)[VT3],
-                                             bool cta = false)
+                                             bool cta = false, bool net = false)
 {
     constexpr int PER = 16 / (int)sizeof(K);          // keys per 16-byte transfer
 #pragma unroll
@@ -299,11 +344,47 @@ __device__ __forceinline__ void merge_round3(uint32_t sbase, int tid, int e0, in
     // last (d + VT3): the latter is the next thread's first (a shuffle),
     // searched here only by lane 31, or the pair's end
     int i, inext;
-    merge_path3x2<K, ORD>(sbase, a0, run, b0, run, d, (lane_id() == 31 && local + 1 < coop), i, inext);
-    const int up = __shfl_down_sync(0xFFFFFFFFu, i, 1);
-    if (lane_id() != 31) inext = up;
-    if (local + 1 == coop) inext = run;
+    if (GNS_K1_COOPEND && coop > 32) {
+        // the warp's last diagonal lies inside the pair: all 32 lanes search
+        // its co-rank together (33-ary, 2-3 rounds) instead of lane 31 running
+        // a second binary search beside its own; it also bounds every lane's
+        // own range (co-rank(d) <= co-rank(de), d - co-rank(d) <= de - co-rank(de))
+        const int lane = lane_id();
+        const int de = (local - lane + 32) * VT3;
+        int ce = run;
+        if (de < 2 * run) {
+            const int l0 = max(0, de - run), h0 = min(de, run);
+            ce = l0;
+            if (l0 < h0)
+                ce = l0 + group_count_true<32>(l0, h0 - 1, lane, 0xFFFFFFFFu, 0, [&](int m) {
+                    const K b = lds_k<K>(sw3<K>(sbase + (uint32_t)sizeof(K) * (b0 + de - 1 - m)));
+                    const K a = lds_k<K>(sw3<K>(sbase + (uint32_t)sizeof(K) * (a0 + m)));
+                    return !kbef<K, ORD>(b, a);
+                });
+        }
+        int hi = min(min(d, run), ce);
+        int lo = min(max(max(0, d - run), ce - (de - d)), hi);
+        while (lo < hi) {
+            const int m = (lo + hi) >> 1;
+            const K b = lds_k<K>(sw3<K>(sbase + (uint32_t)sizeof(K) * (b0 + d - 1 - m)));
+            const K a = lds_k<K>(sw3<K>(sbase + (uint32_t)sizeof(K) * (a0 + m)));
+            if (!kbef<K, ORD>(b, a)) lo = m + 1;
+            else hi = m;
+        }
+        i = lo;
+        inext = __shfl_down_sync(0xFFFFFFFFu, i, 1);
+        if (lane == 31) inext = ce;
+    } else {
+        merge_path3x2<K, ORD>(sbase, a0, run, b0, run, d, (lane_id() == 31 && local + 1 < coop), i, inext);
+        const int up = __shfl_down_sync(0xFFFFFFFFu, i, 1);
+        if (lane_id() != 31) inext = up;
+        if (local + 1 == coop) inext = run;
+    }
     const int dn = d + VT3;
+    if ((GNS_K1_NET & (sizeof(K) == 4 ? 1 : 2)) && net) {
+        net_merge3<K, ORD>(sbase, a0 + i, inext - i, b0 + d - i, k);
+        return;
+    }
     serial_merge3<K, ORD>(sbase, a0, a0 + i, b0, b0 + d - i, b0 + run, a0 + inext, b0 + dn - inext, k);
 }
 
@@ -633,8 +714,12 @@ tile_sort3_kernel(const K *src_k, K *dst_k, long long n, unsigned *unsorted, K *
         // ---- merge-path rounds (runs 2048 -> 8192, or 64 -> 8192)
 #pragma unroll 1
         for (int coop = cta_special ? 2 : (2 << GNS_K1_BITONIC); coop <= NT3; coop <<= 1) {
-            merge_round3<K, ORD>(sbase, tid, e0, coop, k, true);
-            __syncthreads();
+            // rounds inside one warp (coop <= 32: a pair's threads, their spills
+            // and their reads all belong to that warp) synchronise the warp only
+            const bool cta = !GNS_K1_WSYNC || coop > 32;
+            merge_round3<K, ORD>(sbase, tid, e0, coop, k, cta, F64 && !cta_special);
+            if (cta) __syncthreads();
+            else __syncwarp();
         }
     } else {
         __syncthreads();

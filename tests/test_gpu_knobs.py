@@ -122,3 +122,20 @@ def test_four_way_passes_bitexact():
     r = subprocess.run([sys.executable, "-c", SCRIPT4.replace("ROOT_DIR", repr(ROOT))], capture_output=True, text=True, env=e,
                        timeout=900)
     assert r.returncode == 0, (r.stdout[-2000:], r.stderr[-2000:])
+
+
+# The register network merges (compile-time knobs GNS_F2_NET / GNS_K1_NET, `make net`
+# -> libgns_net.so): the binary32 key-only merge pass and K1's merge-path rounds (both
+# key widths) merge a thread's outputs by a bitonic network unless -0.0 / NaN keys are
+# present.  The f64 knob script and the binary32 parity tests run against that build.
+NET_LIB = os.path.join(ROOT, "paper_2402_01816_b200", "libgns_net.so")
+
+
+@pytest.mark.skipif(not os.path.exists(NET_LIB), reason="libgns_net.so not built (make net)")
+def test_network_merge_build_bitexact():
+    e = dict(os.environ, GNS_LIB="libgns_net.so")
+    r = subprocess.run([sys.executable, "-c", SCRIPT.replace("ROOT_DIR", repr(ROOT))], capture_output=True, text=True, env=e, timeout=600)
+    assert r.returncode == 0, (r.stdout[-2000:], r.stderr[-2000:])
+    r = subprocess.run([sys.executable, "-m", "pytest", os.path.join(ROOT, "tests", "test_gpu_parity.py"), "-q", "-x", "-m", "gpu",
+                        "-k", "f32 or tile_sort_step"], capture_output=True, text=True, env=e, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, (r.stdout[-3000:], r.stderr[-2000:])

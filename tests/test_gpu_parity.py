@@ -775,6 +775,46 @@ def test_f32_keys(gns, n, target, payload):
             assert np.array_equal(tv.cpu().numpy(), v[perm]), f"vals n={n} {target}"
 
 
+def _f32_keys_shape(n, seed, shape):
+    """binary32 keys without zeros (uniform / heavy ties) or with a few zeros
+    of both signs: the key-only merge pass merges a thread's outputs by a
+    register network unless its warp holds a zero (csrc/gns_f32.cuh)."""
+    rng = np.random.default_rng(seed)
+    if shape == "uniform":
+        k = (rng.random(n, dtype=np.float32) + np.float32(0.5)) * np.where(rng.random(n) < 0.5, -1, 1).astype(np.float32)
+    elif shape == "ties":
+        k = rng.integers(1, 24, n).astype(np.float32) * np.where(rng.random(n) < 0.3, -1, 1).astype(np.float32)
+    elif shape == "sparse_zeros":
+        k = (rng.standard_normal(n) * 4).astype(np.float32)
+        k[k == 0] = 1.0
+        z = rng.integers(0, max(n, 1), max(1, n // 3000))
+        k[z] = np.where(rng.random(z.size) < 0.5, np.float32(-0.0), np.float32(0.0))
+    elif shape == "runs":
+        k = np.sort((rng.random(n, dtype=np.float32) + np.float32(1.0)))      # presorted halves interleaving by blocks
+        h = n // 2
+        k = np.concatenate([k[h:], k[:h]])
+    else:
+        raise ValueError(shape)
+    return k
+
+
+@pytest.mark.parametrize("shape", ["uniform", "ties", "sparse_zeros", "runs"])
+@pytest.mark.parametrize("target", ["AscLeft", "DescLeft", "AscRight", "DescRight"])
+@pytest.mark.parametrize("n", [4096, T1 + 1, 2 * T1, 3 * T1 + 5, 100003, (1 << 20) + 3, (1 << 22) + 4099])
+def test_f32_keys_network_merge(gns, n, target, shape):
+    """NEXT f3: binary32 key-only merge passes on inputs whose warps hold no
+    zero (the register bitonic merge of a thread's 16 outputs) and on inputs
+    with a few signed zeros (warps falling back to the serial stable merge),
+    vs the oracle's stable order of the exactly widened keys, bit-exact."""
+    k = _f32_keys_shape(n, 77 + n + len(target), shape)
+    _, ev = oracle.sort_target(k.astype(np.float64), synth.iota_u32(n), target)
+    perm = ev.astype(np.int64)
+    tk = torch.from_numpy(k.copy()).cuda()
+    gns.sort_f32_(tk, None, target=target)
+    torch.cuda.synchronize()
+    assert np.array_equal(tk.cpu().numpy().view(np.uint32), k[perm].view(np.uint32)), f"keys n={n} {target} {shape}"
+
+
 def test_f32_keys_full_size(gns):
     """2^24 binary32 keys with payload at full size, vs the oracle."""
     n = 1 << 24
