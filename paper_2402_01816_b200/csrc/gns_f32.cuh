@@ -86,13 +86,17 @@ f32_tile_sort_kernel(const float *src_k, const uint32_t *src_v, float *dst_k, ui
     // shared-memory merge rounds: runs of 32 -> 8192 (merge path + serial merge)
 #pragma unroll 1
     for (int coop = 2; coop <= F_NT; coop <<= 1) {
-        __syncthreads();
+        // (a pair of <= 32 threads lies inside one warp: warp-level sync)
+        const bool wsync = GNS_K1_WSYNC && coop <= 32;
+        if (wsync) __syncwarp();
+        else __syncthreads();
 #pragma unroll
         for (int x = 0; x < F_VT; ++x) {
             sk[fswz(e0 + x)] = k[x];
             if (HV) sv[fswz(e0 + x)] = v[x];
         }
-        __syncthreads();
+        if (wsync) __syncwarp();
+        else __syncthreads();
         const int local = tid & (coop - 1);
         const int a0 = (tid - local) * F_VT;
         const int run = (coop >> 1) * F_VT;

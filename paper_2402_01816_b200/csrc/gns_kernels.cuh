@@ -77,6 +77,11 @@ constexpr int VT = 16;             // outputs per merge thread
 constexpr int MTILE = NT * VT;     // K3/K4 output tile = 4096 elements
 constexpr int MTILE_LOG2 = 12;
 static_assert((1 << MTILE_LOG2) == MTILE, "MTILE_LOG2");
+// tile-sort merge rounds inside one warp synchronise that warp only (K1 with
+// payload here, key-only in gns_tile64.cuh); 0 = CTA barriers in every round
+#ifndef GNS_K1_WSYNC
+#define GNS_K1_WSYNC 1
+#endif
 #ifndef GNS_NT1
 #define GNS_NT1 256
 #endif
@@ -1348,7 +1353,12 @@ tile_sort2_kernel(const double *src_k, const uint32_t *src_v, double *dst_k, uin
                                         (swa(smem_u32(sk) + 8u * (e0 + x)) - smem_u32(sk))) = k[x];
             if (HV) sv[(swa(smem_u32(sk) + 8u * (e0 + x)) - smem_u32(sk)) >> 3] = v[x];
         }
-        __syncthreads();
+        // a pair of <= 32 threads lies inside one warp (its spills, its reads
+        // and the swizzle, which stays inside a 128-byte line): the first
+        // five rounds synchronise the warp only
+        const bool wsync = GNS_K1_WSYNC && coop <= 32;
+        if (wsync) __syncwarp();
+        else __syncthreads();
         {
             const int local = tid & (coop - 1);
             const int a0 = (tid - local) * VT1;
@@ -1358,7 +1368,8 @@ tile_sort2_kernel(const double *src_k, const uint32_t *src_v, double *dst_k, uin
             const int i = merge_path_tile<ORD>(smem_u32(sk), a0, run, b0, run, d);
             serial_merge32<HV, ORD>(sk, sv, a0 + i, b0, b0 + d - i, b0 + run, k, v);
         }
-        __syncthreads();
+        if (wsync) __syncwarp();
+        else __syncthreads();
     }
     } else {
         __syncthreads();                   // the TMA-layout reads are done before the staging writes

@@ -152,13 +152,18 @@ small_sort_kernel(double *keys, uint32_t *vals, long long n)
     SM_PT(2);
 #pragma unroll 1
     for (int coop = 2; coop <= SM_NT; coop <<= 1) {
-        __syncthreads();
+        // a pair of <= 32 threads lies inside one warp (spills, reads and the
+        // 16-element swizzle): those rounds synchronise the warp only
+        const bool wsync = GNS_K1_WSYNC && coop <= 32;
+        if (wsync) __syncwarp();
+        else __syncthreads();
 #pragma unroll
         for (int x = 0; x < SM_VT; ++x) {
             rk[swz16(tid * SM_VT + x)] = k[x];
             if (HV) rv[swz16(tid * SM_VT + x)] = v[x];
         }
-        __syncthreads();
+        if (wsync) __syncwarp();
+        else __syncthreads();
         const int local = tid & (coop - 1);
         const int a0 = (tid - local) * SM_VT;
         const int run = (coop >> 1) * SM_VT;

@@ -19,7 +19,9 @@
 //     (default 2: runs 32 -> 128) unless the CTA holds a -0.0 or NaN key, then
 //     shared-memory merge-path rounds up to 8192 (all of them in the -0.0 /
 //     NaN case), each thread producing VT3 outputs as two independent chains
-//     (merge path + serial merge, left run wins ties);
+//     (merge path + serial merge, left run wins ties); rounds
+//     inside one warp synchronise that warp only, wider rounds the CTA, and
+//     there the warp's end co-rank is one 33-ary search by all 32 lanes;
 //   * the tile arrives by one-dimensional bulk copies (one VT3-key segment
 //     per thread, TMA engine, one mbarrier) into a padded layout whose 16-byte
 //     register transfers are conflict-free, and leaves the same way.
@@ -290,9 +292,25 @@ __device__ __forceinline__ void serial_merge3(uint32_t base, int a0, int ai, int
 #endif
 // merge-path rounds over more than one warp: the warp's end co-rank by a
 // 33-ary search of the whole warp (1) or by lane 31's second search (0)
+// merge-path round synchronisation: rounds inside one warp synchronise that
+// warp only (GNS_K1_WSYNC); rounds over 2 or 4 warps synchronise those warps on
+// a named barrier (GNS_K1_GSYNC); only the last round needs the whole CTA
 #ifndef GNS_K1_WSYNC
-#define GNS_K1_WSYNC 0
+#define GNS_K1_WSYNC 1
 #endif
+#ifndef GNS_K1_GSYNC
+#define GNS_K1_GSYNC 0
+#endif
+// Barrier of the coop threads that merge one pair (coop a power of two).
+__device__ __forceinline__ void pair_sync(int tid, int coop, int nt)
+{
+    if (GNS_K1_WSYNC && coop <= 32) __syncwarp();
+    else if (GNS_K1_GSYNC && GNS_K1_WSYNC && coop < nt && coop <= 128) {
+        // ids 1-4: pairs of 64 threads, 5-6: pairs of 128 threads (id 0 = __syncthreads)
+        const int id = (coop == 64 ? 1 : 5) + tid / coop;
+        asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(coop) : "memory");
+    } else __syncthreads();
+}
 #ifndef GNS_K1_COOPEND
 #define GNS_K1_COOPEND 1
 #endif
@@ -333,7 +351,7 @@ __device__ __forceinline__ void merge_round3(uint32_t sbase, int tid, int e0, in
     constexpr int PER = 16 / (int)sizeof(K);          // keys per 16-byte transfer
 #pragma unroll
     for (int c = 0; c < VT3 / PER; ++c) sts16_k<K>(sw3<K>(sbase + (uint32_t)sizeof(K) * (e0 + PER * c)), &k[PER * c]);
-    if (cta) __syncthreads();
+    if (cta) pair_sync(tid, coop, NT3);
     else __syncwarp();
     const int local = tid & (coop - 1);
     const int a0 = (tid - local) * VT3;
@@ -716,10 +734,8 @@ tile_sort3_kernel(const K *src_k, K *dst_k, long long n, unsigned *unsorted, K *
         for (int coop = cta_special ? 2 : (2 << GNS_K1_BITONIC); coop <= NT3; coop <<= 1) {
             // rounds inside one warp (coop <= 32: a pair's threads, their spills
             // and their reads all belong to that warp) synchronise the warp only
-            const bool cta = !GNS_K1_WSYNC || coop > 32;
-            merge_round3<K, ORD>(sbase, tid, e0, coop, k, cta, F64 && !cta_special);
-            if (cta) __syncthreads();
-            else __syncwarp();
+            merge_round3<K, ORD>(sbase, tid, e0, coop, k, true, F64 && !cta_special);
+            pair_sync(tid, coop, NT3);
         }
     } else {
         __syncthreads();
