@@ -357,7 +357,7 @@ __global__ void __launch_bounds__(F2_THREADS, HV ? 2 : 3)
 f32_merge2_kernel(const float *src, const uint32_t *srcv, float *dst, uint32_t *dstv, long long n, long long L,
                   int ntiles, int per_cta)
 {
-    pdl_wait();
+    if (!GNS_LATE_PDL_WAIT) pdl_wait();
     extern __shared__ __align__(16) unsigned char f2_smem_raw[];
     float *stage = reinterpret_cast<float *>(f2_smem_raw);
     uint32_t *vstage = reinterpret_cast<uint32_t *>(stage + F2_NS * F2_SLOTS);
@@ -383,6 +383,7 @@ f32_merge2_kernel(const float *src, const uint32_t *srcv, float *dst, uint32_t *
         spl_used = 0;
     }
     __syncthreads();
+    if (GNS_LATE_PDL_WAIT) pdl_wait();       // (the prologue above reads nothing of the previous launch)
     auto publish = [&](int j, int c) {
         spl[j % F2_RING] = c;
         __threadfence_block();

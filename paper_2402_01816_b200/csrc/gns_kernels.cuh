@@ -79,6 +79,11 @@ constexpr int MTILE_LOG2 = 12;
 static_assert((1 << MTILE_LOG2) == MTILE, "MTILE_LOG2");
 // tile-sort merge rounds inside one warp synchronise that warp only (K1 with
 // payload here, key-only in gns_tile64.cuh); 0 = CTA barriers in every round
+// merge passes wait for the previous launch (PDL) after their shared-memory
+// prologue instead of at entry
+#ifndef GNS_LATE_PDL_WAIT
+#define GNS_LATE_PDL_WAIT 1
+#endif
 #ifndef GNS_K1_WSYNC
 #define GNS_K1_WSYNC 1
 #endif
@@ -888,15 +893,13 @@ merge_tstore_kernel(PipeGeo pg, int ntiles, int per_cta, const __grid_constant__
     const int tl_slot = min(31, 1 + (63 - __clzll(pg.g.L)) - TILE_LOG2);
 #endif
     const bool chained = !OL && ch.dep != nullptr;
+    // The previous launch's results are first read below the shared-memory
+    // set-up (the list-driven variant reads its list before): waiting for it
+    // there lets a CTA that starts early do its prologue meanwhile.
+    constexpr bool LATE_WAIT = GNS_LATE_PDL_WAIT && !OL;
     if (chained) pdl_trigger();          // (the next pass may launch once every CTA of this one started)
-    else pdl_wait();
+    else if (!LATE_WAIT) pdl_wait();
     GNS_TL_START(tl_slot);
-    // NEXT f2 flag word: loaded now, tested after the first split searches
-    // (which only read), so its latency hides behind them
-    const unsigned f_adapt = ad.flag ? *(volatile const unsigned *)ad.flag : 3u;
-#ifdef GNS_PROF
-    const long long t_flag = clock64();
-#endif
     extern __shared__ __align__(16) unsigned char smem_raw0[];
     // 1 KiB alignment for the swizzled TMA boxes; pointer arithmetic (not an
     // integer round trip) keeps the shared address space visible to ptxas.
@@ -944,6 +947,13 @@ merge_tstore_kernel(PipeGeo pg, int ntiles, int per_cta, const __grid_constant__
         spl_used = 0;
     }
     __syncthreads();
+    if (LATE_WAIT && !chained) pdl_wait();
+    // NEXT f2 flag word: loaded now, tested after the first split searches
+    // (which only read), so its latency hides behind them
+    const unsigned f_adapt = ad.flag ? *(volatile const unsigned *)ad.flag : 3u;
+#ifdef GNS_PROF
+    const long long t_flag = clock64();
+#endif
     auto publish = [&](int j, int c) {
         spl[j % SPL_RING] = c;
         __threadfence_block();
