@@ -81,6 +81,9 @@ static_assert((1 << MTILE_LOG2) == MTILE, "MTILE_LOG2");
 // payload here, key-only in gns_tile64.cuh); 0 = CTA barriers in every round
 // merge passes wait for the previous launch (PDL) after their shared-memory
 // prologue instead of at entry
+#ifndef GNS_TMAP_PREFETCH
+#define GNS_TMAP_PREFETCH 0
+#endif
 #ifndef GNS_LATE_PDL_WAIT
 #define GNS_LATE_PDL_WAIT 1
 #endif
@@ -937,6 +940,13 @@ merge_tstore_kernel(PipeGeo pg, int ntiles, int per_cta, const __grid_constant__
     auto geo = [&](int j) -> const PipeGeo & { return rev(j) ? ol.pg1 : pg; };
     const int nspl = (tile_of(m - 1) + 1 < ntiles) ? m + 1 : m;
     for (int j = tid; j < SPL_RING; j += WS_THREADS) spl_tag[j] = -1;
+    if (GNS_TMAP_PREFETCH && tid == 32) {
+        // the tensor maps are launch parameters: their descriptors can be
+        // fetched before the previous launch has finished
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&amap)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&bmap)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&omap)) : "memory");
+    }
     if (tid == 0) {
 #pragma unroll
         for (int b = 0; b < NS; ++b) {
