@@ -82,7 +82,7 @@ static_assert((1 << MTILE_LOG2) == MTILE, "MTILE_LOG2");
 // merge passes wait for the previous launch (PDL) after their shared-memory
 // prologue instead of at entry
 #ifndef GNS_TMAP_PREFETCH
-#define GNS_TMAP_PREFETCH 0
+#define GNS_TMAP_PREFETCH 1
 #endif
 #ifndef GNS_LATE_PDL_WAIT
 #define GNS_LATE_PDL_WAIT 1
